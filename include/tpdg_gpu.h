@@ -1,0 +1,154 @@
+/* tpdg_gpu.h -- C ABI of the B200 (sm_100a) KSVD-preconditioned matrix-free GMRES hot path.
+ *
+ * Drop-in boundary for the reference library `tpdg` (header-only C++20). Every entry point
+ * replaces one reference interface on the path newton_linear_solve runs
+ * (reference proj/include/tpdg/solve/time_step.hpp:57-122); citations are relative to
+ * /root/reference/proj/include/tpdg/:
+ *
+ *   tpdg_gpu_op_create        make_linearized_operator        ops/linearized.hpp:187-196
+ *                             (+ the LinearizationCache it binds, ops/linearized.hpp:15-33)
+ *   tpdg_gpu_jv               jacobian_apply                  ops/linearized.hpp:201-240
+ *   tpdg_gpu_shuffled         shuffled_apply(_transpose)      ops/shuffled.hpp:509-531
+ *   tpdg_gpu_form_ksvd        form_ksvd_2d / form_ksvd_3d     precond/ksvd.hpp:252-306, 312-372
+ *   tpdg_gpu_pc_apply         KsvdPC2D::apply / KsvdPC3D::apply precond/ksvd.hpp:172-195, 210-233
+ *   tpdg_gpu_pc_fallbacks     KsvdPC*::fallbacks (FallbackEvent) precond/ksvd.hpp:22-28
+ *   tpdg_gpu_gmres            gmres(op, pc, b, GmresConfig)   solve/gmres.hpp:52-179
+ *   status codes              tpdg::Error hierarchy           common/error.hpp:9-42
+ *
+ * Conventions
+ *  - Plain C types only. Arrays are in the reference's own index orders (no re-layout at the
+ *    boundary; kernels re-tile internally):
+ *      state vectors  [e][c][tensor index, x fastest]                  (ops/state.hpp:12-13)
+ *      g, d           mu x (p+1) row-major; gw, dw (p+1) x mu          (dg/reference_element.hpp:24-27)
+ *      w              mu quadrature weights on [0,1]
+ *      jdet           [e][mu^dim]; face_w [e][2*dim][mu^(dim-1)]       (dg/mesh.hpp:87-92)
+ *      conn           [e][2*dim][3] = neighbor, neighbor_face, orientation (dg/mesh.hpp:37-42);
+ *                     neighbor < 0 marks a boundary face
+ *      dft            [e][dir][mu^dim][n_c][n_c]; dfm, dfp [e][face][mu^(dim-1)][n_c][n_c]
+ *  - Functions never throw; they return a tpdg_status. tpdg_gpu_last_error() gives the message of
+ *    the last failure on the calling thread. Per-element singularity is NOT an error: it is
+ *    reported through the fallback list exactly like FallbackEvent.
+ *  - `_host` entry points take host pointers and copy in/out inside the call; the others take
+ *    device pointers and are ordered on the context's CUDA stream (synchronous on return unless
+ *    stated otherwise).
+ *  - Objects are owned by the caller and released with tpdg_gpu_*_destroy.
+ */
+#ifndef TPDG_GPU_H
+#define TPDG_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  TPDG_OK = 0,
+  TPDG_SHAPE = 1,        /* tpdg::ShapeError */
+  TPDG_SINGULAR = 2,     /* tpdg::SingularError */
+  TPDG_STATE = 3,        /* tpdg::StateError */
+  TPDG_CONVERGENCE = 4,  /* tpdg::ConvergenceError / GmresFailure (best iterate still returned) */
+  TPDG_CONFIG = 5,       /* tpdg::ConfigError (incl. stale-cache hash mismatch) */
+  TPDG_CUDA = 6          /* CUDA / NCCL runtime failure (no reference equivalent) */
+} tpdg_status;
+
+typedef struct tpdg_gpu_ctx_s *tpdg_gpu_ctx;
+typedef struct tpdg_gpu_op_s *tpdg_gpu_op;
+typedef struct tpdg_gpu_pc_s *tpdg_gpu_pc;
+
+/* Discretization + linearization as flat host arrays (GLOBAL mesh; see layouts above).
+ * Mirrors Discretization (ops/discretization.hpp:17-35) + LinearizationCache. */
+typedef struct {
+  int dim, n_c, p, mu, n_elements;
+  const double *g, *d, *gw, *dw, *w;
+  const double *jdet, *face_w;
+  const int64_t *conn;
+  const double *dft, *dfm, *dfp;
+  uint64_t state_hash; /* LinearizationCache::hash (ops/linearized.hpp:16) */
+} tpdg_gpu_system;
+
+/* KsvdConfig + LanczosConfig (precond/ksvd.hpp:16-20, tensor/lanczos.hpp:15-30). */
+typedef struct {
+  int terms;               /* r, default 2 */
+  int lanczos_max_it;      /* J, 0 = 2r + 20 */
+  double breakdown_tol;    /* default 1e-12 */
+  uint64_t seed;           /* default 0x5eed */
+  double degenerate_tol;   /* default 1e-12 */
+} tpdg_gpu_ksvd_config;
+
+/* GmresConfig (solve/gmres.hpp:14-29). side: 0 = right (default), 1 = left. */
+typedef struct {
+  double tol;
+  int restart;
+  int max_iterations;
+  int side;
+} tpdg_gpu_gmres_config;
+
+const char *tpdg_gpu_last_error(void);
+const char *tpdg_gpu_version(void);
+
+/* ---- context: one per GPU / rank. nccl_id: 128-byte ncclUniqueId for nranks > 1, else NULL. */
+int tpdg_gpu_ctx_create(int device, int rank, int nranks, const void *nccl_id, tpdg_gpu_ctx *out);
+int tpdg_gpu_ctx_destroy(tpdg_gpu_ctx ctx);
+int tpdg_gpu_ctx_stream(tpdg_gpu_ctx ctx, void **cuda_stream);
+int tpdg_gpu_ctx_sync(tpdg_gpu_ctx ctx);
+int tpdg_gpu_nccl_unique_id(void *out128);
+/* Count of this library's kernel launches on the context so far (bench evidence). */
+int tpdg_gpu_ctx_launches(tpdg_gpu_ctx ctx, int64_t *count);
+
+/* ---- operator (M - dt J) (jacobian_only = 0) or J (jacobian_only = 1) of the elements
+ * [e_begin, e_end) owned by this rank. block_mode: 0 = full, 1 = small. */
+int tpdg_gpu_op_create(tpdg_gpu_ctx ctx, const tpdg_gpu_system *sys, double dt, int jacobian_only, int block_mode,
+                       int e_begin, int e_end, tpdg_gpu_op *out);
+int tpdg_gpu_op_destroy(tpdg_gpu_op op);
+int tpdg_gpu_op_local_size(tpdg_gpu_op op, int64_t *n_local);
+/* check_cache (ops/linearized.hpp:180-184): TPDG_CONFIG when hash != the op's bound hash */
+int tpdg_gpu_op_check_hash(tpdg_gpu_op op, uint64_t expected_hash);
+int tpdg_gpu_jv(tpdg_gpu_op op, const double *d_in, double *d_out);
+int tpdg_gpu_jv_host(tpdg_gpu_op op, const double *h_in, double *h_out);
+/* Matrix-free shuffled product of one (local) element block; test hook. */
+int tpdg_gpu_shuffled_host(tpdg_gpu_op op, int e, int comp, int transpose, const double *h_in, double *h_out);
+
+/* ---- KSVD preconditioner, formed on the device (no host fallback). */
+int tpdg_gpu_form_ksvd(tpdg_gpu_op op, const tpdg_gpu_ksvd_config *cfg, tpdg_gpu_pc *out);
+/* Test hook: build the apply state from externally formed raw factors (2D: a1 b1 a2 b2,
+ * 3D: a1 b1 c1 b2 c2 per block, concatenated for blocks with has[blk] != 0; LU and Schur are
+ * recomputed on the device exactly as make_factors_2d/3d do). Blocks with has == 0 get the
+ * exact block-LU fallback. */
+int tpdg_gpu_pc_import_factors(tpdg_gpu_op op, const double *h_factors, const int64_t *h_has, tpdg_gpu_pc *out);
+int tpdg_gpu_pc_destroy(tpdg_gpu_pc pc);
+int tpdg_gpu_pc_num_fallbacks(tpdg_gpu_pc pc, int *n);
+int tpdg_gpu_pc_fallbacks(tpdg_gpu_pc pc, int64_t *pairs /* (element, component) x n */);
+int tpdg_gpu_pc_factor_len(tpdg_gpu_pc pc, int *len);
+int tpdg_gpu_pc_export_factors(tpdg_gpu_pc pc, int blk, double *h_out, int *has);
+int tpdg_gpu_pc_apply(tpdg_gpu_pc pc, const double *d_in, double *d_out);
+int tpdg_gpu_pc_apply_host(tpdg_gpu_pc pc, const double *h_in, double *h_out);
+
+/* ---- restarted GMRES, device resident. hist (may be NULL) receives |g_{k+1}| per iteration
+ * (GmresResult::residual_history). Returns TPDG_CONVERGENCE (with x = best iterate) when the
+ * budget runs out, like GmresFailure. */
+int tpdg_gpu_gmres(tpdg_gpu_op op, tpdg_gpu_pc pc, const double *d_b, double *d_x, const tpdg_gpu_gmres_config *cfg,
+                   int *iterations, double *hist, int hist_cap, int *converged);
+int tpdg_gpu_gmres_host(tpdg_gpu_op op, tpdg_gpu_pc pc, const double *h_b, double *h_x,
+                        const tpdg_gpu_gmres_config *cfg, int *iterations, double *hist, int hist_cap,
+                        int *converged);
+
+/* ---- host-side input production for the BASELINE configurations (out of the kernel scope;
+ * restates build_reference / generate_mesh(cartesian) / build_cache for scalar advection).
+ * case_kind: 0 = 2D constant velocity (vel[0], vel[1]); 1 = 2D swirl (sin 2 pi y, cos 2 pi x);
+ *            2 = 3D constant velocity (vel[0..2]).
+ * Returned arrays are owned by the setup object. */
+typedef struct tpdg_setup_s *tpdg_setup;
+int tpdg_setup_advection(int case_kind, const double *vel, int nx, int ny, int nz, int p, int periodic,
+                         tpdg_setup *out);
+int tpdg_setup_system(tpdg_setup s, tpdg_gpu_system *sys);
+int tpdg_setup_destroy(tpdg_setup s);
+/* libstdc++ std::mt19937_64 + uniform_real_distribution(-scale, scale) (tests/support/test_rng.hpp) */
+int tpdg_uniform_vector(uint64_t seed, int64_t n, double scale, double *out);
+/* tpdg::detail::seeded_unit_vector (tensor/lanczos.hpp:61-72) */
+int tpdg_seeded_unit_vector(int64_t n, uint64_t seed, double *out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TPDG_GPU_H */

@@ -1,0 +1,920 @@
+// C-ABI layer (include/tpdg_gpu.h): object lifetimes, uploads, KSVD formation orchestration and
+// the device-resident restarted GMRES driver.
+//
+// GMRES (reference solve/gmres.hpp:52-179): the Krylov basis, the operator, the preconditioner
+// and MGS live on the device; per iteration only the Hessenberg column (k+2 doubles) returns to
+// the host, where the Givens rotations run in double precision exactly as the reference writes
+// them (std::hypot, same update formulas), so |g_{k+1}| and the stopping test follow the
+// reference's arithmetic given the same column.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include <nccl.h>
+
+#include "tpdg_internal.hpp"
+
+using namespace tpdg_gpu;
+
+namespace tpdg_gpu {
+
+thread_local std::string g_last_error;
+void set_error(const std::string& what) { g_last_error = what; }
+
+} // namespace tpdg_gpu
+
+namespace {
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return TPDG_OK;
+  } catch (const Failure& e) {
+    set_error(e.what);
+    return e.status;
+  } catch (const std::bad_alloc&) {
+    set_error("host allocation failed");
+    return TPDG_CUDA;
+  } catch (const std::exception& e) {
+    set_error(e.what());
+    return TPDG_CONFIG;
+  }
+}
+
+#define REQUIRE(cond, status, msg)                              \
+  do {                                                          \
+    if (!(cond)) throw Failure{status, std::string(msg)};       \
+  } while (0)
+
+#define NCCL_CHECK(expr)                                                                          \
+  do {                                                                                            \
+    ncclResult_t r__ = (expr);                                                                    \
+    if (r__ != ncclSuccess) throw Failure{TPDG_CUDA, std::string(#expr) + ": " + ncclGetErrorString(r__)}; \
+  } while (0)
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) {
+    o.p = nullptr;
+    o.bytes = 0;
+  }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) {
+      if (p) cudaFree(p);
+      p = o.p;
+      bytes = o.bytes;
+      o.p = nullptr;
+      o.bytes = 0;
+    }
+    return *this;
+  }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  void alloc(size_t b) {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = b;
+    if (b) TPDG_CUDA_CHECK(cudaMalloc(&p, b));
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+template <class T>
+void upload(DevBuf& buf, const T* host, size_t count, cudaStream_t st) {
+  buf.alloc(sizeof(T) * count);
+  if (count) TPDG_CUDA_CHECK(cudaMemcpyAsync(buf.p, host, sizeof(T) * count, cudaMemcpyHostToDevice, st));
+}
+
+} // namespace
+
+// ------------------------------------------------------------------------------------ objects
+struct tpdg_gpu_ctx_s {
+  int device = 0, rank = 0, nranks = 1;
+  cudaStream_t stream = nullptr;
+  ncclComm_t comm = nullptr;
+  int64_t launches_at_create = 0;
+};
+
+struct tpdg_gpu_op_s {
+  tpdg_gpu_ctx ctx = nullptr;
+  DevSys s{};
+  int dim = 2, n_c = 1, p = 1, q = 2, mu = 3;
+  int e_begin = 0, e_end = 0, n_global = 0;
+  int64_t n_local_dofs = 0;
+  uint64_t hash = 0;
+  DevBuf g, d, gw, dw, w, jdet, face_w, dft, dfm, dfp, conn, halo;
+  DevBuf io_a, io_b;  // staging for the host-pointer entry points
+  DevBuf shuf_ws;
+  // halo plan (multi-rank): for each peer rank, local elements to send and halo slots to fill
+  struct Peer {
+    int rank;
+    std::vector<int> send_local;  // local element ids
+    int recv_first, recv_count;   // halo slot range
+    DevBuf send_idx, send_buf;
+  };
+  std::vector<Peer> peers;
+  int n_halo = 0;
+};
+
+struct tpdg_gpu_pc_s {
+  tpdg_gpu_op op = nullptr;
+  DevPC pc{};
+  int nblk = 0, raw_len = 0;
+  DevBuf raw, rec, piv, kind, fb_slot, fb_lu, fb_piv, status;
+  std::vector<int> kind_h;
+  std::vector<int64_t> fallbacks;  // (element, component)
+};
+
+namespace {
+
+DevSys make_devsys(const tpdg_gpu_op_s& op, int block_mode, double a, double b) {
+  DevSys s{};
+  s.dim = op.dim;
+  s.n_c = op.n_c;
+  s.q = op.q;
+  s.mu = op.mu;
+  s.npe = op.dim == 2 ? op.q * op.q : op.q * op.q * op.q;
+  s.nqv = op.dim == 2 ? op.mu * op.mu : op.mu * op.mu * op.mu;
+  s.nqf = s.nqv / op.mu;
+  s.n_local = op.e_end - op.e_begin;
+  s.n_halo = op.n_halo;
+  s.small = block_mode;
+  s.a = a;
+  s.b = b;
+  s.g = op.g.as<double>();
+  s.d = op.d.as<double>();
+  s.gw = op.gw.as<double>();
+  s.dw = op.dw.as<double>();
+  s.w = op.w.as<double>();
+  s.jdet = op.jdet.as<double>();
+  s.face_w = op.face_w.as<double>();
+  s.dft = op.dft.as<double>();
+  s.dfm = op.dfm.as<double>();
+  s.dfp = op.dfp.as<double>();
+  s.conn = op.conn.as<int>();
+  return s;
+}
+
+__global__ void gather_elems_kernel(const double* __restrict__ v, const int* __restrict__ idx, int count, int blk,
+                                    double* __restrict__ out) {
+  const int64_t total = int64_t(count) * blk;
+  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
+    const int e = int(t / blk), i = int(t % blk);
+    out[t] = v[int64_t(idx[e]) * blk + i];
+  }
+}
+
+// Face-neighbour halo exchange (whole element blocks of the elements referenced across ranks).
+void exchange_halo(tpdg_gpu_op op, const double* d_in) {
+  if (op->ctx->nranks == 1 || op->peers.empty()) return;
+  cudaStream_t st = op->ctx->stream;
+  const int blk = op->n_c * op->s.npe;
+  for (auto& p : op->peers) {
+    const int cnt = int(p.send_local.size());
+    if (cnt) {
+      gather_elems_kernel<<<std::min(148 * 4, (cnt * blk + 255) / 256), 256, 0, st>>>(d_in, p.send_idx.as<int>(),
+                                                                                     cnt, blk,
+                                                                                     p.send_buf.as<double>());
+      TPDG_CUDA_CHECK(cudaGetLastError());
+      ++g_launches;
+    }
+  }
+  NCCL_CHECK(ncclGroupStart());
+  for (auto& p : op->peers) {
+    const size_t ns = p.send_local.size() * size_t(blk);
+    if (ns) NCCL_CHECK(ncclSend(p.send_buf.as<double>(), ns, ncclDouble, p.rank, op->ctx->comm, st));
+    const size_t nr = size_t(p.recv_count) * blk;
+    if (nr)
+      NCCL_CHECK(ncclRecv(op->halo.as<double>() + size_t(p.recv_first) * blk, nr, ncclDouble, p.rank, op->ctx->comm,
+                          st));
+  }
+  NCCL_CHECK(ncclGroupEnd());
+}
+
+void allreduce_scalar(tpdg_gpu_ctx ctx, double* d_val, int count = 1) {
+  if (ctx->nranks == 1) return;
+  NCCL_CHECK(ncclAllReduce(d_val, d_val, count, ncclDouble, ncclSum, ctx->comm, ctx->stream));
+}
+
+void jv_device(tpdg_gpu_op op, const double* d_in, double* d_out) {
+  exchange_halo(op, d_in);
+  launch_jv(op->s, d_in, op->halo.as<double>(), d_out, op->ctx->stream);
+}
+
+void pc_apply_device(tpdg_gpu_pc pc, const double* d_in, double* d_out) {
+  launch_pc_apply(pc->pc, d_in, d_out, pc->op->ctx->stream);
+}
+
+// ------------------------------------------------------------------------------------ GMRES
+struct GmresWork {
+  DevBuf V, z, tmp, r, xloc, hcol, partial, counter, y, scal;
+};
+
+
+__global__ void sqrt_inplace_kernel(double* v) { v[0] = sqrt(v[0]); }
+
+double host_norm(tpdg_gpu_ctx ctx, const double* x, int64_t n, GmresWork& W) {
+  double* d = W.scal.as<double>();
+  if (ctx->nranks == 1) {
+    launch_norm(x, n, W.partial.as<double>(), d, W.counter.as<unsigned>(), ctx->stream);
+  } else {
+    launch_dot(x, x, n, W.partial.as<double>(), d, W.counter.as<unsigned>(), ctx->stream);
+    allreduce_scalar(ctx, d);
+    sqrt_inplace_kernel<<<1, 1, 0, ctx->stream>>>(d);
+    ++g_launches;
+  }
+  double h = 0.0;
+  TPDG_CUDA_CHECK(cudaMemcpyAsync(&h, d, sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
+  TPDG_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+  return h;
+}
+
+int run_gmres(tpdg_gpu_op op, tpdg_gpu_pc pc, const double* d_b, double* d_x, const tpdg_gpu_gmres_config& cfg,
+              int* iterations, double* hist, int hist_cap, int* converged_out) {
+  REQUIRE(cfg.tol > 0.0, TPDG_CONFIG, "GmresConfig: tol must be > 0");
+  REQUIRE(cfg.restart >= 1, TPDG_CONFIG, "GmresConfig: restart must be >= 1");
+  REQUIRE(cfg.max_iterations >= 1, TPDG_CONFIG, "GmresConfig: max_iterations must be >= 1");
+  tpdg_gpu_ctx ctx = op->ctx;
+  cudaStream_t st = ctx->stream;
+  const int64_t n = op->n_local_dofs;
+  const bool right = cfg.side == 0;
+  const int m = cfg.restart;
+  const bool multi = ctx->nranks > 1;
+  GmresWork W;
+  W.V.alloc(sizeof(double) * size_t(m + 1) * n);
+  W.z.alloc(sizeof(double) * n);
+  W.tmp.alloc(sizeof(double) * n);
+  W.r.alloc(sizeof(double) * n);
+  W.hcol.alloc(sizeof(double) * (m + 2));
+  W.partial.alloc(sizeof(double) * 148 * 4);
+  W.counter.alloc(sizeof(unsigned) * 4);
+  W.y.alloc(sizeof(double) * (m + 1));
+  W.scal.alloc(sizeof(double) * 4);
+  TPDG_CUDA_CHECK(cudaMemsetAsync(W.counter.p, 0, W.counter.bytes, st));
+  TPDG_CUDA_CHECK(cudaMemsetAsync(d_x, 0, sizeof(double) * n, st));
+  double* V = W.V.as<double>();
+  double* z = W.z.as<double>();
+  double* tmp = W.tmp.as<double>();
+  double* r = W.r.as<double>();
+  double* hc = W.hcol.as<double>();
+  double* part = W.partial.as<double>();
+  unsigned* ctr = W.counter.as<unsigned>();
+  if (pc) TPDG_CUDA_CHECK(cudaMemsetAsync(pc->status.p, 0, sizeof(int), st));
+
+  auto apply_pc = [&](const double* in, double* out) {
+    if (pc)
+      pc_apply_device(pc, in, out);
+    else
+      TPDG_CUDA_CHECK(cudaMemcpyAsync(out, in, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+  };
+
+  int its = 0, nh = 0;
+  bool conv = false;
+  double target;
+  if (right) {
+    target = cfg.tol * host_norm(ctx, d_b, n, W);
+  } else {
+    apply_pc(d_b, r);
+    target = cfg.tol * host_norm(ctx, r, n, W);
+  }
+  std::vector<double> h(size_t(m + 1) * m), cs(m), sn(m), g(m + 1), y(m + 1), col(m + 2);
+  if (target == 0.0) {
+    conv = true;
+  } else {
+    while (its < cfg.max_iterations) {
+      jv_device(op, d_x, tmp);
+      launch_sub(d_b, tmp, tmp, n, st);
+      double* rr = tmp;
+      if (!right) {
+        apply_pc(tmp, r);
+        rr = r;
+      }
+      const double beta = host_norm(ctx, rr, n, W);
+      if (beta <= target) {
+        conv = true;
+        break;
+      }
+      TPDG_CUDA_CHECK(cudaMemcpyAsync(W.scal.as<double>() + 1, &beta, sizeof(double), cudaMemcpyHostToDevice, st));
+      launch_scale_div(rr, W.scal.as<double>() + 1, V, n, st);
+      std::fill(g.begin(), g.end(), 0.0);
+      g[0] = beta;
+      std::fill(h.begin(), h.end(), 0.0);
+      int k = 0;
+      for (; k < m && its < cfg.max_iterations; ++k) {
+        ++its;
+        double* vk = V + size_t(k) * n;
+        double* w = V + size_t(k + 1) * n;
+        if (right) {
+          apply_pc(vk, z);
+          jv_device(op, z, w);
+        } else {
+          jv_device(op, vk, z);
+          apply_pc(z, w);
+        }
+        // MGS: h_j = <v_j, w>, w -= h_j v_j (fused passes)
+        for (int j = 0; j <= k; ++j) {
+          if (!multi) {
+            launch_mgs_step(w, j > 0 ? V + size_t(j - 1) * n : nullptr, hc + (j > 0 ? j - 1 : 0), V + size_t(j) * n,
+                            n, part, hc + j, ctr, st);
+          } else {
+            if (j > 0) launch_axpy_neg(w, hc + j - 1, V + size_t(j - 1) * n, n, st);
+            launch_dot(V + size_t(j) * n, w, n, part, hc + j, ctr, st);
+            allreduce_scalar(ctx, hc + j);
+          }
+        }
+        // w -= h_k v_k ; h_{k+1} = ||w||
+        if (!multi) {
+          launch_mgs_step(w, vk, hc + k, nullptr, n, part, hc + k + 1, ctr, st);
+        } else {
+          launch_axpy_neg(w, hc + k, vk, n, st);
+          launch_dot(w, w, n, part, hc + k + 1, ctr, st);
+          allreduce_scalar(ctx, hc + k + 1);
+          sqrt_inplace_kernel<<<1, 1, 0, st>>>(hc + k + 1);
+          ++g_launches;
+        }
+        launch_scale_div(w, hc + k + 1, w, n, st);
+        TPDG_CUDA_CHECK(cudaMemcpyAsync(col.data(), hc, sizeof(double) * (k + 2), cudaMemcpyDeviceToHost, st));
+        TPDG_CUDA_CHECK(cudaStreamSynchronize(st));
+        for (int j = 0; j <= k + 1; ++j) h[size_t(j) * m + k] = col[j];
+        // Givens (gmres.hpp:122-136)
+        for (int j = 0; j < k; ++j) {
+          const double t1 = h[size_t(j) * m + k], t2 = h[size_t(j + 1) * m + k];
+          h[size_t(j) * m + k] = cs[j] * t1 + sn[j] * t2;
+          h[size_t(j + 1) * m + k] = -sn[j] * t1 + cs[j] * t2;
+        }
+        const double t1 = h[size_t(k) * m + k], t2 = h[size_t(k + 1) * m + k];
+        const double denom = std::hypot(t1, t2);
+        cs[k] = denom == 0.0 ? 1.0 : t1 / denom;
+        sn[k] = denom == 0.0 ? 0.0 : t2 / denom;
+        h[size_t(k) * m + k] = denom;
+        h[size_t(k + 1) * m + k] = 0.0;
+        const double gk = g[k];
+        g[k] = cs[k] * gk;
+        g[k + 1] = -sn[k] * gk;
+        if (hist && nh < hist_cap) hist[nh] = std::abs(g[k + 1]);
+        ++nh;
+        if (std::abs(g[k + 1]) <= target) {
+          ++k;
+          break;
+        }
+      }
+      for (int i = k - 1; i >= 0; --i) {
+        double s = g[i];
+        for (int j = i + 1; j < k; ++j) s -= h[size_t(i) * m + j] * y[j];
+        y[i] = s / h[size_t(i) * m + i];
+      }
+      TPDG_CUDA_CHECK(cudaMemcpyAsync(W.y.p, y.data(), sizeof(double) * std::max(k, 1), cudaMemcpyHostToDevice, st));
+      launch_combine(V, n, W.y.as<double>(), k, tmp, n, st);
+      if (right) {
+        apply_pc(tmp, z);
+        launch_add(d_x, z, n, st);
+      } else {
+        launch_add(d_x, tmp, n, st);
+      }
+      if (nh > 0 && std::abs(g[k]) <= target) {
+        conv = true;
+        break;
+      }
+    }
+    if (!conv) {
+      jv_device(op, d_x, tmp);
+      launch_sub(d_b, tmp, tmp, n, st);
+      double* rr = tmp;
+      if (!right) {
+        apply_pc(tmp, r);
+        rr = r;
+      }
+      conv = host_norm(ctx, rr, n, W) <= target;
+    }
+  }
+  TPDG_CUDA_CHECK(cudaStreamSynchronize(st));
+  if (pc) {
+    int status = 0;
+    TPDG_CUDA_CHECK(cudaMemcpy(&status, pc->status.p, sizeof(int), cudaMemcpyDeviceToHost));
+    REQUIRE(status == 0, TPDG_SINGULAR, "sylvester_solve: singular diagonal pair during the preconditioner apply");
+  }
+  *iterations = its;
+  if (converged_out) *converged_out = conv ? 1 : 0;
+  if (!conv) {
+    set_error("gmres: no convergence within " + std::to_string(cfg.max_iterations) + " iterations");
+    return TPDG_CONVERGENCE;
+  }
+  return TPDG_OK;
+}
+
+tpdg_gpu_ksvd_config default_ksvd(const tpdg_gpu_ksvd_config* c) {
+  tpdg_gpu_ksvd_config k;
+  k.terms = 2;
+  k.lanczos_max_it = 0;
+  k.breakdown_tol = 1e-12;
+  k.seed = 0x5eedULL;
+  k.degenerate_tol = 1e-12;
+  if (c) k = *c;
+  return k;
+}
+
+// Build the fallback LUs of all blocks with kind == 0, then the DevPC view.
+void finish_pc(tpdg_gpu_pc pc) {
+  tpdg_gpu_op op = pc->op;
+  cudaStream_t st = op->ctx->stream;
+  pc->kind_h.assign(pc->nblk, 0);
+  TPDG_CUDA_CHECK(cudaMemcpyAsync(pc->kind_h.data(), pc->kind.p, sizeof(int) * pc->nblk, cudaMemcpyDeviceToHost, st));
+  TPDG_CUDA_CHECK(cudaStreamSynchronize(st));
+  std::vector<int> fb_blocks, slot(pc->nblk, -1);
+  const int bpe = op->s.small ? op->n_c : 1;
+  pc->fallbacks.clear();
+  for (int b = 0; b < pc->nblk; ++b)
+    if (pc->kind_h[b] == 0) {
+      slot[b] = int(fb_blocks.size());
+      fb_blocks.push_back(b);
+      pc->fallbacks.push_back(op->e_begin + b / bpe);
+      pc->fallbacks.push_back(op->s.small ? b % bpe : -1);
+    }
+  upload(pc->fb_slot, slot.data(), slot.size(), st);
+  pc->status.alloc(sizeof(int) * 2);
+  TPDG_CUDA_CHECK(cudaMemsetAsync(pc->status.p, 0, pc->status.bytes, st));
+  const int nfb = int(fb_blocks.size());
+  const int nb = op->s.small ? op->s.npe : op->n_c * op->s.npe;
+  if (nfb) {
+    DevBuf blocks, work;
+    upload(blocks, fb_blocks.data(), fb_blocks.size(), st);
+    pc->fb_lu.alloc(sizeof(double) * size_t(nfb) * nb * nb);
+    pc->fb_piv.alloc(sizeof(int) * size_t(nfb) * nb);
+    work.alloc(sizeof(double) * size_t(probe_grid(nb, nfb)) * probe_work_doubles(op->s));
+    launch_assemble_fallback(op->s, blocks.as<int>(), nfb, pc->fb_lu.as<double>(), work.as<double>(), st);
+    launch_dense_lu(nb, nfb, pc->fb_lu.as<double>(), pc->fb_piv.as<int>(), pc->status.as<int>() + 1, st);
+    TPDG_CUDA_CHECK(cudaStreamSynchronize(st));
+  }
+  DevPC& d = pc->pc;
+  d.dim = op->dim;
+  d.q = op->q;
+  d.n1 = (op->s.small ? 1 : op->n_c) * op->q;
+  d.nblk = pc->nblk;
+  d.blk_len = op->dim == 2 ? d.n1 * op->q : d.n1 * op->q * op->q;
+  d.rec_len = rec_len_of(op->dim, d.n1, op->q);
+  d.piv_len = piv_len_of(op->dim, d.n1, op->q);
+  d.rec = pc->rec.as<double>();
+  d.piv = pc->piv.as<int>();
+  d.kind = pc->kind.as<int>();
+  d.fb_slot = pc->fb_slot.as<int>();
+  d.fb_lu = nfb ? pc->fb_lu.as<double>() : nullptr;
+  d.fb_piv = nfb ? pc->fb_piv.as<int>() : nullptr;
+  d.status = pc->status.as<int>();
+}
+
+void alloc_records(tpdg_gpu_pc pc) {
+  tpdg_gpu_op op = pc->op;
+  const int n1 = (op->s.small ? 1 : op->n_c) * op->q;
+  pc->nblk = op->s.n_local * (op->s.small ? op->n_c : 1);
+  pc->raw_len = raw_len_of(op->dim, n1, op->q);
+  pc->raw.alloc(sizeof(double) * size_t(pc->nblk) * pc->raw_len);
+  pc->rec.alloc(sizeof(double) * size_t(pc->nblk) * rec_len_of(op->dim, n1, op->q));
+  pc->piv.alloc(sizeof(int) * size_t(pc->nblk) * piv_len_of(op->dim, n1, op->q));
+  pc->kind.alloc(sizeof(int) * size_t(pc->nblk));
+}
+
+void make_factors_all(tpdg_gpu_pc pc) {
+  tpdg_gpu_op op = pc->op;
+  const int n1 = (op->s.small ? 1 : op->n_c) * op->q;
+  const int grid = std::min(pc->nblk, 148 * 8);
+  DevBuf work;
+  work.alloc(sizeof(double) * size_t(grid) * (4 * std::max(n1, op->q) + 16));
+  launch_make_factors(op->dim, op->q, n1, pc->nblk, pc->raw.as<double>(), pc->rec.as<double>(), pc->piv.as<int>(),
+                      pc->kind.as<int>(), work.as<double>(), op->ctx->stream);
+  TPDG_CUDA_CHECK(cudaStreamSynchronize(op->ctx->stream));
+}
+
+} // namespace
+
+// ------------------------------------------------------------------------------------ C ABI
+extern "C" {
+
+const char* tpdg_gpu_last_error(void) { return g_last_error.c_str(); }
+const char* tpdg_gpu_version(void) { return "tpdg_gpu 0.1 (sm_100a)"; }
+
+int tpdg_gpu_nccl_unique_id(void* out128) {
+  return guarded([&] {
+    ncclUniqueId id;
+    NCCL_CHECK(ncclGetUniqueId(&id));
+    std::memcpy(out128, &id, sizeof(id));
+  });
+}
+
+int tpdg_gpu_ctx_create(int device, int rank, int nranks, const void* nccl_id, tpdg_gpu_ctx* out) {
+  return guarded([&] {
+    REQUIRE(out, TPDG_CONFIG, "ctx_create: null output");
+    REQUIRE(nranks >= 1 && rank >= 0 && rank < nranks, TPDG_CONFIG, "ctx_create: bad rank / nranks");
+    std::unique_ptr<tpdg_gpu_ctx_s> c(new tpdg_gpu_ctx_s);
+    c->device = device;
+    c->rank = rank;
+    c->nranks = nranks;
+    TPDG_CUDA_CHECK(cudaSetDevice(device));
+    TPDG_CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    if (nranks > 1) {
+      REQUIRE(nccl_id, TPDG_CONFIG, "ctx_create: nranks > 1 needs an ncclUniqueId");
+      ncclUniqueId id;
+      std::memcpy(&id, nccl_id, sizeof(id));
+      NCCL_CHECK(ncclCommInitRank(&c->comm, nranks, id, rank));
+    }
+    c->launches_at_create = g_launches;
+    *out = c.release();
+  });
+}
+
+int tpdg_gpu_ctx_destroy(tpdg_gpu_ctx ctx) {
+  return guarded([&] {
+    if (!ctx) return;
+    if (ctx->comm) ncclCommDestroy(ctx->comm);
+    if (ctx->stream) cudaStreamDestroy(ctx->stream);
+    delete ctx;
+  });
+}
+
+int tpdg_gpu_ctx_stream(tpdg_gpu_ctx ctx, void** stream) {
+  return guarded([&] { *stream = ctx->stream; });
+}
+
+int tpdg_gpu_ctx_sync(tpdg_gpu_ctx ctx) {
+  return guarded([&] { TPDG_CUDA_CHECK(cudaStreamSynchronize(ctx->stream)); });
+}
+
+int tpdg_gpu_ctx_launches(tpdg_gpu_ctx ctx, int64_t* count) {
+  return guarded([&] { *count = g_launches - ctx->launches_at_create; });
+}
+
+int tpdg_gpu_op_create(tpdg_gpu_ctx ctx, const tpdg_gpu_system* sys, double dt, int jacobian_only, int block_mode,
+                       int e_begin, int e_end, tpdg_gpu_op* out) {
+  return guarded([&] {
+    REQUIRE(ctx && sys && out, TPDG_CONFIG, "op_create: null argument");
+    REQUIRE(sys->dim == 2 || sys->dim == 3, TPDG_CONFIG, "op_create: dim must be 2 or 3");
+    REQUIRE(sys->n_c >= 1 && sys->p >= 1 && sys->mu >= sys->p + 1, TPDG_CONFIG, "op_create: bad n_c / p / mu");
+    REQUIRE(0 <= e_begin && e_begin <= e_end && e_end <= sys->n_elements, TPDG_SHAPE, "op_create: bad element range");
+    REQUIRE(block_mode == 0 || block_mode == 1, TPDG_CONFIG, "op_create: block_mode must be 0 (full) or 1 (small)");
+    std::unique_ptr<tpdg_gpu_op_s> op(new tpdg_gpu_op_s);
+    cudaStream_t st = ctx->stream;
+    op->ctx = ctx;
+    op->dim = sys->dim;
+    op->n_c = sys->n_c;
+    op->p = sys->p;
+    op->q = sys->p + 1;
+    op->mu = sys->mu;
+    op->e_begin = e_begin;
+    op->e_end = e_end;
+    op->n_global = sys->n_elements;
+    op->hash = sys->state_hash;
+    const int d = sys->dim, nc = sys->n_c, q = op->q, mu = op->mu;
+    const size_t nqv = d == 2 ? size_t(mu) * mu : size_t(mu) * mu * mu, nqf = nqv / mu;
+    const size_t npe = d == 2 ? size_t(q) * q : size_t(q) * q * q;
+    const size_t nl = size_t(e_end - e_begin);
+    op->n_local_dofs = int64_t(nl * nc * npe);
+    upload(op->g, sys->g, size_t(mu) * q, st);
+    upload(op->d, sys->d, size_t(mu) * q, st);
+    upload(op->gw, sys->gw, size_t(mu) * q, st);
+    upload(op->dw, sys->dw, size_t(mu) * q, st);
+    upload(op->w, sys->w, size_t(mu), st);
+    upload(op->jdet, sys->jdet + size_t(e_begin) * nqv, nl * nqv, st);
+    upload(op->face_w, sys->face_w + size_t(e_begin) * 2 * d * nqf, nl * 2 * d * nqf, st);
+    upload(op->dft, sys->dft + size_t(e_begin) * d * nqv * nc * nc, nl * d * nqv * nc * nc, st);
+    upload(op->dfm, sys->dfm + size_t(e_begin) * 2 * d * nqf * nc * nc, nl * 2 * d * nqf * nc * nc, st);
+    upload(op->dfp, sys->dfp + size_t(e_begin) * 2 * d * nqf * nc * nc, nl * 2 * d * nqf * nc * nc, st);
+    // connectivity: local ids for owned neighbours, halo slots (grouped by owner rank) otherwise
+    const int nranks = ctx->nranks;
+    // rank r owns the contiguous element range [E r / N, E (r+1) / N) (rows in 2D, slabs in 3D)
+    std::vector<int> owner_lo(nranks + 1);
+    for (int r = 0; r <= nranks; ++r) owner_lo[r] = int((int64_t(sys->n_elements) * r) / nranks);
+    if (nranks > 1)
+      REQUIRE(e_begin == owner_lo[ctx->rank] && e_end == owner_lo[ctx->rank + 1], TPDG_CONFIG,
+              "op_create: multi-rank element range must be [E r / N, E (r+1) / N)");
+    auto owner_of = [&](int e) {
+      int r = int(std::upper_bound(owner_lo.begin(), owner_lo.end(), e) - owner_lo.begin()) - 1;
+      return std::min(std::max(r, 0), nranks - 1);
+    };
+    std::vector<std::vector<int>> need(nranks);  // global ids needed from each rank
+    std::vector<int> conn(nl * 2 * d * 3);
+    for (size_t le = 0; le < nl; ++le)
+      for (int f = 0; f < 2 * d; ++f) {
+        const int64_t* fc = sys->conn + ((size_t(e_begin) + le) * 2 * d + f) * 3;
+        const int64_t nb = fc[0];
+        conn[(le * 2 * d + f) * 3 + 1] = int(fc[1]);
+        conn[(le * 2 * d + f) * 3 + 2] = int(fc[2]);
+        if (nb < 0) {
+          conn[(le * 2 * d + f) * 3] = -1;
+        } else if (nb >= e_begin && nb < e_end) {
+          conn[(le * 2 * d + f) * 3] = int(nb - e_begin);
+        } else {
+          REQUIRE(nranks > 1, TPDG_CONFIG, "op_create: neighbour outside the local range needs nranks > 1");
+          conn[(le * 2 * d + f) * 3] = -2 - int(nb);  // resolved below
+          need[owner_of(int(nb))].push_back(int(nb));
+        }
+      }
+    std::vector<int> halo_slot_of;  // sorted unique global ids -> slot
+    std::vector<int> halo_ids;
+    for (int r = 0; r < nranks; ++r) {
+      std::sort(need[r].begin(), need[r].end());
+      need[r].erase(std::unique(need[r].begin(), need[r].end()), need[r].end());
+    }
+    int slot = int(nl);
+    std::vector<std::pair<int, int>> gid_slot;
+    for (int r = 0; r < nranks; ++r) {
+      if (r == ctx->rank || need[r].empty()) continue;
+      tpdg_gpu_op_s::Peer p;
+      p.rank = r;
+      p.recv_first = slot - int(nl);
+      p.recv_count = int(need[r].size());
+      for (int gid : need[r]) gid_slot.push_back({gid, slot++});
+      op->peers.push_back(std::move(p));
+    }
+    std::sort(gid_slot.begin(), gid_slot.end());
+    for (auto& c : conn) (void)c;
+    for (size_t i = 0; i < conn.size(); i += 3)
+      if (conn[i] <= -2) {
+        const int gid = -2 - conn[i];
+        auto it = std::lower_bound(gid_slot.begin(), gid_slot.end(), std::make_pair(gid, -1));
+        conn[i] = it->second;
+      }
+    op->n_halo = slot - int(nl);
+    // Send lists: the elements of mine that peer r needs = my elements adjacent to r's range.
+    // Structured symmetric connectivity: r needs element x of mine iff x has a neighbour owned by r.
+    if (nranks > 1) {
+      for (int r = 0; r < nranks; ++r) {
+        if (r == ctx->rank) continue;
+        std::vector<int> send;
+        for (size_t le = 0; le < nl; ++le)
+          for (int f = 0; f < 2 * d; ++f) {
+            const int64_t nb = sys->conn[((size_t(e_begin) + le) * 2 * d + f) * 3];
+            if (nb >= 0 && owner_of(int(nb)) == r) {
+              send.push_back(int(le));
+              break;
+            }
+          }
+        if (send.empty()) continue;
+        auto it = std::find_if(op->peers.begin(), op->peers.end(), [&](const tpdg_gpu_op_s::Peer& p) { return p.rank == r; });
+        if (it == op->peers.end()) {
+          tpdg_gpu_op_s::Peer p;
+          p.rank = r;
+          p.recv_first = 0;
+          p.recv_count = 0;
+          op->peers.push_back(std::move(p));
+          it = op->peers.end() - 1;
+        }
+        it->send_local = send;  // ascending local id == ascending global id (contiguous ranges)
+        upload(it->send_idx, send.data(), send.size(), st);
+        it->send_buf.alloc(sizeof(double) * send.size() * nc * npe);
+      }
+      op->halo.alloc(sizeof(double) * std::max<size_t>(1, size_t(op->n_halo) * nc * npe));
+    }
+    upload(op->conn, conn.data(), conn.size(), st);
+    const double a = jacobian_only ? 0.0 : 1.0, b = jacobian_only ? 1.0 : -dt;
+    op->s = make_devsys(*op, block_mode, a, b);
+    op->io_a.alloc(sizeof(double) * std::max<int64_t>(1, op->n_local_dofs));
+    op->io_b.alloc(sizeof(double) * std::max<int64_t>(1, op->n_local_dofs));
+    TPDG_CUDA_CHECK(cudaStreamSynchronize(st));
+    *out = op.release();
+  });
+}
+
+int tpdg_gpu_op_destroy(tpdg_gpu_op op) {
+  return guarded([&] { delete op; });
+}
+
+int tpdg_gpu_op_local_size(tpdg_gpu_op op, int64_t* n_local) {
+  return guarded([&] { *n_local = op->n_local_dofs; });
+}
+
+int tpdg_gpu_op_check_hash(tpdg_gpu_op op, uint64_t expected_hash) {
+  return guarded([&] {
+    REQUIRE(op->hash == expected_hash, TPDG_CONFIG, "LinearizedOperator: stale linearization cache (state hash mismatch)");
+  });
+}
+
+int tpdg_gpu_jv(tpdg_gpu_op op, const double* d_in, double* d_out) {
+  return guarded([&] {
+    jv_device(op, d_in, d_out);
+    TPDG_CUDA_CHECK(cudaStreamSynchronize(op->ctx->stream));
+  });
+}
+
+int tpdg_gpu_jv_host(tpdg_gpu_op op, const double* h_in, double* h_out) {
+  return guarded([&] {
+    cudaStream_t st = op->ctx->stream;
+    const size_t bytes = sizeof(double) * op->n_local_dofs;
+    TPDG_CUDA_CHECK(cudaMemcpyAsync(op->io_a.p, h_in, bytes, cudaMemcpyHostToDevice, st));
+    jv_device(op, op->io_a.as<double>(), op->io_b.as<double>());
+    TPDG_CUDA_CHECK(cudaMemcpyAsync(h_out, op->io_b.p, bytes, cudaMemcpyDeviceToHost, st));
+    TPDG_CUDA_CHECK(cudaStreamSynchronize(st));
+  });
+}
+
+int tpdg_gpu_shuffled_host(tpdg_gpu_op op, int e, int comp, int transpose, const double* h_in, double* h_out) {
+  return guarded([&] {
+    REQUIRE(e >= 0 && e < op->s.n_local, TPDG_SHAPE, "shuffled: element out of range");
+    cudaStream_t st = op->ctx->stream;
+    const int ncb = op->s.small ? 1 : op->n_c;
+    const size_t m1 = size_t(ncb) * op->q, m2 = op->dim == 2 ? op->q : size_t(op->q) * op->q;
+    const size_t nin = transpose ? m1 * m1 : m2 * m2, nout = transpose ? m2 * m2 : m1 * m1;
+    DevBuf din, dout;
+    upload(din, h_in, nin, st);
+    dout.alloc(sizeof(double) * nout);
+    if (!op->shuf_ws.p) op->shuf_ws.alloc(sizeof(double) * shuffled_scratch_doubles(op->s));
+    launch_shuffled(op->s, e, comp, transpose, din.as<double>(), dout.as<double>(), op->shuf_ws.as<double>(), st);
+    TPDG_CUDA_CHECK(cudaMemcpyAsync(h_out, dout.p, sizeof(double) * nout, cudaMemcpyDeviceToHost, st));
+    TPDG_CUDA_CHECK(cudaStreamSynchronize(st));
+  });
+}
+
+int tpdg_gpu_form_ksvd(tpdg_gpu_op op, const tpdg_gpu_ksvd_config* cfg_in, tpdg_gpu_pc* out) {
+  return guarded([&] {
+    REQUIRE(op && out, TPDG_CONFIG, "form_ksvd: null argument");
+    const tpdg_gpu_ksvd_config cfg = default_ksvd(cfg_in);
+    REQUIRE(cfg.terms >= 1, TPDG_CONFIG, "LanczosConfig: requested_terms must be >= 1");
+    REQUIRE(cfg.breakdown_tol > 0.0, TPDG_CONFIG, "LanczosConfig: breakdown_tolerance must be > 0");
+    std::unique_ptr<tpdg_gpu_pc_s> pc(new tpdg_gpu_pc_s);
+    pc->op = op;
+    cudaStream_t st = op->ctx->stream;
+    alloc_records(pc.get());
+    const int q = op->q, ncb = op->s.small ? 1 : op->n_c;
+    const int64_t m2 = op->dim == 2 ? q : int64_t(q) * q;
+    std::vector<double> sv(size_t(m2 * m2)), sv2(size_t(q) * q);
+    seeded_unit_vector(m2 * m2, cfg.seed, sv.data());
+    seeded_unit_vector(int64_t(q) * q, cfg.seed, sv2.data());
+    DevBuf dsv, dsv2, work;
+    upload(dsv, sv.data(), sv.size(), st);
+    upload(dsv2, sv2.data(), sv2.size(), st);
+    const int J = std::max(cfg.lanczos_max_it > 0 ? cfg.lanczos_max_it : 2 * cfg.terms + 20, 22);
+    const size_t per = lanczos_work_doubles(op->s, J);
+    // persistent grid, bounded workspace (<= ~4 GiB)
+    int grid = std::min(pc->nblk, 148 * 8);
+    while (grid > 148 && double(grid) * per * 8.0 > 4.0 * (1 << 30)) grid /= 2;
+    if (pc->nblk > 0) {
+      work.alloc(sizeof(double) * size_t(grid) * per);
+      launch_lanczos_form(op->s, cfg, dsv.as<double>(), dsv2.as<double>(), pc->raw.as<double>(), nullptr,
+                          pc->kind.as<int>(), work.as<double>(), per, grid, st);
+      TPDG_CUDA_CHECK(cudaStreamSynchronize(st));
+      make_factors_all(pc.get());
+    }
+    (void)ncb;
+    finish_pc(pc.get());
+    *out = pc.release();
+  });
+}
+
+int tpdg_gpu_pc_import_factors(tpdg_gpu_op op, const double* h_factors, const int64_t* h_has, tpdg_gpu_pc* out) {
+  return guarded([&] {
+    std::unique_ptr<tpdg_gpu_pc_s> pc(new tpdg_gpu_pc_s);
+    pc->op = op;
+    cudaStream_t st = op->ctx->stream;
+    alloc_records(pc.get());
+    std::vector<double> raw(size_t(pc->nblk) * pc->raw_len, 0.0);
+    std::vector<int> kind(pc->nblk, 0);
+    size_t off = 0;
+    for (int b = 0; b < pc->nblk; ++b)
+      if (h_has[b]) {
+        std::copy(h_factors + off, h_factors + off + pc->raw_len, raw.begin() + size_t(b) * pc->raw_len);
+        off += pc->raw_len;
+        kind[b] = 1;
+      }
+    TPDG_CUDA_CHECK(cudaMemcpyAsync(pc->raw.p, raw.data(), sizeof(double) * raw.size(), cudaMemcpyHostToDevice, st));
+    TPDG_CUDA_CHECK(cudaMemcpyAsync(pc->kind.p, kind.data(), sizeof(int) * kind.size(), cudaMemcpyHostToDevice, st));
+    if (pc->nblk > 0) make_factors_all(pc.get());
+    finish_pc(pc.get());
+    *out = pc.release();
+  });
+}
+
+int tpdg_gpu_pc_destroy(tpdg_gpu_pc pc) {
+  return guarded([&] { delete pc; });
+}
+
+int tpdg_gpu_pc_num_fallbacks(tpdg_gpu_pc pc, int* n) {
+  return guarded([&] { *n = int(pc->fallbacks.size() / 2); });
+}
+
+int tpdg_gpu_pc_fallbacks(tpdg_gpu_pc pc, int64_t* pairs) {
+  return guarded([&] { std::copy(pc->fallbacks.begin(), pc->fallbacks.end(), pairs); });
+}
+
+int tpdg_gpu_pc_factor_len(tpdg_gpu_pc pc, int* len) {
+  return guarded([&] { *len = pc->raw_len; });
+}
+
+int tpdg_gpu_pc_export_factors(tpdg_gpu_pc pc, int blk, double* h_out, int* has) {
+  return guarded([&] {
+    REQUIRE(blk >= 0 && blk < pc->nblk, TPDG_SHAPE, "export_factors: block out of range");
+    TPDG_CUDA_CHECK(cudaMemcpy(h_out, pc->raw.as<double>() + size_t(blk) * pc->raw_len, sizeof(double) * pc->raw_len,
+                               cudaMemcpyDeviceToHost));
+    *has = pc->kind_h[blk];
+  });
+}
+
+int tpdg_gpu_pc_apply(tpdg_gpu_pc pc, const double* d_in, double* d_out) {
+  return guarded([&] {
+    pc_apply_device(pc, d_in, d_out);
+    TPDG_CUDA_CHECK(cudaStreamSynchronize(pc->op->ctx->stream));
+  });
+}
+
+int tpdg_gpu_pc_apply_host(tpdg_gpu_pc pc, const double* h_in, double* h_out) {
+  return guarded([&] {
+    tpdg_gpu_op op = pc->op;
+    cudaStream_t st = op->ctx->stream;
+    const size_t bytes = sizeof(double) * op->n_local_dofs;
+    TPDG_CUDA_CHECK(cudaMemsetAsync(pc->status.p, 0, sizeof(int), st));
+    TPDG_CUDA_CHECK(cudaMemcpyAsync(op->io_a.p, h_in, bytes, cudaMemcpyHostToDevice, st));
+    pc_apply_device(pc, op->io_a.as<double>(), op->io_b.as<double>());
+    TPDG_CUDA_CHECK(cudaMemcpyAsync(h_out, op->io_b.p, bytes, cudaMemcpyDeviceToHost, st));
+    int status = 0;
+    TPDG_CUDA_CHECK(cudaMemcpyAsync(&status, pc->status.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+    TPDG_CUDA_CHECK(cudaStreamSynchronize(st));
+    REQUIRE(status == 0, TPDG_SINGULAR, "sylvester_solve: singular diagonal pair");
+  });
+}
+
+int tpdg_gpu_gmres(tpdg_gpu_op op, tpdg_gpu_pc pc, const double* d_b, double* d_x, const tpdg_gpu_gmres_config* cfg,
+                   int* iterations, double* hist, int hist_cap, int* converged) {
+  int rc = TPDG_OK;
+  const int g = guarded([&] { rc = run_gmres(op, pc, d_b, d_x, *cfg, iterations, hist, hist_cap, converged); });
+  return g != TPDG_OK ? g : rc;
+}
+
+int tpdg_gpu_gmres_host(tpdg_gpu_op op, tpdg_gpu_pc pc, const double* h_b, double* h_x,
+                        const tpdg_gpu_gmres_config* cfg, int* iterations, double* hist, int hist_cap,
+                        int* converged) {
+  int rc = TPDG_OK;
+  const int g = guarded([&] {
+    cudaStream_t st = op->ctx->stream;
+    const size_t bytes = sizeof(double) * op->n_local_dofs;
+    TPDG_CUDA_CHECK(cudaMemcpyAsync(op->io_a.p, h_b, bytes, cudaMemcpyHostToDevice, st));
+    rc = run_gmres(op, pc, op->io_a.as<double>(), op->io_b.as<double>(), *cfg, iterations, hist, hist_cap, converged);
+    TPDG_CUDA_CHECK(cudaMemcpyAsync(h_x, op->io_b.p, bytes, cudaMemcpyDeviceToHost, st));
+    TPDG_CUDA_CHECK(cudaStreamSynchronize(st));
+  });
+  return g != TPDG_OK ? g : rc;
+}
+
+// ---- host setup
+struct tpdg_setup_s {
+  Setup s;
+};
+
+int tpdg_setup_advection(int case_kind, const double* vel, int nx, int ny, int nz, int p, int periodic,
+                         tpdg_setup* out) {
+  return guarded([&] {
+    REQUIRE(case_kind >= 0 && case_kind <= 2, TPDG_CONFIG, "setup: case_kind must be 0, 1 or 2");
+    REQUIRE(nx >= 1 && ny >= 1 && (case_kind != 2 || nz >= 1) && p >= 1, TPDG_CONFIG, "setup: bad sizes");
+    std::unique_ptr<tpdg_setup_s> s(new tpdg_setup_s);
+    const double zero[3] = {0, 0, 0};
+    setup_advection(case_kind, vel ? vel : zero, nx, ny, nz, p, periodic, s->s);
+    *out = s.release();
+  });
+}
+
+int tpdg_setup_system(tpdg_setup st, tpdg_gpu_system* sys) {
+  return guarded([&] {
+    const Setup& s = st->s;
+    sys->dim = s.dim;
+    sys->n_c = s.n_c;
+    sys->p = s.p;
+    sys->mu = s.mu;
+    sys->n_elements = s.n_elements;
+    sys->g = s.g.data();
+    sys->d = s.d.data();
+    sys->gw = s.gw.data();
+    sys->dw = s.dw.data();
+    sys->w = s.w.data();
+    sys->jdet = s.jdet.data();
+    sys->face_w = s.face_w.data();
+    sys->conn = s.conn.data();
+    sys->dft = s.dft.data();
+    sys->dfm = s.dfm.data();
+    sys->dfp = s.dfp.data();
+    sys->state_hash = s.state_hash;
+  });
+}
+
+int tpdg_setup_destroy(tpdg_setup s) {
+  return guarded([&] { delete s; });
+}
+
+int tpdg_uniform_vector(uint64_t seed, int64_t n, double scale, double* out) {
+  return guarded([&] { uniform_vector(seed, n, scale, out); });
+}
+
+int tpdg_seeded_unit_vector(int64_t n, uint64_t seed, double* out) {
+  return guarded([&] { seeded_unit_vector(n, seed, out); });
+}
+
+} // extern "C"

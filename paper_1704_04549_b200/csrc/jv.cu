@@ -1,0 +1,422 @@
+// Matrix-free DG operator (a M + b J) v, sum-factorized, one CTA per element.
+//
+// Restates jacobian_apply (reference ops/linearized.hpp:201-240) = element_diag_apply
+// (:107-162: eval_at_quad, mass + contravariant-flux fields, integrate_back, own-trace face
+// terms) + the neighbour coupling through dfp (:216-236), with face_trace / face_lift /
+// neighbor_trace from ops/discretization.hpp:89-181.
+//
+// Parity contract: rel-L2 <= 1e-12 against the reference. The volume and face
+// contributions are fused (one lift per face for own + neighbour trace, one combined
+// integrate-back for the mass and flux fields), so the summation order differs from the
+// reference's; the reference's own FMA/no-FMA builds differ by ~2.5e-16 here.
+//
+// HBM layout (reference orders, read once per launch): v [e][c][tensor, x fastest],
+// jdet [e][mu^d], dft [e][dir][mu^d][nc][nc], dfm/dfp [e][f][mu^(d-1)][nc][nc], face_w.
+#include "tpdg_internal.hpp"
+
+namespace tpdg_gpu {
+
+namespace {
+
+__device__ __forceinline__ const double* nbr_block(const DevSys& s, const double* vin, const double* halo, int nbr) {
+  const size_t blk = size_t(s.n_c) * s.npe;
+  return nbr < s.n_local ? vin + size_t(nbr) * blk : halo + size_t(nbr - s.n_local) * blk;
+}
+
+// ------------------------------------------------------------------------------------ 2D
+__global__ void __launch_bounds__(256) jv2d_kernel(DevSys s, const double* __restrict__ vin,
+                                                    const double* __restrict__ halo, double* __restrict__ vout) {
+  extern __shared__ double sm[];
+  const int e = blockIdx.x;
+  const int q = s.q, mu = s.mu, nc = s.n_c, qq = q * q, mm = mu * mu;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  double* sG = sm;                 // mu*q
+  double* sGW = sG + mu * q;       // q*mu
+  double* sDW = sGW + q * mu;      // q*mu
+  double* sv = sDW + q * mu;       // nc*q*q
+  double* st = sv + nc * qq;       // nc*q*mu    t[c][j][al]
+  double* sval = st + nc * q * mu; // nc*mu*mu   vals[c][be][al]
+  double* sf = sval + nc * mm;     // 3*nc*mu*mu fields M, F0, F1 [r][be][al]
+  double* sA = sf + 3 * nc * mm;   // nc*mu*q    A[r][be][i]
+  double* sB = sA + nc * mu * q;   // nc*mu*q
+  double* str = sB + nc * mu * q;  // 2*4*nc*mu  own / neighbour traces [side][f][c][a]
+  double* sg = str + 8 * nc * mu;  // 4*nc*mu    lifted face data [f][r][a]
+
+  for (int i = tid; i < mu * q; i += nt) {
+    sG[i] = s.g[i];
+    sGW[i] = s.gw[i];
+    sDW[i] = s.dw[i];
+  }
+  const double* ve = vin + size_t(e) * nc * qq;
+  for (int i = tid; i < nc * qq; i += nt) sv[i] = ve[i];
+  __syncthreads();
+
+  // eval_at_quad: x then y contraction with G.
+  for (int idx = tid; idx < nc * q * mu; idx += nt) {
+    const int al = idx % mu, j = (idx / mu) % q, c = idx / (mu * q);
+    const double* row = sv + c * qq + j * q;
+    double acc = 0.0;
+    for (int i = 0; i < q; ++i) acc = fma(sG[al * q + i], row[i], acc);
+    st[idx] = acc;
+  }
+  // own + neighbour face traces (need only sv / global v)
+  for (int idx = tid; idx < 8 * nc * mu; idx += nt) {
+    const int a = idx % mu, c = (idx / mu) % nc, f = (idx / (mu * nc)) % 4, side = idx / (4 * mu * nc);
+    const int* fc = s.conn + (size_t(e) * 4 + f) * 3;
+    double acc = 0.0;
+    if (side == 0) {
+      const int layer = (f % 2) == 0 ? 0 : q - 1;
+      const double* cf = sv + c * qq;
+      if (f / 2 == 0)
+        for (int j = 0; j < q; ++j) acc = fma(sG[a * q + j], cf[j * q + layer], acc);
+      else
+        for (int j = 0; j < q; ++j) acc = fma(sG[a * q + j], cf[layer * q + j], acc);
+    } else if (fc[0] >= 0) {
+      const int nf = fc[1];
+      const int aa = fc[2] == 0 ? a : mu - 1 - a;  // orient_face_coords, dg/mesh.hpp:57-67
+      const int layer = (nf % 2) == 0 ? 0 : q - 1;
+      const double* cf = nbr_block(s, vin, halo, fc[0]) + size_t(c) * qq;
+      if (nf / 2 == 0)
+        for (int j = 0; j < q; ++j) acc = fma(sG[aa * q + j], cf[j * q + layer], acc);
+      else
+        for (int j = 0; j < q; ++j) acc = fma(sG[aa * q + j], cf[layer * q + j], acc);
+    }
+    str[idx] = acc;
+  }
+  __syncthreads();
+  for (int idx = tid; idx < nc * mm; idx += nt) {
+    const int al = idx % mu, be = (idx / mu) % mu, c = idx / mm;
+    const double* tc = st + c * q * mu;
+    double acc = 0.0;
+    for (int j = 0; j < q; ++j) acc = fma(sG[be * q + j], tc[j * mu + al], acc);
+    sval[idx] = acc;
+  }
+  // face data g[f][r][a] = -b fw (dfm tm + dfp tp)
+  for (int idx = tid; idx < 4 * nc * mu; idx += nt) {
+    const int a = idx % mu, r = (idx / mu) % nc, f = idx / (mu * nc);
+    const size_t fq = (size_t(e) * 4 + f) * mu + a;
+    const double* dfm = s.dfm + fq * nc * nc + r * nc;
+    const double* dfp = s.dfp + fq * nc * nc + r * nc;
+    const double* tm = str + (f * nc) * mu + a;
+    const double* tp = str + ((4 + f) * nc) * mu + a;
+    double acc = 0.0;
+    if (!s.small) {
+      for (int c = 0; c < nc; ++c) acc = fma(dfm[c], tm[c * mu], fma(dfp[c], tp[c * mu], acc));
+    } else {
+      acc = fma(dfm[r], tm[r * mu], dfp[r] * tp[r * mu]);
+    }
+    sg[idx] = -s.b * s.face_w[fq] * acc;
+  }
+  __syncthreads();
+  // point-wise fields: M = a jd vals_r ; F_dir = b sum_c dft[dir][q][r][c] vals_c
+  for (int idx = tid; idx < nc * mm; idx += nt) {
+    const int qv = idx % mm, r = idx / mm;
+    const double* d0 = s.dft + ((size_t(e) * 2 + 0) * mm + qv) * nc * nc + r * nc;
+    const double* d1 = s.dft + ((size_t(e) * 2 + 1) * mm + qv) * nc * nc + r * nc;
+    double f0 = 0.0, f1 = 0.0;
+    if (!s.small) {
+      for (int c = 0; c < nc; ++c) {
+        const double vc = sval[c * mm + qv];
+        f0 = fma(d0[c], vc, f0);
+        f1 = fma(d1[c], vc, f1);
+      }
+    } else {
+      f0 = d0[r] * sval[r * mm + qv];
+      f1 = d1[r] * sval[r * mm + qv];
+    }
+    sf[idx] = s.a * s.jdet[size_t(e) * mm + qv] * sval[idx];
+    sf[nc * mm + idx] = s.b * f0;
+    sf[2 * nc * mm + idx] = s.b * f1;
+  }
+  __syncthreads();
+  // integrate_back, x direction: A = GW M + DW F0 ; B = GW F1
+  for (int idx = tid; idx < nc * mu * q; idx += nt) {
+    const int i = idx % q, be = (idx / q) % mu, r = idx / (q * mu);
+    const double* M = sf + r * mm + be * mu;
+    const double* F0 = sf + nc * mm + r * mm + be * mu;
+    const double* F1 = sf + 2 * nc * mm + r * mm + be * mu;
+    double acc_a = 0.0, acc_b = 0.0;
+    for (int al = 0; al < mu; ++al) {
+      acc_a = fma(sGW[i * mu + al], M[al], fma(sDW[i * mu + al], F0[al], acc_a));
+      acc_b = fma(sGW[i * mu + al], F1[al], acc_b);
+    }
+    sA[idx] = acc_a;
+    sB[idx] = acc_b;
+  }
+  __syncthreads();
+  // y direction + face lifts, written straight to HBM
+  double* oe = vout + size_t(e) * nc * qq;
+  for (int idx = tid; idx < nc * qq; idx += nt) {
+    const int i = idx % q, j = (idx / q) % q, r = idx / qq;
+    const double* A = sA + r * mu * q + i;
+    const double* B = sB + r * mu * q + i;
+    double acc = 0.0;
+    for (int be = 0; be < mu; ++be) acc = fma(sGW[j * mu + be], A[be * q], fma(sDW[j * mu + be], B[be * q], acc));
+    // face_lift: x faces hit column i = layer at row j, y faces row j = layer at column i
+    if (i == 0 || i == q - 1) {
+      const double* gf = sg + ((i == 0 ? 0 : 1) * nc + r) * mu;
+      for (int a = 0; a < mu; ++a) acc = fma(sG[a * q + j], gf[a], acc);
+    }
+    if (j == 0 || j == q - 1) {
+      const double* gf = sg + ((j == 0 ? 2 : 3) * nc + r) * mu;
+      for (int a = 0; a < mu; ++a) acc = fma(sG[a * q + i], gf[a], acc);
+    }
+    oe[idx] = acc;
+  }
+}
+
+size_t jv2d_smem(const DevSys& s) {
+  const int q = s.q, mu = s.mu, nc = s.n_c;
+  return sizeof(double) * size_t(3 * mu * q + nc * q * q + nc * q * mu + 4 * nc * mu * mu + 2 * nc * mu * q +
+                                 12 * nc * mu);
+}
+
+// ------------------------------------------------------------------------------------ 3D
+// Face f: axis = f/2, tangents (dg/mesh.hpp:47-52): axis0 -> (y,z), axis1 -> (x,z), axis2 -> (x,y).
+__device__ __forceinline__ int flat_face_node(int q, int f, int j0, int j1) {
+  const int axis = f / 2, layer = (f % 2) == 0 ? 0 : q - 1;
+  int idx[3];
+  idx[axis] = layer;
+  idx[axis == 0 ? 1 : 0] = j0;
+  idx[axis == 2 ? 1 : 2] = j1;
+  return (idx[2] * q + idx[1]) * q + idx[0];
+}
+
+__global__ void __launch_bounds__(256) jv3d_kernel(DevSys s, const double* __restrict__ vin,
+                                                    const double* __restrict__ halo, double* __restrict__ vout) {
+  extern __shared__ double sm[];
+  const int e = blockIdx.x;
+  const int q = s.q, mu = s.mu, nc = s.n_c;
+  const int q3 = q * q * q, m3 = mu * mu * mu, m2 = mu * mu, q2 = q * q;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  double* sG = sm;
+  double* sGW = sG + mu * q;
+  double* sDW = sGW + q * mu;
+  double* sv = sDW + q * mu;          // nc*q^3
+  double* sval = sv + nc * q3;        // nc*mu^3
+  double* sbuf = sval + nc * m3;      // big scratch: max(t1+t2 eval, fields + X + Y)
+  // eval temporaries
+  double* t1 = sbuf;                  // nc * q*q*mu  [c][k][j][al]
+  double* t2 = t1 + nc * q2 * mu;     // nc * q*mu*mu [c][k][be][al]
+  // per-r temporaries
+  double* fM = sbuf;                  // 4 fields mu^3: M, F0, F1, F2
+  double* Xa = fM + 4 * m3;           // mu*mu*q [ga][be][i]
+  double* Xb = Xa + m2 * q;
+  double* Xc = Xb + m2 * q;
+  double* Ya = Xc + m2 * q;           // mu*q*q [ga][j][i]
+  double* Yc = Ya + mu * q2;
+  double* str = Yc + mu * q2;         // 2*6*nc*m2 traces
+  double* wa = str + 12 * nc * m2;    // trace temp: 12*nc*q*mu
+  double* sg = wa + 12 * nc * q * mu; // 6*nc*m2 face data
+  double* sacc = sg + 6 * nc * m2;    // nc*q^3 output accumulator
+
+  for (int i = tid; i < mu * q; i += nt) {
+    sG[i] = s.g[i];
+    sGW[i] = s.gw[i];
+    sDW[i] = s.dw[i];
+  }
+  const double* ve = vin + size_t(e) * nc * q3;
+  for (int i = tid; i < nc * q3; i += nt) sv[i] = ve[i];
+  __syncthreads();
+  // ---- eval_at_quad
+  for (int idx = tid; idx < nc * q2 * mu; idx += nt) {
+    const int al = idx % mu, jk = (idx / mu) % q2, c = idx / (mu * q2);
+    const double* row = sv + c * q3 + jk * q;
+    double acc = 0.0;
+    for (int i = 0; i < q; ++i) acc = fma(sG[al * q + i], row[i], acc);
+    t1[idx] = acc;
+  }
+  __syncthreads();
+  for (int idx = tid; idx < nc * q * m2; idx += nt) {
+    const int al = idx % mu, be = (idx / mu) % mu, k = (idx / m2) % q, c = idx / (m2 * q);
+    const double* col = t1 + (c * q + k) * q * mu + al;
+    double acc = 0.0;
+    for (int j = 0; j < q; ++j) acc = fma(sG[be * q + j], col[j * mu], acc);
+    t2[idx] = acc;
+  }
+  __syncthreads();
+  for (int idx = tid; idx < nc * m3; idx += nt) {
+    const int ab = idx % m2, ga = (idx / m2) % mu, c = idx / m3;
+    const double* col = t2 + c * q * m2 + ab;
+    double acc = 0.0;
+    for (int k = 0; k < q; ++k) acc = fma(sG[ga * q + k], col[k * m2], acc);
+    sval[idx] = acc;
+  }
+  __syncthreads();
+  // ---- face traces (own: side 0, neighbour: side 1), two-stage G along the tangents
+  for (int idx = tid; idx < 12 * nc * q * mu; idx += nt) {
+    const int a = idx % mu, j1 = (idx / mu) % q, c = (idx / (mu * q)) % nc, f = (idx / (mu * q * nc)) % 6;
+    const int side = idx / (6 * mu * q * nc);
+    const int* fc = s.conn + (size_t(e) * 6 + f) * 3;
+    double acc = 0.0;
+    if (side == 0) {
+      const double* cf = sv + c * q3;
+      for (int j0 = 0; j0 < q; ++j0) acc = fma(sG[a * q + j0], cf[flat_face_node(q, f, j0, j1)], acc);
+    } else if (fc[0] >= 0) {
+      const double* cf = nbr_block(s, vin, halo, fc[0]) + size_t(c) * q3;
+      for (int j0 = 0; j0 < q; ++j0) acc = fma(sG[a * q + j0], cf[flat_face_node(q, fc[1], j0, j1)], acc);
+    }
+    wa[idx] = acc;  // [side][f][c][j1][a]
+  }
+  __syncthreads();
+  for (int idx = tid; idx < 12 * nc * m2; idx += nt) {
+    const int a = idx % mu, bb = (idx / mu) % mu, rest = idx / m2;  // rest = (side*6 + f)*nc + c
+    const double* w = wa + size_t(rest) * q * mu + a;
+    double acc = 0.0;
+    for (int j1 = 0; j1 < q; ++j1) acc = fma(sG[bb * q + j1], w[j1 * mu], acc);
+    str[idx] = acc;  // [side][f][c][b][a] in the face's own (a, b) enumeration
+  }
+  __syncthreads();
+  for (int idx = tid; idx < 6 * nc * m2; idx += nt) {
+    const int qf = idx % m2, r = (idx / m2) % nc, f = idx / (m2 * nc);
+    const int* fc = s.conn + (size_t(e) * 6 + f) * 3;
+    const size_t fq = (size_t(e) * 6 + f) * m2 + qf;
+    const double* dfm = s.dfm + fq * nc * nc + r * nc;
+    const double* dfp = s.dfp + fq * nc * nc + r * nc;
+    // neighbour trace permuted into this face's enumeration (orient_face_coords, dg/mesh.hpp:57-67)
+    const int qa = qf % mu, qb = qf / mu;
+    const int code = fc[2];
+    int u = (code & 4) ? qb : qa, v = (code & 4) ? qa : qb;
+    if (code & 1) u = mu - 1 - u;
+    if (code & 2) v = mu - 1 - v;
+    const int qn = v * mu + u;
+    const double* tm = str + (f * nc) * m2;
+    const double* tp = str + ((6 + f) * nc) * m2;
+    double acc = 0.0;
+    if (!s.small) {
+      for (int c = 0; c < nc; ++c) acc = fma(dfm[c], tm[c * m2 + qf], fma(dfp[c], tp[c * m2 + qn], acc));
+    } else {
+      acc = fma(dfm[r], tm[r * m2 + qf], dfp[r] * tp[r * m2 + qn]);
+    }
+    sg[idx] = -s.b * s.face_w[fq] * acc;
+  }
+  __syncthreads();
+  // first stage of face_lift: la[f][r][j0][b] = sum_a G(a, j0) g[f][r][b][a]   (reuses wa)
+  double* la = wa;
+  for (int idx = tid; idx < 6 * nc * q * mu; idx += nt) {
+    const int bb = idx % mu, j0 = (idx / mu) % q, fr = idx / (mu * q);
+    const double* gf = sg + fr * m2 + bb * mu;
+    double acc = 0.0;
+    for (int a = 0; a < mu; ++a) acc = fma(sG[a * q + j0], gf[a], acc);
+    la[idx] = acc;
+  }
+  __syncthreads();
+  // ---- per output component r: fields, three integrate_back contractions
+  for (int r = 0; r < nc; ++r) {
+    for (int idx = tid; idx < m3; idx += nt) {
+      const double* d0 = s.dft + ((size_t(e) * 3 + 0) * m3 + idx) * nc * nc + r * nc;
+      const double* d1 = s.dft + ((size_t(e) * 3 + 1) * m3 + idx) * nc * nc + r * nc;
+      const double* d2 = s.dft + ((size_t(e) * 3 + 2) * m3 + idx) * nc * nc + r * nc;
+      double f0 = 0.0, f1 = 0.0, f2 = 0.0;
+      if (!s.small) {
+        for (int c = 0; c < nc; ++c) {
+          const double vc = sval[c * m3 + idx];
+          f0 = fma(d0[c], vc, f0);
+          f1 = fma(d1[c], vc, f1);
+          f2 = fma(d2[c], vc, f2);
+        }
+      } else {
+        const double vc = sval[r * m3 + idx];
+        f0 = d0[r] * vc;
+        f1 = d1[r] * vc;
+        f2 = d2[r] * vc;
+      }
+      fM[idx] = s.a * s.jdet[size_t(e) * m3 + idx] * sval[r * m3 + idx];
+      fM[m3 + idx] = s.b * f0;
+      fM[2 * m3 + idx] = s.b * f1;
+      fM[3 * m3 + idx] = s.b * f2;
+    }
+    __syncthreads();
+    // x: Xa = GW M + DW F0 ; Xb = GW F1 ; Xc = GW F2
+    for (int idx = tid; idx < m2 * q; idx += nt) {
+      const int i = idx % q, gb = idx / q;  // gb = ga*mu + be
+      const double* M = fM + gb * mu;
+      double xa = 0.0, xb = 0.0, xc = 0.0;
+      for (int al = 0; al < mu; ++al) {
+        const double gw = sGW[i * mu + al];
+        xa = fma(gw, M[al], fma(sDW[i * mu + al], M[m3 + al], xa));
+        xb = fma(gw, M[2 * m3 + al], xb);
+        xc = fma(gw, M[3 * m3 + al], xc);
+      }
+      Xa[idx] = xa;
+      Xb[idx] = xb;
+      Xc[idx] = xc;
+    }
+    __syncthreads();
+    // y: Ya = GW Xa + DW Xb ; Yc = GW Xc
+    for (int idx = tid; idx < mu * q2; idx += nt) {
+      const int i = idx % q, j = (idx / q) % q, ga = idx / q2;
+      double ya = 0.0, yc = 0.0;
+      for (int be = 0; be < mu; ++be) {
+        const int src = (ga * mu + be) * q + i;
+        ya = fma(sGW[j * mu + be], Xa[src], fma(sDW[j * mu + be], Xb[src], ya));
+        yc = fma(sGW[j * mu + be], Xc[src], yc);
+      }
+      Ya[idx] = ya;
+      Yc[idx] = yc;
+    }
+    __syncthreads();
+    // z: out = GW Ya + DW Yc
+    for (int idx = tid; idx < q3; idx += nt) {
+      const int ij = idx % q2, k = idx / q2;
+      double acc = 0.0;
+      for (int ga = 0; ga < mu; ++ga) acc = fma(sGW[k * mu + ga], Ya[ga * q2 + ij], fma(sDW[k * mu + ga], Yc[ga * q2 + ij], acc));
+      sacc[r * q3 + idx] = acc;
+    }
+    __syncthreads();
+  }
+  // ---- face lifts (face_lift, ops/discretization.hpp:148-165): layer nodes only, gathered per node
+  double* oe = vout + size_t(e) * nc * q3;
+  for (int idx = tid; idx < nc * q3; idx += nt) {
+    const int i = idx % q, j = (idx / q) % q, k = (idx / q2) % q, r = idx / q3;
+    double acc = sacc[idx];
+    const int pos[3] = {i, j, k};
+    for (int axis = 0; axis < 3; ++axis) {
+      const int p = pos[axis];
+      if (p != 0 && p != q - 1) continue;
+      const int f = 2 * axis + (p == 0 ? 0 : 1);
+      const int j0 = pos[axis == 0 ? 1 : 0], j1 = pos[axis == 2 ? 1 : 2];
+      const double* lf = la + ((f * nc + r) * q + j0) * mu;
+      double sacc2 = 0.0;
+      for (int bb = 0; bb < mu; ++bb) sacc2 = fma(sG[bb * q + j1], lf[bb], sacc2);
+      acc += sacc2;
+    }
+    oe[idx] = acc;
+  }
+}
+
+size_t jv3d_smem(const DevSys& s) {
+  const size_t q = s.q, mu = s.mu, nc = s.n_c;
+  const size_t q3 = q * q * q, m3 = mu * mu * mu, m2 = mu * mu, q2 = q * q;
+  const size_t eval = nc * q2 * mu + nc * q * m2;
+  const size_t per_r = 4 * m3 + 3 * m2 * q + 2 * mu * q2 + 12 * nc * m2 + 12 * nc * q * mu + 6 * nc * m2 + nc * q3;
+  return sizeof(double) * (3 * mu * q + nc * q3 + nc * m3 + (eval > per_r ? eval : per_r));
+}
+
+} // namespace
+
+size_t jv_smem_bytes(const DevSys& s) { return s.dim == 2 ? jv2d_smem(s) : jv3d_smem(s); }
+
+void launch_jv(const DevSys& s, const double* vin, const double* halo, double* vout, cudaStream_t st) {
+  if (s.n_local == 0) return;
+  const size_t smem = jv_smem_bytes(s);
+  if (s.dim == 2) {
+    static size_t configured = 0;
+    if (smem > configured) {
+      TPDG_CUDA_CHECK(cudaFuncSetAttribute(jv2d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      configured = smem;
+    }
+    jv2d_kernel<<<s.n_local, 256, smem, st>>>(s, vin, halo, vout);
+  } else {
+    static size_t configured = 0;
+    if (smem > configured) {
+      TPDG_CUDA_CHECK(cudaFuncSetAttribute(jv3d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+      configured = smem;
+    }
+    jv3d_kernel<<<s.n_local, 256, smem, st>>>(s, vin, halo, vout);
+  }
+  TPDG_CUDA_CHECK(cudaGetLastError());
+  ++g_launches;
+}
+
+} // namespace tpdg_gpu

@@ -1,0 +1,117 @@
+// Internal declarations shared by the C-ABI layer (capi.cu), the kernels and the host setup.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "tpdg_gpu.h"
+
+namespace tpdg_gpu {
+
+// ---------------------------------------------------------------- errors
+struct Failure {
+  int status;
+  std::string what;
+};
+void set_error(const std::string& what);
+
+#define TPDG_CUDA_CHECK(expr)                                                                         \
+  do {                                                                                                \
+    cudaError_t err__ = (expr);                                                                       \
+    if (err__ != cudaSuccess)                                                                         \
+      throw ::tpdg_gpu::Failure{TPDG_CUDA, std::string(#expr) + ": " + cudaGetErrorString(err__)};    \
+  } while (0)
+
+// ---------------------------------------------------------------- host setup
+struct Setup {
+  int dim = 2, n_c = 1, p = 1, mu = 3, n_elements = 0;
+  std::vector<double> g, d, gw, dw, w, qpoints, jdet, face_w, dft, dfm, dfp, vol_x;
+  std::vector<int64_t> conn;
+  uint64_t state_hash = 0;
+};
+int setup_advection(int kind, const double* vel, int nx, int ny, int nz, int p, int periodic, Setup& s);
+void uniform_vector(uint64_t seed, int64_t n, double scale, double* out);
+void seeded_unit_vector(int64_t n, uint64_t seed, double* out);
+
+// ---------------------------------------------------------------- device views (POD, by value)
+// Discretization + linearization of the local elements, reference layouts.
+struct DevSys {
+  int dim, n_c, q, mu, npe, nqv, nqf, n_local, n_halo;
+  int small;          // BlockMode::small
+  double a, b;        // mass / jacobian coefficients (ops/linearized.hpp:177-178)
+  const double *g, *d, *gw, *dw, *w;
+  const double *jdet, *face_w, *dft, *dfm, *dfp;  // local element 0 first
+  const int* conn;    // [n_local][2d][3]; neighbor index < n_local: local, >= n_local: halo slot
+};
+
+// Formed KSVD preconditioner, device side. One factor record per block (element, or element x
+// component in small mode); record layout (doubles), n1 = ncb*q:
+//   2D: LU(A2) n1^2 | LU(B1) q^2 | Q1 n1^2 | T1 n1^2 | Q2 q^2 | T2 q^2
+//   3D: LU(A1) n1^2 | LU(B2) q^2 | LU(C1) q^2 | Q1 q^2 | T1 q^2 | Q2 q^2 | T2 q^2
+// plus int pivots  2D: n1 + q ; 3D: n1 + 2q.
+struct DevPC {
+  int dim, q, n1, nblk, blk_len;
+  int rec_len, piv_len;
+  const double* rec;     // [nblk][rec_len]
+  const int* piv;        // [nblk][piv_len]
+  const int* kind;       // [nblk]: 1 = Kronecker factors, 0 = dense fallback
+  const int* fb_slot;    // [nblk]: slot into fb_lu for fallback blocks, -1 otherwise
+  const double* fb_lu;   // [n_fb][blk_len^2]
+  const int* fb_piv;     // [n_fb][blk_len]
+  int* status;           // device error flag (SingularError inside the Sylvester solve)
+};
+
+__host__ __device__ inline int rec_len_of(int dim, int n1, int q) {
+  return dim == 2 ? 3 * n1 * n1 + 3 * q * q : n1 * n1 + 6 * q * q;
+}
+__host__ __device__ inline int piv_len_of(int dim, int n1, int q) { return dim == 2 ? n1 + q : n1 + 2 * q; }
+__host__ __device__ inline int raw_len_of(int dim, int n1, int q) { return dim == 2 ? 2 * n1 * n1 + 2 * q * q : n1 * n1 + 4 * q * q; }
+
+// ---------------------------------------------------------------- kernel launchers
+void launch_jv(const DevSys& s, const double* vin, const double* halo, double* vout, cudaStream_t st);
+size_t jv_smem_bytes(const DevSys& s);
+void launch_pc_apply(const DevPC& pc, const double* in, double* out, cudaStream_t st);
+void launch_shuffled(const DevSys& s, int e, int comp, int transpose, const double* in, double* out,
+                     double* scratch, cudaStream_t st);
+size_t shuffled_scratch_doubles(const DevSys& s);
+
+// Form: raw factors -> records (LU, C = A^{-1} B, Schur, Sylvester check, swap).
+// kind_out[blk] = 1 ok, 0 singular (needs fallback).
+struct FormBuffers {
+  double* raw;      // [nblk][raw_len]
+  double* rec;      // [nblk][rec_len]
+  int* piv;         // [nblk][piv_len]
+  int* kind;        // [nblk]
+  double* work;     // scratch
+};
+void launch_lanczos_form(const DevSys& s, const tpdg_gpu_ksvd_config& cfg, const double* start_vec,
+                         const double* start_vec2, double* raw, double* sigma, int* lz_iters, double* work,
+                         size_t work_per_block, int grid, cudaStream_t st);
+size_t lanczos_work_doubles(const DevSys& s, int max_it);
+void launch_make_factors(int dim, int q, int n1, int nblk, const double* raw, double* rec, int* piv, int* kind,
+                         double* work, cudaStream_t st);
+size_t probe_work_doubles(const DevSys& s);
+int probe_grid(int n, int nfb);
+void launch_assemble_fallback(const DevSys& s, const int* blocks, int nfb, double* fb_lu, double* work,
+                              cudaStream_t st);
+void launch_dense_lu(int n, int nfb, double* fb_lu, int* fb_piv, int* fb_status, cudaStream_t st);
+
+// GMRES vector kernels
+void launch_dot(const double* x, const double* y, int64_t n, double* partial, double* result, unsigned* counter,
+                cudaStream_t st);
+void launch_norm(const double* x, int64_t n, double* partial, double* result, unsigned* counter, cudaStream_t st);
+void launch_mgs_step(double* w, const double* vprev, const double* hprev, const double* vj, int64_t n,
+                     double* partial, double* result, unsigned* counter, cudaStream_t st);
+void launch_axpy_neg(double* w, const double* h, const double* v, int64_t n, cudaStream_t st);
+void launch_scale_div(const double* in, const double* den, double* out, int64_t n, cudaStream_t st);
+void launch_sub(const double* b, const double* ax, double* r, int64_t n, cudaStream_t st);
+void launch_combine(const double* v, int64_t ldv, const double* y, int k, double* out, int64_t n, cudaStream_t st);
+void launch_add(double* x, const double* dx, int64_t n, cudaStream_t st);
+int reduce_grid(int64_t n);
+
+extern thread_local int64_t g_launches;
+
+} // namespace tpdg_gpu
