@@ -95,6 +95,10 @@ int tpdg_gpu_ctx_sync(tpdg_gpu_ctx ctx);
 int tpdg_gpu_nccl_unique_id(void *out128);
 /* Count of this library's kernel launches on the context so far (bench evidence). */
 int tpdg_gpu_ctx_launches(tpdg_gpu_ctx ctx, int64_t *count);
+/* CUDA-event timing per kernel class on the context stream (enable resets the record):
+ * class 0 = Kronecker PC apply, 1 = Jv, 2 = MGS + norm passes, 3 = other. */
+int tpdg_gpu_ctx_profile(tpdg_gpu_ctx ctx, int enable);
+int tpdg_gpu_ctx_profile_read(tpdg_gpu_ctx ctx, double *ms /* [4] */, int64_t *counts /* [4] */);
 
 /* ---- operator (M - dt J) (jacobian_only = 0) or J (jacobian_only = 1) of the elements
  * [e_begin, e_end) owned by this rank. block_mode: 0 = full, 1 = small. */

@@ -89,6 +89,7 @@ _lib = None
 EXPORTS = [
     "tpdg_gpu_last_error", "tpdg_gpu_version", "tpdg_gpu_nccl_unique_id", "tpdg_gpu_ctx_create",
     "tpdg_gpu_ctx_destroy", "tpdg_gpu_ctx_stream", "tpdg_gpu_ctx_sync", "tpdg_gpu_ctx_launches",
+    "tpdg_gpu_ctx_profile", "tpdg_gpu_ctx_profile_read",
     "tpdg_gpu_op_create", "tpdg_gpu_op_destroy", "tpdg_gpu_op_local_size", "tpdg_gpu_op_check_hash",
     "tpdg_gpu_jv", "tpdg_gpu_jv_host", "tpdg_gpu_shuffled_host", "tpdg_gpu_form_ksvd",
     "tpdg_gpu_pc_import_factors", "tpdg_gpu_pc_destroy", "tpdg_gpu_pc_num_fallbacks", "tpdg_gpu_pc_fallbacks",
@@ -119,7 +120,8 @@ def lib():
         "tpdg_gpu_nccl_unique_id": [v],
         "tpdg_gpu_ctx_create": [C.c_int, C.c_int, C.c_int, v, C.POINTER(v)],
         "tpdg_gpu_ctx_destroy": [v], "tpdg_gpu_ctx_stream": [v, C.POINTER(v)], "tpdg_gpu_ctx_sync": [v],
-        "tpdg_gpu_ctx_launches": [v, i64p],
+        "tpdg_gpu_ctx_launches": [v, i64p], "tpdg_gpu_ctx_profile": [v, C.c_int],
+        "tpdg_gpu_ctx_profile_read": [v, dp, i64p],
         "tpdg_gpu_op_create": [v, C.POINTER(_System), C.c_double, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(v)],
         "tpdg_gpu_op_destroy": [v], "tpdg_gpu_op_local_size": [v, i64p], "tpdg_gpu_op_check_hash": [v, C.c_uint64],
         "tpdg_gpu_jv": [v, v, v], "tpdg_gpu_jv_host": [v, dp, dp],
@@ -271,6 +273,16 @@ class Context:
         n = C.c_int64()
         _check(lib().tpdg_gpu_ctx_launches(self.h, C.byref(n)))
         return n.value
+
+    def profile(self, enable=True):
+        _check(lib().tpdg_gpu_ctx_profile(self.h, int(enable)))
+
+    def profile_read(self):
+        """{class: (total ms, count)} for classes pc_apply, jv, mgs, other."""
+        ms = np.zeros(4)
+        cnt = np.zeros(4, dtype=np.int64)
+        _check(lib().tpdg_gpu_ctx_profile_read(self.h, _ptr(ms), cnt.ctypes.data_as(i64p)))
+        return {name: (float(ms[i]), int(cnt[i])) for i, name in enumerate(["pc_apply", "jv", "mgs", "other"])}
 
     def close(self):
         if self.h:

@@ -107,6 +107,11 @@ struct tpdg_gpu_ctx_s {
   cudaStream_t stream = nullptr;
   ncclComm_t comm = nullptr;
   int64_t launches_at_create = 0;
+  // optional per-class CUDA-event timing (0 PC apply, 1 Jv, 2 MGS/norm passes, 3 other GMRES vector ops)
+  bool profiling = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pool;
+  std::vector<int> pool_cat;
+  size_t pool_used = 0;
 };
 
 struct tpdg_gpu_op_s {
@@ -140,6 +145,28 @@ struct tpdg_gpu_pc_s {
 };
 
 namespace {
+
+// RAII event pair around a region of stream work, recorded only when profiling is on.
+struct Prof {
+  tpdg_gpu_ctx ctx;
+  size_t slot = size_t(-1);
+  Prof(tpdg_gpu_ctx c, int cat) : ctx(c) {
+    if (!ctx->profiling) return;
+    if (ctx->pool_used == ctx->pool.size()) {
+      cudaEvent_t a, b;
+      TPDG_CUDA_CHECK(cudaEventCreate(&a));
+      TPDG_CUDA_CHECK(cudaEventCreate(&b));
+      ctx->pool.push_back({a, b});
+      ctx->pool_cat.push_back(cat);
+    }
+    slot = ctx->pool_used++;
+    ctx->pool_cat[slot] = cat;
+    TPDG_CUDA_CHECK(cudaEventRecord(ctx->pool[slot].first, ctx->stream));
+  }
+  ~Prof() {
+    if (slot != size_t(-1)) cudaEventRecord(ctx->pool[slot].second, ctx->stream);
+  }
+};
 
 DevSys make_devsys(const tpdg_gpu_op_s& op, int block_mode, double a, double b) {
   DevSys s{};
@@ -212,10 +239,12 @@ void allreduce_scalar(tpdg_gpu_ctx ctx, double* d_val, int count = 1) {
 
 void jv_device(tpdg_gpu_op op, const double* d_in, double* d_out) {
   exchange_halo(op, d_in);
+  Prof pr(op->ctx, 1);
   launch_jv(op->s, d_in, op->halo.as<double>(), d_out, op->ctx->stream);
 }
 
 void pc_apply_device(tpdg_gpu_pc pc, const double* d_in, double* d_out) {
+  Prof pr(pc->op->ctx, 0);
   launch_pc_apply(pc->pc, d_in, d_out, pc->op->ctx->stream);
 }
 
@@ -326,6 +355,7 @@ int run_gmres(tpdg_gpu_op op, tpdg_gpu_pc pc, const double* d_b, double* d_x, co
           apply_pc(z, w);
         }
         // MGS: h_j = <v_j, w>, w -= h_j v_j (fused passes)
+        std::unique_ptr<Prof> pr_mgs(new Prof(ctx, 2));
         for (int j = 0; j <= k; ++j) {
           if (!multi) {
             launch_mgs_step(w, j > 0 ? V + size_t(j - 1) * n : nullptr, hc + (j > 0 ? j - 1 : 0), V + size_t(j) * n,
@@ -347,6 +377,7 @@ int run_gmres(tpdg_gpu_op op, tpdg_gpu_pc pc, const double* d_b, double* d_x, co
           ++g_launches;
         }
         launch_scale_div(w, hc + k + 1, w, n, st);
+        pr_mgs.reset();
         TPDG_CUDA_CHECK(cudaMemcpyAsync(col.data(), hc, sizeof(double) * (k + 2), cudaMemcpyDeviceToHost, st));
         TPDG_CUDA_CHECK(cudaStreamSynchronize(st));
         for (int j = 0; j <= k + 1; ++j) h[size_t(j) * m + k] = col[j];
@@ -538,6 +569,10 @@ int tpdg_gpu_ctx_create(int device, int rank, int nranks, const void* nccl_id, t
 int tpdg_gpu_ctx_destroy(tpdg_gpu_ctx ctx) {
   return guarded([&] {
     if (!ctx) return;
+    for (auto& pr : ctx->pool) {
+      cudaEventDestroy(pr.first);
+      cudaEventDestroy(pr.second);
+    }
     if (ctx->comm) ncclCommDestroy(ctx->comm);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
@@ -554,6 +589,30 @@ int tpdg_gpu_ctx_sync(tpdg_gpu_ctx ctx) {
 
 int tpdg_gpu_ctx_launches(tpdg_gpu_ctx ctx, int64_t* count) {
   return guarded([&] { *count = g_launches - ctx->launches_at_create; });
+}
+
+int tpdg_gpu_ctx_profile(tpdg_gpu_ctx ctx, int enable) {
+  return guarded([&] {
+    TPDG_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    ctx->profiling = enable != 0;
+    ctx->pool_used = 0;
+  });
+}
+
+int tpdg_gpu_ctx_profile_read(tpdg_gpu_ctx ctx, double* ms, int64_t* counts) {
+  return guarded([&] {
+    TPDG_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    for (int c = 0; c < 4; ++c) {
+      ms[c] = 0.0;
+      counts[c] = 0;
+    }
+    for (size_t i = 0; i < ctx->pool_used; ++i) {
+      float t = 0.f;
+      TPDG_CUDA_CHECK(cudaEventElapsedTime(&t, ctx->pool[i].first, ctx->pool[i].second));
+      ms[ctx->pool_cat[i]] += double(t);
+      counts[ctx->pool_cat[i]] += 1;
+    }
+  });
 }
 
 int tpdg_gpu_op_create(tpdg_gpu_ctx ctx, const tpdg_gpu_system* sys, double dt, int jacobian_only, int block_mode,
