@@ -192,6 +192,7 @@ def main_ours(args, rank, world, local_rank):
     cfg = T.GmresConfig(tol=1e-10, restart=30, max_iterations=2000, side="right")
     stream = torch.cuda.ExternalStream(ctx.stream())
 
+    ctx.profile(not args.no_profile)  # grows the event pool outside the timed region
     for _ in range(args.warmup):
         its, conv, _ = T.gmres_device(op, pc, b, x, cfg)
     torch.cuda.synchronize()

@@ -9,6 +9,8 @@
 //
 // MGS is fused: pass j computes w <- w - h_{j-1} v_{j-1} and the partial dot <v_j, w> in one read
 // of (w, v_{j-1}, v_j) and one write of w, so the k+1 MGS steps of iteration k cost k+2 passes.
+#include <cstdint>
+
 #include "tpdg_internal.hpp"
 
 namespace tpdg_gpu {
@@ -31,7 +33,7 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
   return s;  // valid in thread 0
 }
 
-// Last-CTA finalization: result[0] = sum of partials in CTA order (optionally sqrt).
+// Last-CTA finalization: result[0] = fixed-order tree sum of the per-CTA partials (optionally sqrt).
 __device__ __forceinline__ void finalize(double local, double* partial, double* result, unsigned* counter,
                                          bool take_sqrt) {
   __shared__ double sh[32];
@@ -44,40 +46,86 @@ __device__ __forceinline__ void finalize(double local, double* partial, double* 
     last = (t == gridDim.x - 1);
   }
   __syncthreads();
-  if (last && threadIdx.x == 0) {
-    __threadfence();
-    double tot = 0.0;
-    for (unsigned b = 0; b < gridDim.x; ++b) tot += ((volatile double*)partial)[b];
+  if (!last) return;
+  __threadfence();
+  double v = 0.0;
+  for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x) v += ((volatile double*)partial)[b];
+  const double tot = block_sum(v, sh);
+  if (threadIdx.x == 0) {
     result[0] = take_sqrt ? sqrt(tot) : tot;
     *counter = 0u;  // re-arm for the next launch (stream ordered)
   }
 }
 
+__device__ __forceinline__ bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+// Grid-stride over double2 pairs when every operand is 16 B aligned (an odd n is finished by the
+// scalar tail in the first CTA); otherwise a scalar grid-stride loop.
 __global__ void __launch_bounds__(kRedThreads) dot_kernel(const double* __restrict__ x, const double* __restrict__ y,
                                                            int64_t n, double* partial, double* result,
                                                            unsigned* counter, int take_sqrt) {
-  double s = 0.0;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
-    s += x[i] * y[i];
-  finalize(s, partial, result, counter, take_sqrt != 0);
+  double s0 = 0.0, s1 = 0.0;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x, t0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (aligned16(x) && aligned16(y)) {
+    const int64_t n2 = n / 2;
+    const double2* x2 = reinterpret_cast<const double2*>(x);
+    const double2* y2 = reinterpret_cast<const double2*>(y);
+    for (int64_t i = t0; i < n2; i += stride) {
+      const double2 a = x2[i], b = y2[i];
+      s0 += a.x * b.x;
+      s1 += a.y * b.y;
+    }
+    if ((n & 1) && t0 == 0) s0 += x[n - 1] * y[n - 1];
+  } else {
+    for (int64_t i = t0; i < n; i += stride) s0 += x[i] * y[i];
+  }
+  finalize(s0 + s1, partial, result, counter, take_sqrt != 0);
 }
 
-// w <- w - hprev[0] * vprev (if vprev), then partial <vj, w>.
+// w <- w - hprev[0] * vprev (if vprev), then partial <vj, w> (or <w, w> when vj is null).
 __global__ void __launch_bounds__(kRedThreads) mgs_kernel(double* __restrict__ w, const double* __restrict__ vprev,
                                                            const double* __restrict__ hprev,
                                                            const double* __restrict__ vj, int64_t n, double* partial,
                                                            double* result, unsigned* counter, int take_sqrt) {
   const double h = vprev ? hprev[0] : 0.0;
-  double s = 0.0;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
-    double wi = w[i];
-    if (vprev) {
-      wi = wi - h * vprev[i];
-      w[i] = wi;
+  double s0 = 0.0, s1 = 0.0;
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x, t0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (aligned16(w) && (!vprev || aligned16(vprev)) && (!vj || aligned16(vj))) {
+    const int64_t n2 = n / 2;
+    double2* w2 = reinterpret_cast<double2*>(w);
+    const double2* p2 = reinterpret_cast<const double2*>(vprev);
+    const double2* j2 = reinterpret_cast<const double2*>(vj);
+    for (int64_t i = t0; i < n2; i += stride) {
+      double2 wi = w2[i];
+      if (vprev) {
+        const double2 pv = p2[i];
+        wi.x = wi.x - h * pv.x;
+        wi.y = wi.y - h * pv.y;
+        w2[i] = wi;
+      }
+      const double2 a = vj ? j2[i] : wi;
+      s0 += a.x * wi.x;
+      s1 += a.y * wi.y;
     }
-    s += (vj ? vj[i] : wi) * wi;
+    if ((n & 1) && t0 == 0) {
+      double wi = w[n - 1];
+      if (vprev) {
+        wi = wi - h * vprev[n - 1];
+        w[n - 1] = wi;
+      }
+      s0 += (vj ? vj[n - 1] : wi) * wi;
+    }
+  } else {
+    for (int64_t i = t0; i < n; i += stride) {
+      double wi = w[i];
+      if (vprev) {
+        wi = wi - h * vprev[i];
+        w[i] = wi;
+      }
+      s0 += (vj ? vj[i] : wi) * wi;
+    }
   }
-  finalize(s, partial, result, counter, take_sqrt != 0);
+  finalize(s0 + s1, partial, result, counter, take_sqrt != 0);
 }
 
 __global__ void axpy_neg_kernel(double* __restrict__ w, const double* __restrict__ h, const double* __restrict__ v,
@@ -125,8 +173,8 @@ int stream_grid(int64_t n) {
 } // namespace
 
 int reduce_grid(int64_t n) {
-  const int64_t want = (n + kRedThreads * 4 - 1) / (kRedThreads * 4);
-  const int64_t cap = 148 * 4;
+  const int64_t want = (n / 2 + kRedThreads - 1) / kRedThreads;
+  const int64_t cap = 148 * 8;
   return int(want < cap ? (want > 0 ? want : 1) : cap);
 }
 

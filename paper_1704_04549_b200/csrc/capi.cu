@@ -284,12 +284,13 @@ int run_gmres(tpdg_gpu_op op, tpdg_gpu_pc pc, const double* d_b, double* d_x, co
   const int m = cfg.restart;
   const bool multi = ctx->nranks > 1;
   GmresWork W;
-  W.V.alloc(sizeof(double) * size_t(m + 1) * n);
+  const int64_t ldv = (n + 31) & ~int64_t(31);  // 256 B aligned Krylov slices (vectorized passes)
+  W.V.alloc(sizeof(double) * size_t(m + 1) * ldv);
   W.z.alloc(sizeof(double) * n);
   W.tmp.alloc(sizeof(double) * n);
   W.r.alloc(sizeof(double) * n);
   W.hcol.alloc(sizeof(double) * (m + 2));
-  W.partial.alloc(sizeof(double) * 148 * 4);
+  W.partial.alloc(sizeof(double) * 148 * 8);
   W.counter.alloc(sizeof(unsigned) * 4);
   W.y.alloc(sizeof(double) * (m + 1));
   W.scal.alloc(sizeof(double) * 4);
@@ -345,8 +346,8 @@ int run_gmres(tpdg_gpu_op op, tpdg_gpu_pc pc, const double* d_b, double* d_x, co
       int k = 0;
       for (; k < m && its < cfg.max_iterations; ++k) {
         ++its;
-        double* vk = V + size_t(k) * n;
-        double* w = V + size_t(k + 1) * n;
+        double* vk = V + size_t(k) * ldv;
+        double* w = V + size_t(k + 1) * ldv;
         if (right) {
           apply_pc(vk, z);
           jv_device(op, z, w);
@@ -358,11 +359,11 @@ int run_gmres(tpdg_gpu_op op, tpdg_gpu_pc pc, const double* d_b, double* d_x, co
         std::unique_ptr<Prof> pr_mgs(new Prof(ctx, 2));
         for (int j = 0; j <= k; ++j) {
           if (!multi) {
-            launch_mgs_step(w, j > 0 ? V + size_t(j - 1) * n : nullptr, hc + (j > 0 ? j - 1 : 0), V + size_t(j) * n,
+            launch_mgs_step(w, j > 0 ? V + size_t(j - 1) * ldv : nullptr, hc + (j > 0 ? j - 1 : 0), V + size_t(j) * ldv,
                             n, part, hc + j, ctr, st);
           } else {
-            if (j > 0) launch_axpy_neg(w, hc + j - 1, V + size_t(j - 1) * n, n, st);
-            launch_dot(V + size_t(j) * n, w, n, part, hc + j, ctr, st);
+            if (j > 0) launch_axpy_neg(w, hc + j - 1, V + size_t(j - 1) * ldv, n, st);
+            launch_dot(V + size_t(j) * ldv, w, n, part, hc + j, ctr, st);
             allreduce_scalar(ctx, hc + j);
           }
         }
@@ -409,7 +410,7 @@ int run_gmres(tpdg_gpu_op op, tpdg_gpu_pc pc, const double* d_b, double* d_x, co
         y[i] = s / h[size_t(i) * m + i];
       }
       TPDG_CUDA_CHECK(cudaMemcpyAsync(W.y.p, y.data(), sizeof(double) * std::max(k, 1), cudaMemcpyHostToDevice, st));
-      launch_combine(V, n, W.y.as<double>(), k, tmp, n, st);
+      launch_combine(V, ldv, W.y.as<double>(), k, tmp, n, st);
       if (right) {
         apply_pc(tmp, z);
         launch_add(d_x, z, n, st);

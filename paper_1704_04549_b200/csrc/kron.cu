@@ -244,6 +244,320 @@ size_t kron2d_smem(const DevPC& pc) {
          sizeof(int) * size_t(pc.piv_len + 2 * n1 + 2 * n2) + 16;
 }
 
+// ------------------------------------------------------------------------------------ 2D, sized
+// Latency-oriented variant for compile-time (N1, N2): the element's work is a chain of
+// dependent fp64 operations (LU substitutions with divisions, the Sylvester wavefront), so the
+// kernel minimizes the chain: fibers live in registers with fully unrolled substitutions, the
+// Sylvester cells are specialized on their block shape (1x1 / 1x2 / 2x1 / 2x2) with the tiny
+// pivoted solve unrolled in registers, and the wavefront runs in one warp (__syncwarp per step).
+// 64 threads per element keep many elements resident per SM. Same arithmetic as above.
+constexpr int kSizedThreads = 64;
+
+template <int N>
+__device__ __forceinline__ void lu_fiber_reg(const double* __restrict__ lu, const int* __restrict__ perm, double* col,
+                                             int stride) {
+  double x[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) x[k] = col[perm[k] * stride];
+#pragma unroll
+  for (int r = 1; r < N; ++r) {
+    double s = x[r];
+#pragma unroll
+    for (int j = 0; j < r; ++j) s = fmsc(s, lu[r * N + j], x[j]);
+    x[r] = s;
+  }
+#pragma unroll
+  for (int r = N - 1; r >= 0; --r) {
+    double s = x[r];
+#pragma unroll
+    for (int j = r + 1; j < N; ++j) s = fmsc(s, lu[r * N + j], x[j]);
+    x[r] = fdiv(s, lu[r * N + r]);
+  }
+#pragma unroll
+  for (int k = 0; k < N; ++k) col[k * stride] = x[k];
+}
+
+// solve_tiny<4> on an n x n (n = IS*KS) register system; row swaps via predicated selects.
+template <int NS>
+__device__ __forceinline__ bool solve_tiny_reg(double (&a)[NS][NS], double (&b)[NS], double tol) {
+#pragma unroll
+  for (int k = 0; k < NS; ++k) {
+    int piv = k;
+    double pv = a[k][k];
+#pragma unroll
+    for (int i = k + 1; i < NS; ++i)
+      if (fabs(a[i][k]) > fabs(pv)) {
+        pv = a[i][k];
+        piv = i;
+      }
+    if (fabs(pv) < tol) return false;
+#pragma unroll
+    for (int i = k + 1; i < NS; ++i)
+      if (piv == i) {
+#pragma unroll
+        for (int j = 0; j < NS; ++j) {
+          const double t = a[i][j];
+          a[i][j] = a[k][j];
+          a[k][j] = t;
+        }
+        const double t = b[i];
+        b[i] = b[k];
+        b[k] = t;
+      }
+    const double inv = fdiv(1.0, a[k][k]);
+#pragma unroll
+    for (int i = k + 1; i < NS; ++i) {
+      const double m = fmul(a[i][k], inv);
+      if (m == 0.0) continue;
+#pragma unroll
+      for (int j = k; j < NS; ++j) a[i][j] = fmsc(a[i][j], m, a[k][j]);
+      b[i] = fmsc(b[i], m, b[k]);
+    }
+  }
+#pragma unroll
+  for (int i = NS - 1; i >= 0; --i) {
+#pragma unroll
+    for (int j = i + 1; j < NS; ++j) b[i] = fmsc(b[i], a[i][j], b[j]);
+    b[i] = fdiv(b[i], a[i][i]);
+  }
+  return true;
+}
+
+// Warp-level tiled product O = op(A) op(B) (R x K x C), lane tile TI x TJ; each output still
+// accumulates k ascending from +0.0 with separate mul / add roundings (faithful).
+template <int R, int K, int C, bool AT, bool BT, int TI, int TJ>
+__device__ __forceinline__ void warp_mm(const double* A, int lda, const double* B, int ldb, double* O, int ldo,
+                                        int lane) {
+  constexpr int NTI = (R + TI - 1) / TI, NTJ = (C + TJ - 1) / TJ;
+  for (int t = lane; t < NTI * NTJ; t += 32) {
+    const int i0 = (t / NTJ) * TI, j0 = (t % NTJ) * TJ;
+    double acc[TI][TJ];
+#pragma unroll
+    for (int ii = 0; ii < TI; ++ii)
+#pragma unroll
+      for (int jj = 0; jj < TJ; ++jj) acc[ii][jj] = 0.0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      double a[TI], b[TJ];
+#pragma unroll
+      for (int ii = 0; ii < TI; ++ii) {
+        const int i = i0 + ii < R ? i0 + ii : R - 1;
+        a[ii] = AT ? A[k * lda + i] : A[i * lda + k];
+      }
+#pragma unroll
+      for (int jj = 0; jj < TJ; ++jj) {
+        const int j = j0 + jj < C ? j0 + jj : C - 1;
+        b[jj] = BT ? B[j * ldb + k] : B[k * ldb + j];
+      }
+#pragma unroll
+      for (int ii = 0; ii < TI; ++ii)
+#pragma unroll
+        for (int jj = 0; jj < TJ; ++jj) acc[ii][jj] = fmac(acc[ii][jj], a[ii], b[jj]);
+    }
+#pragma unroll
+    for (int ii = 0; ii < TI; ++ii)
+#pragma unroll
+      for (int jj = 0; jj < TJ; ++jj)
+        if (i0 + ii < R && j0 + jj < C) O[(i0 + ii) * ldo + j0 + jj] = acc[ii][jj];
+  }
+}
+
+// Right-hand side of one Sylvester entry: B minus the solved rows below (j ascending), then the
+// solved columns to the right (l ascending), exactly sylvester.hpp:84-99.
+__device__ __forceinline__ double sylv_rhs(const double* __restrict__ t1, int n1, const double* __restrict__ t2,
+                                           int n2, const double* M, const double* Y, int ld, int i, int k,
+                                           int jfirst, int lfirst) {
+  double s = M[i * ld + k];
+  const double* trow = t1 + i * n1;
+#pragma unroll 4
+  for (int j = jfirst; j < n1; ++j) s = fmsc(s, trow[j], Y[j * ld + k]);
+  const double* t2row = t2 + k * n2;
+  const double* yrow = Y + i * ld;
+#pragma unroll 4
+  for (int l = lfirst; l < n2; ++l) s = fmsc(s, t2row[l], yrow[l]);
+  return s;
+}
+
+template <int IS, int KS>
+__device__ __forceinline__ double sylv_solve_group(const double* t1, int n1, const double* t2, int n2, int i0, int k0,
+                                                   const double (&rg)[4], int e, double tol, int* status) {
+  constexpr int NS = IS * KS;
+  double a[NS][NS], r[NS];
+#pragma unroll
+  for (int ai = 0; ai < IS; ++ai)
+#pragma unroll
+    for (int kb = 0; kb < KS; ++kb) {
+      r[ai * KS + kb] = rg[ai * KS + kb];
+#pragma unroll
+      for (int a2 = 0; a2 < IS; ++a2)
+#pragma unroll
+        for (int kb2 = 0; kb2 < KS; ++kb2) {
+          double coef = 0.0;
+          if (kb == kb2) coef = fadd(coef, t1[(i0 + ai) * n1 + i0 + a2]);
+          if (ai == a2) coef = fadd(coef, t2[(k0 + kb) * n2 + k0 + kb2]);
+          a[ai * KS + kb][a2 * KS + kb2] = coef;
+        }
+    }
+  if (!solve_tiny_reg<NS>(a, r, tol)) atomicExch(status, int(TPDG_SINGULAR));
+  double y = r[0];
+#pragma unroll
+  for (int t = 1; t < NS; ++t)
+    if (e == t) y = r[t];
+  return y;
+}
+
+// One warp per element: every phase is warp-synchronous (no CTA barriers), so several elements
+// proceed independently on an SM and their dependency chains overlap.
+template <int N1, int N2>
+struct Kron2dWarpLayout {
+  static constexpr int ld = (N2 + 1) & ~1;
+  static constexpr int rec = 3 * N1 * N1 + 3 * N2 * N2;
+  static constexpr int ints = (N1 + N2) + 2 * N1 + 2 * N2 + 4;
+  static constexpr int per = 2 * N1 * ld + rec + ((ints + 1) / 2) + 2;
+  static constexpr int per_even = (per + 1) & ~1;
+};
+
+template <int N1, int N2>
+__global__ void __launch_bounds__(kSizedThreads) kron2d_sized_kernel(DevPC pc, const double* __restrict__ in,
+                                                                      double* __restrict__ out) {
+  using L = Kron2dWarpLayout<N1, N2>;
+  constexpr int ld = L::ld, rec = L::rec;
+  extern __shared__ double sm_all[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int blk = blockIdx.x * (kSizedThreads / 32) + warp;
+  if (blk >= pc.nblk || pc.kind[blk] == 0) return;
+  double* sX = sm_all + size_t(warp) * L::per_even;
+  double* sT = sX + N1 * ld;
+  double* sR = sT + N1 * ld;
+  double* sTol = sR + rec;
+  int* sPiv = reinterpret_cast<int*>(sTol + 2);
+  int* sb = sPiv + N1 + N2;  // s1[N1] z1[N1] s2[N2] z2[N2] nb1 nb2 all11
+  {
+    const double* r = pc.rec + size_t(blk) * rec;
+    for (int i = lane; i < rec; i += 32) sR[i] = r[i];
+    for (int i = lane; i < N1 + N2; i += 32) sPiv[i] = pc.piv[size_t(blk) * (N1 + N2) + i];
+    const double* x = in + size_t(blk) * (N1 * N2);
+    for (int i = lane; i < N1 * N2; i += 32) sX[(i / N2) * ld + i % N2] = x[i];
+  }
+  __syncwarp();
+  const double* luA2 = sR;
+  const double* luB1 = luA2 + N1 * N1;
+  const double* Q1 = luB1 + N2 * N2;
+  const double* T1 = Q1 + N1 * N1;
+  const double* Q2 = T1 + N1 * N1;
+  const double* T2 = Q2 + N2 * N2;
+  // (A2^{-1} (x) I): one column fiber per lane
+  for (int c = lane; c < N2; c += 32) lu_fiber_reg<N1>(luA2, sPiv, sX + c, ld);
+  // Sylvester plan: row sums of |T| (in order), max, quasi-block structure
+  for (int i = lane; i < N1 + N2; i += 32) {
+    const double* row = i < N1 ? T1 + i * N1 : T2 + (i - N1) * N2;
+    const int n = i < N1 ? N1 : N2;
+    double s = 0.0;
+    for (int j = 0; j < n; ++j) s = fadd(s, fabs(row[j]));
+    sT[i] = s;
+  }
+  __syncwarp();
+  if (lane == 0) {
+    double m1 = 0.0, m2 = 0.0;
+    for (int i = 0; i < N1; ++i) m1 = fmax(m1, sT[i]);
+    for (int i = 0; i < N2; ++i) m2 = fmax(m2, sT[N1 + i]);
+    sTol[0] = fmul(1e-14, fmax(fadd(m1, m2), 1e-300));
+    const int nb1 = quasi_blocks_dev(T1, N1, sb, sb + N1);
+    const int nb2 = quasi_blocks_dev(T2, N2, sb + 2 * N1, sb + 2 * N1 + N2);
+    sb[2 * N1 + 2 * N2] = nb1;
+    sb[2 * N1 + 2 * N2 + 1] = nb2;
+    sb[2 * N1 + 2 * N2 + 2] = (nb1 == N1 && nb2 == N2) ? 1 : 0;
+  }
+  __syncwarp();
+  // (I (x) B1^{-1}): one row fiber per lane
+  for (int r = lane; r < N1; r += 32) lu_fiber_reg<N2>(luB1, sPiv + N1, sX + r * ld, 1);
+  __syncwarp();
+  warp_mm<N1, N1, N2, true, false, 2, 4>(Q1, N1, sX, ld, sT, ld, lane);  // Q1^T X
+  __syncwarp();
+  warp_mm<N1, N2, N2, false, false, 2, 4>(sT, ld, Q2, N2, sX, ld, lane);  // (.) Q2 -> M
+  __syncwarp();
+  {  // Y (into sT): T1 Y + Y T2^T = M, block anti-diagonal wavefront
+    const int nb1 = sb[2 * N1 + 2 * N2], nb2 = sb[2 * N1 + 2 * N2 + 1];
+    const bool all11 = sb[2 * N1 + 2 * N2 + 2] != 0;
+    const int *s1 = sb, *z1 = sb + N1, *s2 = sb + 2 * N1, *z2 = sb + 2 * N1 + N2;
+    const double tol = sTol[0];
+    for (int step = 0; step <= nb1 + nb2 - 2; ++step) {
+      const int d1lo = step - (nb2 - 1) > 0 ? step - (nb2 - 1) : 0;
+      const int d1hi = step < nb1 - 1 ? step : nb1 - 1;
+      if (all11) {  // 1 x 1 blocks: one lane per cell; solve_tiny<1> is y = r / (t1_ii + t2_kk)
+        for (int d1 = d1lo + lane; d1 <= d1hi; d1 += 32) {
+          const int i = nb1 - 1 - d1, k = nb2 - 1 - (step - d1);
+          const double s = sylv_rhs(T1, N1, T2, N2, sX, sT, ld, i, k, i + 1, k + 1);
+          const double coef = fadd(fadd(0.0, T1[i * N1 + i]), T2[k * N2 + k]);
+          if (fabs(coef) < tol) atomicExch(pc.status, int(TPDG_SINGULAR));
+          sT[i * ld + k] = fdiv(s, coef);
+        }
+      } else {  // 4 lanes per cell (one per entry), tiny solve replicated in the group
+        for (int base = d1lo; base <= d1hi; base += 8) {
+          const int d1 = base + (lane >> 2), e = lane & 3;
+          const bool cell_ok = d1 <= d1hi;
+          int i0 = 0, k0 = 0, isz = 1, ksz = 1;
+          double s = 0.0;
+          if (cell_ok) {
+            const int bi = nb1 - 1 - d1, bj = nb2 - 1 - (step - d1);
+            i0 = s1[bi];
+            isz = z1[bi];
+            k0 = s2[bj];
+            ksz = z2[bj];
+            if (e < isz * ksz)
+              s = sylv_rhs(T1, N1, T2, N2, sX, sT, ld, i0 + e / ksz, k0 + e % ksz, i0 + isz, k0 + ksz);
+          }
+          double rg[4];
+          const int g = lane & ~3;
+#pragma unroll
+          for (int t = 0; t < 4; ++t) rg[t] = __shfl_sync(0xffffffffu, s, g + t);
+          if (cell_ok && e < isz * ksz) {
+            const int code = (isz - 1) * 2 + (ksz - 1);
+            double y;
+            if (code == 0) y = sylv_solve_group<1, 1>(T1, N1, T2, N2, i0, k0, rg, e, tol, pc.status);
+            else if (code == 1) y = sylv_solve_group<1, 2>(T1, N1, T2, N2, i0, k0, rg, e, tol, pc.status);
+            else if (code == 2) y = sylv_solve_group<2, 1>(T1, N1, T2, N2, i0, k0, rg, e, tol, pc.status);
+            else y = sylv_solve_group<2, 2>(T1, N1, T2, N2, i0, k0, rg, e, tol, pc.status);
+            sT[(i0 + e / ksz) * ld + k0 + e % ksz] = y;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  }
+  warp_mm<N1, N1, N2, false, false, 2, 4>(Q1, N1, sT, ld, sX, ld, lane);  // Q1 Y
+  __syncwarp();
+  warp_mm<N1, N2, N2, false, true, 2, 4>(sX, ld, Q2, N2, out + size_t(blk) * (N1 * N2), N2, lane);  // (.) Q2^T
+}
+
+template <int N1, int N2>
+size_t kron2d_sized_smem() {
+  return sizeof(double) * size_t(Kron2dWarpLayout<N1, N2>::per_even) * (kSizedThreads / 32);
+}
+
+template <int N1, int N2>
+bool try_kron2d_sized(const DevPC& pc, const double* in, double* out, cudaStream_t st) {
+  if (pc.n1 != N1 || pc.q != N2) return false;
+  static bool configured = false;
+  const size_t smem = kron2d_sized_smem<N1, N2>();
+  if (!configured) {
+    TPDG_CUDA_CHECK(cudaFuncSetAttribute(kron2d_sized_kernel<N1, N2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(smem)));
+    TPDG_CUDA_CHECK(cudaFuncSetAttribute(kron2d_sized_kernel<N1, N2>,
+                                         cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    configured = true;
+  }
+  const int per_cta = kSizedThreads / 32;
+  kron2d_sized_kernel<N1, N2><<<(pc.nblk + per_cta - 1) / per_cta, kSizedThreads, smem, st>>>(pc, in, out);
+  return true;
+}
+
+bool launch_kron2d_sized(const DevPC& pc, const double* in, double* out, cudaStream_t st) {
+  return try_kron2d_sized<5, 5>(pc, in, out, st) || try_kron2d_sized<9, 9>(pc, in, out, st) ||
+         try_kron2d_sized<16, 16>(pc, in, out, st) || try_kron2d_sized<21, 21>(pc, in, out, st) ||
+         try_kron2d_sized<31, 31>(pc, in, out, st);
+}
+
 // ------------------------------------------------------------------------------------ 3D
 __global__ void __launch_bounds__(kApplyThreads) kron3d_apply_kernel(DevPC pc, const double* __restrict__ in,
                                                                       double* __restrict__ out) {
@@ -365,8 +679,10 @@ void launch_pc_apply(const DevPC& pc, const double* in, double* out, cudaStream_
   if (smem > 227 * 1024)
     throw Failure{TPDG_CONFIG, "pc_apply: factor record of " + std::to_string(smem) + " B exceeds shared memory"};
   if (pc.dim == 2) {
-    set_smem(kron2d_apply_kernel, smem, c2);
-    kron2d_apply_kernel<<<pc.nblk, kApplyThreads, smem, st>>>(pc, in, out);
+    if (!launch_kron2d_sized(pc, in, out, st)) {
+      set_smem(kron2d_apply_kernel, smem, c2);
+      kron2d_apply_kernel<<<pc.nblk, kApplyThreads, smem, st>>>(pc, in, out);
+    }
   } else {
     set_smem(kron3d_apply_kernel, smem, c3);
     kron3d_apply_kernel<<<pc.nblk, kApplyThreads, smem, st>>>(pc, in, out);
