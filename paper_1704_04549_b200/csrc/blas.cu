@@ -86,7 +86,9 @@ __global__ void __launch_bounds__(kRedThreads) dot_kernel(const double* __restri
 __global__ void __launch_bounds__(kRedThreads) mgs_kernel(double* __restrict__ w, const double* __restrict__ vprev,
                                                            const double* __restrict__ hprev,
                                                            const double* __restrict__ vj, int64_t n, double* partial,
-                                                           double* result, unsigned* counter, int take_sqrt) {
+                                                           double* result, unsigned* counter, int take_sqrt,
+                                                           const int* skip) {
+  if (skip && *skip) return;
   const double h = vprev ? hprev[0] : 0.0;
   double s0 = 0.0, s1 = 0.0;
   const int64_t stride = int64_t(gridDim.x) * blockDim.x, t0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -137,7 +139,8 @@ __global__ void axpy_neg_kernel(double* __restrict__ w, const double* __restrict
 
 // out = in / den[0] when den[0] > 0 (reference: `if (hkk > 0) v /= hkk`), else out = in.
 __global__ void scale_div_kernel(const double* __restrict__ in, const double* __restrict__ den,
-                                 double* __restrict__ out, int64_t n) {
+                                 double* __restrict__ out, int64_t n, const int* skip) {
+  if (skip && *skip) return;
   const double d = den[0];
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
     out[i] = d > 0.0 ? in[i] / d : in[i];
@@ -162,6 +165,48 @@ __global__ void combine_kernel(const double* __restrict__ v, int64_t ldv, const 
 __global__ void add_kernel(double* __restrict__ x, const double* __restrict__ dx, int64_t n) {
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
     x[i] = x[i] + dx[i];
+}
+
+// Givens step of iteration k (solve/gmres.hpp:122-141), one thread. hc holds the raw Hessenberg
+// column h(0..k+1, k) from MGS; the rotated column goes to H(:, k). Writes |g_{k+1}| and the
+// convergence decision to the host-mapped status slot and raises `done` on convergence.
+__global__ void givens_kernel(GmresDev G, int k, GmresStatus* status) {
+  if (threadIdx.x != 0 || *G.done) return;
+  const int m = G.m;
+  for (int j = 0; j <= k + 1; ++j) G.H[j * m + k] = G.hc[j];
+  for (int j = 0; j < k; ++j) {
+    const double t1 = G.H[j * m + k], t2 = G.H[(j + 1) * m + k];
+    G.H[j * m + k] = G.cs[j] * t1 + G.sn[j] * t2;
+    G.H[(j + 1) * m + k] = -G.sn[j] * t1 + G.cs[j] * t2;
+  }
+  const double t1 = G.H[k * m + k], t2 = G.H[(k + 1) * m + k];
+  const double denom = hypot(t1, t2);
+  G.cs[k] = denom == 0.0 ? 1.0 : t1 / denom;
+  G.sn[k] = denom == 0.0 ? 0.0 : t2 / denom;
+  G.H[k * m + k] = denom;
+  G.H[(k + 1) * m + k] = 0.0;
+  const double gk = G.g[k];
+  G.g[k] = G.cs[k] * gk;
+  G.g[k + 1] = -G.sn[k] * gk;
+  const double res = fabs(G.g[k + 1]);
+  const int conv = res <= G.target ? 1 : 0;
+  if (conv) *G.done = 1;
+  status[k].res = res;
+  status[k].conv = conv;
+  __threadfence_system();
+  status[k].valid = 1;
+  __threadfence_system();
+}
+
+// y = H(0:k, 0:k)^{-1} g (back substitution, solve/gmres.hpp:145-150), one thread.
+__global__ void backsolve_kernel(GmresDev G, int k) {
+  if (threadIdx.x != 0) return;
+  const int m = G.m;
+  for (int i = k - 1; i >= 0; --i) {
+    double s = G.g[i];
+    for (int j = i + 1; j < k; ++j) s -= G.H[i * m + j] * G.y[j];
+    G.y[i] = s / G.H[i * m + i];
+  }
 }
 
 int stream_grid(int64_t n) {
@@ -192,9 +237,9 @@ void launch_norm(const double* x, int64_t n, double* partial, double* result, un
 }
 
 void launch_mgs_step(double* w, const double* vprev, const double* hprev, const double* vj, int64_t n,
-                     double* partial, double* result, unsigned* counter, cudaStream_t st) {
+                     double* partial, double* result, unsigned* counter, cudaStream_t st, const int* skip) {
   mgs_kernel<<<reduce_grid(n), kRedThreads, 0, st>>>(w, vprev, hprev, vj, n, partial, result, counter,
-                                                      vj == nullptr ? 1 : 0);
+                                                      vj == nullptr ? 1 : 0, skip);
   TPDG_CUDA_CHECK(cudaGetLastError());
   ++g_launches;
 }
@@ -205,8 +250,21 @@ void launch_axpy_neg(double* w, const double* h, const double* v, int64_t n, cud
   ++g_launches;
 }
 
-void launch_scale_div(const double* in, const double* den, double* out, int64_t n, cudaStream_t st) {
-  scale_div_kernel<<<stream_grid(n), 256, 0, st>>>(in, den, out, n);
+void launch_scale_div(const double* in, const double* den, double* out, int64_t n, cudaStream_t st,
+                      const int* skip) {
+  scale_div_kernel<<<stream_grid(n), 256, 0, st>>>(in, den, out, n, skip);
+  TPDG_CUDA_CHECK(cudaGetLastError());
+  ++g_launches;
+}
+
+void launch_givens(const GmresDev& G, int k, GmresStatus* status, cudaStream_t st) {
+  givens_kernel<<<1, 32, 0, st>>>(G, k, status);
+  TPDG_CUDA_CHECK(cudaGetLastError());
+  ++g_launches;
+}
+
+void launch_backsolve(const GmresDev& G, int k, cudaStream_t st) {
+  backsolve_kernel<<<1, 32, 0, st>>>(G, k);
   TPDG_CUDA_CHECK(cudaGetLastError());
   ++g_launches;
 }

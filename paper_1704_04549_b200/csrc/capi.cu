@@ -114,6 +114,27 @@ struct tpdg_gpu_ctx_s {
   size_t pool_used = 0;
 };
 
+struct GmresWork {
+  int64_t n = 0;
+  int m = 0;
+  DevBuf V, z, tmp, r, xloc, hcol, partial, counter, y, scal;
+};
+
+struct MappedStatus {
+  GmresStatus* host = nullptr;
+  GmresStatus* dev = nullptr;
+  MappedStatus() = default;
+  MappedStatus(const MappedStatus&) = delete;
+  void alloc(int m) {
+    if (host) cudaFreeHost(host);
+    TPDG_CUDA_CHECK(cudaHostAlloc(reinterpret_cast<void**>(&host), sizeof(GmresStatus) * m, cudaHostAllocMapped));
+    TPDG_CUDA_CHECK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dev), host, 0));
+  }
+  ~MappedStatus() {
+    if (host) cudaFreeHost(host);
+  }
+};
+
 struct tpdg_gpu_op_s {
   tpdg_gpu_ctx ctx = nullptr;
   DevSys s{};
@@ -133,6 +154,10 @@ struct tpdg_gpu_op_s {
   };
   std::vector<Peer> peers;
   int n_halo = 0;
+  // GMRES workspace, allocated on first use and reused (no allocation inside a solve)
+  GmresWork gws;
+  MappedStatus gstatus;
+  DevBuf gdone;
 };
 
 struct tpdg_gpu_pc_s {
@@ -249,9 +274,7 @@ void pc_apply_device(tpdg_gpu_pc pc, const double* d_in, double* d_out) {
 }
 
 // ------------------------------------------------------------------------------------ GMRES
-struct GmresWork {
-  DevBuf V, z, tmp, r, xloc, hcol, partial, counter, y, scal;
-};
+
 
 
 __global__ void sqrt_inplace_kernel(double* v) { v[0] = sqrt(v[0]); }
@@ -272,6 +295,32 @@ double host_norm(tpdg_gpu_ctx ctx, const double* x, int64_t n, GmresWork& W) {
   return h;
 }
 
+__global__ void init_cycle_kernel(GmresDev G, double beta) {
+  for (int i = threadIdx.x; i <= G.m; i += blockDim.x) G.g[i] = i == 0 ? beta : 0.0;
+  if (threadIdx.x == 0) *G.done = 0;
+}
+
+// Spin on a host-mapped status slot written by givens_kernel (bounded by stream error checks).
+void wait_status(volatile GmresStatus* st, int k, cudaStream_t stream) {
+  long spins = 0;
+  while (st[k].valid == 0) {
+    if ((++spins & 0xFFFF) == 0) {
+      const cudaError_t e = cudaStreamQuery(stream);
+      if (e != cudaSuccess && e != cudaErrorNotReady)
+        throw Failure{TPDG_CUDA, std::string("gmres: device failure: ") + cudaGetErrorString(e)};
+      if (e == cudaSuccess && st[k].valid == 0)
+        throw Failure{TPDG_CUDA, "gmres: stream idle but iteration status missing"};
+    }
+  }
+}
+
+
+
+// Restarted GMRES (solve/gmres.hpp:52-179), device resident. Per iteration k the host only
+// enqueues work: P^{-1}, J, the fused MGS passes, the normalization and the Givens step (one
+// thread on the device, which also decides convergence). Iteration k+1 is enqueued before the
+// host waits for iteration k's status (lag 1), so the GPU never idles on the host; a launched
+// iteration that follows convergence is turned into no-ops by the device `done` flag.
 int run_gmres(tpdg_gpu_op op, tpdg_gpu_pc pc, const double* d_b, double* d_x, const tpdg_gpu_gmres_config& cfg,
               int* iterations, double* hist, int hist_cap, int* converged_out) {
   REQUIRE(cfg.tol > 0.0, TPDG_CONFIG, "GmresConfig: tol must be > 0");
@@ -283,33 +332,63 @@ int run_gmres(tpdg_gpu_op op, tpdg_gpu_pc pc, const double* d_b, double* d_x, co
   const bool right = cfg.side == 0;
   const int m = cfg.restart;
   const bool multi = ctx->nranks > 1;
-  GmresWork W;
   const int64_t ldv = (n + 31) & ~int64_t(31);  // 256 B aligned Krylov slices (vectorized passes)
-  W.V.alloc(sizeof(double) * size_t(m + 1) * ldv);
-  W.z.alloc(sizeof(double) * n);
-  W.tmp.alloc(sizeof(double) * n);
-  W.r.alloc(sizeof(double) * n);
-  W.hcol.alloc(sizeof(double) * (m + 2));
-  W.partial.alloc(sizeof(double) * 148 * 8);
-  W.counter.alloc(sizeof(unsigned) * 4);
-  W.y.alloc(sizeof(double) * (m + 1));
-  W.scal.alloc(sizeof(double) * 4);
+  GmresWork& W = op->gws;
+  if (W.n != n || W.m != m) {
+    W.V.alloc(sizeof(double) * size_t(m + 1) * ldv);
+    W.z.alloc(sizeof(double) * n);
+    W.tmp.alloc(sizeof(double) * n);
+    W.r.alloc(sizeof(double) * n);
+    W.hcol.alloc(sizeof(double) * (size_t(m + 1) * m + 4 * (m + 2)));
+    W.partial.alloc(sizeof(double) * 148 * 8);
+    W.counter.alloc(sizeof(unsigned) * 4);
+    W.y.alloc(sizeof(double) * (m + 2));
+    W.scal.alloc(sizeof(double) * 4);
+    op->gstatus.alloc(m);
+    op->gdone.alloc(sizeof(int) * 2);
+    W.n = n;
+    W.m = m;
+  }
   TPDG_CUDA_CHECK(cudaMemsetAsync(W.counter.p, 0, W.counter.bytes, st));
   TPDG_CUDA_CHECK(cudaMemsetAsync(d_x, 0, sizeof(double) * n, st));
   double* V = W.V.as<double>();
   double* z = W.z.as<double>();
   double* tmp = W.tmp.as<double>();
   double* r = W.r.as<double>();
-  double* hc = W.hcol.as<double>();
   double* part = W.partial.as<double>();
   unsigned* ctr = W.counter.as<unsigned>();
-  if (pc) TPDG_CUDA_CHECK(cudaMemsetAsync(pc->status.p, 0, sizeof(int), st));
+  GmresDev G;
+  G.H = W.hcol.as<double>();
+  G.hc = G.H + size_t(m + 1) * m;
+  G.cs = G.hc + (m + 2);
+  G.sn = G.cs + (m + 2);
+  G.g = G.sn + (m + 2);
+  G.y = W.y.as<double>();
+  TPDG_CUDA_CHECK(cudaMemsetAsync(op->gdone.p, 0, op->gdone.bytes, st));
+  G.done = op->gdone.as<int>();
+  G.m = m;
+  MappedStatus& status = op->gstatus;
+  DevSys sk = op->s;  // operator / preconditioner views that honour the done flag
+  sk.skip = G.done;
+  DevPC pk{};
+  if (pc) {
+    pk = pc->pc;
+    pk.skip = G.done;
+    TPDG_CUDA_CHECK(cudaMemsetAsync(pc->status.p, 0, sizeof(int), st));
+  }
+  double* hc = G.hc;
 
-  auto apply_pc = [&](const double* in, double* out) {
+  auto apply_pc = [&](const double* in, double* out, bool guarded) {
+    Prof pr(ctx, 0);
     if (pc)
-      pc_apply_device(pc, in, out);
+      launch_pc_apply(guarded ? pk : pc->pc, in, out, st);
     else
       TPDG_CUDA_CHECK(cudaMemcpyAsync(out, in, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
+  };
+  auto apply_op = [&](const double* in, double* out, bool guarded) {
+    exchange_halo(op, in);
+    Prof pr(ctx, 1);
+    launch_jv(guarded ? sk : op->s, in, op->halo.as<double>(), out, st);
   };
 
   int its = 0, nh = 0;
@@ -318,19 +397,19 @@ int run_gmres(tpdg_gpu_op op, tpdg_gpu_pc pc, const double* d_b, double* d_x, co
   if (right) {
     target = cfg.tol * host_norm(ctx, d_b, n, W);
   } else {
-    apply_pc(d_b, r);
+    apply_pc(d_b, r, false);
     target = cfg.tol * host_norm(ctx, r, n, W);
   }
-  std::vector<double> h(size_t(m + 1) * m), cs(m), sn(m), g(m + 1), y(m + 1), col(m + 2);
+  G.target = target;
   if (target == 0.0) {
     conv = true;
   } else {
     while (its < cfg.max_iterations) {
-      jv_device(op, d_x, tmp);
+      apply_op(d_x, tmp, false);
       launch_sub(d_b, tmp, tmp, n, st);
       double* rr = tmp;
       if (!right) {
-        apply_pc(tmp, r);
+        apply_pc(tmp, r, false);
         rr = r;
       }
       const double beta = host_norm(ctx, rr, n, W);
@@ -340,36 +419,34 @@ int run_gmres(tpdg_gpu_op op, tpdg_gpu_pc pc, const double* d_b, double* d_x, co
       }
       TPDG_CUDA_CHECK(cudaMemcpyAsync(W.scal.as<double>() + 1, &beta, sizeof(double), cudaMemcpyHostToDevice, st));
       launch_scale_div(rr, W.scal.as<double>() + 1, V, n, st);
-      std::fill(g.begin(), g.end(), 0.0);
-      g[0] = beta;
-      std::fill(h.begin(), h.end(), 0.0);
-      int k = 0;
-      for (; k < m && its < cfg.max_iterations; ++k) {
-        ++its;
+      init_cycle_kernel<<<1, 64, 0, st>>>(G, beta);
+      TPDG_CUDA_CHECK(cudaGetLastError());
+      ++g_launches;
+      for (int k = 0; k < m; ++k) status.host[k].valid = 0;
+      const int kmax = std::min(m, cfg.max_iterations - its);
+      auto launch_iteration = [&](int k) {
         double* vk = V + size_t(k) * ldv;
         double* w = V + size_t(k + 1) * ldv;
         if (right) {
-          apply_pc(vk, z);
-          jv_device(op, z, w);
+          apply_pc(vk, z, true);
+          apply_op(z, w, true);
         } else {
-          jv_device(op, vk, z);
-          apply_pc(z, w);
+          apply_op(vk, z, true);
+          apply_pc(z, w, true);
         }
-        // MGS: h_j = <v_j, w>, w -= h_j v_j (fused passes)
-        std::unique_ptr<Prof> pr_mgs(new Prof(ctx, 2));
-        for (int j = 0; j <= k; ++j) {
+        Prof pr(ctx, 2);
+        for (int j = 0; j <= k; ++j) {  // MGS: h_j = <v_j, w>, w -= h_j v_j (fused passes)
           if (!multi) {
-            launch_mgs_step(w, j > 0 ? V + size_t(j - 1) * ldv : nullptr, hc + (j > 0 ? j - 1 : 0), V + size_t(j) * ldv,
-                            n, part, hc + j, ctr, st);
+            launch_mgs_step(w, j > 0 ? V + size_t(j - 1) * ldv : nullptr, hc + (j > 0 ? j - 1 : 0),
+                            V + size_t(j) * ldv, n, part, hc + j, ctr, st, G.done);
           } else {
             if (j > 0) launch_axpy_neg(w, hc + j - 1, V + size_t(j - 1) * ldv, n, st);
             launch_dot(V + size_t(j) * ldv, w, n, part, hc + j, ctr, st);
             allreduce_scalar(ctx, hc + j);
           }
         }
-        // w -= h_k v_k ; h_{k+1} = ||w||
-        if (!multi) {
-          launch_mgs_step(w, vk, hc + k, nullptr, n, part, hc + k + 1, ctr, st);
+        if (!multi) {  // w -= h_k v_k ; h_{k+1} = ||w||
+          launch_mgs_step(w, vk, hc + k, nullptr, n, part, hc + k + 1, ctr, st, G.done);
         } else {
           launch_axpy_neg(w, hc + k, vk, n, st);
           launch_dot(w, w, n, part, hc + k + 1, ctr, st);
@@ -377,57 +454,48 @@ int run_gmres(tpdg_gpu_op op, tpdg_gpu_pc pc, const double* d_b, double* d_x, co
           sqrt_inplace_kernel<<<1, 1, 0, st>>>(hc + k + 1);
           ++g_launches;
         }
-        launch_scale_div(w, hc + k + 1, w, n, st);
-        pr_mgs.reset();
-        TPDG_CUDA_CHECK(cudaMemcpyAsync(col.data(), hc, sizeof(double) * (k + 2), cudaMemcpyDeviceToHost, st));
-        TPDG_CUDA_CHECK(cudaStreamSynchronize(st));
-        for (int j = 0; j <= k + 1; ++j) h[size_t(j) * m + k] = col[j];
-        // Givens (gmres.hpp:122-136)
-        for (int j = 0; j < k; ++j) {
-          const double t1 = h[size_t(j) * m + k], t2 = h[size_t(j + 1) * m + k];
-          h[size_t(j) * m + k] = cs[j] * t1 + sn[j] * t2;
-          h[size_t(j + 1) * m + k] = -sn[j] * t1 + cs[j] * t2;
-        }
-        const double t1 = h[size_t(k) * m + k], t2 = h[size_t(k + 1) * m + k];
-        const double denom = std::hypot(t1, t2);
-        cs[k] = denom == 0.0 ? 1.0 : t1 / denom;
-        sn[k] = denom == 0.0 ? 0.0 : t2 / denom;
-        h[size_t(k) * m + k] = denom;
-        h[size_t(k + 1) * m + k] = 0.0;
-        const double gk = g[k];
-        g[k] = cs[k] * gk;
-        g[k + 1] = -sn[k] * gk;
-        if (hist && nh < hist_cap) hist[nh] = std::abs(g[k + 1]);
-        ++nh;
-        if (std::abs(g[k + 1]) <= target) {
-          ++k;
+        launch_scale_div(w, hc + k + 1, w, n, st, G.done);
+        launch_givens(G, k, status.dev, st);
+      };
+      int k_end = -1;
+      launch_iteration(0);
+      for (int k = 1; k < kmax; ++k) {
+        launch_iteration(k);  // speculative: the GPU is still on iteration k-1
+        wait_status(status.host, k - 1, st);
+        if (status.host[k - 1].conv) {
+          k_end = k;
           break;
         }
       }
-      for (int i = k - 1; i >= 0; --i) {
-        double s = g[i];
-        for (int j = i + 1; j < k; ++j) s -= h[size_t(i) * m + j] * y[j];
-        y[i] = s / h[size_t(i) * m + i];
+      if (k_end < 0) {
+        wait_status(status.host, kmax - 1, st);
+        k_end = kmax;
       }
-      TPDG_CUDA_CHECK(cudaMemcpyAsync(W.y.p, y.data(), sizeof(double) * std::max(k, 1), cudaMemcpyHostToDevice, st));
-      launch_combine(V, ldv, W.y.as<double>(), k, tmp, n, st);
+      for (int k = 0; k < k_end; ++k) {
+        if (hist && nh < hist_cap) hist[nh] = status.host[k].res;
+        ++nh;
+      }
+      its += k_end;
+      const bool cyc_conv = status.host[k_end - 1].conv != 0;
+      launch_backsolve(G, k_end, st);
+      launch_combine(V, ldv, G.y, k_end, tmp, n, st);
       if (right) {
-        apply_pc(tmp, z);
+        apply_pc(tmp, z, false);
         launch_add(d_x, z, n, st);
       } else {
         launch_add(d_x, tmp, n, st);
       }
-      if (nh > 0 && std::abs(g[k]) <= target) {
+      if (cyc_conv) {
         conv = true;
         break;
       }
     }
     if (!conv) {
-      jv_device(op, d_x, tmp);
+      apply_op(d_x, tmp, false);
       launch_sub(d_b, tmp, tmp, n, st);
       double* rr = tmp;
       if (!right) {
-        apply_pc(tmp, r);
+        apply_pc(tmp, r, false);
         rr = r;
       }
       conv = host_norm(ctx, rr, n, W) <= target;
@@ -435,9 +503,9 @@ int run_gmres(tpdg_gpu_op op, tpdg_gpu_pc pc, const double* d_b, double* d_x, co
   }
   TPDG_CUDA_CHECK(cudaStreamSynchronize(st));
   if (pc) {
-    int status = 0;
-    TPDG_CUDA_CHECK(cudaMemcpy(&status, pc->status.p, sizeof(int), cudaMemcpyDeviceToHost));
-    REQUIRE(status == 0, TPDG_SINGULAR, "sylvester_solve: singular diagonal pair during the preconditioner apply");
+    int status_flag = 0;
+    TPDG_CUDA_CHECK(cudaMemcpy(&status_flag, pc->status.p, sizeof(int), cudaMemcpyDeviceToHost));
+    REQUIRE(status_flag == 0, TPDG_SINGULAR, "sylvester_solve: singular diagonal pair during the preconditioner apply");
   }
   *iterations = its;
   if (converged_out) *converged_out = conv ? 1 : 0;

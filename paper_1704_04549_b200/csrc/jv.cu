@@ -27,6 +27,7 @@ __device__ __forceinline__ const double* nbr_block(const DevSys& s, const double
 __global__ void __launch_bounds__(256) jv2d_kernel(DevSys s, const double* __restrict__ vin,
                                                     const double* __restrict__ halo, double* __restrict__ vout) {
   extern __shared__ double sm[];
+  if (s.skip && *s.skip) return;
   const int e = blockIdx.x;
   const int q = s.q, mu = s.mu, nc = s.n_c, qq = q * q, mm = mu * mu;
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -185,6 +186,7 @@ __device__ __forceinline__ int flat_face_node(int q, int f, int j0, int j1) {
 __global__ void __launch_bounds__(256) jv3d_kernel(DevSys s, const double* __restrict__ vin,
                                                     const double* __restrict__ halo, double* __restrict__ vout) {
   extern __shared__ double sm[];
+  if (s.skip && *s.skip) return;
   const int e = blockIdx.x;
   const int q = s.q, mu = s.mu, nc = s.n_c;
   const int q3 = q * q * q, m3 = mu * mu * mu, m2 = mu * mu, q2 = q * q;

@@ -189,7 +189,7 @@ __device__ void mm_slices(int r, int kk, int c, const double* a, int lda, bool a
 __global__ void __launch_bounds__(kApplyThreads) kron2d_apply_kernel(DevPC pc, const double* __restrict__ in,
                                                                       double* __restrict__ out) {
   const int blk = blockIdx.x;
-  if (pc.kind[blk] == 0) return;
+  if (pc.kind[blk] == 0 || (pc.skip && *pc.skip)) return;
   extern __shared__ double sm[];
   const int n1 = pc.n1, n2 = pc.q, ld = n2 | 1;
   double* sX = sm;
@@ -425,7 +425,7 @@ __global__ void __launch_bounds__(kSizedThreads) kron2d_sized_kernel(DevPC pc, c
   extern __shared__ double sm_all[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int blk = blockIdx.x * (kSizedThreads / 32) + warp;
-  if (blk >= pc.nblk || pc.kind[blk] == 0) return;
+  if (blk >= pc.nblk || pc.kind[blk] == 0 || (pc.skip && *pc.skip)) return;
   double* sX = sm_all + size_t(warp) * L::per_even;
   double* sT = sX + N1 * ld;
   double* sR = sT + N1 * ld;
@@ -562,7 +562,7 @@ bool launch_kron2d_sized(const DevPC& pc, const double* in, double* out, cudaStr
 __global__ void __launch_bounds__(kApplyThreads) kron3d_apply_kernel(DevPC pc, const double* __restrict__ in,
                                                                       double* __restrict__ out) {
   const int blk = blockIdx.x;
-  if (pc.kind[blk] == 0) return;
+  if (pc.kind[blk] == 0 || (pc.skip && *pc.skip)) return;
   extern __shared__ double sm[];
   const int n1 = pc.n1, q = pc.q, ld = q | 1, ss = q * ld;  // slice stride
   double* sX = sm;
@@ -635,7 +635,7 @@ size_t kron3d_smem(const DevPC& pc) {
 __global__ void __launch_bounds__(256) kron_fallback_kernel(DevPC pc, const double* __restrict__ in,
                                                              double* __restrict__ out) {
   const int blk = blockIdx.x;
-  if (pc.kind[blk] != 0) return;
+  if (pc.kind[blk] != 0 || (pc.skip && *pc.skip)) return;
   extern __shared__ double sx[];
   const int n = pc.blk_len;
   const int slot = pc.fb_slot[blk];

@@ -45,6 +45,7 @@ struct DevSys {
   const double *g, *d, *gw, *dw, *w;
   const double *jdet, *face_w, *dft, *dfm, *dfp;  // local element 0 first
   const int* conn;    // [n_local][2d][3]; neighbor index < n_local: local, >= n_local: halo slot
+  const int* skip;    // optional device flag: kernels return immediately when *skip != 0
 };
 
 // Formed KSVD preconditioner, device side. One factor record per block (element, or element x
@@ -62,6 +63,7 @@ struct DevPC {
   const double* fb_lu;   // [n_fb][blk_len^2]
   const int* fb_piv;     // [n_fb][blk_len]
   int* status;           // device error flag (SingularError inside the Sylvester solve)
+  const int* skip;       // optional device flag: kernels return immediately when *skip != 0
 };
 
 __host__ __device__ inline int rec_len_of(int dim, int n1, int q) {
@@ -104,9 +106,24 @@ void launch_dot(const double* x, const double* y, int64_t n, double* partial, do
                 cudaStream_t st);
 void launch_norm(const double* x, int64_t n, double* partial, double* result, unsigned* counter, cudaStream_t st);
 void launch_mgs_step(double* w, const double* vprev, const double* hprev, const double* vj, int64_t n,
-                     double* partial, double* result, unsigned* counter, cudaStream_t st);
+                     double* partial, double* result, unsigned* counter, cudaStream_t st, const int* skip = nullptr);
 void launch_axpy_neg(double* w, const double* h, const double* v, int64_t n, cudaStream_t st);
-void launch_scale_div(const double* in, const double* den, double* out, int64_t n, cudaStream_t st);
+void launch_scale_div(const double* in, const double* den, double* out, int64_t n, cudaStream_t st,
+                      const int* skip = nullptr);
+// Device-side Givens step of GMRES iteration k (solve/gmres.hpp:122-141); see blas.cu.
+struct GmresDev {
+  double *hc, *H, *cs, *sn, *g, *y;
+  int* done;
+  double target;
+  int m;
+};
+struct GmresStatus {  // host-mapped, one per iteration of a cycle
+  double res;
+  int conv;
+  int valid;
+};
+void launch_givens(const GmresDev& G, int k, GmresStatus* status, cudaStream_t st);
+void launch_backsolve(const GmresDev& G, int k, cudaStream_t st);
 void launch_sub(const double* b, const double* ax, double* r, int64_t n, cudaStream_t st);
 void launch_combine(const double* v, int64_t ldv, const double* y, int k, double* out, int64_t n, cudaStream_t st);
 void launch_add(double* x, const double* dx, int64_t n, cudaStream_t st);
