@@ -9,7 +9,10 @@
 //
 // MGS is fused: pass j computes w <- w - h_{j-1} v_{j-1} and the partial dot <v_j, w> in one read
 // of (w, v_{j-1}, v_j) and one write of w, so the k+1 MGS steps of iteration k cost k+2 passes.
+#include <algorithm>
 #include <cstdint>
+
+#include <cooperative_groups.h>
 
 #include "tpdg_internal.hpp"
 
@@ -209,6 +212,143 @@ __global__ void backsolve_kernel(GmresDev G, int k) {
   }
 }
 
+// All MGS passes of Arnoldi iteration k in one cooperative persistent launch (single rank):
+//   pass j <= k : w <- w - h_{j-1} v_{j-1} (j > 0), partial <v_j, w>
+//   pass k+1    : w <- w - h_k v_k, partial <w, w>; then w /= ||w|| when > 0.
+// Each CTA owns a fixed contiguous slice of w (updated only by it), so passes need no data
+// exchange; between passes a grid-wide barrier publishes the per-CTA partials, and every CTA sums
+// them in the same fixed order (deterministic, identical on all CTAs).
+constexpr int kCoopThreads = 1024;
+
+// Generation barrier for a co-resident (cooperative) grid: bar[0] = arrivals, bar[1] = generation.
+// The last arriver resets the count and bumps the generation, so the state is clean after every
+// barrier (launches that exit early on the skip flag leave it untouched).
+__device__ __forceinline__ void coop_barrier(unsigned* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* gen = bar + 1;
+    const unsigned g = *gen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+      bar[0] = 0u;
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*gen == g) {
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// MODE 0: w in global/L2; 1: w slice in shared memory; 2: w and the previous basis vector's slice
+// in shared memory (each pass then streams only v_j from HBM).
+template <int MODE>
+__global__ void __launch_bounds__(kCoopThreads) mgs_coop_kernel(double* __restrict__ V, int64_t ldv, int k,
+                                                                 int64_t n, int64_t chunk, double* __restrict__ hc,
+                                                                 double* __restrict__ partial, unsigned* bar,
+                                                                 const int* skip) {
+  if (skip && *skip) return;
+  extern __shared__ double wsm[];
+  __shared__ double sh[32];
+  __shared__ double hval;
+  const unsigned nb = gridDim.x;
+  const int64_t lo = int64_t(blockIdx.x) * chunk;
+  const int64_t hi = lo + chunk < n ? lo + chunk : n;
+  const int64_t len = hi > lo ? hi - lo : 0;
+  double* wg = V + int64_t(k + 1) * ldv + lo;
+  double* w = MODE >= 1 ? wsm : wg;
+  double* vs = wsm + chunk;  // MODE 2: previous basis vector slice
+  if (MODE >= 1) {
+    for (int64_t i = 2 * threadIdx.x; i + 1 < len; i += 2 * blockDim.x)
+      *reinterpret_cast<double2*>(wsm + i) = *reinterpret_cast<const double2*>(wg + i);
+    if ((len & 1) && threadIdx.x == 0) wsm[len - 1] = wg[len - 1];
+    __syncthreads();
+  }
+  double h = 0.0;
+  for (int j = 0; j <= k + 1; ++j) {
+    const double* vp = j > 0 ? (MODE == 2 ? vs : V + int64_t(j - 1) * ldv + lo) : nullptr;
+    const double* vj = j <= k ? V + int64_t(j) * ldv + lo : nullptr;
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll 2
+    for (int64_t i = 2 * threadIdx.x; i < len; i += 2 * blockDim.x) {
+      if (i + 1 < len) {
+        double2 wi = *reinterpret_cast<const double2*>(w + i);
+        if (vp) {
+          const double2 pv = *reinterpret_cast<const double2*>(vp + i);
+          wi.x = wi.x - h * pv.x;
+          wi.y = wi.y - h * pv.y;
+          *reinterpret_cast<double2*>(w + i) = wi;
+        }
+        double2 a = wi;
+        if (vj) {
+          a = __ldg(reinterpret_cast<const double2*>(vj + i));
+          if (MODE == 2) *reinterpret_cast<double2*>(vs + i) = a;
+        }
+        s0 += a.x * wi.x;
+        s1 += a.y * wi.y;
+      } else {
+        double wi = w[i];
+        if (vp) {
+          wi = wi - h * vp[i];
+          w[i] = wi;
+        }
+        double a = wi;
+        if (vj) {
+          a = vj[i];
+          if (MODE == 2) vs[i] = a;
+        }
+        s0 += a * wi;
+      }
+    }
+    const double bs = block_sum(s0 + s1, sh);
+    if (threadIdx.x == 0) partial[size_t(j) * nb + blockIdx.x] = bs;
+    coop_barrier(bar);
+    // fixed-order tree over the per-CTA partials (one parallel load round)
+    double v = threadIdx.x < nb ? reinterpret_cast<volatile double*>(partial)[size_t(j) * nb + threadIdx.x] : 0.0;
+    for (unsigned b = threadIdx.x + blockDim.x; b < nb; b += blockDim.x)
+      v += reinterpret_cast<volatile double*>(partial)[size_t(j) * nb + b];
+    const double tot = block_sum(v, sh);
+    if (threadIdx.x == 0) hval = j <= k ? tot : sqrt(tot);
+    __syncthreads();
+    h = hval;
+    if (blockIdx.x == 0 && threadIdx.x == 0) hc[j] = h;
+  }
+  // reference: if (hkk > 0) v[k+1] /= hkk
+  for (int64_t i = threadIdx.x; i < len; i += blockDim.x) wg[i] = h > 0.0 ? w[i] / h : w[i];
+}
+
+struct CoopPlan {
+  int grid;
+  int64_t chunk;
+  size_t smem;
+  int mode;
+};
+
+// One 1024-thread CTA per SM (cheap barrier); the most shared-memory residency that fits.
+CoopPlan mgs_coop_plan(int64_t n) {
+  int dev = 0, sms = 0;
+  TPDG_CUDA_CHECK(cudaGetDevice(&dev));
+  TPDG_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  constexpr size_t kMax = 210 * 1024;
+  TPDG_CUDA_CHECK(cudaFuncSetAttribute(mgs_coop_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kMax)));
+  TPDG_CUDA_CHECK(cudaFuncSetAttribute(mgs_coop_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kMax)));
+  int64_t chunk = (n + sms - 1) / sms;
+  chunk = (chunk + 1) & ~int64_t(1);
+  const size_t one = size_t(chunk) * sizeof(double);
+  int fit = 0;
+  if (2 * one <= kMax) {
+    TPDG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, mgs_coop_kernel<2>, kCoopThreads, 2 * one));
+    if (fit >= 1) return {sms, chunk, 2 * one, 2};
+  }
+  if (one <= kMax) {
+    TPDG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, mgs_coop_kernel<1>, kCoopThreads, one));
+    if (fit >= 1) return {sms, chunk, one, 1};
+  }
+  return {sms, chunk, 0, 0};
+}
+
 int stream_grid(int64_t n) {
   const int64_t want = (n + 255) / 256;
   const int64_t cap = 148 * 8;
@@ -256,6 +396,25 @@ void launch_scale_div(const double* in, const double* den, double* out, int64_t 
   TPDG_CUDA_CHECK(cudaGetLastError());
   ++g_launches;
 }
+
+void launch_mgs_iteration(double* V, int64_t ldv, int k, int64_t n, double* hc, double* partial, unsigned* bar,
+                          const int* skip, cudaStream_t st) {
+  static int64_t planned_n = -1;
+  static CoopPlan plan;
+  if (planned_n != n) {
+    plan = mgs_coop_plan(n);
+    planned_n = n;
+  }
+  int64_t chunk = plan.chunk;
+  void* args[] = {&V, &ldv, &k, &n, &chunk, &hc, &partial, &bar, &skip};
+  void* fn = plan.mode == 2   ? reinterpret_cast<void*>(mgs_coop_kernel<2>)
+             : plan.mode == 1 ? reinterpret_cast<void*>(mgs_coop_kernel<1>)
+                              : reinterpret_cast<void*>(mgs_coop_kernel<0>);
+  TPDG_CUDA_CHECK(cudaLaunchCooperativeKernel(fn, dim3(plan.grid), dim3(kCoopThreads), args, plan.smem, st));
+  ++g_launches;
+}
+
+int mgs_partial_doubles(int m) { return (m + 2) * 256; }
 
 void launch_givens(const GmresDev& G, int k, GmresStatus* status, cudaStream_t st) {
   givens_kernel<<<1, 32, 0, st>>>(G, k, status);

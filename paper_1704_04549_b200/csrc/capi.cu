@@ -117,6 +117,7 @@ struct tpdg_gpu_ctx_s {
 struct GmresWork {
   int64_t n = 0;
   int m = 0;
+  unsigned epoch = 0;  // MGS grid-barrier epoch (monotone counters in `counter` + 4)
   DevBuf V, z, tmp, r, xloc, hcol, partial, counter, y, scal;
 };
 
@@ -340,8 +341,10 @@ int run_gmres(tpdg_gpu_op op, tpdg_gpu_pc pc, const double* d_b, double* d_x, co
     W.tmp.alloc(sizeof(double) * n);
     W.r.alloc(sizeof(double) * n);
     W.hcol.alloc(sizeof(double) * (size_t(m + 1) * m + 4 * (m + 2)));
-    W.partial.alloc(sizeof(double) * 148 * 8);
-    W.counter.alloc(sizeof(unsigned) * 4);
+    W.partial.alloc(sizeof(double) * std::max<size_t>(148 * 8, size_t(mgs_partial_doubles(m))));
+    W.counter.alloc(sizeof(unsigned) * (4 + m + 2));
+    TPDG_CUDA_CHECK(cudaMemsetAsync(W.counter.p, 0, W.counter.bytes, st));
+    W.epoch = 0;
     W.y.alloc(sizeof(double) * (m + 2));
     W.scal.alloc(sizeof(double) * 4);
     op->gstatus.alloc(m);
@@ -349,7 +352,7 @@ int run_gmres(tpdg_gpu_op op, tpdg_gpu_pc pc, const double* d_b, double* d_x, co
     W.n = n;
     W.m = m;
   }
-  TPDG_CUDA_CHECK(cudaMemsetAsync(W.counter.p, 0, W.counter.bytes, st));
+  TPDG_CUDA_CHECK(cudaMemsetAsync(W.counter.p, 0, sizeof(unsigned) * 4, st));
   TPDG_CUDA_CHECK(cudaMemsetAsync(d_x, 0, sizeof(double) * n, st));
   double* V = W.V.as<double>();
   double* z = W.z.as<double>();
@@ -435,26 +438,21 @@ int run_gmres(tpdg_gpu_op op, tpdg_gpu_pc pc, const double* d_b, double* d_x, co
           apply_pc(z, w, true);
         }
         Prof pr(ctx, 2);
-        for (int j = 0; j <= k; ++j) {  // MGS: h_j = <v_j, w>, w -= h_j v_j (fused passes)
-          if (!multi) {
-            launch_mgs_step(w, j > 0 ? V + size_t(j - 1) * ldv : nullptr, hc + (j > 0 ? j - 1 : 0),
-                            V + size_t(j) * ldv, n, part, hc + j, ctr, st, G.done);
-          } else {
+        if (!multi) {  // fused MGS passes + normalization (one cooperative launch)
+          launch_mgs_iteration(V, ldv, k, n, hc, part, ctr + 4, G.done, st);
+        } else {
+          for (int j = 0; j <= k; ++j) {  // MGS with a cross-rank reduction per dot
             if (j > 0) launch_axpy_neg(w, hc + j - 1, V + size_t(j - 1) * ldv, n, st);
             launch_dot(V + size_t(j) * ldv, w, n, part, hc + j, ctr, st);
             allreduce_scalar(ctx, hc + j);
           }
-        }
-        if (!multi) {  // w -= h_k v_k ; h_{k+1} = ||w||
-          launch_mgs_step(w, vk, hc + k, nullptr, n, part, hc + k + 1, ctr, st, G.done);
-        } else {
           launch_axpy_neg(w, hc + k, vk, n, st);
           launch_dot(w, w, n, part, hc + k + 1, ctr, st);
           allreduce_scalar(ctx, hc + k + 1);
           sqrt_inplace_kernel<<<1, 1, 0, st>>>(hc + k + 1);
           ++g_launches;
+          launch_scale_div(w, hc + k + 1, w, n, st, G.done);
         }
-        launch_scale_div(w, hc + k + 1, w, n, st, G.done);
         launch_givens(G, k, status.dev, st);
       };
       int k_end = -1;

@@ -12,6 +12,8 @@
 //
 // HBM layout (reference orders, read once per launch): v [e][c][tensor, x fastest],
 // jdet [e][mu^d], dft [e][dir][mu^d][nc][nc], dfm/dfp [e][f][mu^(d-1)][nc][nc], face_w.
+#include <algorithm>
+
 #include "tpdg_internal.hpp"
 
 namespace tpdg_gpu {
@@ -170,6 +172,200 @@ size_t jv2d_smem(const DevSys& s) {
   const int q = s.q, mu = s.mu, nc = s.n_c;
   return sizeof(double) * size_t(3 * mu * q + nc * q * q + nc * q * mu + 4 * nc * mu * mu + 2 * nc * mu * q +
                                  12 * nc * mu);
+}
+
+// ------------------------------------------------------------------------------------ 2D, sized
+// Scalar (n_c = 1) 2D operator with compile-time (Q, MU), one warp per element, CTA-shared
+// weights, persistent grid. The five sum-factorized stages are written as register-tiled small
+// products with stacked K so that the mass and flux integrations share one pass:
+//   t    = v G^T                      (q x q) (q x mu)
+//   vals = G t                        (mu x q) (q x mu)
+//   AB   = [a jd vals | b dft0 vals ; b dft1 vals | 0] [GW^T ; DW^T]     (2 mu x 2 mu)(2 mu x q)
+//   out  = [GW | DW] AB  + face lifts (q x 2 mu)(2 mu x q)
+// FMA contraction is allowed here (the operator's parity gate is 1e-12).
+
+template <int R, int K, int C, bool BT, int TI, int TJ>
+__device__ __forceinline__ void warp_mm_fma(const double* A, int lda, const double* B, int ldb, double* O, int ldo,
+                                            int lane) {
+  constexpr int NTI = (R + TI - 1) / TI, NTJ = (C + TJ - 1) / TJ;
+  for (int t = lane; t < NTI * NTJ; t += 32) {
+    const int i0 = (t / NTJ) * TI, j0 = (t % NTJ) * TJ;
+    double acc[TI][TJ];
+#pragma unroll
+    for (int ii = 0; ii < TI; ++ii)
+#pragma unroll
+      for (int jj = 0; jj < TJ; ++jj) acc[ii][jj] = 0.0;
+#pragma unroll 2
+    for (int k = 0; k < K; ++k) {
+      double a[TI], b[TJ];
+#pragma unroll
+      for (int ii = 0; ii < TI; ++ii) a[ii] = A[(i0 + ii < R ? i0 + ii : R - 1) * lda + k];
+#pragma unroll
+      for (int jj = 0; jj < TJ; ++jj) {
+        const int j = j0 + jj < C ? j0 + jj : C - 1;
+        b[jj] = BT ? B[j * ldb + k] : B[k * ldb + j];
+      }
+#pragma unroll
+      for (int ii = 0; ii < TI; ++ii)
+#pragma unroll
+        for (int jj = 0; jj < TJ; ++jj) acc[ii][jj] = fma(a[ii], b[jj], acc[ii][jj]);
+    }
+#pragma unroll
+    for (int ii = 0; ii < TI; ++ii)
+#pragma unroll
+      for (int jj = 0; jj < TJ; ++jj)
+        if (i0 + ii < R && j0 + jj < C) O[(i0 + ii) * ldo + j0 + jj] = acc[ii][jj];
+  }
+}
+
+template <int Q, int MU>
+struct Jv2dLayout {
+  static constexpr int M2 = 2 * MU;
+  // CTA-shared weights
+  static constexpr int w_G = 0;                      // G      MU x Q
+  static constexpr int w_W4 = w_G + MU * Q;          // [GW^T ; DW^T]  2MU x Q
+  static constexpr int w_W5 = w_W4 + M2 * Q;         // [GW | DW]      Q x 2MU
+  static constexpr int weights = w_W5 + Q * M2;
+  // per-warp element workspace (dead buffers aliased)
+  static constexpr int e_v = 0;                      // v (Q x Q), later out
+  static constexpr int e_t = e_v + Q * Q;            // t (Q x MU), later AB (2MU x Q)
+  static constexpr int e_val = e_t + M2 * Q;         // vals (MU x MU)
+  static constexpr int e_mf = e_val + MU * MU;       // [M | F0] (MU x 2MU), F1 (MU x MU)
+  static constexpr int e_tr = e_mf + 3 * MU * MU;    // traces 8 x MU, face data 4 x MU
+  static constexpr int per_elem = ((e_tr + 12 * MU) + 1) & ~1;
+  static constexpr int budget = (227 * 1024) / 8 - weights - 64;
+  static constexpr int warps = budget / per_elem >= 4 ? 4 : (budget / per_elem >= 1 ? budget / per_elem : 1);
+};
+
+template <int Q, int MU>
+__global__ void __launch_bounds__(128) jv2d_sized_kernel(DevSys s, const double* __restrict__ vin,
+                                                          const double* __restrict__ halo, double* __restrict__ vout) {
+  if (s.skip && *s.skip) return;
+  using L = Jv2dLayout<Q, MU>;
+  constexpr int M2 = L::M2, QQ = Q * Q, MM = MU * MU, NW = L::warps;
+  extern __shared__ double sm[];
+  double* W = sm;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  double* E = sm + L::weights + warp * L::per_elem;
+  for (int i = threadIdx.x; i < MU * Q; i += blockDim.x) {
+    const int a = i / Q, j = i % Q;
+    W[L::w_G + i] = s.g[i];
+    W[L::w_W4 + a * Q + j] = s.gw[j * MU + a];          // GW^T
+    W[L::w_W4 + (MU + a) * Q + j] = s.dw[j * MU + a];   // DW^T
+    W[L::w_W5 + j * M2 + a] = s.gw[j * MU + a];         // GW
+    W[L::w_W5 + j * M2 + MU + a] = s.dw[j * MU + a];    // DW
+  }
+  __syncthreads();
+  if (warp >= NW) return;
+  const double* G = W + L::w_G;
+  for (int e = blockIdx.x * NW + warp; e < s.n_local; e += gridDim.x * NW) {
+    double* v = E + L::e_v;
+    double* t = E + L::e_t;
+    double* ab = E + L::e_t;
+    double* val = E + L::e_val;
+    double* mf = E + L::e_mf;
+    double* f1 = mf + MU * M2;
+    double* tr = E + L::e_tr;
+    const double* ve = vin + size_t(e) * QQ;
+    for (int i = lane; i < QQ; i += 32) v[i] = ve[i];
+    __syncwarp();
+    // face traces: own (from v) and neighbour (global), tr[side][f][a]
+    for (int idx = lane; idx < 8 * MU; idx += 32) {
+      const int a = idx % MU, f = (idx / MU) % 4, side = idx / (4 * MU);
+      double acc = 0.0;
+      if (side == 0) {
+        const int layer = (f % 2) == 0 ? 0 : Q - 1;
+        if (f / 2 == 0)
+          for (int j = 0; j < Q; ++j) acc = fma(G[a * Q + j], v[j * Q + layer], acc);
+        else
+          for (int j = 0; j < Q; ++j) acc = fma(G[a * Q + j], v[layer * Q + j], acc);
+      } else {
+        const int* fc = s.conn + (size_t(e) * 4 + f) * 3;
+        if (fc[0] >= 0) {
+          const int nf = fc[1];
+          const int aa = fc[2] == 0 ? a : MU - 1 - a;
+          const int layer = (nf % 2) == 0 ? 0 : Q - 1;
+          const double* cf = nbr_block(s, vin, halo, fc[0]);
+          if (nf / 2 == 0)
+            for (int j = 0; j < Q; ++j) acc = fma(G[aa * Q + j], cf[j * Q + layer], acc);
+          else
+            for (int j = 0; j < Q; ++j) acc = fma(G[aa * Q + j], cf[layer * Q + j], acc);
+        }
+      }
+      tr[idx] = acc;
+    }
+    warp_mm_fma<Q, Q, MU, true, 2, 4>(v, Q, G, Q, t, MU, lane);  // t = v G^T
+    __syncwarp();
+    for (int idx = lane; idx < 4 * MU; idx += 32) {  // face data g[f][a]
+      const int a = idx % MU, f = idx / MU;
+      const size_t fq = (size_t(e) * 4 + f) * MU + a;
+      const double acc = fma(s.dfm[fq], tr[f * MU + a], s.dfp[fq] * tr[(4 + f) * MU + a]);
+      tr[8 * MU + idx] = -s.b * s.face_w[fq] * acc;
+    }
+    warp_mm_fma<MU, Q, MU, false, 2, 4>(G, Q, t, MU, val, MU, lane);  // vals = G t
+    __syncwarp();
+    const double* jd = s.jdet + size_t(e) * MM;
+    const double* d0 = s.dft + size_t(e) * 2 * MM;
+    const double* d1 = d0 + MM;
+    for (int qv = lane; qv < MM; qv += 32) {
+      const int be = qv / MU, al = qv % MU;
+      const double x = val[qv];
+      mf[be * M2 + al] = s.a * jd[qv] * x;
+      mf[be * M2 + MU + al] = s.b * (d0[qv] * x);
+      f1[qv] = s.b * (d1[qv] * x);
+    }
+    __syncwarp();
+    warp_mm_fma<MU, M2, Q, false, 2, 4>(mf, M2, W + L::w_W4, Q, ab, Q, lane);       // A = [M|F0][GW^T;DW^T]
+    warp_mm_fma<MU, MU, Q, false, 2, 4>(f1, MU, W + L::w_W4, Q, ab + MU * Q, Q, lane);  // B = F1 GW^T
+    __syncwarp();
+    warp_mm_fma<Q, M2, Q, false, 2, 4>(W + L::w_W5, M2, ab, Q, v, Q, lane);  // out = [GW|DW][A;B] (into v)
+    __syncwarp();
+    double* oe = vout + size_t(e) * QQ;
+    const double* gf = tr + 8 * MU;
+    for (int idx = lane; idx < QQ; idx += 32) {
+      const int i = idx % Q, j = idx / Q;
+      double acc = v[idx];
+      if (i == 0 || i == Q - 1) {
+        const double* g = gf + (i == 0 ? 0 : 1) * MU;
+        for (int a = 0; a < MU; ++a) acc = fma(G[a * Q + j], g[a], acc);
+      }
+      if (j == 0 || j == Q - 1) {
+        const double* g = gf + (j == 0 ? 2 : 3) * MU;
+        for (int a = 0; a < MU; ++a) acc = fma(G[a * Q + i], g[a], acc);
+      }
+      oe[idx] = acc;
+    }
+    __syncwarp();
+  }
+}
+
+template <int Q, int MU>
+bool try_jv2d_sized(const DevSys& s, const double* vin, const double* halo, double* vout, cudaStream_t st) {
+  if (s.dim != 2 || s.n_c != 1 || s.q != Q || s.mu != MU) return false;
+  using L = Jv2dLayout<Q, MU>;
+  const size_t smem = sizeof(double) * size_t(L::weights + L::warps * L::per_elem);
+  static int grid = 0;
+  if (!grid) {
+    TPDG_CUDA_CHECK(cudaFuncSetAttribute(jv2d_sized_kernel<Q, MU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(smem)));
+    TPDG_CUDA_CHECK(cudaFuncSetAttribute(jv2d_sized_kernel<Q, MU>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                         100));
+    int per_sm = 0;
+    TPDG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jv2d_sized_kernel<Q, MU>, 128, smem));
+    int dev = 0, sms = 0;
+    TPDG_CUDA_CHECK(cudaGetDevice(&dev));
+    TPDG_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    grid = std::max(1, per_sm) * sms;
+  }
+  const int need = (s.n_local + L::warps - 1) / L::warps;
+  jv2d_sized_kernel<Q, MU><<<std::min(grid, need), 128, smem, st>>>(s, vin, halo, vout);
+  return true;
+}
+
+bool launch_jv2d_sized(const DevSys& s, const double* vin, const double* halo, double* vout, cudaStream_t st) {
+  return try_jv2d_sized<5, 6>(s, vin, halo, vout, st) || try_jv2d_sized<9, 10>(s, vin, halo, vout, st) ||
+         try_jv2d_sized<16, 17>(s, vin, halo, vout, st) || try_jv2d_sized<21, 22>(s, vin, halo, vout, st) ||
+         try_jv2d_sized<31, 32>(s, vin, halo, vout, st);
 }
 
 // ------------------------------------------------------------------------------------ 3D
@@ -402,6 +598,11 @@ size_t jv_smem_bytes(const DevSys& s) { return s.dim == 2 ? jv2d_smem(s) : jv3d_
 void launch_jv(const DevSys& s, const double* vin, const double* halo, double* vout, cudaStream_t st) {
   if (s.n_local == 0) return;
   const size_t smem = jv_smem_bytes(s);
+  if (s.dim == 2 && launch_jv2d_sized(s, vin, halo, vout, st)) {
+    TPDG_CUDA_CHECK(cudaGetLastError());
+    ++g_launches;
+    return;
+  }
   if (s.dim == 2) {
     static size_t configured = 0;
     if (smem > configured) {

@@ -123,6 +123,10 @@ struct GmresStatus {  // host-mapped, one per iteration of a cycle
   int valid;
 };
 void launch_givens(const GmresDev& G, int k, GmresStatus* status, cudaStream_t st);
+// All MGS passes + normalization of iteration k in one cooperative launch (single rank).
+void launch_mgs_iteration(double* V, int64_t ldv, int k, int64_t n, double* hc, double* partial, unsigned* bar,
+                          const int* skip, cudaStream_t st);
+int mgs_partial_doubles(int m);
 void launch_backsolve(const GmresDev& G, int k, cudaStream_t st);
 void launch_sub(const double* b, const double* ax, double* r, int64_t n, cudaStream_t st);
 void launch_combine(const double* v, int64_t ldv, const double* y, int k, double* out, int64_t n, cudaStream_t st);
