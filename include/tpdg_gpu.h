@@ -137,6 +137,19 @@ int tpdg_gpu_gmres_host(tpdg_gpu_op op, tpdg_gpu_pc pc, const double *h_b, doubl
                         const tpdg_gpu_gmres_config *cfg, int *iterations, double *hist, int hist_cap,
                         int *converged);
 
+/* ---- multi-rank element partition and face-neighbour halo plan (host only; what op_create uses
+ * for nranks > 1). Rank r owns [E r / N, E (r+1) / N). conn: [n_local][2d][3] with neighbours
+ * mapped to local ids (< n_local) or halo slots (n_local + s); halo_gid: global id per slot;
+ * peer i: elements this rank sends (local ids, ascending) and the halo slot range it receives. */
+typedef struct tpdg_halo_plan_s *tpdg_halo_plan;
+int tpdg_halo_plan_create(const tpdg_gpu_system *sys, int rank, int nranks, tpdg_halo_plan *out);
+int tpdg_halo_plan_query(tpdg_halo_plan h, int *e_begin, int *e_end, int *n_halo, int *n_peers);
+int tpdg_halo_plan_conn(tpdg_halo_plan h, int *conn_out);
+int tpdg_halo_plan_halo_gid(tpdg_halo_plan h, int *gid_out);
+int tpdg_halo_plan_peer(tpdg_halo_plan h, int i, int *rank, int *n_send, int *send_local, int *recv_first,
+                        int *recv_count);
+int tpdg_halo_plan_destroy(tpdg_halo_plan h);
+
 /* ---- host-side input production for the BASELINE configurations (out of the kernel scope;
  * restates build_reference / generate_mesh(cartesian) / build_cache for scalar advection).
  * case_kind: 0 = 2D constant velocity (vel[0], vel[1]); 1 = 2D swirl (sin 2 pi y, cos 2 pi x);

@@ -95,7 +95,8 @@ EXPORTS = [
     "tpdg_gpu_pc_import_factors", "tpdg_gpu_pc_destroy", "tpdg_gpu_pc_num_fallbacks", "tpdg_gpu_pc_fallbacks",
     "tpdg_gpu_pc_factor_len", "tpdg_gpu_pc_export_factors", "tpdg_gpu_pc_apply", "tpdg_gpu_pc_apply_host",
     "tpdg_gpu_gmres", "tpdg_gpu_gmres_host", "tpdg_setup_advection", "tpdg_setup_system", "tpdg_setup_destroy",
-    "tpdg_uniform_vector", "tpdg_seeded_unit_vector",
+    "tpdg_uniform_vector", "tpdg_seeded_unit_vector", "tpdg_halo_plan_create", "tpdg_halo_plan_query",
+    "tpdg_halo_plan_conn", "tpdg_halo_plan_halo_gid", "tpdg_halo_plan_peer", "tpdg_halo_plan_destroy",
 ]
 
 
@@ -139,6 +140,12 @@ def lib():
         "tpdg_setup_system": [v, C.POINTER(_System)], "tpdg_setup_destroy": [v],
         "tpdg_uniform_vector": [C.c_uint64, C.c_int64, C.c_double, dp],
         "tpdg_seeded_unit_vector": [C.c_int64, C.c_uint64, dp],
+        "tpdg_halo_plan_create": [C.POINTER(_System), C.c_int, C.c_int, C.POINTER(v)],
+        "tpdg_halo_plan_query": [v] + [C.POINTER(C.c_int)] * 4,
+        "tpdg_halo_plan_conn": [v, C.POINTER(C.c_int)], "tpdg_halo_plan_halo_gid": [v, C.POINTER(C.c_int)],
+        "tpdg_halo_plan_peer": [v, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                C.POINTER(C.c_int), C.POINTER(C.c_int)],
+        "tpdg_halo_plan_destroy": [v],
     }
     for name, args in sig.items():
         f = getattr(L, name)
@@ -241,6 +248,35 @@ def setup_advection(kind, nx, ny=None, nz=1, p=1, vel=(1.0, 0.5, 0.0), periodic=
         return System(dim, 1, s.p, mu, E, arrays, s.state_hash)
     finally:
         lib().tpdg_setup_destroy(h)
+
+
+def halo_plan(sys: "System", rank: int, nranks: int) -> dict:
+    """Element partition + face-neighbour halo plan of one rank (host only; op_create uses the
+    same plan for nranks > 1). See include/tpdg_gpu.h."""
+    h = C.c_void_p()
+    cs = sys._c()
+    _check(lib().tpdg_halo_plan_create(C.byref(cs), rank, nranks, C.byref(h)))
+    try:
+        eb, ee, nh, npeer = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        _check(lib().tpdg_halo_plan_query(h, C.byref(eb), C.byref(ee), C.byref(nh), C.byref(npeer)))
+        nl = ee.value - eb.value
+        conn = np.zeros(max(1, nl * 2 * sys.dim * 3), dtype=np.int32)
+        _check(lib().tpdg_halo_plan_conn(h, conn.ctypes.data_as(C.POINTER(C.c_int))))
+        gid = np.zeros(max(1, nh.value), dtype=np.int32)
+        _check(lib().tpdg_halo_plan_halo_gid(h, gid.ctypes.data_as(C.POINTER(C.c_int))))
+        peers = []
+        for i in range(npeer.value):
+            r, ns, rf, rc = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+            _check(lib().tpdg_halo_plan_peer(h, i, C.byref(r), C.byref(ns), None, C.byref(rf), C.byref(rc)))
+            send = np.zeros(max(1, ns.value), dtype=np.int32)
+            _check(lib().tpdg_halo_plan_peer(h, i, C.byref(r), C.byref(ns),
+                                             send.ctypes.data_as(C.POINTER(C.c_int)), C.byref(rf), C.byref(rc)))
+            peers.append({"rank": r.value, "send_local": send[: ns.value].copy(), "recv_first": rf.value,
+                          "recv_count": rc.value})
+        return {"e_begin": eb.value, "e_end": ee.value, "n_halo": nh.value,
+                "conn": conn[: nl * 2 * sys.dim * 3].copy(), "halo_gid": gid[: nh.value].copy(), "peers": peers}
+    finally:
+        lib().tpdg_halo_plan_destroy(h)
 
 
 # --------------------------------------------------------------------------- device objects

@@ -148,9 +148,9 @@ struct tpdg_gpu_op_s {
   DevBuf shuf_ws;
   // halo plan (multi-rank): for each peer rank, local elements to send and halo slots to fill
   struct Peer {
-    int rank;
+    int rank = 0;
     std::vector<int> send_local;  // local element ids
-    int recv_first, recv_count;   // halo slot range
+    int recv_first = 0, recv_count = 0;  // halo slot range
     DevBuf send_idx, send_buf;
   };
   std::vector<Peer> peers;
@@ -717,92 +717,23 @@ int tpdg_gpu_op_create(tpdg_gpu_ctx ctx, const tpdg_gpu_system* sys, double dt, 
     upload(op->dft, sys->dft + size_t(e_begin) * d * nqv * nc * nc, nl * d * nqv * nc * nc, st);
     upload(op->dfm, sys->dfm + size_t(e_begin) * 2 * d * nqf * nc * nc, nl * 2 * d * nqf * nc * nc, st);
     upload(op->dfp, sys->dfp + size_t(e_begin) * 2 * d * nqf * nc * nc, nl * 2 * d * nqf * nc * nc, st);
-    // connectivity: local ids for owned neighbours, halo slots (grouped by owner rank) otherwise
-    const int nranks = ctx->nranks;
-    // rank r owns the contiguous element range [E r / N, E (r+1) / N) (rows in 2D, slabs in 3D)
-    std::vector<int> owner_lo(nranks + 1);
-    for (int r = 0; r <= nranks; ++r) owner_lo[r] = int((int64_t(sys->n_elements) * r) / nranks);
-    if (nranks > 1)
-      REQUIRE(e_begin == owner_lo[ctx->rank] && e_end == owner_lo[ctx->rank + 1], TPDG_CONFIG,
-              "op_create: multi-rank element range must be [E r / N, E (r+1) / N)");
-    auto owner_of = [&](int e) {
-      int r = int(std::upper_bound(owner_lo.begin(), owner_lo.end(), e) - owner_lo.begin()) - 1;
-      return std::min(std::max(r, 0), nranks - 1);
-    };
-    std::vector<std::vector<int>> need(nranks);  // global ids needed from each rank
-    std::vector<int> conn(nl * 2 * d * 3);
-    for (size_t le = 0; le < nl; ++le)
-      for (int f = 0; f < 2 * d; ++f) {
-        const int64_t* fc = sys->conn + ((size_t(e_begin) + le) * 2 * d + f) * 3;
-        const int64_t nb = fc[0];
-        conn[(le * 2 * d + f) * 3 + 1] = int(fc[1]);
-        conn[(le * 2 * d + f) * 3 + 2] = int(fc[2]);
-        if (nb < 0) {
-          conn[(le * 2 * d + f) * 3] = -1;
-        } else if (nb >= e_begin && nb < e_end) {
-          conn[(le * 2 * d + f) * 3] = int(nb - e_begin);
-        } else {
-          REQUIRE(nranks > 1, TPDG_CONFIG, "op_create: neighbour outside the local range needs nranks > 1");
-          conn[(le * 2 * d + f) * 3] = -2 - int(nb);  // resolved below
-          need[owner_of(int(nb))].push_back(int(nb));
-        }
-      }
-    std::vector<int> halo_slot_of;  // sorted unique global ids -> slot
-    std::vector<int> halo_ids;
-    for (int r = 0; r < nranks; ++r) {
-      std::sort(need[r].begin(), need[r].end());
-      need[r].erase(std::unique(need[r].begin(), need[r].end()), need[r].end());
-    }
-    int slot = int(nl);
-    std::vector<std::pair<int, int>> gid_slot;
-    for (int r = 0; r < nranks; ++r) {
-      if (r == ctx->rank || need[r].empty()) continue;
+    // partition + halo plan (halo.cpp)
+    const HaloPlan plan = build_halo_plan(sys, ctx->rank, ctx->nranks, e_begin, e_end);
+    const std::vector<int>& conn = plan.conn;
+    op->n_halo = plan.n_halo;
+    for (const auto& pp : plan.peers) {
       tpdg_gpu_op_s::Peer p;
-      p.rank = r;
-      p.recv_first = slot - int(nl);
-      p.recv_count = int(need[r].size());
-      for (int gid : need[r]) gid_slot.push_back({gid, slot++});
+      p.rank = pp.rank;
+      p.send_local = pp.send_local;
+      p.recv_first = pp.recv_first;
+      p.recv_count = pp.recv_count;
+      if (!p.send_local.empty()) {
+        upload(p.send_idx, p.send_local.data(), p.send_local.size(), st);
+        p.send_buf.alloc(sizeof(double) * p.send_local.size() * nc * npe);
+      }
       op->peers.push_back(std::move(p));
     }
-    std::sort(gid_slot.begin(), gid_slot.end());
-    for (auto& c : conn) (void)c;
-    for (size_t i = 0; i < conn.size(); i += 3)
-      if (conn[i] <= -2) {
-        const int gid = -2 - conn[i];
-        auto it = std::lower_bound(gid_slot.begin(), gid_slot.end(), std::make_pair(gid, -1));
-        conn[i] = it->second;
-      }
-    op->n_halo = slot - int(nl);
-    // Send lists: the elements of mine that peer r needs = my elements adjacent to r's range.
-    // Structured symmetric connectivity: r needs element x of mine iff x has a neighbour owned by r.
-    if (nranks > 1) {
-      for (int r = 0; r < nranks; ++r) {
-        if (r == ctx->rank) continue;
-        std::vector<int> send;
-        for (size_t le = 0; le < nl; ++le)
-          for (int f = 0; f < 2 * d; ++f) {
-            const int64_t nb = sys->conn[((size_t(e_begin) + le) * 2 * d + f) * 3];
-            if (nb >= 0 && owner_of(int(nb)) == r) {
-              send.push_back(int(le));
-              break;
-            }
-          }
-        if (send.empty()) continue;
-        auto it = std::find_if(op->peers.begin(), op->peers.end(), [&](const tpdg_gpu_op_s::Peer& p) { return p.rank == r; });
-        if (it == op->peers.end()) {
-          tpdg_gpu_op_s::Peer p;
-          p.rank = r;
-          p.recv_first = 0;
-          p.recv_count = 0;
-          op->peers.push_back(std::move(p));
-          it = op->peers.end() - 1;
-        }
-        it->send_local = send;  // ascending local id == ascending global id (contiguous ranges)
-        upload(it->send_idx, send.data(), send.size(), st);
-        it->send_buf.alloc(sizeof(double) * send.size() * nc * npe);
-      }
-      op->halo.alloc(sizeof(double) * std::max<size_t>(1, size_t(op->n_halo) * nc * npe));
-    }
+    if (ctx->nranks > 1) op->halo.alloc(sizeof(double) * std::max<size_t>(1, size_t(op->n_halo) * nc * npe));
     upload(op->conn, conn.data(), conn.size(), st);
     const double a = jacobian_only ? 0.0 : 1.0, b = jacobian_only ? 1.0 : -dt;
     op->s = make_devsys(*op, block_mode, a, b);
@@ -989,6 +920,58 @@ int tpdg_gpu_gmres_host(tpdg_gpu_op op, tpdg_gpu_pc pc, const double* h_b, doubl
     TPDG_CUDA_CHECK(cudaStreamSynchronize(st));
   });
   return g != TPDG_OK ? g : rc;
+}
+
+// ---- multi-rank plan (host only; tested with gloo on CPU)
+struct tpdg_halo_plan_s {
+  HaloPlan p;
+  int dim;
+};
+
+int tpdg_halo_plan_create(const tpdg_gpu_system* sys, int rank, int nranks, tpdg_halo_plan* out) {
+  return guarded([&] {
+    REQUIRE(sys && out, TPDG_CONFIG, "halo_plan: null argument");
+    const int lo = int((int64_t(sys->n_elements) * rank) / nranks);
+    const int hi = int((int64_t(sys->n_elements) * (rank + 1)) / nranks);
+    std::unique_ptr<tpdg_halo_plan_s> h(new tpdg_halo_plan_s);
+    h->p = build_halo_plan(sys, rank, nranks, lo, hi);
+    h->dim = sys->dim;
+    *out = h.release();
+  });
+}
+
+int tpdg_halo_plan_query(tpdg_halo_plan h, int* e_begin, int* e_end, int* n_halo, int* n_peers) {
+  return guarded([&] {
+    *e_begin = h->p.e_begin;
+    *e_end = h->p.e_end;
+    *n_halo = h->p.n_halo;
+    *n_peers = int(h->p.peers.size());
+  });
+}
+
+int tpdg_halo_plan_conn(tpdg_halo_plan h, int* conn_out) {
+  return guarded([&] { std::copy(h->p.conn.begin(), h->p.conn.end(), conn_out); });
+}
+
+int tpdg_halo_plan_halo_gid(tpdg_halo_plan h, int* gid_out) {
+  return guarded([&] { std::copy(h->p.halo_gid.begin(), h->p.halo_gid.end(), gid_out); });
+}
+
+int tpdg_halo_plan_peer(tpdg_halo_plan h, int i, int* rank, int* n_send, int* send_local, int* recv_first,
+                        int* recv_count) {
+  return guarded([&] {
+    REQUIRE(i >= 0 && i < int(h->p.peers.size()), TPDG_SHAPE, "halo_plan_peer: index out of range");
+    const auto& p = h->p.peers[i];
+    *rank = p.rank;
+    *n_send = int(p.send_local.size());
+    if (send_local) std::copy(p.send_local.begin(), p.send_local.end(), send_local);
+    *recv_first = p.recv_first;
+    *recv_count = p.recv_count;
+  });
+}
+
+int tpdg_halo_plan_destroy(tpdg_halo_plan h) {
+  return guarded([&] { delete h; });
 }
 
 // ---- host setup

@@ -36,6 +36,20 @@ int setup_advection(int kind, const double* vel, int nx, int ny, int nz, int p, 
 void uniform_vector(uint64_t seed, int64_t n, double scale, double* out);
 void seeded_unit_vector(int64_t n, uint64_t seed, double* out);
 
+// ---------------------------------------------------------------- multi-rank plan (halo.cpp)
+struct HaloPlan {
+  int e_begin = 0, e_end = 0, n_halo = 0;
+  std::vector<int> conn;          // [n_local][2d][3]: neighbour -> local id (< n_local) or halo slot
+  std::vector<int> halo_gid;      // global element id of each halo slot
+  struct Peer {
+    int rank = 0;
+    std::vector<int> send_local;  // local elements sent to this peer (ascending)
+    int recv_first = 0, recv_count = 0;  // halo slot range received from this peer
+  };
+  std::vector<Peer> peers;
+};
+HaloPlan build_halo_plan(const tpdg_gpu_system* sys, int rank, int nranks, int e_begin, int e_end);
+
 // ---------------------------------------------------------------- device views (POD, by value)
 // Discretization + linearization of the local elements, reference layouts.
 struct DevSys {

@@ -1,0 +1,46 @@
+"""Drop-in boundary: the C++ wrapper (include/tpdg_gpu.hpp) over the C ABI, fed by the reference's own
+types. The demo binary is compiled in the build container against the unmodified reference headers
+(tests/dropin/Makefile) and travels to the GPU box; it runs the reference's CPU gmres and the B200
+path on the same LinearizedOperator and exits non-zero unless the iteration counts agree."""
+import json
+import os
+import shutil
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+DEMO = os.path.join(ROOT, "tests", "dropin", "_build", "dropin_demo")
+
+
+def test_wrapper_header_compiles_without_reference():
+    gxx = shutil.which("g++")
+    if not gxx:
+        pytest.skip("no g++")
+    src = '#include "tpdg_gpu.hpp"\nint main() { return 0; }\n'
+    r = subprocess.run([gxx, "-std=c++20", "-fsyntax-only", "-I", os.path.join(ROOT, "include"), "-x", "c++", "-"],
+                       input=src, text=True, capture_output=True)
+    assert r.returncode == 0, r.stderr
+
+
+def test_c_header_is_plain_c():
+    gcc = shutil.which("gcc")
+    if not gcc:
+        pytest.skip("no gcc")
+    src = '#include "tpdg_gpu.h"\nint main(void) { return 0; }\n'
+    r = subprocess.run([gcc, "-std=c99", "-Wall", "-Werror", "-fsyntax-only", "-I", os.path.join(ROOT, "include"),
+                        "-x", "c", "-"], input=src, text=True, capture_output=True)
+    assert r.returncode == 0, r.stderr
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,p", [(8, 8), (16, 15)])
+def test_reference_types_through_the_dropin(n, p):
+    if not os.path.exists(DEMO):
+        pytest.skip("dropin demo not built (needs /root/reference at build time)")
+    r = subprocess.run([DEMO, str(n), str(p)], capture_output=True, text=True, timeout=600)
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    print(line)
+    assert r.returncode == 0 and line["ref_its"] == line["gpu_its"]
+    assert line["jv_rel"] <= 1e-12
+    assert line["ref_fallbacks"] == line["gpu_fallbacks"]
