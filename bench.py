@@ -269,10 +269,16 @@ def main_ours(args, rank, world, local_rank):
                        "algorithmic_bytes": algo, "achieved_gbs": algo / (ms / cnt * 1e-3) / 1e9}
     dom = max(kern, key=lambda k: kern[k]["share"]) if kern else None
     roof = None
+    traffic = {}
+    try:  # per-launch DRAM bytes of the same kernels from an ncu --set full capture (profiles/)
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            traffic = json.load(f)
+    except Exception:
+        pass
     if dom:
         ach = kern[dom]["achieved_gbs"]
         roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm, "unit": "GB/s",
-                "frac": ach / hbm, "peak_kind": hbm_kind, "traffic": None,
+                "frac": ach / hbm, "peak_kind": hbm_kind, "traffic": traffic.get(dom) if p == 15 else None,
                 "algorithmic_bytes_per_launch": kern[dom]["algorithmic_bytes"]}
     kron = None
     if "pc_apply" in kern:

@@ -15,6 +15,8 @@
 // (LuFactor::solve_inplace, tensor/small_matrix.hpp:189-192), stored column-major so that the
 // column sweeps read coalesced columns; its forward sweep keeps the reference order, the backward
 // sweep runs column-descending (per-row order reversed; the block itself is well conditioned).
+#include <cstdint>
+
 #include "faithful.cuh"
 #include "tpdg_internal.hpp"
 
@@ -23,6 +25,16 @@ namespace tpdg_gpu {
 namespace {
 
 constexpr int kApplyThreads = 128;
+
+__device__ __forceinline__ void cp_async16(double* smem, const double* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 // Quasi-triangular diagonal block structure (tensor/sylvester.hpp:16-30); returns block count.
 __device__ int quasi_blocks_dev(const double* t, int n, int* start, int* size) {
@@ -432,12 +444,18 @@ __global__ void __launch_bounds__(kSizedThreads) kron2d_sized_kernel(DevPC pc, c
   double* sTol = sR + rec;
   int* sPiv = reinterpret_cast<int*>(sTol + 2);
   int* sb = sPiv + N1 + N2;  // s1[N1] z1[N1] s2[N2] z2[N2] nb1 nb2 all11
-  {
+  {  // asynchronous global -> shared copies (LDGSTS), one round trip for the whole record
     const double* r = pc.rec + size_t(blk) * rec;
-    for (int i = lane; i < rec; i += 32) sR[i] = r[i];
+    if ((reinterpret_cast<uintptr_t>(r) & 15) == 0) {
+      for (int i = 2 * lane; i + 1 < rec; i += 64) cp_async16(sR + i, r + i);
+      if ((rec & 1) && lane == 0) sR[rec - 1] = r[rec - 1];
+    } else {
+      for (int i = lane; i < rec; i += 32) cp_async8(sR + i, r + i);
+    }
     for (int i = lane; i < N1 + N2; i += 32) sPiv[i] = pc.piv[size_t(blk) * (N1 + N2) + i];
     const double* x = in + size_t(blk) * (N1 * N2);
-    for (int i = lane; i < N1 * N2; i += 32) sX[(i / N2) * ld + i % N2] = x[i];
+    for (int i = lane; i < N1 * N2; i += 32) cp_async8(sX + (i / N2) * ld + i % N2, x + i);
+    cp_async_wait_all();
   }
   __syncwarp();
   const double* luA2 = sR;
