@@ -178,13 +178,18 @@ def main_ours(args, rank, world, local_rank):
         if dist:
             dist.barrier()
 
-    # ---- form (timed separately; once per solve in the reference's newton_linear_solve)
-    torch.cuda.synchronize()
-    barrier()
-    t0 = time.perf_counter()
+    # ---- form (timed separately; once per solve in the reference's newton_linear_solve):
+    # one warm-up formation, then the median of 3
     pc = T.form_ksvd(op)
-    torch.cuda.synchronize()
-    form_s = time.perf_counter() - t0
+    form_times = []
+    for _ in range(3):
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        pc = T.form_ksvd(op)
+        torch.cuda.synchronize()
+        form_times.append(time.perf_counter() - t0)
+    form_s = statistics.median(form_times)
     nfb = len(pc.fallbacks)
 
     b = torch.from_numpy(b_host).to(dev)

@@ -588,9 +588,8 @@ void alloc_records(tpdg_gpu_pc pc) {
 void make_factors_all(tpdg_gpu_pc pc) {
   tpdg_gpu_op op = pc->op;
   const int n1 = (op->s.small ? 1 : op->n_c) * op->q;
-  const int grid = std::min(pc->nblk, 148 * 8);
   DevBuf work;
-  work.alloc(sizeof(double) * size_t(grid) * (4 * std::max(n1, op->q) + 16));
+  work.alloc(sizeof(double) * size_t(make_factors_work_groups()) * (4 * std::max(n1, op->q) + 16));
   launch_make_factors(op->dim, op->q, n1, pc->nblk, pc->raw.as<double>(), pc->rec.as<double>(), pc->piv.as<int>(),
                       pc->kind.as<int>(), work.as<double>(), op->ctx->stream);
   TPDG_CUDA_CHECK(cudaStreamSynchronize(op->ctx->stream));
@@ -813,11 +812,12 @@ int tpdg_gpu_form_ksvd(tpdg_gpu_op op, const tpdg_gpu_ksvd_config* cfg_in, tpdg_
     upload(dsv2, sv2.data(), sv2.size(), st);
     const int J = std::max(cfg.lanczos_max_it > 0 ? cfg.lanczos_max_it : 2 * cfg.terms + 20, 22);
     const size_t per = lanczos_work_doubles(op->s, J);
-    // persistent grid, bounded workspace (<= ~4 GiB)
-    int grid = std::min(pc->nblk, 148 * 8);
-    while (grid > 148 && double(grid) * per * 8.0 > 4.0 * (1 << 30)) grid /= 2;
+    // persistent grid of 8-warp CTAs, one block per warp, bounded workspace (<= ~4 GiB)
+    int groups = std::min(pc->nblk, 148 * 16);
+    while (groups > 148 && double(groups) * per * 8.0 > 4.0 * (1 << 30)) groups /= 2;
+    const int grid = (groups + 7) / 8;
     if (pc->nblk > 0) {
-      work.alloc(sizeof(double) * size_t(grid) * per);
+      work.alloc(sizeof(double) * size_t(grid) * 8 * per);
       launch_lanczos_form(op->s, cfg, dsv.as<double>(), dsv2.as<double>(), pc->raw.as<double>(), nullptr,
                           pc->kind.as<int>(), work.as<double>(), per, grid, st);
       TPDG_CUDA_CHECK(cudaStreamSynchronize(st));

@@ -18,6 +18,7 @@
 // Householder columns/rows, rotation columns), which leaves each result bit-identical to the
 // reference's sequential code. The only non-bit-identical operations are CUDA's libm sin / cos /
 // atan / atan2 inside standardize_2x2 (<= 2 ulp vs glibc).
+#include <algorithm>
 #include <cstdio>
 
 #include "faithful.cuh"
@@ -30,30 +31,42 @@ namespace {
 
 constexpr int kFormThreads = 256;
 
+constexpr int kMaxGroups = kFormThreads / 32;
+template <class G>
+__device__ __forceinline__ int groups_per_cta() {
+  return 1;
+}
+template <>
+__device__ __forceinline__ int groups_per_cta<WarpGroup>() {
+  return int(blockDim.x >> 5);
+}
+
 __device__ __forceinline__ void bsync() { __syncthreads(); }
 
 // ---------------------------------------------------------------- sequential reductions
 // dot / norm in the reference's order (single thread), broadcast through shared memory.
-__device__ double seq_dot(const double* a, const double* b, long n, double* sh) {
-  if (threadIdx.x == 0) {
+template <class Grp>
+__device__ double seq_dot(const Grp& g, const double* a, const double* b, long n, double* sh) {
+  if (g.rank() == 0) {
     double s = 0.0;
     for (long i = 0; i < n; ++i) s += a[i] * b[i];
     *sh = s;
   }
-  bsync();
+  g.sync();
   const double r = *sh;
-  bsync();
+  g.sync();
   return r;
 }
-__device__ double seq_norm(const double* a, long n, double* sh) {
-  if (threadIdx.x == 0) {
+template <class Grp>
+__device__ double seq_norm(const Grp& g, const double* a, long n, double* sh) {
+  if (g.rank() == 0) {
     double s = 0.0;
     for (long i = 0; i < n; ++i) s += a[i] * a[i];
     *sh = sqrt(s);
   }
-  bsync();
+  g.sync();
   const double r = *sh;
-  bsync();
+  g.sync();
   return r;
 }
 
@@ -67,31 +80,33 @@ struct LzOp {
   __host__ __device__ long cols() const { return long(m2) * n2; }
 };
 
-__device__ void op_apply(const LzOp& op, const double* x, double* y, double* ws) {
+template <class Grp>
+__device__ void op_apply(const Grp& g, const LzOp& op, const double* x, double* y, double* ws) {
   if (op.kind == 0) {
-    if (op.k.s.dim == 2) shuf_apply_2d_dev(op.k, x, y, ws); else shuf_apply_3d_dev(op.k, x, y, ws);
+    if (op.k.s.dim == 2) shuf_apply_2d_dev(g, op.k, x, y, ws); else shuf_apply_3d_dev(g, op.k, x, y, ws);
     return;
   }
   const long R = op.rows(), Cn = op.cols();
-  for (long i = threadIdx.x; i < R; i += blockDim.x) {  // matvec (small_matrix.hpp:116-124)
+  for (long i = g.rank(); i < R; i += g.size()) {  // matvec (small_matrix.hpp:116-124)
     double s = 0.0;
     for (long j = 0; j < Cn; ++j) s += op.dense[i * Cn + j] * x[j];
     y[i] = s;
   }
-  bsync();
+  g.sync();
 }
-__device__ void op_apply_t(const LzOp& op, const double* x, double* y, double* ws) {
+template <class Grp>
+__device__ void op_apply_t(const Grp& g, const LzOp& op, const double* x, double* y, double* ws) {
   if (op.kind == 0) {
-    if (op.k.s.dim == 2) shuf_apply_t_2d_dev(op.k, x, y, ws); else shuf_apply_t_3d_dev(op.k, x, y, ws);
+    if (op.k.s.dim == 2) shuf_apply_t_2d_dev(g, op.k, x, y, ws); else shuf_apply_t_3d_dev(g, op.k, x, y, ws);
     return;
   }
   const long R = op.rows(), Cn = op.cols();
-  for (long j = threadIdx.x; j < Cn; j += blockDim.x) {  // matvec_transpose (small_matrix.hpp:127-135)
+  for (long j = g.rank(); j < Cn; j += g.size()) {  // matvec_transpose (small_matrix.hpp:127-135)
     double s = 0.0;
     for (long i = 0; i < R; ++i) s += op.dense[i * Cn + j] * x[i];
     y[j] = s;
   }
-  bsync();
+  g.sync();
 }
 
 // ---------------------------------------------------------------- Jacobi SVD (single thread)
@@ -180,64 +195,65 @@ struct LzWork {
 };
 
 // fa: r x (m1 x n1), fb: r x (m2 x n2), sig: r. Returns iterations (reference `iterations`).
-__device__ int lanczos_dev(const LzOp& op, int r, int max_iter, double breakdown, const double* start, double* fa,
+template <class Grp>
+__device__ int lanczos_dev(const Grp& g, const LzOp& op, int r, int max_iter, double breakdown, const double* start, double* fa,
                            double* fb, double* sig, LzWork& W, double* sh) {
   const long nrows = op.rows(), ncols = op.cols();
-  const int tid = threadIdx.x, nt = blockDim.x;
+  const int tid = g.rank(), nt = g.size();
   for (long i = tid; i < r * nrows; i += nt) fa[i] = 0.0;
   for (long i = tid; i < r * ncols; i += nt) fb[i] = 0.0;
   if (tid < r) sig[tid] = 0.0;
   for (long i = tid; i < ncols; i += nt) W.V[i] = start[i];
-  bsync();
-  op_apply(op, W.V, W.U, W.opws);
-  double alpha = seq_norm(W.U, nrows, sh);
+  g.sync();
+  op_apply(g, op, W.V, W.U, W.opws);
+  double alpha = seq_norm(g, W.U, nrows, sh);
   const double tol = breakdown * fmax(alpha, 1e-300);
   if (alpha < 1e-300) return 0;
   for (long i = tid; i < nrows; i += nt) W.U[i] = W.U[i] / alpha;
   if (tid == 0) W.alpha[0] = alpha;
   int nv = 1, nu = 1, na = 1, nb = 0, iters = 1;
-  bsync();
+  g.sync();
   while (na < max_iter) {
     double* p = W.V + size_t(nv) * ncols;
-    op_apply_t(op, W.U + size_t(nu - 1) * nrows, p, W.opws);
+    op_apply_t(g, op, W.U + size_t(nu - 1) * nrows, p, W.opws);
     const double al = W.alpha[na - 1];
     const double* vl = W.V + size_t(nv - 1) * ncols;
     for (long i = tid; i < ncols; i += nt) p[i] = p[i] - al * vl[i];
-    bsync();
+    g.sync();
     for (int pass = 0; pass < 2; ++pass)
       for (int j = 0; j < nv; ++j) {
         const double* qj = W.V + size_t(j) * ncols;
-        const double dot = seq_dot(qj, p, ncols, sh);
+        const double dot = seq_dot(g, qj, p, ncols, sh);
         for (long i = tid; i < ncols; i += nt) p[i] = p[i] - dot * qj[i];
-        bsync();
+        g.sync();
       }
-    const double beta = seq_norm(p, ncols, sh);
+    const double beta = seq_norm(g, p, ncols, sh);
     ++iters;
     if (beta < tol) break;
     for (long i = tid; i < ncols; i += nt) p[i] = p[i] / beta;
     if (tid == 0) W.beta[nb] = beta;
     ++nv;
     ++nb;
-    bsync();
+    g.sync();
     double* rv = W.U + size_t(nu) * nrows;
-    op_apply(op, W.V + size_t(nv - 1) * ncols, rv, W.opws);
+    op_apply(g, op, W.V + size_t(nv - 1) * ncols, rv, W.opws);
     const double* ul = W.U + size_t(nu - 1) * nrows;
     for (long i = tid; i < nrows; i += nt) rv[i] = rv[i] - beta * ul[i];
-    bsync();
+    g.sync();
     for (int pass = 0; pass < 2; ++pass)
       for (int j = 0; j < nu; ++j) {
         const double* qj = W.U + size_t(j) * nrows;
-        const double dot = seq_dot(qj, rv, nrows, sh);
+        const double dot = seq_dot(g, qj, rv, nrows, sh);
         for (long i = tid; i < nrows; i += nt) rv[i] = rv[i] - dot * qj[i];
-        bsync();
+        g.sync();
       }
-    alpha = seq_norm(rv, nrows, sh);
+    alpha = seq_norm(g, rv, nrows, sh);
     if (alpha < tol) break;
     for (long i = tid; i < nrows; i += nt) rv[i] = rv[i] / alpha;
     if (tid == 0) W.alpha[na] = alpha;
     ++nu;
     ++na;
-    bsync();
+    g.sync();
   }
   const int ku = nu, kv = nv, kmin = ku < kv ? ku : kv;
   if (tid == 0) {
@@ -250,7 +266,7 @@ __device__ int lanczos_dev(const LzOp& op, int r, int max_iter, double breakdown
     svd_small_dev(ku, kv, W.B, W.bu, W.bs, W.bv, W.sw, W.sw + J1 * J1, W.sw + 2 * J1 * J1, W.order);
     for (int j = 0; j < r; ++j) sig[j] = (j < kmin && W.bs[j] > 0.0) ? W.bs[j] : 0.0;
   }
-  bsync();
+  g.sync();
   for (int j = 0; j < r; ++j) {
     if (!(j < kmin && W.bs[j] > 0.0)) continue;
     const double scale = sqrt(W.bs[j]);
@@ -265,12 +281,13 @@ __device__ int lanczos_dev(const LzOp& op, int r, int max_iter, double breakdown
       fb[j * ncols + (i % op.m2) * op.n2 + i / op.m2] = scale * s;
     }
   }
-  bsync();
+  g.sync();
   return iters;
 }
 
-__device__ void set_identity_dev(int n, double* m) {
-  for (int i = threadIdx.x; i < n * n; i += blockDim.x) m[i] = (i / n == i % n) ? 1.0 : 0.0;
+template <class Grp>
+__device__ void set_identity_dev(const Grp& g, int n, double* m) {
+  for (int i = g.rank(); i < n * n; i += g.size()) m[i] = (i / n == i % n) ? 1.0 : 0.0;
 }
 
 // Lanczos work layout per CTA.
@@ -298,19 +315,24 @@ __device__ LzWork carve_lz(double* base, int J, long rows, long cols) {
 
 // Per block: raw factors (2D: a1 b1 a2 b2 ; 3D: a1 b1 c1 b2 c2) after the degenerate collapse;
 // kind[blk] = 0 when the 3D stage-1 singular value vanishes (-> fallback), else 1 (pending).
+template <class Grp>
 __global__ void __launch_bounds__(kFormThreads) lanczos_form_kernel(DevSys s, tpdg_gpu_ksvd_config cfg,
                                                                      const double* start_vec,
                                                                      const double* start_vec2, double* raw,
                                                                      int* kind, double* work, size_t work_per_cta,
                                                                      int nblk) {
-  __shared__ double sh[4];
+  const int NG = groups_per_cta<Grp>();
+  const Grp g;
+  const int gid = NG == 1 ? 0 : int(threadIdx.x >> 5);
+  __shared__ double sh_all[kMaxGroups][4];
+  double* sh = sh_all[gid];
   const int q = s.q, ncb = s.small ? 1 : s.n_c, m1 = ncb * q, m2 = s.dim == 2 ? q : q * q;
   const int terms = cfg.terms;
   const int J = cfg.lanczos_max_it > 0 ? cfg.lanczos_max_it : 2 * terms + 20;
   const int J1 = cfg.lanczos_max_it > 0 ? cfg.lanczos_max_it : 2 * 1 + 20;
   const int rl = raw_len_of(s.dim, m1, q);
-  double* wbase = work + size_t(blockIdx.x) * work_per_cta;
-  for (int blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+  double* wbase = work + (size_t(blockIdx.x) * NG + gid) * work_per_cta;
+  for (int blk = blockIdx.x * NG + gid; blk < nblk; blk += gridDim.x * NG) {
     const int bpe = s.small ? s.n_c : 1;
     const int e = blk / bpe, comp = blk % bpe;
     LzOp op;
@@ -330,26 +352,26 @@ __global__ void __launch_bounds__(kFormThreads) lanczos_form_kernel(DevSys s, tp
       double* fa = W.opws + opws;              // terms x m1^2
       double* fb = fa + size_t(terms) * m1 * m1;  // terms x q^2
       double* sig = fb + size_t(terms) * q * q;
-      lanczos_dev(op, terms, Jm, cfg.breakdown_tol, start_vec, fa, fb, sig, W, sh);
+      lanczos_dev(g, op, terms, Jm, cfg.breakdown_tol, start_vec, fa, fb, sig, W, sh);
       double* a1 = rb;
       double* b1 = a1 + m1 * m1;
       double* a2 = b1 + q * q;
       double* b2 = a2 + m1 * m1;
-      for (int i = threadIdx.x; i < m1 * m1; i += blockDim.x) {
+      for (int i = g.rank(); i < m1 * m1; i += g.size()) {
         a1[i] = fa[i];
         a2[i] = terms > 1 ? fa[m1 * m1 + i] : 0.0;
       }
-      for (int i = threadIdx.x; i < q * q; i += blockDim.x) {
+      for (int i = g.rank(); i < q * q; i += g.size()) {
         b1[i] = fb[i];
         b2[i] = terms > 1 ? fb[q * q + i] : 0.0;
       }
-      bsync();
+      g.sync();
       if (terms < 2 || sig[1] <= cfg.degenerate_tol * sig[0]) {
-        set_identity_dev(m1, a2);
-        for (int i = threadIdx.x; i < q * q; i += blockDim.x) b2[i] = 0.0;
+        set_identity_dev(g, m1, a2);
+        for (int i = g.rank(); i < q * q; i += g.size()) b2[i] = 0.0;
       }
-      if (threadIdx.x == 0) kind[blk] = 1;
-      bsync();
+      if (g.rank() == 0) kind[blk] = 1;
+      g.sync();
     } else {
       // stage 1: A ~ A1 (x) D1 (r = 1)
       LzWork W = carve_lz(wbase, J1, op.rows(), op.cols());
@@ -360,52 +382,53 @@ __global__ void __launch_bounds__(kFormThreads) lanczos_form_kernel(DevSys s, tp
       double* fb2 = shd + size_t(m2) * m2;  // terms x q^2
       double* fc2 = fb2 + size_t(terms) * q * q;
       double* sig2 = fc2 + size_t(terms) * q * q;
-      lanczos_dev(op, 1, J1, cfg.breakdown_tol, start_vec, fa, d1, sig1, W, sh);
+      lanczos_dev(g, op, 1, J1, cfg.breakdown_tol, start_vec, fa, d1, sig1, W, sh);
       if (!(sig1[0] > 0.0)) {
-        if (threadIdx.x == 0) kind[blk] = 0;
-        bsync();
+        if (g.rank() == 0) kind[blk] = 0;
+        g.sync();
         continue;
       }
       // shuffle_dense(D1, q, q, q, q) (tensor/shuffle.hpp:16-25)
-      for (int t = threadIdx.x; t < m2 * m2; t += blockDim.x) {
+      for (int t = g.rank(); t < m2 * m2; t += g.size()) {
         const int c = t % q, r = (t / q) % q, j = (t / (q * q)) % q, i = t / (q * q * q);
         shd[(j * q + i) * (q * q) + c * q + r] = d1[(i * q + r) * (q * q) + j * q + c];
       }
-      bsync();
+      g.sync();
       LzOp op2;
       op2.kind = 1;
       op2.k = op.k;
       op2.dense = shd;
       op2.m1 = op2.n1 = op2.m2 = op2.n2 = q;
       LzWork W2 = carve_lz(wbase, J, op2.rows(), op2.cols());
-      lanczos_dev(op2, terms, J, cfg.breakdown_tol, start_vec2, fb2, fc2, sig2, W2, sh);
+      lanczos_dev(g, op2, terms, J, cfg.breakdown_tol, start_vec2, fb2, fc2, sig2, W2, sh);
       double* a1 = rb;
       double* b1 = a1 + m1 * m1;
       double* c1 = b1 + q * q;
       double* b2 = c1 + q * q;
       double* c2 = b2 + q * q;
-      for (int i = threadIdx.x; i < m1 * m1; i += blockDim.x) a1[i] = fa[i];
-      for (int i = threadIdx.x; i < q * q; i += blockDim.x) {
+      for (int i = g.rank(); i < m1 * m1; i += g.size()) a1[i] = fa[i];
+      for (int i = g.rank(); i < q * q; i += g.size()) {
         b1[i] = fb2[i];
         c1[i] = fc2[i];
         b2[i] = terms > 1 ? fb2[q * q + i] : 0.0;
         c2[i] = terms > 1 ? fc2[q * q + i] : 0.0;
       }
-      bsync();
+      g.sync();
       if (terms < 2 || sig2[1] <= cfg.degenerate_tol * sig2[0]) {
-        set_identity_dev(q, b2);
-        for (int i = threadIdx.x; i < q * q; i += blockDim.x) c2[i] = 0.0;
+        set_identity_dev(g, q, b2);
+        for (int i = g.rank(); i < q * q; i += g.size()) c2[i] = 0.0;
       }
-      if (threadIdx.x == 0) kind[blk] = 1;
-      bsync();
+      if (g.rank() == 0) kind[blk] = 1;
+      g.sync();
     }
   }
 }
 
 // ---------------------------------------------------------------- dense LU (CTA-cooperative)
 // LuFactor ctor on an n x n row-major matrix (copied to lu). Returns false if singular.
-__device__ bool lu_factor_dev(int n, const double* a, double* lu, int* perm, double* sh, int* ish) {
-  const int tid = threadIdx.x, nt = blockDim.x;
+template <class Grp>
+__device__ bool lu_factor_dev(const Grp& g, int n, const double* a, double* lu, int* perm, double* sh, int* ish) {
+  const int tid = g.rank(), nt = g.size();
   for (int i = tid; i < n * n; i += nt) lu[i] = a[i];
   for (int i = tid; i < n; i += nt) perm[i] = i;
   // inf_norm: row sums in order, then max
@@ -418,7 +441,7 @@ __device__ bool lu_factor_dev(int n, const double* a, double* lu, int* perm, dou
     }
     sh[0] = 1e-14 * fmax(m, 1e-300);
   }
-  bsync();
+  g.sync();
   const double tol = sh[0];
   for (int k = 0; k < n; ++k) {
     if (tid == 0) {
@@ -438,7 +461,7 @@ __device__ bool lu_factor_dev(int n, const double* a, double* lu, int* perm, dou
         perm[piv] = t;
       }
     }
-    bsync();
+    g.sync();
     const int piv = ish[0];
     if (piv < 0) return false;
     if (piv != k)
@@ -447,23 +470,24 @@ __device__ bool lu_factor_dev(int n, const double* a, double* lu, int* perm, dou
         lu[k * n + j] = lu[piv * n + j];
         lu[piv * n + j] = t;
       }
-    bsync();
+    g.sync();
     const double inv = 1.0 / lu[k * n + k];
     for (int i = k + 1 + tid; i < n; i += nt) lu[i * n + k] = lu[i * n + k] * inv;
-    bsync();
+    g.sync();
     const int rem = n - k - 1;
     for (int t = tid; t < rem * rem; t += nt) {
       const int i = k + 1 + t / rem, j = k + 1 + t % rem;
       lu[i * n + j] -= lu[i * n + k] * lu[k * n + j];
     }
-    bsync();
+    g.sync();
   }
   return true;
 }
 
 // lu_solve_matrix (ksvd.hpp:48-57): x(:, j) = LU^{-1} rhs(:, j), columns in parallel.
-__device__ void lu_solve_cols_dev(int n, const double* lu, const int* perm, int cols, const double* rhs, double* x) {
-  for (int j = threadIdx.x; j < cols; j += blockDim.x) {
+template <class Grp>
+__device__ void lu_solve_cols_dev(const Grp& g, int n, const double* lu, const int* perm, int cols, const double* rhs, double* x) {
+  for (int j = g.rank(); j < cols; j += g.size()) {
     for (int i = 0; i < n; ++i) x[i * cols + j] = rhs[perm[i] * cols + j];
     for (int i = 0; i < n; ++i) {
       double s = x[i * cols + j];
@@ -476,19 +500,21 @@ __device__ void lu_solve_cols_dev(int n, const double* lu, const int* perm, int 
       x[i * cols + j] = s / lu[i * n + i];
     }
   }
-  bsync();
+  g.sync();
 }
 
 // ---------------------------------------------------------------- real Schur (CTA-cooperative)
-__device__ void rot_left_dev(double* m, int n, int i, int j, double c, double s) {
-  for (int k = threadIdx.x; k < n; k += blockDim.x) {
+template <class Grp>
+__device__ void rot_left_dev(const Grp& g, double* m, int n, int i, int j, double c, double s) {
+  for (int k = g.rank(); k < n; k += g.size()) {
     const double x = m[i * n + k], y = m[j * n + k];
     m[i * n + k] = c * x + s * y;
     m[j * n + k] = -s * x + c * y;
   }
 }
-__device__ void rot_right_dev(double* m, int n, int i, int j, double c, double s) {
-  for (int k = threadIdx.x; k < n; k += blockDim.x) {
+template <class Grp>
+__device__ void rot_right_dev(const Grp& g, double* m, int n, int i, int j, double c, double s) {
+  for (int k = g.rank(); k < n; k += g.size()) {
     const double x = m[k * n + i], y = m[k * n + j];
     m[k * n + i] = c * x + s * y;
     m[k * n + j] = -s * x + c * y;
@@ -496,8 +522,9 @@ __device__ void rot_right_dev(double* m, int n, int i, int j, double c, double s
 }
 
 // standardize_2x2 (schur.hpp:86-113)
-__device__ void standardize_2x2_dev(double* h, double* q, int n, int l, double* sh) {
-  if (threadIdx.x == 0) {
+template <class Grp>
+__device__ void standardize_2x2_dev(const Grp& g, double* h, double* q, int n, int l, double* sh) {
+  if (g.rank() == 0) {
     const double a = h[l * n + l], b = h[l * n + l + 1], c = h[(l + 1) * n + l], d = h[(l + 1) * n + l + 1];
     sh[2] = 0.0;
     if (c == 0.0) {
@@ -523,27 +550,28 @@ __device__ void standardize_2x2_dev(double* h, double* q, int n, int l, double* 
       sh[3] = 1.0;
     }
   }
-  bsync();
+  g.sync();
   if (sh[3] < 0.0) {
-    bsync();
+    g.sync();
     return;
   }
   const double cc = sh[0], ss = sh[1];
   const bool real_pair = sh[2] != 0.0;
-  rot_left_dev(h, n, l, l + 1, cc, ss);
-  bsync();
-  rot_right_dev(h, n, l, l + 1, cc, ss);
-  rot_right_dev(q, n, l, l + 1, cc, ss);
-  bsync();
-  if (threadIdx.x == 0 && real_pair) h[(l + 1) * n + l] = 0.0;
-  bsync();
+  rot_left_dev(g, h, n, l, l + 1, cc, ss);
+  g.sync();
+  rot_right_dev(g, h, n, l, l + 1, cc, ss);
+  rot_right_dev(g, q, n, l, l + 1, cc, ss);
+  g.sync();
+  if (g.rank() == 0 && real_pair) h[(l + 1) * n + l] = 0.0;
+  g.sync();
 }
 
 // real_schur (schur.hpp:119-232). h holds C on entry, T on exit; returns false on budget exhaustion.
-__device__ bool real_schur_dev(int n, double* h, double* q, double* v, double* sh, int* ish) {
-  const int tid = threadIdx.x, nt = blockDim.x;
+template <class Grp>
+__device__ bool real_schur_dev(const Grp& g, int n, double* h, double* q, double* v, double* sh, int* ish) {
+  const int tid = g.rank(), nt = g.size();
   for (int i = tid; i < n * n; i += nt) q[i] = (i / n == i % n) ? 1.0 : 0.0;
-  bsync();
+  g.sync();
   if (n == 1) return true;
   // Householder Hessenberg (schur.hpp:38-79)
   for (int k = 0; k + 2 < n; ++k) {
@@ -567,7 +595,7 @@ __device__ bool real_schur_dev(int n, double* h, double* q, double* v, double* s
         }
       }
     }
-    bsync();
+    g.sync();
     if (ish[0] == 0) continue;
     const double beta = sh[0], alpha = sh[1];
     for (int j = k + tid; j < n; j += nt) {  // H <- P H
@@ -576,7 +604,7 @@ __device__ bool real_schur_dev(int n, double* h, double* q, double* v, double* s
       dot *= beta;
       for (int i = k + 1; i < n; ++i) h[i * n + j] -= dot * v[i];
     }
-    bsync();
+    g.sync();
     for (int i = tid; i < n; i += nt) {  // H <- H P ; Q <- Q P
       double dot = 0.0;
       for (int j = k + 1; j < n; ++j) dot += h[i * n + j] * v[j];
@@ -587,12 +615,12 @@ __device__ bool real_schur_dev(int n, double* h, double* q, double* v, double* s
       dq *= beta;
       for (int j = k + 1; j < n; ++j) q[i * n + j] -= dq * v[j];
     }
-    bsync();
+    g.sync();
     if (tid == 0) {
       for (int i = k + 2; i < n; ++i) h[i * n + k] = 0.0;
       h[(k + 1) * n + k] = alpha;
     }
-    bsync();
+    g.sync();
   }
   double hnorm;
   if (tid == 0) {
@@ -604,9 +632,9 @@ __device__ bool real_schur_dev(int n, double* h, double* q, double* v, double* s
     }
     sh[0] = fmax(m, 1e-300);
   }
-  bsync();
+  g.sync();
   hnorm = sh[0];
-  bsync();
+  g.sync();
   const double eps = 2.3e-16;
   int m = n - 1, iter = 0, total = 0;
   const int budget = 60 * n;
@@ -625,16 +653,16 @@ __device__ bool real_schur_dev(int n, double* h, double* q, double* v, double* s
       }
       ish[0] = l;
     }
-    bsync();
+    g.sync();
     const int l = ish[0];
-    bsync();
+    g.sync();
     if (l == m) {
       m -= 1;
       iter = 0;
       continue;
     }
     if (l == m - 1) {
-      standardize_2x2_dev(h, q, n, l, sh);
+      standardize_2x2_dev(g, h, q, n, l, sh);
       m -= 2;
       iter = 0;
       continue;
@@ -677,7 +705,7 @@ __device__ bool real_schur_dev(int n, double* h, double* q, double* v, double* s
           }
         }
       }
-      bsync();
+      g.sync();
       if (ish[1]) {
         const double beta = sh[0];
         const int row_hi = (k + len < n) ? k + len : n;
@@ -688,7 +716,7 @@ __device__ bool real_schur_dev(int n, double* h, double* q, double* v, double* s
           dot *= beta;
           for (int i = 0; i < len; ++i) H(k + i, j) -= dot * v[i];
         }
-        bsync();
+        g.sync();
         const int row_top = ((m < k + len) ? m : k + len) + 1;
         for (int i = tid; i < n; i += nt) {
           if (i < row_top) {
@@ -702,24 +730,24 @@ __device__ bool real_schur_dev(int n, double* h, double* q, double* v, double* s
           dq *= beta;
           for (int j = k; j < row_hi; ++j) q[i * n + j] -= dq * v[j - k];
         }
-        bsync();
+        g.sync();
       }
       x = H(k + 1, k);
       if (k + 2 <= m) y = H(k + 2, k);
       if (k + 3 <= m) z = H(k + 3, k);
-      bsync();
+      g.sync();
     }
     for (int t = tid; t < n * n; t += nt) {
       const int i = t / n, j = t % n;
       if (i >= l + 2 && i <= m && j >= l && j <= i - 2) H(i, j) = 0.0;
     }
-    bsync();
+    g.sync();
 #undef H
   }
   for (int l = 0; l + 1 < n; ++l) {
     const double sub = h[(l + 1) * n + l];
-    bsync();
-    if (sub != 0.0) standardize_2x2_dev(h, q, n, l, sh);
+    g.sync();
+    if (sub != 0.0) standardize_2x2_dev(g, h, q, n, l, sh);
   }
   return true;
 }
@@ -766,33 +794,35 @@ __device__ double inf_norm_seq(int n, const double* a) {
 }
 
 // check_sylvester_pair (ksvd.hpp:61-73): true when usable.
-__device__ bool check_pair_dev(int n1, const double* t1, int n2, const double* t2, double* eig, double* sh,
+template <class Grp>
+__device__ bool check_pair_dev(const Grp& g, int n1, const double* t1, int n2, const double* t2, double* eig, double* sh,
                                int* ish) {
   double* re1 = eig;
   double* im1 = re1 + n1;
   double* re2 = im1 + n1;
   double* im2 = re2 + n2;
-  if (threadIdx.x == 0) {
+  if (g.rank() == 0) {
     quasi_eigs_dev(n1, t1, re1, im1);
     quasi_eigs_dev(n2, t2, re2, im2);
     sh[0] = inf_norm_seq(n1, t1) + inf_norm_seq(n2, t2);
     ish[0] = 0;
   }
-  bsync();
+  g.sync();
   const double thr = 1e-12 * fmax(sh[0], 1e-300);
-  for (int t = threadIdx.x; t < n1 * n2; t += blockDim.x) {
+  for (int t = g.rank(); t < n1 * n2; t += g.size()) {
     const int i = t / n2, j = t % n2;
     const double re = re1[i] + re2[j], im = im1[i] + im2[j];
     if (sqrt(re * re + im * im) < thr) ish[0] = 1;
   }
-  bsync();
+  g.sync();
   const bool ok = ish[0] == 0;
-  bsync();
+  g.sync();
   return ok;
 }
 
 // make_factors_2d / 3d into a record (layout in tpdg_internal.hpp). Returns true when usable.
-__device__ bool make_factors_dev(int dim, int q, int n1, const double* raw, double* rec, int* piv, double* w,
+template <class Grp>
+__device__ bool make_factors_dev(const Grp& g, int dim, int q, int n1, const double* raw, double* rec, int* piv, double* w,
                                  double* sh, int* ish) {
   if (dim == 2) {
     const double* a1 = raw;
@@ -805,13 +835,13 @@ __device__ bool make_factors_dev(int dim, int q, int n1, const double* raw, doub
     double* T1 = Q1 + n1 * n1;
     double* Q2 = T1 + n1 * n1;
     double* T2 = Q2 + q * q;
-    if (!lu_factor_dev(n1, a2, luA2, piv, sh, ish)) return false;
-    if (!lu_factor_dev(q, b1, luB1, piv + n1, sh, ish)) return false;
-    lu_solve_cols_dev(n1, luA2, piv, n1, a1, T1);      // C1 = A2^{-1} A1 (Schur in place in T1)
-    lu_solve_cols_dev(q, luB1, piv + n1, q, b2, T2);   // C2 = B1^{-1} B2
-    if (!real_schur_dev(n1, T1, Q1, w, sh, ish)) return false;
-    if (!real_schur_dev(q, T2, Q2, w, sh, ish)) return false;
-    return check_pair_dev(n1, T1, q, T2, w, sh, ish);
+    if (!lu_factor_dev(g, n1, a2, luA2, piv, sh, ish)) return false;
+    if (!lu_factor_dev(g, q, b1, luB1, piv + n1, sh, ish)) return false;
+    lu_solve_cols_dev(g, n1, luA2, piv, n1, a1, T1);      // C1 = A2^{-1} A1 (Schur in place in T1)
+    lu_solve_cols_dev(g, q, luB1, piv + n1, q, b2, T2);   // C2 = B1^{-1} B2
+    if (!real_schur_dev(g, n1, T1, Q1, w, sh, ish)) return false;
+    if (!real_schur_dev(g, q, T2, Q2, w, sh, ish)) return false;
+    return check_pair_dev(g, n1, T1, q, T2, w, sh, ish);
   }
   const double* a1 = raw;
   const double* b1 = a1 + n1 * n1;
@@ -825,59 +855,88 @@ __device__ bool make_factors_dev(int dim, int q, int n1, const double* raw, doub
   double* T1 = Q1 + q * q;
   double* Q2 = T1 + q * q;
   double* T2 = Q2 + q * q;
-  if (!lu_factor_dev(n1, a1, luA1, piv, sh, ish)) return false;
-  if (!lu_factor_dev(q, b2, luB2, piv + n1, sh, ish)) return false;
-  if (!lu_factor_dev(q, c1, luC1, piv + n1 + q, sh, ish)) return false;
-  lu_solve_cols_dev(q, luB2, piv + n1, q, b1, T1);       // G1 = B2^{-1} B1
-  lu_solve_cols_dev(q, luC1, piv + n1 + q, q, c2, T2);   // G2 = C1^{-1} C2
-  if (!real_schur_dev(q, T1, Q1, w, sh, ish)) return false;
-  if (!real_schur_dev(q, T2, Q2, w, sh, ish)) return false;
-  return check_pair_dev(q, T1, q, T2, w, sh, ish);
+  if (!lu_factor_dev(g, n1, a1, luA1, piv, sh, ish)) return false;
+  if (!lu_factor_dev(g, q, b2, luB2, piv + n1, sh, ish)) return false;
+  if (!lu_factor_dev(g, q, c1, luC1, piv + n1 + q, sh, ish)) return false;
+  lu_solve_cols_dev(g, q, luB2, piv + n1, q, b1, T1);       // G1 = B2^{-1} B1
+  lu_solve_cols_dev(g, q, luC1, piv + n1 + q, q, c2, T2);   // G2 = C1^{-1} C2
+  if (!real_schur_dev(g, q, T1, Q1, w, sh, ish)) return false;
+  if (!real_schur_dev(g, q, T2, Q2, w, sh, ish)) return false;
+  return check_pair_dev(g, q, T1, q, T2, w, sh, ish);
 }
 
 // Per block with kind == 1: factors; on failure swap the (second-stage) terms and retry;
 // on second failure kind = 0 (fallback). NOTE: the reference lets a Schur ConvergenceError
 // escape (process abort); here it is routed to the swap / fallback path.
+// The whole per-block working set (raw factors, the record being built, pivots, scratch) lives in
+// shared memory when it fits (SMEM = true): the serial sections of LU / Hessenberg / Francis QR then
+// pay shared-memory rather than L2 latency per access. Results are copied out at the end.
+template <bool SMEM, class Grp>
 __global__ void __launch_bounds__(kFormThreads) make_factors_kernel(int dim, int q, int n1, int nblk,
                                                                      double* raw, double* rec, int* piv, int* kind,
                                                                      double* work) {
-  __shared__ double sh[8];
-  __shared__ int ish[4];
+  const int NG = groups_per_cta<Grp>();
+  const Grp g;
+  const int gid = NG == 1 ? 0 : int(threadIdx.x >> 5);
+  __shared__ double sh_all[kMaxGroups][8];
+  __shared__ int ish_all[kMaxGroups][4];
+  double* sh = sh_all[gid];
+  int* ish = ish_all[gid];
+  extern __shared__ double fsm_all[];
   const int rl = raw_len_of(dim, n1, q), rcl = rec_len_of(dim, n1, q), pl = piv_len_of(dim, n1, q);
-  double* w = work + size_t(blockIdx.x) * (4 * (n1 > q ? n1 : q) + 16);
-  for (int blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+  const int wl = 4 * (n1 > q ? n1 : q) + 16;
+  const size_t per_group = size_t(wl + rl + rcl) + size_t(pl + 1) / 2 + 2;
+  double* fsm = fsm_all + (SMEM ? size_t(gid) * per_group : 0);
+  double* w = SMEM ? fsm : work + (size_t(blockIdx.x) * NG + gid) * wl;
+  double* rb_s = fsm + wl;
+  double* rc_s = rb_s + rl;
+  int* pv_s = reinterpret_cast<int*>(rc_s + rcl);
+  for (int blk = blockIdx.x * NG + gid; blk < nblk; blk += gridDim.x * NG) {
     if (kind[blk] == 0) continue;
-    double* rb = raw + size_t(blk) * rl;
-    double* rc = rec + size_t(blk) * rcl;
-    int* pv = piv + size_t(blk) * pl;
-    bool ok = make_factors_dev(dim, q, n1, rb, rc, pv, w, sh, ish);
+    double* rb_g = raw + size_t(blk) * rl;
+    double* rb = SMEM ? rb_s : rb_g;
+    double* rc = SMEM ? rc_s : rec + size_t(blk) * rcl;
+    int* pv = SMEM ? pv_s : piv + size_t(blk) * pl;
+    if (SMEM) {
+      for (int i = g.rank(); i < rl; i += g.size()) rb_s[i] = rb_g[i];
+      g.sync();
+    }
+    bool ok = make_factors_dev(g, dim, q, n1, rb, rc, pv, w, sh, ish);
     if (!ok) {
       // swap: 2D (a1,b1,a2,b2) -> (a2,b2,a1,b1); 3D (b1,c1) <-> (b2,c2)
       if (dim == 2) {
         const int la = n1 * n1, lb = q * q;
-        for (int i = threadIdx.x; i < la; i += blockDim.x) {
+        for (int i = g.rank(); i < la; i += g.size()) {
           const double t = rb[i];
           rb[i] = rb[la + lb + i];
           rb[la + lb + i] = t;
         }
-        for (int i = threadIdx.x; i < lb; i += blockDim.x) {
+        for (int i = g.rank(); i < lb; i += g.size()) {
           const double t = rb[la + i];
           rb[la + i] = rb[2 * la + lb + i];
           rb[2 * la + lb + i] = t;
         }
       } else {
         const int base = n1 * n1, lb = q * q;
-        for (int i = threadIdx.x; i < 2 * lb; i += blockDim.x) {
+        for (int i = g.rank(); i < 2 * lb; i += g.size()) {
           const double t = rb[base + i];
           rb[base + i] = rb[base + 2 * lb + i];
           rb[base + 2 * lb + i] = t;
         }
       }
-      bsync();
-      ok = make_factors_dev(dim, q, n1, rb, rc, pv, w, sh, ish);
+      g.sync();
+      ok = make_factors_dev(g, dim, q, n1, rb, rc, pv, w, sh, ish);
+      if (SMEM)
+        for (int i = g.rank(); i < rl; i += g.size()) rb_g[i] = rb_s[i];  // export the swapped terms
     }
-    if (threadIdx.x == 0) kind[blk] = ok ? 1 : 0;
-    bsync();
+    if (SMEM && ok) {
+      double* rcg = rec + size_t(blk) * rcl;
+      int* pvg = piv + size_t(blk) * pl;
+      for (int i = g.rank(); i < rcl; i += g.size()) rcg[i] = rc_s[i];
+      for (int i = g.rank(); i < pl; i += g.size()) pvg[i] = pv_s[i];
+    }
+    if (g.rank() == 0) kind[blk] = ok ? 1 : 0;
+    g.sync();
   }
 }
 
@@ -1190,15 +1249,16 @@ __global__ void __launch_bounds__(1024) dense_lu_kernel(int n, double* lu_all, i
 // Test hook: one element's shuffled product.
 __global__ void __launch_bounds__(kFormThreads) shuffled_kernel(DevSys s, int e, int comp, int transpose,
                                                                  const double* in, double* out, double* ws) {
+  const CtaGroup g;
   ShufCtx k;
   k.s = s;
   k.e = e;
   k.comp = comp;
   k.ncb = s.small ? 1 : s.n_c;
   if (s.dim == 2) {
-    if (transpose) shuf_apply_t_2d_dev(k, in, out, ws); else shuf_apply_2d_dev(k, in, out, ws);
+    if (transpose) shuf_apply_t_2d_dev(g, k, in, out, ws); else shuf_apply_2d_dev(g, k, in, out, ws);
   } else {
-    if (transpose) shuf_apply_t_3d_dev(k, in, out, ws); else shuf_apply_3d_dev(k, in, out, ws);
+    if (transpose) shuf_apply_t_3d_dev(g, k, in, out, ws); else shuf_apply_3d_dev(g, k, in, out, ws);
   }
 }
 
@@ -1231,7 +1291,7 @@ void launch_lanczos_form(const DevSys& s, const tpdg_gpu_ksvd_config& cfg, const
                          size_t work_per_block, int grid, cudaStream_t st) {
   (void)sigma;
   const int nblk = s.n_local * (s.small ? s.n_c : 1);
-  lanczos_form_kernel<<<grid, kFormThreads, 0, st>>>(s, cfg, start_vec, start_vec2, raw, kind, work,
+  lanczos_form_kernel<WarpGroup><<<grid, kFormThreads, 0, st>>>(s, cfg, start_vec, start_vec2, raw, kind, work,
                                                       work_per_block, nblk);
   TPDG_CUDA_CHECK(cudaGetLastError());
   ++g_launches;
@@ -1239,12 +1299,39 @@ void launch_lanczos_form(const DevSys& s, const tpdg_gpu_ksvd_config& cfg, const
 
 void launch_make_factors(int dim, int q, int n1, int nblk, const double* raw, double* rec, int* piv, int* kind,
                          double* work, cudaStream_t st) {
-  const int grid = nblk < 148 * 8 ? nblk : 148 * 8;
-  make_factors_kernel<<<grid, kFormThreads, 0, st>>>(dim, q, n1, nblk, const_cast<double*>(raw), rec, piv, kind,
-                                                      work);
+  // one warp per block; the per-block working set in shared memory when it fits
+  const int wl = 4 * (n1 > q ? n1 : q) + 16;
+  const size_t per_group = sizeof(double) * (size_t(wl + raw_len_of(dim, n1, q) + rec_len_of(dim, n1, q)) +
+                                             size_t(piv_len_of(dim, n1, q) + 1) / 2 + 2);
+  constexpr size_t kMax = 200 * 1024;
+  int dev = 0, sms = 0;
+  TPDG_CUDA_CHECK(cudaGetDevice(&dev));
+  TPDG_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  if (per_group <= kMax) {
+    const int groups = int(std::min<size_t>(kMaxGroups, kMax / per_group));
+    const size_t smem = per_group * groups;
+    static size_t configured = 0;
+    if (smem > configured) {
+      TPDG_CUDA_CHECK(cudaFuncSetAttribute(make_factors_kernel<true, WarpGroup>,
+                                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(kMax)));
+      configured = kMax;
+    }
+    int per_sm = 0;
+    TPDG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, make_factors_kernel<true, WarpGroup>,
+                                                                  32 * groups, smem));
+    const int grid = std::min((nblk + groups - 1) / groups, std::max(1, per_sm) * sms);
+    make_factors_kernel<true, WarpGroup><<<grid, 32 * groups, smem, st>>>(dim, q, n1, nblk, const_cast<double*>(raw),
+                                                                         rec, piv, kind, work);
+  } else {  // global working set (work holds make_factors_work_groups() x wl doubles)
+    const int grid = std::min((nblk + kMaxGroups - 1) / kMaxGroups, 148 * 2);
+    make_factors_kernel<false, WarpGroup><<<grid, kFormThreads, 0, st>>>(dim, q, n1, nblk, const_cast<double*>(raw),
+                                                                        rec, piv, kind, work);
+  }
   TPDG_CUDA_CHECK(cudaGetLastError());
   ++g_launches;
 }
+
+int make_factors_work_groups() { return 148 * 2 * kMaxGroups; }
 
 size_t probe_work_doubles(const DevSys& s) {
   const size_t nfull = size_t(s.n_c) * s.npe;

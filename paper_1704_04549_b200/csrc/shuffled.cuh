@@ -12,6 +12,18 @@
 
 namespace tpdg_gpu {
 
+// Cooperating thread groups: a whole CTA or one warp works on one block.
+struct CtaGroup {
+  __device__ __forceinline__ int rank() const { return threadIdx.x; }
+  __device__ __forceinline__ int size() const { return blockDim.x; }
+  __device__ __forceinline__ void sync() const { __syncthreads(); }
+};
+struct WarpGroup {
+  __device__ __forceinline__ int rank() const { return threadIdx.x & 31; }
+  __device__ __forceinline__ int size() const { return 32; }
+  __device__ __forceinline__ void sync() const { __syncwarp(); }
+};
+
 struct ShufCtx {
   DevSys s;
   int e, comp, ncb;  // element (local), component (small mode), components in the block
@@ -32,9 +44,10 @@ __device__ __forceinline__ double sh_dfm(const ShufCtx& k, int f, int qf, int r,
 #define SD(a, j) (S.d[(a) * q + (j)])
 
 // u = Atilde v (2D). ws >= 2*mu + mu + 2*nc*nc*mu
-__device__ void shuf_apply_2d_dev(const ShufCtx& k, const double* v, double* u, double* ws) {
+template <class Grp>
+__device__ void shuf_apply_2d_dev(const Grp& g, const ShufCtx& k, const double* v, double* u, double* ws) {
   const DevSys& S = k.s;
-  const int q = S.q, mu = S.mu, nc = k.ncb, m1 = nc * q, tid = threadIdx.x, nt = blockDim.x;
+  const int q = S.q, mu = S.mu, nc = k.ncb, m1 = nc * q, tid = g.rank(), nt = g.size();
   const double a = S.a, b = S.b;
   double* tgg = ws;
   double* tdg = tgg + mu;
@@ -56,7 +69,7 @@ __device__ void shuf_apply_2d_dev(const ShufCtx& k, const double* v, double* u, 
     tgg[al] = sg;
     tdg[al] = sd;
   }
-  __syncthreads();
+  g.sync();
   for (int t = tid; t < mu * (1 + nc * nc); t += nt) {
     const int be = t % mu, rc = t / mu;  // rc == 0: sm ; rc-1 = cr*nc + cc
     if (rc == 0) {
@@ -75,7 +88,7 @@ __device__ void shuf_apply_2d_dev(const ShufCtx& k, const double* v, double* u, 
       r2[(cr * nc + cc) * mu + be] = x2;
     }
   }
-  __syncthreads();
+  g.sync();
   for (int t = tid; t < m1 * m1; t += nt) {
     const int br = t % q, cr = (t / q) % nc, dc = (t / m1) % q, cc = t / (m1 * q);
     double acc = 0.0;
@@ -104,13 +117,14 @@ __device__ void shuf_apply_2d_dev(const ShufCtx& k, const double* v, double* u, 
       }
     u[t] = acc;  // index (cc*q + dc)*m1 + cr*q + br
   }
-  __syncthreads();
+  g.sync();
 }
 
 // v = Atilde^T u (2D). ws >= 2*nc*nc*mu + 3*mu + 4*mu
-__device__ void shuf_apply_t_2d_dev(const ShufCtx& k, const double* u, double* v, double* ws) {
+template <class Grp>
+__device__ void shuf_apply_t_2d_dev(const Grp& g, const ShufCtx& k, const double* u, double* v, double* ws) {
   const DevSys& S = k.s;
-  const int q = S.q, mu = S.mu, nc = k.ncb, m1 = nc * q, tid = threadIdx.x, nt = blockDim.x;
+  const int q = S.q, mu = S.mu, nc = k.ncb, m1 = nc * q, tid = g.rank(), nt = g.size();
   const double a = S.a, b = S.b;
 #define UU(cr, br, cc, dc) u[((cc) * q + (dc)) * m1 + (cr) * q + (br)]
   double* hgg = ws;
@@ -135,7 +149,7 @@ __device__ void shuf_apply_t_2d_dev(const ShufCtx& k, const double* u, double* v
     hgg[t] = sg;
     hdg[t] = sd;
   }
-  __syncthreads();
+  g.sync();
   for (int al = tid; al < mu; al += nt) {
     double xm = 0.0, x1 = 0.0, x2 = 0.0;
     for (int be = 0; be < mu; ++be) {
@@ -184,7 +198,7 @@ __device__ void shuf_apply_t_2d_dev(const ShufCtx& k, const double* u, double* v
       fs[t] = b * fw[al] * sc;
     }
   }
-  __syncthreads();
+  g.sync();
   for (int t = tid; t < q * q; t += nt) {
     const int ar = t % q, ec = t / q;
     double acc = 0.0;
@@ -204,14 +218,15 @@ __device__ void shuf_apply_t_2d_dev(const ShufCtx& k, const double* u, double* v
       }
     v[t] = acc;
   }
-  __syncthreads();
+  g.sync();
 #undef UU
 }
 
 // u = Atilde v (3D, O(p^5)).
-__device__ void shuf_apply_3d_dev(const ShufCtx& k, const double* v, double* u, double* ws) {
+template <class Grp>
+__device__ void shuf_apply_3d_dev(const Grp& g, const ShufCtx& k, const double* v, double* u, double* ws) {
   const DevSys& S = k.s;
-  const int q = S.q, mu = S.mu, nc = k.ncb, m1 = nc * q, q2 = q * q, tid = threadIdx.x, nt = blockDim.x;
+  const int q = S.q, mu = S.mu, nc = k.ncb, m1 = nc * q, q2 = q * q, tid = g.rank(), nt = g.size();
   const double a = S.a, b = S.b;
 #define VV(a1, a2, e1, e2) v[((e2) * q + (e1)) * q2 + (a2) * q + (a1)]
   const int n4 = mu * q * q * q;
@@ -249,7 +264,7 @@ __device__ void shuf_apply_3d_dev(const ShufCtx& k, const double* v, double* u, 
       }
     wbuf[t] = s;
   }
-  __syncthreads();
+  g.sync();
   for (int t = tid; t < mu * mu; t += nt) {
     const int be = t % mu, al = t / mu;
     double sx = 0.0, sy = 0.0, sg = 0.0;
@@ -280,7 +295,7 @@ __device__ void shuf_apply_3d_dev(const ShufCtx& k, const double* v, double* u, 
     for (int al = 0; al < mu; ++al) s += fw[be * mu + al] * sh_dfm(k, f, be * mu + al, cr, cc) * wbuf[f * mu + al];
     inner[t] = s;
   }
-  __syncthreads();
+  g.sync();
   const double* jd = S.jdet + size_t(k.e) * mu * mu * mu;
   for (int t = tid; t < mu * (1 + nc * nc) + 2 * nc * nc; t += nt) {
     if (t < mu * (1 + nc * nc)) {
@@ -319,7 +334,7 @@ __device__ void shuf_apply_3d_dev(const ShufCtx& k, const double* v, double* u, 
       s2f[tt] = s;
     }
   }
-  __syncthreads();
+  g.sync();
   for (int t = tid; t < m1 * m1; t += nt) {
     const int b3 = t % q, cr = (t / q) % nc, d3 = (t / m1) % q, cc = t / (m1 * q);
     double acc = 0.0;
@@ -345,14 +360,15 @@ __device__ void shuf_apply_3d_dev(const ShufCtx& k, const double* v, double* u, 
       }
     u[t] = acc;
   }
-  __syncthreads();
+  g.sync();
 #undef VV
 }
 
 // v = Atilde^T u (3D).
-__device__ void shuf_apply_t_3d_dev(const ShufCtx& k, const double* u, double* v, double* ws) {
+template <class Grp>
+__device__ void shuf_apply_t_3d_dev(const Grp& g, const ShufCtx& k, const double* u, double* v, double* ws) {
   const DevSys& S = k.s;
-  const int q = S.q, mu = S.mu, nc = k.ncb, m1 = nc * q, q2 = q * q, tid = threadIdx.x, nt = blockDim.x;
+  const int q = S.q, mu = S.mu, nc = k.ncb, m1 = nc * q, q2 = q * q, tid = g.rank(), nt = g.size();
   const double a = S.a, b = S.b;
 #define UU(cr, b3, cc, d3) u[((cc) * q + (d3)) * m1 + (cr) * q + (b3)]
   double* hgg = ws;
@@ -379,7 +395,7 @@ __device__ void shuf_apply_t_3d_dev(const ShufCtx& k, const double* u, double* v
     hgg[t] = sg;
     hdg[t] = sd;
   }
-  __syncthreads();
+  g.sync();
   const double* jd = S.jdet + size_t(k.e) * mu * mu * mu;
   for (int t = tid; t < mu * mu + 4 * mu; t += nt) {
     if (t < mu * mu) {
@@ -432,7 +448,7 @@ __device__ void shuf_apply_t_3d_dev(const ShufCtx& k, const double* u, double* v
       lbuf[tt] = s;
     }
   }
-  __syncthreads();
+  g.sync();
   for (int t = tid; t < mu * q * q; t += nt) {
     const int e2 = t % q, a2 = (t / q) % q, al = t / q2;
     double sx = 0.0, sy = 0.0, sg = 0.0;
@@ -446,7 +462,7 @@ __device__ void shuf_apply_t_3d_dev(const ShufCtx& k, const double* u, double* v
     p1y[t] = sy;
     p1g[t] = sg;
   }
-  __syncthreads();
+  g.sync();
   for (int t = tid; t < q2 * q2; t += nt) {
     const int a1 = t % q, a2 = (t / q) % q, e1 = (t / q2) % q, e2 = t / (q2 * q);
     double acc = 0.0;
@@ -475,7 +491,7 @@ __device__ void shuf_apply_t_3d_dev(const ShufCtx& k, const double* u, double* v
       }
     v[t] = acc;  // index ((e2*q + e1)*q2 + a2*q + a1)
   }
-  __syncthreads();
+  g.sync();
 #undef UU
 }
 

@@ -109,6 +109,7 @@ void launch_lanczos_form(const DevSys& s, const tpdg_gpu_ksvd_config& cfg, const
 size_t lanczos_work_doubles(const DevSys& s, int max_it);
 void launch_make_factors(int dim, int q, int n1, int nblk, const double* raw, double* rec, int* piv, int* kind,
                          double* work, cudaStream_t st);
+int make_factors_work_groups();
 size_t probe_work_doubles(const DevSys& s);
 int probe_grid(int n, int nfb);
 void launch_assemble_fallback(const DevSys& s, const int* blocks, int nfb, double* fb_lu, double* work,
