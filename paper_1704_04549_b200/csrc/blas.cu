@@ -302,6 +302,10 @@ __global__ void __launch_bounds__(kCoopThreads) mgs_coop_kernel(double* __restri
         s0 += a * wi;
       }
     }
+    // prefetch the next basis vector's slice into L2 while the grid waits at the barrier
+    if (j + 1 <= k)
+      for (int64_t i = 16 * int64_t(threadIdx.x); i < len; i += 16 * int64_t(blockDim.x))
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(V + int64_t(j + 1) * ldv + lo + i));
     const double bs = block_sum(s0 + s1, sh);
     if (threadIdx.x == 0) partial[size_t(j) * nb + blockIdx.x] = bs;
     coop_barrier(bar);
@@ -319,6 +323,82 @@ __global__ void __launch_bounds__(kCoopThreads) mgs_coop_kernel(double* __restri
   for (int64_t i = threadIdx.x; i < len; i += blockDim.x) wg[i] = h > 0.0 ? w[i] / h : w[i];
 }
 
+// MODE 3: w plus two basis-vector slices in shared memory; the slice of v_{j+1} is streamed with
+// cp.async (LDGSTS) right after pass j's arithmetic, so its HBM latency overlaps the grid barrier
+// and the reduction, and every pass computes from shared memory only. Each thread copies and later
+// reads exactly its own indices, so the only synchronization needed is its own cp.async.wait.
+__device__ __forceinline__ void cp16(double* smem, const double* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
+
+__global__ void __launch_bounds__(kCoopThreads) mgs_pipe_kernel(double* __restrict__ V, int64_t ldv, int k, int64_t n,
+                                                                 int64_t chunk, double* __restrict__ hc,
+                                                                 double* __restrict__ partial, unsigned* bar,
+                                                                 const int* skip) {
+  if (skip && *skip) return;
+  extern __shared__ double sm3[];
+  __shared__ double sh[32];
+  __shared__ double hval;
+  const unsigned nb = gridDim.x;
+  const int64_t lo = int64_t(blockIdx.x) * chunk;
+  const int64_t hi = lo + chunk < n ? lo + chunk : n;
+  const int64_t len = hi > lo ? hi - lo : 0;  // even except possibly for the last CTA
+  double* w = sm3;
+  double* buf[2] = {sm3 + chunk, sm3 + 2 * chunk};
+  double* wg = V + int64_t(k + 1) * ldv + lo;
+  auto issue = [&](double* dst, const double* src) {
+    for (int64_t i = 2 * threadIdx.x; i + 1 < len; i += 2 * blockDim.x) cp16(dst + i, src + i);
+    if ((len & 1) && threadIdx.x == 0) dst[len - 1] = src[len - 1];
+  };
+  issue(w, wg);
+  issue(buf[0], V + lo);  // v_0
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncthreads();
+  double h = 0.0;
+  for (int j = 0; j <= k + 1; ++j) {
+    const double* vp = j > 0 ? buf[(j - 1) & 1] : nullptr;
+    const double* vj = j <= k ? buf[j & 1] : nullptr;
+    double s0 = 0.0, s1 = 0.0;
+    for (int64_t i = 2 * threadIdx.x; i < len; i += 2 * blockDim.x) {
+      if (i + 1 < len) {
+        double2 wi = *reinterpret_cast<const double2*>(w + i);
+        if (vp) {
+          const double2 pv = *reinterpret_cast<const double2*>(vp + i);
+          wi.x = wi.x - h * pv.x;
+          wi.y = wi.y - h * pv.y;
+          *reinterpret_cast<double2*>(w + i) = wi;
+        }
+        const double2 a = vj ? *reinterpret_cast<const double2*>(vj + i) : wi;
+        s0 += a.x * wi.x;
+        s1 += a.y * wi.y;
+      } else {
+        double wi = w[i];
+        if (vp) {
+          wi = wi - h * vp[i];
+          w[i] = wi;
+        }
+        s0 += (vj ? vj[i] : wi) * wi;
+      }
+    }
+    if (j + 1 <= k) issue(buf[(j + 1) & 1], V + int64_t(j + 1) * ldv + lo);  // v_{j+1} over v_{j-1}
+    const double bs = block_sum(s0 + s1, sh);
+    if (threadIdx.x == 0) partial[size_t(j) * nb + blockIdx.x] = bs;
+    coop_barrier(bar);
+    double v = threadIdx.x < nb ? reinterpret_cast<volatile double*>(partial)[size_t(j) * nb + threadIdx.x] : 0.0;
+    for (unsigned b = threadIdx.x + blockDim.x; b < nb; b += blockDim.x)
+      v += reinterpret_cast<volatile double*>(partial)[size_t(j) * nb + b];
+    const double tot = block_sum(v, sh);
+    if (threadIdx.x == 0) hval = j <= k ? tot : sqrt(tot);
+    __syncthreads();
+    h = hval;
+    if (blockIdx.x == 0 && threadIdx.x == 0) hc[j] = h;
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    if (len & 1) __syncthreads();  // the scalar tail element is copied by thread 0 only
+  }
+  for (int64_t i = threadIdx.x; i < len; i += blockDim.x) wg[i] = h > 0.0 ? w[i] / h : w[i];
+}
+
 struct CoopPlan {
   int grid;
   int64_t chunk;
@@ -332,12 +412,17 @@ CoopPlan mgs_coop_plan(int64_t n) {
   TPDG_CUDA_CHECK(cudaGetDevice(&dev));
   TPDG_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   constexpr size_t kMax = 210 * 1024;
+  TPDG_CUDA_CHECK(cudaFuncSetAttribute(mgs_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kMax)));
   TPDG_CUDA_CHECK(cudaFuncSetAttribute(mgs_coop_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kMax)));
   TPDG_CUDA_CHECK(cudaFuncSetAttribute(mgs_coop_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kMax)));
   int64_t chunk = (n + sms - 1) / sms;
   chunk = (chunk + 1) & ~int64_t(1);
   const size_t one = size_t(chunk) * sizeof(double);
   int fit = 0;
+  if (3 * one <= kMax) {
+    TPDG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, mgs_pipe_kernel, kCoopThreads, 3 * one));
+    if (fit >= 1) return {sms, chunk, 3 * one, 3};
+  }
   if (2 * one <= kMax) {
     TPDG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, mgs_coop_kernel<2>, kCoopThreads, 2 * one));
     if (fit >= 1) return {sms, chunk, 2 * one, 2};
@@ -407,7 +492,8 @@ void launch_mgs_iteration(double* V, int64_t ldv, int k, int64_t n, double* hc, 
   }
   int64_t chunk = plan.chunk;
   void* args[] = {&V, &ldv, &k, &n, &chunk, &hc, &partial, &bar, &skip};
-  void* fn = plan.mode == 2   ? reinterpret_cast<void*>(mgs_coop_kernel<2>)
+  void* fn = plan.mode == 3   ? reinterpret_cast<void*>(mgs_pipe_kernel)
+             : plan.mode == 2 ? reinterpret_cast<void*>(mgs_coop_kernel<2>)
              : plan.mode == 1 ? reinterpret_cast<void*>(mgs_coop_kernel<1>)
                               : reinterpret_cast<void*>(mgs_coop_kernel<0>);
   TPDG_CUDA_CHECK(cudaLaunchCooperativeKernel(fn, dim3(plan.grid), dim3(kCoopThreads), args, plan.smem, st));

@@ -425,7 +425,7 @@ struct Kron2dWarpLayout {
   static constexpr int ld = (N2 + 1) & ~1;
   static constexpr int rec = 3 * N1 * N1 + 3 * N2 * N2;
   static constexpr int ints = (N1 + N2) + 2 * N1 + 2 * N2 + 4;
-  static constexpr int per = 2 * N1 * ld + rec + ((ints + 1) / 2) + 2;
+  static constexpr int per = N1 * ld + rec + (N1 + N2) + ((ints + 1) / 2) + 2;
   static constexpr int per_even = (per + 1) & ~1;
 };
 
@@ -439,9 +439,10 @@ __global__ void __launch_bounds__(kSizedThreads) kron2d_sized_kernel(DevPC pc, c
   const int blk = blockIdx.x * (kSizedThreads / 32) + warp;
   if (blk >= pc.nblk || pc.kind[blk] == 0 || (pc.skip && *pc.skip)) return;
   double* sX = sm_all + size_t(warp) * L::per_even;
-  double* sT = sX + N1 * ld;
-  double* sR = sT + N1 * ld;
-  double* sTol = sR + rec;
+  double* sR = sX + N1 * ld;
+  double* sT = sR;  // product scratch: aliases LU(A2), LU(B1) once both fiber solves are done
+  double* sRow = sR + rec;
+  double* sTol = sRow + (N1 + N2);
   int* sPiv = reinterpret_cast<int*>(sTol + 2);
   int* sb = sPiv + N1 + N2;  // s1[N1] z1[N1] s2[N2] z2[N2] nb1 nb2 all11
   {  // asynchronous global -> shared copies (LDGSTS), one round trip for the whole record
@@ -472,13 +473,13 @@ __global__ void __launch_bounds__(kSizedThreads) kron2d_sized_kernel(DevPC pc, c
     const int n = i < N1 ? N1 : N2;
     double s = 0.0;
     for (int j = 0; j < n; ++j) s = fadd(s, fabs(row[j]));
-    sT[i] = s;
+    sRow[i] = s;
   }
   __syncwarp();
   if (lane == 0) {
     double m1 = 0.0, m2 = 0.0;
-    for (int i = 0; i < N1; ++i) m1 = fmax(m1, sT[i]);
-    for (int i = 0; i < N2; ++i) m2 = fmax(m2, sT[N1 + i]);
+    for (int i = 0; i < N1; ++i) m1 = fmax(m1, sRow[i]);
+    for (int i = 0; i < N2; ++i) m2 = fmax(m2, sRow[N1 + i]);
     sTol[0] = fmul(1e-14, fmax(fadd(m1, m2), 1e-300));
     const int nb1 = quasi_blocks_dev(T1, N1, sb, sb + N1);
     const int nb2 = quasi_blocks_dev(T2, N2, sb + 2 * N1, sb + 2 * N1 + N2);
@@ -494,7 +495,7 @@ __global__ void __launch_bounds__(kSizedThreads) kron2d_sized_kernel(DevPC pc, c
   __syncwarp();
   warp_mm<N1, N2, N2, false, false, 2, 4>(sT, ld, Q2, N2, sX, ld, lane);  // (.) Q2 -> M
   __syncwarp();
-  {  // Y (into sT): T1 Y + Y T2^T = M, block anti-diagonal wavefront
+  {  // Y overwrites M in place (sX): T1 Y + Y T2^T = M, block anti-diagonal wavefront
     const int nb1 = sb[2 * N1 + 2 * N2], nb2 = sb[2 * N1 + 2 * N2 + 1];
     const bool all11 = sb[2 * N1 + 2 * N2 + 2] != 0;
     const int *s1 = sb, *z1 = sb + N1, *s2 = sb + 2 * N1, *z2 = sb + 2 * N1 + N2;
@@ -505,10 +506,10 @@ __global__ void __launch_bounds__(kSizedThreads) kron2d_sized_kernel(DevPC pc, c
       if (all11) {  // 1 x 1 blocks: one lane per cell; solve_tiny<1> is y = r / (t1_ii + t2_kk)
         for (int d1 = d1lo + lane; d1 <= d1hi; d1 += 32) {
           const int i = nb1 - 1 - d1, k = nb2 - 1 - (step - d1);
-          const double s = sylv_rhs(T1, N1, T2, N2, sX, sT, ld, i, k, i + 1, k + 1);
+          const double s = sylv_rhs(T1, N1, T2, N2, sX, sX, ld, i, k, i + 1, k + 1);
           const double coef = fadd(fadd(0.0, T1[i * N1 + i]), T2[k * N2 + k]);
           if (fabs(coef) < tol) atomicExch(pc.status, int(TPDG_SINGULAR));
-          sT[i * ld + k] = fdiv(s, coef);
+          sX[i * ld + k] = fdiv(s, coef);
         }
       } else {  // 4 lanes per cell (one per entry), tiny solve replicated in the group
         for (int base = d1lo; base <= d1hi; base += 8) {
@@ -523,7 +524,7 @@ __global__ void __launch_bounds__(kSizedThreads) kron2d_sized_kernel(DevPC pc, c
             k0 = s2[bj];
             ksz = z2[bj];
             if (e < isz * ksz)
-              s = sylv_rhs(T1, N1, T2, N2, sX, sT, ld, i0 + e / ksz, k0 + e % ksz, i0 + isz, k0 + ksz);
+              s = sylv_rhs(T1, N1, T2, N2, sX, sX, ld, i0 + e / ksz, k0 + e % ksz, i0 + isz, k0 + ksz);
           }
           double rg[4];
           const int g = lane & ~3;
@@ -536,16 +537,16 @@ __global__ void __launch_bounds__(kSizedThreads) kron2d_sized_kernel(DevPC pc, c
             else if (code == 1) y = sylv_solve_group<1, 2>(T1, N1, T2, N2, i0, k0, rg, e, tol, pc.status);
             else if (code == 2) y = sylv_solve_group<2, 1>(T1, N1, T2, N2, i0, k0, rg, e, tol, pc.status);
             else y = sylv_solve_group<2, 2>(T1, N1, T2, N2, i0, k0, rg, e, tol, pc.status);
-            sT[(i0 + e / ksz) * ld + k0 + e % ksz] = y;
+            sX[(i0 + e / ksz) * ld + k0 + e % ksz] = y;
           }
         }
       }
       __syncwarp();
     }
   }
-  warp_mm<N1, N1, N2, false, false, 2, 4>(Q1, N1, sT, ld, sX, ld, lane);  // Q1 Y
+  warp_mm<N1, N1, N2, false, false, 2, 4>(Q1, N1, sX, ld, sT, ld, lane);  // Q1 Y
   __syncwarp();
-  warp_mm<N1, N2, N2, false, true, 2, 4>(sX, ld, Q2, N2, out + size_t(blk) * (N1 * N2), N2, lane);  // (.) Q2^T
+  warp_mm<N1, N2, N2, false, true, 2, 4>(sT, ld, Q2, N2, out + size_t(blk) * (N1 * N2), N2, lane);  // (.) Q2^T
 }
 
 template <int N1, int N2>
