@@ -33,10 +33,26 @@ REF_BENCH = os.path.join(ROOT, "oracle", "_ref", "tpdg_ref_bench")
 GOLDEN_ITS = {4: 17, 8: 18, 15: 25, 20: 39, 30: 21}  # reference GMRES counts, tests/golden/cfg2_p*.npz
 
 
-def workload(p):
+def workload(p, case="cfg2"):
+    if case == "cfg4":
+        return ("cfg4: 3D advection, velocity (1, 0.7, 0.4), periodic unit cube, 16x16x16 hexes, Gauss-Lobatto "
+                "p=10, backward Euler dt=0.01, A = M - dt J, right 3D KSVD (rank-1 x rank-2) preconditioner, "
+                "GMRES(30) rel tol 1e-10, RHS uniform[-1,1] mt19937_64(12345), fp64")
+    if case == "cfg1":
+        return ("cfg1: 2D advection, velocity (1, 0.5), periodic unit square, 8x8 quads, Gauss-Lobatto p=8, "
+                "backward Euler dt=0.01, right KSVD r=2, GMRES(30) rel tol 1e-10, RHS uniform[-1,1], fp64")
     return (f"cfg2: 2D advection, velocity (sin 2pi y, cos 2pi x), periodic unit square, 64x64 quads, "
             f"Gauss-Lobatto p={p}, backward Euler dt=0.005, A = M - dt J, right KSVD r=2 preconditioner, "
             f"GMRES(30) rel tol 1e-10, RHS uniform[-1,1] mt19937_64(12345), fp64")
+
+
+def build_case(T, case, p):
+    """(system, dt, golden case name, golden iteration count) of a BASELINE configuration."""
+    if case == "cfg4":
+        return T.setup_advection("const3d", 16, 16, 16, p=10, vel=(1.0, 0.7, 0.4)), 0.01, "cfg4", 159
+    if case == "cfg1":
+        return T.setup_advection("const2d", 8, 8, p=8, vel=(1.0, 0.5, 0.0)), 0.01, "cfg1", 11
+    return T.setup_advection("swirl2d", 64, 64, p=p), 0.005, f"cfg2_p{p}", GOLDEN_ITS.get(p)
 
 
 def peaks():
@@ -125,7 +141,8 @@ def main_reference(args, rank):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/tpdg_ref_bench not built"}))
         return 0
     th = cpu_threads()
-    r = run_reference_bench(f"cfg2_p{args.p}", th, 2000, args.warmup + args.steps)
+    ref_case = {"cfg4": "cfg4", "cfg1": "cfg1"}.get(args.case, f"cfg2_p{args.p}")
+    r = run_reference_bench(ref_case, th, 2000, args.warmup + args.steps)
     times = r["gmres_s"][args.warmup:]
     t = statistics.median(times)
     N, its = r["N"], r["gmres_its"]
@@ -134,7 +151,7 @@ def main_reference(args, rank):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GDOF-it/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload(args.p), "N": N, "iterations": its, "p": args.p},
+        "config": {"workload": workload(args.p, args.case), "N": N, "iterations": its, "p": args.p},
         "cpu_baseline": {"value": value, "unit": "GDOF-it/s", "cores": th, "kind": "reference",
                          "sample": f"{args.steps} full GMRES solves ({its} iterations each) after {args.warmup} "
                                    f"warm-up solves; unmodified reference, g++ -O3 -march=x86-64-v3, "
@@ -166,8 +183,7 @@ def main_ours(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     ctx = T.Context(local_rank, rank, world, nccl_id)
     p = args.p
-    sysm = T.setup_advection("swirl2d", 64, 64, p=p)
-    dt = 0.005
+    sysm, dt, ref_case, ref_its = build_case(T, args.case, p)
     op = T.LinearizedOperator(ctx, sysm, dt)
     N = sysm.N
     e0, e1 = op.e_begin, op.e_end
@@ -252,8 +268,12 @@ def main_ours(args, rank, world, local_rank):
     q, mu, nc, d = sysm.q, sysm.mu, sysm.n_c, sysm.dim
     n_loc = e1 - e0
     n1 = nc * q
-    bytes_pc = n_loc * 8.0 * (2 * n1 * q + 3 * n1 * n1 + 3 * q * q)
-    flops_pc = n_loc * 7.0 * n1 * q * (n1 + q)
+    if d == 2:
+        bytes_pc = n_loc * 8.0 * (2 * n1 * q + 3 * n1 * n1 + 3 * q * q)
+        flops_pc = n_loc * 7.0 * n1 * q * (n1 + q)
+    else:  # B = 8 (2 n1 q^2 + n1^2 + 6 q^2), F = 2 n1^2 q^2 + 14 n1 q^3
+        bytes_pc = n_loc * 8.0 * (2 * n1 * q * q + n1 * n1 + 6 * q * q)
+        flops_pc = n_loc * (2.0 * n1 * n1 * q * q + 14.0 * n1 * q ** 3)
     bytes_jv = n_loc * 8.0 * (2 * nc * q ** d + mu ** d * (1 + d * nc * nc) + 4 * d * mu ** (d - 1) * nc * nc)
     n_local = n_loc * nc * npe
     # MGS region of iteration k (0-based in its cycle): 8 (5 (k+1) + 3) bytes per DOF
@@ -283,7 +303,8 @@ def main_ours(args, rank, world, local_rank):
     if dom:
         ach = kern[dom]["achieved_gbs"]
         roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm, "unit": "GB/s",
-                "frac": ach / hbm, "peak_kind": hbm_kind, "traffic": traffic.get(dom) if p == 15 else None,
+                "frac": ach / hbm, "peak_kind": hbm_kind,
+                "traffic": traffic.get(dom) if (p == 15 and args.case == "cfg2") else None,
                 "algorithmic_bytes_per_launch": kern[dom]["algorithmic_bytes"]}
     kron = None
     if "pc_apply" in kern:
@@ -297,7 +318,7 @@ def main_ours(args, rank, world, local_rank):
     if rank == 0 and world == 1 and not args.no_cpu_baseline and os.path.exists(REF_BENCH):
         th = cpu_threads()
         try:
-            r = run_reference_bench(f"cfg2_p{p}", th, 2000, 1, timeout=900)
+            r = run_reference_bench(ref_case, th, 2000, 1, timeout=900)
             v = r["N"] * r["gmres_its"] / r["gmres_s"][-1] / 1e9
             cpu = {"value": v, "unit": "GDOF-it/s", "cores": th, "kind": "reference",
                    "sample": f"one full GMRES solve ({r['gmres_its']} iterations) of the same workload, unmodified "
@@ -312,8 +333,9 @@ def main_ours(args, rank, world, local_rank):
             "metric": METRIC, "value": value, "unit": "GDOF-it/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload(p), "N": N, "iterations_per_solve": its_list[0] if its_list else None,
-                       "reference_iterations": GOLDEN_ITS.get(p), "fallbacks": nfb, "p": p,
+            "config": {"workload": workload(p, args.case), "N": N,
+                       "iterations_per_solve": its_list[0] if its_list else None,
+                       "reference_iterations": ref_its, "fallbacks": nfb, "p": p if args.case == "cfg2" else None,
                        "parallelism": f"element rows x{world}",
                        "l2": "inputs larger than L2 (Krylov basis 31 x N x 8 B + factors + operator data > 126 MB)"},
             "roofline": roof, "kron_apply": kron, "kernels": kern, "cpu_baseline": cpu,
@@ -334,7 +356,9 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--p", type=int, default=15, choices=[4, 8, 15, 20, 30])
+    ap.add_argument("--p", type=int, default=15, choices=[4, 8, 15, 20, 30], help="cfg2 polynomial degree")
+    ap.add_argument("--case", default="cfg2", choices=["cfg2", "cfg1", "cfg4"],
+                    help="BASELINE config (headline: cfg2 = configs[1]; others for measurement)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true", help="diagnostic: do not sample nvidia-smi")
     ap.add_argument("--no-profile", action="store_true", help="diagnostic: no per-kernel events")

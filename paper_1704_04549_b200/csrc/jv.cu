@@ -583,6 +583,288 @@ __global__ void __launch_bounds__(256) jv3d_kernel(DevSys s, const double* __res
   }
 }
 
+// ------------------------------------------------------------------------------------ 3D, sized
+// Scalar 3D operator with compile-time (Q, MU), one CTA per element (persistent). Every stage is a
+// set of independent 1D "pencil" contractions: a thread owns one pencil, keeps its accumulators in
+// registers and reads the (broadcast) 1D weights from shared memory. The point-wise fields are
+// formed inside the x-direction integration (never stored), and dead buffers are aliased, so an
+// element needs ~11 K doubles of shared memory (cfg4) instead of ~24 K.
+template <int Q, int MU>
+struct Jv3dLayout {
+  static constexpr int Q2 = Q * Q, Q3 = Q * Q * Q, M2 = MU * MU, M3 = MU * MU * MU;
+  static constexpr int SLAB = (MU + 1) / 2;  // quadrature z-slabs per integration round
+  static constexpr int w_G = 0, w_GW = MU * Q, w_DW = 2 * MU * Q, weights = 3 * MU * Q;
+  // A: t1 + t2 (eval) | X for one slab group (3 SLAB MU Q)
+  static constexpr int a_size = (Q2 * MU + Q * M2) > 3 * SLAB * MU * Q ? (Q2 * MU + Q * M2) : 3 * SLAB * MU * Q;
+  // C: v (Q3) | traces str (12 M2) | Ya, Yc (2 MU Q2)
+  static constexpr int c_a = Q3 > 12 * M2 ? Q3 : 12 * M2;
+  static constexpr int c_size = c_a > 2 * MU * Q2 ? c_a : 2 * MU * Q2;
+  static constexpr int val_size = M3 > 12 * Q * MU ? M3 : 12 * Q * MU;  // vals | trace stage 1
+  static constexpr int r_a = weights, r_val = r_a + a_size, r_c = r_val + val_size, r_d = r_c + c_size;
+  static constexpr int total = r_d + 6 * Q * MU + 6 * M2;  // D: lift stage wa (6 Q MU), face data sg (6 M2)
+};
+
+template <int Q, int MU>
+__global__ void __launch_bounds__(256) jv3d_sized_kernel(DevSys s, const double* __restrict__ vin,
+                                                          const double* __restrict__ halo, double* __restrict__ vout) {
+  if (s.skip && *s.skip) return;
+  using L = Jv3dLayout<Q, MU>;
+  constexpr int Q2 = L::Q2, Q3 = L::Q3, M2 = L::M2, M3 = L::M3, SLAB = L::SLAB;
+  constexpr int QH = (Q + 1) / 2;  // output halves per pencil in the integration stages
+  extern __shared__ double sm[];
+  double* G = sm + L::w_G;    // [a][j]
+  double* GW = sm + L::w_GW;  // [j][a]
+  double* DW = sm + L::w_DW;  // [j][a]
+  double* t1 = sm + L::r_a;
+  double* t2 = t1 + Q2 * MU;
+  double* X = sm + L::r_a;
+  double* val = sm + L::r_val;
+  double* v = sm + L::r_c;
+  double* str = sm + L::r_c;
+  double* Ya = sm + L::r_c;
+  double* Yc = Ya + MU * Q2;
+  double* wa = sm + L::r_d;       // lift stage [f][j0][b]
+  double* sg = wa + 6 * Q * MU;   // face data [f][b][a]
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int i = tid; i < MU * Q; i += nt) {
+    G[i] = s.g[i];
+    GW[i] = s.gw[i];
+    DW[i] = s.dw[i];
+  }
+  for (int e = blockIdx.x; e < s.n_local; e += gridDim.x) {
+    __syncthreads();
+    const double* ve = vin + size_t(e) * Q3;
+    for (int i = tid; i < Q3; i += nt) v[i] = ve[i];
+    __syncthreads();
+    // ---- eval_at_quad, x pencils (k,j) -> t1[k][j][al]; trace stage 1 into val (free until z-eval)
+    double* tw = val;  // [side][f][j1][a], 12 Q MU <= M3
+    for (int p = tid; p < Q2 + 12 * Q; p += nt) {
+      double acc[MU];
+#pragma unroll
+      for (int a = 0; a < MU; ++a) acc[a] = 0.0;
+      if (p < Q2) {
+        const double* row = v + p * Q;
+#pragma unroll
+        for (int i = 0; i < Q; ++i) {
+          const double x = row[i];
+#pragma unroll
+          for (int a = 0; a < MU; ++a) acc[a] = fma(G[a * Q + i], x, acc[a]);
+        }
+#pragma unroll
+        for (int a = 0; a < MU; ++a) t1[p * MU + a] = acc[a];
+      } else {
+        const int idx = p - Q2, j1 = idx % Q, f = (idx / Q) % 6, side = idx / (6 * Q);
+        const double* cf = v;
+        int ff = f;
+        bool ok = true;
+        if (side == 1) {
+          const int* fc = s.conn + (size_t(e) * 6 + f) * 3;
+          ok = fc[0] >= 0;
+          if (ok) {
+            cf = nbr_block(s, vin, halo, fc[0]);
+            ff = fc[1];
+          }
+        }
+        if (ok)
+          for (int j0 = 0; j0 < Q; ++j0) {
+            const double x = cf[flat_face_node(Q, ff, j0, j1)];
+#pragma unroll
+            for (int a = 0; a < MU; ++a) acc[a] = fma(G[a * Q + j0], x, acc[a]);
+          }
+#pragma unroll
+        for (int a = 0; a < MU; ++a) tw[(idx / Q) * Q * MU + j1 * MU + a] = acc[a];
+      }
+    }
+    __syncthreads();
+    // y pencils (k, al) -> t2[k][be][al]; trace stage 2 -> str[side][f][b][a] (over v, now dead)
+    for (int p = tid; p < Q * MU + 12 * MU; p += nt) {
+      double acc[MU];
+#pragma unroll
+      for (int b = 0; b < MU; ++b) acc[b] = 0.0;
+      if (p < Q * MU) {
+        const int k = p / MU, al = p % MU;
+#pragma unroll
+        for (int j = 0; j < Q; ++j) {
+          const double x = t1[(k * Q + j) * MU + al];
+#pragma unroll
+          for (int b = 0; b < MU; ++b) acc[b] = fma(G[b * Q + j], x, acc[b]);
+        }
+#pragma unroll
+        for (int b = 0; b < MU; ++b) t2[(k * MU + b) * MU + al] = acc[b];
+      } else {
+        const int idx = p - Q * MU, a = idx % MU, sf = idx / MU;
+        for (int j1 = 0; j1 < Q; ++j1) {
+          const double x = tw[sf * Q * MU + j1 * MU + a];
+#pragma unroll
+          for (int b = 0; b < MU; ++b) acc[b] = fma(G[b * Q + j1], x, acc[b]);
+        }
+#pragma unroll
+        for (int b = 0; b < MU; ++b) str[sf * M2 + b * MU + a] = acc[b];
+      }
+    }
+    __syncthreads();
+    // z pencils (be, al) -> vals[ga][be][al]; face data g[f][qf] (neighbour trace oriented)
+    for (int p = tid; p < M2 + 6 * M2; p += nt) {
+      if (p < M2) {
+        double acc[MU];
+#pragma unroll
+        for (int g = 0; g < MU; ++g) acc[g] = 0.0;
+#pragma unroll
+        for (int k = 0; k < Q; ++k) {
+          const double x = t2[k * M2 + p];
+#pragma unroll
+          for (int g = 0; g < MU; ++g) acc[g] = fma(G[g * Q + k], x, acc[g]);
+        }
+#pragma unroll
+        for (int g = 0; g < MU; ++g) val[g * M2 + p] = acc[g];
+      } else {
+        const int idx = p - M2, qf = idx % M2, f = idx / M2;
+        const int* fc = s.conn + (size_t(e) * 6 + f) * 3;
+        const size_t fq = (size_t(e) * 6 + f) * M2 + qf;
+        const int qa = qf % MU, qb = qf / MU, code = fc[2];
+        int u = (code & 4) ? qb : qa, w = (code & 4) ? qa : qb;
+        if (code & 1) u = MU - 1 - u;
+        if (code & 2) w = MU - 1 - w;
+        const double tm = str[f * M2 + qf], tp = str[(6 + f) * M2 + w * MU + u];
+        sg[idx] = -s.b * s.face_w[fq] * fma(s.dfm[fq], tm, s.dfp[fq] * tp);
+      }
+    }
+    __syncthreads();
+    // lift stage 1: wa[f][j0][b] = sum_a G(a, j0) g[f][b][a]
+    for (int idx = tid; idx < 6 * MU; idx += nt) {
+      const int b = idx % MU, f = idx / MU;
+      double acc[Q];
+#pragma unroll
+      for (int j = 0; j < Q; ++j) acc[j] = 0.0;
+      for (int a = 0; a < MU; ++a) {
+        const double x = sg[f * M2 + b * MU + a];
+#pragma unroll
+        for (int j = 0; j < Q; ++j) acc[j] = fma(G[a * Q + j], x, acc[j]);
+      }
+#pragma unroll
+      for (int j = 0; j < Q; ++j) wa[(f * Q + j) * MU + b] = acc[j];
+    }
+    // ---- integration in rounds of SLAB quadrature z-slabs: fields + x (into X), then y (into Ya, Yc)
+    const double* jd = s.jdet + size_t(e) * M3;
+    const double* d0 = s.dft + size_t(e) * 3 * M3;
+    const double* d1 = d0 + M3;
+    const double* d2 = d1 + M3;
+    for (int g0 = 0; g0 < MU; g0 += SLAB) {
+      const int ng = MU - g0 < SLAB ? MU - g0 : SLAB;
+      for (int p = tid; p < ng * MU * 2; p += nt) {  // pencil (ga, be), half h of the outputs i
+        const int hh = p % 2, pb = p / 2, ga = g0 + pb / MU, be = pb % MU;
+        const int i0 = hh * QH, ni = hh == 0 ? QH : Q - QH;
+        double xa[QH], xb[QH], xc[QH];
+#pragma unroll
+        for (int i = 0; i < QH; ++i) xa[i] = xb[i] = xc[i] = 0.0;
+        for (int al = 0; al < MU; ++al) {
+          const int qv = (ga * MU + be) * MU + al;
+          const double x = val[qv];
+          const double fm = s.a * jd[qv] * x, f0 = s.b * (d0[qv] * x), f1 = s.b * (d1[qv] * x),
+                       f2 = s.b * (d2[qv] * x);
+#pragma unroll
+          for (int i = 0; i < QH; ++i) {
+            if (i < ni) {
+              const double gw = GW[(i0 + i) * MU + al];
+              xa[i] = fma(gw, fm, fma(DW[(i0 + i) * MU + al], f0, xa[i]));
+              xb[i] = fma(gw, f1, xb[i]);
+              xc[i] = fma(gw, f2, xc[i]);
+            }
+          }
+        }
+        const int row = (pb)*Q + i0;  // X[(ga-g0)][be][i]
+#pragma unroll
+        for (int i = 0; i < QH; ++i)
+          if (i < ni) {
+            X[row + i] = xa[i];
+            X[SLAB * MU * Q + row + i] = xb[i];
+            X[2 * SLAB * MU * Q + row + i] = xc[i];
+          }
+      }
+      __syncthreads();
+      for (int p = tid; p < ng * Q * 2; p += nt) {  // pencil (ga, i), half of the outputs j
+        const int hh = p % 2, pb = p / 2, gl = pb / Q, i = pb % Q, ga = g0 + gl;
+        const int j0 = hh * QH, nj = hh == 0 ? QH : Q - QH;
+        double ya[QH], yc[QH];
+#pragma unroll
+        for (int j = 0; j < QH; ++j) ya[j] = yc[j] = 0.0;
+        for (int be = 0; be < MU; ++be) {
+          const int src = (gl * MU + be) * Q + i;
+          const double xa = X[src], xb = X[SLAB * MU * Q + src], xc = X[2 * SLAB * MU * Q + src];
+#pragma unroll
+          for (int j = 0; j < QH; ++j)
+            if (j < nj) {
+              ya[j] = fma(GW[(j0 + j) * MU + be], xa, fma(DW[(j0 + j) * MU + be], xb, ya[j]));
+              yc[j] = fma(GW[(j0 + j) * MU + be], xc, yc[j]);
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < QH; ++j)
+          if (j < nj) {
+            Ya[(ga * Q + j0 + j) * Q + i] = ya[j];
+            Yc[(ga * Q + j0 + j) * Q + i] = yc[j];
+          }
+      }
+      __syncthreads();
+    }
+    // z integration, pencils (j, i) + face lifts, straight to HBM
+    double* oe = vout + size_t(e) * Q3;
+    for (int p = tid; p < Q2; p += nt) {
+      double acc[Q];
+#pragma unroll
+      for (int k = 0; k < Q; ++k) acc[k] = 0.0;
+      for (int ga = 0; ga < MU; ++ga) {
+        const double ya = Ya[ga * Q2 + p], yc = Yc[ga * Q2 + p];
+#pragma unroll
+        for (int k = 0; k < Q; ++k) acc[k] = fma(GW[k * MU + ga], ya, fma(DW[k * MU + ga], yc, acc[k]));
+      }
+      const int i = p % Q, j = p / Q;
+#pragma unroll
+      for (int k = 0; k < Q; ++k) {
+        double r = acc[k];
+        const int pos[3] = {i, j, k};
+#pragma unroll
+        for (int axis = 0; axis < 3; ++axis) {
+          const int pp = pos[axis];
+          if (pp != 0 && pp != Q - 1) continue;
+          const int f = 2 * axis + (pp == 0 ? 0 : 1);
+          const int j0 = pos[axis == 0 ? 1 : 0], j1 = pos[axis == 2 ? 1 : 2];
+          const double* lf = wa + (f * Q + j0) * MU;
+          double s2 = 0.0;
+          for (int bb = 0; bb < MU; ++bb) s2 = fma(G[bb * Q + j1], lf[bb], s2);
+          r += s2;
+        }
+        oe[k * Q2 + p] = r;
+      }
+    }
+  }
+}
+
+template <int Q, int MU>
+bool try_jv3d_sized(const DevSys& s, const double* vin, const double* halo, double* vout, cudaStream_t st) {
+  if (s.dim != 3 || s.n_c != 1 || s.q != Q || s.mu != MU) return false;
+  const size_t smem = sizeof(double) * size_t(Jv3dLayout<Q, MU>::total);
+  static int grid = 0;
+  if (!grid) {
+    TPDG_CUDA_CHECK(cudaFuncSetAttribute(jv3d_sized_kernel<Q, MU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(smem)));
+    TPDG_CUDA_CHECK(cudaFuncSetAttribute(jv3d_sized_kernel<Q, MU>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                         100));
+    int per_sm = 0, dev = 0, sms = 0;
+    TPDG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jv3d_sized_kernel<Q, MU>, 256, smem));
+    TPDG_CUDA_CHECK(cudaGetDevice(&dev));
+    TPDG_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    grid = std::max(1, per_sm) * sms;
+  }
+  jv3d_sized_kernel<Q, MU><<<std::min(grid, s.n_local), 256, smem, st>>>(s, vin, halo, vout);
+  return true;
+}
+
+bool launch_jv3d_sized(const DevSys& s, const double* vin, const double* halo, double* vout, cudaStream_t st) {
+  return try_jv3d_sized<4, 5>(s, vin, halo, vout, st) || try_jv3d_sized<5, 6>(s, vin, halo, vout, st) ||
+         try_jv3d_sized<8, 9>(s, vin, halo, vout, st) || try_jv3d_sized<11, 12>(s, vin, halo, vout, st);
+}
+
 size_t jv3d_smem(const DevSys& s) {
   const size_t q = s.q, mu = s.mu, nc = s.n_c;
   const size_t q3 = q * q * q, m3 = mu * mu * mu, m2 = mu * mu, q2 = q * q;
@@ -599,6 +881,11 @@ void launch_jv(const DevSys& s, const double* vin, const double* halo, double* v
   if (s.n_local == 0) return;
   const size_t smem = jv_smem_bytes(s);
   if (s.dim == 2 && launch_jv2d_sized(s, vin, halo, vout, st)) {
+    TPDG_CUDA_CHECK(cudaGetLastError());
+    ++g_launches;
+    return;
+  }
+  if (s.dim == 3 && launch_jv3d_sized(s, vin, halo, vout, st)) {
     TPDG_CUDA_CHECK(cudaGetLastError());
     ++g_launches;
     return;

@@ -577,6 +577,215 @@ bool launch_kron2d_sized(const DevPC& pc, const double* in, double* out, cudaStr
          try_kron2d_sized<31, 31>(pc, in, out, st);
 }
 
+// ------------------------------------------------------------------------------------ 3D, sized
+// apply_factors_3d (precond/ksvd.hpp:132-153) with compile-time (N1 outer, Q): one 128-thread CTA
+// per block. Three LU axis solves with register-resident fibers, then the N1 outer slices share
+// one Sylvester plan: the wavefront runs all slices at once (4 lanes per cell and slice, tiny
+// solve replicated in the group), and the rotations are tiled CTA products over all slices.
+constexpr int k3Threads = 128;
+
+template <int R, int K, int C, bool AT, bool BT, int TI, int TJ>
+__device__ __forceinline__ void cta_mm_slices(const double* A, int lda, int a_slice, const double* B, int ldb,
+                                              int b_slice, double* O, int ldo, int o_slice, int nslices) {
+  constexpr int NTI = (R + TI - 1) / TI, NTJ = (C + TJ - 1) / TJ, PER = NTI * NTJ;
+  for (int t = threadIdx.x; t < PER * nslices; t += k3Threads) {
+    const int sl = t / PER, tt = t % PER, i0 = (tt / NTJ) * TI, j0 = (tt % NTJ) * TJ;
+    const double* As = A + sl * a_slice;
+    const double* Bs = B + sl * b_slice;
+    double acc[TI][TJ];
+#pragma unroll
+    for (int ii = 0; ii < TI; ++ii)
+#pragma unroll
+      for (int jj = 0; jj < TJ; ++jj) acc[ii][jj] = 0.0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      double a[TI], b[TJ];
+#pragma unroll
+      for (int ii = 0; ii < TI; ++ii) {
+        const int i = i0 + ii < R ? i0 + ii : R - 1;
+        a[ii] = AT ? As[k * lda + i] : As[i * lda + k];
+      }
+#pragma unroll
+      for (int jj = 0; jj < TJ; ++jj) {
+        const int j = j0 + jj < C ? j0 + jj : C - 1;
+        b[jj] = BT ? Bs[j * ldb + k] : Bs[k * ldb + j];
+      }
+#pragma unroll
+      for (int ii = 0; ii < TI; ++ii)
+#pragma unroll
+        for (int jj = 0; jj < TJ; ++jj) acc[ii][jj] = fmac(acc[ii][jj], a[ii], b[jj]);
+    }
+    double* Os = O + sl * o_slice;
+#pragma unroll
+    for (int ii = 0; ii < TI; ++ii)
+#pragma unroll
+      for (int jj = 0; jj < TJ; ++jj)
+        if (i0 + ii < R && j0 + jj < C) Os[(i0 + ii) * ldo + j0 + jj] = acc[ii][jj];
+  }
+}
+
+template <int N1, int Q>
+struct Kron3dLayout {
+  static constexpr int ld = Q | 1, ss = Q * ld;  // row stride, slice stride (odd: conflict-free fibers)
+  static constexpr int rec = N1 * N1 + 6 * Q * Q;
+  static constexpr int total = 2 * N1 * ss + rec + 2 * Q + ((N1 + 2 * Q + 4 * Q + 4) + 1) / 2 + 4;
+};
+
+template <int N1, int Q>
+__global__ void __launch_bounds__(k3Threads) kron3d_sized_kernel(DevPC pc, const double* __restrict__ in,
+                                                                  double* __restrict__ out) {
+  const int blk = blockIdx.x;
+  if (pc.kind[blk] == 0 || (pc.skip && *pc.skip)) return;
+  using L = Kron3dLayout<N1, Q>;
+  constexpr int ld = L::ld, ss = L::ss, rec = L::rec;
+  extern __shared__ double sm[];
+  double* sX = sm;
+  double* sT = sX + N1 * ss;
+  double* sR = sT + N1 * ss;
+  double* sRow = sR + rec;
+  double* sTol = sRow + 2 * Q;
+  int* sPiv = reinterpret_cast<int*>(sTol + 2);
+  int* sb = sPiv + N1 + 2 * Q;  // s1 z1 s2 z2 (Q each) nb1 nb2 all11
+  const int tid = threadIdx.x;
+  {
+    const double* r = pc.rec + size_t(blk) * rec;
+    if ((reinterpret_cast<uintptr_t>(r) & 15) == 0 && (reinterpret_cast<uintptr_t>(sR) & 15) == 0) {
+      for (int i = 2 * tid; i + 1 < rec; i += 2 * k3Threads) cp_async16(sR + i, r + i);
+      if ((rec & 1) && tid == 0) sR[rec - 1] = r[rec - 1];
+    } else {
+      for (int i = tid; i < rec; i += k3Threads) cp_async8(sR + i, r + i);
+    }
+    for (int i = tid; i < N1 + 2 * Q; i += k3Threads) sPiv[i] = pc.piv[size_t(blk) * (N1 + 2 * Q) + i];
+    const double* x = in + size_t(blk) * (N1 * Q * Q);
+    for (int i = tid; i < N1 * Q * Q; i += k3Threads) {
+      const int j = i % Q, rr = (i / Q) % Q, sl = i / (Q * Q);
+      cp_async8(sX + sl * ss + rr * ld + j, x + i);
+    }
+    cp_async_wait_all();
+  }
+  __syncthreads();
+  const double* luA1 = sR;
+  const double* luB2 = luA1 + N1 * N1;
+  const double* luC1 = luB2 + Q * Q;
+  const double* Q1 = luC1 + Q * Q;
+  const double* T1 = Q1 + Q * Q;
+  const double* Q2 = T1 + Q * Q;
+  const double* T2 = Q2 + Q * Q;
+  // axis 2 (outer, A1): fibers over (r, j)
+  for (int f = tid; f < Q * Q; f += k3Threads) lu_fiber_reg<N1>(luA1, sPiv, sX + (f / Q) * ld + f % Q, ss);
+  // Sylvester plan (independent of the data)
+  for (int i = tid; i < 2 * Q; i += k3Threads) {
+    const double* row = i < Q ? T1 + i * Q : T2 + (i - Q) * Q;
+    double s = 0.0;
+    for (int j = 0; j < Q; ++j) s = fadd(s, fabs(row[j]));
+    sRow[i] = s;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    double m1 = 0.0, m2 = 0.0;
+    for (int i = 0; i < Q; ++i) m1 = fmax(m1, sRow[i]);
+    for (int i = 0; i < Q; ++i) m2 = fmax(m2, sRow[Q + i]);
+    sTol[0] = fmul(1e-14, fmax(fadd(m1, m2), 1e-300));
+    const int nb1 = quasi_blocks_dev(T1, Q, sb, sb + Q);
+    const int nb2 = quasi_blocks_dev(T2, Q, sb + 2 * Q, sb + 3 * Q);
+    sb[4 * Q] = nb1;
+    sb[4 * Q + 1] = nb2;
+    sb[4 * Q + 2] = (nb1 == Q && nb2 == Q) ? 1 : 0;
+  }
+  // axis 1 (middle, B2): fibers over (s, j)
+  for (int f = tid; f < N1 * Q; f += k3Threads) lu_fiber_reg<Q>(luB2, sPiv + N1, sX + (f / Q) * ss + f % Q, ld);
+  __syncthreads();
+  // axis 0 (inner, C1): rows
+  for (int f = tid; f < N1 * Q; f += k3Threads)
+    lu_fiber_reg<Q>(luC1, sPiv + N1 + Q, sX + (f / Q) * ss + (f % Q) * ld, 1);
+  __syncthreads();
+  cta_mm_slices<Q, Q, Q, true, false, 2, 4>(Q1, Q, 0, sX, ld, ss, sT, ld, ss, N1);  // Q1^T X_s
+  __syncthreads();
+  cta_mm_slices<Q, Q, Q, false, false, 2, 4>(sT, ld, ss, Q2, Q, 0, sX, ld, ss, N1);  // (.) Q2 -> M_s
+  __syncthreads();
+  {  // Y_s overwrites M_s: wavefront over all slices at once
+    const int nb1 = sb[4 * Q], nb2 = sb[4 * Q + 1];
+    const bool all11 = sb[4 * Q + 2] != 0;
+    const int *s1 = sb, *z1 = sb + Q, *s2 = sb + 2 * Q, *z2 = sb + 3 * Q;
+    const double tol = sTol[0];
+    for (int step = 0; step <= nb1 + nb2 - 2; ++step) {
+      const int d1lo = step - (nb2 - 1) > 0 ? step - (nb2 - 1) : 0;
+      const int d1hi = step < nb1 - 1 ? step : nb1 - 1;
+      const int ncell = d1hi - d1lo + 1;
+      if (all11) {
+        for (int t = tid; t < ncell * N1; t += k3Threads) {
+          const int sl = t / ncell, d1 = d1lo + t % ncell;
+          double* Ms = sX + sl * ss;
+          const int i = nb1 - 1 - d1, k = nb2 - 1 - (step - d1);
+          const double s = sylv_rhs(T1, Q, T2, Q, Ms, Ms, ld, i, k, i + 1, k + 1);
+          const double coef = fadd(fadd(0.0, T1[i * Q + i]), T2[k * Q + k]);
+          if (fabs(coef) < tol) atomicExch(pc.status, int(TPDG_SINGULAR));
+          Ms[i * ld + k] = fdiv(s, coef);
+        }
+      } else {
+        const int ngroups = ncell * N1;  // (cell, slice) groups of 4 lanes
+        for (int base = 0; base < ngroups * 4; base += k3Threads) {
+          const int t = base + tid, grp = t >> 2, e = t & 3;
+          const bool ok = grp < ngroups;
+          int i0 = 0, k0 = 0, isz = 1, ksz = 1;
+          double* Ms = sX;
+          double s = 0.0;
+          if (ok) {
+            const int sl = grp / ncell, d1 = d1lo + grp % ncell;
+            Ms = sX + sl * ss;
+            const int bi = nb1 - 1 - d1, bj = nb2 - 1 - (step - d1);
+            i0 = s1[bi];
+            isz = z1[bi];
+            k0 = s2[bj];
+            ksz = z2[bj];
+            if (e < isz * ksz)
+              s = sylv_rhs(T1, Q, T2, Q, Ms, Ms, ld, i0 + e / ksz, k0 + e % ksz, i0 + isz, k0 + ksz);
+          }
+          double rg[4];
+          const int lane = tid & 31, gl = lane & ~3;
+#pragma unroll
+          for (int u = 0; u < 4; ++u) rg[u] = __shfl_sync(0xffffffffu, s, gl + u);
+          if (ok && e < isz * ksz) {
+            const int code = (isz - 1) * 2 + (ksz - 1);
+            double y;
+            if (code == 0) y = sylv_solve_group<1, 1>(T1, Q, T2, Q, i0, k0, rg, e, tol, pc.status);
+            else if (code == 1) y = sylv_solve_group<1, 2>(T1, Q, T2, Q, i0, k0, rg, e, tol, pc.status);
+            else if (code == 2) y = sylv_solve_group<2, 1>(T1, Q, T2, Q, i0, k0, rg, e, tol, pc.status);
+            else y = sylv_solve_group<2, 2>(T1, Q, T2, Q, i0, k0, rg, e, tol, pc.status);
+            Ms[(i0 + e / ksz) * ld + k0 + e % ksz] = y;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  cta_mm_slices<Q, Q, Q, false, false, 2, 4>(Q1, Q, 0, sX, ld, ss, sT, ld, ss, N1);  // Q1 Y_s
+  __syncthreads();
+  cta_mm_slices<Q, Q, Q, false, true, 2, 4>(sT, ld, ss, Q2, Q, 0, out + size_t(blk) * (N1 * Q * Q), Q, Q * Q,
+                                            N1);  // (.) Q2^T
+}
+
+template <int N1, int Q>
+bool try_kron3d_sized(const DevPC& pc, const double* in, double* out, cudaStream_t st) {
+  if (pc.dim != 3 || pc.n1 != N1 || pc.q != Q) return false;
+  const size_t smem = sizeof(double) * size_t(Kron3dLayout<N1, Q>::total);
+  static bool configured = false;
+  if (!configured) {
+    TPDG_CUDA_CHECK(cudaFuncSetAttribute(kron3d_sized_kernel<N1, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(smem)));
+    TPDG_CUDA_CHECK(cudaFuncSetAttribute(kron3d_sized_kernel<N1, Q>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                         100));
+    configured = true;
+  }
+  kron3d_sized_kernel<N1, Q><<<pc.nblk, k3Threads, smem, st>>>(pc, in, out);
+  return true;
+}
+
+bool launch_kron3d_sized(const DevPC& pc, const double* in, double* out, cudaStream_t st) {
+  return try_kron3d_sized<4, 4>(pc, in, out, st) || try_kron3d_sized<5, 5>(pc, in, out, st) ||
+         try_kron3d_sized<8, 8>(pc, in, out, st) || try_kron3d_sized<11, 11>(pc, in, out, st);
+}
+
 // ------------------------------------------------------------------------------------ 3D
 __global__ void __launch_bounds__(kApplyThreads) kron3d_apply_kernel(DevPC pc, const double* __restrict__ in,
                                                                       double* __restrict__ out) {
@@ -702,7 +911,7 @@ void launch_pc_apply(const DevPC& pc, const double* in, double* out, cudaStream_
       set_smem(kron2d_apply_kernel, smem, c2);
       kron2d_apply_kernel<<<pc.nblk, kApplyThreads, smem, st>>>(pc, in, out);
     }
-  } else {
+  } else if (!launch_kron3d_sized(pc, in, out, st)) {
     set_smem(kron3d_apply_kernel, smem, c3);
     kron3d_apply_kernel<<<pc.nblk, kApplyThreads, smem, st>>>(pc, in, out);
   }

@@ -20,7 +20,7 @@ HEADER = os.path.join(O.ROOT, "include", "tpdg_gpu.h")
 
 def declared_symbols():
     src = open(HEADER).read()
-    return sorted(set(re.findall(r"\b(tpdg_(?:gpu_|setup_|uniform|seeded)\w*)\s*\(", src)))
+    return sorted(set(re.findall(r"\b(tpdg_(?:gpu_|setup_|uniform|seeded|halo_plan_)\w*)\s*\(", src)))
 
 
 def test_library_exports_every_declared_symbol():
