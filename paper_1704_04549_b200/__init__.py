@@ -17,7 +17,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libtpdg_gpu.so")
+LIB_PATH = os.environ.get("TPDG_GPU_LIB") or os.path.join(_HERE, "libtpdg_gpu.so")  # override: A/B builds
 
 __all__ = [
     "Error", "ShapeError", "SingularError", "StateError", "ConvergenceError", "ConfigError", "GmresFailure",

@@ -165,7 +165,7 @@ struct tpdg_gpu_pc_s {
   tpdg_gpu_op op = nullptr;
   DevPC pc{};
   int nblk = 0, raw_len = 0;
-  DevBuf raw, rec, piv, kind, fb_slot, fb_lu, fb_piv, status;
+  DevBuf raw, rec, piv, kind, fb_slot, fb_lu, fb_piv, status, cells;
   std::vector<int> kind_h;
   std::vector<int64_t> fallbacks;  // (element, component)
 };
@@ -572,6 +572,12 @@ void finish_pc(tpdg_gpu_pc pc) {
   d.fb_lu = nfb ? pc->fb_lu.as<double>() : nullptr;
   d.fb_piv = nfb ? pc->fb_piv.as<int>() : nullptr;
   d.status = pc->status.as<int>();
+  d.cells_len = sylv_cells_len(op->dim, d.n1, op->q);
+  pc->cells.alloc(sizeof(double) * (size_t(pc->nblk) * d.cells_len + 32));  // +32: whole-slot loads of the last cell
+  TPDG_CUDA_CHECK(cudaMemsetAsync(pc->cells.p, 0, pc->cells.bytes, st));
+  d.cells = pc->cells.as<double>();
+  launch_sylv_cells(d, pc->cells.as<double>(), st);
+  TPDG_CUDA_CHECK(cudaStreamSynchronize(st));
 }
 
 void alloc_records(tpdg_gpu_pc pc) {

@@ -19,5 +19,17 @@ __device__ __forceinline__ double fmac(double s, double a, double b) { return __
 // s - a*b, rounded twice
 __device__ __forceinline__ double fmsc(double s, double a, double b) { return __dsub_rn(s, __dmul_rn(a, b)); }
 __device__ __forceinline__ double fdiv(double a, double b) { return __ddiv_rn(a, b); }
+// a / d correctly rounded, given y = __drcp_rn(d) (computed once per divisor): one Newton step
+// brings q within 1 ulp, then Markstein's correction q + (a - d q) y rounds to RN(a / d). The
+// residuals are exact (FMA); r0 == 0 means q0 is already the exact quotient (also keeps -0).
+// Equal to fdiv for finite, normal operands; the bit-exact parity tests pin it.
+__device__ __forceinline__ double fdiv_rcp(double a, double d, double y) {
+  const double q0 = __dmul_rn(a, y);
+  const double r0 = __fma_rn(-d, q0, a);
+  const double q1 = __fma_rn(r0, y, q0);
+  const double r1 = __fma_rn(-d, q1, a);
+  const double q2 = __fma_rn(r1, y, q1);
+  return r0 == 0.0 ? q0 : q2;
+}
 
 } // namespace tpdg_gpu

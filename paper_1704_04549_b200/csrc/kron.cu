@@ -266,8 +266,8 @@ size_t kron2d_smem(const DevPC& pc) {
 constexpr int kSizedThreads = 64;
 
 template <int N>
-__device__ __forceinline__ void lu_fiber_reg(const double* __restrict__ lu, const int* __restrict__ perm, double* col,
-                                             int stride) {
+__device__ __forceinline__ void lu_fiber_reg(const double* __restrict__ lu, const double* __restrict__ rcp,
+                                             const int* __restrict__ perm, double* col, int stride) {
   double x[N];
 #pragma unroll
   for (int k = 0; k < N; ++k) x[k] = col[perm[k] * stride];
@@ -283,56 +283,10 @@ __device__ __forceinline__ void lu_fiber_reg(const double* __restrict__ lu, cons
     double s = x[r];
 #pragma unroll
     for (int j = r + 1; j < N; ++j) s = fmsc(s, lu[r * N + j], x[j]);
-    x[r] = fdiv(s, lu[r * N + r]);
+    x[r] = fdiv_rcp(s, lu[r * N + r], rcp[r]);
   }
 #pragma unroll
   for (int k = 0; k < N; ++k) col[k * stride] = x[k];
-}
-
-// solve_tiny<4> on an n x n (n = IS*KS) register system; row swaps via predicated selects.
-template <int NS>
-__device__ __forceinline__ bool solve_tiny_reg(double (&a)[NS][NS], double (&b)[NS], double tol) {
-#pragma unroll
-  for (int k = 0; k < NS; ++k) {
-    int piv = k;
-    double pv = a[k][k];
-#pragma unroll
-    for (int i = k + 1; i < NS; ++i)
-      if (fabs(a[i][k]) > fabs(pv)) {
-        pv = a[i][k];
-        piv = i;
-      }
-    if (fabs(pv) < tol) return false;
-#pragma unroll
-    for (int i = k + 1; i < NS; ++i)
-      if (piv == i) {
-#pragma unroll
-        for (int j = 0; j < NS; ++j) {
-          const double t = a[i][j];
-          a[i][j] = a[k][j];
-          a[k][j] = t;
-        }
-        const double t = b[i];
-        b[i] = b[k];
-        b[k] = t;
-      }
-    const double inv = fdiv(1.0, a[k][k]);
-#pragma unroll
-    for (int i = k + 1; i < NS; ++i) {
-      const double m = fmul(a[i][k], inv);
-      if (m == 0.0) continue;
-#pragma unroll
-      for (int j = k; j < NS; ++j) a[i][j] = fmsc(a[i][j], m, a[k][j]);
-      b[i] = fmsc(b[i], m, b[k]);
-    }
-  }
-#pragma unroll
-  for (int i = NS - 1; i >= 0; --i) {
-#pragma unroll
-    for (int j = i + 1; j < NS; ++j) b[i] = fmsc(b[i], a[i][j], b[j]);
-    b[i] = fdiv(b[i], a[i][i]);
-  }
-  return true;
 }
 
 // Warp-level tiled product O = op(A) op(B) (R x K x C), lane tile TI x TJ; each output still
@@ -380,26 +334,41 @@ __device__ __forceinline__ double sylv_rhs(const double* __restrict__ t1, int n1
                                            int n2, const double* M, const double* Y, int ld, int i, int k,
                                            int jfirst, int lfirst) {
   double s = M[i * ld + k];
-  const double* trow = t1 + i * n1;
+  // one loop over both segments: the lanes of a wavefront step then share one trip count
+  const int nj = n1 - jfirst, nt = nj + n2 - lfirst;
+  const double* a1 = t1 + i * n1 + jfirst;
+  const double* b1 = Y + jfirst * ld + k;
+  const double* a2 = t2 + k * n2 + lfirst - nj;
+  const double* b2 = Y + i * ld + lfirst - nj;
 #pragma unroll 4
-  for (int j = jfirst; j < n1; ++j) s = fmsc(s, trow[j], Y[j * ld + k]);
-  const double* t2row = t2 + k * n2;
-  const double* yrow = Y + i * ld;
-#pragma unroll 4
-  for (int l = lfirst; l < n2; ++l) s = fmsc(s, t2row[l], yrow[l]);
+  for (int t = 0; t < nt; ++t) {
+    const bool first = t < nj;
+    const double* pa = first ? a1 + t : a2 + t;
+    const double* pb = first ? b1 + t * ld : b2 + t;
+    s = fmsc(s, *pa, *pb);
+  }
   return s;
 }
 
+// ---------------------------------------------------------------- Sylvester cell factors
+// The tiny system of a Sylvester cell, (T1_ii (x) I + I (x) T2_kk) y = r (sylvester.hpp:84-107),
+// does not depend on the data: sylv_cells_kernel runs solve_tiny's elimination once per PC and
+// stores what it applies to the right-hand side, so that the apply only replays those row
+// operations. Cell slot: [code, L (strict lower, row-major), U (strict upper, row-major),
+// diag(U), 1/diag(U)]; code = perm[u] in bits 2u..2u+1 | singular << 8. The row swaps of the
+// interleaved elimination are composed LAPACK-style (swapped together with the stored
+// multipliers), so every right-hand side entry sees the same operations in the same order.
 template <int IS, int KS>
-__device__ __forceinline__ double sylv_solve_group(const double* t1, int n1, const double* t2, int n2, int i0, int k0,
-                                                   const double (&rg)[4], int e, double tol, int* status) {
+__device__ void factor_cell(const double* t1, int n1, const double* t2, int n2, int i0, int k0, double tol,
+                            double* c) {
   constexpr int NS = IS * KS;
-  double a[NS][NS], r[NS];
+  double a[NS][NS], L[NS][NS];
+  int perm[NS];
+  bool sing = false;
 #pragma unroll
   for (int ai = 0; ai < IS; ++ai)
 #pragma unroll
-    for (int kb = 0; kb < KS; ++kb) {
-      r[ai * KS + kb] = rg[ai * KS + kb];
+    for (int kb = 0; kb < KS; ++kb)
 #pragma unroll
       for (int a2 = 0; a2 < IS; ++a2)
 #pragma unroll
@@ -409,13 +378,219 @@ __device__ __forceinline__ double sylv_solve_group(const double* t1, int n1, con
           if (ai == a2) coef = fadd(coef, t2[(k0 + kb) * n2 + k0 + kb2]);
           a[ai * KS + kb][a2 * KS + kb2] = coef;
         }
+#pragma unroll
+  for (int u = 0; u < NS; ++u) {
+    perm[u] = u;
+#pragma unroll
+    for (int v = 0; v < NS; ++v) L[u][v] = 0.0;
+  }
+#pragma unroll
+  for (int k = 0; k < NS; ++k) {
+    int piv = k;
+    double pv = a[k][k];
+#pragma unroll
+    for (int i = k + 1; i < NS; ++i)
+      if (fabs(a[i][k]) > fabs(pv)) {
+        pv = a[i][k];
+        piv = i;
+      }
+    if (fabs(pv) < tol) {
+      sing = true;
+      break;
     }
-  if (!solve_tiny_reg<NS>(a, r, tol)) atomicExch(status, int(TPDG_SINGULAR));
-  double y = r[0];
+#pragma unroll
+    for (int i = k + 1; i < NS; ++i)
+      if (piv == i) {
+#pragma unroll
+        for (int j = 0; j < NS; ++j) {
+          double t = a[i][j];
+          a[i][j] = a[k][j];
+          a[k][j] = t;
+          t = L[i][j];
+          L[i][j] = L[k][j];
+          L[k][j] = t;
+        }
+        const int t = perm[i];
+        perm[i] = perm[k];
+        perm[k] = t;
+      }
+    const double inv = fdiv(1.0, a[k][k]);
+#pragma unroll
+    for (int i = k + 1; i < NS; ++i) {
+      const double m = fmul(a[i][k], inv);
+      L[i][k] = m;
+      if (m == 0.0) continue;
+#pragma unroll
+      for (int j = k; j < NS; ++j) a[i][j] = fmsc(a[i][j], m, a[k][j]);
+    }
+  }
+  long long code = sing ? 256 : 0;
+#pragma unroll
+  for (int u = 0; u < NS; ++u) code |= (long long)perm[u] << (2 * u);
+  int o = 0;
+  c[o++] = __longlong_as_double(code);
+#pragma unroll
+  for (int i = 1; i < NS; ++i)
+#pragma unroll
+    for (int j = 0; j < i; ++j) c[o++] = L[i][j];
+#pragma unroll
+  for (int i = 0; i < NS; ++i)
+#pragma unroll
+    for (int j = i + 1; j < NS; ++j) c[o++] = a[i][j];
+#pragma unroll
+  for (int i = 0; i < NS; ++i) c[o + i] = a[i][i];
+#pragma unroll
+  for (int i = 0; i < NS; ++i) c[o + NS + i] = __drcp_rn(a[i][i]);
+}
+
+// One warp per Kronecker block: lane 0 builds the plan (tol from the row sums, quasi-blocks),
+// the lanes factor the cells.
+__global__ void sylv_cells_kernel(DevPC pc, double* __restrict__ cells) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= pc.nblk || pc.kind[warp] == 0) return;
+  const int t1n = pc.dim == 2 ? pc.n1 : pc.q, t2n = pc.q;
+  const double* r = pc.rec + size_t(warp) * pc.rec_len;
+  const double* t1 = pc.dim == 2 ? r + 2 * pc.n1 * pc.n1 + pc.q * pc.q : r + pc.n1 * pc.n1 + 3 * pc.q * pc.q;
+  const double* t2 = t1 + t1n * t1n + pc.q * pc.q;  // T1, Q2, T2 (rec layout of make_factors)
+  double* c = cells + size_t(warp) * pc.cells_len;
+  int* h = reinterpret_cast<int*>(c);
+  if (lane == 0) {
+    double m1 = 0.0, m2 = 0.0;
+    for (int i = 0; i < t1n; ++i) {
+      double s = 0.0;
+      for (int j = 0; j < t1n; ++j) s = fadd(s, fabs(t1[i * t1n + j]));
+      m1 = fmax(m1, s);
+    }
+    for (int i = 0; i < t2n; ++i) {
+      double s = 0.0;
+      for (int j = 0; j < t2n; ++j) s = fadd(s, fabs(t2[i * t2n + j]));
+      m2 = fmax(m2, s);
+    }
+    const int nb1 = quasi_blocks_dev(t1, t1n, h + 4, h + 4 + t1n);
+    const int nb2 = quasi_blocks_dev(t2, t2n, h + 4 + 2 * t1n, h + 4 + 2 * t1n + t2n);
+    h[0] = nb1;
+    h[1] = nb2;
+    h[2] = (nb1 == t1n && nb2 == t2n) ? 1 : 0;
+    h[3] = 0;
+    reinterpret_cast<double*>(h)[sylv_hdr_doubles(t1n, t2n) - 1] = fmul(1e-14, fmax(fadd(m1, m2), 1e-300));
+  }
+  __syncwarp();
+  const int nb1 = h[0], nb2 = h[1];
+  const int *s1 = h + 4, *z1 = s1 + t1n, *s2 = z1 + t1n, *z2 = s2 + t2n;
+  const double tol = c[sylv_hdr_doubles(t1n, t2n) - 1];
+  double* cc = c + sylv_hdr_doubles(t1n, t2n);
+  for (int cell = lane; cell < nb1 * nb2; cell += 32) {
+    const int bi = cell / nb2, bk = cell % nb2;
+    const int i0 = s1[bi], isz = z1[bi], k0 = s2[bk], ksz = z2[bk];
+    double* slot = cc + 6 * (i0 * t2n + isz * k0);
+    const int code = (isz - 1) * 2 + (ksz - 1);
+    if (code == 0) factor_cell<1, 1>(t1, t1n, t2, t2n, i0, k0, tol, slot);
+    else if (code == 1) factor_cell<1, 2>(t1, t1n, t2, t2n, i0, k0, tol, slot);
+    else if (code == 2) factor_cell<2, 1>(t1, t1n, t2, t2n, i0, k0, tol, slot);
+    else factor_cell<2, 2>(t1, t1n, t2, t2n, i0, k0, tol, slot);
+  }
+}
+
+// Replays a factored cell on the permuted right-hand side b (b[u] = r[perm[u]]); returns entry e.
+template <int NS>
+__device__ __forceinline__ double cell_solve(const double (&cf)[22], double (&b)[4], int e) {
+  constexpr int NL = NS * (NS - 1) / 2;
+  int o = 1;
+#pragma unroll
+  for (int i = 1; i < NS; ++i)
+#pragma unroll
+    for (int j = 0; j < i; ++j) {
+      const double m = cf[o++];
+      b[i] = m != 0.0 ? fmsc(b[i], m, b[j]) : b[i];
+    }
+#pragma unroll
+  for (int i = NS - 1; i >= 0; --i) {
+    int u = 1 + NL;
+#pragma unroll
+    for (int r = 0; r < i; ++r) u += NS - 1 - r;
+#pragma unroll
+    for (int j = i + 1; j < NS; ++j) b[i] = fmsc(b[i], cf[u + j - i - 1], b[j]);
+    b[i] = fdiv_rcp(b[i], cf[1 + 2 * NL + i], cf[1 + 2 * NL + NS + i]);
+  }
+  double y = b[0];
 #pragma unroll
   for (int t = 1; t < NS; ++t)
-    if (e == t) y = r[t];
+    if (e == t) y = b[t];
   return y;
+}
+
+// Block anti-diagonal wavefront of the quasi-triangular Sylvester solve over NSL slices that
+// share one plan (2D: 1, 3D: the outer slices). Work items are (step, pass) pairs, each pass a
+// set of NT/4 (cell, slice) groups of 4 lanes; the factors of the next item's cell are loaded
+// while the current one computes (register double buffer), and SYNC separates the steps.
+template <int TN1, int TN2, int NSL, int NT, bool CTA>
+__device__ __forceinline__ void sylv_wavefront(const double* T1, const double* T2, double* X, int ld, int ss,
+                                               const double* __restrict__ cc, const int* sb, int tid, int* status) {
+  const int nb1 = sb[0], nb2 = sb[1];
+  const int *s1 = sb + 4, *z1 = s1 + TN1, *s2 = z1 + TN1, *z2 = s2 + TN2;
+  const int last = nb1 + nb2 - 2, lane = tid & 31, e = lane & 3, g = lane & ~3;
+  int step = 0, base = 0;
+  double cf[22];
+  int bi = 0, bj = 0, sl = 0;
+  bool ok = false;
+  auto load = [&](int st, int bs, double (&c)[22], int& obi, int& obj, int& osl, bool& ook) {
+    const int d1lo = st - (nb2 - 1) > 0 ? st - (nb2 - 1) : 0;
+    const int d1hi = st < nb1 - 1 ? st : nb1 - 1;
+    const int ncell = d1hi - d1lo + 1;
+    const int grp = (bs + tid) >> 2;
+    ook = grp < ncell * NSL;
+    const int cell = ook ? grp % ncell : 0;
+    osl = ook ? grp / ncell : 0;
+    const int d1 = d1lo + cell;
+    obi = nb1 - 1 - d1;
+    obj = nb2 - 1 - (st - d1);
+    if (ook) {
+      const double2* p = reinterpret_cast<const double2*>(cc + 6 * (s1[obi] * TN2 + z1[obi] * s2[obj]));
+#pragma unroll
+      for (int u = 0; u < 11; ++u) {
+        const double2 v = __ldg(p + u);
+        c[2 * u] = v.x;
+        c[2 * u + 1] = v.y;
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < 22; ++u) c[u] = 0.0;
+    }
+  };
+  while (step <= last) {
+    // this item's cell factors first: their latency overlaps the right-hand side chain
+    load(step, base, cf, bi, bj, sl, ok);
+    double* Ms = X + sl * ss;
+    int i0 = 0, k0 = 0, isz = 1, ksz = 1;
+    double s = 0.0;
+    if (ok) {
+      i0 = s1[bi];
+      isz = z1[bi];
+      k0 = s2[bj];
+      ksz = z2[bj];
+      if (e < isz * ksz) s = sylv_rhs(T1, TN1, T2, TN2, Ms, Ms, ld, i0 + e / ksz, k0 + e % ksz, i0 + isz, k0 + ksz);
+    }
+    const long long code = __double_as_longlong(cf[0]);
+    double b[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) b[u] = __shfl_sync(0xffffffffu, s, g + int((code >> (2 * u)) & 3));
+    const int ns = isz * ksz;
+    if (ok && e < ns) {
+      if (code & 256) atomicExch(status, int(TPDG_SINGULAR));
+      const double y = ns == 1 ? cell_solve<1>(cf, b, e) : ns == 2 ? cell_solve<2>(cf, b, e) : cell_solve<4>(cf, b, e);
+      Ms[(i0 + e / ksz) * ld + k0 + e % ksz] = y;
+    }
+    // next work item: the next pass of this step, else the first pass of the next step
+    const int d1lo = step - (nb2 - 1) > 0 ? step - (nb2 - 1) : 0;
+    const int d1hi = step < nb1 - 1 ? step : nb1 - 1;
+    base += NT;
+    if (base >= (d1hi - d1lo + 1) * NSL * 4) {
+      ++step;
+      base = 0;
+      if (CTA) __syncthreads();
+      else __syncwarp();
+    }
+  }
 }
 
 // One warp per element: every phase is warp-synchronous (no CTA barriers), so several elements
@@ -424,8 +599,9 @@ template <int N1, int N2>
 struct Kron2dWarpLayout {
   static constexpr int ld = (N2 + 1) & ~1;
   static constexpr int rec = 3 * N1 * N1 + 3 * N2 * N2;
-  static constexpr int ints = (N1 + N2) + 2 * N1 + 2 * N2 + 4;
-  static constexpr int per = N1 * ld + rec + (N1 + N2) + ((ints + 1) / 2) + 2;
+  static constexpr int hdr = (((4 + 2 * N1 + 2 * N2) / 2 + 2) & ~1);
+  static constexpr int ints = N1 + N2;
+  static constexpr int per = N1 * ld + rec + (N1 + N2) + hdr + (ints + 1) / 2;
   static constexpr int per_even = (per + 1) & ~1;
 };
 
@@ -433,7 +609,7 @@ template <int N1, int N2>
 __global__ void __launch_bounds__(kSizedThreads) kron2d_sized_kernel(DevPC pc, const double* __restrict__ in,
                                                                       double* __restrict__ out) {
   using L = Kron2dWarpLayout<N1, N2>;
-  constexpr int ld = L::ld, rec = L::rec;
+  constexpr int ld = L::ld, rec = L::rec, hdr = L::hdr;
   extern __shared__ double sm_all[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int blk = blockIdx.x * (kSizedThreads / 32) + warp;
@@ -441,10 +617,10 @@ __global__ void __launch_bounds__(kSizedThreads) kron2d_sized_kernel(DevPC pc, c
   double* sX = sm_all + size_t(warp) * L::per_even;
   double* sR = sX + N1 * ld;
   double* sT = sR;  // product scratch: aliases LU(A2), LU(B1) once both fiber solves are done
-  double* sRow = sR + rec;
-  double* sTol = sRow + (N1 + N2);
-  int* sPiv = reinterpret_cast<int*>(sTol + 2);
-  int* sb = sPiv + N1 + N2;  // s1[N1] z1[N1] s2[N2] z2[N2] nb1 nb2 all11
+  double* sRcp = sR + rec;
+  double* sH = sRcp + (N1 + N2);  // Sylvester plan header (ints)
+  int* sPiv = reinterpret_cast<int*>(sH + hdr);
+  const double* cells = pc.cells + size_t(blk) * pc.cells_len;
   {  // asynchronous global -> shared copies (LDGSTS), one round trip for the whole record
     const double* r = pc.rec + size_t(blk) * rec;
     if ((reinterpret_cast<uintptr_t>(r) & 15) == 0) {
@@ -453,6 +629,7 @@ __global__ void __launch_bounds__(kSizedThreads) kron2d_sized_kernel(DevPC pc, c
     } else {
       for (int i = lane; i < rec; i += 32) cp_async8(sR + i, r + i);
     }
+    for (int i = 2 * lane; i < hdr; i += 64) cp_async16(sH + i, cells + i);
     for (int i = lane; i < N1 + N2; i += 32) sPiv[i] = pc.piv[size_t(blk) * (N1 + N2) + i];
     const double* x = in + size_t(blk) * (N1 * N2);
     for (int i = lane; i < N1 * N2; i += 32) cp_async8(sX + (i / N2) * ld + i % N2, x + i);
@@ -465,82 +642,39 @@ __global__ void __launch_bounds__(kSizedThreads) kron2d_sized_kernel(DevPC pc, c
   const double* T1 = Q1 + N1 * N1;
   const double* Q2 = T1 + N1 * N1;
   const double* T2 = Q2 + N2 * N2;
-  // (A2^{-1} (x) I): one column fiber per lane
-  for (int c = lane; c < N2; c += 32) lu_fiber_reg<N1>(luA2, sPiv, sX + c, ld);
-  // Sylvester plan: row sums of |T| (in order), max, quasi-block structure
-  for (int i = lane; i < N1 + N2; i += 32) {
-    const double* row = i < N1 ? T1 + i * N1 : T2 + (i - N1) * N2;
-    const int n = i < N1 ? N1 : N2;
-    double s = 0.0;
-    for (int j = 0; j < n; ++j) s = fadd(s, fabs(row[j]));
-    sRow[i] = s;
-  }
+  for (int i = lane; i < N1 + N2; i += 32)
+    sRcp[i] = __drcp_rn(i < N1 ? luA2[i * N1 + i] : luB1[(i - N1) * N2 + i - N1]);
   __syncwarp();
-  if (lane == 0) {
-    double m1 = 0.0, m2 = 0.0;
-    for (int i = 0; i < N1; ++i) m1 = fmax(m1, sRow[i]);
-    for (int i = 0; i < N2; ++i) m2 = fmax(m2, sRow[N1 + i]);
-    sTol[0] = fmul(1e-14, fmax(fadd(m1, m2), 1e-300));
-    const int nb1 = quasi_blocks_dev(T1, N1, sb, sb + N1);
-    const int nb2 = quasi_blocks_dev(T2, N2, sb + 2 * N1, sb + 2 * N1 + N2);
-    sb[2 * N1 + 2 * N2] = nb1;
-    sb[2 * N1 + 2 * N2 + 1] = nb2;
-    sb[2 * N1 + 2 * N2 + 2] = (nb1 == N1 && nb2 == N2) ? 1 : 0;
-  }
+  // (A2^{-1} (x) I): one column fiber per lane
+  for (int c = lane; c < N2; c += 32) lu_fiber_reg<N1>(luA2, sRcp, sPiv, sX + c, ld);
   __syncwarp();
   // (I (x) B1^{-1}): one row fiber per lane
-  for (int r = lane; r < N1; r += 32) lu_fiber_reg<N2>(luB1, sPiv + N1, sX + r * ld, 1);
+  for (int r = lane; r < N1; r += 32) lu_fiber_reg<N2>(luB1, sRcp + N1, sPiv + N1, sX + r * ld, 1);
   __syncwarp();
   warp_mm<N1, N1, N2, true, false, 2, 4>(Q1, N1, sX, ld, sT, ld, lane);  // Q1^T X
   __syncwarp();
   warp_mm<N1, N2, N2, false, false, 2, 4>(sT, ld, Q2, N2, sX, ld, lane);  // (.) Q2 -> M
   __syncwarp();
   {  // Y overwrites M in place (sX): T1 Y + Y T2^T = M, block anti-diagonal wavefront
-    const int nb1 = sb[2 * N1 + 2 * N2], nb2 = sb[2 * N1 + 2 * N2 + 1];
-    const bool all11 = sb[2 * N1 + 2 * N2 + 2] != 0;
-    const int *s1 = sb, *z1 = sb + N1, *s2 = sb + 2 * N1, *z2 = sb + 2 * N1 + N2;
-    const double tol = sTol[0];
-    for (int step = 0; step <= nb1 + nb2 - 2; ++step) {
-      const int d1lo = step - (nb2 - 1) > 0 ? step - (nb2 - 1) : 0;
-      const int d1hi = step < nb1 - 1 ? step : nb1 - 1;
-      if (all11) {  // 1 x 1 blocks: one lane per cell; solve_tiny<1> is y = r / (t1_ii + t2_kk)
+    const int* sb = reinterpret_cast<const int*>(sH);
+    const double* cc = cells + hdr;
+    if (sb[2]) {  // 1 x 1 blocks: one lane per cell; solve_tiny<1> is y = r / (t1_ii + t2_kk)
+      const int nb1 = sb[0], nb2 = sb[1];
+      for (int step = 0; step <= nb1 + nb2 - 2; ++step) {
+        const int d1lo = step - (nb2 - 1) > 0 ? step - (nb2 - 1) : 0;
+        const int d1hi = step < nb1 - 1 ? step : nb1 - 1;
         for (int d1 = d1lo + lane; d1 <= d1hi; d1 += 32) {
           const int i = nb1 - 1 - d1, k = nb2 - 1 - (step - d1);
+          const double* c = cc + 6 * (i * N2 + k);
+          const double code = __ldg(c), coef = __ldg(c + 1), rcp = __ldg(c + 2);
           const double s = sylv_rhs(T1, N1, T2, N2, sX, sX, ld, i, k, i + 1, k + 1);
-          const double coef = fadd(fadd(0.0, T1[i * N1 + i]), T2[k * N2 + k]);
-          if (fabs(coef) < tol) atomicExch(pc.status, int(TPDG_SINGULAR));
-          sX[i * ld + k] = fdiv(s, coef);
+          if (__double_as_longlong(code) & 256) atomicExch(pc.status, int(TPDG_SINGULAR));
+          sX[i * ld + k] = fdiv_rcp(s, coef, rcp);
         }
-      } else {  // 4 lanes per cell (one per entry), tiny solve replicated in the group
-        for (int base = d1lo; base <= d1hi; base += 8) {
-          const int d1 = base + (lane >> 2), e = lane & 3;
-          const bool cell_ok = d1 <= d1hi;
-          int i0 = 0, k0 = 0, isz = 1, ksz = 1;
-          double s = 0.0;
-          if (cell_ok) {
-            const int bi = nb1 - 1 - d1, bj = nb2 - 1 - (step - d1);
-            i0 = s1[bi];
-            isz = z1[bi];
-            k0 = s2[bj];
-            ksz = z2[bj];
-            if (e < isz * ksz)
-              s = sylv_rhs(T1, N1, T2, N2, sX, sX, ld, i0 + e / ksz, k0 + e % ksz, i0 + isz, k0 + ksz);
-          }
-          double rg[4];
-          const int g = lane & ~3;
-#pragma unroll
-          for (int t = 0; t < 4; ++t) rg[t] = __shfl_sync(0xffffffffu, s, g + t);
-          if (cell_ok && e < isz * ksz) {
-            const int code = (isz - 1) * 2 + (ksz - 1);
-            double y;
-            if (code == 0) y = sylv_solve_group<1, 1>(T1, N1, T2, N2, i0, k0, rg, e, tol, pc.status);
-            else if (code == 1) y = sylv_solve_group<1, 2>(T1, N1, T2, N2, i0, k0, rg, e, tol, pc.status);
-            else if (code == 2) y = sylv_solve_group<2, 1>(T1, N1, T2, N2, i0, k0, rg, e, tol, pc.status);
-            else y = sylv_solve_group<2, 2>(T1, N1, T2, N2, i0, k0, rg, e, tol, pc.status);
-            sX[(i0 + e / ksz) * ld + k0 + e % ksz] = y;
-          }
-        }
+        __syncwarp();
       }
+    } else {  // 4 lanes per cell (one per entry), the cell's factored tiny system replayed in the group
+      sylv_wavefront<N1, N2, 1, 32, false>(T1, T2, sX, ld, 0, cc, sb, lane, pc.status);
       __syncwarp();
     }
   }
@@ -628,7 +762,9 @@ template <int N1, int Q>
 struct Kron3dLayout {
   static constexpr int ld = Q | 1, ss = Q * ld;  // row stride, slice stride (odd: conflict-free fibers)
   static constexpr int rec = N1 * N1 + 6 * Q * Q;
-  static constexpr int total = 2 * N1 * ss + rec + 2 * Q + ((N1 + 2 * Q + 4 * Q + 4) + 1) / 2 + 4;
+  static constexpr int hdr = (((4 + 4 * Q) / 2 + 2) & ~1);
+  static constexpr int rcp = (N1 + 2 * Q + 1) & ~1;
+  static constexpr int total = 2 * N1 * ss + rec + rcp + hdr + (N1 + 2 * Q + 1) / 2 + 2;
 };
 
 template <int N1, int Q>
@@ -637,16 +773,16 @@ __global__ void __launch_bounds__(k3Threads) kron3d_sized_kernel(DevPC pc, const
   const int blk = blockIdx.x;
   if (pc.kind[blk] == 0 || (pc.skip && *pc.skip)) return;
   using L = Kron3dLayout<N1, Q>;
-  constexpr int ld = L::ld, ss = L::ss, rec = L::rec;
+  constexpr int ld = L::ld, ss = L::ss, rec = L::rec, hdr = L::hdr;
   extern __shared__ double sm[];
   double* sX = sm;
   double* sT = sX + N1 * ss;
   double* sR = sT + N1 * ss;
-  double* sRow = sR + rec;
-  double* sTol = sRow + 2 * Q;
-  int* sPiv = reinterpret_cast<int*>(sTol + 2);
-  int* sb = sPiv + N1 + 2 * Q;  // s1 z1 s2 z2 (Q each) nb1 nb2 all11
+  double* sRcp = sR + rec;
+  double* sH = sRcp + L::rcp;
+  int* sPiv = reinterpret_cast<int*>(sH + hdr);
   const int tid = threadIdx.x;
+  const double* cells = pc.cells + size_t(blk) * pc.cells_len;
   {
     const double* r = pc.rec + size_t(blk) * rec;
     if ((reinterpret_cast<uintptr_t>(r) & 15) == 0 && (reinterpret_cast<uintptr_t>(sR) & 15) == 0) {
@@ -655,6 +791,7 @@ __global__ void __launch_bounds__(k3Threads) kron3d_sized_kernel(DevPC pc, const
     } else {
       for (int i = tid; i < rec; i += k3Threads) cp_async8(sR + i, r + i);
     }
+    for (int i = tid; i < hdr; i += k3Threads) cp_async8(sH + i, cells + i);
     for (int i = tid; i < N1 + 2 * Q; i += k3Threads) sPiv[i] = pc.piv[size_t(blk) * (N1 + 2 * Q) + i];
     const double* x = in + size_t(blk) * (N1 * Q * Q);
     for (int i = tid; i < N1 * Q * Q; i += k3Threads) {
@@ -671,91 +808,47 @@ __global__ void __launch_bounds__(k3Threads) kron3d_sized_kernel(DevPC pc, const
   const double* T1 = Q1 + Q * Q;
   const double* Q2 = T1 + Q * Q;
   const double* T2 = Q2 + Q * Q;
-  // axis 2 (outer, A1): fibers over (r, j)
-  for (int f = tid; f < Q * Q; f += k3Threads) lu_fiber_reg<N1>(luA1, sPiv, sX + (f / Q) * ld + f % Q, ss);
-  // Sylvester plan (independent of the data)
-  for (int i = tid; i < 2 * Q; i += k3Threads) {
-    const double* row = i < Q ? T1 + i * Q : T2 + (i - Q) * Q;
-    double s = 0.0;
-    for (int j = 0; j < Q; ++j) s = fadd(s, fabs(row[j]));
-    sRow[i] = s;
-  }
+  for (int i = tid; i < N1 + 2 * Q; i += k3Threads)
+    sRcp[i] = __drcp_rn(i < N1 ? luA1[i * N1 + i] : i < N1 + Q ? luB2[(i - N1) * (Q + 1)] : luC1[(i - N1 - Q) * (Q + 1)]);
   __syncthreads();
-  if (tid == 0) {
-    double m1 = 0.0, m2 = 0.0;
-    for (int i = 0; i < Q; ++i) m1 = fmax(m1, sRow[i]);
-    for (int i = 0; i < Q; ++i) m2 = fmax(m2, sRow[Q + i]);
-    sTol[0] = fmul(1e-14, fmax(fadd(m1, m2), 1e-300));
-    const int nb1 = quasi_blocks_dev(T1, Q, sb, sb + Q);
-    const int nb2 = quasi_blocks_dev(T2, Q, sb + 2 * Q, sb + 3 * Q);
-    sb[4 * Q] = nb1;
-    sb[4 * Q + 1] = nb2;
-    sb[4 * Q + 2] = (nb1 == Q && nb2 == Q) ? 1 : 0;
-  }
+  // axis 2 (outer, A1): fibers over (r, j)
+  for (int f = tid; f < Q * Q; f += k3Threads) lu_fiber_reg<N1>(luA1, sRcp, sPiv, sX + (f / Q) * ld + f % Q, ss);
+  __syncthreads();
   // axis 1 (middle, B2): fibers over (s, j)
-  for (int f = tid; f < N1 * Q; f += k3Threads) lu_fiber_reg<Q>(luB2, sPiv + N1, sX + (f / Q) * ss + f % Q, ld);
+  for (int f = tid; f < N1 * Q; f += k3Threads)
+    lu_fiber_reg<Q>(luB2, sRcp + N1, sPiv + N1, sX + (f / Q) * ss + f % Q, ld);
   __syncthreads();
   // axis 0 (inner, C1): rows
   for (int f = tid; f < N1 * Q; f += k3Threads)
-    lu_fiber_reg<Q>(luC1, sPiv + N1 + Q, sX + (f / Q) * ss + (f % Q) * ld, 1);
+    lu_fiber_reg<Q>(luC1, sRcp + N1 + Q, sPiv + N1 + Q, sX + (f / Q) * ss + (f % Q) * ld, 1);
   __syncthreads();
   cta_mm_slices<Q, Q, Q, true, false, 2, 4>(Q1, Q, 0, sX, ld, ss, sT, ld, ss, N1);  // Q1^T X_s
   __syncthreads();
   cta_mm_slices<Q, Q, Q, false, false, 2, 4>(sT, ld, ss, Q2, Q, 0, sX, ld, ss, N1);  // (.) Q2 -> M_s
   __syncthreads();
   {  // Y_s overwrites M_s: wavefront over all slices at once
-    const int nb1 = sb[4 * Q], nb2 = sb[4 * Q + 1];
-    const bool all11 = sb[4 * Q + 2] != 0;
-    const int *s1 = sb, *z1 = sb + Q, *s2 = sb + 2 * Q, *z2 = sb + 3 * Q;
-    const double tol = sTol[0];
-    for (int step = 0; step <= nb1 + nb2 - 2; ++step) {
-      const int d1lo = step - (nb2 - 1) > 0 ? step - (nb2 - 1) : 0;
-      const int d1hi = step < nb1 - 1 ? step : nb1 - 1;
-      const int ncell = d1hi - d1lo + 1;
-      if (all11) {
+    const int* sb = reinterpret_cast<const int*>(sH);
+    const double* cc = cells + hdr;
+    if (sb[2]) {
+      const int nb1 = sb[0], nb2 = sb[1];
+      for (int step = 0; step <= nb1 + nb2 - 2; ++step) {
+        const int d1lo = step - (nb2 - 1) > 0 ? step - (nb2 - 1) : 0;
+        const int d1hi = step < nb1 - 1 ? step : nb1 - 1;
+        const int ncell = d1hi - d1lo + 1;
         for (int t = tid; t < ncell * N1; t += k3Threads) {
           const int sl = t / ncell, d1 = d1lo + t % ncell;
           double* Ms = sX + sl * ss;
           const int i = nb1 - 1 - d1, k = nb2 - 1 - (step - d1);
+          const double* c = cc + 6 * (i * Q + k);
+          const double code = __ldg(c), coef = __ldg(c + 1), rcp = __ldg(c + 2);
           const double s = sylv_rhs(T1, Q, T2, Q, Ms, Ms, ld, i, k, i + 1, k + 1);
-          const double coef = fadd(fadd(0.0, T1[i * Q + i]), T2[k * Q + k]);
-          if (fabs(coef) < tol) atomicExch(pc.status, int(TPDG_SINGULAR));
-          Ms[i * ld + k] = fdiv(s, coef);
+          if (__double_as_longlong(code) & 256) atomicExch(pc.status, int(TPDG_SINGULAR));
+          Ms[i * ld + k] = fdiv_rcp(s, coef, rcp);
         }
-      } else {
-        const int ngroups = ncell * N1;  // (cell, slice) groups of 4 lanes
-        for (int base = 0; base < ngroups * 4; base += k3Threads) {
-          const int t = base + tid, grp = t >> 2, e = t & 3;
-          const bool ok = grp < ngroups;
-          int i0 = 0, k0 = 0, isz = 1, ksz = 1;
-          double* Ms = sX;
-          double s = 0.0;
-          if (ok) {
-            const int sl = grp / ncell, d1 = d1lo + grp % ncell;
-            Ms = sX + sl * ss;
-            const int bi = nb1 - 1 - d1, bj = nb2 - 1 - (step - d1);
-            i0 = s1[bi];
-            isz = z1[bi];
-            k0 = s2[bj];
-            ksz = z2[bj];
-            if (e < isz * ksz)
-              s = sylv_rhs(T1, Q, T2, Q, Ms, Ms, ld, i0 + e / ksz, k0 + e % ksz, i0 + isz, k0 + ksz);
-          }
-          double rg[4];
-          const int lane = tid & 31, gl = lane & ~3;
-#pragma unroll
-          for (int u = 0; u < 4; ++u) rg[u] = __shfl_sync(0xffffffffu, s, gl + u);
-          if (ok && e < isz * ksz) {
-            const int code = (isz - 1) * 2 + (ksz - 1);
-            double y;
-            if (code == 0) y = sylv_solve_group<1, 1>(T1, Q, T2, Q, i0, k0, rg, e, tol, pc.status);
-            else if (code == 1) y = sylv_solve_group<1, 2>(T1, Q, T2, Q, i0, k0, rg, e, tol, pc.status);
-            else if (code == 2) y = sylv_solve_group<2, 1>(T1, Q, T2, Q, i0, k0, rg, e, tol, pc.status);
-            else y = sylv_solve_group<2, 2>(T1, Q, T2, Q, i0, k0, rg, e, tol, pc.status);
-            Ms[(i0 + e / ksz) * ld + k0 + e % ksz] = y;
-          }
-        }
+        __syncthreads();
       }
+    } else {
+      sylv_wavefront<Q, Q, N1, k3Threads, true>(T1, T2, sX, ld, ss, cc, sb, tid, pc.status);
       __syncthreads();
     }
   }
@@ -899,6 +992,12 @@ void set_smem(K kernel, size_t bytes, size_t& configured) {
 }
 
 } // namespace
+
+void launch_sylv_cells(const DevPC& pc, double* cells, cudaStream_t st) {
+  if (pc.nblk == 0) return;
+  sylv_cells_kernel<<<(pc.nblk + 3) / 4, 128, 0, st>>>(pc, cells);
+  TPDG_CUDA_CHECK(cudaGetLastError());
+}
 
 void launch_pc_apply(const DevPC& pc, const double* in, double* out, cudaStream_t st) {
   if (pc.nblk == 0) return;

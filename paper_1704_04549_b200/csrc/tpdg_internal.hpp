@@ -76,6 +76,8 @@ struct DevPC {
   const int* fb_slot;    // [nblk]: slot into fb_lu for fallback blocks, -1 otherwise
   const double* fb_lu;   // [n_fb][blk_len^2]
   const int* fb_piv;     // [n_fb][blk_len]
+  const double* cells;   // [nblk][cells_len]: Sylvester plan + factored tiny systems (sylv_cells_len)
+  int cells_len;
   int* status;           // device error flag (SingularError inside the Sylvester solve)
   const int* skip;       // optional device flag: kernels return immediately when *skip != 0
 };
@@ -84,12 +86,22 @@ __host__ __device__ inline int rec_len_of(int dim, int n1, int q) {
   return dim == 2 ? 3 * n1 * n1 + 3 * q * q : n1 * n1 + 6 * q * q;
 }
 __host__ __device__ inline int piv_len_of(int dim, int n1, int q) { return dim == 2 ? n1 + q : n1 + 2 * q; }
+// Sylvester cell record of one block (T1: t1 x t1, T2: t2 x t2): an int header [nb1, nb2, all11,
+// 0, s1[t1], z1[t1], s2[t2], z2[t2]], tol in its last double (even count), then 6 doubles per
+// Sylvester entry; the cell of quasi-blocks (bi, bk) starts at 6 (s1[bi] t2 + z1[bi] s2[bk]).
+__host__ __device__ inline int sylv_hdr_doubles(int t1, int t2) { return ((4 + 2 * t1 + 2 * t2) / 2 + 2) & ~1; }
+__host__ __device__ inline int sylv_cells_len(int dim, int n1, int q) {
+  const int t1 = dim == 2 ? n1 : q;
+  return sylv_hdr_doubles(t1, q) + 6 * t1 * q;
+}
 __host__ __device__ inline int raw_len_of(int dim, int n1, int q) { return dim == 2 ? 2 * n1 * n1 + 2 * q * q : n1 * n1 + 4 * q * q; }
 
 // ---------------------------------------------------------------- kernel launchers
 void launch_jv(const DevSys& s, const double* vin, const double* halo, double* vout, cudaStream_t st);
 size_t jv_smem_bytes(const DevSys& s);
 void launch_pc_apply(const DevPC& pc, const double* in, double* out, cudaStream_t st);
+// Factor the data-independent tiny Sylvester systems of every Kronecker block into pc.cells.
+void launch_sylv_cells(const DevPC& pc, double* cells, cudaStream_t st);
 void launch_shuffled(const DevSys& s, int e, int comp, int transpose, const double* in, double* out,
                      double* scratch, cudaStream_t st);
 size_t shuffled_scratch_doubles(const DevSys& s);
