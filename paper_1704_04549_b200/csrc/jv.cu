@@ -880,7 +880,7 @@ size_t jv_smem_bytes(const DevSys& s) { return s.dim == 2 ? jv2d_smem(s) : jv3d_
 void launch_jv(const DevSys& s, const double* vin, const double* halo, double* vout, cudaStream_t st) {
   if (s.n_local == 0) return;
   const size_t smem = jv_smem_bytes(s);
-  if (s.dim == 2 && launch_jv2d_sized(s, vin, halo, vout, st)) {
+  if (s.dim == 2 && (launch_jv2d_mma(s, vin, halo, vout, st) || launch_jv2d_sized(s, vin, halo, vout, st))) {
     TPDG_CUDA_CHECK(cudaGetLastError());
     ++g_launches;
     return;

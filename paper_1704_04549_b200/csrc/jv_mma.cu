@@ -1,0 +1,299 @@
+// Scalar 2D operator (a M + b J) v on the FP64 tensor cores (DMMA.8x8x4, mma.sync m8n8k4 f64),
+// one warp per element, persistent grid. Same operator as jv2d_sized_kernel (jv.cu; reference
+// ops/linearized.hpp:107-162,201-240), with every sum-factorized stage a warp-level DMMA product:
+//
+//   (1) t    = v G^T                    Q x Q   . Q x MU      (+ 6 spare columns, see below)
+//   (2) vals = G t                      MU x Q  . Q x NT1
+//   (3) A    = [M | F0] [GW^T ; DW^T]   MU x 2MU . 2MU x Q
+//   (4) B    = F1 GW^T                  MU x MU . MU x Q
+//   (5) out  = [GW | DW] [A ; B]        Q x 2MU . 2MU x Q      + face lifts, straight to HBM
+//
+// The face traces ride along in (1)-(2): the spare columns of t hold the element's two x-face
+// layers v[:, 0], v[:, Q-1] and the four neighbour face layers, so that (2) also returns
+// G v[:, layer] (own x-face traces) and G (neighbour layer) (neighbour traces); the own y-face
+// traces are rows 0 and Q-1 of t. F1 overwrites vals in place.
+//
+// Fragment layouts (PTX mma.m8n8k4 .f64, row.col): A 8x4: lane l holds A[l/4][l%4]; B 4x8:
+// B[l%4][l/4]; C 8x8: C[l/4][2(l%4) + {0,1}]. Leading dimensions are chosen so that every
+// fragment load is two conflict-free shared-memory wavefronts: ld = 4 (mod 8) for A and for
+// column-major B, ld = 8 (mod 16) for row-major B.
+//
+// Parity: FMA and DMMA change the summation order; the operator's gate is rel-L2 <= 1e-12
+// (SURVEY.md sec.8c), measured ~1e-16.
+#include <algorithm>
+
+#include "tpdg_internal.hpp"
+
+namespace tpdg_gpu {
+
+namespace {
+
+constexpr int p8(int x) { return (x + 7) & ~7; }
+constexpr int p4(int x) { return (x + 3) & ~3; }
+constexpr int lda4(int x) { return (x + 3) / 8 * 8 + 4; }   // smallest y >= x, y = 4 (mod 8)
+constexpr int ldb8(int x) { return (x + 7) / 16 * 16 + 8; }  // smallest y >= x, y = 8 (mod 16)
+
+__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(c[0]), "+d"(c[1])
+      : "d"(a), "d"(b));
+}
+
+// acc[MT][NT] += A[8MT x 4KC] B[4KC x 8NT]; A row-major (lda), B row-major (ldb) or, if BCOL,
+// stored as B^T row-major (B[k][n] = Bs[n * ldb + k]).
+template <int MT, int NT, int KC, bool BCOL>
+__device__ __forceinline__ void mma_tiles(double (&acc)[MT][NT][2], const double* A, int lda, const double* B, int ldb,
+                                          int lane) {
+  const int r = lane >> 2, kq = lane & 3;
+#pragma unroll
+  for (int kc = 0; kc < KC; ++kc) {
+    double a[MT], b[NT];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt) a[mt] = A[(8 * mt + r) * lda + 4 * kc + kq];
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) b[nt] = BCOL ? B[(8 * nt + r) * ldb + 4 * kc + kq] : B[(4 * kc + kq) * ldb + 8 * nt + r];
+#pragma unroll
+    for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < NT; ++nt) dmma(acc[mt][nt], a[mt], b[nt]);
+  }
+}
+
+template <int MT, int NT>
+__device__ __forceinline__ void zero_tiles(double (&acc)[MT][NT][2]) {
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
+}
+
+// Store rows [0, rows) of the tiles at O + row_off * ldo (ldo even: 16-byte stores).
+template <int MT, int NT>
+__device__ __forceinline__ void store_tiles(const double (&acc)[MT][NT][2], double* O, int ldo, int rows, int lane) {
+  const int r = lane >> 2, c = 2 * (lane & 3);
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int nt = 0; nt < NT; ++nt)
+      if (8 * mt + r < rows)
+        *reinterpret_cast<double2*>(O + (8 * mt + r) * ldo + 8 * nt + c) = make_double2(acc[mt][nt][0], acc[mt][nt][1]);
+}
+
+__device__ __forceinline__ const double* nbr_vals(const DevSys& s, const double* vin, const double* halo, int nbr,
+                                                  int qq) {
+  return nbr < s.n_local ? vin + size_t(nbr) * qq : halo + size_t(nbr - s.n_local) * qq;
+}
+
+template <int Q, int MU>
+struct JvMmaLayout {
+  static constexpr int QP = p8(Q), MP = p8(MU), KQ = p4(Q), KM = p4(MU), K2 = p4(2 * MU);
+  static constexpr int NT1 = p8(MU + 6);  // t / vals columns: MU + 6 spare (2 own x layers, 4 neighbour layers)
+  static constexpr int LV = lda4(KQ), LG = lda4(KQ), LT = ldb8(NT1), LVAL = lda4(NT1), LMF = lda4(K2),
+                       LAB = ldb8(QP), LW5 = lda4(K2), LWG = lda4(KM);
+  static constexpr int GROWS = NT1 > MP ? NT1 : MP;
+  // CTA-shared weights
+  static constexpr int w_G = 0;                       // G (GROWS x LG), zero padded
+  static constexpr int w_W5 = w_G + GROWS * LG;       // [GW | DW] (QP x LW5), zero padded
+  static constexpr int w_WG = w_W5 + QP * LW5;        // GW (QP x LWG), columns >= MU zero
+  static constexpr int weights = (w_WG + QP * LWG + 1) & ~1;
+  // per-warp workspace: region 0 = v, t (early) / [A ; B] (late); vals/F1; [M | F0]; faces
+  static constexpr int e_v = 0;
+  static constexpr int e_t = e_v + QP * LV;
+  static constexpr int r0_early = e_t + KQ * LT;
+  static constexpr int r0_late = K2 * LAB;
+  static constexpr int r0 = ((r0_early > r0_late ? r0_early : r0_late) + 1) & ~1;
+  static constexpr int e_val = r0;
+  static constexpr int e_mf = e_val + MP * LVAL;
+  static constexpr int e_g = e_mf + MP * LMF;          // g[4][MU]
+  static constexpr int e_lift = e_g + 4 * MU;          // lift vectors [4][Q]
+  static constexpr int per_warp = (e_lift + 4 * Q + 1) & ~1;
+  static constexpr int budget = (227 * 1024) / 8 - weights - 16;
+  static constexpr int warps = budget / per_warp > 8 ? 8 : budget / per_warp;
+};
+
+template <int Q, int MU>
+__global__ void __launch_bounds__(256) jv2d_mma_kernel(DevSys s, const double* __restrict__ vin,
+                                                        const double* __restrict__ halo, double* __restrict__ vout) {
+  if (s.skip && *s.skip) return;
+  using L = JvMmaLayout<Q, MU>;
+  constexpr int QP = L::QP, MP = L::MP, KQ = L::KQ, KM = L::KM, K2 = L::K2, NT1 = L::NT1;
+  constexpr int LV = L::LV, LG = L::LG, LT = L::LT, LVAL = L::LVAL, LMF = L::LMF, LAB = L::LAB, LW5 = L::LW5,
+                LWG = L::LWG, NW = L::warps, QQ = Q * Q, MM = MU * MU;
+  extern __shared__ double sm[];
+  double* W = sm;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int i = threadIdx.x; i < L::weights; i += blockDim.x) W[i] = 0.0;
+  __syncthreads();
+  for (int i = threadIdx.x; i < MU * Q; i += blockDim.x) {
+    const int a = i / Q, j = i % Q;
+    W[L::w_G + a * LG + j] = s.g[i];                   // G[a][j]
+    W[L::w_W5 + j * LW5 + a] = s.gw[j * MU + a];       // GW[j][a]
+    W[L::w_W5 + j * LW5 + MU + a] = s.dw[j * MU + a];  // DW[j][a]
+    W[L::w_WG + j * LWG + a] = s.gw[j * MU + a];
+  }
+  double* E = sm + L::weights + warp * L::per_warp;
+  for (int i = lane; i < L::per_warp; i += 32) E[i] = 0.0;  // zero pads (rows / columns never written)
+  __syncthreads();
+  if (warp >= NW) return;
+  const double* G = W + L::w_G;
+  const double* W5 = W + L::w_W5;
+  const double* WG = W + L::w_WG;
+  double* sv = E + L::e_v;
+  double* st = E + L::e_t;
+  double* sab = E;
+  double* sval = E + L::e_val;
+  double* smf = E + L::e_mf;
+  double* sg = E + L::e_g;
+  double* slift = E + L::e_lift;
+  const int r = lane >> 2, c2 = 2 * (lane & 3);
+
+  for (int e = blockIdx.x * NW + warp; e < s.n_local; e += gridDim.x * NW) {
+    // neighbour face layers (registers, consumed after step 1): 4 faces x Q values
+    constexpr int NL = (4 * Q + 31) / 32;
+    double nl[NL];
+#pragma unroll
+    for (int u = 0; u < NL; ++u) {
+      const int idx = lane + 32 * u;
+      double x = 0.0;
+      if (idx < 4 * Q) {
+        const int f = idx / Q, j = idx % Q;
+        const int* fc = s.conn + (size_t(e) * 4 + f) * 3;
+        if (fc[0] >= 0) {
+          const int nf = fc[1], layer = (nf % 2) == 0 ? 0 : Q - 1;
+          const double* cf = nbr_vals(s, vin, halo, fc[0], QQ);
+          x = nf / 2 == 0 ? cf[j * Q + layer] : cf[layer * Q + j];
+        }
+      }
+      nl[u] = x;
+    }
+    const double* ve = vin + size_t(e) * QQ;
+    for (int i = lane; i < QQ; i += 32) sv[(i / Q) * LV + i % Q] = ve[i];
+    __syncwarp();
+    {  // (1) t = v G^T
+      double acc[QP / 8][NT1 / 8][2];
+      zero_tiles(acc);
+      mma_tiles<QP / 8, NT1 / 8, KQ / 4, true>(acc, sv, LV, G, LG, lane);
+      store_tiles(acc, st, LT, KQ, lane);
+    }
+    __syncwarp();
+    for (int j = lane; j < Q; j += 32) {  // spare columns: own x-face layers
+      st[j * LT + MU] = sv[j * LV];
+      st[j * LT + MU + 1] = sv[j * LV + Q - 1];
+    }
+#pragma unroll
+    for (int u = 0; u < NL; ++u) {
+      const int idx = lane + 32 * u;
+      if (idx < 4 * Q) st[(idx % Q) * LT + MU + 2 + idx / Q] = nl[u];
+    }
+    __syncwarp();
+    {  // (2) vals = G t
+      double acc[MP / 8][NT1 / 8][2];
+      zero_tiles(acc);
+      mma_tiles<MP / 8, NT1 / 8, KQ / 4, false>(acc, G, LG, st, LT, lane);
+      store_tiles(acc, sval, LVAL, MP, lane);
+    }
+    __syncwarp();
+    // face data g[f][a] = -b fw (dfm tm + dfp tp)
+    for (int idx = lane; idx < 4 * MU; idx += 32) {
+      const int a = idx % MU, f = idx / MU;
+      const int* fc = s.conn + (size_t(e) * 4 + f) * 3;
+      const double tm = f < 2 ? sval[a * LVAL + MU + f] : st[(f == 2 ? 0 : Q - 1) * LT + a];
+      double tp = 0.0;
+      if (fc[0] >= 0) tp = sval[(fc[2] == 0 ? a : MU - 1 - a) * LVAL + MU + 2 + f];
+      const size_t fq = (size_t(e) * 4 + f) * MU + a;
+      sg[idx] = -s.b * s.face_w[fq] * fma(s.dfm[fq], tm, s.dfp[fq] * tp);
+    }
+    // point-wise fields: [M | F0] -> smf, F1 -> vals in place
+    {
+      const double* jd = s.jdet + size_t(e) * MM;
+      const double* d0 = s.dft + size_t(e) * 2 * MM;
+      const double* d1 = d0 + MM;
+      for (int qv = lane; qv < MM; qv += 32) {
+        const int be = qv / MU, al = qv % MU;
+        const double x = sval[be * LVAL + al];
+        smf[be * LMF + al] = s.a * jd[qv] * x;
+        smf[be * LMF + MU + al] = s.b * (d0[qv] * x);
+        sval[be * LVAL + al] = s.b * (d1[qv] * x);
+      }
+    }
+    __syncwarp();
+    // lift vectors: x faces Lf[j] = sum_a G[a][j] g[f][a]; y faces the same over i
+    for (int idx = lane; idx < 4 * Q; idx += 32) {
+      const int f = idx / Q, j = idx % Q;
+      double acc = 0.0;
+      for (int a = 0; a < MU; ++a) acc = fma(G[a * LG + j], sg[f * MU + a], acc);
+      slift[idx] = acc;
+    }
+    {  // (3) A = [M | F0] [GW^T ; DW^T] -> rows 0..MU-1 of [A ; B]; (4) B = F1 GW^T -> rows MU..2MU-1
+      double acc[MP / 8][QP / 8][2];
+      zero_tiles(acc);
+      mma_tiles<MP / 8, QP / 8, K2 / 4, true>(acc, smf, LMF, W5, LW5, lane);
+      double acc4[MP / 8][QP / 8][2];
+      zero_tiles(acc4);
+      mma_tiles<MP / 8, QP / 8, KM / 4, true>(acc4, sval, LVAL, WG, LWG, lane);
+      store_tiles(acc, sab, LAB, MU, lane);
+      store_tiles(acc4, sab + MU * LAB, LAB, MU, lane);
+    }
+    __syncwarp();
+    {  // (5) out = [GW | DW] [A ; B] + lifts
+      double acc[QP / 8][QP / 8][2];
+      zero_tiles(acc);
+      mma_tiles<QP / 8, QP / 8, K2 / 4, false>(acc, W5, LW5, sab, LAB, lane);
+      double* oe = vout + size_t(e) * QQ;
+#pragma unroll
+      for (int mt = 0; mt < QP / 8; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < QP / 8; ++nt) {
+          const int j = 8 * mt + r;
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int i = 8 * nt + c2 + u;
+            if (j < Q && i < Q) {
+              double x = acc[mt][nt][u];
+              if (i == 0) x += slift[0 * Q + j];
+              if (i == Q - 1) x += slift[1 * Q + j];
+              if (j == 0) x += slift[2 * Q + i];
+              if (j == Q - 1) x += slift[3 * Q + i];
+              oe[j * Q + i] = x;
+            }
+          }
+        }
+    }
+    __syncwarp();
+  }
+}
+
+template <int Q, int MU>
+bool try_jv2d_mma(const DevSys& s, const double* vin, const double* halo, double* vout, cudaStream_t st) {
+  if (s.dim != 2 || s.n_c != 1 || s.q != Q || s.mu != MU) return false;
+  using L = JvMmaLayout<Q, MU>;
+  static_assert(L::warps >= 1, "element workspace exceeds shared memory");
+  const size_t smem = sizeof(double) * size_t(L::weights + L::warps * L::per_warp);
+  static int grid = 0;
+  if (!grid) {
+    TPDG_CUDA_CHECK(cudaFuncSetAttribute(jv2d_mma_kernel<Q, MU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(smem)));
+    TPDG_CUDA_CHECK(cudaFuncSetAttribute(jv2d_mma_kernel<Q, MU>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                         100));
+    int per_sm = 0;
+    TPDG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jv2d_mma_kernel<Q, MU>, 32 * L::warps,
+                                                                  smem));
+    int dev = 0, sms = 0;
+    TPDG_CUDA_CHECK(cudaGetDevice(&dev));
+    TPDG_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    grid = std::max(1, per_sm) * sms;
+  }
+  const int need = (s.n_local + L::warps - 1) / L::warps;
+  jv2d_mma_kernel<Q, MU><<<std::min(grid, need), 32 * L::warps, smem, st>>>(s, vin, halo, vout);
+  return true;
+}
+
+} // namespace
+
+bool launch_jv2d_mma(const DevSys& s, const double* vin, const double* halo, double* vout, cudaStream_t st) {
+  return try_jv2d_mma<5, 6>(s, vin, halo, vout, st) || try_jv2d_mma<9, 10>(s, vin, halo, vout, st) ||
+         try_jv2d_mma<16, 17>(s, vin, halo, vout, st) || try_jv2d_mma<21, 22>(s, vin, halo, vout, st) ||
+         try_jv2d_mma<31, 32>(s, vin, halo, vout, st);
+}
+
+} // namespace tpdg_gpu

@@ -98,6 +98,7 @@ __host__ __device__ inline int raw_len_of(int dim, int n1, int q) { return dim =
 
 // ---------------------------------------------------------------- kernel launchers
 void launch_jv(const DevSys& s, const double* vin, const double* halo, double* vout, cudaStream_t st);
+bool launch_jv2d_mma(const DevSys& s, const double* vin, const double* halo, double* vout, cudaStream_t st);
 size_t jv_smem_bytes(const DevSys& s);
 void launch_pc_apply(const DevPC& pc, const double* in, double* out, cudaStream_t st);
 // Factor the data-independent tiny Sylvester systems of every Kronecker block into pc.cells.
