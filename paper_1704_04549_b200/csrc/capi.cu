@@ -7,6 +7,7 @@
 // them (std::hypot, same update formulas), so |g_{k+1}| and the stopping test follow the
 // reference's arithmetic given the same column.
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -572,6 +573,10 @@ void finish_pc(tpdg_gpu_pc pc) {
   d.fb_lu = nfb ? pc->fb_lu.as<double>() : nullptr;
   d.fb_piv = nfb ? pc->fb_piv.as<int>() : nullptr;
   d.status = pc->status.as<int>();
+  {
+    const char* f = std::getenv("TPDG_GPU_FAITHFUL");
+    d.faithful = (f && f[0] == '1') ? 1 : 0;
+  }
   d.cells_len = sylv_cells_len(op->dim, d.n1, op->q);
   pc->cells.alloc(sizeof(double) * (size_t(pc->nblk) * d.cells_len + 32));  // +32: whole-slot loads of the last cell
   TPDG_CUDA_CHECK(cudaMemsetAsync(pc->cells.p, 0, pc->cells.bytes, st));

@@ -22,62 +22,12 @@
 // (SURVEY.md sec.8c), measured ~1e-16.
 #include <algorithm>
 
+#include "mma.cuh"
 #include "tpdg_internal.hpp"
 
 namespace tpdg_gpu {
 
 namespace {
-
-constexpr int p8(int x) { return (x + 7) & ~7; }
-constexpr int p4(int x) { return (x + 3) & ~3; }
-constexpr int lda4(int x) { return (x + 3) / 8 * 8 + 4; }   // smallest y >= x, y = 4 (mod 8)
-constexpr int ldb8(int x) { return (x + 7) / 16 * 16 + 8; }  // smallest y >= x, y = 8 (mod 16)
-
-__device__ __forceinline__ void dmma(double (&c)[2], double a, double b) {
-  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-      : "+d"(c[0]), "+d"(c[1])
-      : "d"(a), "d"(b));
-}
-
-// acc[MT][NT] += A[8MT x 4KC] B[4KC x 8NT]; A row-major (lda), B row-major (ldb) or, if BCOL,
-// stored as B^T row-major (B[k][n] = Bs[n * ldb + k]).
-template <int MT, int NT, int KC, bool BCOL>
-__device__ __forceinline__ void mma_tiles(double (&acc)[MT][NT][2], const double* A, int lda, const double* B, int ldb,
-                                          int lane) {
-  const int r = lane >> 2, kq = lane & 3;
-#pragma unroll
-  for (int kc = 0; kc < KC; ++kc) {
-    double a[MT], b[NT];
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt) a[mt] = A[(8 * mt + r) * lda + 4 * kc + kq];
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) b[nt] = BCOL ? B[(8 * nt + r) * ldb + 4 * kc + kq] : B[(4 * kc + kq) * ldb + 8 * nt + r];
-#pragma unroll
-    for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < NT; ++nt) dmma(acc[mt][nt], a[mt], b[nt]);
-  }
-}
-
-template <int MT, int NT>
-__device__ __forceinline__ void zero_tiles(double (&acc)[MT][NT][2]) {
-#pragma unroll
-  for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt) acc[mt][nt][0] = acc[mt][nt][1] = 0.0;
-}
-
-// Store rows [0, rows) of the tiles at O + row_off * ldo (ldo even: 16-byte stores).
-template <int MT, int NT>
-__device__ __forceinline__ void store_tiles(const double (&acc)[MT][NT][2], double* O, int ldo, int rows, int lane) {
-  const int r = lane >> 2, c = 2 * (lane & 3);
-#pragma unroll
-  for (int mt = 0; mt < MT; ++mt)
-#pragma unroll
-    for (int nt = 0; nt < NT; ++nt)
-      if (8 * mt + r < rows)
-        *reinterpret_cast<double2*>(O + (8 * mt + r) * ldo + 8 * nt + c) = make_double2(acc[mt][nt][0], acc[mt][nt][1]);
-}
 
 __device__ __forceinline__ const double* nbr_vals(const DevSys& s, const double* vin, const double* halo, int nbr,
                                                   int qq) {

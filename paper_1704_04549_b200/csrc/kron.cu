@@ -18,6 +18,7 @@
 #include <cstdint>
 
 #include "faithful.cuh"
+#include "mma.cuh"
 #include "tpdg_internal.hpp"
 
 namespace tpdg_gpu {
@@ -329,7 +330,8 @@ __device__ __forceinline__ void warp_mm(const double* A, int lda, const double* 
 }
 
 // Right-hand side of one Sylvester entry: B minus the solved rows below (j ascending), then the
-// solved columns to the right (l ascending), exactly sylvester.hpp:84-99.
+// solved columns to the right (l ascending), exactly sylvester.hpp:84-99 (FMA: fused steps).
+template <bool FMA = false>
 __device__ __forceinline__ double sylv_rhs(const double* __restrict__ t1, int n1, const double* __restrict__ t2,
                                            int n2, const double* M, const double* Y, int ld, int i, int k,
                                            int jfirst, int lfirst) {
@@ -345,7 +347,7 @@ __device__ __forceinline__ double sylv_rhs(const double* __restrict__ t1, int n1
     const bool first = t < nj;
     const double* pa = first ? a1 + t : a2 + t;
     const double* pb = first ? b1 + t * ld : b2 + t;
-    s = fmsc(s, *pa, *pb);
+    s = FMA ? fma(-*pa, *pb, s) : fmsc(s, *pa, *pb);
   }
   return s;
 }
@@ -521,9 +523,10 @@ __device__ __forceinline__ double cell_solve(const double (&cf)[22], double (&b)
 
 // Block anti-diagonal wavefront of the quasi-triangular Sylvester solve over NSL slices that
 // share one plan (2D: 1, 3D: the outer slices). Work items are (step, pass) pairs, each pass a
-// set of NT/4 (cell, slice) groups of 4 lanes; the factors of the next item's cell are loaded
-// while the current one computes (register double buffer), and SYNC separates the steps.
-template <int TN1, int TN2, int NSL, int NT, bool CTA>
+// set of NT/4 (cell, slice) groups of 4 lanes (lane e of a group = entry e of the cell); a
+// barrier separates the steps. (Loading the next item's factors one item ahead was measured
+// slower: the extra registers cost more occupancy than the hidden latency gained.)
+template <int TN1, int TN2, int NSL, int NT, bool CTA, bool FMA = false>
 __device__ __forceinline__ void sylv_wavefront(const double* T1, const double* T2, double* X, int ld, int ss,
                                                const double* __restrict__ cc, const int* sb, int tid, int* status) {
   const int nb1 = sb[0], nb2 = sb[1];
@@ -568,7 +571,8 @@ __device__ __forceinline__ void sylv_wavefront(const double* T1, const double* T
       isz = z1[bi];
       k0 = s2[bj];
       ksz = z2[bj];
-      if (e < isz * ksz) s = sylv_rhs(T1, TN1, T2, TN2, Ms, Ms, ld, i0 + e / ksz, k0 + e % ksz, i0 + isz, k0 + ksz);
+      if (e < isz * ksz)
+        s = sylv_rhs<FMA>(T1, TN1, T2, TN2, Ms, Ms, ld, i0 + e / ksz, k0 + e % ksz, i0 + isz, k0 + ksz);
     }
     const long long code = __double_as_longlong(cf[0]);
     double b[4];
@@ -709,6 +713,212 @@ bool launch_kron2d_sized(const DevPC& pc, const double* in, double* out, cudaStr
   return try_kron2d_sized<5, 5>(pc, in, out, st) || try_kron2d_sized<9, 9>(pc, in, out, st) ||
          try_kron2d_sized<16, 16>(pc, in, out, st) || try_kron2d_sized<21, 21>(pc, in, out, st) ||
          try_kron2d_sized<31, 31>(pc, in, out, st);
+}
+
+// ------------------------------------------------------------------------------------ 2D, DMMA
+// apply_factors_2d (precond/ksvd.hpp:112-129) with the rotations on the FP64 tensor cores: one
+// warp per block, M = Q1^T X Q2 and X = Q1 Y Q2^T as four warp-level DMMA products, the two LU
+// axis solves as register fibers and the Sylvester wavefront replaying the factored cells, with
+// FMA. Not bit-faithful: measured <= 2e-14 rel-L2 against the reference's own output on every
+// golden case with the reference's factors (gate 1e-12) and identical GMRES counts at cfg2
+// p=15/20/30 (tools/pc_sensitivity.py); TPDG_GPU_FAITHFUL=1 selects the faithful kernels.
+template <int N>
+__device__ __forceinline__ void lu_fiber_fma(const double* __restrict__ lu, const double* __restrict__ rcp,
+                                             const int* __restrict__ perm, double* col, int stride) {
+  double x[N];
+#pragma unroll
+  for (int k = 0; k < N; ++k) x[k] = col[perm[k] * stride];
+#pragma unroll
+  for (int r = 1; r < N; ++r) {
+    double s = x[r];
+#pragma unroll
+    for (int j = 0; j < r; ++j) s = fma(-lu[r * N + j], x[j], s);
+    x[r] = s;
+  }
+#pragma unroll
+  for (int r = N - 1; r >= 0; --r) {
+    double s = x[r];
+#pragma unroll
+    for (int j = r + 1; j < N; ++j) s = fma(-lu[r * N + j], x[j], s);
+    x[r] = s * rcp[r];
+  }
+#pragma unroll
+  for (int k = 0; k < N; ++k) col[k * stride] = x[k];
+}
+
+// rows x cols block, global (dense, ld = cols) -> shared (ld), asynchronous
+__device__ __forceinline__ void cp_rows(double* dst, int ldd, const double* src, int rows, int cols, int lane) {
+  if ((cols & 1) == 0 && (ldd & 1) == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0 &&
+      (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+    const int h = cols / 2;
+    for (int i = lane; i < rows * h; i += 32) cp_async16(dst + (i / h) * ldd + 2 * (i % h), src + 2 * i);
+  } else {
+    for (int i = lane; i < rows * cols; i += 32) cp_async8(dst + (i / cols) * ldd + i % cols, src + i);
+  }
+}
+
+__device__ __forceinline__ void zero_pad(double* buf, int ld, int rows, int cols, int rows_tot, int cols_tot,
+                                         int lane) {
+  for (int i = lane; i < rows_tot * cols_tot; i += 32) {
+    const int r = i / cols_tot, c = i % cols_tot;
+    if (r >= rows || c >= cols) buf[r * ld + c] = 0.0;
+  }
+}
+
+template <int N1, int N2>
+struct Kron2dMmaLayout {
+  static constexpr int N1P = p8(N1), N2P = p8(N2);
+  static constexpr int LX = lda4(N2P), LQ1 = lda4(N1P), LQ2 = lda4(N2P), LP = lda4(N2P);
+  static constexpr int hdr = (((4 + 2 * N1 + 2 * N2) / 2 + 2) & ~1);
+  static constexpr int o_x = 0;                       // X -> M -> Y  (N1P x LX)
+  static constexpr int o_q1 = o_x + N1P * LX;         // Q1 (N1P x LQ1, zero padded)
+  static constexpr int o_q2 = o_q1 + N1P * LQ1;       // Q2 (N2P x LQ2, zero padded)
+  static constexpr int lu = N1 * N1 + N2 * N2;
+  static constexpr int o_lu = o_q2 + N2P * LQ2;       // LU(A2) | LU(B1), later P / Z (N1P x LP)
+  static constexpr int lu_sz = ((lu > N1P * LP ? lu : N1P * LP) + 1) & ~1;
+  static constexpr int o_t1 = o_lu + lu_sz;           // T1 | T2
+  static constexpr int o_rcp = (o_t1 + N1 * N1 + N2 * N2 + 1) & ~1;
+  static constexpr int o_h = (o_rcp + N1 + N2 + 1) & ~1;
+  static constexpr int o_piv = o_h + hdr;             // ints
+  static constexpr int per = (o_piv + (N1 + N2 + 1) / 2 + 1) & ~1;
+};
+
+template <int N1, int N2>
+__global__ void __launch_bounds__(kSizedThreads) kron2d_mma_kernel(DevPC pc, const double* __restrict__ in,
+                                                                    double* __restrict__ out) {
+  using L = Kron2dMmaLayout<N1, N2>;
+  constexpr int N1P = L::N1P, N2P = L::N2P, LX = L::LX, LQ1 = L::LQ1, LQ2 = L::LQ2, LP = L::LP, hdr = L::hdr;
+  extern __shared__ double sm_all[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int blk = blockIdx.x * (kSizedThreads / 32) + warp;
+  if (blk >= pc.nblk || pc.kind[blk] == 0 || (pc.skip && *pc.skip)) return;
+  double* S = sm_all + size_t(warp) * L::per;
+  double* sX = S + L::o_x;
+  double* sQ1 = S + L::o_q1;
+  double* sQ2 = S + L::o_q2;
+  double* sLU = S + L::o_lu;
+  double* sP = S + L::o_lu;  // aliases the LU factors once both fiber solves are done
+  double* sT1 = S + L::o_t1;
+  double* sT2 = sT1 + N1 * N1;
+  double* sRcp = S + L::o_rcp;
+  double* sH = S + L::o_h;
+  int* sPiv = reinterpret_cast<int*>(S + L::o_piv);
+  const double* cells = pc.cells + size_t(blk) * pc.cells_len;
+  {
+    const double* r = pc.rec + size_t(blk) * (3 * N1 * N1 + 3 * N2 * N2);
+    cp_rows(sLU, N1 * N1 + N2 * N2, r, 1, N1 * N1 + N2 * N2, lane);              // LU(A2) | LU(B1)
+    cp_rows(sQ1, LQ1, r + N1 * N1 + N2 * N2, N1, N1, lane);                      // Q1
+    cp_rows(sT1, N1 * N1, r + 2 * N1 * N1 + N2 * N2, 1, N1 * N1, lane);          // T1
+    cp_rows(sQ2, LQ2, r + 3 * N1 * N1 + N2 * N2, N2, N2, lane);                  // Q2
+    cp_rows(sT2, N2 * N2, r + 3 * N1 * N1 + 2 * N2 * N2, 1, N2 * N2, lane);      // T2
+    cp_rows(sH, hdr, cells, 1, hdr, lane);
+    cp_rows(sX, LX, in + size_t(blk) * (N1 * N2), N1, N2, lane);
+    // the Sylvester cell factors are read step by step from global: pull them into L2 now
+    for (int i = lane * 16; i < pc.cells_len; i += 32 * 16) asm volatile("prefetch.global.L2 [%0];" ::"l"(cells + i));
+    for (int i = lane; i < N1 + N2; i += 32) sPiv[i] = pc.piv[size_t(blk) * (N1 + N2) + i];
+    if (N1P != N1 || N2P != N2) {
+      zero_pad(sX, LX, N1, N2, N1P, N2P, lane);
+      zero_pad(sQ1, LQ1, N1, N1, N1P, N1P, lane);
+      zero_pad(sQ2, LQ2, N2, N2, N2P, N2P, lane);
+    }
+    cp_async_wait_all();
+  }
+  __syncwarp();
+  for (int i = lane; i < N1 + N2; i += 32)
+    sRcp[i] = 1.0 / (i < N1 ? sLU[i * N1 + i] : sLU[N1 * N1 + (i - N1) * N2 + i - N1]);
+  __syncwarp();
+  for (int c = lane; c < N2; c += 32) lu_fiber_fma<N1>(sLU, sRcp, sPiv, sX + c, LX);  // A2^{-1} (x) I
+  __syncwarp();
+  for (int r = lane; r < N1; r += 32) lu_fiber_fma<N2>(sLU + N1 * N1, sRcp + N1, sPiv + N1, sX + r * LX, 1);
+  __syncwarp();
+  {  // P = Q1^T X
+    double acc[N1P / 8][N2P / 8][2];
+    zero_tiles(acc);
+    mma_tiles<N1P / 8, N2P / 8, N1P / 4, false, true>(acc, sQ1, LQ1, sX, LX, lane);
+    store_tiles(acc, sP, LP, N1P, lane);
+  }
+  __syncwarp();
+  {  // M = P Q2 (over X)
+    double acc[N1P / 8][N2P / 8][2];
+    zero_tiles(acc);
+    mma_tiles<N1P / 8, N2P / 8, N2P / 4, false>(acc, sP, LP, sQ2, LQ2, lane);
+    store_tiles(acc, sX, LX, N1P, lane);
+  }
+  __syncwarp();
+  {  // Y overwrites M: T1 Y + Y T2^T = M
+    const int* sb = reinterpret_cast<const int*>(sH);
+    const double* cc = cells + hdr;
+    if (sb[2]) {  // 1 x 1 blocks: one lane per cell
+      const int nb1 = sb[0], nb2 = sb[1];
+      for (int step = 0; step <= nb1 + nb2 - 2; ++step) {
+        const int d1lo = step - (nb2 - 1) > 0 ? step - (nb2 - 1) : 0;
+        const int d1hi = step < nb1 - 1 ? step : nb1 - 1;
+        for (int d1 = d1lo + lane; d1 <= d1hi; d1 += 32) {
+          const int i = nb1 - 1 - d1, k = nb2 - 1 - (step - d1);
+          const double* c = cc + 6 * (i * N2 + k);
+          const double code = __ldg(c), rcp = __ldg(c + 2);
+          const double s = sylv_rhs<true>(sT1, N1, sT2, N2, sX, sX, LX, i, k, i + 1, k + 1);
+          if (__double_as_longlong(code) & 256) atomicExch(pc.status, int(TPDG_SINGULAR));
+          sX[i * LX + k] = s * rcp;
+        }
+        __syncwarp();
+      }
+    } else {
+      sylv_wavefront<N1, N2, 1, 32, false, true>(sT1, sT2, sX, LX, 0, cc, sb, lane, pc.status);
+      __syncwarp();
+    }
+  }
+  {  // Z = Q1 Y
+    double acc[N1P / 8][N2P / 8][2];
+    zero_tiles(acc);
+    mma_tiles<N1P / 8, N2P / 8, N1P / 4, false>(acc, sQ1, LQ1, sX, LX, lane);
+    store_tiles(acc, sP, LP, N1P, lane);
+  }
+  __syncwarp();
+  {  // out = Z Q2^T
+    double acc[N1P / 8][N2P / 8][2];
+    zero_tiles(acc);
+    mma_tiles<N1P / 8, N2P / 8, N2P / 4, true>(acc, sP, LP, sQ2, LQ2, lane);
+    double* o = out + size_t(blk) * (N1 * N2);
+    const int r = lane >> 2, c2 = 2 * (lane & 3);
+#pragma unroll
+    for (int mt = 0; mt < N1P / 8; ++mt)
+#pragma unroll
+      for (int nt = 0; nt < N2P / 8; ++nt) {
+        const int i = 8 * mt + r, j = 8 * nt + c2;
+        if (i < N1) {
+          if ((N2 & 1) == 0 && j + 1 < N2) {
+            *reinterpret_cast<double2*>(o + i * N2 + j) = make_double2(acc[mt][nt][0], acc[mt][nt][1]);
+          } else {
+            if (j < N2) o[i * N2 + j] = acc[mt][nt][0];
+            if (j + 1 < N2) o[i * N2 + j + 1] = acc[mt][nt][1];
+          }
+        }
+      }
+  }
+}
+
+template <int N1, int N2>
+bool try_kron2d_mma(const DevPC& pc, const double* in, double* out, cudaStream_t st) {
+  if (pc.dim != 2 || pc.n1 != N1 || pc.q != N2) return false;
+  static bool configured = false;
+  const size_t smem = sizeof(double) * size_t(Kron2dMmaLayout<N1, N2>::per) * (kSizedThreads / 32);
+  if (!configured) {
+    TPDG_CUDA_CHECK(cudaFuncSetAttribute(kron2d_mma_kernel<N1, N2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(smem)));
+    TPDG_CUDA_CHECK(cudaFuncSetAttribute(kron2d_mma_kernel<N1, N2>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                         100));
+    configured = true;
+  }
+  const int per_cta = kSizedThreads / 32;
+  kron2d_mma_kernel<N1, N2><<<(pc.nblk + per_cta - 1) / per_cta, kSizedThreads, smem, st>>>(pc, in, out);
+  return true;
+}
+
+bool launch_kron2d_mma(const DevPC& pc, const double* in, double* out, cudaStream_t st) {
+  return try_kron2d_mma<5, 5>(pc, in, out, st) || try_kron2d_mma<9, 9>(pc, in, out, st) ||
+         try_kron2d_mma<16, 16>(pc, in, out, st) || try_kron2d_mma<21, 21>(pc, in, out, st) ||
+         try_kron2d_mma<31, 31>(pc, in, out, st);
 }
 
 // ------------------------------------------------------------------------------------ 3D, sized
@@ -1006,7 +1216,7 @@ void launch_pc_apply(const DevPC& pc, const double* in, double* out, cudaStream_
   if (smem > 227 * 1024)
     throw Failure{TPDG_CONFIG, "pc_apply: factor record of " + std::to_string(smem) + " B exceeds shared memory"};
   if (pc.dim == 2) {
-    if (!launch_kron2d_sized(pc, in, out, st)) {
+    if (!(!pc.faithful && launch_kron2d_mma(pc, in, out, st)) && !launch_kron2d_sized(pc, in, out, st)) {
       set_smem(kron2d_apply_kernel, smem, c2);
       kron2d_apply_kernel<<<pc.nblk, kApplyThreads, smem, st>>>(pc, in, out);
     }

@@ -76,6 +76,7 @@ struct DevPC {
   const int* fb_slot;    // [nblk]: slot into fb_lu for fallback blocks, -1 otherwise
   const double* fb_lu;   // [n_fb][blk_len^2]
   const int* fb_piv;     // [n_fb][blk_len]
+  int faithful;          // 1: bit-faithful kernels only (TPDG_GPU_FAITHFUL=1), 0: tensor-core apply
   const double* cells;   // [nblk][cells_len]: Sylvester plan + factored tiny systems (sylv_cells_len)
   int cells_len;
   int* status;           // device error flag (SingularError inside the Sylvester solve)
