@@ -166,7 +166,7 @@ struct tpdg_gpu_pc_s {
   tpdg_gpu_op op = nullptr;
   DevPC pc{};
   int nblk = 0, raw_len = 0;
-  DevBuf raw, rec, piv, kind, fb_slot, fb_lu, fb_piv, status, cells;
+  DevBuf raw, rec, piv, kind, fb_slot, fb_lu, fb_piv, status, cells, cinv;
   std::vector<int> kind_h;
   std::vector<int64_t> fallbacks;  // (element, component)
 };
@@ -581,7 +581,14 @@ void finish_pc(tpdg_gpu_pc pc) {
   pc->cells.alloc(sizeof(double) * (size_t(pc->nblk) * d.cells_len + 32));  // +32: whole-slot loads of the last cell
   TPDG_CUDA_CHECK(cudaMemsetAsync(pc->cells.p, 0, pc->cells.bytes, st));
   d.cells = pc->cells.as<double>();
-  launch_sylv_cells(d, pc->cells.as<double>(), st);
+  d.cinv = nullptr;
+  if (!d.faithful) {
+    const int t1 = op->dim == 2 ? d.n1 : op->q;
+    pc->cinv.alloc(sizeof(double) * size_t(pc->nblk) * 4 * t1 * op->q);
+    TPDG_CUDA_CHECK(cudaMemsetAsync(pc->cinv.p, 0, pc->cinv.bytes, st));
+    d.cinv = pc->cinv.as<double>();
+  }
+  launch_sylv_cells(d, pc->cells.as<double>(), pc->cinv.as<double>(), st);
   TPDG_CUDA_CHECK(cudaStreamSynchronize(st));
 }
 

@@ -445,9 +445,37 @@ __device__ void factor_cell(const double* t1, int n1, const double* t2, int n2, 
   for (int i = 0; i < NS; ++i) c[o + NS + i] = __drcp_rn(a[i][i]);
 }
 
+// Replays a factored cell on the permuted right-hand side b (b[u] = r[perm[u]]); returns entry e.
+template <int NS>
+__device__ __forceinline__ double cell_solve(const double (&cf)[22], double (&b)[4], int e) {
+  constexpr int NL = NS * (NS - 1) / 2;
+  int o = 1;
+#pragma unroll
+  for (int i = 1; i < NS; ++i)
+#pragma unroll
+    for (int j = 0; j < i; ++j) {
+      const double m = cf[o++];
+      b[i] = m != 0.0 ? fmsc(b[i], m, b[j]) : b[i];
+    }
+#pragma unroll
+  for (int i = NS - 1; i >= 0; --i) {
+    int u = 1 + NL;
+#pragma unroll
+    for (int r = 0; r < i; ++r) u += NS - 1 - r;
+#pragma unroll
+    for (int j = i + 1; j < NS; ++j) b[i] = fmsc(b[i], cf[u + j - i - 1], b[j]);
+    b[i] = fdiv_rcp(b[i], cf[1 + 2 * NL + i], cf[1 + 2 * NL + NS + i]);
+  }
+  double y = b[0];
+#pragma unroll
+  for (int t = 1; t < NS; ++t)
+    if (e == t) y = b[t];
+  return y;
+}
+
 // One warp per Kronecker block: lane 0 builds the plan (tol from the row sums, quasi-blocks),
 // the lanes factor the cells.
-__global__ void sylv_cells_kernel(DevPC pc, double* __restrict__ cells) {
+__global__ void sylv_cells_kernel(DevPC pc, double* __restrict__ cells, double* __restrict__ cinv) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= pc.nblk || pc.kind[warp] == 0) return;
   const int t1n = pc.dim == 2 ? pc.n1 : pc.q, t2n = pc.q;
@@ -490,110 +518,145 @@ __global__ void sylv_cells_kernel(DevPC pc, double* __restrict__ cells) {
     else if (code == 1) factor_cell<1, 2>(t1, t1n, t2, t2n, i0, k0, tol, slot);
     else if (code == 2) factor_cell<2, 1>(t1, t1n, t2, t2n, i0, k0, tol, slot);
     else factor_cell<2, 2>(t1, t1n, t2, t2n, i0, k0, tol, slot);
+    const long long cw = __double_as_longlong(slot[0]);
+    if (cw & 256) atomicOr(h + 3, 1);
+    if (cinv) {  // rows of S^{-1} (tensor-core path): column j = replay of the permuted unit vector e_j
+      const int ns = isz * ksz;
+      double cf[22], inv[4][4];
+      for (int u = 0; u < 22; ++u) cf[u] = slot[u];
+      for (int j = 0; j < ns; ++j) {
+        for (int ee = 0; ee < ns; ++ee) {
+          double b[4];
+          for (int u = 0; u < 4; ++u) b[u] = (u < ns && int((cw >> (2 * u)) & 3) == j) ? 1.0 : 0.0;
+          inv[ee][j] = ns == 1 ? b[0] * cf[2] : ns == 2 ? cell_solve<2>(cf, b, ee) : cell_solve<4>(cf, b, ee);
+        }
+      }
+      double* ci = cinv + size_t(warp) * (4 * t1n * t2n);
+      for (int ee = 0; ee < ns; ++ee) {
+        const int x = i0 + ee / ksz, y = k0 + ee % ksz;
+        for (int u = 0; u < 4; ++u) ci[4 * (x * t2n + y) + u] = u < ns ? inv[ee][u] : 0.0;
+      }
+    }
   }
 }
 
-// Replays a factored cell on the permuted right-hand side b (b[u] = r[perm[u]]); returns entry e.
-template <int NS>
-__device__ __forceinline__ double cell_solve(const double (&cf)[22], double (&b)[4], int e) {
-  constexpr int NL = NS * (NS - 1) / 2;
-  int o = 1;
-#pragma unroll
-  for (int i = 1; i < NS; ++i)
-#pragma unroll
-    for (int j = 0; j < i; ++j) {
-      const double m = cf[o++];
-      b[i] = m != 0.0 ? fmsc(b[i], m, b[j]) : b[i];
-    }
-#pragma unroll
-  for (int i = NS - 1; i >= 0; --i) {
-    int u = 1 + NL;
-#pragma unroll
-    for (int r = 0; r < i; ++r) u += NS - 1 - r;
-#pragma unroll
-    for (int j = i + 1; j < NS; ++j) b[i] = fmsc(b[i], cf[u + j - i - 1], b[j]);
-    b[i] = fdiv_rcp(b[i], cf[1 + 2 * NL + i], cf[1 + 2 * NL + NS + i]);
-  }
-  double y = b[0];
-#pragma unroll
-  for (int t = 1; t < NS; ++t)
-    if (e == t) y = b[t];
-  return y;
-}
 
 // Block anti-diagonal wavefront of the quasi-triangular Sylvester solve over NSL slices that
 // share one plan (2D: 1, 3D: the outer slices). Work items are (step, pass) pairs, each pass a
 // set of NT/4 (cell, slice) groups of 4 lanes (lane e of a group = entry e of the cell); a
 // barrier separates the steps. (Loading the next item's factors one item ahead was measured
 // slower: the extra registers cost more occupancy than the hidden latency gained.)
-template <int TN1, int TN2, int NSL, int NT, bool CTA, bool FMA = false>
+template <int TN1, int TN2, int NSL, int NT, bool CTA, bool FMA = false, bool INV = false>
 __device__ __forceinline__ void sylv_wavefront(const double* T1, const double* T2, double* X, int ld, int ss,
                                                const double* __restrict__ cc, const int* sb, int tid, int* status) {
+  // INV: cc = rows of the inverted cell systems, 4 doubles per entry at 4 (x TN2 + y) (sylv_cells_kernel);
+  // else cc = the replay slots of the factored cells.
   const int nb1 = sb[0], nb2 = sb[1];
   const int *s1 = sb + 4, *z1 = s1 + TN1, *s2 = z1 + TN1, *z2 = s2 + TN2;
   const int last = nb1 + nb2 - 2, lane = tid & 31, e = lane & 3, g = lane & ~3;
-  int step = 0, base = 0;
-  double cf[22];
-  int bi = 0, bj = 0, sl = 0;
-  bool ok = false;
-  auto load = [&](int st, int bs, double (&c)[22], int& obi, int& obj, int& osl, bool& ook) {
+  constexpr int NCF = INV ? 4 : 22;
+  struct Item {
+    int bi, bj, sl;
+    bool ok;
+  };
+  auto locate = [&](int st, int bs) {
+    Item it;
     const int d1lo = st - (nb2 - 1) > 0 ? st - (nb2 - 1) : 0;
     const int d1hi = st < nb1 - 1 ? st : nb1 - 1;
     const int ncell = d1hi - d1lo + 1;
     const int grp = (bs + tid) >> 2;
-    ook = grp < ncell * NSL;
-    const int cell = ook ? grp % ncell : 0;
-    osl = ook ? grp / ncell : 0;
+    it.ok = grp < ncell * NSL;
+    const int cell = !it.ok ? 0 : NSL == 1 ? grp : grp % ncell;
+    it.sl = !it.ok || NSL == 1 ? 0 : grp / ncell;
     const int d1 = d1lo + cell;
-    obi = nb1 - 1 - d1;
-    obj = nb2 - 1 - (st - d1);
-    if (ook) {
-      const double2* p = reinterpret_cast<const double2*>(cc + 6 * (s1[obi] * TN2 + z1[obi] * s2[obj]));
+    it.bi = nb1 - 1 - d1;
+    it.bj = nb2 - 1 - (st - d1);
+    return it;
+  };
+  auto load = [&](const Item& it, double (&c)[NCF]) {
 #pragma unroll
-      for (int u = 0; u < 11; ++u) {
+    for (int u = 0; u < NCF; ++u) c[u] = 0.0;
+    if (!it.ok) return;
+    const int i0 = s1[it.bi], isz = z1[it.bi], k0 = s2[it.bj], ksz = z2[it.bj];
+    if constexpr (INV) {
+      if (e < isz * ksz) {
+        const int x = i0 + (ksz == 2 ? e >> 1 : e), y = k0 + (ksz == 2 ? e & 1 : 0);
+        const double2* p = reinterpret_cast<const double2*>(cc + 4 * (x * TN2 + y));
+        const double2 v0 = __ldg(p), v1 = __ldg(p + 1);
+        c[0] = v0.x;
+        c[1] = v0.y;
+        c[2] = v1.x;
+        c[3] = v1.y;
+      }
+    } else {
+      const double2* p = reinterpret_cast<const double2*>(cc + 6 * (i0 * TN2 + isz * k0));
+#pragma unroll
+      for (int u = 0; u < NCF / 2; ++u) {
         const double2 v = __ldg(p + u);
         c[2 * u] = v.x;
         c[2 * u + 1] = v.y;
       }
-    } else {
-#pragma unroll
-      for (int u = 0; u < 22; ++u) c[u] = 0.0;
     }
   };
+  int step = 0, base = 0;
+  Item cur = locate(0, 0);
+  double cf[NCF];
+  load(cur, cf);
   while (step <= last) {
-    // this item's cell factors first: their latency overlaps the right-hand side chain
-    load(step, base, cf, bi, bj, sl, ok);
-    double* Ms = X + sl * ss;
+    // next work item: the next pass of this step, else the first pass of the next step
+    int nstep = step, nbase = base + NT;
+    {
+      const int d1lo = step - (nb2 - 1) > 0 ? step - (nb2 - 1) : 0;
+      const int d1hi = step < nb1 - 1 ? step : nb1 - 1;
+      if (nbase >= (d1hi - d1lo + 1) * NSL * 4) {
+        ++nstep;
+        nbase = 0;
+      }
+    }
+    const Item nxt = locate(nstep, nbase);
+    double cn[NCF];
+    if (INV && nstep <= last) load(nxt, cn);  // 4 doubles: cheap enough to load one item ahead
+    double* Ms = X + cur.sl * ss;
     int i0 = 0, k0 = 0, isz = 1, ksz = 1;
     double s = 0.0;
-    if (ok) {
-      i0 = s1[bi];
-      isz = z1[bi];
-      k0 = s2[bj];
-      ksz = z2[bj];
+    if (cur.ok) {
+      i0 = s1[cur.bi];
+      isz = z1[cur.bi];
+      k0 = s2[cur.bj];
+      ksz = z2[cur.bj];
       if (e < isz * ksz)
-        s = sylv_rhs<FMA>(T1, TN1, T2, TN2, Ms, Ms, ld, i0 + e / ksz, k0 + e % ksz, i0 + isz, k0 + ksz);
+        s = sylv_rhs<FMA>(T1, TN1, T2, TN2, Ms, Ms, ld, i0 + (ksz == 2 ? e >> 1 : e), k0 + (ksz == 2 ? e & 1 : 0),
+                          i0 + isz, k0 + ksz);
     }
-    const long long code = __double_as_longlong(cf[0]);
-    double b[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) b[u] = __shfl_sync(0xffffffffu, s, g + int((code >> (2 * u)) & 3));
     const int ns = isz * ksz;
-    if (ok && e < ns) {
-      if (code & 256) atomicExch(status, int(TPDG_SINGULAR));
-      const double y = ns == 1 ? cell_solve<1>(cf, b, e) : ns == 2 ? cell_solve<2>(cf, b, e) : cell_solve<4>(cf, b, e);
-      Ms[(i0 + e / ksz) * ld + k0 + e % ksz] = y;
+    double y = 0.0;
+    if constexpr (INV) {
+      double b[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) b[u] = __shfl_sync(0xffffffffu, s, g + u);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) y = fma(cf[u], b[u], y);  // rows are zero beyond ns
+    } else {
+      const long long code = __double_as_longlong(cf[0]);
+      double b[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) b[u] = __shfl_sync(0xffffffffu, s, g + int((code >> (2 * u)) & 3));
+      if (cur.ok && e < ns) {
+        if (code & 256) atomicExch(status, int(TPDG_SINGULAR));
+        y = ns == 1 ? cell_solve<1>(cf, b, e) : ns == 2 ? cell_solve<2>(cf, b, e) : cell_solve<4>(cf, b, e);
+      }
     }
-    // next work item: the next pass of this step, else the first pass of the next step
-    const int d1lo = step - (nb2 - 1) > 0 ? step - (nb2 - 1) : 0;
-    const int d1hi = step < nb1 - 1 ? step : nb1 - 1;
-    base += NT;
-    if (base >= (d1hi - d1lo + 1) * NSL * 4) {
-      ++step;
-      base = 0;
+    if (cur.ok && e < ns) Ms[(i0 + (ksz == 2 ? e >> 1 : e)) * ld + k0 + (ksz == 2 ? e & 1 : 0)] = y;
+    if (nstep != step) {
       if (CTA) __syncthreads();
       else __syncwarp();
     }
+    if (!INV && nstep <= last) load(nxt, cn);
+#pragma unroll
+    for (int u = 0; u < NCF; ++u) cf[u] = cn[u];
+    cur = nxt;
+    step = nstep;
+    base = nbase;
   }
 }
 
@@ -779,7 +842,7 @@ struct Kron2dMmaLayout {
   static constexpr int o_t1 = o_lu + lu_sz;           // T1 | T2
   static constexpr int o_rcp = (o_t1 + N1 * N1 + N2 * N2 + 1) & ~1;
   static constexpr int o_h = (o_rcp + N1 + N2 + 1) & ~1;
-  static constexpr int o_piv = o_h + hdr;             // ints
+  static constexpr int o_piv = o_h + hdr;             // ints: pivots
   static constexpr int per = (o_piv + (N1 + N2 + 1) / 2 + 1) & ~1;
 };
 
@@ -845,28 +908,12 @@ __global__ void __launch_bounds__(kSizedThreads) kron2d_mma_kernel(DevPC pc, con
     store_tiles(acc, sX, LX, N1P, lane);
   }
   __syncwarp();
-  {  // Y overwrites M: T1 Y + Y T2^T = M
+  {  // Y overwrites M: T1 Y + Y T2^T = M (block wavefront, inverse rows of the cell systems)
     const int* sb = reinterpret_cast<const int*>(sH);
-    const double* cc = cells + hdr;
-    if (sb[2]) {  // 1 x 1 blocks: one lane per cell
-      const int nb1 = sb[0], nb2 = sb[1];
-      for (int step = 0; step <= nb1 + nb2 - 2; ++step) {
-        const int d1lo = step - (nb2 - 1) > 0 ? step - (nb2 - 1) : 0;
-        const int d1hi = step < nb1 - 1 ? step : nb1 - 1;
-        for (int d1 = d1lo + lane; d1 <= d1hi; d1 += 32) {
-          const int i = nb1 - 1 - d1, k = nb2 - 1 - (step - d1);
-          const double* c = cc + 6 * (i * N2 + k);
-          const double code = __ldg(c), rcp = __ldg(c + 2);
-          const double s = sylv_rhs<true>(sT1, N1, sT2, N2, sX, sX, LX, i, k, i + 1, k + 1);
-          if (__double_as_longlong(code) & 256) atomicExch(pc.status, int(TPDG_SINGULAR));
-          sX[i * LX + k] = s * rcp;
-        }
-        __syncwarp();
-      }
-    } else {
-      sylv_wavefront<N1, N2, 1, 32, false, true>(sT1, sT2, sX, LX, 0, cc, sb, lane, pc.status);
-      __syncwarp();
-    }
+    if (sb[3]) atomicExch(pc.status, int(TPDG_SINGULAR));
+    sylv_wavefront<N1, N2, 1, 32, false, true, true>(sT1, sT2, sX, LX, 0, pc.cinv + size_t(blk) * (4 * N1 * N2), sb,
+                                                     lane, pc.status);
+    __syncwarp();
   }
   {  // Z = Q1 Y
     double acc[N1P / 8][N2P / 8][2];
@@ -1203,9 +1250,9 @@ void set_smem(K kernel, size_t bytes, size_t& configured) {
 
 } // namespace
 
-void launch_sylv_cells(const DevPC& pc, double* cells, cudaStream_t st) {
+void launch_sylv_cells(const DevPC& pc, double* cells, double* cinv, cudaStream_t st) {
   if (pc.nblk == 0) return;
-  sylv_cells_kernel<<<(pc.nblk + 3) / 4, 128, 0, st>>>(pc, cells);
+  sylv_cells_kernel<<<(pc.nblk + 3) / 4, 128, 0, st>>>(pc, cells, cinv);
   TPDG_CUDA_CHECK(cudaGetLastError());
 }
 

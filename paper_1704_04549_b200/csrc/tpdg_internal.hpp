@@ -79,6 +79,7 @@ struct DevPC {
   int faithful;          // 1: bit-faithful kernels only (TPDG_GPU_FAITHFUL=1), 0: tensor-core apply
   const double* cells;   // [nblk][cells_len]: Sylvester plan + factored tiny systems (sylv_cells_len)
   int cells_len;
+  const double* cinv;    // [nblk][4 t1 t2]: row e of the inverted cell system of every Sylvester entry
   int* status;           // device error flag (SingularError inside the Sylvester solve)
   const int* skip;       // optional device flag: kernels return immediately when *skip != 0
 };
@@ -103,7 +104,7 @@ bool launch_jv2d_mma(const DevSys& s, const double* vin, const double* halo, dou
 size_t jv_smem_bytes(const DevSys& s);
 void launch_pc_apply(const DevPC& pc, const double* in, double* out, cudaStream_t st);
 // Factor the data-independent tiny Sylvester systems of every Kronecker block into pc.cells.
-void launch_sylv_cells(const DevPC& pc, double* cells, cudaStream_t st);
+void launch_sylv_cells(const DevPC& pc, double* cells, double* cinv, cudaStream_t st);
 void launch_shuffled(const DevSys& s, int e, int comp, int transpose, const double* in, double* out,
                      double* scratch, cudaStream_t st);
 size_t shuffled_scratch_doubles(const DevSys& s);
