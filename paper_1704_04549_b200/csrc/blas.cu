@@ -174,31 +174,47 @@ __global__ void add_kernel(double* __restrict__ x, const double* __restrict__ dx
 // column h(0..k+1, k) from MGS; the rotated column goes to H(:, k). Writes |g_{k+1}| and the
 // convergence decision to the host-mapped status slot and raises `done` on convergence.
 __global__ void givens_kernel(GmresDev G, int k, GmresStatus* status) {
-  if (threadIdx.x != 0 || *G.done) return;
+  // one warp stages the column and the previous rotations in shared memory (independent loads,
+  // one round trip), then lane 0 runs the dependent rotation chain on-chip
+  extern __shared__ double gsm[];  // col[m + 2] | cs[m + 1] | sn[m + 1]
+  if (*G.done) return;
   const int m = G.m;
-  for (int j = 0; j <= k + 1; ++j) G.H[j * m + k] = G.hc[j];
-  for (int j = 0; j < k; ++j) {
-    const double t1 = G.H[j * m + k], t2 = G.H[(j + 1) * m + k];
-    G.H[j * m + k] = G.cs[j] * t1 + G.sn[j] * t2;
-    G.H[(j + 1) * m + k] = -G.sn[j] * t1 + G.cs[j] * t2;
+  double* col = gsm;
+  double* cs = col + m + 2;
+  double* sn = cs + m + 1;
+  for (int j = threadIdx.x; j <= k + 1; j += blockDim.x) col[j] = G.hc[j];
+  for (int j = threadIdx.x; j < k; j += blockDim.x) {
+    cs[j] = G.cs[j];
+    sn[j] = G.sn[j];
   }
-  const double t1 = G.H[k * m + k], t2 = G.H[(k + 1) * m + k];
-  const double denom = hypot(t1, t2);
-  G.cs[k] = denom == 0.0 ? 1.0 : t1 / denom;
-  G.sn[k] = denom == 0.0 ? 0.0 : t2 / denom;
-  G.H[k * m + k] = denom;
-  G.H[(k + 1) * m + k] = 0.0;
-  const double gk = G.g[k];
-  G.g[k] = G.cs[k] * gk;
-  G.g[k + 1] = -G.sn[k] * gk;
-  const double res = fabs(G.g[k + 1]);
-  const int conv = res <= G.target ? 1 : 0;
-  if (conv) *G.done = 1;
-  status[k].res = res;
-  status[k].conv = conv;
-  __threadfence_system();
-  status[k].valid = 1;
-  __threadfence_system();
+  __syncwarp();
+  if (threadIdx.x == 0) {
+    for (int j = 0; j < k; ++j) {
+      const double t1 = col[j], t2 = col[j + 1];
+      col[j] = cs[j] * t1 + sn[j] * t2;
+      col[j + 1] = -sn[j] * t1 + cs[j] * t2;
+    }
+    const double t1 = col[k], t2 = col[k + 1];
+    const double denom = hypot(t1, t2);
+    const double c = denom == 0.0 ? 1.0 : t1 / denom, sv = denom == 0.0 ? 0.0 : t2 / denom;
+    G.cs[k] = c;
+    G.sn[k] = sv;
+    col[k] = denom;
+    col[k + 1] = 0.0;
+    const double gk = G.g[k];
+    G.g[k] = c * gk;
+    G.g[k + 1] = -sv * gk;
+    const double res = fabs(sv * gk);
+    const int conv = res <= G.target ? 1 : 0;
+    if (conv) *G.done = 1;
+    status[k].res = res;
+    status[k].conv = conv;
+    __threadfence_system();
+    status[k].valid = 1;
+    __threadfence_system();
+  }
+  __syncwarp();
+  for (int j = threadIdx.x; j <= k + 1; j += blockDim.x) G.H[j * m + k] = col[j];
 }
 
 // y = H(0:k, 0:k)^{-1} g (back substitution, solve/gmres.hpp:145-150), one thread.
@@ -503,7 +519,7 @@ void launch_mgs_iteration(double* V, int64_t ldv, int k, int64_t n, double* hc, 
 int mgs_partial_doubles(int m) { return (m + 2) * 256; }
 
 void launch_givens(const GmresDev& G, int k, GmresStatus* status, cudaStream_t st) {
-  givens_kernel<<<1, 32, 0, st>>>(G, k, status);
+  givens_kernel<<<1, 32, sizeof(double) * size_t(3 * G.m + 4), st>>>(G, k, status);
   TPDG_CUDA_CHECK(cudaGetLastError());
   ++g_launches;
 }

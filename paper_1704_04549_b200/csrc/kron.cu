@@ -35,6 +35,10 @@ __device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
   const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
 }
+__device__ __forceinline__ void cp_async4(int* smem, const int* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem));
+}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 // Quasi-triangular diagonal block structure (tensor/sylvester.hpp:16-30); returns block count.
@@ -876,9 +880,7 @@ __global__ void __launch_bounds__(kSizedThreads) kron2d_mma_kernel(DevPC pc, con
     cp_rows(sT2, N2 * N2, r + 3 * N1 * N1 + 2 * N2 * N2, 1, N2 * N2, lane);      // T2
     cp_rows(sH, hdr, cells, 1, hdr, lane);
     cp_rows(sX, LX, in + size_t(blk) * (N1 * N2), N1, N2, lane);
-    // the Sylvester cell factors are read step by step from global: pull them into L2 now
-    for (int i = lane * 16; i < pc.cells_len; i += 32 * 16) asm volatile("prefetch.global.L2 [%0];" ::"l"(cells + i));
-    for (int i = lane; i < N1 + N2; i += 32) sPiv[i] = pc.piv[size_t(blk) * (N1 + N2) + i];
+    for (int i = lane; i < N1 + N2; i += 32) cp_async4(sPiv + i, pc.piv + size_t(blk) * (N1 + N2) + i);
     if (N1P != N1 || N2P != N2) {
       zero_pad(sX, LX, N1, N2, N1P, N2P, lane);
       zero_pad(sQ1, LQ1, N1, N1, N1P, N1P, lane);
