@@ -177,16 +177,19 @@ __global__ void givens_kernel(GmresDev G, int k, GmresStatus* status) {
   // one warp stages the column and the previous rotations in shared memory (independent loads,
   // one round trip), then lane 0 runs the dependent rotation chain on-chip
   extern __shared__ double gsm[];  // col[m + 2] | cs[m + 1] | sn[m + 1]
-  if (*G.done) return;
   const int m = G.m;
   double* col = gsm;
   double* cs = col + m + 2;
   double* sn = cs + m + 1;
+  // every operand is loaded in one round trip (done flag, g_k, the column, the old rotations)
+  const int done = *G.done;
+  const double gk = G.g[k];
   for (int j = threadIdx.x; j <= k + 1; j += blockDim.x) col[j] = G.hc[j];
   for (int j = threadIdx.x; j < k; j += blockDim.x) {
     cs[j] = G.cs[j];
     sn[j] = G.sn[j];
   }
+  if (done) return;
   __syncwarp();
   if (threadIdx.x == 0) {
     for (int j = 0; j < k; ++j) {
@@ -197,21 +200,19 @@ __global__ void givens_kernel(GmresDev G, int k, GmresStatus* status) {
     const double t1 = col[k], t2 = col[k + 1];
     const double denom = hypot(t1, t2);
     const double c = denom == 0.0 ? 1.0 : t1 / denom, sv = denom == 0.0 ? 0.0 : t2 / denom;
-    G.cs[k] = c;
-    G.sn[k] = sv;
-    col[k] = denom;
-    col[k + 1] = 0.0;
-    const double gk = G.g[k];
-    G.g[k] = c * gk;
-    G.g[k + 1] = -sv * gk;
     const double res = fabs(sv * gk);
     const int conv = res <= G.target ? 1 : 0;
-    if (conv) *G.done = 1;
     status[k].res = res;
     status[k].conv = conv;
-    __threadfence_system();
+    __threadfence_system();  // payload before the valid flag (the host polls `valid`)
     status[k].valid = 1;
-    __threadfence_system();
+    if (conv) *G.done = 1;
+    G.cs[k] = c;
+    G.sn[k] = sv;
+    G.g[k] = c * gk;
+    G.g[k + 1] = -sv * gk;
+    col[k] = denom;
+    col[k + 1] = 0.0;
   }
   __syncwarp();
   for (int j = threadIdx.x; j <= k + 1; j += blockDim.x) G.H[j * m + k] = col[j];
