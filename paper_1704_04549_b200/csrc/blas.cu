@@ -344,6 +344,45 @@ __global__ void __launch_bounds__(kCoopThreads) mgs_coop_kernel(double* __restri
 // cp.async (LDGSTS) right after pass j's arithmetic, so its HBM latency overlaps the grid barrier
 // and the reduction, and every pass computes from shared memory only. Each thread copies and later
 // reads exactly its own indices, so the only synchronization needed is its own cp.async.wait.
+// Grid reduction of one MGS pass: CTA partial (warp trees, then the 32 warp sums in order), the
+// generation barrier, and every thread summing the per-CTA partials in the same fixed order.
+// Three __syncthreads; bit-identical to block_sum + barrier + block_sum. Returns the total.
+__device__ __forceinline__ double mgs_grid_sum(double v, double* part, unsigned* bar, double* shA, double* shB) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const unsigned nb = gridDim.x;
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) shA[wid] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double bs = 0.0;
+    for (int w2 = 0; w2 < int(blockDim.x >> 5); ++w2) bs += shA[w2];
+    part[blockIdx.x] = bs;
+    // release/acquire instead of full fences: the arrival publishes this CTA's partial, the last
+    // arriver (acq_rel) re-arms the counter and releases the generation, waiters acquire it
+    unsigned g, t;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(bar + 1) : "memory");
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(t) : "l"(bar) : "memory");
+    if (t == nb - 1) {
+      asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(bar) : "memory");
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar + 1) : "memory");
+    } else {
+      unsigned cur;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(bar + 1) : "memory");
+      } while (cur == g);
+    }
+  }
+  __syncthreads();
+  double pv = threadIdx.x < nb ? reinterpret_cast<volatile double*>(part)[threadIdx.x] : 0.0;
+  for (unsigned b = threadIdx.x + blockDim.x; b < nb; b += blockDim.x) pv += reinterpret_cast<volatile double*>(part)[b];
+  for (int o = 16; o > 0; o >>= 1) pv += __shfl_xor_sync(0xffffffffu, pv, o);
+  if (lane == 0) shB[wid] = pv;
+  __syncthreads();
+  double tot = 0.0;
+  for (int w2 = 0; w2 < int(blockDim.x >> 5); ++w2) tot += shB[w2];
+  return tot;
+}
+
 __device__ __forceinline__ void cp16(double* smem, const double* gmem) {
   const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
@@ -355,8 +394,7 @@ __global__ void __launch_bounds__(kCoopThreads) mgs_pipe_kernel(double* __restri
                                                                  const int* skip) {
   if (skip && *skip) return;
   extern __shared__ double sm3[];
-  __shared__ double sh[32];
-  __shared__ double hval;
+  __shared__ double shA[32], shB[32];
   const unsigned nb = gridDim.x;
   const int64_t lo = int64_t(blockIdx.x) * chunk;
   const int64_t hi = lo + chunk < n ? lo + chunk : n;
@@ -399,21 +437,95 @@ __global__ void __launch_bounds__(kCoopThreads) mgs_pipe_kernel(double* __restri
       }
     }
     if (j + 1 <= k) issue(buf[(j + 1) & 1], V + int64_t(j + 1) * ldv + lo);  // v_{j+1} over v_{j-1}
-    const double bs = block_sum(s0 + s1, sh);
-    if (threadIdx.x == 0) partial[size_t(j) * nb + blockIdx.x] = bs;
-    coop_barrier(bar);
-    double v = threadIdx.x < nb ? reinterpret_cast<volatile double*>(partial)[size_t(j) * nb + threadIdx.x] : 0.0;
-    for (unsigned b = threadIdx.x + blockDim.x; b < nb; b += blockDim.x)
-      v += reinterpret_cast<volatile double*>(partial)[size_t(j) * nb + b];
-    const double tot = block_sum(v, sh);
-    if (threadIdx.x == 0) hval = j <= k ? tot : sqrt(tot);
-    __syncthreads();
-    h = hval;
+    {
+      const double tot = mgs_grid_sum(s0 + s1, partial + size_t(j) * nb, bar, shA, shB);
+      h = j <= k ? tot : sqrt(tot);
+    }
     if (blockIdx.x == 0 && threadIdx.x == 0) hc[j] = h;
     asm volatile("cp.async.wait_all;\n" ::: "memory");
     if (len & 1) __syncthreads();  // the scalar tail element is copied by thread 0 only
   }
   for (int64_t i = threadIdx.x; i < len; i += blockDim.x) wg[i] = h > 0.0 ? w[i] / h : w[i];
+}
+
+// MODE 4 (chunk <= 8192): w and the previous basis vector live in registers (thread t owns the
+// pairs 2t + 2048 r, the same assignment and accumulation order as MODE 3, so the result is
+// bit-identical); only v_j passes through shared memory (cp.async double buffer).
+template <int R>
+__global__ void __launch_bounds__(kCoopThreads) mgs_reg_kernel(double* __restrict__ V, int64_t ldv, int k, int64_t n,
+                                                                int64_t chunk, double* __restrict__ hc,
+                                                                double* __restrict__ partial, unsigned* bar,
+                                                                const int* skip) {
+  if (skip && *skip) return;
+  extern __shared__ double sm4[];
+  __shared__ double shA[32], shB[32];
+  const unsigned nb = gridDim.x;
+  const int64_t lo = int64_t(blockIdx.x) * chunk;
+  const int64_t hi = lo + chunk < n ? lo + chunk : n;
+  const int len = int(hi > lo ? hi - lo : 0);
+  double* buf[2] = {sm4, sm4 + chunk};
+  double* wg = V + int64_t(k + 1) * ldv + lo;
+  const int t = threadIdx.x;
+  auto issue = [&](double* dst, const double* src) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int i = 2 * t + 2 * kCoopThreads * r;
+      if (i + 1 < len) cp16(dst + i, src + i);
+      else if (i < len) dst[i] = src[i];
+    }
+  };
+  double2 w[R], vp[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int i = 2 * t + 2 * kCoopThreads * r;
+    w[r] = i + 1 < len ? *reinterpret_cast<const double2*>(wg + i) : make_double2(i < len ? wg[i] : 0.0, 0.0);
+    vp[r] = make_double2(0.0, 0.0);
+  }
+  issue(buf[0], V + lo);  // v_0
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+  __syncthreads();
+  double h = 0.0;
+  for (int j = 0; j <= k + 1; ++j) {
+    double s0 = 0.0, s1 = 0.0;
+    const double* vj = buf[j & 1];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int i = 2 * t + 2 * kCoopThreads * r;
+      if (i < len) {
+        double2 wi = w[r];
+        if (j > 0) {
+          wi.x = wi.x - h * vp[r].x;
+          if (i + 1 < len) wi.y = wi.y - h * vp[r].y;
+          w[r] = wi;
+        }
+        if (i + 1 < len) {
+          const double2 a = j <= k ? *reinterpret_cast<const double2*>(vj + i) : wi;
+          s0 += a.x * wi.x;
+          s1 += a.y * wi.y;
+          vp[r] = a;
+        } else {
+          const double a = j <= k ? vj[i] : wi.x;
+          s0 += a * wi.x;
+          vp[r] = make_double2(a, 0.0);
+        }
+      }
+    }
+    if (j + 1 <= k) issue(buf[(j + 1) & 1], V + int64_t(j + 1) * ldv + lo);
+    const double tot = mgs_grid_sum(s0 + s1, partial + size_t(j) * nb, bar, shA, shB);
+    h = j <= k ? tot : sqrt(tot);
+    if (blockIdx.x == 0 && t == 0) hc[j] = h;
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    if (len & 1) __syncthreads();  // a scalar tail element is copied by one thread only
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int i = 2 * t + 2 * kCoopThreads * r;
+    if (i + 1 < len) {
+      *reinterpret_cast<double2*>(wg + i) = h > 0.0 ? make_double2(w[r].x / h, w[r].y / h) : w[r];
+    } else if (i < len) {
+      wg[i] = h > 0.0 ? w[r].x / h : w[r].x;
+    }
+  }
 }
 
 struct CoopPlan {
@@ -436,6 +548,14 @@ CoopPlan mgs_coop_plan(int64_t n) {
   chunk = (chunk + 1) & ~int64_t(1);
   const size_t one = size_t(chunk) * sizeof(double);
   int fit = 0;
+  if (chunk <= 4 * 2 * kCoopThreads) {  // register-resident w (MODE 4 + R)
+    const int R = int((chunk + 2 * kCoopThreads - 1) / (2 * kCoopThreads));
+    const void* fns[4] = {reinterpret_cast<const void*>(mgs_reg_kernel<1>), reinterpret_cast<const void*>(mgs_reg_kernel<2>),
+                          reinterpret_cast<const void*>(mgs_reg_kernel<3>), reinterpret_cast<const void*>(mgs_reg_kernel<4>)};
+    TPDG_CUDA_CHECK(cudaFuncSetAttribute(fns[R - 1], cudaFuncAttributeMaxDynamicSharedMemorySize, int(2 * one)));
+    TPDG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, fns[R - 1], kCoopThreads, 2 * one));
+    if (fit >= 1) return {sms, chunk, 2 * one, 4 + R};
+  }
   if (3 * one <= kMax) {
     TPDG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, mgs_pipe_kernel, kCoopThreads, 3 * one));
     if (fit >= 1) return {sms, chunk, 3 * one, 3};
@@ -509,7 +629,11 @@ void launch_mgs_iteration(double* V, int64_t ldv, int k, int64_t n, double* hc, 
   }
   int64_t chunk = plan.chunk;
   void* args[] = {&V, &ldv, &k, &n, &chunk, &hc, &partial, &bar, &skip};
-  void* fn = plan.mode == 3   ? reinterpret_cast<void*>(mgs_pipe_kernel)
+  void* fn = plan.mode == 5   ? reinterpret_cast<void*>(mgs_reg_kernel<1>)
+             : plan.mode == 6 ? reinterpret_cast<void*>(mgs_reg_kernel<2>)
+             : plan.mode == 7 ? reinterpret_cast<void*>(mgs_reg_kernel<3>)
+             : plan.mode == 8 ? reinterpret_cast<void*>(mgs_reg_kernel<4>)
+             : plan.mode == 3 ? reinterpret_cast<void*>(mgs_pipe_kernel)
              : plan.mode == 2 ? reinterpret_cast<void*>(mgs_coop_kernel<2>)
              : plan.mode == 1 ? reinterpret_cast<void*>(mgs_coop_kernel<1>)
                               : reinterpret_cast<void*>(mgs_coop_kernel<0>);

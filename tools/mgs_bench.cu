@@ -1,0 +1,42 @@
+// MGS kernel microbenchmark (study tool): times launch_mgs_iteration for k = 0..K-1 on random
+// data of size n, as inside one GMRES(30) cycle.
+//   nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -Ipaper_1704_04549_b200/csrc -Iinclude \
+//        -o /tmp/mgs_bench tools/mgs_bench.cu paper_1704_04549_b200/csrc/blas.cu
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "tpdg_internal.hpp"
+
+int main(int argc, char** argv) {
+  const int64_t n = argc > 1 ? atoll(argv[1]) : 1048576;
+  const int K = argc > 2 ? atoi(argv[2]) : 25;
+  const int64_t ldv = (n + 31) & ~int64_t(31);
+  double *V, *hc, *part;
+  unsigned* ctr;
+  cudaMalloc(&V, sizeof(double) * ldv * 32);
+  cudaMalloc(&hc, sizeof(double) * 64);
+  cudaMalloc(&part, sizeof(double) * 256 * 64);
+  cudaMalloc(&ctr, sizeof(unsigned) * 512);
+  cudaMemset(ctr, 0, sizeof(unsigned) * 512);
+  std::vector<double> h(ldv * 32);
+  srand(1);
+  for (auto& x : h) x = rand() / double(RAND_MAX) - 0.5;
+  cudaStream_t st;
+  cudaStreamCreate(&st);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  for (int rep = 0; rep < 3; ++rep) {
+    cudaMemcpy(V, h.data(), sizeof(double) * ldv * 32, cudaMemcpyHostToDevice);
+    cudaEventRecord(a, st);
+    for (int k = 0; k < K; ++k) tpdg_gpu::launch_mgs_iteration(V, ldv, k, n, hc, part, ctr + 4, nullptr, st);
+    cudaEventRecord(b, st);
+    cudaEventSynchronize(b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    if (rep == 2) printf("n=%lld K=%d: %.1f us per MGS launch (avg k+1 = %.1f), %.2f us per pass\n", (long long)n, K,
+                         ms * 1e3 / K, (K + 1) / 2.0, ms * 1e3 / (K * ((K + 1) / 2.0 + 1)));
+  }
+  return 0;
+}
