@@ -375,12 +375,21 @@ __device__ __forceinline__ double mgs_grid_sum(double v, double* part, unsigned*
   __syncthreads();
   double pv = threadIdx.x < nb ? reinterpret_cast<volatile double*>(part)[threadIdx.x] : 0.0;
   for (unsigned b = threadIdx.x + blockDim.x; b < nb; b += blockDim.x) pv += reinterpret_cast<volatile double*>(part)[b];
-  for (int o = 16; o > 0; o >>= 1) pv += __shfl_xor_sync(0xffffffffu, pv, o);
-  if (lane == 0) shB[wid] = pv;
+  // only the warps holding partials reduce; warp 0 then sums the warp sums in order and
+  // broadcasts (the ordered 32-term sum in every thread cost more issue slots than a barrier)
+  const int nw = int((nb + 31) / 32);
+  if (wid < nw) {
+    for (int o = 16; o > 0; o >>= 1) pv += __shfl_xor_sync(0xffffffffu, pv, o);
+    if (lane == 0) shB[wid] = pv;
+  }
   __syncthreads();
-  double tot = 0.0;
-  for (int w2 = 0; w2 < int(blockDim.x >> 5); ++w2) tot += shB[w2];
-  return tot;
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+    for (int w2 = 0; w2 < nw; ++w2) tot += shB[w2];
+    shB[32] = tot;
+  }
+  __syncthreads();
+  return shB[32];
 }
 
 __device__ __forceinline__ void cp16(double* smem, const double* gmem) {
@@ -394,7 +403,7 @@ __global__ void __launch_bounds__(kCoopThreads) mgs_pipe_kernel(double* __restri
                                                                  const int* skip) {
   if (skip && *skip) return;
   extern __shared__ double sm3[];
-  __shared__ double shA[32], shB[32];
+  __shared__ double shA[32], shB[33];
   const unsigned nb = gridDim.x;
   const int64_t lo = int64_t(blockIdx.x) * chunk;
   const int64_t hi = lo + chunk < n ? lo + chunk : n;
@@ -458,7 +467,7 @@ __global__ void __launch_bounds__(kCoopThreads) mgs_reg_kernel(double* __restric
                                                                 const int* skip) {
   if (skip && *skip) return;
   extern __shared__ double sm4[];
-  __shared__ double shA[32], shB[32];
+  __shared__ double shA[32], shB[33];
   const unsigned nb = gridDim.x;
   const int64_t lo = int64_t(blockIdx.x) * chunk;
   const int64_t hi = lo + chunk < n ? lo + chunk : n;
