@@ -29,6 +29,11 @@ namespace tpdg_gpu {
 
 namespace {
 
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
+  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+
 __device__ __forceinline__ const double* nbr_vals(const DevSys& s, const double* vin, const double* halo, int nbr,
                                                   int qq) {
   return nbr < s.n_local ? vin + size_t(nbr) * qq : halo + size_t(nbr - s.n_local) * qq;
@@ -56,7 +61,8 @@ struct JvMmaLayout {
   static constexpr int e_mf = e_val + MP * LVAL;
   static constexpr int e_g = e_mf + MP * LMF;          // g[4][MU]
   static constexpr int e_lift = e_g + 4 * MU;          // lift vectors [4][Q]
-  static constexpr int per_warp = (e_lift + 4 * Q + 1) & ~1;
+  static constexpr int e_pw = (e_lift + 4 * Q + 1) & ~1; // jd | dft0 | dft1 of the element (cp.async, prefetched)
+  static constexpr int per_warp = (e_pw + 3 * MU * MU + 1) & ~1;
   static constexpr int budget = (227 * 1024) / 8 - weights - 16;
   static constexpr int warps = budget / per_warp > 8 ? 8 : budget / per_warp;
 };
@@ -97,10 +103,18 @@ __global__ void __launch_bounds__(256) jv2d_mma_kernel(DevSys s, const double* _
   double* slift = E + L::e_lift;
   const int r = lane >> 2, c2 = 2 * (lane & 3);
 
-  for (int e = blockIdx.x * NW + warp; e < s.n_local; e += gridDim.x * NW) {
-    // neighbour face layers (registers, consumed after step 1): 4 faces x Q values
-    constexpr int NL = (4 * Q + 31) / 32;
-    double nl[NL];
+  double* spw = E + L::e_pw;
+  constexpr int NL = (4 * Q + 31) / 32, NV = (QQ + 31) / 32, NF = (4 * MU + 31) / 32;
+  // per-element global data, fetched one element ahead: v and the neighbour face layers into
+  // registers, jd / dft into shared memory with cp.async (consumed by the point-wise pass)
+  auto fetch_regs = [&](int e, double (&vr)[NV], double (&nr)[NL]) {
+    if (e >= s.n_local) return;
+    const double* ve = vin + size_t(e) * QQ;
+#pragma unroll
+    for (int u = 0; u < NV; ++u) {
+      const int i = lane + 32 * u;
+      vr[u] = i < QQ ? ve[i] : 0.0;
+    }
 #pragma unroll
     for (int u = 0; u < NL; ++u) {
       const int idx = lane + 32 * u;
@@ -114,10 +128,51 @@ __global__ void __launch_bounds__(256) jv2d_mma_kernel(DevSys s, const double* _
           x = nf / 2 == 0 ? cf[j * Q + layer] : cf[layer * Q + j];
         }
       }
-      nl[u] = x;
+      nr[u] = x;
     }
-    const double* ve = vin + size_t(e) * QQ;
-    for (int i = lane; i < QQ; i += 32) sv[(i / Q) * LV + i % Q] = ve[i];
+  };
+  auto fetch_pw = [&](int e) {
+    if (e >= s.n_local) return;
+    const double* jd = s.jdet + size_t(e) * MM;
+    const double* d0 = s.dft + size_t(e) * 2 * MM;
+    for (int i = lane; i < MM; i += 32) cp_async8(spw + i, jd + i);
+    for (int i = lane; i < 2 * MM; i += 32) cp_async8(spw + MM + i, d0 + i);
+  };
+  const int stride = gridDim.x * NW;
+  double vr[NV], nr[NL];
+  int e = blockIdx.x * NW + warp;
+  fetch_regs(e, vr, nr);
+  fetch_pw(e);
+  for (; e < s.n_local; e += stride) {
+    // face data of this element (registers; consumed after step 2)
+    double fdm[NF], fdp[NF], ffw[NF];
+    int fnb[NF], ffl[NF];
+#pragma unroll
+    for (int u = 0; u < NF; ++u) {
+      const int idx = lane + 32 * u;
+      fdm[u] = fdp[u] = ffw[u] = 0.0;
+      fnb[u] = -1;
+      ffl[u] = 0;
+      if (idx < 4 * MU) {
+        const int f = idx / MU;
+        const size_t fq = size_t(e) * 4 * MU + idx;
+        const int* fc = s.conn + (size_t(e) * 4 + f) * 3;
+        fdm[u] = s.dfm[fq];
+        fdp[u] = s.dfp[fq];
+        ffw[u] = s.face_w[fq];
+        fnb[u] = fc[0];
+        ffl[u] = fc[2];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < NV; ++u) {
+      const int i = lane + 32 * u;
+      if (i < QQ) sv[(i / Q) * LV + i % Q] = vr[u];
+    }
+    double nl[NL];
+#pragma unroll
+    for (int u = 0; u < NL; ++u) nl[u] = nr[u];
+    fetch_regs(e + stride, vr, nr);  // next element, in flight during this one
     __syncwarp();
     {  // (1) t = v G^T
       double acc[QP / 8][NT1 / 8][2];
@@ -144,29 +199,29 @@ __global__ void __launch_bounds__(256) jv2d_mma_kernel(DevSys s, const double* _
     }
     __syncwarp();
     // face data g[f][a] = -b fw (dfm tm + dfp tp)
-    for (int idx = lane; idx < 4 * MU; idx += 32) {
-      const int a = idx % MU, f = idx / MU;
-      const int* fc = s.conn + (size_t(e) * 4 + f) * 3;
-      const double tm = f < 2 ? sval[a * LVAL + MU + f] : st[(f == 2 ? 0 : Q - 1) * LT + a];
-      double tp = 0.0;
-      if (fc[0] >= 0) tp = sval[(fc[2] == 0 ? a : MU - 1 - a) * LVAL + MU + 2 + f];
-      const size_t fq = (size_t(e) * 4 + f) * MU + a;
-      sg[idx] = -s.b * s.face_w[fq] * fma(s.dfm[fq], tm, s.dfp[fq] * tp);
-    }
-    // point-wise fields: [M | F0] -> smf, F1 -> vals in place
-    {
-      const double* jd = s.jdet + size_t(e) * MM;
-      const double* d0 = s.dft + size_t(e) * 2 * MM;
-      const double* d1 = d0 + MM;
-      for (int qv = lane; qv < MM; qv += 32) {
-        const int be = qv / MU, al = qv % MU;
-        const double x = sval[be * LVAL + al];
-        smf[be * LMF + al] = s.a * jd[qv] * x;
-        smf[be * LMF + MU + al] = s.b * (d0[qv] * x);
-        sval[be * LVAL + al] = s.b * (d1[qv] * x);
+#pragma unroll
+    for (int u = 0; u < NF; ++u) {
+      const int idx = lane + 32 * u;
+      if (idx < 4 * MU) {
+        const int a = idx % MU, f = idx / MU;
+        const double tm = f < 2 ? sval[a * LVAL + MU + f] : st[(f == 2 ? 0 : Q - 1) * LT + a];
+        double tp = 0.0;
+        if (fnb[u] >= 0) tp = sval[(ffl[u] == 0 ? a : MU - 1 - a) * LVAL + MU + 2 + f];
+        sg[idx] = -s.b * ffw[u] * fma(fdm[u], tm, fdp[u] * tp);
       }
     }
+    // point-wise fields: [M | F0] -> smf, F1 -> vals in place
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
     __syncwarp();
+    for (int qv = lane; qv < MM; qv += 32) {
+      const int be = qv / MU, al = qv % MU;
+      const double x = sval[be * LVAL + al];
+      smf[be * LMF + al] = s.a * spw[qv] * x;
+      smf[be * LMF + MU + al] = s.b * (spw[MM + qv] * x);
+      sval[be * LVAL + al] = s.b * (spw[2 * MM + qv] * x);
+    }
+    __syncwarp();
+    fetch_pw(e + stride);  // the buffer is free: next element's jd / dft
     // lift vectors: x faces Lf[j] = sum_a G[a][j] g[f][a]; y faces the same over i
     for (int idx = lane; idx < 4 * Q; idx += 32) {
       const int f = idx / Q, j = idx % Q;
