@@ -259,6 +259,28 @@ __device__ __forceinline__ void coop_barrier(unsigned* bar) {
   __syncthreads();
 }
 
+// L2 eviction-priority hints (createpolicy + .L2::cache_hint): in MODE 0 the working vector w
+// and the current basis vector are kept L2-resident across passes (evict_last), so a pass streams
+// only v_j from HBM instead of w (read + write), v_{j-1} and v_j.
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ double2 ld2_hint(const double* a, uint64_t pol) {
+  double2 v;
+  asm volatile("ld.global.L2::cache_hint.v2.f64 {%0,%1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st2_hint(double* a, double2 v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1,%2}, %3;" ::"l"(a), "d"(v.x), "d"(v.y), "l"(pol) : "memory");
+}
+
 // MODE 0: w in global/L2; 1: w slice in shared memory; 2: w and the previous basis vector's slice
 // in shared memory (each pass then streams only v_j from HBM).
 template <int MODE>
@@ -284,23 +306,27 @@ __global__ void __launch_bounds__(kCoopThreads) mgs_coop_kernel(double* __restri
     __syncthreads();
   }
   double h = 0.0;
+  const uint64_t keep = policy_evict_last(), drop = policy_evict_first();
   for (int j = 0; j <= k + 1; ++j) {
     const double* vp = j > 0 ? (MODE == 2 ? vs : V + int64_t(j - 1) * ldv + lo) : nullptr;
     const double* vj = j <= k ? V + int64_t(j) * ldv + lo : nullptr;
     double s0 = 0.0, s1 = 0.0;
-#pragma unroll 2
+#pragma unroll 4
     for (int64_t i = 2 * threadIdx.x; i < len; i += 2 * blockDim.x) {
       if (i + 1 < len) {
-        double2 wi = *reinterpret_cast<const double2*>(w + i);
+        double2 wi = MODE == 0 ? ld2_hint(w + i, keep) : *reinterpret_cast<const double2*>(w + i);
         if (vp) {
-          const double2 pv = *reinterpret_cast<const double2*>(vp + i);
+          const double2 pv = MODE == 0 ? ld2_hint(vp + i, drop) : *reinterpret_cast<const double2*>(vp + i);
           wi.x = wi.x - h * pv.x;
           wi.y = wi.y - h * pv.y;
-          *reinterpret_cast<double2*>(w + i) = wi;
+          if (MODE == 0)
+            st2_hint(w + i, wi, keep);
+          else
+            *reinterpret_cast<double2*>(w + i) = wi;
         }
         double2 a = wi;
         if (vj) {
-          a = __ldg(reinterpret_cast<const double2*>(vj + i));
+          a = MODE == 0 ? ld2_hint(vj + i, keep) : __ldg(reinterpret_cast<const double2*>(vj + i));
           if (MODE == 2) *reinterpret_cast<double2*>(vs + i) = a;
         }
         s0 += a.x * wi.x;
@@ -537,6 +563,88 @@ __global__ void __launch_bounds__(kCoopThreads) mgs_reg_kernel(double* __restric
   }
 }
 
+// MODE 9 (chunk too large for the shared-memory modes): w split between registers (the first
+// RR pairs of every thread) and shared memory (the rest), so a pass streams only v_{j-1} (L2) and
+// v_j (HBM, kept in L2 for the next pass). Same element assignment and accumulation order as
+// MODE 0 (pairs 2t + 2048 r, r ascending): bit-identical results.
+template <int RR>
+__global__ void __launch_bounds__(kCoopThreads) mgs_split_kernel(double* __restrict__ V, int64_t ldv, int k, int64_t n,
+                                                                  int64_t chunk, double* __restrict__ hc,
+                                                                  double* __restrict__ partial, unsigned* bar,
+                                                                  const int* skip) {
+  if (skip && *skip) return;
+  extern __shared__ double wsm5[];  // w pairs r >= RR: local index i - 2048 RR
+  __shared__ double shA[32], shB[33];
+  const unsigned nb = gridDim.x;
+  const int64_t lo = int64_t(blockIdx.x) * chunk;
+  const int64_t hi = lo + chunk < n ? lo + chunk : n;
+  const int len = int(hi > lo ? hi - lo : 0);
+  constexpr int SPLIT = 2 * kCoopThreads * RR;
+  double* wg = V + int64_t(k + 1) * ldv + lo;
+  const int t = threadIdx.x;
+  const uint64_t keep = policy_evict_last(), drop = policy_evict_first();
+  double2 wr[RR];
+#pragma unroll
+  for (int r = 0; r < RR; ++r) {
+    const int i = 2 * t + 2 * kCoopThreads * r;
+    wr[r] = i + 1 < len ? *reinterpret_cast<const double2*>(wg + i) : make_double2(i < len ? wg[i] : 0.0, 0.0);
+  }
+  for (int i = SPLIT + 2 * t; i < len; i += 2 * kCoopThreads) {
+    if (i + 1 < len)
+      *reinterpret_cast<double2*>(wsm5 + i - SPLIT) = *reinterpret_cast<const double2*>(wg + i);
+    else
+      wsm5[i - SPLIT] = wg[i];
+  }
+  __syncthreads();
+  double h = 0.0;
+  for (int j = 0; j <= k + 1; ++j) {
+    const double* vp = j > 0 ? V + int64_t(j - 1) * ldv + lo : nullptr;
+    const double* vj = j <= k ? V + int64_t(j) * ldv + lo : nullptr;
+    double s0 = 0.0, s1 = 0.0;
+    auto pass = [&](double2& wi, int i) {
+      if (i + 1 < len) {
+        if (vp) {
+          const double2 pv = ld2_hint(vp + i, drop);
+          wi.x = wi.x - h * pv.x;
+          wi.y = wi.y - h * pv.y;
+        }
+        const double2 a = vj ? ld2_hint(vj + i, keep) : wi;
+        s0 += a.x * wi.x;
+        s1 += a.y * wi.y;
+      } else if (i < len) {
+        if (vp) wi.x = wi.x - h * vp[i];
+        const double a = vj ? vj[i] : wi.x;
+        s0 += a * wi.x;
+      }
+    };
+#pragma unroll
+    for (int r = 0; r < RR; ++r) pass(wr[r], 2 * t + 2 * kCoopThreads * r);
+#pragma unroll 4
+    for (int i = SPLIT + 2 * t; i < len; i += 2 * kCoopThreads) {
+      double2 wi = i + 1 < len ? *reinterpret_cast<const double2*>(wsm5 + i - SPLIT) : make_double2(wsm5[i - SPLIT], 0.0);
+      pass(wi, i);
+      if (vp) {
+        if (i + 1 < len)
+          *reinterpret_cast<double2*>(wsm5 + i - SPLIT) = wi;
+        else
+          wsm5[i - SPLIT] = wi.x;
+      }
+    }
+    const double tot = mgs_grid_sum(s0 + s1, partial + size_t(j) * nb, bar, shA, shB);
+    h = j <= k ? tot : sqrt(tot);
+    if (blockIdx.x == 0 && t == 0) hc[j] = h;
+  }
+#pragma unroll
+  for (int r = 0; r < RR; ++r) {
+    const int i = 2 * t + 2 * kCoopThreads * r;
+    if (i + 1 < len)
+      *reinterpret_cast<double2*>(wg + i) = h > 0.0 ? make_double2(wr[r].x / h, wr[r].y / h) : wr[r];
+    else if (i < len)
+      wg[i] = h > 0.0 ? wr[r].x / h : wr[r].x;
+  }
+  for (int i = SPLIT + t; i < len; i += kCoopThreads) wg[i] = h > 0.0 ? wsm5[i - SPLIT] / h : wsm5[i - SPLIT];
+}
+
 struct CoopPlan {
   int grid;
   int64_t chunk;
@@ -576,6 +684,16 @@ CoopPlan mgs_coop_plan(int64_t n) {
   if (one <= kMax) {
     TPDG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, mgs_coop_kernel<1>, kCoopThreads, one));
     if (fit >= 1) return {sms, chunk, one, 1};
+  }
+  {  // MODE 9: w split registers (8 pairs per thread) + shared memory
+    constexpr int RR = 8;
+    const int64_t rest = chunk - 2 * kCoopThreads * RR;
+    if (rest > 0 && size_t(rest) * sizeof(double) <= kMax) {
+      const size_t sm = size_t(rest) * sizeof(double);
+      TPDG_CUDA_CHECK(cudaFuncSetAttribute(mgs_split_kernel<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+      TPDG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, mgs_split_kernel<RR>, kCoopThreads, sm));
+      if (fit >= 1) return {sms, chunk, sm, 9};
+    }
   }
   return {sms, chunk, 0, 0};
 }
@@ -638,7 +756,8 @@ void launch_mgs_iteration(double* V, int64_t ldv, int k, int64_t n, double* hc, 
   }
   int64_t chunk = plan.chunk;
   void* args[] = {&V, &ldv, &k, &n, &chunk, &hc, &partial, &bar, &skip};
-  void* fn = plan.mode == 5   ? reinterpret_cast<void*>(mgs_reg_kernel<1>)
+  void* fn = plan.mode == 9   ? reinterpret_cast<void*>(mgs_split_kernel<8>)
+             : plan.mode == 5 ? reinterpret_cast<void*>(mgs_reg_kernel<1>)
              : plan.mode == 6 ? reinterpret_cast<void*>(mgs_reg_kernel<2>)
              : plan.mode == 7 ? reinterpret_cast<void*>(mgs_reg_kernel<3>)
              : plan.mode == 8 ? reinterpret_cast<void*>(mgs_reg_kernel<4>)
