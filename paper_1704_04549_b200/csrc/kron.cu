@@ -1117,6 +1117,191 @@ __global__ void __launch_bounds__(k3Threads) kron3d_sized_kernel(DevPC pc, const
                                             N1);  // (.) Q2^T
 }
 
+// ------------------------------------------------------------------------------------ 3D, DMMA
+// apply_factors_3d (precond/ksvd.hpp:132-153) on the tensor cores, one 128-thread CTA per block.
+// The element lives in shared memory as Xr[r][(s, j)] (B2 index r outermost, then the outer slice
+// s and the C1 index j), so that the rotations of all N1 slices are four single DMMA products:
+//   P = Q1^T Xr (Q x N1 Q),  M = P_rows Q2 ((N1 Q) x Q),  Z = Q1 Y,  out = Z_rows Q2^T,
+// with each product's C fragments stored straight into the layout the next one reads. The three
+// LU axis solves are register fibers over Xr (FMA) and the slices share one Sylvester wavefront
+// (inverse rows of the cell systems). Parity as the 2D tensor-core apply (<= 1e-12 gate).
+template <int N1, int Q>
+struct Kron3dMmaLayout {
+  static constexpr int QP = p8(Q), KQ = p4(Q), NC = N1 * Q, NCP = p8(NC);
+  static constexpr int LDR = lda4(NCP), LDP = lda4(KQ), LQ = lda4(QP);
+  static constexpr int o_x = 0;                          // Xr: KQ x LDR
+  static constexpr int o_p = o_x + KQ * LDR;             // P / Z rows: NCP x LDP
+  static constexpr int o_q1 = o_p + NCP * LDP;           // Q1: QP x LQ (zero padded)
+  static constexpr int o_q2 = o_q1 + QP * LQ;            // Q2: QP x LQ
+  static constexpr int o_lu = o_q2 + QP * LQ;            // LU(A1) N1^2 | LU(B2) | LU(C1) | T1 | T2 (Q^2 each)
+  static constexpr int o_rcp = (o_lu + N1 * N1 + 4 * Q * Q + 1) & ~1;
+  static constexpr int hdr = (((4 + 4 * Q) / 2 + 2) & ~1);
+  static constexpr int o_h = (o_rcp + N1 + 2 * Q + 1) & ~1;
+  static constexpr int o_piv = o_h + hdr;
+  static constexpr int total = (o_piv + (N1 + 2 * Q + 1) / 2 + 1) & ~1;
+  static constexpr int NT = NCP / 8, NTW = (NT + 3) / 4;  // column tiles, per warp
+};
+
+template <int N1, int Q>
+__global__ void __launch_bounds__(k3Threads) kron3d_mma_kernel(DevPC pc, const double* __restrict__ in,
+                                                                double* __restrict__ out) {
+  const int blk = blockIdx.x;
+  if (pc.kind[blk] == 0 || (pc.skip && *pc.skip)) return;
+  using L = Kron3dMmaLayout<N1, Q>;
+  constexpr int QP = L::QP, KQ = L::KQ, NC = L::NC, LDR = L::LDR, LDP = L::LDP, LQ = L::LQ, NTW = L::NTW,
+                NT = L::NT, hdr = L::hdr;
+  extern __shared__ double sm[];
+  double* Xr = sm + L::o_x;
+  double* Pr = sm + L::o_p;
+  double* sQ1 = sm + L::o_q1;
+  double* sQ2 = sm + L::o_q2;
+  double* sLU = sm + L::o_lu;
+  double* sRcp = sm + L::o_rcp;
+  double* sH = sm + L::o_h;
+  int* sPiv = reinterpret_cast<int*>(sm + L::o_piv);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < L::o_lu; i += k3Threads) sm[i] = 0.0;  // pads of Xr, P/Z, Q1, Q2
+  __syncthreads();
+  {
+    const double* r = pc.rec + size_t(blk) * (N1 * N1 + 6 * Q * Q);
+    // record: LU(A1) | LU(B2) | LU(C1) | Q1 | T1 | Q2 | T2
+    for (int i = tid; i < N1 * N1 + 2 * Q * Q; i += k3Threads) cp_async8(sLU + i, r + i);
+    for (int i = tid; i < Q * Q; i += k3Threads) {
+      cp_async8(sQ1 + (i / Q) * LQ + i % Q, r + N1 * N1 + 2 * Q * Q + i);
+      cp_async8(sLU + N1 * N1 + 2 * Q * Q + i, r + N1 * N1 + 3 * Q * Q + i);  // T1
+      cp_async8(sQ2 + (i / Q) * LQ + i % Q, r + N1 * N1 + 4 * Q * Q + i);
+      cp_async8(sLU + N1 * N1 + 3 * Q * Q + i, r + N1 * N1 + 5 * Q * Q + i);  // T2
+    }
+    const double* cells = pc.cells + size_t(blk) * pc.cells_len;
+    for (int i = tid; i < hdr; i += k3Threads) cp_async8(sH + i, cells + i);
+    for (int i = tid; i < N1 + 2 * Q; i += k3Threads) cp_async4(sPiv + i, pc.piv + size_t(blk) * (N1 + 2 * Q) + i);
+    const double* x = in + size_t(blk) * (N1 * Q * Q);
+    for (int i = tid; i < N1 * Q * Q; i += k3Threads) {  // x[s][r][j] -> Xr[r][s Q + j]
+      const int j = i % Q, rr = (i / Q) % Q, s = i / (Q * Q);
+      cp_async8(Xr + rr * LDR + s * Q + j, x + i);
+    }
+    cp_async_wait_all();
+  }
+  __syncthreads();
+  const double* luA1 = sLU;
+  const double* luB2 = luA1 + N1 * N1;
+  const double* luC1 = luB2 + Q * Q;
+  const double* T1 = luC1 + Q * Q;
+  const double* T2 = T1 + Q * Q;
+  for (int i = tid; i < N1 + 2 * Q; i += k3Threads)
+    sRcp[i] = 1.0 / (i < N1 ? luA1[i * N1 + i] : i < N1 + Q ? luB2[(i - N1) * (Q + 1)] : luC1[(i - N1 - Q) * (Q + 1)]);
+  __syncthreads();
+  for (int f = tid; f < Q * Q; f += k3Threads) lu_fiber_fma<N1>(luA1, sRcp, sPiv, Xr + (f / Q) * LDR + f % Q, Q);
+  __syncthreads();
+  for (int f = tid; f < NC; f += k3Threads)
+    lu_fiber_fma<Q>(luB2, sRcp + N1, sPiv + N1, Xr + (f / Q) * Q + f % Q, LDR);
+  __syncthreads();
+  for (int f = tid; f < NC; f += k3Threads)
+    lu_fiber_fma<Q>(luC1, sRcp + N1 + Q, sPiv + N1 + Q, Xr + (f % Q) * LDR + (f / Q) * Q, 1);
+  __syncthreads();
+  const int fr = lane >> 2, fc = 2 * (lane & 3);
+  {  // P = Q1^T Xr -> P rows (s Q + r', j)
+    double acc[QP / 8][NTW][2];
+    zero_tiles(acc);
+    const int nt0 = warp * NTW;
+    if (nt0 < NT) {
+      mma_tiles<QP / 8, NTW, KQ / 4, false, true>(acc, sQ1, LQ, Xr + 8 * nt0, LDR, lane);
+#pragma unroll
+      for (int mt = 0; mt < QP / 8; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NTW; ++nt)
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int m = 8 * mt + fr, n = 8 * (nt0 + nt) + fc + u;
+            if (m < Q && n < NC) Pr[((n / Q) * Q + m) * LDP + n % Q] = acc[mt][nt][u];
+          }
+    }
+  }
+  __syncthreads();
+  {  // M = P_rows Q2 -> Xr[r'][s Q + j']
+    double acc[NTW][QP / 8][2];
+    zero_tiles(acc);
+    const int mt0 = warp * NTW;
+    if (mt0 < NT) {
+      mma_tiles<NTW, QP / 8, KQ / 4, false>(acc, Pr + 8 * mt0 * LDP, LDP, sQ2, LQ, lane);
+#pragma unroll
+      for (int mt = 0; mt < NTW; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < QP / 8; ++nt)
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int m = 8 * (mt0 + mt) + fr, n = 8 * nt + fc + u;
+            if (m < NC && n < Q) Xr[(m % Q) * LDR + (m / Q) * Q + n] = acc[mt][nt][u];
+          }
+    }
+  }
+  __syncthreads();
+  {  // Sylvester per slice (shared plan), Y over M in Xr: slice s at column s Q, rows stride LDR
+    const int* sb = reinterpret_cast<const int*>(sH);
+    if (sb[3]) atomicExch(pc.status, int(TPDG_SINGULAR));
+    sylv_wavefront<Q, Q, N1, k3Threads, true, true, true>(T1, T2, Xr, LDR, Q, pc.cinv + size_t(blk) * (4 * Q * Q), sb,
+                                                            tid, pc.status);
+    __syncthreads();
+  }
+  {  // Z = Q1 Y -> Z rows (s Q + r, j')
+    double acc[QP / 8][NTW][2];
+    zero_tiles(acc);
+    const int nt0 = warp * NTW;
+    if (nt0 < NT) {
+      mma_tiles<QP / 8, NTW, KQ / 4, false>(acc, sQ1, LQ, Xr + 8 * nt0, LDR, lane);
+#pragma unroll
+      for (int mt = 0; mt < QP / 8; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < NTW; ++nt)
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int m = 8 * mt + fr, n = 8 * (nt0 + nt) + fc + u;
+            if (m < Q && n < NC) Pr[((n / Q) * Q + m) * LDP + n % Q] = acc[mt][nt][u];
+          }
+    }
+  }
+  __syncthreads();
+  {  // out = Z_rows Q2^T -> out[s][r][j]
+    double acc[NTW][QP / 8][2];
+    zero_tiles(acc);
+    const int mt0 = warp * NTW;
+    if (mt0 < NT) {
+      mma_tiles<NTW, QP / 8, KQ / 4, true>(acc, Pr + 8 * mt0 * LDP, LDP, sQ2, LQ, lane);
+      double* o = out + size_t(blk) * (N1 * Q * Q);
+#pragma unroll
+      for (int mt = 0; mt < NTW; ++mt)
+#pragma unroll
+        for (int nt = 0; nt < QP / 8; ++nt)
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int m = 8 * (mt0 + mt) + fr, n = 8 * nt + fc + u;
+            if (m < NC && n < Q) o[m * Q + n] = acc[mt][nt][u];
+          }
+    }
+  }
+}
+
+template <int N1, int Q>
+bool try_kron3d_mma(const DevPC& pc, const double* in, double* out, cudaStream_t st) {
+  if (pc.dim != 3 || pc.n1 != N1 || pc.q != Q) return false;
+  const size_t smem = sizeof(double) * size_t(Kron3dMmaLayout<N1, Q>::total);
+  static bool configured = false;
+  if (!configured) {
+    TPDG_CUDA_CHECK(cudaFuncSetAttribute(kron3d_mma_kernel<N1, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(smem)));
+    TPDG_CUDA_CHECK(cudaFuncSetAttribute(kron3d_mma_kernel<N1, Q>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                         100));
+    configured = true;
+  }
+  kron3d_mma_kernel<N1, Q><<<pc.nblk, k3Threads, smem, st>>>(pc, in, out);
+  return true;
+}
+
+bool launch_kron3d_mma(const DevPC& pc, const double* in, double* out, cudaStream_t st) {
+  return try_kron3d_mma<4, 4>(pc, in, out, st) || try_kron3d_mma<5, 5>(pc, in, out, st) ||
+         try_kron3d_mma<8, 8>(pc, in, out, st) || try_kron3d_mma<11, 11>(pc, in, out, st);
+}
+
 template <int N1, int Q>
 bool try_kron3d_sized(const DevPC& pc, const double* in, double* out, cudaStream_t st) {
   if (pc.dim != 3 || pc.n1 != N1 || pc.q != Q) return false;
@@ -1269,7 +1454,7 @@ void launch_pc_apply(const DevPC& pc, const double* in, double* out, cudaStream_
       set_smem(kron2d_apply_kernel, smem, c2);
       kron2d_apply_kernel<<<pc.nblk, kApplyThreads, smem, st>>>(pc, in, out);
     }
-  } else if (!launch_kron3d_sized(pc, in, out, st)) {
+  } else if (!(!pc.faithful && launch_kron3d_mma(pc, in, out, st)) && !launch_kron3d_sized(pc, in, out, st)) {
     set_smem(kron3d_apply_kernel, smem, c3);
     kron3d_apply_kernel<<<pc.nblk, kApplyThreads, smem, st>>>(pc, in, out);
   }
