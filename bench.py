@@ -314,6 +314,8 @@ def main_ours(args, rank, world, local_rank):
             traffic = json.load(f)
     except Exception:
         pass
+    if "mgs_bytes_per_pass" in traffic and ks:
+        traffic["mgs"] = traffic["mgs_bytes_per_pass"] * float(np.mean([k + 2 for k in ks]))
     if dom:
         ach = kern[dom]["achieved_gbs"]
         roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm, "unit": "GB/s",
@@ -323,9 +325,17 @@ def main_ours(args, rank, world, local_rank):
     kron = None
     if "pc_apply" in kern:
         avg_s = kern["pc_apply"]["avg_us"] * 1e-6
+        # T_roof = max(B / BW_HBM, F / P_FP64); P_FP64 measured on the box (tools/fp64_peak.cu)
+        p64 = 37.06
+        try:
+            with open(os.path.join(ROOT, "profiles", "fp64_peak.json")) as f:
+                p64 = float(json.load(f)["fp64_dmma_tflops"])
+        except Exception:
+            pass
+        t_roof = max(bytes_pc / (hbm * 1e9), flops_pc / (p64 * 1e12))
         kron = {"value": n_local / avg_s / 1e9 * world, "unit": "GDOF/s",
-                "roofline_frac": kern["pc_apply"]["achieved_gbs"] / hbm, "bound": "hbm",
-                "flops_per_launch": flops_pc, "achieved_tflops": flops_pc / avg_s / 1e12}
+                "roofline_frac": t_roof / avg_s, "bound": "hbm" if bytes_pc / hbm * 1e-9 >= flops_pc / p64 * 1e-12 else "fp64",
+                "flops_per_launch": flops_pc, "achieved_tflops": flops_pc / avg_s / 1e12, "fp64_peak_tflops": p64}
 
     # ---- CPU baseline (rank 0, N = 1): the unmodified reference on this host
     cpu = None

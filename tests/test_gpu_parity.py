@@ -130,3 +130,19 @@ def test_pc_apply_formed_on_gpu(ctx, case):
     err = O.rel_l2(pc.apply(z["rhs"]), z["pc_out"])
     print(f"{case}: GPU-formed PC apply rel-L2 vs reference = {err:.3e}")
     assert err <= 1e-8
+
+
+@pytest.mark.parametrize("case", ["cfg1", "cfg2s_p15", "adv3d_p4", "euler2d"])
+def test_pc_apply_faithful_path(ctx, case):
+    """TPDG_GPU_FAITHFUL=1 (read when a PC is built) selects the order-faithful, FMA-free kernels."""
+    import os
+    z, op = op_for(ctx, case)
+    os.environ["TPDG_GPU_FAITHFUL"] = "1"
+    try:
+        pc = T.import_factors(op, z["factors"], z["has_factors"])
+    finally:
+        del os.environ["TPDG_GPU_FAITHFUL"]
+    out = pc.apply(z["rhs"])
+    assert O.rel_l2(out, z["pc_out"]) <= 1e-12, O.rel_l2(out, z["pc_out"])
+    res = T.gmres(op, pc, z["rhs"], T.GmresConfig(tol=1e-10, restart=30, max_iterations=2000))
+    assert res.iterations == int(z["gmres_meta"][0])
