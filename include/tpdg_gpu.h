@@ -120,6 +120,13 @@ int tpdg_gpu_form_ksvd(tpdg_gpu_op op, const tpdg_gpu_ksvd_config *cfg, tpdg_gpu
  * recomputed on the device exactly as make_factors_2d/3d do). Blocks with has == 0 get the
  * exact block-LU fallback. */
 int tpdg_gpu_pc_import_factors(tpdg_gpu_op op, const double *h_factors, const int64_t *h_has, tpdg_gpu_pc *out);
+/* As import_factors, but the apply state of every factored block is taken as given instead of
+ * recomputed: h_rec = per block (has != 0, concatenated) the LU factors then the Schur pairs
+ * (2D: LU(A2) LU(B1) Q1 T1 Q2 T2; 3D: LU(A1) LU(B2) LU(C1) Q1 T1 Q2 T2, the LuFactor and
+ * SchurPair members of Factors2D / Factors3D, precond/ksvd.hpp:34-46), h_piv = their pivots.
+ * Isolates the apply (ksvd.hpp:112-153) from the formation's libm-dependent Schur rotations. */
+int tpdg_gpu_pc_import_record(tpdg_gpu_op op, const double *h_factors, const int64_t *h_has, const double *h_rec,
+                              const int *h_piv, tpdg_gpu_pc *out);
 int tpdg_gpu_pc_destroy(tpdg_gpu_pc pc);
 int tpdg_gpu_pc_num_fallbacks(tpdg_gpu_pc pc, int *n);
 int tpdg_gpu_pc_fallbacks(tpdg_gpu_pc pc, int64_t *pairs /* (element, component) x n */);

@@ -1708,6 +1708,14 @@ void or_pc_factors(const or_pc *pc, int blk, double *out) {
   memcpy(out, pc->fac + (size_t)blk * pc->flen, sizeof(double) * pc->flen);
 }
 
+int or_pc_record_len(const or_pc *pc) { return pc_lu_len(pc) + pc_sq_len(pc); }
+int or_pc_piv_len(const or_pc *pc) { return pc_perm_len(pc); }
+void or_pc_record(const or_pc *pc, int blk, double *rec, int *piv) {
+  memcpy(rec, pc->lu + (size_t)blk * pc_lu_len(pc), sizeof(double) * pc_lu_len(pc));
+  memcpy(rec + pc_lu_len(pc), pc->sq + (size_t)blk * pc_sq_len(pc), sizeof(double) * pc_sq_len(pc));
+  memcpy(piv, pc->perm + (size_t)blk * pc_perm_len(pc), sizeof(int) * pc_perm_len(pc));
+}
+
 /* matmul (tensor/small_matrix.hpp:103-113): c = a (r x k) b (k x c) */
 static void matmul(int r, int kk, int cc, const double *a, const double *b, double *c) {
   for (int i = 0; i < r * cc; ++i) c[i] = 0.0;

@@ -65,6 +65,10 @@ void or_pc_fallbacks(const or_pc *pc, int64_t *out); /* pairs (element, componen
 int or_pc_has_factors(const or_pc *pc, int blk);
 /* 2D: a1 b1 a2 b2 ; 3D: a1 b1 c1 b2 c2 (row-major, concatenated) */
 void or_pc_factors(const or_pc *pc, int blk, double *out);
+/* formed apply state of one block: LU factors then Schur pairs (Q1 T1 Q2 T2), and the pivots */
+int or_pc_record_len(const or_pc *pc);
+int or_pc_piv_len(const or_pc *pc);
+void or_pc_record(const or_pc *pc, int blk, double *rec, int *piv);
 int or_pc_factor_len(const or_pc *pc);
 void or_pc_apply(const or_pc *pc, const double *in, double *out);
 /* 2D apply of given factors (reference ksvd.hpp:75-129), rhs overwritten */

@@ -67,6 +67,7 @@ _STATUS = {1: ShapeError, 2: SingularError, 3: StateError, 4: ConvergenceError, 
 
 dp = C.POINTER(C.c_double)
 i64p = C.POINTER(C.c_int64)
+ip = C.POINTER(C.c_int)
 
 
 class _System(C.Structure):
@@ -92,7 +93,7 @@ EXPORTS = [
     "tpdg_gpu_ctx_profile", "tpdg_gpu_ctx_profile_read",
     "tpdg_gpu_op_create", "tpdg_gpu_op_destroy", "tpdg_gpu_op_local_size", "tpdg_gpu_op_check_hash",
     "tpdg_gpu_jv", "tpdg_gpu_jv_host", "tpdg_gpu_shuffled_host", "tpdg_gpu_form_ksvd",
-    "tpdg_gpu_pc_import_factors", "tpdg_gpu_pc_destroy", "tpdg_gpu_pc_num_fallbacks", "tpdg_gpu_pc_fallbacks",
+    "tpdg_gpu_pc_import_factors", "tpdg_gpu_pc_import_record", "tpdg_gpu_pc_destroy", "tpdg_gpu_pc_num_fallbacks", "tpdg_gpu_pc_fallbacks",
     "tpdg_gpu_pc_factor_len", "tpdg_gpu_pc_export_factors", "tpdg_gpu_pc_apply", "tpdg_gpu_pc_apply_host",
     "tpdg_gpu_gmres", "tpdg_gpu_gmres_host", "tpdg_setup_advection", "tpdg_setup_system", "tpdg_setup_destroy",
     "tpdg_uniform_vector", "tpdg_seeded_unit_vector", "tpdg_halo_plan_create", "tpdg_halo_plan_query",
@@ -129,6 +130,7 @@ def lib():
         "tpdg_gpu_shuffled_host": [v, C.c_int, C.c_int, C.c_int, dp, dp],
         "tpdg_gpu_form_ksvd": [v, C.POINTER(_KsvdCfg), C.POINTER(v)],
         "tpdg_gpu_pc_import_factors": [v, dp, i64p, C.POINTER(v)],
+        "tpdg_gpu_pc_import_record": [v, dp, i64p, dp, ip, C.POINTER(v)],
         "tpdg_gpu_pc_destroy": [v], "tpdg_gpu_pc_num_fallbacks": [v, C.POINTER(C.c_int)],
         "tpdg_gpu_pc_fallbacks": [v, i64p], "tpdg_gpu_pc_factor_len": [v, C.POINTER(C.c_int)],
         "tpdg_gpu_pc_export_factors": [v, C.c_int, dp, C.POINTER(C.c_int)],
@@ -480,6 +482,19 @@ def import_factors(op: LinearizedOperator, factors, has) -> KsvdPC:
     hs = np.ascontiguousarray(has, dtype=np.int64)
     h = C.c_void_p()
     _check(lib().tpdg_gpu_pc_import_factors(op.h, _ptr(f), hs.ctypes.data_as(i64p), C.byref(h)))
+    return KsvdPC(op, h)
+
+
+def import_record(op: LinearizedOperator, factors, has, rec, piv) -> KsvdPC:
+    """Test hook: preconditioner from an externally formed apply state (LU + Schur pairs and
+    pivots of every factored block, e.g. the reference's), not recomputed on the device."""
+    f = np.ascontiguousarray(factors, dtype=np.float64)
+    hs = np.ascontiguousarray(has, dtype=np.int64)
+    r = np.ascontiguousarray(rec, dtype=np.float64)
+    pv = np.ascontiguousarray(piv, dtype=np.int32)
+    h = C.c_void_p()
+    _check(lib().tpdg_gpu_pc_import_record(op.h, _ptr(f), hs.ctypes.data_as(i64p), _ptr(r),
+                                           pv.ctypes.data_as(ip), C.byref(h)))
     return KsvdPC(op, h)
 
 

@@ -870,6 +870,35 @@ int tpdg_gpu_pc_import_factors(tpdg_gpu_op op, const double* h_factors, const in
   });
 }
 
+int tpdg_gpu_pc_import_record(tpdg_gpu_op op, const double* h_factors, const int64_t* h_has, const double* h_rec,
+                              const int* h_piv, tpdg_gpu_pc* out) {
+  return guarded([&] {
+    std::unique_ptr<tpdg_gpu_pc_s> pc(new tpdg_gpu_pc_s);
+    pc->op = op;
+    cudaStream_t st = op->ctx->stream;
+    alloc_records(pc.get());
+    const int n1 = (op->s.small ? 1 : op->n_c) * op->q;
+    const size_t rl = rec_len_of(op->dim, n1, op->q), pl = piv_len_of(op->dim, n1, op->q);
+    std::vector<double> raw(size_t(pc->nblk) * pc->raw_len, 0.0), rec(size_t(pc->nblk) * rl, 0.0);
+    std::vector<int> kind(pc->nblk, 0), piv(size_t(pc->nblk) * pl, 0);
+    size_t k = 0;
+    for (int b = 0; b < pc->nblk; ++b)
+      if (h_has[b]) {
+        std::copy(h_factors + k * pc->raw_len, h_factors + (k + 1) * pc->raw_len, raw.begin() + size_t(b) * pc->raw_len);
+        std::copy(h_rec + k * rl, h_rec + (k + 1) * rl, rec.begin() + size_t(b) * rl);
+        std::copy(h_piv + k * pl, h_piv + (k + 1) * pl, piv.begin() + size_t(b) * pl);
+        kind[b] = 1;
+        ++k;
+      }
+    TPDG_CUDA_CHECK(cudaMemcpyAsync(pc->raw.p, raw.data(), sizeof(double) * raw.size(), cudaMemcpyHostToDevice, st));
+    TPDG_CUDA_CHECK(cudaMemcpyAsync(pc->rec.p, rec.data(), sizeof(double) * rec.size(), cudaMemcpyHostToDevice, st));
+    TPDG_CUDA_CHECK(cudaMemcpyAsync(pc->piv.p, piv.data(), sizeof(int) * piv.size(), cudaMemcpyHostToDevice, st));
+    TPDG_CUDA_CHECK(cudaMemcpyAsync(pc->kind.p, kind.data(), sizeof(int) * kind.size(), cudaMemcpyHostToDevice, st));
+    finish_pc(pc.get());
+    *out = pc.release();
+  });
+}
+
 int tpdg_gpu_pc_destroy(tpdg_gpu_pc pc) {
   return guarded([&] { delete pc; });
 }

@@ -16,6 +16,7 @@
 // column sweeps read coalesced columns; its forward sweep keeps the reference order, the backward
 // sweep runs column-descending (per-row order reversed; the block itself is well conditioned).
 #include <cstdint>
+#include <cstdlib>
 
 #include "faithful.cuh"
 #include "mma.cuh"
@@ -269,6 +270,16 @@ size_t kron2d_smem(const DevPC& pc) {
 // pivoted solve unrolled in registers, and the wavefront runs in one warp (__syncwarp per step).
 // 64 threads per element keep many elements resident per SM. Same arithmetic as above.
 constexpr int kSizedThreads = 64;
+
+#ifndef SYLV_FAST
+#define SYLV_FAST 1
+#endif
+#ifndef SYLV_EXP
+#define SYLV_EXP 0  // study builds only: 1 no cell loads, 2 no tiny solves
+#endif
+#ifndef KRON_SKIP
+#define KRON_SKIP 0  // study builds only: bit mask of skipped phases (tools/kron_variants.sh)
+#endif
 
 template <int N>
 __device__ __forceinline__ void lu_fiber_reg(const double* __restrict__ lu, const double* __restrict__ rcp,
@@ -580,7 +591,7 @@ __device__ __forceinline__ void sylv_wavefront(const double* T1, const double* T
   auto load = [&](const Item& it, double (&c)[NCF]) {
 #pragma unroll
     for (int u = 0; u < NCF; ++u) c[u] = 0.0;
-    if (!it.ok) return;
+    if (!it.ok || (SYLV_EXP & 1)) return;
     const int i0 = s1[it.bi], isz = z1[it.bi], k0 = s2[it.bj], ksz = z2[it.bj];
     if constexpr (INV) {
       if (e < isz * ksz) {
@@ -647,7 +658,8 @@ __device__ __forceinline__ void sylv_wavefront(const double* T1, const double* T
       for (int u = 0; u < 4; ++u) b[u] = __shfl_sync(0xffffffffu, s, g + int((code >> (2 * u)) & 3));
       if (cur.ok && e < ns) {
         if (code & 256) atomicExch(status, int(TPDG_SINGULAR));
-        y = ns == 1 ? cell_solve<1>(cf, b, e) : ns == 2 ? cell_solve<2>(cf, b, e) : cell_solve<4>(cf, b, e);
+        if (SYLV_EXP & 2) y = b[0];
+        else y = ns == 1 ? cell_solve<1>(cf, b, e) : ns == 2 ? cell_solve<2>(cf, b, e) : cell_solve<4>(cf, b, e);
       }
     }
     if (cur.ok && e < ns) Ms[(i0 + (ksz == 2 ? e >> 1 : e)) * ld + k0 + (ksz == 2 ? e & 1 : 0)] = y;
@@ -664,15 +676,99 @@ __device__ __forceinline__ void sylv_wavefront(const double* T1, const double* T
   }
 }
 
+// Faithful quasi-triangular Sylvester solve (sylvester.hpp:72-127) of one block by one warp, in
+// place on X (ld): the block anti-diagonal wavefront with one lane per Sylvester entry. Cells of
+// a step are processed in groups of gs lanes (gs = the largest cell of the block: 1, 2 or 4), so
+// 32 / gs cells per pass. Each lane forms its entry's right-hand side in the reference order
+// (B, then the solved rows below j ascending, then the solved columns to the right l ascending,
+// separate mul / sub roundings); the gs lanes of a cell exchange their right-hand sides with
+// shuffles and each replays the cell's factored tiny system (sylv_cells_kernel), whose slot is
+// loaded before the chains so that its latency hides behind them. 1 x 1 cells divide by
+// t1_ii + t2_kk directly (solve_tiny<1>). The singular flag comes from the plan (sylv_cells).
+template <int N1, int N2>
+__device__ __forceinline__ void sylv_fast(const double* __restrict__ T1, const double* __restrict__ T2, double* X,
+                                          int ld, const int* sb, const double* __restrict__ cc, int lane,
+                                          int* status) {
+  const int nb1 = sb[0], nb2 = sb[1];
+  const int *s1 = sb + 4, *z1 = s1 + N1, *s2 = z1 + N1, *z2 = s2 + N2;
+  if (sb[3] && lane == 0) atomicExch(status, int(TPDG_SINGULAR));
+  const int lg = (nb1 < N1 ? 1 : 0) + (nb2 < N2 ? 1 : 0);  // log2 of the group size
+  const int gs = 1 << lg, per = 32 >> lg;
+  const int g = lane >> lg, e = lane & (gs - 1), gbase = g << lg;
+  const int last = nb1 + nb2 - 2;
+  for (int st = 0; st <= last; ++st) {
+    const int d1lo = st - (nb2 - 1) > 0 ? st - (nb2 - 1) : 0;
+    const int d1hi = st < nb1 - 1 ? st : nb1 - 1;
+    const int ncell = d1hi - d1lo + 1;
+    for (int c0 = 0; c0 < ncell; c0 += per) {
+      const int cell = c0 + g;
+      const bool ok = cell < ncell;
+      int i0 = 0, isz = 1, k0 = 0, ksz = 1;
+      if (ok) {
+        const int d1 = d1lo + cell, bi = nb1 - 1 - d1, bk = nb2 - 1 - (st - d1);
+        i0 = s1[bi];
+        isz = z1[bi];
+        k0 = s2[bk];
+        ksz = z2[bk];
+      }
+      const int ns = isz * ksz;
+      const bool act = ok && e < ns;
+      const int i = i0 + (ksz == 2 ? e >> 1 : e), k = k0 + (ksz == 2 ? e & 1 : 0);
+      // the cell's factored system (ns > 1), loaded ahead of the chains
+      double cf[22];
+      cf[0] = 0.0;
+      if (ns > 1) {
+        const double* slot = cc + 6 * (i0 * N2 + isz * k0);
+        const int ncf = ns == 2 ? 7 : 21;
+#pragma unroll
+        for (int u = 0; u < 21; ++u) cf[u] = (ok && u < ncf) ? __ldg(slot + u) : 0.0;
+      }
+      double s = 0.0;
+      if (act) {
+        s = X[i * ld + k];
+        const int jf = i0 + isz, lf = k0 + ksz;
+        const double* pt = T1 + i * N1 + jf;
+        const double* py = X + jf * ld + k;
+#pragma unroll 4
+        for (int t = 0; t < N1 - jf; ++t) s = fmsc(s, pt[t], py[t * ld]);
+        pt = T2 + k * N2 + lf;
+        py = X + i * ld + lf;
+#pragma unroll 4
+        for (int t = 0; t < N2 - lf; ++t) s = fmsc(s, pt[t], py[t]);
+      }
+      double y = 0.0;
+      if (lg == 0) {
+        if (act) y = fdiv(s, fadd(T1[i0 * N1 + i0], T2[k0 * N2 + k0]));
+      } else {
+        const long long code = __double_as_longlong(cf[0]);
+        double b[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int src = ns > 1 ? int((code >> (2 * u)) & 3) : u;
+          b[u] = __shfl_sync(0xffffffffu, s, gbase + (src & (gs - 1)));
+        }
+        if (act) {
+          if (ns == 1) y = fdiv(s, fadd(T1[i0 * N1 + i0], T2[k0 * N2 + k0]));
+          else if (ns == 2) y = cell_solve<2>(cf, b, e);
+          else y = cell_solve<4>(cf, b, e);
+        }
+      }
+      if (act) X[i * ld + k] = y;
+    }
+    __syncwarp();
+  }
+}
+
 // One warp per element: every phase is warp-synchronous (no CTA barriers), so several elements
 // proceed independently on an SM and their dependency chains overlap.
 template <int N1, int N2>
 struct Kron2dWarpLayout {
-  static constexpr int ld = (N2 + 1) & ~1;
+  static constexpr int ld = N2 | 1;  // odd: row fibers and column accesses are conflict-free
+  static constexpr int xsz = (N1 * ld + 1) & ~1;
   static constexpr int rec = 3 * N1 * N1 + 3 * N2 * N2;
   static constexpr int hdr = (((4 + 2 * N1 + 2 * N2) / 2 + 2) & ~1);
   static constexpr int ints = N1 + N2;
-  static constexpr int per = N1 * ld + rec + (N1 + N2) + hdr + (ints + 1) / 2;
+  static constexpr int per = xsz + rec + ((N1 + N2 + 1) & ~1) + hdr + (ints + 1) / 2;
   static constexpr int per_even = (per + 1) & ~1;
 };
 
@@ -686,10 +782,10 @@ __global__ void __launch_bounds__(kSizedThreads) kron2d_sized_kernel(DevPC pc, c
   const int blk = blockIdx.x * (kSizedThreads / 32) + warp;
   if (blk >= pc.nblk || pc.kind[blk] == 0 || (pc.skip && *pc.skip)) return;
   double* sX = sm_all + size_t(warp) * L::per_even;
-  double* sR = sX + N1 * ld;
+  double* sR = sX + L::xsz;
   double* sT = sR;  // product scratch: aliases LU(A2), LU(B1) once both fiber solves are done
   double* sRcp = sR + rec;
-  double* sH = sRcp + (N1 + N2);  // Sylvester plan header (ints)
+  double* sH = sRcp + ((N1 + N2 + 1) & ~1);  // Sylvester plan header (ints)
   int* sPiv = reinterpret_cast<int*>(sH + hdr);
   const double* cells = pc.cells + size_t(blk) * pc.cells_len;
   {  // asynchronous global -> shared copies (LDGSTS), one round trip for the whole record
@@ -716,20 +812,26 @@ __global__ void __launch_bounds__(kSizedThreads) kron2d_sized_kernel(DevPC pc, c
   for (int i = lane; i < N1 + N2; i += 32)
     sRcp[i] = __drcp_rn(i < N1 ? luA2[i * N1 + i] : luB1[(i - N1) * N2 + i - N1]);
   __syncwarp();
+  if (!(KRON_SKIP & 1)) {
   // (A2^{-1} (x) I): one column fiber per lane
   for (int c = lane; c < N2; c += 32) lu_fiber_reg<N1>(luA2, sRcp, sPiv, sX + c, ld);
   __syncwarp();
   // (I (x) B1^{-1}): one row fiber per lane
   for (int r = lane; r < N1; r += 32) lu_fiber_reg<N2>(luB1, sRcp + N1, sPiv + N1, sX + r * ld, 1);
   __syncwarp();
+  }
+  if (!(KRON_SKIP & 2)) {
   warp_mm<N1, N1, N2, true, false, 2, 4>(Q1, N1, sX, ld, sT, ld, lane);  // Q1^T X
   __syncwarp();
   warp_mm<N1, N2, N2, false, false, 2, 4>(sT, ld, Q2, N2, sX, ld, lane);  // (.) Q2 -> M
   __syncwarp();
-  {  // Y overwrites M in place (sX): T1 Y + Y T2^T = M, block anti-diagonal wavefront
+  }
+  if (!(KRON_SKIP & 4)) {  // Y overwrites M in place (sX): T1 Y + Y T2^T = M, block anti-diagonal wavefront
     const int* sb = reinterpret_cast<const int*>(sH);
     const double* cc = cells + hdr;
-    if (sb[2]) {  // 1 x 1 blocks: one lane per cell; solve_tiny<1> is y = r / (t1_ii + t2_kk)
+    if (SYLV_FAST) {
+      sylv_fast<N1, N2>(T1, T2, sX, ld, sb, cc, lane, pc.status);
+    } else if (sb[2]) {  // 1 x 1 blocks: one lane per cell; solve_tiny<1> is y = r / (t1_ii + t2_kk)
       const int nb1 = sb[0], nb2 = sb[1];
       for (int step = 0; step <= nb1 + nb2 - 2; ++step) {
         const int d1lo = step - (nb2 - 1) > 0 ? step - (nb2 - 1) : 0;
@@ -748,6 +850,10 @@ __global__ void __launch_bounds__(kSizedThreads) kron2d_sized_kernel(DevPC pc, c
       sylv_wavefront<N1, N2, 1, 32, false>(T1, T2, sX, ld, 0, cc, sb, lane, pc.status);
       __syncwarp();
     }
+  }
+  if (KRON_SKIP & 8) {
+    for (int i = lane; i < N1 * N2; i += 32) out[size_t(blk) * (N1 * N2) + i] = sX[(i / N2) * ld + i % N2];
+    return;
   }
   warp_mm<N1, N1, N2, false, false, 2, 4>(Q1, N1, sX, ld, sT, ld, lane);  // Q1 Y
   __syncwarp();
@@ -892,10 +998,13 @@ __global__ void __launch_bounds__(kSizedThreads) kron2d_mma_kernel(DevPC pc, con
   for (int i = lane; i < N1 + N2; i += 32)
     sRcp[i] = 1.0 / (i < N1 ? sLU[i * N1 + i] : sLU[N1 * N1 + (i - N1) * N2 + i - N1]);
   __syncwarp();
+  if (!(KRON_SKIP & 1)) {
   for (int c = lane; c < N2; c += 32) lu_fiber_fma<N1>(sLU, sRcp, sPiv, sX + c, LX);  // A2^{-1} (x) I
   __syncwarp();
   for (int r = lane; r < N1; r += 32) lu_fiber_fma<N2>(sLU + N1 * N1, sRcp + N1, sPiv + N1, sX + r * LX, 1);
   __syncwarp();
+  }
+  if (!(KRON_SKIP & 2)) {
   {  // P = Q1^T X
     double acc[N1P / 8][N2P / 8][2];
     zero_tiles(acc);
@@ -910,12 +1019,17 @@ __global__ void __launch_bounds__(kSizedThreads) kron2d_mma_kernel(DevPC pc, con
     store_tiles(acc, sX, LX, N1P, lane);
   }
   __syncwarp();
-  {  // Y overwrites M: T1 Y + Y T2^T = M (block wavefront, inverse rows of the cell systems)
+  }
+  if (!(KRON_SKIP & 4)) {  // Y overwrites M: T1 Y + Y T2^T = M (block wavefront, inverse rows of the cell systems)
     const int* sb = reinterpret_cast<const int*>(sH);
     if (sb[3]) atomicExch(pc.status, int(TPDG_SINGULAR));
     sylv_wavefront<N1, N2, 1, 32, false, true, true>(sT1, sT2, sX, LX, 0, pc.cinv + size_t(blk) * (4 * N1 * N2), sb,
                                                      lane, pc.status);
     __syncwarp();
+  }
+  if (KRON_SKIP & 8) {
+    for (int i = lane; i < N1 * N2; i += 32) out[size_t(blk) * (N1 * N2) + i] = sX[(i / N2) * LX + i % N2];
+    return;
   }
   {  // Z = Q1 Y
     double acc[N1P / 8][N2P / 8][2];
@@ -1450,7 +1564,15 @@ void launch_pc_apply(const DevPC& pc, const double* in, double* out, cudaStream_
   if (smem > 227 * 1024)
     throw Failure{TPDG_CONFIG, "pc_apply: factor record of " + std::to_string(smem) + " B exceeds shared memory"};
   if (pc.dim == 2) {
-    if (!(!pc.faithful && launch_kron2d_mma(pc, in, out, st)) && !launch_kron2d_sized(pc, in, out, st)) {
+    // default: the bit-faithful multi-block kernel (kron_ew.cu); TPDG_GPU_KRON=mma / sized selects
+    // the tensor-core (not faithful) / one-block-per-warp kernels for comparison
+    static const int kmode = [] {
+      const char* k = std::getenv("TPDG_GPU_KRON");
+      return !k ? 0 : k[0] == 'm' ? 1 : k[0] == 's' ? 2 : 0;
+    }();
+    const bool done = (kmode == 0 && launch_kron2d_ew(pc, in, out, st)) ||
+                      (kmode == 1 && !pc.faithful && launch_kron2d_mma(pc, in, out, st));
+    if (!done && !launch_kron2d_sized(pc, in, out, st)) {
       set_smem(kron2d_apply_kernel, smem, c2);
       kron2d_apply_kernel<<<pc.nblk, kApplyThreads, smem, st>>>(pc, in, out);
     }

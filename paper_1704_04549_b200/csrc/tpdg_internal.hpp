@@ -103,6 +103,8 @@ void launch_jv(const DevSys& s, const double* vin, const double* halo, double* v
 bool launch_jv2d_mma(const DevSys& s, const double* vin, const double* halo, double* vout, cudaStream_t st);
 size_t jv_smem_bytes(const DevSys& s);
 void launch_pc_apply(const DevPC& pc, const double* in, double* out, cudaStream_t st);
+// bit-faithful 2D apply, several blocks per warp (kron_ew.cu); false if no sized variant fits
+bool launch_kron2d_ew(const DevPC& pc, const double* in, double* out, cudaStream_t st);
 // Factor the data-independent tiny Sylvester systems of every Kronecker block into pc.cells.
 void launch_sylv_cells(const DevPC& pc, double* cells, double* cinv, cudaStream_t st);
 void launch_shuffled(const DevSys& s, int e, int comp, int transpose, const double* in, double* out,

@@ -44,6 +44,11 @@ def lib():
         L.or_pc_has_factors.argtypes = [C.c_void_p, C.c_int]
         L.or_pc_factors.argtypes = [C.c_void_p, C.c_int, dp]
         L.or_pc_apply.argtypes = [C.c_void_p, dp, dp]
+        L.or_pc_record_len.argtypes = [C.c_void_p]
+        L.or_pc_record_len.restype = C.c_int
+        L.or_pc_piv_len.argtypes = [C.c_void_p]
+        L.or_pc_piv_len.restype = C.c_int
+        L.or_pc_record.argtypes = [C.c_void_p, C.c_int, dp, ip]
         L.or_gmres.argtypes = [C.POINTER(OrSys), C.c_double, C.c_double, C.c_int, C.c_void_p, dp, C.c_double,
                                C.c_int, C.c_int, C.c_int, dp, ip, dp, C.c_int, ip]
         _lib = L
@@ -138,6 +143,13 @@ class OraclePC:
         out = np.zeros(lib().or_pc_factor_len(self.h))
         lib().or_pc_factors(self.h, blk, ptr(out))
         return out
+
+    def record(self, blk):
+        """(LU factors + Schur pairs, pivots) of one factored block."""
+        rec = np.zeros(lib().or_pc_record_len(self.h))
+        piv = np.zeros(lib().or_pc_piv_len(self.h), dtype=np.int32)
+        lib().or_pc_record(self.h, blk, ptr(rec), piv.ctypes.data_as(ip))
+        return rec, piv
 
     def apply(self, x):
         out = np.zeros(self.sys.N)
