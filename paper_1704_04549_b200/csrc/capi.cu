@@ -166,7 +166,7 @@ struct tpdg_gpu_pc_s {
   tpdg_gpu_op op = nullptr;
   DevPC pc{};
   int nblk = 0, raw_len = 0;
-  DevBuf raw, rec, piv, kind, fb_slot, fb_lu, fb_piv, status, cells, cinv;
+  DevBuf raw, rec, piv, kind, fb_slot, fb_list, fb_lu, fb_piv, status, cells, cinv;
   std::vector<int> kind_h;
   std::vector<int64_t> fallbacks;  // (element, component)
 };
@@ -549,7 +549,8 @@ void finish_pc(tpdg_gpu_pc pc) {
   const int nfb = int(fb_blocks.size());
   const int nb = op->s.small ? op->s.npe : op->n_c * op->s.npe;
   if (nfb) {
-    DevBuf blocks, work;
+    DevBuf work;
+    DevBuf& blocks = pc->fb_list;
     upload(blocks, fb_blocks.data(), fb_blocks.size(), st);
     pc->fb_lu.alloc(sizeof(double) * size_t(nfb) * nb * nb);
     pc->fb_piv.alloc(sizeof(int) * size_t(nfb) * nb);
@@ -571,6 +572,8 @@ void finish_pc(tpdg_gpu_pc pc) {
   d.kind = pc->kind.as<int>();
   d.fb_slot = pc->fb_slot.as<int>();
   d.fb_lu = nfb ? pc->fb_lu.as<double>() : nullptr;
+  d.fb_list = nfb ? pc->fb_list.as<int>() : nullptr;
+  d.n_fb = nfb;
   d.fb_piv = nfb ? pc->fb_piv.as<int>() : nullptr;
   d.status = pc->status.as<int>();
   {

@@ -1584,8 +1584,10 @@ void launch_pc_apply(const DevPC& pc, const double* in, double* out, cudaStream_
   ++g_launches;
   if (pc.fb_lu) {
     const size_t fsm = sizeof(double) * size_t(pc.blk_len);
-    set_smem(kron_fallback_kernel, fsm, cf);
-    kron_fallback_kernel<<<pc.nblk, 256, fsm, st>>>(pc, in, out);
+    if (!launch_fallback_apply(pc, in, out, st)) {  // blocks beyond 2048 rows: one column sweep per step
+      set_smem(kron_fallback_kernel, fsm, cf);
+      kron_fallback_kernel<<<pc.nblk, 256, fsm, st>>>(pc, in, out);
+    }
     TPDG_CUDA_CHECK(cudaGetLastError());
     ++g_launches;
   }

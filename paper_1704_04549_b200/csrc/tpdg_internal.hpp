@@ -76,6 +76,8 @@ struct DevPC {
   const int* fb_slot;    // [nblk]: slot into fb_lu for fallback blocks, -1 otherwise
   const double* fb_lu;   // [n_fb][blk_len^2]
   const int* fb_piv;     // [n_fb][blk_len]
+  const int* fb_list;    // [n_fb]: block of each fallback slot
+  int n_fb;
   int faithful;          // 1: bit-faithful kernels only (TPDG_GPU_FAITHFUL=1), 0: tensor-core apply
   const double* cells;   // [nblk][cells_len]: Sylvester plan + factored tiny systems (sylv_cells_len)
   int cells_len;
@@ -105,6 +107,8 @@ size_t jv_smem_bytes(const DevSys& s);
 void launch_pc_apply(const DevPC& pc, const double* in, double* out, cudaStream_t st);
 // bit-faithful 2D apply, several blocks per warp (kron_ew.cu); false if no sized variant fits
 bool launch_kron2d_ew(const DevPC& pc, const double* in, double* out, cudaStream_t st);
+// dense-LU fallback blocks, one CTA per fallback block (kron_fallback.cu); false if n is too large
+bool launch_fallback_apply(const DevPC& pc, const double* in, double* out, cudaStream_t st);
 // Factor the data-independent tiny Sylvester systems of every Kronecker block into pc.cells.
 void launch_sylv_cells(const DevPC& pc, double* cells, double* cinv, cudaStream_t st);
 void launch_shuffled(const DevSys& s, int e, int comp, int transpose, const double* in, double* out,
