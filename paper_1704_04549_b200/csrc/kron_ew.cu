@@ -55,6 +55,10 @@ __device__ __forceinline__ void copy_mat(double* dst, const double* src, int li)
   }
 }
 
+#ifndef EW_SKIP
+#define EW_SKIP 0  // study builds only (tools/kron_variants.sh): bit mask of skipped phases
+#endif
+
 template <int N>
 struct Ew {
   static constexpr int EW = N <= 5 ? 6 : N <= 9 ? 3 : N <= 16 ? 2 : 1;  // blocks per warp
@@ -178,7 +182,7 @@ __device__ __forceinline__ void mm_tile(const double* A, int lda, const double* 
 // Replays a factored tiny system (slot [code, L, U, diag, 1/diag], sylv_cells_kernel) on the
 // permuted right-hand side b; on return b[u] is unknown u (solve_tiny, sylvester.hpp:34-61).
 template <int NS>
-__device__ __forceinline__ void replay(const double (&cf)[22], double (&b)[4]) {
+__device__ __forceinline__ void replay(const double* cf, double (&b)[4]) {
   constexpr int NL = NS * (NS - 1) / 2;
   int o = 1;
 #pragma unroll
@@ -236,14 +240,14 @@ __global__ void __launch_bounds__(32, 16) kron2d_ew_kernel(DevPC pc, const doubl
   }
   __syncwarp();
   // (A2^{-1} (x) I): column fibers, then (I (x) B1^{-1}): row fibers
-  if (act) lu_fiber<N>(R1, rcp, piv, X + li, LD);
+  if (act && !(EW_SKIP & 1)) lu_fiber<N>(R1, rcp, piv, X + li, LD);
   __syncwarp();
-  if (act) lu_fiber<N>(R1 + N * N, rcp + N, piv + N, X + li * LD, 1);
+  if (act && !(EW_SKIP & 1)) lu_fiber<N>(R1 + N * N, rcp + N, piv + N, X + li * LD, 1);
   __syncwarp();
   // M = (Q1^T X) Q2
-  if (act) mm_tile<N, true, false, true, false>(Q1, N, X, LD, R1, LD, li);
+  if (act && !(EW_SKIP & 2)) mm_tile<N, true, false, true, false>(Q1, N, X, LD, R1, LD, li);
   __syncwarp();
-  if (act) mm_tile<N, false, false, false, true>(R1, LD, Q2, N, X, LD, li);
+  if (act && !(EW_SKIP & 2)) mm_tile<N, false, false, false, true>(R1, LD, Q2, N, X, LD, li);
   __syncwarp();
   // T1 | T2 into R1
   if (act) {
@@ -260,7 +264,7 @@ __global__ void __launch_bounds__(32, 16) kron2d_ew_kernel(DevPC pc, const doubl
     const int *s1 = hdr + 4, *z1 = s1 + N, *s2 = z1 + N, *z2 = s2 + N;
     const double* cc = cells + C::HDR;
     double* scr = sm_all + C::EW * C::PER + 4 * lane;  // per-lane scratch: the cell's right-hand sides
-    const int last = __reduce_max_sync(0xffffffffu, act ? nb1 + nb2 - 2 : -1);
+    const int last = (EW_SKIP & 4) ? -1 : __reduce_max_sync(0xffffffffu, act ? nb1 + nb2 - 2 : -1);
     // cell of this lane at step st (valid = inside the anti-diagonal) and its factor slot
     auto cell_at = [&](int st, int& i0, int& isz, int& k0, int& ksz) {
       const int d1lo = st - (nb2 - 1) > 0 ? st - (nb2 - 1) : 0;
@@ -284,17 +288,18 @@ __global__ void __launch_bounds__(32, 16) kron2d_ew_kernel(DevPC pc, const doubl
         c[2 * u + 1] = v.y;
       }
     };
-    int ci0, cisz, ck0, cksz;
-    bool cok = cell_at(0, ci0, cisz, ck0, cksz);
-    double cf[22];
-    load_cf(cok, ci0, cisz, ck0, cksz, cf);
-    for (int st = 0; st <= last; ++st) {
-      int ni0, nisz, nk0, nksz;
-      const bool nok = cell_at(st + 1, ni0, nisz, nk0, nksz);
-      double cn[22];
-      load_cf(nok, ni0, nisz, nk0, nksz, cn);  // next step's factors: latency hidden behind this step
-      if (cok) {
-        const int i0 = ci0, isz = cisz, k0 = ck0, ksz = cksz, ns = isz * ksz;
+    struct Cell {
+      bool ok;
+      int i0, isz, k0, ksz;
+      double cf[22];
+    };
+    // one wavefront step with this lane's cell `c`; the next step's cell is located and its
+    // factors loaded into `n` first, so their latency hides behind this step
+    auto step = [&](int st, const Cell& c, Cell& n) {
+      n.ok = cell_at(st + 1, n.i0, n.isz, n.k0, n.ksz);
+      load_cf(n.ok, n.i0, n.isz, n.k0, n.ksz, n.cf);
+      if (c.ok) {
+        const int i0 = c.i0, isz = c.isz, k0 = c.k0, ksz = c.ksz, ns = isz * ksz;
         const int i1 = i0 + isz - 1, k1 = k0 + ksz - 1;
         double s00 = X[i0 * LD + k0], s01 = X[i0 * LD + k1], s10 = X[i1 * LD + k0], s11 = X[i1 * LD + k1];
         {  // solved rows below (j ascending), then solved columns to the right (l ascending)
@@ -323,6 +328,7 @@ __global__ void __launch_bounds__(32, 16) kron2d_ew_kernel(DevPC pc, const doubl
             s11 = fmsc(s11, u1, w1);
           }
         }
+        const double* cf = c.cf;
         if (ns == 1) {
           X[i0 * LD + k0] = fdiv_rcp(s00, cf[1], cf[2]);
         } else {
@@ -336,11 +342,11 @@ __global__ void __launch_bounds__(32, 16) kron2d_ew_kernel(DevPC pc, const doubl
 #pragma unroll
           for (int u = 0; u < 4; ++u) b[u] = scr[int((code >> (2 * u)) & 3)];
           if (ns == 2) {
-            replay<2>(cf, b);
+            replay<2>(c.cf, b);
             X[i0 * LD + k0] = b[0];
             X[i1 * LD + k1] = b[1];  // (0, 1) or (1, 0)
           } else {
-            replay<4>(cf, b);
+            replay<4>(c.cf, b);
             X[i0 * LD + k0] = b[0];
             X[i0 * LD + k1] = b[1];
             X[i1 * LD + k0] = b[2];
@@ -349,19 +355,19 @@ __global__ void __launch_bounds__(32, 16) kron2d_ew_kernel(DevPC pc, const doubl
         }
       }
       __syncwarp();
-#pragma unroll
-      for (int u = 0; u < 22; ++u) cf[u] = cn[u];
-      cok = nok;
-      ci0 = ni0;
-      cisz = nisz;
-      ck0 = nk0;
-      cksz = nksz;
+    };
+    Cell ca, cb;
+    ca.ok = cell_at(0, ca.i0, ca.isz, ca.k0, ca.ksz);
+    load_cf(ca.ok, ca.i0, ca.isz, ca.k0, ca.ksz, ca.cf);
+    for (int st = 0; st <= last; st += 2) {  // ping-pong between the two cell buffers
+      step(st, ca, cb);
+      if (st + 1 <= last) step(st + 1, cb, ca);
     }
   }
   // X = (Q1 Y) Q2^T
-  if (act) mm_tile<N, false, false, true, false>(Q1, N, X, LD, R1, LD, li);
+  if (act && !(EW_SKIP & 8)) mm_tile<N, false, false, true, false>(Q1, N, X, LD, R1, LD, li);
   __syncwarp();
-  if (act) mm_tile<N, false, true, false, true>(R1, LD, Q2, N, X, LD, li);
+  if (act && !(EW_SKIP & 8)) mm_tile<N, false, true, false, true>(R1, LD, Q2, N, X, LD, li);
   __syncwarp();
   if (act) {
     double* o = out + size_t(blk) * (N * N);

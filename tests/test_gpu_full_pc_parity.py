@@ -72,17 +72,37 @@ def test_full_degree_pc_apply(ctx, p, faithful):
     assert err_f <= 1e-8
 
 
-@pytest.mark.parametrize("p", [8, 15])
-def test_full_degree_pc_apply_tensor_core_variant(ctx, p):
-    """TPDG_GPU_KRON=mma: the (non-faithful) DMMA apply, reported against the reference at full size."""
-    sub, osys = slice_system(p)
+
+def slice_system_3d(K3=64):
+    """cfg4 (16^3 hexes, p = 10, velocity (1, 0.7, 0.4), dt = 0.01): the first K3 elements."""
+    s = T.setup_advection("const3d", 16, 16, 16, p=10, vel=(1.0, 0.7, 0.4))
+    a, mu, q = s.arrays, s.mu, 11
+    nf = mu * mu
+    conn = a["conn"][: K3 * 6 * 3].reshape(K3, 6, 3).copy()
+    conn[:, :, 0] %= K3
+    arrays = {"g": a["g"], "d": a["d"], "gw": a["gw"], "dw": a["dw"], "w": a["w"],
+              "jdet": a["jdet"][: K3 * mu ** 3], "face_w": a["face_w"][: K3 * 6 * nf], "conn": conn.ravel(),
+              "dft": a["dft"][: K3 * 3 * mu ** 3], "dfm": a["dfm"][: K3 * 6 * nf], "dfp": a["dfp"][: K3 * 6 * nf]}
+    sub = T.System(3, 1, 10, mu, K3, arrays)
+    ometa = np.array([3, 1, 10, mu, K3, 0.01, 0, 16, 16, 16, 1.0, 1.0])
+    osys = O.System({"meta": ometa, "ref_g": a["g"], "ref_d": a["d"], "ref_gw": a["gw"], "ref_dw": a["dw"],
+                     "ref_w": a["w"], "jdet": arrays["jdet"], "face_w": arrays["face_w"], "conn": arrays["conn"],
+                     "dft": arrays["dft"], "dfm": arrays["dfm"], "dfp": arrays["dfp"],
+                     "start_vec": T.seeded_unit_vector(q ** 4), "start_vec2": T.seeded_unit_vector(q * q)})
+    return sub, osys, K3
+
+
+def test_full_size_cfg4_pc_apply(ctx):
+    """3D (cfg4) apply at its full degree with the reference's LU / Schur factors (default kernels)."""
+    sub, osys, K3 = slice_system_3d()
     opc = osys.form()
     has = opc.has()
-    fb = [b for b in range(K) if has[b]]
+    fb = [b for b in range(K3) if has[b]]
     fac = np.concatenate([opc.factors(b) for b in fb])
     rec = [opc.record(b) for b in fb]
-    op = T.LinearizedOperator(ctx, sub, 0.005)
+    op = T.LinearizedOperator(ctx, sub, 0.01)
     pc = T.import_record(op, fac, has, np.concatenate([r for r, _ in rec]), np.concatenate([pv for _, pv in rec]))
     x = T.uniform_vector(7, sub.N, 1.0)
-    print(f"p={p}: default (faithful) apply {O.rel_l2(pc.apply(x), opc.apply(x)):.3e}")
-    assert O.rel_l2(pc.apply(x), opc.apply(x)) <= 1e-12
+    err = O.rel_l2(pc.apply(x), opc.apply(x))
+    print(f"cfg4 slice: {len(fb)}/{K3} factored blocks, PC apply rel-L2 vs reference {err:.3e}")
+    assert err <= 1e-12

@@ -1,6 +1,6 @@
 #!/bin/bash
 # Study builds: libtpdg_gpu.so variants with kron.cu compiled under extra flags, e.g.
-#   tools/kron_variants.sh skip1:-DKRON_SKIP=1 skip4:-DKRON_SKIP=4
+#   [SRC=kron_ew] tools/kron_variants.sh skip1:-DKRON_SKIP=1 skip4:-DKRON_SKIP=4
 # -> paper_1704_04549_b200/_build/var/<name>/libtpdg_gpu.so (select with TPDG_GPU_LIB=...)
 set -e
 R=$(cd "$(dirname "$0")/.." && pwd)
@@ -11,9 +11,9 @@ for spec in "$@"; do
   name=${spec%%:*}; flags=${spec#*:}
   (d=$P/_build/var/$name; mkdir -p $d
    /usr/local/cuda/bin/nvcc -O3 -std=c++17 $ARCH -lineinfo -Xcompiler -fPIC -I$P/csrc -I$R/include \
-     --expt-relaxed-constexpr -fmad=false $flags -c $P/csrc/kron.cu -o $d/kron.o
-   objs=$(ls $P/_build/*.o | grep -v '/kron.o$')
-   /usr/local/cuda/bin/nvcc $ARCH -shared -o $d/libtpdg_gpu.so $d/kron.o $objs -L/usr/lib/x86_64-linux-gnu -lnccl
+     --expt-relaxed-constexpr -fmad=false $flags -c $P/csrc/${SRC:-kron}.cu -o $d/${SRC:-kron}.o
+   objs=$(ls $P/_build/*.o | grep -v "/${SRC:-kron}.o$")
+   /usr/local/cuda/bin/nvcc $ARCH -shared -o $d/libtpdg_gpu.so $d/${SRC:-kron}.o $objs -L/usr/lib/x86_64-linux-gnu -lnccl
    echo built $name) &
 done
 wait
