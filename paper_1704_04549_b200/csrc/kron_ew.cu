@@ -55,6 +55,9 @@ __device__ __forceinline__ void copy_mat(double* dst, const double* src, int li)
   }
 }
 
+#ifndef EW_CLOCK
+#define EW_CLOCK 0  // study builds only: clock64 breakdown of the Sylvester steps (block 100, lane 0)
+#endif
 #ifndef EW_SKIP
 #define EW_SKIP 0  // study builds only (tools/kron_variants.sh): bit mask of skipped phases
 #endif
@@ -288,18 +291,21 @@ __global__ void __launch_bounds__(32, 16) kron2d_ew_kernel(DevPC pc, const doubl
         c[2 * u + 1] = v.y;
       }
     };
-    struct Cell {
-      bool ok;
-      int i0, isz, k0, ksz;
-      double cf[22];
-    };
-    // one wavefront step with this lane's cell `c`; the next step's cell is located and its
-    // factors loaded into `n` first, so their latency hides behind this step
-    auto step = [&](int st, const Cell& c, Cell& n) {
-      n.ok = cell_at(st + 1, n.i0, n.isz, n.k0, n.ksz);
-      load_cf(n.ok, n.i0, n.isz, n.k0, n.ksz, n.cf);
-      if (c.ok) {
-        const int i0 = c.i0, isz = c.isz, k0 = c.k0, ksz = c.ksz, ns = isz * ksz;
+    long long t_a = 0, t_b = 0, t_c = 0;
+    // one wavefront step with this lane's cell (ok, i0, isz, k0, ksz); the next step's cell is
+    // located first and its factor slot prefetched into L1, so that the factors, loaded after
+    // the chains (registers stay free for the chains' load pipelining), arrive from L1
+    auto step = [&](int st, bool ok, int i0, int isz, int k0, int ksz, bool& nok, int& ni0, int& nisz, int& nk0,
+                    int& nksz) {
+      long long c0 = EW_CLOCK ? clock64() : 0;
+      nok = cell_at(st + 1, ni0, nisz, nk0, nksz);
+      if (nok) {
+        const double* sp = cc + 6 * (ni0 * N + nisz * nk0);
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(sp));
+        if (nisz * nksz == 4) asm volatile("prefetch.global.L1 [%0];" ::"l"(sp + 16));
+      }
+      if (ok) {
+        const int ns = isz * ksz;
         const int i1 = i0 + isz - 1, k1 = k0 + ksz - 1;
         double s00 = X[i0 * LD + k0], s01 = X[i0 * LD + k1], s10 = X[i1 * LD + k0], s11 = X[i1 * LD + k1];
         {  // solved rows below (j ascending), then solved columns to the right (l ascending)
@@ -328,7 +334,13 @@ __global__ void __launch_bounds__(32, 16) kron2d_ew_kernel(DevPC pc, const doubl
             s11 = fmsc(s11, u1, w1);
           }
         }
-        const double* cf = c.cf;
+        if (EW_CLOCK) {
+          const long long c1 = clock64();
+          t_a += c1 - c0;
+          c0 = c1;
+        }
+        double cf[22];
+        load_cf(true, i0, isz, k0, ksz, cf);
         if (ns == 1) {
           X[i0 * LD + k0] = fdiv_rcp(s00, cf[1], cf[2]);
         } else {
@@ -342,11 +354,11 @@ __global__ void __launch_bounds__(32, 16) kron2d_ew_kernel(DevPC pc, const doubl
 #pragma unroll
           for (int u = 0; u < 4; ++u) b[u] = scr[int((code >> (2 * u)) & 3)];
           if (ns == 2) {
-            replay<2>(c.cf, b);
+            replay<2>(cf, b);
             X[i0 * LD + k0] = b[0];
             X[i1 * LD + k1] = b[1];  // (0, 1) or (1, 0)
           } else {
-            replay<4>(c.cf, b);
+            replay<4>(cf, b);
             X[i0 * LD + k0] = b[0];
             X[i0 * LD + k1] = b[1];
             X[i1 * LD + k0] = b[2];
@@ -354,15 +366,25 @@ __global__ void __launch_bounds__(32, 16) kron2d_ew_kernel(DevPC pc, const doubl
           }
         }
       }
+      if (EW_CLOCK) {
+        const long long c1 = clock64();
+        t_b += c1 - c0;
+        c0 = c1;
+      }
       __syncwarp();
+      if (EW_CLOCK) t_c += clock64() - c0;
     };
-    Cell ca, cb;
-    ca.ok = cell_at(0, ca.i0, ca.isz, ca.k0, ca.ksz);
-    load_cf(ca.ok, ca.i0, ca.isz, ca.k0, ca.ksz, ca.cf);
-    for (int st = 0; st <= last; st += 2) {  // ping-pong between the two cell buffers
-      step(st, ca, cb);
-      if (st + 1 <= last) step(st + 1, cb, ca);
+    bool aok, bok;
+    int ai0, aisz, ak0, aksz, bi0, bisz, bk0, bksz;
+    aok = cell_at(0, ai0, aisz, ak0, aksz);
+    const long long t0 = EW_CLOCK ? clock64() : 0;
+    for (int st = 0; st <= last; st += 2) {  // ping-pong between the two cell descriptors
+      step(st, aok, ai0, aisz, ak0, aksz, bok, bi0, bisz, bk0, bksz);
+      if (st + 1 <= last) step(st + 1, bok, bi0, bisz, bk0, bksz, aok, ai0, aisz, ak0, aksz);
     }
+    if (EW_CLOCK && blockIdx.x == 100 && lane == 0)
+      printf("ew clock: steps %d, total %lld cycles, chains(lane0) %lld, solve %lld, sync %lld\n", last + 1,
+             clock64() - t0, t_a, t_b, t_c);
   }
   // X = (Q1 Y) Q2^T
   if (act && !(EW_SKIP & 8)) mm_tile<N, false, false, true, false>(Q1, N, X, LD, R1, LD, li);
