@@ -502,11 +502,14 @@ def _gcfg(cfg):
     return _GmresCfg(cfg.tol, cfg.restart, cfg.max_iterations, 0 if cfg.side == "right" else 1)
 
 
-def gmres(op: LinearizedOperator, pc: KsvdPC | None, b, cfg: GmresConfig | None = None) -> GmresResult:
-    """Restarted GMRES (solve/gmres.hpp:52) with host arrays; raises GmresFailure on budget."""
+def gmres(op: LinearizedOperator, pc: KsvdPC | None, b, cfg: GmresConfig | None = None, out=None) -> GmresResult:
+    """Restarted GMRES (solve/gmres.hpp:52) with host arrays; raises GmresFailure on budget.
+    out: optional preallocated (e.g. pinned) float64 host array for x."""
     cfg = cfg or GmresConfig()
     b = np.ascontiguousarray(b, dtype=np.float64)
-    x = np.empty(op.n_local)
+    x = out if out is not None else np.empty(op.n_local)
+    if x.dtype != np.float64 or not x.flags["C_CONTIGUOUS"] or x.size != op.n_local:
+        raise ShapeError("gmres: out must be a contiguous float64 array of the local size")
     its = C.c_int()
     conv = C.c_int()
     hist = np.zeros(cfg.max_iterations + 1)

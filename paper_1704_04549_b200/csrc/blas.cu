@@ -726,9 +726,10 @@ void launch_norm(const double* x, int64_t n, double* partial, double* result, un
 }
 
 void launch_mgs_step(double* w, const double* vprev, const double* hprev, const double* vj, int64_t n,
-                     double* partial, double* result, unsigned* counter, cudaStream_t st, const int* skip) {
+                     double* partial, double* result, unsigned* counter, cudaStream_t st, const int* skip,
+                     bool sqrt_norm) {
   mgs_kernel<<<reduce_grid(n), kRedThreads, 0, st>>>(w, vprev, hprev, vj, n, partial, result, counter,
-                                                      vj == nullptr ? 1 : 0, skip);
+                                                      vj == nullptr && sqrt_norm ? 1 : 0, skip);
   TPDG_CUDA_CHECK(cudaGetLastError());
   ++g_launches;
 }

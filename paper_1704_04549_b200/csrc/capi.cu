@@ -333,7 +333,13 @@ int run_gmres(tpdg_gpu_op op, tpdg_gpu_pc pc, const double* d_b, double* d_x, co
   const int64_t n = op->n_local_dofs;
   const bool right = cfg.side == 0;
   const int m = cfg.restart;
-  const bool multi = ctx->nranks > 1;
+  // multi-rank MGS (one fused w-update + partial dot kernel and one allreduce per pass);
+  // TPDG_GPU_MULTI_MGS=1 selects it on one rank too (tests of the multi-rank code path)
+  static const bool force_multi = [] {
+    const char* f = std::getenv("TPDG_GPU_MULTI_MGS");
+    return f && f[0] == '1';
+  }();
+  const bool multi = ctx->nranks > 1 || force_multi;
   const int64_t ldv = (n + 31) & ~int64_t(31);  // 256 B aligned Krylov slices (vectorized passes)
   GmresWork& W = op->gws;
   if (W.n != n || W.m != m) {
@@ -442,13 +448,12 @@ int run_gmres(tpdg_gpu_op op, tpdg_gpu_pc pc, const double* d_b, double* d_x, co
         if (!multi) {  // fused MGS passes + normalization (one cooperative launch)
           launch_mgs_iteration(V, ldv, k, n, hc, part, ctr + 4, G.done, st);
         } else {
-          for (int j = 0; j <= k; ++j) {  // MGS with a cross-rank reduction per dot
-            if (j > 0) launch_axpy_neg(w, hc + j - 1, V + size_t(j - 1) * ldv, n, st);
-            launch_dot(V + size_t(j) * ldv, w, n, part, hc + j, ctr, st);
+          for (int j = 0; j <= k; ++j) {  // pass j: w -= h_{j-1} v_{j-1}, then h_j = <v_j, w> over all ranks
+            launch_mgs_step(w, j > 0 ? V + size_t(j - 1) * ldv : nullptr, j > 0 ? hc + j - 1 : nullptr,
+                            V + size_t(j) * ldv, n, part, hc + j, ctr, st, G.done);
             allreduce_scalar(ctx, hc + j);
           }
-          launch_axpy_neg(w, hc + k, vk, n, st);
-          launch_dot(w, w, n, part, hc + k + 1, ctr, st);
+          launch_mgs_step(w, vk, hc + k, nullptr, n, part, hc + k + 1, ctr, st, G.done, false);  // <w, w>
           allreduce_scalar(ctx, hc + k + 1);
           sqrt_inplace_kernel<<<1, 1, 0, st>>>(hc + k + 1);
           ++g_launches;

@@ -46,15 +46,18 @@ __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefe
 
 // LEN contiguous doubles global -> shared by the N lanes of one block: 16-byte copies when both
 // ends are aligned (even N: every offset used here is even), else 8-byte copies.
-template <int LEN, int N>
+template <int LEN, int N, int P>
 __device__ __forceinline__ void copy_mat(double* dst, const double* src, int li) {
   if ((N & 1) == 0 && ((reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src)) & 15) == 0) {
-    for (int i = 2 * li; i < LEN; i += 2 * N) cpa16(dst + i, src + i);
+    for (int i = 2 * li; i < LEN; i += 2 * P) cpa16(dst + i, src + i);
   } else {
-    for (int i = li; i < LEN; i += N) cpa8(dst + i, src + i);
+    for (int i = li; i < LEN; i += P) cpa8(dst + i, src + i);
   }
 }
 
+#ifndef EW16_LANES
+#define EW16_LANES 16  // lanes per block at N = 16 (2 blocks per warp); 8 (4 per warp) measured 114 vs 91 us
+#endif
 #ifndef EW_CLOCK
 #define EW_CLOCK 0  // study builds only: clock64 breakdown of the Sylvester steps (block 100, lane 0)
 #endif
@@ -62,9 +65,9 @@ __device__ __forceinline__ void copy_mat(double* dst, const double* src, int li)
 #define EW_SKIP 0  // study builds only (tools/kron_variants.sh): bit mask of skipped phases
 #endif
 
-template <int N>
+template <int N, int P = N>  // P lanes per block
 struct Ew {
-  static constexpr int EW = N <= 5 ? 6 : N <= 9 ? 3 : N <= 16 ? 2 : 1;  // blocks per warp
+  static constexpr int EW = 32 / P;  // blocks per warp
   static constexpr int LD = N + 3;
   static constexpr int XSZ = (N * LD + 1) & ~1;
   static constexpr int R1 = (2 * N * N > XSZ ? 2 * N * N : XSZ);
@@ -72,11 +75,12 @@ struct Ew {
   static constexpr int O_X = R1, O_RCP = O_X + XSZ, O_H = O_RCP + 2 * N, O_PIV = O_H + HDR;
   static constexpr int PER0 = O_PIV + N;                   // 2N int pivots
   static constexpr int PER = PER0 + ((8 - PER0 % 16) + 16) % 16;  // = 8 (mod 16): slots start half a bank row apart
-  // rotation tile (TI x TJ per lane, N lanes per block)
-  static constexpr int TI = N == 16 ? 4 : N == 9 ? 3 : N == 21 ? 3 : 1;
-  static constexpr int TJ = N == 16 ? 4 : N == 9 ? 3 : N == 21 ? 7 : N;
+  // rotation tile (TI x TJ per lane, P lanes per block)
+  static constexpr int TI = P == 8 && N == 16 ? 4 : N == 16 ? 4 : N == 9 ? 3 : N == 21 ? 3 : 1;
+  static constexpr int TJ = P == 8 && N == 16 ? 8 : N == 16 ? 4 : N == 9 ? 3 : N == 21 ? 7 : N;
   static constexpr int NTJ = N / TJ;
-  static_assert((N / TI) * (N / TJ) == N, "one tile per lane");
+  static_assert((N / TI) * (N / TJ) == P, "one tile per lane");
+  static_assert(EW * P <= 32, "lanes");
 };
 
 // x := A^{-1} x for one fiber (LuFactor::solve): gather through the pivots, forward then backward
@@ -105,14 +109,27 @@ __device__ __forceinline__ void lu_fiber(const double* __restrict__ lu, const do
   for (int k = 0; k < N; ++k) col[k * stride] = x[k];
 }
 
+// fibers li, li + P, ... of a block (P lanes per block), one call each
+template <int N, int P, typename F>
+__device__ __forceinline__ void for_fibers(int li, F&& f) {
+  f(li);
+  if constexpr (P < N) {
+    asm volatile("" ::: "memory");  // one fiber at a time (interleaving two unrolled fibers spills)
+    if (li + P < N) f(li + P);
+  }
+  if constexpr (2 * P < N) {
+    for (int c = li + 2 * P; c < N; c += P) f(c);
+  }
+}
+
 // One lane's TI x TJ tile of O = op(A) op(B) (N x N x N), k ascending (matmul order). AG / BG:
 // that operand is a Schur factor read from global memory through L1 (read-only path; the two
 // rotations reuse it), 16-byte loads when N is even; the other operand is in shared memory.
-template <int N, bool AT, bool BT, bool AG, bool BG>
+template <int N, int P, bool AT, bool BT, bool AG, bool BG>
 __device__ __forceinline__ void mm_tile(const double* A, int lda, const double* B, int ldb, double* O, int ldo,
                                         int li) {
-  using C = Ew<N>;
-  constexpr int TI = C::TI, TJ = C::TJ, KP = (N % 2 == 0) ? 2 : 1;
+  using C = Ew<N, P>;
+  constexpr int TI = C::TI, TJ = C::TJ, KP = (N % 2 == 0 && TI * TJ <= 16) ? 2 : 1;
   const int i0 = (li / C::NTJ) * TI, j0 = (li % C::NTJ) * TJ;
   double acc[TI][TJ];
 #pragma unroll
@@ -206,13 +223,13 @@ __device__ __forceinline__ void replay(const double* cf, double (&b)[4]) {
   }
 }
 
-template <int N>
-__global__ void __launch_bounds__(32, 16) kron2d_ew_kernel(DevPC pc, const double* __restrict__ in,
+template <int N, int P>
+__global__ void __launch_bounds__(32, P < N ? 7 : 16) kron2d_ew_kernel(DevPC pc, const double* __restrict__ in,
                                                         double* __restrict__ out) {
-  using C = Ew<N>;
+  using C = Ew<N, P>;
   constexpr int EW = C::EW, LD = C::LD;
   extern __shared__ double sm_all[];
-  const int lane = threadIdx.x, g = lane / N, li = lane % N;
+  const int lane = threadIdx.x, g = lane / P, li = lane % P;
   const int blk = blockIdx.x * EW + g;
   const bool act = g < EW && blk < pc.nblk && pc.kind[blk] != 0 && !(pc.skip && *pc.skip);
   double* S = sm_all + (g < EW ? g : 0) * C::PER;
@@ -227,35 +244,38 @@ __global__ void __launch_bounds__(32, 16) kron2d_ew_kernel(DevPC pc, const doubl
   const double* cells = pc.cells + size_t(act ? blk : 0) * pc.cells_len;
   if (act) {
     // L2 prefetch of what the later phases read: Q1 | T1 | Q2 | T2 and the cell factors
-    for (int o = 16 * li; o < 4 * N * N; o += 16 * N) prefetch_l2(rec + 2 * N * N + o);
-    for (int o = C::HDR + 16 * li; o < pc.cells_len; o += 16 * N) prefetch_l2(cells + o);
-    copy_mat<2 * N * N, N>(R1, rec, li);               // LU(A2) | LU(B1)
-    for (int i = 2 * li; i < C::HDR; i += 2 * N) cpa16(reinterpret_cast<double*>(hdr) + i, cells + i);
-    for (int i = li; i < 2 * N; i += N) cpa4(piv + i, pc.piv + size_t(blk) * (2 * N) + i);
+    for (int o = 16 * li; o < 4 * N * N; o += 16 * P) prefetch_l2(rec + 2 * N * N + o);
+    for (int o = C::HDR + 16 * li; o < pc.cells_len; o += 16 * P) prefetch_l2(cells + o);
+    copy_mat<2 * N * N, N, P>(R1, rec, li);               // LU(A2) | LU(B1)
+    for (int i = 2 * li; i < C::HDR; i += 2 * P) cpa16(reinterpret_cast<double*>(hdr) + i, cells + i);
+    for (int i = li; i < 2 * N; i += P) cpa4(piv + i, pc.piv + size_t(blk) * (2 * N) + i);
     const double* x = in + size_t(blk) * (N * N);
-    for (int i = li; i < N * N; i += N) cpa8(X + (i / N) * LD + i % N, x + i);
+    for (int i = li; i < N * N; i += P) cpa8(X + (i / N) * LD + i % N, x + i);
   }
   cpa_wait();
   __syncwarp();
-  if (act) {
-    rcp[li] = __drcp_rn(R1[li * N + li]);
-    rcp[N + li] = __drcp_rn(R1[N * N + li * N + li]);
-  }
+  if (act)
+    for (int i = li; i < N; i += P) {
+      rcp[i] = __drcp_rn(R1[i * N + i]);
+      rcp[N + i] = __drcp_rn(R1[N * N + i * N + i]);
+    }
   __syncwarp();
   // (A2^{-1} (x) I): column fibers, then (I (x) B1^{-1}): row fibers
-  if (act && !(EW_SKIP & 1)) lu_fiber<N>(R1, rcp, piv, X + li, LD);
+  if (act && !(EW_SKIP & 1))
+    for_fibers<N, P>(li, [&](int c) { lu_fiber<N>(R1, rcp, piv, X + c, LD); });
   __syncwarp();
-  if (act && !(EW_SKIP & 1)) lu_fiber<N>(R1 + N * N, rcp + N, piv + N, X + li * LD, 1);
+  if (act && !(EW_SKIP & 1))
+    for_fibers<N, P>(li, [&](int r) { lu_fiber<N>(R1 + N * N, rcp + N, piv + N, X + r * LD, 1); });
   __syncwarp();
   // M = (Q1^T X) Q2
-  if (act && !(EW_SKIP & 2)) mm_tile<N, true, false, true, false>(Q1, N, X, LD, R1, LD, li);
+  if (act && !(EW_SKIP & 2)) mm_tile<N, P, true, false, true, false>(Q1, N, X, LD, R1, LD, li);
   __syncwarp();
-  if (act && !(EW_SKIP & 2)) mm_tile<N, false, false, false, true>(R1, LD, Q2, N, X, LD, li);
+  if (act && !(EW_SKIP & 2)) mm_tile<N, P, false, false, false, true>(R1, LD, Q2, N, X, LD, li);
   __syncwarp();
   // T1 | T2 into R1
   if (act) {
-    copy_mat<N * N, N>(R1, rec + 3 * N * N, li);
-    copy_mat<N * N, N>(R1 + N * N, rec + 5 * N * N, li);
+    copy_mat<N * N, N, P>(R1, rec + 3 * N * N, li);
+    copy_mat<N * N, N, P>(R1 + N * N, rec + 5 * N * N, li);
   }
   cpa_wait();
   __syncwarp();
@@ -269,10 +289,10 @@ __global__ void __launch_bounds__(32, 16) kron2d_ew_kernel(DevPC pc, const doubl
     double* scr = sm_all + C::EW * C::PER + 4 * lane;  // per-lane scratch: the cell's right-hand sides
     const int last = (EW_SKIP & 4) ? -1 : __reduce_max_sync(0xffffffffu, act ? nb1 + nb2 - 2 : -1);
     // cell of this lane at step st (valid = inside the anti-diagonal) and its factor slot
-    auto cell_at = [&](int st, int& i0, int& isz, int& k0, int& ksz) {
+    auto cell_at = [&](int st, int& i0, int& isz, int& k0, int& ksz, int off = 0) {
       const int d1lo = st - (nb2 - 1) > 0 ? st - (nb2 - 1) : 0;
       const int d1hi = st < nb1 - 1 ? st : nb1 - 1;
-      const int d1 = d1lo + li;
+      const int d1 = d1lo + li + off;
       const bool ok = act && st <= nb1 + nb2 - 2 && d1 <= d1hi;
       const int bi = ok ? nb1 - 1 - d1 : 0, bk = ok ? nb2 - 1 - (st - d1) : 0;
       i0 = s1[bi];
@@ -295,15 +315,8 @@ __global__ void __launch_bounds__(32, 16) kron2d_ew_kernel(DevPC pc, const doubl
     // one wavefront step with this lane's cell (ok, i0, isz, k0, ksz); the next step's cell is
     // located first and its factor slot prefetched into L1, so that the factors, loaded after
     // the chains (registers stay free for the chains' load pipelining), arrive from L1
-    auto step = [&](int st, bool ok, int i0, int isz, int k0, int ksz, bool& nok, int& ni0, int& nisz, int& nk0,
-                    int& nksz) {
-      long long c0 = EW_CLOCK ? clock64() : 0;
-      nok = cell_at(st + 1, ni0, nisz, nk0, nksz);
-      if (nok) {
-        const double* sp = cc + 6 * (ni0 * N + nisz * nk0);
-        asm volatile("prefetch.global.L1 [%0];" ::"l"(sp));
-        if (nisz * nksz == 4) asm volatile("prefetch.global.L1 [%0];" ::"l"(sp + 16));
-      }
+    // chains + tiny-system replay of one cell (ok, i0, isz, k0, ksz); c0: clock of the step start
+    auto do_cell = [&](bool ok, int i0, int isz, int k0, int ksz, long long& c0) {
       if (ok) {
         const int ns = isz * ksz;
         const int i1 = i0 + isz - 1, k1 = k0 + ksz - 1;
@@ -366,6 +379,27 @@ __global__ void __launch_bounds__(32, 16) kron2d_ew_kernel(DevPC pc, const doubl
           }
         }
       }
+    };
+    auto step = [&](int st, bool ok, int i0, int isz, int k0, int ksz, bool& nok, int& ni0, int& nisz, int& nk0,
+                    int& nksz) {
+      long long c0 = EW_CLOCK ? clock64() : 0;
+      nok = cell_at(st + 1, ni0, nisz, nk0, nksz);
+      if (nok) {
+        const double* sp = cc + 6 * (ni0 * N + nisz * nk0);
+        asm volatile("prefetch.global.L1 [%0];" ::"l"(sp));
+        if (nisz * nksz == 4) asm volatile("prefetch.global.L1 [%0];" ::"l"(sp + 16));
+      }
+      do_cell(ok, i0, isz, k0, ksz, c0);
+      if constexpr (P < N) {  // more cells on this anti-diagonal than lanes per block: further passes
+        const int d1lo = st - (nb2 - 1) > 0 ? st - (nb2 - 1) : 0;
+        const int d1hi = st < nb1 - 1 ? st : nb1 - 1;
+        const int nc = __reduce_max_sync(0xffffffffu, act && st <= nb1 + nb2 - 2 ? d1hi - d1lo + 1 : 0);
+        for (int off = P; off < nc; off += P) {
+          int xi0, xisz, xk0, xksz;
+          const bool xok = cell_at(st, xi0, xisz, xk0, xksz, off);
+          do_cell(xok, xi0, xisz, xk0, xksz, c0);
+        }
+      }
       if (EW_CLOCK) {
         const long long c1 = clock64();
         t_b += c1 - c0;
@@ -387,35 +421,35 @@ __global__ void __launch_bounds__(32, 16) kron2d_ew_kernel(DevPC pc, const doubl
              clock64() - t0, t_a, t_b, t_c);
   }
   // X = (Q1 Y) Q2^T
-  if (act && !(EW_SKIP & 8)) mm_tile<N, false, false, true, false>(Q1, N, X, LD, R1, LD, li);
+  if (act && !(EW_SKIP & 8)) mm_tile<N, P, false, false, true, false>(Q1, N, X, LD, R1, LD, li);
   __syncwarp();
-  if (act && !(EW_SKIP & 8)) mm_tile<N, false, true, false, true>(R1, LD, Q2, N, X, LD, li);
+  if (act && !(EW_SKIP & 8)) mm_tile<N, P, false, true, false, true>(R1, LD, Q2, N, X, LD, li);
   __syncwarp();
   if (act) {
     double* o = out + size_t(blk) * (N * N);
-    for (int i = li; i < N * N; i += N) o[i] = X[(i / N) * LD + i % N];
+    for (int i = li; i < N * N; i += P) o[i] = X[(i / N) * LD + i % N];
   }
 }
 
-template <int N>
+template <int N, int P = N>
 bool try_ew(const DevPC& pc, const double* in, double* out, cudaStream_t st) {
   if (pc.dim != 2 || pc.n1 != N || pc.q != N) return false;
-  using C = Ew<N>;
+  using C = Ew<N, P>;
   static bool configured = false;
   const size_t smem = sizeof(double) * (size_t(C::PER) * C::EW + 4 * 32);
   if (!configured) {
-    TPDG_CUDA_CHECK(cudaFuncSetAttribute(kron2d_ew_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    TPDG_CUDA_CHECK(cudaFuncSetAttribute(kron2d_ew_kernel<N>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
+    TPDG_CUDA_CHECK(cudaFuncSetAttribute(kron2d_ew_kernel<N, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    TPDG_CUDA_CHECK(cudaFuncSetAttribute(kron2d_ew_kernel<N, P>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     configured = true;
   }
-  kron2d_ew_kernel<N><<<(pc.nblk + C::EW - 1) / C::EW, 32, smem, st>>>(pc, in, out);
+  kron2d_ew_kernel<N, P><<<(pc.nblk + C::EW - 1) / C::EW, 32, smem, st>>>(pc, in, out);
   return true;
 }
 
 } // namespace
 
 bool launch_kron2d_ew(const DevPC& pc, const double* in, double* out, cudaStream_t st) {
-  return try_ew<5>(pc, in, out, st) || try_ew<9>(pc, in, out, st) || try_ew<16>(pc, in, out, st) ||
+  return try_ew<5>(pc, in, out, st) || try_ew<9>(pc, in, out, st) || try_ew<16, EW16_LANES>(pc, in, out, st) ||
          try_ew<21>(pc, in, out, st) || try_ew<31>(pc, in, out, st);
 }
 

@@ -142,7 +142,8 @@ void launch_dot(const double* x, const double* y, int64_t n, double* partial, do
                 cudaStream_t st);
 void launch_norm(const double* x, int64_t n, double* partial, double* result, unsigned* counter, cudaStream_t st);
 void launch_mgs_step(double* w, const double* vprev, const double* hprev, const double* vj, int64_t n,
-                     double* partial, double* result, unsigned* counter, cudaStream_t st, const int* skip = nullptr);
+                     double* partial, double* result, unsigned* counter, cudaStream_t st, const int* skip,
+                     bool sqrt_norm = true);
 void launch_axpy_neg(double* w, const double* h, const double* v, int64_t n, cudaStream_t st);
 void launch_scale_div(const double* in, const double* den, double* out, int64_t n, cudaStream_t st,
                       const int* skip = nullptr);
