@@ -38,5 +38,10 @@ int main(int argc, char** argv) {
     if (rep == 2) printf("n=%lld K=%d: %.1f us per MGS launch (avg k+1 = %.1f), %.2f us per pass\n", (long long)n, K,
                          ms * 1e3 / K, (K + 1) / 2.0, ms * 1e3 / (K * ((K + 1) / 2.0 + 1)));
   }
+  std::vector<double> hh(64);
+  cudaMemcpy(hh.data(), hc, sizeof(double) * 64, cudaMemcpyDeviceToHost);
+  unsigned long long x = 0;
+  for (int j = 0; j <= K; ++j) x ^= reinterpret_cast<unsigned long long&>(hh[j]) * (j + 1);
+  printf("hc checksum %016llx (h0 %.17g)\n", x, hh[0]);
   return 0;
 }
