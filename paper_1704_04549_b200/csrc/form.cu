@@ -19,6 +19,7 @@
 // reference's sequential code. The only non-bit-identical operations are CUDA's libm sin / cos /
 // atan / atan2 inside standardize_2x2 (<= 2 ulp vs glibc).
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 
 #include "faithful.cuh"
@@ -32,6 +33,10 @@ namespace {
 constexpr int kFormThreads = 256;
 
 constexpr int kMaxGroups = kFormThreads / 32;
+#ifndef FORM_GLOBAL_CTAS
+#define FORM_GLOBAL_CTAS 4  // measured at cfg2 p=15: 2 -> 8.2 ms, 3 -> 7.1, 4 -> 5.3, 6 -> 6.5, 8 -> 6.9
+#endif
+constexpr int kFormGlobalCtas = FORM_GLOBAL_CTAS;  // resident CTAs per SM of the global-working-set make_factors
 template <class G>
 __device__ __forceinline__ int groups_per_cta() {
   return 1;
@@ -872,7 +877,7 @@ __device__ bool make_factors_dev(const Grp& g, int dim, int q, int n1, const dou
 // shared memory when it fits (SMEM = true): the serial sections of LU / Hessenberg / Francis QR then
 // pay shared-memory rather than L2 latency per access. Results are copied out at the end.
 template <bool SMEM, class Grp>
-__global__ void __launch_bounds__(kFormThreads) make_factors_kernel(int dim, int q, int n1, int nblk,
+__global__ void __launch_bounds__(kFormThreads, SMEM ? 1 : kFormGlobalCtas) make_factors_kernel(int dim, int q, int n1, int nblk,
                                                                      double* raw, double* rec, int* piv, int* kind,
                                                                      double* work) {
   const int NG = groups_per_cta<Grp>();
@@ -1307,7 +1312,15 @@ void launch_make_factors(int dim, int q, int n1, int nblk, const double* raw, do
   int dev = 0, sms = 0;
   TPDG_CUDA_CHECK(cudaGetDevice(&dev));
   TPDG_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  if (per_group <= kMax) {
+  // The per-block working set in shared memory (one CTA of up to 8 warps per SM) loses to the
+  // global (L1-resident) working set with 4 CTAs per SM: the Francis QR sweeps are dependent
+  // chains, so resident warps matter more than access latency (cfg2 p=15: 10.5 -> 5.3 ms).
+  // TPDG_FORM_SMEM=1 selects the shared-memory variant.
+  static const bool use_smem = [] {
+    const char* f = std::getenv("TPDG_FORM_SMEM");
+    return f && f[0] == '1';
+  }();
+  if (per_group <= kMax && use_smem) {
     const int groups = int(std::min<size_t>(kMaxGroups, kMax / per_group));
     const size_t smem = per_group * groups;
     static size_t configured = 0;
@@ -1323,7 +1336,7 @@ void launch_make_factors(int dim, int q, int n1, int nblk, const double* raw, do
     make_factors_kernel<true, WarpGroup><<<grid, 32 * groups, smem, st>>>(dim, q, n1, nblk, const_cast<double*>(raw),
                                                                          rec, piv, kind, work);
   } else {  // global working set (work holds make_factors_work_groups() x wl doubles)
-    const int grid = std::min((nblk + kMaxGroups - 1) / kMaxGroups, 148 * 2);
+    const int grid = std::min((nblk + kMaxGroups - 1) / kMaxGroups, 148 * kFormGlobalCtas);
     make_factors_kernel<false, WarpGroup><<<grid, kFormThreads, 0, st>>>(dim, q, n1, nblk, const_cast<double*>(raw),
                                                                         rec, piv, kind, work);
   }
@@ -1331,7 +1344,7 @@ void launch_make_factors(int dim, int q, int n1, int nblk, const double* raw, do
   ++g_launches;
 }
 
-int make_factors_work_groups() { return 148 * 2 * kMaxGroups; }
+int make_factors_work_groups() { return 148 * kFormGlobalCtas * kMaxGroups; }
 
 size_t probe_work_doubles(const DevSys& s) {
   const size_t nfull = size_t(s.n_c) * s.npe;
