@@ -173,10 +173,9 @@ __global__ void add_kernel(double* __restrict__ x, const double* __restrict__ dx
 // Givens step of iteration k (solve/gmres.hpp:122-141), one thread. hc holds the raw Hessenberg
 // column h(0..k+1, k) from MGS; the rotated column goes to H(:, k). Writes |g_{k+1}| and the
 // convergence decision to the host-mapped status slot and raises `done` on convergence.
-__global__ void givens_kernel(GmresDev G, int k, GmresStatus* status) {
+__device__ __forceinline__ void givens_warp(const GmresDev& G, int k, GmresStatus* status, double* gsm) {
   // one warp stages the column and the previous rotations in shared memory (independent loads,
-  // one round trip), then lane 0 runs the dependent rotation chain on-chip
-  extern __shared__ double gsm[];  // col[m + 2] | cs[m + 1] | sn[m + 1]
+  // one round trip), then lane 0 runs the dependent rotation chain on-chip; gsm: col[m + 2] | cs[m + 1] | sn[m + 1]
   const int m = G.m;
   double* col = gsm;
   double* cs = col + m + 2;
@@ -184,8 +183,8 @@ __global__ void givens_kernel(GmresDev G, int k, GmresStatus* status) {
   // every operand is loaded in one round trip (done flag, g_k, the column, the old rotations)
   const int done = *G.done;
   const double gk = G.g[k];
-  for (int j = threadIdx.x; j <= k + 1; j += blockDim.x) col[j] = G.hc[j];
-  for (int j = threadIdx.x; j < k; j += blockDim.x) {
+  for (int j = threadIdx.x; j <= k + 1; j += 32) col[j] = G.hc[j];
+  for (int j = threadIdx.x; j < k; j += 32) {
     cs[j] = G.cs[j];
     sn[j] = G.sn[j];
   }
@@ -215,7 +214,22 @@ __global__ void givens_kernel(GmresDev G, int k, GmresStatus* status) {
     col[k + 1] = 0.0;
   }
   __syncwarp();
-  for (int j = threadIdx.x; j <= k + 1; j += blockDim.x) G.H[j * m + k] = col[j];
+  for (int j = threadIdx.x; j <= k + 1; j += 32) G.H[j * m + k] = col[j];
+}
+
+__global__ void givens_kernel(GmresDev G, int k, GmresStatus* status) {
+  extern __shared__ double gsm[];
+  givens_warp(G, k, status, gsm);
+}
+
+// The Givens step fused at the end of the cooperative MGS launch (single rank): block 0's first
+// warp runs it once the iteration's column h(0..k+1, k) is complete (written by block 0 itself).
+constexpr int kFusedGivensMaxM = 62;
+__device__ __forceinline__ void fused_givens(const GmresDev& G, int k, GmresStatus* status) {
+  __shared__ double gsm[3 * kFusedGivensMaxM + 4];
+  if (status == nullptr || blockIdx.x != 0) return;
+  __syncthreads();
+  if (threadIdx.x < 32) givens_warp(G, k, status, gsm);
 }
 
 // y = H(0:k, 0:k)^{-1} g (back substitution, solve/gmres.hpp:145-150), one thread.
@@ -287,7 +301,7 @@ template <int MODE>
 __global__ void __launch_bounds__(kCoopThreads) mgs_coop_kernel(double* __restrict__ V, int64_t ldv, int k,
                                                                  int64_t n, int64_t chunk, double* __restrict__ hc,
                                                                  double* __restrict__ partial, unsigned* bar,
-                                                                 const int* skip) {
+                                                                 const int* skip, GmresDev G, GmresStatus* gstatus) {
   if (skip && *skip) return;
   extern __shared__ double wsm[];
   __shared__ double sh[32];
@@ -364,6 +378,7 @@ __global__ void __launch_bounds__(kCoopThreads) mgs_coop_kernel(double* __restri
   }
   // reference: if (hkk > 0) v[k+1] /= hkk
   for (int64_t i = threadIdx.x; i < len; i += blockDim.x) wg[i] = h > 0.0 ? w[i] / h : w[i];
+  fused_givens(G, k, gstatus);
 }
 
 // MODE 3: w plus two basis-vector slices in shared memory; the slice of v_{j+1} is streamed with
@@ -426,7 +441,7 @@ __device__ __forceinline__ void cp16(double* smem, const double* gmem) {
 __global__ void __launch_bounds__(kCoopThreads) mgs_pipe_kernel(double* __restrict__ V, int64_t ldv, int k, int64_t n,
                                                                  int64_t chunk, double* __restrict__ hc,
                                                                  double* __restrict__ partial, unsigned* bar,
-                                                                 const int* skip) {
+                                                                 const int* skip, GmresDev G, GmresStatus* gstatus) {
   if (skip && *skip) return;
   extern __shared__ double sm3[];
   __shared__ double shA[32], shB[33];
@@ -481,6 +496,7 @@ __global__ void __launch_bounds__(kCoopThreads) mgs_pipe_kernel(double* __restri
     if (len & 1) __syncthreads();  // the scalar tail element is copied by thread 0 only
   }
   for (int64_t i = threadIdx.x; i < len; i += blockDim.x) wg[i] = h > 0.0 ? w[i] / h : w[i];
+  fused_givens(G, k, gstatus);
 }
 
 // MODE 4 (chunk <= 8192): w and the previous basis vector live in registers (thread t owns the
@@ -490,7 +506,7 @@ template <int R>
 __global__ void __launch_bounds__(kCoopThreads) mgs_reg_kernel(double* __restrict__ V, int64_t ldv, int k, int64_t n,
                                                                 int64_t chunk, double* __restrict__ hc,
                                                                 double* __restrict__ partial, unsigned* bar,
-                                                                const int* skip) {
+                                                                const int* skip, GmresDev G, GmresStatus* gstatus) {
   if (skip && *skip) return;
   extern __shared__ double sm4[];
   __shared__ double shA[32], shB[33];
@@ -561,6 +577,7 @@ __global__ void __launch_bounds__(kCoopThreads) mgs_reg_kernel(double* __restric
       wg[i] = h > 0.0 ? w[r].x / h : w[r].x;
     }
   }
+  fused_givens(G, k, gstatus);
 }
 
 // MODE 9 (chunk too large for the shared-memory modes): w split between registers (the first
@@ -571,7 +588,7 @@ template <int RR>
 __global__ void __launch_bounds__(kCoopThreads) mgs_split_kernel(double* __restrict__ V, int64_t ldv, int k, int64_t n,
                                                                   int64_t chunk, double* __restrict__ hc,
                                                                   double* __restrict__ partial, unsigned* bar,
-                                                                  const int* skip) {
+                                                                  const int* skip, GmresDev G, GmresStatus* gstatus) {
   if (skip && *skip) return;
   extern __shared__ double wsm5[];  // w pairs r >= RR: local index i - 2048 RR
   __shared__ double shA[32], shB[33];
@@ -643,6 +660,7 @@ __global__ void __launch_bounds__(kCoopThreads) mgs_split_kernel(double* __restr
       wg[i] = h > 0.0 ? wr[r].x / h : wr[r].x;
   }
   for (int i = SPLIT + t; i < len; i += kCoopThreads) wg[i] = h > 0.0 ? wsm5[i - SPLIT] / h : wsm5[i - SPLIT];
+  fused_givens(G, k, gstatus);
 }
 
 struct CoopPlan {
@@ -748,7 +766,7 @@ void launch_scale_div(const double* in, const double* den, double* out, int64_t 
 }
 
 void launch_mgs_iteration(double* V, int64_t ldv, int k, int64_t n, double* hc, double* partial, unsigned* bar,
-                          const int* skip, cudaStream_t st) {
+                          const int* skip, cudaStream_t st, const GmresDev* G, GmresStatus* status) {
   static int64_t planned_n = -1;
   static CoopPlan plan;
   if (planned_n != n) {
@@ -756,7 +774,9 @@ void launch_mgs_iteration(double* V, int64_t ldv, int k, int64_t n, double* hc, 
     planned_n = n;
   }
   int64_t chunk = plan.chunk;
-  void* args[] = {&V, &ldv, &k, &n, &chunk, &hc, &partial, &bar, &skip};
+  GmresDev g = G && G->m <= kFusedGivensMaxM ? *G : GmresDev{};
+  GmresStatus* gs = G && G->m <= kFusedGivensMaxM ? status : nullptr;
+  void* args[] = {&V, &ldv, &k, &n, &chunk, &hc, &partial, &bar, &skip, &g, &gs};
   void* fn = plan.mode == 9   ? reinterpret_cast<void*>(mgs_split_kernel<8>)
              : plan.mode == 5 ? reinterpret_cast<void*>(mgs_reg_kernel<1>)
              : plan.mode == 6 ? reinterpret_cast<void*>(mgs_reg_kernel<2>)
@@ -771,6 +791,8 @@ void launch_mgs_iteration(double* V, int64_t ldv, int k, int64_t n, double* hc, 
 }
 
 int mgs_partial_doubles(int m) { return (m + 2) * 256; }
+
+bool mgs_fuses_givens(int m) { return m <= kFusedGivensMaxM; }
 
 void launch_givens(const GmresDev& G, int k, GmresStatus* status, cudaStream_t st) {
   givens_kernel<<<1, 32, sizeof(double) * size_t(3 * G.m + 4), st>>>(G, k, status);

@@ -446,7 +446,7 @@ int run_gmres(tpdg_gpu_op op, tpdg_gpu_pc pc, const double* d_b, double* d_x, co
         }
         Prof pr(ctx, 2);
         if (!multi) {  // fused MGS passes + normalization (one cooperative launch)
-          launch_mgs_iteration(V, ldv, k, n, hc, part, ctr + 4, G.done, st);
+          launch_mgs_iteration(V, ldv, k, n, hc, part, ctr + 4, G.done, st, &G, status.dev);
         } else {
           for (int j = 0; j <= k; ++j) {  // pass j: w -= h_{j-1} v_{j-1}, then h_j = <v_j, w> over all ranks
             launch_mgs_step(w, j > 0 ? V + size_t(j - 1) * ldv : nullptr, j > 0 ? hc + j - 1 : nullptr,
@@ -459,7 +459,7 @@ int run_gmres(tpdg_gpu_op op, tpdg_gpu_pc pc, const double* d_b, double* d_x, co
           ++g_launches;
           launch_scale_div(w, hc + k + 1, w, n, st, G.done);
         }
-        launch_givens(G, k, status.dev, st);
+        if (multi || !mgs_fuses_givens(m)) launch_givens(G, k, status.dev, st);
       };
       int k_end = -1;
       launch_iteration(0);

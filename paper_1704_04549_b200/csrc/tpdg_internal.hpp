@@ -161,8 +161,11 @@ struct GmresStatus {  // host-mapped, one per iteration of a cycle
 };
 void launch_givens(const GmresDev& G, int k, GmresStatus* status, cudaStream_t st);
 // All MGS passes + normalization of iteration k in one cooperative launch (single rank).
+// With G / status, the iteration's Givens step runs at the end of the same launch (m <= 62).
 void launch_mgs_iteration(double* V, int64_t ldv, int k, int64_t n, double* hc, double* partial, unsigned* bar,
-                          const int* skip, cudaStream_t st);
+                          const int* skip, cudaStream_t st, const GmresDev* G = nullptr,
+                          GmresStatus* status = nullptr);
+bool mgs_fuses_givens(int m);
 int mgs_partial_doubles(int m);
 void launch_backsolve(const GmresDev& G, int k, cudaStream_t st);
 void launch_sub(const double* b, const double* ax, double* r, int64_t n, cudaStream_t st);
