@@ -7,11 +7,12 @@ R=$(cd "$(dirname "$0")/.." && pwd)
 P=$R/paper_1704_04549_b200
 make -C $P/csrc -j8 >/dev/null
 ARCH="-gencode arch=compute_100a,code=sm_100a"
+case "${SRC:-kron}" in kron|kron_ew|kron_fallback|form) FMAD=-fmad=false ;; *) FMAD= ;; esac
 for spec in "$@"; do
   name=${spec%%:*}; flags=${spec#*:}
   (d=$P/_build/var/$name; mkdir -p $d
    /usr/local/cuda/bin/nvcc -O3 -std=c++17 $ARCH -lineinfo -Xcompiler -fPIC -I$P/csrc -I$R/include \
-     --expt-relaxed-constexpr -fmad=false $flags -c $P/csrc/${SRC:-kron}.cu -o $d/${SRC:-kron}.o
+     --expt-relaxed-constexpr $FMAD $flags -c $P/csrc/${SRC:-kron}.cu -o $d/${SRC:-kron}.o
    objs=$(ls $P/_build/*.o | grep -v "/${SRC:-kron}.o$")
    /usr/local/cuda/bin/nvcc $ARCH -shared -o $d/libtpdg_gpu.so $d/${SRC:-kron}.o $objs -L/usr/lib/x86_64-linux-gnu -lnccl
    echo built $name) &
