@@ -39,11 +39,6 @@ __device__ __forceinline__ const double* nbr_vals(const DevSys& s, const double*
   return nbr < s.n_local ? vin + size_t(nbr) * qq : halo + size_t(nbr - s.n_local) * qq;
 }
 
-#ifndef JV_PW_REGS
-#define JV_PW_REGS 0
-#endif
-constexpr int kJvMaxWarps = JV_PW_REGS ? 12 : 8;
-
 template <int Q, int MU>
 struct JvMmaLayout {
   static constexpr int QP = p8(Q), MP = p8(MU), KQ = p4(Q), KM = p4(MU), K2 = p4(2 * MU);
@@ -67,14 +62,13 @@ struct JvMmaLayout {
   static constexpr int e_g = e_mf + MP * LMF;          // g[4][MU]
   static constexpr int e_lift = e_g + 4 * MU;          // lift vectors [4][Q]
   static constexpr int e_pw = (e_lift + 4 * Q + 1) & ~1; // jd | dft0 | dft1 of the element (cp.async, prefetched)
-  // JV_PW_REGS: jd / dft prefetched into registers instead (no staging region: more warps per SM)
-  static constexpr int per_warp = JV_PW_REGS ? e_pw : (e_pw + 3 * MU * MU + 1) & ~1;
+  static constexpr int per_warp = (e_pw + 3 * MU * MU + 1) & ~1;
   static constexpr int budget = (227 * 1024) / 8 - weights - 16;
-  static constexpr int warps = budget / per_warp > kJvMaxWarps ? kJvMaxWarps : budget / per_warp;
+  static constexpr int warps = budget / per_warp > 8 ? 8 : budget / per_warp;
 };
 
 template <int Q, int MU>
-__global__ void __launch_bounds__(32 * kJvMaxWarps) jv2d_mma_kernel(DevSys s, const double* __restrict__ vin,
+__global__ void __launch_bounds__(256) jv2d_mma_kernel(DevSys s, const double* __restrict__ vin,
                                                         const double* __restrict__ halo, double* __restrict__ vout) {
   if (s.skip && *s.skip) return;
   using L = JvMmaLayout<Q, MU>;
@@ -137,25 +131,7 @@ __global__ void __launch_bounds__(32 * kJvMaxWarps) jv2d_mma_kernel(DevSys s, co
       nr[u] = x;
     }
   };
-  constexpr int NPW = (MM + 31) / 32;
-  double pwr[3][NPW];
-  auto fetch_pw_regs = [&](int e) {
-    if (e >= s.n_local) return;
-    const double* jd = s.jdet + size_t(e) * MM;
-    const double* d0 = s.dft + size_t(e) * 2 * MM;
-#pragma unroll
-    for (int u = 0; u < NPW; ++u) {
-      const int qv = lane + 32 * u;
-      pwr[0][u] = qv < MM ? __ldg(jd + qv) : 0.0;
-      pwr[1][u] = qv < MM ? __ldg(d0 + qv) : 0.0;
-      pwr[2][u] = qv < MM ? __ldg(d0 + MM + qv) : 0.0;
-    }
-  };
   auto fetch_pw = [&](int e) {
-    if (JV_PW_REGS) {
-      fetch_pw_regs(e);
-      return;
-    }
     if (e >= s.n_local) return;
     const double* jd = s.jdet + size_t(e) * MM;
     const double* d0 = s.dft + size_t(e) * 2 * MM;
@@ -237,26 +213,12 @@ __global__ void __launch_bounds__(32 * kJvMaxWarps) jv2d_mma_kernel(DevSys s, co
     // point-wise fields: [M | F0] -> smf, F1 -> vals in place
     asm volatile("cp.async.wait_all;\n" ::: "memory");
     __syncwarp();
-    if (JV_PW_REGS) {
-#pragma unroll
-      for (int u = 0; u < NPW; ++u) {
-        const int qv = lane + 32 * u;
-        if (qv < MM) {
-          const int be = qv / MU, al = qv % MU;
-          const double x = sval[be * LVAL + al];
-          smf[be * LMF + al] = s.a * pwr[0][u] * x;
-          smf[be * LMF + MU + al] = s.b * (pwr[1][u] * x);
-          sval[be * LVAL + al] = s.b * (pwr[2][u] * x);
-        }
-      }
-    } else {
-      for (int qv = lane; qv < MM; qv += 32) {
-        const int be = qv / MU, al = qv % MU;
-        const double x = sval[be * LVAL + al];
-        smf[be * LMF + al] = s.a * spw[qv] * x;
-        smf[be * LMF + MU + al] = s.b * (spw[MM + qv] * x);
-        sval[be * LVAL + al] = s.b * (spw[2 * MM + qv] * x);
-      }
+    for (int qv = lane; qv < MM; qv += 32) {
+      const int be = qv / MU, al = qv % MU;
+      const double x = sval[be * LVAL + al];
+      smf[be * LMF + al] = s.a * spw[qv] * x;
+      smf[be * LMF + MU + al] = s.b * (spw[MM + qv] * x);
+      sval[be * LVAL + al] = s.b * (spw[2 * MM + qv] * x);
     }
     __syncwarp();
     fetch_pw(e + stride);  // the buffer is free: next element's jd / dft
