@@ -10,6 +10,7 @@
  *   tpdg_gpu_jv               jacobian_apply                  ops/linearized.hpp:201-240
  *   tpdg_gpu_shuffled         shuffled_apply(_transpose)      ops/shuffled.hpp:509-531
  *   tpdg_gpu_form_ksvd        form_ksvd_2d / form_ksvd_3d     precond/ksvd.hpp:252-306, 312-372
+ *   tpdg_gpu_form_block_jacobi form_block_jacobi              precond/block_jacobi.hpp:38-72
  *   tpdg_gpu_pc_apply         KsvdPC2D::apply / KsvdPC3D::apply precond/ksvd.hpp:172-195, 210-233
  *   tpdg_gpu_pc_fallbacks     KsvdPC*::fallbacks (FallbackEvent) precond/ksvd.hpp:22-28
  *   tpdg_gpu_gmres            gmres(op, pc, b, GmresConfig)   solve/gmres.hpp:52-179
@@ -115,6 +116,12 @@ int tpdg_gpu_shuffled_host(tpdg_gpu_op op, int e, int comp, int transpose, const
 
 /* ---- KSVD preconditioner, formed on the device (no host fallback). */
 int tpdg_gpu_form_ksvd(tpdg_gpu_op op, const tpdg_gpu_ksvd_config *cfg, tpdg_gpu_pc *out);
+/* Exact block-Jacobi preconditioner (BlockJacobiPC / form_block_jacobi, precond/block_jacobi.hpp:13-72):
+ * every diagonal block (element, or element x component in small mode) assembled on the device by
+ * probing the element operator and LU-factored with partial pivoting; applied with the same
+ * tpdg_gpu_pc_apply. ConfigError when block^2 x blocks exceeds max_total_entries (<= 0: the
+ * reference's default 3e8), SingularError on a singular block. The paper's comparison baseline. */
+int tpdg_gpu_form_block_jacobi(tpdg_gpu_op op, int64_t max_total_entries, tpdg_gpu_pc *out);
 /* Test hook: build the apply state from externally formed raw factors (2D: a1 b1 a2 b2,
  * 3D: a1 b1 c1 b2 c2 per block, concatenated for blocks with has[blk] != 0; LU and Schur are
  * recomputed on the device exactly as make_factors_2d/3d do). Blocks with has == 0 get the

@@ -93,7 +93,7 @@ EXPORTS = [
     "tpdg_gpu_ctx_profile", "tpdg_gpu_ctx_profile_read",
     "tpdg_gpu_op_create", "tpdg_gpu_op_destroy", "tpdg_gpu_op_local_size", "tpdg_gpu_op_check_hash",
     "tpdg_gpu_jv", "tpdg_gpu_jv_host", "tpdg_gpu_shuffled_host", "tpdg_gpu_form_ksvd",
-    "tpdg_gpu_pc_import_factors", "tpdg_gpu_pc_import_record", "tpdg_gpu_pc_destroy", "tpdg_gpu_pc_num_fallbacks", "tpdg_gpu_pc_fallbacks",
+    "tpdg_gpu_pc_import_factors", "tpdg_gpu_pc_import_record", "tpdg_gpu_form_block_jacobi", "tpdg_gpu_pc_destroy", "tpdg_gpu_pc_num_fallbacks", "tpdg_gpu_pc_fallbacks",
     "tpdg_gpu_pc_factor_len", "tpdg_gpu_pc_export_factors", "tpdg_gpu_pc_apply", "tpdg_gpu_pc_apply_host",
     "tpdg_gpu_gmres", "tpdg_gpu_gmres_host", "tpdg_setup_advection", "tpdg_setup_system", "tpdg_setup_destroy",
     "tpdg_uniform_vector", "tpdg_seeded_unit_vector", "tpdg_halo_plan_create", "tpdg_halo_plan_query",
@@ -131,6 +131,7 @@ def lib():
         "tpdg_gpu_form_ksvd": [v, C.POINTER(_KsvdCfg), C.POINTER(v)],
         "tpdg_gpu_pc_import_factors": [v, dp, i64p, C.POINTER(v)],
         "tpdg_gpu_pc_import_record": [v, dp, i64p, dp, ip, C.POINTER(v)],
+        "tpdg_gpu_form_block_jacobi": [v, C.c_int64, C.POINTER(v)],
         "tpdg_gpu_pc_destroy": [v], "tpdg_gpu_pc_num_fallbacks": [v, C.POINTER(C.c_int)],
         "tpdg_gpu_pc_fallbacks": [v, i64p], "tpdg_gpu_pc_factor_len": [v, C.POINTER(C.c_int)],
         "tpdg_gpu_pc_export_factors": [v, C.c_int, dp, C.POINTER(C.c_int)],
@@ -473,6 +474,14 @@ def form_ksvd(op: LinearizedOperator, cfg: KsvdConfig | None = None) -> KsvdPC:
     c = _KsvdCfg(cfg.terms, cfg.lanczos_max_it, cfg.breakdown_tol, C.c_uint64(cfg.seed), cfg.degenerate_tol)
     h = C.c_void_p()
     _check(lib().tpdg_gpu_form_ksvd(op.h, C.byref(c), C.byref(h)))
+    return KsvdPC(op, h)
+
+
+def form_block_jacobi(op: LinearizedOperator, max_total_entries: int = 300_000_000) -> KsvdPC:
+    """form_block_jacobi (precond/block_jacobi.hpp:38-72): exact block-LU preconditioner on the device
+    (same apply contract as the KSVD preconditioner)."""
+    h = C.c_void_p()
+    _check(lib().tpdg_gpu_form_block_jacobi(op.h, C.c_int64(max_total_entries), C.byref(h)))
     return KsvdPC(op, h)
 
 

@@ -855,6 +855,33 @@ int tpdg_gpu_form_ksvd(tpdg_gpu_op op, const tpdg_gpu_ksvd_config* cfg_in, tpdg_
   });
 }
 
+int tpdg_gpu_form_block_jacobi(tpdg_gpu_op op, int64_t max_total_entries, tpdg_gpu_pc* out) {
+  return guarded([&] {
+    REQUIRE(op && out, TPDG_CONFIG, "form_block_jacobi: null argument");
+    std::unique_ptr<tpdg_gpu_pc_s> pc(new tpdg_gpu_pc_s);
+    pc->op = op;
+    cudaStream_t st = op->ctx->stream;
+    alloc_records(pc.get());
+    // budget check of block_jacobi.hpp:40-47 (over the whole mesh, like the reference)
+    const int64_t block = op->s.small ? op->s.npe : int64_t(op->n_c) * op->s.npe;
+    const int64_t per_elem = op->s.small ? op->n_c : 1;
+    const int64_t total = block * block * per_elem * int64_t(op->n_global);
+    const int64_t budget = max_total_entries > 0 ? max_total_entries : 300000000;
+    REQUIRE(total <= budget, TPDG_CONFIG,
+            "form_block_jacobi: " + std::to_string(total) + " entries exceed the budget");
+    // every block takes the exact block-LU path: assembled by probing the element operator and
+    // factored with partial pivoting (assemble_diag_block(_small) + LuFactor), applied by the
+    // dense-LU kernel (kron_fallback.cu)
+    TPDG_CUDA_CHECK(cudaMemsetAsync(pc->kind.p, 0, sizeof(int) * size_t(pc->nblk), st));
+    finish_pc(pc.get());
+    int sing = 0;
+    TPDG_CUDA_CHECK(cudaMemcpy(&sing, pc->status.as<int>() + 1, sizeof(int), cudaMemcpyDeviceToHost));
+    REQUIRE(sing == 0, TPDG_SINGULAR, "form_block_jacobi: singular diagonal block");
+    pc->fallbacks.clear();  // not KSVD fallbacks: every block is exact by construction
+    *out = pc.release();
+  });
+}
+
 int tpdg_gpu_pc_import_factors(tpdg_gpu_op op, const double* h_factors, const int64_t* h_has, tpdg_gpu_pc* out) {
   return guarded([&] {
     std::unique_ptr<tpdg_gpu_pc_s> pc(new tpdg_gpu_pc_s);

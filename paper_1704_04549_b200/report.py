@@ -83,22 +83,24 @@ def write_report_csv(rows, path):
             f.write(report_row_csv(r) + "\n")
 
 
-def run_cell(ctx, case, p, tol=1e-10, restart=30, max_iterations=2000, seed=12345):
-    """One BASELINE cell on the device: formation, then one GMRES solve of a seeded RHS."""
-    from . import GmresConfig, LinearizedOperator, form_ksvd, gmres, setup_advection, uniform_vector
+def run_cell(ctx, case, p, tol=1e-10, restart=30, max_iterations=2000, seed=12345, precond="ksvd_full"):
+    """One BASELINE cell on the device: formation, then one GMRES solve of a seeded RHS.
+    precond: "ksvd_full" (the KSVD preconditioner) or "jacobi_full" (exact block Jacobi)."""
+    from . import (GmresConfig, LinearizedOperator, form_block_jacobi, form_ksvd, gmres, setup_advection,
+                   uniform_vector)
     if case == "cfg4":
         sysm, dt, name = setup_advection("const3d", 16, 16, 16, p=p, vel=(1.0, 0.7, 0.4)), 0.01, "advection_3d"
     elif case == "cfg1":
         sysm, dt, name = setup_advection("const2d", 8, 8, p=p, vel=(1.0, 0.5, 0.0)), 0.01, "advection_const"
     else:
         sysm, dt, name = setup_advection("swirl2d", 64, 64, p=p), 0.005, "advection_swirl"
-    row = ReportRow(case_id=name, p=p, dt=dt)
+    row = ReportRow(case_id=name, p=p, dt=dt, precond=precond)
     t0 = time.perf_counter()
     try:
         op = LinearizedOperator(ctx, sysm, dt)
         ctx.sync()
         tf = time.perf_counter()
-        pc = form_ksvd(op)
+        pc = form_block_jacobi(op) if precond == "jacobi_full" else form_ksvd(op)
         ctx.sync()
         row.form_seconds = time.perf_counter() - tf
         b = uniform_vector(seed, sysm.N, 1.0)
@@ -122,11 +124,12 @@ def main(argv=None):
     ap = argparse.ArgumentParser(description=__doc__.splitlines()[0])
     ap.add_argument("--case", default="cfg2", choices=["cfg1", "cfg2", "cfg4"])
     ap.add_argument("--p", type=int, nargs="+", default=[4, 8, 15, 20, 30])
+    ap.add_argument("--precond", nargs="+", default=["ksvd_full"], choices=["ksvd_full", "jacobi_full"])
     ap.add_argument("--out", default="-")
     a = ap.parse_args(argv)
     from . import Context
     ctx = Context(0)
-    rows = [run_cell(ctx, a.case, p) for p in a.p]
+    rows = [run_cell(ctx, a.case, p, precond=pk) for p in a.p for pk in a.precond]
     if a.out == "-":
         print(REPORT_CSV_HEADER)
         for r in rows:
