@@ -158,9 +158,14 @@ __global__ void sub_kernel(const double* __restrict__ b, const double* __restric
 // out[i] = sum_j y_j v_j[i], j ascending (reference: tmp[i] += y[j] * v[j][i]).
 __global__ void combine_kernel(const double* __restrict__ v, int64_t ldv, const double* __restrict__ y, int k,
                                double* __restrict__ out, int64_t n) {
+  __shared__ double ys[64];
+  for (int j = threadIdx.x; j < k && j < 64; j += blockDim.x) ys[j] = y[j];
+  __syncthreads();
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
     double s = 0.0;
-    for (int j = 0; j < k; ++j) s += y[j] * v[j * ldv + i];
+    // same j-ascending chain; unrolled so that the basis loads are in flight together
+#pragma unroll 8
+    for (int j = 0; j < k; ++j) s += (j < 64 ? ys[j] : y[j]) * v[j * ldv + i];
     out[i] = s;
   }
 }
@@ -234,13 +239,36 @@ __device__ __forceinline__ void fused_givens(const GmresDev& G, int k, GmresStat
 
 // y = H(0:k, 0:k)^{-1} g (back substitution, solve/gmres.hpp:145-150), one thread.
 __global__ void backsolve_kernel(GmresDev G, int k) {
-  if (threadIdx.x != 0) return;
+  // the warp stages H(0:k, 0:k) and g in shared memory (one round trip), then lane 0 runs the
+  // sequential back substitution on-chip (same order as before)
+  extern __shared__ double bs_sm[];  // H rows (k x k) | g (k) | y (k)
   const int m = G.m;
-  for (int i = k - 1; i >= 0; --i) {
-    double s = G.g[i];
-    for (int j = i + 1; j < k; ++j) s -= G.H[i * m + j] * G.y[j];
-    G.y[i] = s / G.H[i * m + i];
+  double* Hs = bs_sm;
+  double* gs = Hs + k * k;
+  double* ys = gs + k;
+  if (k <= 32) {  // all loads of a lane issued before any store (one memory round trip)
+    double hv[32];
+#pragma unroll
+    for (int r = 0; r < 32; ++r) hv[r] = (r < k && int(threadIdx.x) < k) ? G.H[r * m + threadIdx.x] : 0.0;
+    const double gv = int(threadIdx.x) < k ? G.g[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int r = 0; r < 32; ++r)
+      if (r < k && int(threadIdx.x) < k) Hs[r * k + threadIdx.x] = hv[r];
+    if (int(threadIdx.x) < k) gs[threadIdx.x] = gv;
+  } else {
+    for (int t = threadIdx.x; t < k * k; t += blockDim.x) Hs[t] = G.H[(t / k) * m + t % k];
+    for (int t = threadIdx.x; t < k; t += blockDim.x) gs[t] = G.g[t];
   }
+  __syncwarp();
+  if (threadIdx.x == 0) {
+    for (int i = k - 1; i >= 0; --i) {
+      double s = gs[i];
+      for (int j = i + 1; j < k; ++j) s -= Hs[i * k + j] * ys[j];
+      ys[i] = s / Hs[i * k + i];
+    }
+  }
+  __syncwarp();
+  for (int t = threadIdx.x; t < k; t += blockDim.x) G.y[t] = ys[t];
 }
 
 // All MGS passes of Arnoldi iteration k in one cooperative persistent launch (single rank):
@@ -801,7 +829,7 @@ void launch_givens(const GmresDev& G, int k, GmresStatus* status, cudaStream_t s
 }
 
 void launch_backsolve(const GmresDev& G, int k, cudaStream_t st) {
-  backsolve_kernel<<<1, 32, 0, st>>>(G, k);
+  backsolve_kernel<<<1, 32, sizeof(double) * size_t(k * k + 2 * k + 1), st>>>(G, k);
   TPDG_CUDA_CHECK(cudaGetLastError());
   ++g_launches;
 }
