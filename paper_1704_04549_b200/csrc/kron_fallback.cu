@@ -15,6 +15,7 @@
 //            is reversed with respect to the reference (well-conditioned dense block:
 //            tests/test_gpu_full_pc_parity.py measures ~1e-15).
 #include <cstdint>
+#include <cstdlib>
 
 #include "faithful.cuh"
 #include "tpdg_internal.hpp"
@@ -103,6 +104,158 @@ __global__ void __launch_bounds__(kFbThreads) fb_apply_kernel(DevPC pc, const do
   for (int i = t; i < n; i += kFbThreads) o[i] = sx[i];
 }
 
+// Panel-blocked variant (default): the same per-row operation order as fb_apply_kernel, with two
+// block barriers per 32-column panel instead of one per column. Forward, panel [c0, c0 + 32):
+// (1) the panel's 32 rows go to warp 0, which solves the unit-lower 32 x 32 triangle with shuffles
+// (row r subtracts L(r, c) x_c for c ascending) and publishes x; (2) every thread subtracts the
+// panel's 32 columns from its rows below the panel (c ascending, coalesced column loads, eight
+// columns in flight). Backward mirrors it with panels from the bottom, columns descending,
+// divisions by the diagonal in the triangle. Per-element latency drops ~16x, so the kernel is
+// bound by the n^2 stream of the factor.
+constexpr int kPanel = 32;
+
+template <int R>
+__global__ void __launch_bounds__(kFbThreads, R <= 4 ? 3 : 1) fb_panel_kernel(DevPC pc, const double* __restrict__ in,
+                                                               double* __restrict__ out) {
+  if (pc.skip && *pc.skip) return;
+  extern __shared__ double sx[];  // x (n) | panel rows (kPanel)
+  double* sp = sx + pc.blk_len;
+  const int slot = blockIdx.x, blk = pc.fb_list[slot];
+  const int n = pc.blk_len, t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const double* lu = pc.fb_lu + size_t(slot) * n * n;
+  const int* perm = pc.fb_piv + size_t(slot) * n;
+  const double* b = in + size_t(blk) * n;
+  double s[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int i = t + kFbThreads * r;
+    s[r] = i < n ? b[perm[i]] : 0.0;
+  }
+  const int np = (n + kPanel - 1) / kPanel;
+  // ---- forward (unit lower), panels ascending
+  for (int pp = 0; pp < np; ++pp) {
+    const int c0 = pp * kPanel, cw = n - c0 < kPanel ? n - c0 : kPanel;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int i = t + kFbThreads * r;
+      if (i >= c0 && i < c0 + cw) sp[i - c0] = s[r];
+    }
+    __syncthreads();
+    if (warp == 0) {
+      const double* col = lu + size_t(c0) * n + c0 + lane;  // L(c0 + lane, c0 + c) at col[c n]
+      double tl[kPanel];
+#pragma unroll
+      for (int c = 0; c < kPanel; ++c) tl[c] = (lane > c && lane < cw) ? col[size_t(c) * n] : 0.0;
+      double v = lane < cw ? sp[lane] : 0.0;
+#pragma unroll
+      for (int c = 0; c < kPanel; ++c) {
+        const double xc = __shfl_sync(0xffffffffu, v, c);
+        if (lane > c && lane < cw) v = fmsc(v, tl[c], xc);
+      }
+      if (lane < cw) sx[c0 + lane] = v;
+    }
+    __syncthreads();
+    // rows below the panel: s_i -= L(i, c0 + c) x_{c0 + c}, c ascending
+    for (int cb = 0; cb < cw; cb += 8) {
+      double lv[8][R];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int i = t + kFbThreads * r, c = cb + u;
+          lv[u][r] = (c < cw && i >= c0 + cw && i < n) ? __ldcs(lu + size_t(c0 + c) * n + i) : 0.0;
+        }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int c = cb + u;
+        if (c < cw) {
+          const double xc = sx[c0 + c];
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const int i = t + kFbThreads * r;
+            if (i >= c0 + cw && i < n) s[r] = fmsc(s[r], lv[u][r], xc);
+          }
+        }
+      }
+    }
+  }
+  // the forward solution is in sx; rows keep it in s as the backward right-hand side
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int i = t + kFbThreads * r;
+    if (i < n) s[r] = sx[i];
+  }
+  __syncthreads();
+  // ---- backward (upper, with the diagonal), panels descending, columns descending
+  for (int pp = np - 1; pp >= 0; --pp) {
+    const int c0 = pp * kPanel, cw = n - c0 < kPanel ? n - c0 : kPanel;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int i = t + kFbThreads * r;
+      if (i >= c0 && i < c0 + cw) sp[i - c0] = s[r];
+    }
+    __syncthreads();
+    if (warp == 0) {
+      const double* col = lu + size_t(c0) * n + c0 + lane;  // U(c0 + lane, c0 + c) at col[c n]
+      double tu[kPanel];
+#pragma unroll
+      for (int c = 0; c < kPanel; ++c) tu[c] = (lane < c && c < cw) ? col[size_t(c) * n] : 0.0;
+      const double d = lane < cw ? lu[size_t(c0 + lane) * n + c0 + lane] : 1.0;
+      const double rdv = __drcp_rn(d);
+      double v = lane < cw ? sp[lane] : 0.0;
+#pragma unroll
+      for (int c = kPanel - 1; c >= 0; --c) {
+        if (c < cw) {
+          if (lane == c) v = fdiv_rcp(v, d, rdv);
+          const double xc = __shfl_sync(0xffffffffu, v, c);
+          if (lane < c) v = fmsc(v, tu[c], xc);
+        }
+      }
+      if (lane < cw) sx[c0 + lane] = v;
+    }
+    __syncthreads();
+    // rows above the panel: s_i -= U(i, c0 + c) x_{c0 + c}, c descending
+    for (int cb = cw - 1; cb >= 0; cb -= 8) {
+      double lv[8][R];
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int i = t + kFbThreads * r, c = cb - u;
+          lv[u][r] = (c >= 0 && i < c0) ? __ldcs(lu + size_t(c0 + c) * n + i) : 0.0;
+        }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int c = cb - u;
+        if (c >= 0) {
+          const double xc = sx[c0 + c];
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const int i = t + kFbThreads * r;
+            if (i < c0) s[r] = fmsc(s[r], lv[u][r], xc);
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+  double* o = out + size_t(blk) * n;
+  for (int i = t; i < n; i += kFbThreads) o[i] = sx[i];
+}
+
+template <int R>
+bool try_fb_panel(const DevPC& pc, const double* in, double* out, cudaStream_t st) {
+  if (pc.blk_len > R * kFbThreads) return false;
+  const size_t smem = sizeof(double) * size_t(pc.blk_len + kPanel);
+  static size_t configured = 0;
+  if (smem > configured) {
+    TPDG_CUDA_CHECK(cudaFuncSetAttribute(fb_panel_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    configured = smem;
+  }
+  fb_panel_kernel<R><<<pc.n_fb, kFbThreads, smem, st>>>(pc, in, out);
+  return true;
+}
+
 template <int R>
 bool try_fb(const DevPC& pc, const double* in, double* out, cudaStream_t st) {
   if (pc.blk_len > R * kFbThreads) return false;
@@ -121,6 +274,13 @@ bool try_fb(const DevPC& pc, const double* in, double* out, cudaStream_t st) {
 
 bool launch_fallback_apply(const DevPC& pc, const double* in, double* out, cudaStream_t st) {
   if (pc.n_fb == 0) return true;
+  static const bool columns = [] {  // TPDG_GPU_FB=col: one block barrier per column (fb_apply_kernel)
+    const char* f = std::getenv("TPDG_GPU_FB");
+    return f && f[0] == 'c';
+  }();
+  if (!columns)
+    return try_fb_panel<1>(pc, in, out, st) || try_fb_panel<2>(pc, in, out, st) ||
+           try_fb_panel<4>(pc, in, out, st) || try_fb_panel<8>(pc, in, out, st);
   return try_fb<1>(pc, in, out, st) || try_fb<2>(pc, in, out, st) || try_fb<4>(pc, in, out, st) ||
          try_fb<8>(pc, in, out, st);
 }
