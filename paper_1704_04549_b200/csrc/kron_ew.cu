@@ -224,7 +224,7 @@ __device__ __forceinline__ void replay(const double* cf, double (&b)[4]) {
 }
 
 template <int N, int P>
-__global__ void __launch_bounds__(32, P < N ? 7 : 16) kron2d_ew_kernel(DevPC pc, const double* __restrict__ in,
+__global__ void __launch_bounds__(32, P < N ? 7 : N > 24 ? 8 : 16) kron2d_ew_kernel(DevPC pc, const double* __restrict__ in,
                                                         double* __restrict__ out) {
   using C = Ew<N, P>;
   constexpr int EW = C::EW, LD = C::LD;
