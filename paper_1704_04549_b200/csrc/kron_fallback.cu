@@ -278,9 +278,10 @@ bool launch_fallback_apply(const DevPC& pc, const double* in, double* out, cudaS
     const char* f = std::getenv("TPDG_GPU_FB");
     return f && f[0] == 'c';
   }();
-  if (!columns)
-    return try_fb_panel<1>(pc, in, out, st) || try_fb_panel<2>(pc, in, out, st) ||
-           try_fb_panel<4>(pc, in, out, st) || try_fb_panel<8>(pc, in, out, st);
+  // panels pay off for large blocks (cfg2 p = 30, n = 961: 1.44 -> 0.91 ms); at n = 441 (p = 20) the
+  // per-column kernel's deeper prefetch ring is faster (209 vs 232 us)
+  if (!columns && pc.blk_len > 2 * kFbThreads)
+    return try_fb_panel<4>(pc, in, out, st) || try_fb_panel<8>(pc, in, out, st);
   return try_fb<1>(pc, in, out, st) || try_fb<2>(pc, in, out, st) || try_fb<4>(pc, in, out, st) ||
          try_fb<8>(pc, in, out, st);
 }
