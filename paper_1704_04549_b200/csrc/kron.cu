@@ -272,7 +272,7 @@ size_t kron2d_smem(const DevPC& pc) {
 constexpr int kSizedThreads = 64;
 
 #ifndef SYLV_FAST
-#define SYLV_FAST 1
+#define SYLV_FAST 0  // sized kernel: 1 = sylv_fast (lane per entry, measured 167 us at p=15) vs 132 us for the wavefront
 #endif
 #ifndef SYLV_EXP
 #define SYLV_EXP 0  // study builds only: 1 no cell loads, 2 no tiny solves
