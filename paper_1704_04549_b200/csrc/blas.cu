@@ -14,6 +14,8 @@
 
 #include <cooperative_groups.h>
 
+#include <cstdlib>
+
 #include "tpdg_internal.hpp"
 
 namespace tpdg_gpu {
@@ -608,6 +610,81 @@ __global__ void __launch_bounds__(kCoopThreads) mgs_reg_kernel(double* __restric
   fused_givens(G, k, gstatus);
 }
 
+// MODE 4 with the basis slice in registers (default for chunk <= 8192): the thread's pairs of v_j are
+// loaded straight into registers (16-byte loads) right after pass j-1's arithmetic, so they travel
+// during that pass's grid reduction; no shared-memory staging, no cp.async issue. Same pairs, same
+// operations and order as mgs_reg_kernel: bit-identical.
+template <int R>
+__global__ void __launch_bounds__(kCoopThreads) mgs_regv_kernel(double* __restrict__ V, int64_t ldv, int k, int64_t n,
+                                                                 int64_t chunk, double* __restrict__ hc,
+                                                                 double* __restrict__ partial, unsigned* bar,
+                                                                 const int* skip, GmresDev G, GmresStatus* gstatus) {
+  if (skip && *skip) return;
+  __shared__ double shA[32], shB[33];
+  const unsigned nb = gridDim.x;
+  const int64_t lo = int64_t(blockIdx.x) * chunk;
+  const int64_t hi = lo + chunk < n ? lo + chunk : n;
+  const int len = int(hi > lo ? hi - lo : 0);
+  double* wg = V + int64_t(k + 1) * ldv + lo;
+  const int t = threadIdx.x;
+  auto fetch = [&](const double* src, double2 (&dst)[R]) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int i = 2 * t + 2 * kCoopThreads * r;
+      dst[r] = i + 1 < len ? __ldcg(reinterpret_cast<const double2*>(src + i))
+                           : make_double2(i < len ? __ldcg(src + i) : 0.0, 0.0);
+    }
+  };
+  double2 w[R], vp[R], vq[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int i = 2 * t + 2 * kCoopThreads * r;
+    w[r] = i + 1 < len ? *reinterpret_cast<const double2*>(wg + i) : make_double2(i < len ? wg[i] : 0.0, 0.0);
+    vp[r] = make_double2(0.0, 0.0);
+  }
+  fetch(V + lo, vq);  // v_0
+  double h = 0.0;
+  for (int j = 0; j <= k + 1; ++j) {
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int i = 2 * t + 2 * kCoopThreads * r;
+      if (i < len) {
+        double2 wi = w[r];
+        if (j > 0) {
+          wi.x = wi.x - h * vp[r].x;
+          if (i + 1 < len) wi.y = wi.y - h * vp[r].y;
+          w[r] = wi;
+        }
+        if (i + 1 < len) {
+          const double2 a = j <= k ? vq[r] : wi;
+          s0 += a.x * wi.x;
+          s1 += a.y * wi.y;
+          vp[r] = a;
+        } else {
+          const double a = j <= k ? vq[r].x : wi.x;
+          s0 += a * wi.x;
+          vp[r] = make_double2(a, 0.0);
+        }
+      }
+    }
+    if (j + 1 <= k) fetch(V + int64_t(j + 1) * ldv + lo, vq);  // in flight during the grid reduction
+    const double tot = mgs_grid_sum(s0 + s1, partial + size_t(j) * nb, bar, shA, shB);
+    h = j <= k ? tot : sqrt(tot);
+    if (blockIdx.x == 0 && t == 0) hc[j] = h;
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int i = 2 * t + 2 * kCoopThreads * r;
+    if (i + 1 < len) {
+      *reinterpret_cast<double2*>(wg + i) = h > 0.0 ? make_double2(w[r].x / h, w[r].y / h) : w[r];
+    } else if (i < len) {
+      wg[i] = h > 0.0 ? w[r].x / h : w[r].x;
+    }
+  }
+  fused_givens(G, k, gstatus);
+}
+
 // MODE 9 (chunk too large for the shared-memory modes): w split between registers (the first
 // RR pairs of every thread) and shared memory (the rest), so a pass streams only v_{j-1} (L2) and
 // v_j (HBM, kept in L2 for the next pass). Same element assignment and accumulation order as
@@ -699,6 +776,14 @@ struct CoopPlan {
 };
 
 // One 1024-thread CTA per SM (cheap barrier); the most shared-memory residency that fits.
+bool mgs_smem_slices() {  // TPDG_GPU_MGS=smem: the shared-memory staged basis slices (mgs_reg_kernel)
+  static const bool v = [] {
+    const char* f = std::getenv("TPDG_GPU_MGS");
+    return f && f[0] == 's';
+  }();
+  return v;
+}
+
 CoopPlan mgs_coop_plan(int64_t n) {
   int dev = 0, sms = 0;
   TPDG_CUDA_CHECK(cudaGetDevice(&dev));
@@ -711,6 +796,10 @@ CoopPlan mgs_coop_plan(int64_t n) {
   chunk = (chunk + 1) & ~int64_t(1);
   const size_t one = size_t(chunk) * sizeof(double);
   int fit = 0;
+  if (chunk <= 4 * 2 * kCoopThreads && !mgs_smem_slices()) {  // w and v_j in registers (MODE 10 + R)
+    const int R = int((chunk + 2 * kCoopThreads - 1) / (2 * kCoopThreads));
+    return {sms, chunk, 0, 10 + R};
+  }
   if (chunk <= 4 * 2 * kCoopThreads) {  // register-resident w (MODE 4 + R)
     const int R = int((chunk + 2 * kCoopThreads - 1) / (2 * kCoopThreads));
     const void* fns[4] = {reinterpret_cast<const void*>(mgs_reg_kernel<1>), reinterpret_cast<const void*>(mgs_reg_kernel<2>),
@@ -805,7 +894,11 @@ void launch_mgs_iteration(double* V, int64_t ldv, int k, int64_t n, double* hc, 
   GmresDev g = G && G->m <= kFusedGivensMaxM ? *G : GmresDev{};
   GmresStatus* gs = G && G->m <= kFusedGivensMaxM ? status : nullptr;
   void* args[] = {&V, &ldv, &k, &n, &chunk, &hc, &partial, &bar, &skip, &g, &gs};
-  void* fn = plan.mode == 9   ? reinterpret_cast<void*>(mgs_split_kernel<8>)
+  void* fn = plan.mode == 11  ? reinterpret_cast<void*>(mgs_regv_kernel<1>)
+             : plan.mode == 12 ? reinterpret_cast<void*>(mgs_regv_kernel<2>)
+             : plan.mode == 13 ? reinterpret_cast<void*>(mgs_regv_kernel<3>)
+             : plan.mode == 14 ? reinterpret_cast<void*>(mgs_regv_kernel<4>)
+             : plan.mode == 9  ? reinterpret_cast<void*>(mgs_split_kernel<8>)
              : plan.mode == 5 ? reinterpret_cast<void*>(mgs_reg_kernel<1>)
              : plan.mode == 6 ? reinterpret_cast<void*>(mgs_reg_kernel<2>)
              : plan.mode == 7 ? reinterpret_cast<void*>(mgs_reg_kernel<3>)
