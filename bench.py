@@ -199,6 +199,7 @@ def main_ours(args, rank, world, local_rank):
     pc = T.form_ksvd(op)
     form_times = []
     for _ in range(3):
+        pc.close()  # release the previous preconditioner outside the timed region (cudaFree synchronizes)
         torch.cuda.synchronize()
         barrier()
         t0 = time.perf_counter()

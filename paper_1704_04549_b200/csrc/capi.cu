@@ -147,6 +147,7 @@ struct tpdg_gpu_op_s {
   DevBuf g, d, gw, dw, w, jdet, face_w, dft, dfm, dfp, conn, halo;
   DevBuf io_a, io_b;  // staging for the host-pointer entry points
   DevBuf shuf_ws;
+  DevBuf form_ws;  // Lanczos workspace of form_ksvd, kept across formations (up to ~4 GiB at cfg4)
   // halo plan (multi-rank): for each peer rank, local elements to send and halo slots to fill
   struct Peer {
     int rank = 0;
@@ -833,7 +834,8 @@ int tpdg_gpu_form_ksvd(tpdg_gpu_op op, const tpdg_gpu_ksvd_config* cfg_in, tpdg_
     std::vector<double> sv(size_t(m2 * m2)), sv2(size_t(q) * q);
     seeded_unit_vector(m2 * m2, cfg.seed, sv.data());
     seeded_unit_vector(int64_t(q) * q, cfg.seed, sv2.data());
-    DevBuf dsv, dsv2, work;
+    DevBuf dsv, dsv2;
+    DevBuf& work = op->form_ws;
     upload(dsv, sv.data(), sv.size(), st);
     upload(dsv2, sv2.data(), sv2.size(), st);
     const int J = std::max(cfg.lanczos_max_it > 0 ? cfg.lanczos_max_it : 2 * cfg.terms + 20, 22);
@@ -843,7 +845,8 @@ int tpdg_gpu_form_ksvd(tpdg_gpu_op op, const tpdg_gpu_ksvd_config* cfg_in, tpdg_
     while (groups > 148 && double(groups) * per * 8.0 > 4.0 * (1 << 30)) groups /= 2;
     const int grid = (groups + 7) / 8;
     if (pc->nblk > 0) {
-      work.alloc(sizeof(double) * size_t(grid) * 8 * per);
+      const size_t need = sizeof(double) * size_t(grid) * 8 * per;
+      if (work.bytes < need) work.alloc(need);
       launch_lanczos_form(op->s, cfg, dsv.as<double>(), dsv2.as<double>(), pc->raw.as<double>(), nullptr,
                           pc->kind.as<int>(), work.as<double>(), per, grid, st);
       TPDG_CUDA_CHECK(cudaStreamSynchronize(st));
