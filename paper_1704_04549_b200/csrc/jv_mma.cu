@@ -39,6 +39,8 @@ __device__ __forceinline__ const double* nbr_vals(const DevSys& s, const double*
   return nbr < s.n_local ? vin + size_t(nbr) * qq : halo + size_t(nbr - s.n_local) * qq;
 }
 
+constexpr int kJvWarps = 12;
+
 template <int Q, int MU>
 struct JvMmaLayout {
   static constexpr int QP = p8(Q), MP = p8(MU), KQ = p4(Q), KM = p4(MU), K2 = p4(2 * MU);
@@ -58,17 +60,22 @@ struct JvMmaLayout {
   static constexpr int r0_late = K2 * LAB;
   static constexpr int r0 = ((r0_early > r0_late ? r0_early : r0_late) + 1) & ~1;
   static constexpr int e_val = r0;
-  static constexpr int e_mf = e_val + MP * LVAL;
-  static constexpr int e_g = e_mf + MP * LMF;          // g[4][MU]
+  // [M | F0] is written by the point-wise pass, after v and t are dead, and read by product (3) before
+  // [A ; B] is stored: it shares region 0 when it fits
+  static constexpr bool mf_in_r0 = MP * LMF <= r0;
+  static constexpr int e_mf = mf_in_r0 ? 0 : e_val + MP * LVAL;
+  static constexpr int e_g = mf_in_r0 ? e_val + MP * LVAL : e_mf + MP * LMF;  // g[4][MU]
   static constexpr int e_lift = e_g + 4 * MU;          // lift vectors [4][Q]
   static constexpr int e_pw = (e_lift + 4 * Q + 1) & ~1; // jd | dft0 | dft1 of the element (cp.async, prefetched)
   static constexpr int per_warp = (e_pw + 3 * MU * MU + 1) & ~1;
   static constexpr int budget = (227 * 1024) / 8 - weights - 16;
-  static constexpr int warps = budget / per_warp > 8 ? 8 : budget / per_warp;
+  // 12 warps pay at q >= 16 (p = 15 / 20 / 30: 42 -> 41, 83 -> 81, 249 -> 207 us); p = 8 is faster with 8
+  static constexpr int wcap = Q >= 16 ? kJvWarps : 8;
+  static constexpr int warps = budget / per_warp > wcap ? wcap : budget / per_warp;
 };
 
 template <int Q, int MU>
-__global__ void __launch_bounds__(256) jv2d_mma_kernel(DevSys s, const double* __restrict__ vin,
+__global__ void __launch_bounds__(32 * kJvWarps) jv2d_mma_kernel(DevSys s, const double* __restrict__ vin,
                                                         const double* __restrict__ halo, double* __restrict__ vout) {
   if (s.skip && *s.skip) return;
   using L = JvMmaLayout<Q, MU>;
