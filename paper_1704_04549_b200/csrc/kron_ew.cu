@@ -55,6 +55,9 @@ __device__ __forceinline__ void copy_mat(double* dst, const double* src, int li)
   }
 }
 
+#ifndef EW_LDPAD
+#define EW_LDPAD 3
+#endif
 #ifndef EW16_LANES
 #define EW16_LANES 16  // lanes per block at N = 16 (2 blocks per warp); 8 (4 per warp) measured 114 vs 91 us
 #endif
@@ -68,7 +71,7 @@ __device__ __forceinline__ void copy_mat(double* dst, const double* src, int li)
 template <int N, int P = N>  // P lanes per block
 struct Ew {
   static constexpr int EW = 32 / P;  // blocks per warp
-  static constexpr int LD = N + 3;
+  static constexpr int LD = N + EW_LDPAD;  // X leading dimension (odd for even N: conflict-free fibers)
   static constexpr int XSZ = (N * LD + 1) & ~1;
   static constexpr int R1 = (2 * N * N > XSZ ? 2 * N * N : XSZ);
   static constexpr int HDR = ((4 + 4 * N) / 2 + 2) & ~1;  // sylv_hdr_doubles(N, N)
