@@ -1364,8 +1364,168 @@ void launch_assemble_fallback(const DevSys& s, const int* blocks, int nfb, doubl
   ++g_launches;
 }
 
+// Blocked variant of dense_lu_kernel with the same operations in the same order per entry
+// (LuFactor, tensor/small_matrix.hpp:143-172: partial pivoting with full-row swaps, multipliers
+// a_ik * (1 / a_kk), rank-1 updates a_ij -= l_ik u_kj in k order, separate mul / sub roundings).
+// Columns are processed in panels of KB: the panel is factored right-looking (its rows swapped at
+// each step), the panel's swaps are then applied to the other columns, and the trailing columns
+// receive the panel's KB rank-1 updates in k order in one pass (U-block rows first, by shuffles
+// inside the column's warp; then the rows below with the panel's multipliers staged in shared
+// memory). Each trailing entry sees exactly the unblocked sequence; the trailing matrix streams
+// once per panel instead of once per pivot (p = 30: 961^2 blocks).
+template <int KB>
+__global__ void __launch_bounds__(1024) dense_lu_blocked_kernel(int n, double* lu_all, int* piv_all, int* status) {
+  __shared__ double red_v[32];
+  __shared__ int red_i[32];
+  __shared__ double tol_sh;
+  __shared__ int piv_sh, piv_blk[KB];
+  extern __shared__ double Ls[];  // panel multipliers, [kk][i - k0] (n - k0 <= n rows)
+  double* lu = lu_all + size_t(blockIdx.x) * n * n;
+  int* perm = piv_all + size_t(blockIdx.x) * n;
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, wid = tid >> 5, nw = nt >> 5;
+#define A(i, j) lu[size_t(j) * n + (i)]
+  for (int i = tid; i < n; i += nt) perm[i] = i;
+  double m = 0.0;
+  for (int i = tid; i < n; i += nt) {
+    double s = 0.0;
+    for (int j = 0; j < n; ++j) s += fabs(A(i, j));
+    m = fmax(m, s);
+  }
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (lane == 0) red_v[wid] = m;
+  __syncthreads();
+  if (tid == 0) {
+    double mm = 0.0;
+    for (int w = 0; w < nw; ++w) mm = fmax(mm, red_v[w]);
+    tol_sh = 1e-14 * fmax(mm, 1e-300);
+  }
+  __syncthreads();
+  const double tol = tol_sh;
+  for (int k0 = 0; k0 < n; k0 += KB) {
+    const int kb = n - k0 < KB ? n - k0 : KB, kend = k0 + kb;
+    // ---- (1) panel factorization (columns [k0, kend))
+    for (int k = k0; k < kend; ++k) {
+      double best = -1.0;
+      int bi = n;
+      for (int i = k + tid; i < n; i += nt) {
+        const double v = fabs(A(i, k));
+        if (v > best) {
+          best = v;
+          bi = i;
+        }
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > best || (ov == best && oi < bi)) {
+          best = ov;
+          bi = oi;
+        }
+      }
+      if (lane == 0) {
+        red_v[wid] = best;
+        red_i[wid] = bi;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        double bv = red_v[0];
+        int bix = red_i[0];
+        for (int w = 1; w < nw; ++w)
+          if (red_v[w] > bv || (red_v[w] == bv && red_i[w] < bix)) {
+            bv = red_v[w];
+            bix = red_i[w];
+          }
+        if (bv < tol) {
+          atomicExch(status, int(TPDG_SINGULAR));
+          bix = k;
+        }
+        piv_sh = bix;
+        piv_blk[k - k0] = bix;
+        if (bix != k) {
+          const int t = perm[k];
+          perm[k] = perm[bix];
+          perm[bix] = t;
+        }
+      }
+      __syncthreads();
+      const int piv = piv_sh;
+      if (piv != k)
+        for (int j = k0 + tid; j < kend; j += nt) {
+          const double t = A(k, j);
+          A(k, j) = A(piv, j);
+          A(piv, j) = t;
+        }
+      __syncthreads();
+      const double inv = 1.0 / A(k, k);
+      for (int i = k + 1 + tid; i < n; i += nt) A(i, k) = A(i, k) * inv;
+      __syncthreads();
+      for (int j = k + 1 + wid; j < kend; j += nw) {
+        const double ukj = A(k, j);
+        for (int i = k + 1 + lane; i < n; i += 32) A(i, j) -= A(i, k) * ukj;
+      }
+      __syncthreads();
+    }
+    // ---- (2) the panel's row swaps on the other columns (per column, in pivot order)
+    for (int j = tid; j < n; j += nt) {
+      if (j >= k0 && j < kend) continue;
+      for (int kk = 0; kk < kb; ++kk) {
+        const int k = k0 + kk, piv = piv_blk[kk];
+        if (piv != k) {
+          const double t = A(k, j);
+          A(k, j) = A(piv, j);
+          A(piv, j) = t;
+        }
+      }
+    }
+    // panel multipliers of the rows below the panel into shared memory
+    for (int kk = 0; kk < kb; ++kk)
+      for (int i = kend + tid; i < n; i += nt) Ls[size_t(kk) * (n - kend) + (i - kend)] = A(i, k0 + kk);
+    __syncthreads();
+    // ---- (3) trailing columns: the panel's kb rank-1 updates in k order, one warp per column
+    for (int j = kend + wid; j < n; j += nw) {
+      // (3a) U-block rows k0 .. kend-1 (lane kk holds row k0 + kk)
+      double u = lane < kb ? A(k0 + lane, j) : 0.0;
+      for (int kk = 0; kk < kb; ++kk) {
+        const double ukk = __shfl_sync(0xffffffffu, u, kk);
+        const double l = (lane > kk && lane < kb) ? A(k0 + lane, k0 + kk) : 0.0;
+        if (lane > kk && lane < kb) u -= l * ukk;
+      }
+      if (lane < kb) A(k0 + lane, j) = u;
+      double ub[KB];  // the column's U-block values, broadcast while the warp is converged
+#pragma unroll
+      for (int kk = 0; kk < KB; ++kk) ub[kk] = __shfl_sync(0xffffffffu, u, kk);
+      // (3b) rows below the panel
+      for (int i = kend + lane; i < n; i += 32) {
+        double a = A(i, j);
+#pragma unroll
+        for (int kk = 0; kk < KB; ++kk)
+          if (kk < kb) a -= Ls[size_t(kk) * (n - kend) + (i - kend)] * ub[kk];
+        A(i, j) = a;
+      }
+    }
+    __syncthreads();
+  }
+#undef A
+}
+
 void launch_dense_lu(int n, int nfb, double* fb_lu, int* fb_piv, int* fb_status, cudaStream_t st) {
-  dense_lu_kernel<<<nfb, 1024, 0, st>>>(n, fb_lu, fb_piv, fb_status);
+  static const bool unblocked = [] {  // TPDG_GPU_DENSE_LU=unblocked: one trailing pass per pivot
+    const char* f = std::getenv("TPDG_GPU_DENSE_LU");
+    return f && f[0] == 'u';
+  }();
+  constexpr int KB = 16;
+  const size_t ls = sizeof(double) * size_t(KB) * size_t(n);
+  if (!unblocked && ls <= 200 * 1024) {
+    static size_t configured = 0;
+    if (ls > configured) {
+      TPDG_CUDA_CHECK(cudaFuncSetAttribute(dense_lu_blocked_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           int(ls)));
+      configured = ls;
+    }
+    dense_lu_blocked_kernel<KB><<<nfb, 1024, ls, st>>>(n, fb_lu, fb_piv, fb_status);
+  } else {
+    dense_lu_kernel<<<nfb, 1024, 0, st>>>(n, fb_lu, fb_piv, fb_status);
+  }
   TPDG_CUDA_CHECK(cudaGetLastError());
   ++g_launches;
 }

@@ -46,3 +46,26 @@ def test_block_jacobi_budget(ctx):
     op = T.LinearizedOperator(ctx, T.System.from_golden(z), float(z["meta"][5]))
     with pytest.raises(T.ConfigError):
         T.form_block_jacobi(op, max_total_entries=1000)
+
+
+def test_blocked_dense_lu_is_bit_identical():
+    """The panel-blocked dense LU (default) gives the same factors as the unblocked kernel: block-Jacobi applies of
+    golden cases compared bit for bit between two processes (TPDG_GPU_DENSE_LU is read once per process)."""
+    import json
+    import os
+    import subprocess
+    import sys
+    import tempfile
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for mode in ("", "unblocked"):
+        fd, path = tempfile.mkstemp(suffix=".json")
+        os.close(fd)
+        env = dict(os.environ, TPDG_GPU_DENSE_LU=mode)
+        r = subprocess.run([sys.executable, os.path.join(root, "tools", "dense_lu_compare.py"), path], env=env,
+                           cwd=root, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+        outs.append(json.load(open(path)))
+        os.unlink(path)
+    for case in outs[0]:
+        assert np.array_equal(np.array(outs[0][case]), np.array(outs[1][case])), case
