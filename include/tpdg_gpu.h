@@ -173,6 +173,17 @@ typedef struct tpdg_setup_s *tpdg_setup;
 int tpdg_setup_advection(int case_kind, const double *vel, int nx, int ny, int nz, int p, int periodic,
                          tpdg_setup *out);
 int tpdg_setup_system(tpdg_setup s, tpdg_gpu_system *sys);
+/* geometry at the quadrature points: adjugates [E][nvol][d][d], points [E][nvol][d], face unit normals and
+ * points [E][2d][nface][d] (mesh.hpp:72-106 adj_at / vol_x_at / face_n_at / face_x_at) */
+int tpdg_setup_geometry(tpdg_setup s, const double **adj, const double **vol_x, const double **face_n,
+                        const double **face_x, int *nvol, int *nface);
+/* build_cache (ops/linearized.hpp:38-100) of scalar upwind advection on the device, from device copies of the
+ * geometry: dft [E][d][nvol], dfm / dfp [E][2d][nface] (n_c = 1). field: 0 / 2 constant velocity vel (2D / 3D),
+ * 1 = (sin 2 pi y, cos 2 pi x). SURVEY.md sec.8f row 1 for the advection laws. */
+int tpdg_gpu_build_cache_advection(tpdg_gpu_ctx ctx, int dim, int n_elements, int nvol, int nface, const double *d_adj,
+                                   const double *d_vol_x, const double *d_face_n, const double *d_face_x,
+                                   const int64_t *d_conn, int field, const double *vel, double *d_dft, double *d_dfm,
+                                   double *d_dfp);
 int tpdg_setup_destroy(tpdg_setup s);
 /* libstdc++ std::mt19937_64 + uniform_real_distribution(-scale, scale) (tests/support/test_rng.hpp) */
 int tpdg_uniform_vector(uint64_t seed, int64_t n, double scale, double *out);

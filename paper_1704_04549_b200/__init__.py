@@ -22,7 +22,7 @@ LIB_PATH = os.environ.get("TPDG_GPU_LIB") or os.path.join(_HERE, "libtpdg_gpu.so
 __all__ = [
     "Error", "ShapeError", "SingularError", "StateError", "ConvergenceError", "ConfigError", "GmresFailure",
     "Context", "System", "LinearizedOperator", "KsvdConfig", "GmresConfig", "GmresResult", "KsvdPC",
-    "form_ksvd", "gmres", "setup_advection", "uniform_vector", "seeded_unit_vector", "lib", "build",
+    "form_ksvd", "gmres", "setup_advection", "uniform_vector", "seeded_unit_vector", "lib", "build", "build_advection_cache",
 ]
 
 
@@ -95,7 +95,8 @@ EXPORTS = [
     "tpdg_gpu_jv", "tpdg_gpu_jv_host", "tpdg_gpu_shuffled_host", "tpdg_gpu_form_ksvd",
     "tpdg_gpu_pc_import_factors", "tpdg_gpu_pc_import_record", "tpdg_gpu_form_block_jacobi", "tpdg_gpu_pc_destroy", "tpdg_gpu_pc_num_fallbacks", "tpdg_gpu_pc_fallbacks",
     "tpdg_gpu_pc_factor_len", "tpdg_gpu_pc_export_factors", "tpdg_gpu_pc_apply", "tpdg_gpu_pc_apply_host",
-    "tpdg_gpu_gmres", "tpdg_gpu_gmres_host", "tpdg_setup_advection", "tpdg_setup_system", "tpdg_setup_destroy",
+    "tpdg_gpu_gmres", "tpdg_gpu_gmres_host", "tpdg_setup_advection", "tpdg_setup_system", "tpdg_setup_destroy", "tpdg_setup_geometry",
+    "tpdg_gpu_build_cache_advection",
     "tpdg_uniform_vector", "tpdg_seeded_unit_vector", "tpdg_halo_plan_create", "tpdg_halo_plan_query",
     "tpdg_halo_plan_conn", "tpdg_halo_plan_halo_gid", "tpdg_halo_plan_peer", "tpdg_halo_plan_destroy",
 ]
@@ -114,6 +115,10 @@ def lib():
         return _lib
     if not os.path.exists(LIB_PATH):
         raise ImportError(f"{LIB_PATH} is missing: run paper_1704_04549_b200.build() (there is no CPU fallback)")
+    try:  # torch first: its bundled libnccl.so.2 (newer) then also serves this library's NCCL dependency;
+        import torch  # noqa: F401  loading ours first would bind the older system NCCL and break torch's import
+    except ImportError:
+        pass
     L = C.CDLL(LIB_PATH)
     v = C.c_void_p
     L.tpdg_gpu_last_error.restype = C.c_char_p
@@ -141,6 +146,9 @@ def lib():
                                 C.POINTER(C.c_int)],
         "tpdg_setup_advection": [C.c_int, dp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(v)],
         "tpdg_setup_system": [v, C.POINTER(_System)], "tpdg_setup_destroy": [v],
+        "tpdg_setup_geometry": [v, C.POINTER(dp), C.POINTER(dp), C.POINTER(dp), C.POINTER(dp), C.POINTER(C.c_int),
+                                C.POINTER(C.c_int)],
+        "tpdg_gpu_build_cache_advection": [v, C.c_int, C.c_int, C.c_int, C.c_int, v, v, v, v, v, C.c_int, dp, v, v, v],
         "tpdg_uniform_vector": [C.c_uint64, C.c_int64, C.c_double, dp],
         "tpdg_seeded_unit_vector": [C.c_int64, C.c_uint64, dp],
         "tpdg_halo_plan_create": [C.POINTER(_System), C.c_int, C.c_int, C.POINTER(v)],
@@ -248,9 +256,38 @@ def setup_advection(kind, nx, ny=None, nz=1, p=1, vel=(1.0, 0.5, 0.0), periodic=
                   "conn": arr(s.conn, E * 2 * dim * 3, np.int64), "dft": arr(s.dft, E * dim * nqv),
                   "dfm": arr(s.dfm, E * 2 * dim * nqf), "dfp": arr(s.dfp, E * 2 * dim * nqf)}
         del npe
-        return System(dim, 1, s.p, mu, E, arrays, s.state_hash)
+        sysm = System(dim, 1, s.p, mu, E, arrays, s.state_hash)
+        ga, gx, gn, gf = dp(), dp(), dp(), dp()
+        nv, nf = C.c_int(), C.c_int()
+        _check(lib().tpdg_setup_geometry(h, C.byref(ga), C.byref(gx), C.byref(gn), C.byref(gf), C.byref(nv),
+                                         C.byref(nf)))
+        sysm.geometry = {"adj": arr(ga, E * nv.value * dim * dim), "vol_x": arr(gx, E * nv.value * dim),
+                         "face_n": arr(gn, E * 2 * dim * nf.value * dim), "face_x": arr(gf, E * 2 * dim * nf.value * dim),
+                         "field": k, "vel": np.array([v[0], v[1], v[2] if dim == 3 else 0.0])}
+        return sysm
     finally:
         lib().tpdg_setup_destroy(h)
+
+
+def build_advection_cache(ctx: "Context", sysm: "System"):
+    """build_cache (ops/linearized.hpp:38-100) of scalar upwind advection on the device from the geometry of a
+    setup_advection system: returns host copies (dft, dfm, dfp) in the reference layouts."""
+    import torch
+    g = sysm.geometry
+    dim, E, mu = sysm.dim, sysm.n_elements, sysm.mu
+    nvol, nface = mu ** dim, mu ** (dim - 1)
+    dev = torch.device("cuda", ctx.device)
+    t = {k: torch.from_numpy(np.ascontiguousarray(g[k])).to(dev) for k in ("adj", "vol_x", "face_n", "face_x")}
+    conn = torch.from_numpy(sysm.arrays["conn"]).to(dev)
+    dft = torch.empty(E * dim * nvol, dtype=torch.float64, device=dev)
+    dfm = torch.empty(E * 2 * dim * nface, dtype=torch.float64, device=dev)
+    dfp = torch.empty_like(dfm)
+    vel = np.ascontiguousarray(g["vel"], dtype=np.float64)
+    _check(lib().tpdg_gpu_build_cache_advection(ctx.h, dim, E, nvol, nface, *(C.c_void_p(t[k].data_ptr()) for k in
+                                                ("adj", "vol_x", "face_n", "face_x")), C.c_void_p(conn.data_ptr()),
+                                                int(g["field"]), _ptr(vel), C.c_void_p(dft.data_ptr()),
+                                                C.c_void_p(dfm.data_ptr()), C.c_void_p(dfp.data_ptr())))
+    return dft.cpu().numpy(), dfm.cpu().numpy(), dfp.cpu().numpy()
 
 
 def halo_plan(sys: "System", rank: int, nranks: int) -> dict:

@@ -1076,6 +1076,32 @@ int tpdg_setup_advection(int case_kind, const double* vel, int nx, int ny, int n
   });
 }
 
+int tpdg_setup_geometry(tpdg_setup st, const double** adj, const double** vol_x, const double** face_n,
+                        const double** face_x, int* nvol, int* nface) {
+  return guarded([&] {
+    const Setup& s = st->s;
+    *adj = s.adj.data();
+    *vol_x = s.vol_x.data();
+    *face_n = s.face_n.data();
+    *face_x = s.face_x.data();
+    *nvol = s.dim == 2 ? s.mu * s.mu : s.mu * s.mu * s.mu;
+    *nface = s.dim == 2 ? s.mu : s.mu * s.mu;
+  });
+}
+
+int tpdg_gpu_build_cache_advection(tpdg_gpu_ctx ctx, int dim, int n_elements, int nvol, int nface, const double* d_adj,
+                                   const double* d_vol_x, const double* d_face_n, const double* d_face_x,
+                                   const int64_t* d_conn, int field, const double* vel, double* d_dft, double* d_dfm,
+                                   double* d_dfp) {
+  return guarded([&] {
+    REQUIRE(ctx && vel, TPDG_CONFIG, "build_cache_advection: null argument");
+    REQUIRE((dim == 2 || dim == 3) && field >= 0 && field <= 2, TPDG_CONFIG, "build_cache_advection: bad kind");
+    launch_build_cache_advection(dim, n_elements, nvol, nface, d_adj, d_vol_x, d_face_n, d_face_x, d_conn, field,
+                                 vel, d_dft, d_dfm, d_dfp, ctx->stream);
+    TPDG_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
 int tpdg_setup_system(tpdg_setup st, tpdg_gpu_system* sys) {
   return guarded([&] {
     const Setup& s = st->s;

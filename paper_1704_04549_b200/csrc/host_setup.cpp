@@ -300,6 +300,9 @@ int setup_advection(int kind, const double* vel, int nx, int ny, int nz, int p, 
     }
   }
   S.vol_x = vol_x;
+  S.adj = adj;
+  S.face_n = face_n;
+  S.face_x = face_x;
   // ---- linearization cache of scalar upwind advection (ops/linearized.hpp:38-100)
   auto velocity = [&](const double* xx, double* v) {
     if (kind == 1) {

@@ -29,11 +29,17 @@ void set_error(const std::string& what);
 struct Setup {
   int dim = 2, n_c = 1, p = 1, mu = 3, n_elements = 0;
   std::vector<double> g, d, gw, dw, w, qpoints, jdet, face_w, dft, dfm, dfp, vol_x;
+  std::vector<double> adj, face_n, face_x;  // geometry at the quadrature points (build_cache inputs)
   std::vector<int64_t> conn;
   uint64_t state_hash = 0;
 };
 int setup_advection(int kind, const double* vel, int nx, int ny, int nz, int p, int periodic, Setup& s);
 void uniform_vector(uint64_t seed, int64_t n, double scale, double* out);
+// build_cache of scalar upwind advection on the device (cache.cu); device pointers
+void launch_build_cache_advection(int dim, int n_elements, int nvol, int nface, const double* adj,
+                                  const double* vol_x, const double* face_n, const double* face_x,
+                                  const int64_t* conn, int field, const double* vel, double* dft, double* dfm,
+                                  double* dfp, cudaStream_t st);
 void seeded_unit_vector(int64_t n, uint64_t seed, double* out);
 
 // ---------------------------------------------------------------- multi-rank plan (halo.cpp)
