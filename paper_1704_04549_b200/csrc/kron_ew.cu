@@ -55,6 +55,9 @@ __device__ __forceinline__ void copy_mat(double* dst, const double* src, int li)
   }
 }
 
+#ifndef EW_BIGN
+#define EW_BIGN 24  // N above which the kernel may use up to 254 registers (8 warps per SM)
+#endif
 #ifndef EW_LDPAD
 #define EW_LDPAD 3
 #endif
@@ -227,7 +230,7 @@ __device__ __forceinline__ void replay(const double* cf, double (&b)[4]) {
 }
 
 template <int N, int P>
-__global__ void __launch_bounds__(32, P < N ? 7 : N > 24 ? 8 : 16) kron2d_ew_kernel(DevPC pc, const double* __restrict__ in,
+__global__ void __launch_bounds__(32, P < N ? 7 : N > EW_BIGN ? 8 : 16) kron2d_ew_kernel(DevPC pc, const double* __restrict__ in,
                                                         double* __restrict__ out) {
   using C = Ew<N, P>;
   constexpr int EW = C::EW, LD = C::LD;
