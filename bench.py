@@ -1,18 +1,23 @@
 #!/usr/bin/env python
-"""Benchmark: KSVD-preconditioned matrix-free GMRES on B200 (BASELINE.json configs[1]).
+"""Benchmark: KSVD-preconditioned matrix-free GMRES on B200.
 
-Workload (N=1 headline): 2D scalar linear advection, velocity (sin 2 pi y, cos 2 pi x), periodic
-unit square, 64x64 quads, Gauss-Lobatto p=15 (q=16, mu=17), backward Euler dt=0.005, operator
-A = M - dt J, right KSVD (r=2) preconditioner formed on the device, GMRES(30) to rel. tol 1e-10,
-RHS uniform[-1,1] from std::mt19937_64(12345). Synthetic inputs with exactly the config's
-shapes (there is no dataset). One step = one full GMRES solve from x0 = 0 on resident inputs.
+Headline workload (N=1): BASELINE.json configs[3] = cfg4, the largest single-GPU configuration
+(N = 5 451 776 DOF): 3D scalar linear advection, velocity (1, 0.7, 0.4), periodic unit cube,
+16x16x16 hexes, Gauss-Lobatto p=10 (q=11, mu=12), backward Euler dt=0.01, operator A = M - dt J,
+right 3D KSVD preconditioner (rank-1 x rank-2) formed on the device, GMRES(30) to rel. tol 1e-10,
+RHS uniform[-1,1] from std::mt19937_64(12345). Synthetic inputs with exactly the config's shapes
+(there is no dataset). One step = one full GMRES solve from x0 = 0 on resident inputs
+(159 iterations, the reference's count). cfg2 (configs[1]) at p = 15 and p = 30 ride along as
+extra keys (`extra`), measured the same way.
 
 value  = GDOF-iterations/s = N * iterations / t_solve (device CUDA events, max over ranks)
 e2e    = same metric through the C ABI with HOST buffers (pinned H2D of b + D2H of x per step)
 --impl reference : the reference CPU implementation (oracle/_ref/tpdg_ref_bench, compiled
-                   in place from the unmodified reference) on this box's host cores.
-Multi-GPU (torchrun): element rows partitioned across ranks, NCCL halo + allreduce (strong
-scaling of the fixed 64x64 problem).
+                   in place from the unmodified reference) on this box's host cores; each step is
+                   a bounded sample of the same workload (the first REF_ITS GMRES iterations of the
+                   solve, GDOF-it/s is a per-iteration metric).
+Multi-GPU (torchrun): element rows / slabs partitioned across ranks, NCCL halo + allreduce (strong
+scaling of the fixed problem).
 """
 import argparse
 import json
@@ -31,6 +36,7 @@ sys.path.insert(0, ROOT)
 METRIC = "preconditioned GMRES GDOF-iterations/s; Kronecker-apply GDOF/s vs roofline"
 REF_BENCH = os.path.join(ROOT, "oracle", "_ref", "tpdg_ref_bench")
 GOLDEN_ITS = {4: 17, 8: 18, 15: 25, 20: 39, 30: 21}  # reference GMRES counts, tests/golden/cfg2_p*.npz
+REF_ITS = 10  # GMRES iterations per reference step (bounded sample: ~0.85 s per cfg4 iteration on 16 cores)
 
 
 def workload(p, case="cfg2"):
@@ -44,6 +50,14 @@ def workload(p, case="cfg2"):
     return (f"cfg2: 2D advection, velocity (sin 2pi y, cos 2pi x), periodic unit square, 64x64 quads, "
             f"Gauss-Lobatto p={p}, backward Euler dt=0.005, A = M - dt J, right KSVD r=2 preconditioner, "
             f"GMRES(30) rel tol 1e-10, RHS uniform[-1,1] mt19937_64(12345), fp64")
+
+
+def config_of(case, p, N, world):
+    """The config dict both arms print (identical keys and values)."""
+    dims = {"cfg4": (3, 10, "16x16x16"), "cfg1": (2, 8, "8x8")}.get(case, (2, p, "64x64"))
+    return {"workload": workload(p, case), "case": case, "dim": dims[0], "p": dims[1], "mesh": dims[2], "N": N,
+            "parallelism": f"element rows/slabs x{world}",
+            "l2": "inputs larger than L2 (Krylov basis 31 x N x 8 B + factors + operator data > 126 MB)"}
 
 
 def build_case(T, case, p):
@@ -142,48 +156,81 @@ def main_reference(args, rank):
         return 0
     th = cpu_threads()
     ref_case = {"cfg4": "cfg4", "cfg1": "cfg1"}.get(args.case, f"cfg2_p{args.p}")
-    r = run_reference_bench(ref_case, th, 2000, args.warmup + args.steps)
+    r = run_reference_bench(ref_case, th, REF_ITS, args.warmup + args.steps, timeout=3600)
     times = r["gmres_s"][args.warmup:]
-    t = statistics.median(times)
     N, its = r["N"], r["gmres_its"]
-    value = N * its / t / 1e9
+    t_tot = sum(times)
+    value = N * its * len(times) / t_tot / 1e9
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GDOF-it/s", "n_gpus": args.gpus,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_tot / len(times) * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": workload(args.p, args.case), "N": N, "iterations": its, "p": args.p},
+        "config": config_of(args.case, args.p, N, args.gpus),
         "cpu_baseline": {"value": value, "unit": "GDOF-it/s", "cores": th, "kind": "reference",
-                         "sample": f"{args.steps} full GMRES solves ({its} iterations each) after {args.warmup} "
-                                   f"warm-up solves; unmodified reference, g++ -O3 -march=x86-64-v3, "
-                                   f"thread_count()={th}; form {r['form_s']:.3f} s, "
-                                   f"PC apply {r['pc_apply_s']:.3f} s, Jv {r['jv_s']:.3f} s"},
+                         "sample": f"each step = the first {its} GMRES(30) iterations of the solve (one step of "
+                                   f"{its} iterations after {args.warmup} warm-up steps); unmodified reference "
+                                   f"(oracle/_ref/tpdg_ref_bench, g++ -O3 -march=x86-64-v3), thread_count()={th}; "
+                                   f"form {r['form_s']:.3f} s, one PC apply {r['pc_apply_s']:.3f} s, one Jv "
+                                   f"{r['jv_s']:.3f} s"},
         "e2e": {"value": value, "unit": "GDOF-it/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "form_s": r["form_s"], "fallbacks": r["fallbacks"],
+        "iterations_per_step": its, "form_s": r["form_s"], "fallbacks": r["fallbacks"],
     }
     print(json.dumps(line))
     return 0
 
 
 # --------------------------------------------------------------------------- our arm
-def main_ours(args, rank, world, local_rank):
-    import torch
-    import paper_1704_04549_b200 as T
+def fp64_peaks():
+    """DFMA / DMMA FP64 rates measured on a pool B200 (tools/fp64_peak.cu -> profiles/fp64_peak.json)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peak.json")) as f:
+            d = json.load(f)
+        return float(d["fp64_dfma_tflops"]), float(d["fp64_dmma_tflops"])
+    except Exception:
+        return 35.91, 37.06
 
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl")
-        obj = [T.Context.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
+
+def load_traffic(case, p):
+    """Per-launch DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) from the committed ncu --set full
+    captures of this case (profiles/traffic.json, keyed by case tag), or {}."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f)
+    except Exception:
+        return {}
+    tag = case if case in ("cfg4", "cfg1") else f"cfg2_p{p}"
+    return {k: v for k, v in t.get(tag, {}).items() if not k.startswith("_")}
+
+
+def algorithmic_work(sysm, n_loc, nfb):
+    """Algorithmic bytes / flops per launch of the PC apply and the Jv (SURVEY.md sec.8d formulas).
+    Fallback blocks (dense block LU) count x, y and both LU triangles: 8 (2 n + n^2) bytes, 2 n^2 flops."""
+    q, mu, nc, d = sysm.q, sysm.mu, sysm.n_c, sysm.dim
+    n1 = nc * q
+    nk = n_loc - nfb
+    if d == 2:
+        bytes_pc = nk * 8.0 * (2 * n1 * q + 3 * n1 * n1 + 3 * q * q)
+        flops_pc = nk * 7.0 * n1 * q * (n1 + q)
+    else:  # 3D: B = 8 (2 n1 q^2 + n1^2 + 6 q^2), F = 2 n1^2 q^2 + 14 n1 q^3
+        bytes_pc = nk * 8.0 * (2 * n1 * q * q + n1 * n1 + 6 * q * q)
+        flops_pc = nk * (2.0 * n1 * n1 * q * q + 14.0 * n1 * q ** 3)
+    nb = nc * q ** d
+    bytes_pc += nfb * 8.0 * (2 * nb + nb * nb)
+    flops_pc += nfb * 2.0 * nb * nb
+    # Jv: B = 8 (2 n_c q^d + mu^d (1 + d n_c^2) + 4 d mu^(d-1) n_c^2)
+    bytes_jv = n_loc * 8.0 * (2 * nc * q ** d + mu ** d * (1 + d * nc * nc) + 4 * d * mu ** (d - 1) * nc * nc)
+    if d == 2:
+        T_ = 2 * mu * q * q + 2 * mu * mu * q
+        Tf = 2 * mu * q
     else:
-        torch.cuda.set_device(local_rank)
-        nccl_id = None
-    dev = torch.device("cuda", local_rank)
-    ctx = T.Context(local_rank, rank, world, nccl_id)
-    p = args.p
-    sysm, dt, ref_case, ref_its = build_case(T, args.case, p)
+        T_ = 2 * mu * q ** 3 + 2 * mu * mu * q * q + 2 * mu ** 3 * q
+        Tf = 2 * mu * q * q + 2 * mu * mu * q
+    flops_jv = n_loc * ((d + 2) * nc * T_ + 2 * d * nc * nc * mu ** d + 2 * d * (4 * nc * Tf + 4 * nc * nc * mu ** (d - 1)))
+    return bytes_pc, flops_pc, bytes_jv, flops_jv
+
+
+def measure_case(T, torch, ctx, dev, args, case, p, rank, world, local_rank, dist, cpu_leg, steps, warmup):
+    sysm, dt, ref_case, ref_its = build_case(T, case, p)
     op = T.LinearizedOperator(ctx, sysm, dt)
     N = sysm.N
     e0, e1 = op.e_begin, op.e_end
@@ -214,7 +261,7 @@ def main_ours(args, rank, world, local_rank):
     cfg = T.GmresConfig(tol=1e-10, restart=30, max_iterations=2000, side="right")
     stream = torch.cuda.ExternalStream(ctx.stream())
 
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         its, conv, _ = T.gmres_device(op, pc, b, x, cfg)
     torch.cuda.synchronize()
     barrier()
@@ -226,7 +273,7 @@ def main_ours(args, rank, world, local_rank):
         torch.cuda.synchronize()
         barrier()
         ev0.record(stream)
-        for _ in range(args.steps):
+        for _ in range(steps):
             its, conv, _ = T.gmres_device(op, pc, b, x, cfg)
             its_list.append(its)
         ev1.record(stream)
@@ -234,8 +281,8 @@ def main_ours(args, rank, world, local_rank):
         barrier()
     t_ms = ev0.elapsed_time(ev1)
     launches = ctx.launches() - launches0
-    # per-kernel breakdown: a separate pass with CUDA events around every PC / Jv / MGS launch
-    # (the events cost ~7 %, so they stay out of the timed region above)
+    # per-kernel breakdown: a separate pass with CUDA events around every PC / Jv / MGS launch on the
+    # library's stream (the events cost a few %, so they stay out of the timed region above)
     prof = {"pc_apply": (0.0, 0), "jv": (0.0, 0), "mgs": (0.0, 0)}
     t_prof_ms = t_ms
     if not args.no_profile:
@@ -245,7 +292,7 @@ def main_ours(args, rank, world, local_rank):
         ctx.profile(True)
         torch.cuda.synchronize()
         ev0.record(stream)
-        for _ in range(args.steps):
+        for _ in range(steps):
             T.gmres_device(op, pc, b, x, cfg)
         ev1.record(stream)
         torch.cuda.synchronize()
@@ -259,7 +306,7 @@ def main_ours(args, rank, world, local_rank):
     its_total = int(sum(its_list))
     value = N * its_total / (t_ms * 1e-3) / 1e9
 
-    # ---- end to end through the C ABI with host buffers (pinned)
+    # ---- end to end through the C ABI with host buffers (pinned): H2D of b and D2H of x inside every step
     bh = torch.from_numpy(b_host).pin_memory()
     xh = torch.empty_like(bh).pin_memory()
     bh_np, xh_np = bh.numpy(), xh.numpy()
@@ -268,7 +315,7 @@ def main_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     e2e_its = 0
-    for _ in range(args.steps):
+    for _ in range(steps):
         res = T.gmres(op, pc, bh_np, cfg, out=xh_np)
         e2e_its += res.iterations
     torch.cuda.synchronize()
@@ -277,110 +324,118 @@ def main_ours(args, rank, world, local_rank):
     if dist:
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     e2e_value = N * e2e_its / float(e2e_t.item()) / 1e9
-
-    # ---- roofline of the dominant kernel class (algorithmic bytes per SURVEY.md sec.8d)
-    hbm, hbm_kind = peaks()
-    q, mu, nc, d = sysm.q, sysm.mu, sysm.n_c, sysm.dim
     n_loc = e1 - e0
-    n1 = nc * q
-    if d == 2:
-        bytes_pc = n_loc * 8.0 * (2 * n1 * q + 3 * n1 * n1 + 3 * q * q)
-        flops_pc = n_loc * 7.0 * n1 * q * (n1 + q)
-    else:  # B = 8 (2 n1 q^2 + n1^2 + 6 q^2), F = 2 n1^2 q^2 + 14 n1 q^3
-        bytes_pc = n_loc * 8.0 * (2 * n1 * q * q + n1 * n1 + 6 * q * q)
-        flops_pc = n_loc * (2.0 * n1 * n1 * q * q + 14.0 * n1 * q ** 3)
-    bytes_jv = n_loc * 8.0 * (2 * nc * q ** d + mu ** d * (1 + d * nc * nc) + 4 * d * mu ** (d - 1) * nc * nc)
-    n_local = n_loc * nc * npe
-    # MGS region of iteration k (0-based in its cycle): 8 (5 (k+1) + 3) bytes per DOF
+    n_local = n_loc * sysm.n_c * npe
+
+    # ---- roofline per kernel class (algorithmic bytes per SURVEY.md sec.8d; MGS: the bytes the fused
+    # pass streams with w resident on chip = read w, read v_0..v_k, write v_{k+1}: 8 N (k + 3))
+    hbm, hbm_kind = peaks()
+    dfma, dmma = fp64_peaks()
+    bytes_pc, flops_pc, bytes_jv, flops_jv = algorithmic_work(sysm, n_loc, nfb)
     per_solve_its = its_list[0] if its_list else 0
     ks = [i % 30 for i in range(per_solve_its)]
-    bytes_mgs_per_it = [n_local * 8.0 * (5 * (k + 1) + 3) for k in ks]
+    bytes_mgs = float(np.mean([n_local * 8.0 * (k + 3) for k in ks])) if ks else 0.0
+    flops_mgs = float(np.mean([n_local * (4.0 * (k + 1) + 3) for k in ks])) if ks else 0.0
+    traffic = load_traffic(case, p)
+    # FP64 ceiling per kernel family: the bit-faithful 2D apply issues one FP64 instruction per flop
+    # (no FMA): half the DFMA rate; 3D apply and the Jv kernels contract with FMA / DMMA
+    p_pc = dfma / 2 if sysm.dim == 2 else dmma
+    p_jv = dmma if sysm.dim == 2 else dfma
     kern = {}
-    for name, algo in (("pc_apply", bytes_pc), ("jv", bytes_jv)):
+    for name, algo_b, algo_f, p64 in (("pc_apply", bytes_pc, flops_pc, p_pc), ("jv", bytes_jv, flops_jv, p_jv),
+                                       ("mgs", bytes_mgs, flops_mgs, dfma)):
         ms, cnt = prof[name]
-        if cnt:
-            avg = ms / cnt
-            kern[name] = {"launches": cnt, "avg_us": avg * 1e3, "share": ms / t_prof_ms,
-                          "algorithmic_bytes": algo, "achieved_gbs": algo / (avg * 1e-3) / 1e9}
-    ms, cnt = prof["mgs"]
-    if cnt:
-        algo = float(np.mean(bytes_mgs_per_it)) if bytes_mgs_per_it else 0.0
-        kern["mgs"] = {"launches": cnt, "avg_us": ms / cnt * 1e3, "share": ms / t_prof_ms,
-                       "algorithmic_bytes": algo, "achieved_gbs": algo / (ms / cnt * 1e-3) / 1e9}
+        if not cnt:
+            continue
+        avg_s = ms / cnt * 1e-3
+        t_hbm = algo_b / (hbm * 1e9)
+        t_fp = algo_f / (p64 * 1e12)
+        kern[name] = {"launches": cnt, "avg_us": avg_s * 1e6, "share": ms / t_prof_ms,
+                      "algorithmic_bytes": algo_b, "algorithmic_flops": algo_f,
+                      "achieved_gbs": algo_b / avg_s / 1e9, "hbm_frac": t_hbm / avg_s,
+                      "achieved_tflops": algo_f / avg_s / 1e12, "fp64_peak_tflops": p64, "fp64_frac": t_fp / avg_s,
+                      "bound": "hbm" if t_hbm >= t_fp else "fp64", "roofline_frac": max(t_hbm, t_fp) / avg_s,
+                      "dram_bytes_per_launch": traffic.get(name)}
     dom = max(kern, key=lambda k: kern[k]["share"]) if kern else None
     roof = None
-    traffic = {}
-    try:  # per-launch DRAM bytes of the same kernels from an ncu --set full capture (profiles/)
-        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
-            traffic = json.load(f)
-    except Exception:
-        pass
-    if "mgs_bytes_per_pass" in traffic and ks:
-        traffic["mgs"] = traffic["mgs_bytes_per_pass"] * float(np.mean([k + 2 for k in ks]))
     if dom:
-        ach = kern[dom]["achieved_gbs"]
-        roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm, "unit": "GB/s",
-                "frac": ach / hbm, "peak_kind": hbm_kind,
-                "traffic": traffic.get(dom) if (p == 15 and args.case == "cfg2") else None,
-                "algorithmic_bytes_per_launch": kern[dom]["algorithmic_bytes"]}
+        k = kern[dom]
+        roof = {"bound": "hbm", "kernel": dom, "achieved": k["achieved_gbs"], "peak": hbm, "unit": "GB/s",
+                "frac": k["hbm_frac"], "peak_kind": hbm_kind, "traffic": traffic.get(dom),
+                "algorithmic_bytes_per_launch": k["algorithmic_bytes"],
+                "fp64": {"achieved_tflops": k["achieved_tflops"], "peak_tflops": k["fp64_peak_tflops"],
+                         "frac": k["fp64_frac"], "peak_kind": "measured (profiles/fp64_peak.json)"},
+                "binding": k["bound"], "binding_frac": k["roofline_frac"]}
     kron = None
     if "pc_apply" in kern:
-        avg_s = kern["pc_apply"]["avg_us"] * 1e-6
-        # T_roof = max(B / BW_HBM, F / P_FP64); P_FP64 measured on the box (tools/fp64_peak.cu)
-        p64 = 37.06
-        try:
-            with open(os.path.join(ROOT, "profiles", "fp64_peak.json")) as f:
-                p64 = float(json.load(f)["fp64_dmma_tflops"])
-        except Exception:
-            pass
-        # 2D default kernel (kron_ew.cu) is bit-faithful: separate mul / add roundings, one flop per
-        # FP64 instruction, so its FP64 ceiling is half the DFMA rate; TPDG_GPU_KRON=mma and the 3D
-        # kernel use DMMA products (peak: measured DMMA rate)
-        faithful = d == 2 and os.environ.get("TPDG_GPU_KRON", "ew")[:1] not in ("m",)
-        p64_dfma = 35.91
-        try:
-            with open(os.path.join(ROOT, "profiles", "fp64_peak.json")) as f:
-                p64_dfma = float(json.load(f)["fp64_dfma_tflops"])
-        except Exception:
-            pass
-        p_eff = p64_dfma / 2 if faithful else p64
-        t_roof = max(bytes_pc / (hbm * 1e9), flops_pc / (p_eff * 1e12))
-        kron = {"value": n_local / avg_s / 1e9 * world, "unit": "GDOF/s",
-                "roofline_frac": t_roof / avg_s,
-                "bound": "hbm" if bytes_pc / hbm * 1e-9 >= flops_pc / p_eff * 1e-12 else "fp64",
-                "arithmetic": "bit-faithful (no FMA)" if faithful else "DMMA / FMA",
-                "flops_per_launch": flops_pc, "achieved_tflops": flops_pc / avg_s / 1e12, "fp64_peak_tflops": p_eff,
-                "hbm_frac": bytes_pc / (hbm * 1e9) / avg_s}
+        k = kern["pc_apply"]
+        kron = {"value": n_local / (k["avg_us"] * 1e-6) / 1e9 * world, "unit": "GDOF/s",
+                "roofline_frac": k["roofline_frac"], "bound": k["bound"], "hbm_frac": k["hbm_frac"],
+                "fp64_frac": k["fp64_frac"],
+                "arithmetic": "bit-faithful (no FMA)" if sysm.dim == 2 else "DMMA / FMA"}
 
-    # ---- CPU baseline (rank 0, N = 1): the unmodified reference on this host
+    # ---- CPU baseline (rank 0, N = 1): the unmodified reference on this host, bounded sample
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and os.path.exists(REF_BENCH):
+    if cpu_leg and os.path.exists(REF_BENCH):
         th = cpu_threads()
         try:
-            r = run_reference_bench(ref_case, th, 2000, 1, timeout=900)
+            r = run_reference_bench(ref_case, th, REF_ITS, 1, timeout=900)
             v = r["N"] * r["gmres_its"] / r["gmres_s"][-1] / 1e9
             cpu = {"value": v, "unit": "GDOF-it/s", "cores": th, "kind": "reference",
-                   "sample": f"one full GMRES solve ({r['gmres_its']} iterations) of the same workload, unmodified "
-                             f"reference (oracle/_ref/tpdg_ref_bench, g++ -O3 -march=x86-64-v3), "
-                             f"thread_count()={th}; form {r['form_s']:.3f} s, PC apply {r['pc_apply_s']:.3f} s, "
-                             f"Jv {r['jv_s']:.3f} s"}
+                   "sample": f"the first {r['gmres_its']} GMRES(30) iterations of the same solve, unmodified reference "
+                             f"(oracle/_ref/tpdg_ref_bench, g++ -O3 -march=x86-64-v3), thread_count()={th}; form "
+                             f"{r['form_s']:.3f} s, one PC apply {r['pc_apply_s']:.3f} s, one Jv {r['jv_s']:.3f} s"}
         except Exception as ex:  # reported, never fatal
             cpu = {"value": None, "unit": "GDOF-it/s", "cores": th, "kind": "reference", "sample": f"failed: {ex}"}
+    out = {"value": value, "ms_per_step": t_ms / steps, "N": N, "iterations_per_solve": per_solve_its,
+           "reference_iterations": ref_its, "fallbacks": nfb, "form_ms": form_s * 1e3,
+           "roofline": roof, "kron_apply": kron, "kernels": kern, "cpu_baseline": cpu,
+           "e2e": {"value": e2e_value, "unit": "GDOF-it/s", "h2d_bytes_per_step": 8 * n_local * world,
+                   "d2h_bytes_per_step": 8 * n_local * world},
+           "gpu_launches": launches, "clocks": clk.summary()}
+    pc.close()
+    op.close()
+    return out
 
+
+def main_ours(args, rank, world, local_rank):
+    import torch
+    import paper_1704_04549_b200 as T
+
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl")
+        obj = [T.Context.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    else:
+        torch.cuda.set_device(local_rank)
+        nccl_id = None
+    dev = torch.device("cuda", local_rank)
+    ctx = T.Context(local_rank, rank, world, nccl_id)
+    cpu_leg = rank == 0 and world == 1 and not args.no_cpu_baseline
+    h = measure_case(T, torch, ctx, dev, args, args.case, args.p, rank, world, local_rank, dist, cpu_leg,
+                     args.steps, args.warmup)
+    extra = {}
+    if world == 1 and args.extras and args.case == "cfg4":
+        for pp in (15, 30):  # BASELINE configs[1] points named in the sweep, same method, no CPU leg
+            e = measure_case(T, torch, ctx, dev, args, "cfg2", pp, rank, world, local_rank, dist, False,
+                             max(3, min(args.steps, 10)), args.warmup)
+            extra[f"cfg2_p{pp}"] = {k: e[k] for k in ("value", "ms_per_step", "N", "iterations_per_solve",
+                                                       "reference_iterations", "fallbacks", "form_ms", "e2e",
+                                                       "roofline", "kernels", "clocks")}
     if rank == 0:
+        cfgd = config_of(args.case, args.p, h["N"], world)
         line = {
-            "metric": METRIC, "value": value, "unit": "GDOF-it/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": t_ms / args.steps, "higher_is_better": True, "scaling": "strong",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": workload(p, args.case), "N": N,
-                       "iterations_per_solve": its_list[0] if its_list else None,
-                       "reference_iterations": ref_its, "fallbacks": nfb, "p": p if args.case == "cfg2" else None,
-                       "parallelism": f"element rows x{world}",
-                       "l2": "inputs larger than L2 (Krylov basis 31 x N x 8 B + factors + operator data > 126 MB)"},
-            "roofline": roof, "kron_apply": kron, "kernels": kern, "cpu_baseline": cpu,
-            "e2e": {"value": e2e_value, "unit": "GDOF-it/s", "h2d_bytes_per_step": 8 * n_local * world,
-                    "d2h_bytes_per_step": 8 * n_local * world},
-            "gpu_launches": launches, "clocks": clk.summary(), "form_ms": form_s * 1e3,
+            "metric": METRIC, "value": h["value"], "unit": "GDOF-it/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": h["ms_per_step"], "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic", "config": cfgd,
+            "iterations_per_solve": h["iterations_per_solve"], "reference_iterations": h["reference_iterations"],
+            "fallbacks": h["fallbacks"], "roofline": h["roofline"], "kron_apply": h["kron_apply"],
+            "kernels": h["kernels"], "cpu_baseline": h["cpu_baseline"], "e2e": h["e2e"],
+            "gpu_launches": h["gpu_launches"], "clocks": h["clocks"], "form_ms": h["form_ms"], "extra": extra,
         }
         print(json.dumps(line))
     if dist:
@@ -396,8 +451,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--p", type=int, default=15, choices=[4, 8, 15, 20, 30], help="cfg2 polynomial degree")
-    ap.add_argument("--case", default="cfg2", choices=["cfg2", "cfg1", "cfg4"],
-                    help="BASELINE config (headline: cfg2 = configs[1]; others for measurement)")
+    ap.add_argument("--case", default="cfg4", choices=["cfg4", "cfg2", "cfg1"],
+                    help="BASELINE config (headline: cfg4 = configs[3], the largest single-GPU config)")
+    ap.add_argument("--no-extras", dest="extras", action="store_false",
+                    help="skip the cfg2 p = 15 / p = 30 extra keys")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-clocks", action="store_true", help="diagnostic: do not sample nvidia-smi")
     ap.add_argument("--no-profile", action="store_true", help="diagnostic: no per-kernel events")

@@ -10,6 +10,8 @@
 //   KsvdPC2D::apply(in, out)                    pc.apply(in, out)            (host spans)
 //   KsvdPC2D::fallbacks                         pc.fallbacks()
 //   gmres(op, pc, b, GmresConfig)               tpdg::gpu::gmres(op, pc, b, cfg)
+//   form_block_jacobi(lin, mode, budget)        tpdg::gpu::form_block_jacobi(op, budget)
+//   GmresFailure{what, GmresResult}             tpdg::GmresFailure (reference types) / gpu::GmresFailure
 //
 // Define TPDG_GPU_WITH_REFERENCE (with the reference's proj/include on the include path) to get the
 // constructors taking the reference's own types and errors re-thrown as the reference's exception
@@ -19,6 +21,7 @@
 #include <cstdint>
 #include <span>
 #include <stdexcept>
+#include <algorithm>
 #include <string>
 #include <utility>
 #include <vector>
@@ -112,15 +115,21 @@ inline SystemArrays system_of(const tpdg::LinearizedOperator& lin) {
 class LinearizedOperator {
  public:
   // dt: backward-Euler step (operator M - dt J, the reference's mass_minus_dt_jacobian mode).
+  // jacobian_only = 1: J alone (LinearizedOperator::Mode::jacobian_only, ops/linearized.hpp:167-178).
   LinearizedOperator(const Context& ctx, const tpdg_gpu_system& sys, double dt, int block_mode = 0,
-                     int e_begin = 0, int e_end = -1) {
-    check(tpdg_gpu_op_create(ctx.handle(), &sys, dt, 0, block_mode, e_begin, e_end < 0 ? sys.n_elements : e_end,
-                             &h_));
+                     int e_begin = 0, int e_end = -1, int jacobian_only = 0)
+      : n_c_(sys.n_c), npe_(sys.dim == 2 ? (sys.p + 1) * (sys.p + 1) : (sys.p + 1) * (sys.p + 1) * (sys.p + 1)),
+        block_mode_(block_mode), jacobian_only_(jacobian_only), n1d_(sys.p + 1) {
+    check(tpdg_gpu_op_create(ctx.handle(), &sys, dt, jacobian_only, block_mode, e_begin,
+                             e_end < 0 ? sys.n_elements : e_end, &h_));
     check(tpdg_gpu_op_local_size(h_, &n_));
+    n_elements_ = int(n_ / (std::int64_t(n_c_) * npe_));
   }
 #ifdef TPDG_GPU_REFERENCE_TYPES
+  // Honours lin.mode and lin.block_mode; lin.check_cache() runs inside system_of (stale hash -> ConfigError).
   LinearizedOperator(const Context& ctx, const tpdg::LinearizedOperator& lin)
-      : LinearizedOperator(ctx, system_of(lin).sys, lin.dt, lin.block_mode == tpdg::BlockMode::small ? 1 : 0) {}
+      : LinearizedOperator(ctx, system_of(lin).sys, lin.dt, lin.block_mode == tpdg::BlockMode::small ? 1 : 0, 0, -1,
+                           lin.mode == tpdg::LinearizedOperator::Mode::jacobian_only ? 1 : 0) {}
 #endif
   ~LinearizedOperator() { tpdg_gpu_op_destroy(h_); }
   LinearizedOperator(const LinearizedOperator&) = delete;
@@ -132,11 +141,18 @@ class LinearizedOperator {
   }
   std::int64_t size() const { return n_; }
   tpdg_gpu_op handle() const { return h_; }
+  int n_elements() const { return n_elements_; }
+  int n_c() const { return n_c_; }
+  int npe() const { return npe_; }
+  int n1d() const { return n1d_; }
+  int block_mode() const { return block_mode_; }
+  bool jacobian_only() const { return jacobian_only_ != 0; }
 
  private:
   [[noreturn]] static void check_shape() { throw Error(TPDG_SHAPE, "jacobian_apply: state shape mismatch"); }
   tpdg_gpu_op h_ = nullptr;
   std::int64_t n_ = 0;
+  int n_c_ = 1, npe_ = 1, block_mode_ = 0, jacobian_only_ = 0, n1d_ = 1, n_elements_ = 0;
 };
 
 struct FallbackEvent {
@@ -144,13 +160,25 @@ struct FallbackEvent {
   int component = -1;
 };
 
+// KsvdPC2D / KsvdPC3D (precond/ksvd.hpp:161-170, 199-208) and BlockJacobiPC (block_jacobi.hpp:13-19):
+// the public shape fields of the reference classes, the factors stay on the device.
 class KsvdPC {
  public:
-  explicit KsvdPC(tpdg_gpu_pc h, std::int64_t n) : h_(h), n_(n) {}
+  KsvdPC(tpdg_gpu_pc h, const LinearizedOperator& op)
+      : mode(op.block_mode()), n_elements(op.n_elements()), n_c(op.n_c()), npe(op.npe()), n1d(op.n1d()), h_(h),
+        n_(op.size()) {}
   ~KsvdPC() { tpdg_gpu_pc_destroy(h_); }
   KsvdPC(const KsvdPC&) = delete;
   KsvdPC& operator=(const KsvdPC&) = delete;
-  KsvdPC(KsvdPC&& o) noexcept : h_(std::exchange(o.h_, nullptr)), n_(o.n_) {}
+  KsvdPC(KsvdPC&& o) noexcept
+      : mode(o.mode), n_elements(o.n_elements), n_c(o.n_c), npe(o.npe), n1d(o.n1d), h_(std::exchange(o.h_, nullptr)),
+        n_(o.n_) {}
+
+  int mode = 0;  // BlockMode: 0 = full, 1 = small
+  int n_elements = 0;
+  int n_c = 0;
+  int npe = 0;
+  int n1d = 0;
 
   void apply(std::span<const double> in, std::span<double> out) const {
     check(tpdg_gpu_pc_apply_host(h_, in.data(), out.data()));
@@ -174,15 +202,33 @@ class KsvdPC {
 inline KsvdPC form_ksvd(const LinearizedOperator& op, tpdg_gpu_ksvd_config cfg = {2, 0, 1e-12, 0x5eedULL, 1e-12}) {
   tpdg_gpu_pc h = nullptr;
   check(tpdg_gpu_form_ksvd(op.handle(), &cfg, &h));
-  return KsvdPC(h, op.size());
+  return KsvdPC(h, op);
 }
 
+// form_block_jacobi (precond/block_jacobi.hpp:38-72): the block mode is the operator's; max_total_entries <= 0
+// selects the reference's default budget (3e8). ConfigError over budget, SingularError on a singular block.
+inline KsvdPC form_block_jacobi(const LinearizedOperator& op, long max_total_entries = 300'000'000) {
+  tpdg_gpu_pc h = nullptr;
+  check(tpdg_gpu_form_block_jacobi(op.handle(), max_total_entries, &h));
+  return KsvdPC(h, op);
+}
+
+#ifdef TPDG_GPU_REFERENCE_TYPES
+using GmresResult = tpdg::GmresResult;
+using GmresFailure = tpdg::GmresFailure;
+#else
 struct GmresResult {
   std::vector<double> x;
   int iterations = 0;
   std::vector<double> residual_history;
   bool converged = false;
 };
+// solve/gmres.hpp:39-44: thrown when the iteration budget runs out; carries the best iterate.
+struct GmresFailure : Error {
+  GmresFailure(const std::string& what, GmresResult r) : Error(TPDG_CONVERGENCE, what), result(std::move(r)) {}
+  GmresResult result;
+};
+#endif
 
 inline GmresResult gmres(const LinearizedOperator& op, const KsvdPC& pc, std::span<const double> b,
                          tpdg_gpu_gmres_config cfg = {1e-5, 60, 2000, 0}) {
@@ -192,9 +238,11 @@ inline GmresResult gmres(const LinearizedOperator& op, const KsvdPC& pc, std::sp
   int conv = 0;
   const int rc = tpdg_gpu_gmres_host(op.handle(), pc.handle(), b.data(), r.x.data(), &cfg, &r.iterations,
                                      r.residual_history.data(), int(r.residual_history.size()), &conv);
-  r.residual_history.resize(std::size_t(r.iterations));
+  r.residual_history.resize(std::min(r.residual_history.size(), std::size_t(r.iterations)));
   r.converged = conv != 0;
-  if (rc != TPDG_OK) check(rc);  // TPDG_CONVERGENCE <-> GmresFailure (best iterate in r.x)
+  // budget exhausted: GmresFailure carrying the best iterate, like gmres.hpp:165-178
+  if (rc == TPDG_CONVERGENCE) throw GmresFailure(tpdg_gpu_last_error(), std::move(r));
+  if (rc != TPDG_OK) check(rc);
   return r;
 }
 

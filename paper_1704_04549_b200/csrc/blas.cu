@@ -240,6 +240,19 @@ __device__ __forceinline__ void fused_givens(const GmresDev& G, int k, GmresStat
 }
 
 // y = H(0:k, 0:k)^{-1} g (back substitution, solve/gmres.hpp:145-150), one thread.
+// Restarts whose H(0:k, 0:k) does not fit in shared memory (k > kBacksolveSmemMax) run the same
+// sequence straight from global memory (G.y as the solution buffer).
+constexpr int kBacksolveSmemMax = 160;  // 8 (k^2 + 2k + 1) B <= 227 KB
+__global__ void backsolve_global_kernel(GmresDev G, int k) {
+  if (threadIdx.x != 0) return;
+  const int m = G.m;
+  for (int i = k - 1; i >= 0; --i) {
+    double s = G.g[i];
+    for (int j = i + 1; j < k; ++j) s -= G.H[i * m + j] * G.y[j];
+    G.y[i] = s / G.H[i * m + i];
+  }
+}
+
 __global__ void backsolve_kernel(GmresDev G, int k) {
   // the warp stages H(0:k, 0:k) and g in shared memory (one round trip), then lane 0 runs the
   // sequential back substitution on-chip (same order as before)
@@ -922,7 +935,16 @@ void launch_givens(const GmresDev& G, int k, GmresStatus* status, cudaStream_t s
 }
 
 void launch_backsolve(const GmresDev& G, int k, cudaStream_t st) {
-  backsolve_kernel<<<1, 32, sizeof(double) * size_t(k * k + 2 * k + 1), st>>>(G, k);
+  if (k > kBacksolveSmemMax) {
+    backsolve_global_kernel<<<1, 32, 0, st>>>(G, k);
+    TPDG_CUDA_CHECK(cudaGetLastError());
+    ++g_launches;
+    return;
+  }
+  const size_t smem = sizeof(double) * size_t(k * k + 2 * k + 1);
+  if (smem > 48 * 1024)  // per call: cudaFuncSetAttribute is per device and cheap
+    TPDG_CUDA_CHECK(cudaFuncSetAttribute(backsolve_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  backsolve_kernel<<<1, 32, smem, st>>>(G, k);
   TPDG_CUDA_CHECK(cudaGetLastError());
   ++g_launches;
 }

@@ -563,7 +563,12 @@ void finish_pc(tpdg_gpu_pc pc) {
     work.alloc(sizeof(double) * size_t(probe_grid(nb, nfb)) * probe_work_doubles(op->s));
     launch_assemble_fallback(op->s, blocks.as<int>(), nfb, pc->fb_lu.as<double>(), work.as<double>(), st);
     launch_dense_lu(nb, nfb, pc->fb_lu.as<double>(), pc->fb_piv.as<int>(), pc->status.as<int>() + 1, st);
+    int sing = 0;
+    TPDG_CUDA_CHECK(cudaMemcpyAsync(&sing, pc->status.as<int>() + 1, sizeof(int), cudaMemcpyDeviceToHost, st));
     TPDG_CUDA_CHECK(cudaStreamSynchronize(st));
+    // LuFactor(assemble_diag_block(...)) of a fallback block throws SingularError out of form_ksvd_2d/3d
+    // (precond/ksvd.hpp:292-300, tensor/small_matrix.hpp:146-160) and out of form_block_jacobi
+    REQUIRE(sing == 0, TPDG_SINGULAR, "LuFactor: singular diagonal block (block-LU fallback)");
   }
   DevPC& d = pc->pc;
   d.dim = op->dim;
@@ -876,10 +881,7 @@ int tpdg_gpu_form_block_jacobi(tpdg_gpu_op op, int64_t max_total_entries, tpdg_g
     // factored with partial pivoting (assemble_diag_block(_small) + LuFactor), applied by the
     // dense-LU kernel (kron_fallback.cu)
     TPDG_CUDA_CHECK(cudaMemsetAsync(pc->kind.p, 0, sizeof(int) * size_t(pc->nblk), st));
-    finish_pc(pc.get());
-    int sing = 0;
-    TPDG_CUDA_CHECK(cudaMemcpy(&sing, pc->status.as<int>() + 1, sizeof(int), cudaMemcpyDeviceToHost));
-    REQUIRE(sing == 0, TPDG_SINGULAR, "form_block_jacobi: singular diagonal block");
+    finish_pc(pc.get());  // SingularError on a singular block
     pc->fallbacks.clear();  // not KSVD fallbacks: every block is exact by construction
     *out = pc.release();
   });

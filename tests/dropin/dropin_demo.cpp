@@ -2,12 +2,14 @@
 // run on the GPU box): the reference's own Discretization / LinearizationCache / LinearizedOperator
 // feed the B200 path through include/tpdg_gpu.hpp, and the reference's CPU gmres runs beside it.
 // Prints one JSON line: GMRES counts of both, Jv and PC-apply differences.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <random>
 
 #define TPDG_GPU_WITH_REFERENCE 1
 #include "tpdg/laws/advection.hpp"
+#include "tpdg/precond/block_jacobi.hpp"
 #include "tpdg/precond/ksvd.hpp"
 #include "tpdg/solve/gmres.hpp"
 #include "tpdg_gpu.hpp"
@@ -82,9 +84,55 @@ int main(int argc, char** argv) {
     }
     return std::sqrt(nn / dd);
   };
+
+  // Mode::jacobian_only (ops/linearized.hpp:167-178): the drop-in honours lin.mode
+  auto lin_j = make_linearized_operator(sys, cache, 0.005, LinearizedOperator::Mode::jacobian_only);
+  tpdg::gpu::LinearizedOperator gop_j(ctx, lin_j);
+  StateVector vb = sys.make_state();
+  vb.data = b;
+  const StateVector jref_j = jacobian_apply(lin_j, vb);
+  std::vector<double> jg_j(b.size());
+  gop_j.apply(b, jg_j);
+
+  // budget exhausted: both implementations throw GmresFailure carrying the best iterate (gmres.hpp:165-178)
+  GmresConfig gf = gc;
+  gf.max_iterations = 3;
+  int ref_fail_its = -1, gpu_fail_its = -1;
+  double fail_hist_rel = -1.0, fail_x_rel = -1.0;
+  std::vector<double> ref_fail_x, ref_fail_hist;
+  try {
+    gmres(op, [&](auto in, auto out) { kpc.apply(in, out); }, b, gf);
+  } catch (const GmresFailure& f) {
+    ref_fail_its = f.result.iterations;
+    ref_fail_x = f.result.x;
+    ref_fail_hist = f.result.residual_history;
+  }
+  try {
+    tpdg::gpu::gmres(gop, gpc, b, {1e-10, 30, 3, 0});
+  } catch (const GmresFailure& f) {  // tpdg::GmresFailure: the reference's own class
+    gpu_fail_its = f.result.iterations;
+    fail_x_rel = rel(f.result.x, ref_fail_x);
+    double mx = 0.0;
+    for (std::size_t i = 0; i < f.result.residual_history.size() && i < ref_fail_hist.size(); ++i)
+      mx = std::max(mx, std::abs(f.result.residual_history[i] - ref_fail_hist[i]) / ref_fail_hist[i]);
+    fail_hist_rel = f.result.residual_history.size() == ref_fail_hist.size() ? mx : 1.0;
+  }
+
+  // form_block_jacobi (precond/block_jacobi.hpp:38-72) through the same wrapper
+  const auto bj = form_block_jacobi(lin);
+  const auto gbj = tpdg::gpu::form_block_jacobi(gop);
+  std::vector<double> br(b.size()), bg(b.size());
+  bj.apply(b, br);
+  gbj.apply(b, bg);
+  const bool fields = gpc.mode == 0 && gpc.n_elements == kpc.n_elements && gpc.n_c == kpc.n_c && gpc.npe == kpc.npe &&
+                      gpc.n1d == kpc.n1d;
+
   std::printf("{\"n\": %d, \"p\": %d, \"ref_its\": %d, \"gpu_its\": %d, \"ref_fallbacks\": %zu, "
-              "\"gpu_fallbacks\": %zu, \"jv_rel\": %.3e, \"pc_rel\": %.3e}\n",
+              "\"gpu_fallbacks\": %zu, \"jv_rel\": %.3e, \"pc_rel\": %.3e, \"jv_jacobian_only_rel\": %.3e, "
+              "\"ref_fail_its\": %d, \"gpu_fail_its\": %d, \"fail_x_rel\": %.3e, \"fail_hist_rel\": %.3e, "
+              "\"block_jacobi_rel\": %.3e, \"pc_fields_match\": %d}\n",
               n, p, ref_res.iterations, gres.iterations, kpc.fallbacks.size(), gpc.fallbacks().size(), rel(jg, jr),
-              rel(zg, zr));
+              rel(zg, zr), rel(jg_j, jref_j.data), ref_fail_its, gpu_fail_its, fail_x_rel, fail_hist_rel,
+              rel(bg, br), int(fields));
   return ref_res.iterations == gres.iterations ? 0 : 1;
 }

@@ -10,6 +10,8 @@ import subprocess
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+# GPU-formed KSVD apply vs the reference's (north_star gate 1e-12; see test_gpu_parity.py for the trig note)
+PC_REL_GATE = 1e-12
 DEMO = os.path.join(ROOT, "tests", "dropin", "_build", "dropin_demo")
 
 
@@ -44,3 +46,10 @@ def test_reference_types_through_the_dropin(n, p):
     assert r.returncode == 0 and line["ref_its"] == line["gpu_its"]
     assert line["jv_rel"] <= 1e-12
     assert line["ref_fallbacks"] == line["gpu_fallbacks"]
+    assert line["jv_jacobian_only_rel"] <= 1e-12  # LinearizedOperator::Mode::jacobian_only honoured
+    # GmresFailure with the best iterate on both sides (solve/gmres.hpp:165-178)
+    assert line["ref_fail_its"] == line["gpu_fail_its"] == 3
+    assert line["fail_hist_rel"] <= 1e-8 and line["fail_x_rel"] <= 1e-8
+    assert line["block_jacobi_rel"] <= 1e-12
+    assert line["pc_fields_match"] == 1
+    assert line["pc_rel"] <= PC_REL_GATE
