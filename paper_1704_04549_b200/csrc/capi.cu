@@ -145,6 +145,9 @@ struct tpdg_gpu_op_s {
   int64_t n_local_dofs = 0;
   uint64_t hash = 0;
   DevBuf g, d, gw, dw, w, jdet, face_w, dft, dfm, dfp, conn, halo;
+  DevBuf cdfm, cdfp;                 // -b fw dfm, -b fw dfp (folded face data of the fast 3D operator)
+  DevBuf pw;                         // 3D n_c = 1: interleaved point-wise coefficients (jv3d.cu)
+  std::vector<double> hg, hgw, hdw;  // host copies of the 1D matrices (kernel-parameter packing)
   DevBuf io_a, io_b;  // staging for the host-pointer entry points
   DevBuf shuf_ws;
   DevBuf form_ws;  // Lanczos workspace of form_ksvd, kept across formations (up to ~4 GiB at cfg4)
@@ -221,6 +224,12 @@ DevSys make_devsys(const tpdg_gpu_op_s& op, int block_mode, double a, double b) 
   s.dfm = op.dfm.as<double>();
   s.dfp = op.dfp.as<double>();
   s.conn = op.conn.as<int>();
+  s.cdfm = op.cdfm.as<double>();
+  s.cdfp = op.cdfp.as<double>();
+  s.pw = op.pw.as<double>();
+  s.hg = op.hg.empty() ? nullptr : op.hg.data();
+  s.hgw = op.hgw.empty() ? nullptr : op.hgw.data();
+  s.hdw = op.hdw.empty() ? nullptr : op.hdw.data();
   return s;
 }
 
@@ -748,6 +757,40 @@ int tpdg_gpu_op_create(tpdg_gpu_ctx ctx, const tpdg_gpu_system* sys, double dt, 
     upload(op->dft, sys->dft + size_t(e_begin) * d * nqv * nc * nc, nl * d * nqv * nc * nc, st);
     upload(op->dfm, sys->dfm + size_t(e_begin) * 2 * d * nqf * nc * nc, nl * 2 * d * nqf * nc * nc, st);
     upload(op->dfp, sys->dfp + size_t(e_begin) * 2 * d * nqf * nc * nc, nl * 2 * d * nqf * nc * nc, st);
+    op->hg.assign(sys->g, sys->g + size_t(mu) * q);
+    op->hgw.assign(sys->gw, sys->gw + size_t(mu) * q);
+    op->hdw.assign(sys->dw, sys->dw + size_t(mu) * q);
+    {  // face data pre-scaled by -b fw (the factor face_lift applies, discretization.hpp:133-166)
+      const double bb = jacobian_only ? 1.0 : -dt;
+      const size_t nf = nl * 2 * d * nqf, ncc = size_t(nc) * nc;
+      std::vector<double> cm(nf * ncc), cp(nf * ncc);
+      const double* fw = sys->face_w + size_t(e_begin) * 2 * d * nqf;
+      const double* dm = sys->dfm + size_t(e_begin) * 2 * d * nqf * ncc;
+      const double* dp = sys->dfp + size_t(e_begin) * 2 * d * nqf * ncc;
+      for (size_t i = 0; i < nf; ++i) {
+        const double sc = -bb * fw[i];
+        for (size_t r = 0; r < ncc; ++r) {
+          cm[i * ncc + r] = sc * dm[i * ncc + r];
+          cp[i * ncc + r] = sc * dp[i * ncc + r];
+        }
+      }
+      upload(op->cdfm, cm.data(), cm.size(), st);
+      upload(op->cdfp, cp.data(), cp.size(), st);
+      if (d == 3 && nc == 1) {  // [e][point][a jdet, b dft_x, b dft_y, b dft_z] (linearized.hpp:112-140 fields)
+        const double aa = jacobian_only ? 0.0 : 1.0;
+        std::vector<double> pw(nl * nqv * 4);
+        const double* jd = sys->jdet + size_t(e_begin) * nqv;
+        const double* df = sys->dft + size_t(e_begin) * 3 * nqv;
+        for (size_t e = 0; e < nl; ++e)
+          for (size_t q0 = 0; q0 < nqv; ++q0) {
+            double* o = pw.data() + (e * nqv + q0) * 4;
+            o[0] = aa * jd[e * nqv + q0];
+            for (int r = 0; r < 3; ++r) o[1 + r] = bb * df[(e * 3 + r) * nqv + q0];
+          }
+        upload(op->pw, pw.data(), pw.size(), st);
+      }
+      TPDG_CUDA_CHECK(cudaStreamSynchronize(st));
+    }
     // partition + halo plan (halo.cpp)
     const HaloPlan plan = build_halo_plan(sys, ctx->rank, ctx->nranks, e_begin, e_end);
     const std::vector<int>& conn = plan.conn;

@@ -885,7 +885,7 @@ void launch_jv(const DevSys& s, const double* vin, const double* halo, double* v
     ++g_launches;
     return;
   }
-  if (s.dim == 3 && launch_jv3d_sized(s, vin, halo, vout, st)) {
+  if (s.dim == 3 && (launch_jv3d_fast(s, vin, halo, vout, st) || launch_jv3d_sized(s, vin, halo, vout, st))) {
     TPDG_CUDA_CHECK(cudaGetLastError());
     ++g_launches;
     return;

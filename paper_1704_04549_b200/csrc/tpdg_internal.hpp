@@ -66,6 +66,9 @@ struct DevSys {
   const double *jdet, *face_w, *dft, *dfm, *dfp;  // local element 0 first
   const int* conn;    // [n_local][2d][3]; neighbor index < n_local: local, >= n_local: halo slot
   const int* skip;    // optional device flag: kernels return immediately when *skip != 0
+  const double *cdfm, *cdfp;  // face Jacobians pre-scaled by -b fw (device; read by jv3d_fast)
+  const double* pw;           // 3D n_c = 1: [e][mu^3][a jdet, b dft_x, b dft_y, b dft_z] (device)
+  const double *hg, *hgw, *hdw;  // HOST copies of g, gw, dw (packed into kernel parameters at launch)
 };
 
 // Formed KSVD preconditioner, device side. One factor record per block (element, or element x
@@ -108,6 +111,8 @@ __host__ __device__ inline int raw_len_of(int dim, int n1, int q) { return dim =
 
 // ---------------------------------------------------------------- kernel launchers
 void launch_jv(const DevSys& s, const double* vin, const double* halo, double* vout, cudaStream_t st);
+// 3D n_c = 1 operator with constant-bank weights (jv3d.cu); false if no instance fits
+bool launch_jv3d_fast(const DevSys& s, const double* vin, const double* halo, double* vout, cudaStream_t st);
 bool launch_jv2d_mma(const DevSys& s, const double* vin, const double* halo, double* vout, cudaStream_t st);
 size_t jv_smem_bytes(const DevSys& s);
 void launch_pc_apply(const DevPC& pc, const double* in, double* out, cudaStream_t st);

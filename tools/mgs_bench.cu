@@ -24,6 +24,15 @@ int main(int argc, char** argv) {
   for (auto& x : h) x = rand() / double(RAND_MAX) - 0.5;
   cudaStream_t st;
   cudaStreamCreate(&st);
+  if (getenv("L2P")) {  // persisting L2 set-aside (evict_last lines) = the device maximum
+    int mx = 0;
+    cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, 0);
+    const size_t want = size_t(atof(getenv("L2P")) * mx);
+    cudaError_t e = cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+    size_t got = 0;
+    cudaDeviceGetLimit(&got, cudaLimitPersistingL2CacheSize);
+    printf("max persisting L2 %d B, set %zu -> %s, now %zu\n", mx, want, cudaGetErrorString(e), got);
+  }
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
