@@ -184,6 +184,9 @@ int tpdg_gpu_build_cache_advection(tpdg_gpu_ctx ctx, int dim, int n_elements, in
                                    const double *d_vol_x, const double *d_face_n, const double *d_face_x,
                                    const int64_t *d_conn, int field, const double *vel, double *d_dft, double *d_dfm,
                                    double *d_dfp);
+/* Test hook: the device libm of the formation (csrc/glibm.cuh, glibc 2.39's sin/cos/atan/atan2 as called by
+ * standardize_2x2, tensor/schur.hpp:91-108) on n device arguments. fn: 0 sin, 1 cos, 2 atan, 3 atan2(x, y). */
+int tpdg_gpu_libm_eval(tpdg_gpu_ctx ctx, int fn, int64_t n, const double *d_x, const double *d_y, double *d_out);
 int tpdg_setup_destroy(tpdg_setup s);
 /* libstdc++ std::mt19937_64 + uniform_real_distribution(-scale, scale) (tests/support/test_rng.hpp) */
 int tpdg_uniform_vector(uint64_t seed, int64_t n, double scale, double *out);

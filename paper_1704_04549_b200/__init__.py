@@ -96,7 +96,7 @@ EXPORTS = [
     "tpdg_gpu_pc_import_factors", "tpdg_gpu_pc_import_record", "tpdg_gpu_form_block_jacobi", "tpdg_gpu_pc_destroy", "tpdg_gpu_pc_num_fallbacks", "tpdg_gpu_pc_fallbacks",
     "tpdg_gpu_pc_factor_len", "tpdg_gpu_pc_export_factors", "tpdg_gpu_pc_apply", "tpdg_gpu_pc_apply_host",
     "tpdg_gpu_gmres", "tpdg_gpu_gmres_host", "tpdg_setup_advection", "tpdg_setup_system", "tpdg_setup_destroy", "tpdg_setup_geometry",
-    "tpdg_gpu_build_cache_advection",
+    "tpdg_gpu_build_cache_advection", "tpdg_gpu_libm_eval",
     "tpdg_uniform_vector", "tpdg_seeded_unit_vector", "tpdg_halo_plan_create", "tpdg_halo_plan_query",
     "tpdg_halo_plan_conn", "tpdg_halo_plan_halo_gid", "tpdg_halo_plan_peer", "tpdg_halo_plan_destroy",
 ]
@@ -149,6 +149,7 @@ def lib():
         "tpdg_setup_geometry": [v, C.POINTER(dp), C.POINTER(dp), C.POINTER(dp), C.POINTER(dp), C.POINTER(C.c_int),
                                 C.POINTER(C.c_int)],
         "tpdg_gpu_build_cache_advection": [v, C.c_int, C.c_int, C.c_int, C.c_int, v, v, v, v, v, C.c_int, dp, v, v, v],
+        "tpdg_gpu_libm_eval": [v, C.c_int, C.c_int64, v, v, v],
         "tpdg_uniform_vector": [C.c_uint64, C.c_int64, C.c_double, dp],
         "tpdg_seeded_unit_vector": [C.c_int64, C.c_uint64, dp],
         "tpdg_halo_plan_create": [C.POINTER(_System), C.c_int, C.c_int, C.POINTER(v)],
@@ -288,6 +289,20 @@ def build_advection_cache(ctx: "Context", sysm: "System"):
                                                 int(g["field"]), _ptr(vel), C.c_void_p(dft.data_ptr()),
                                                 C.c_void_p(dfm.data_ptr()), C.c_void_p(dfp.data_ptr())))
     return dft.cpu().numpy(), dfm.cpu().numpy(), dfp.cpu().numpy()
+
+
+def libm_eval(ctx: "Context", fn: str, x, y=None) -> np.ndarray:
+    """Test hook: the formation's device libm (csrc/glibm.cuh: glibc 2.39 sin/cos/atan/atan2 restated, as
+    standardize_2x2 calls them, tensor/schur.hpp:91-108) over the host arrays x (and y for atan2(x, y))."""
+    import torch
+    code = {"sin": 0, "cos": 1, "atan": 2, "atan2": 3}[fn]
+    dev = torch.device("cuda", ctx.device)
+    dx = torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).to(dev)
+    dy = torch.from_numpy(np.ascontiguousarray(y, dtype=np.float64)).to(dev) if y is not None else None
+    out = torch.empty_like(dx)
+    _check(lib().tpdg_gpu_libm_eval(ctx.h, code, dx.numel(), C.c_void_p(dx.data_ptr()),
+                                    C.c_void_p(dy.data_ptr()) if dy is not None else None, C.c_void_p(out.data_ptr())))
+    return out.cpu().numpy()
 
 
 def halo_plan(sys: "System", rank: int, nranks: int) -> dict:

@@ -7,9 +7,10 @@
 //   dfp[e][f][q] = min(v(x_q) . n_q, 0) on interior faces, 0 on boundary faces.
 // field 0 / 2: constant velocity (2D / 3D); 1: (sin 2 pi y, cos 2 pi x). Same operation order as
 // the host restatement (host_setup.cpp, bit-exact vs the reference) and no FMA (-fmad=false): the
-// constant fields reproduce it bit for bit; the swirl field differs by CUDA's sin/cos (<= 1 ulp).
+// fields reproduce it bit for bit (the swirl field's sin/cos in glibc's arithmetic, glibm.cuh).
 #include <cstdint>
 
+#include "glibm.cuh"
 #include "tpdg_internal.hpp"
 
 namespace tpdg_gpu {
@@ -18,8 +19,8 @@ namespace {
 
 __device__ __forceinline__ void velocity(int field, const double* vel, const double* x, double* v) {
   if (field == 1) {
-    v[0] = sin(2.0 * 3.14159265358979323846 * x[1]);
-    v[1] = cos(2.0 * 3.14159265358979323846 * x[0]);
+    v[0] = glibm_sin(2.0 * 3.14159265358979323846 * x[1]);
+    v[1] = glibm_cos(2.0 * 3.14159265358979323846 * x[0]);
     v[2] = 0.0;
   } else {
     v[0] = vel[0];
@@ -65,7 +66,21 @@ __global__ void cache_face_kernel(CacheArgs a) {
   }
 }
 
+// Test hook: fn 0 sin, 1 cos, 2 atan, 3 atan2(x, y) of glibm.cuh over n arguments.
+__global__ void libm_eval_kernel(int fn, int64_t n, const double* x, const double* y, double* out) {
+  for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const double a = x[i];
+    out[i] = fn == 0 ? glibm_sin(a) : fn == 1 ? glibm_cos(a) : fn == 2 ? glibm_atan(a) : glibm_atan2(a, y[i]);
+  }
+}
+
 } // namespace
+
+void launch_libm_eval(int fn, int64_t n, const double* x, const double* y, double* out, cudaStream_t st) {
+  libm_eval_kernel<<<148 * 8, 256, 0, st>>>(fn, n, x, y, out);
+  TPDG_CUDA_CHECK(cudaGetLastError());
+  g_launches += 1;
+}
 
 void launch_build_cache_advection(int dim, int n_elements, int nvol, int nface, const double* adj,
                                   const double* vol_x, const double* face_n, const double* face_x,

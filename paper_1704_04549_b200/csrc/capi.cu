@@ -1147,6 +1147,15 @@ int tpdg_gpu_build_cache_advection(tpdg_gpu_ctx ctx, int dim, int n_elements, in
   });
 }
 
+int tpdg_gpu_libm_eval(tpdg_gpu_ctx ctx, int fn, int64_t n, const double* d_x, const double* d_y, double* d_out) {
+  return guarded([&] {
+    REQUIRE(ctx && d_x && d_out && (fn != 3 || d_y), TPDG_CONFIG, "libm_eval: null argument");
+    REQUIRE(fn >= 0 && fn <= 3 && n >= 0, TPDG_CONFIG, "libm_eval: bad function");
+    launch_libm_eval(fn, n, d_x, d_y, d_out, ctx->stream);
+    TPDG_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
 int tpdg_setup_system(tpdg_setup st, tpdg_gpu_system* sys) {
   return guarded([&] {
     const Setup& s = st->s;

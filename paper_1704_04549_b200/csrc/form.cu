@@ -23,6 +23,7 @@
 #include <cstdio>
 
 #include "faithful.cuh"
+#include "glibm.cuh"
 #include "shuffled.cuh"
 #include "tpdg_internal.hpp"
 
@@ -535,8 +536,9 @@ __device__ void standardize_2x2_dev(const Grp& g, double* h, double* q, int n, i
     if (c == 0.0) {
       sh[3] = -1.0;
     } else {
-      const double th1 = 0.5 * atan2(d - a, b + c);
-      double cc = cos(th1), ss = sin(th1);
+      // libm calls in glibc's own arithmetic (glibm.cuh): bit-identical rotations to the reference
+      const double th1 = 0.5 * glibm_atan2(d - a, b + c);
+      double cc = glibm_cos(th1), ss = glibm_sin(th1);
       const double bt = cc * cc * b - ss * ss * c + cc * ss * (d - a);
       const double ct = cc * cc * c - ss * ss * b + cc * ss * (d - a);
       const bool real_pair = bt * ct >= 0.0;
@@ -544,13 +546,13 @@ __device__ void standardize_2x2_dev(const Grp& g, double* h, double* q, int n, i
       if (real_pair) {
         double th2;
         if (bt == 0.0)
-          th2 = (ct == 0.0) ? 0.0 : 2.0 * atan(1.0);
+          th2 = (ct == 0.0) ? 0.0 : 2.0 * glibm_atan(1.0);
         else
-          th2 = atan(sqrt(ct / bt));
+          th2 = glibm_atan(sqrt(ct / bt));
         th += th2;
       }
-      sh[0] = cos(th);
-      sh[1] = sin(th);
+      sh[0] = glibm_cos(th);
+      sh[1] = glibm_sin(th);
       sh[2] = real_pair ? 1.0 : 0.0;
       sh[3] = 1.0;
     }

@@ -36,6 +36,7 @@ struct Setup {
 int setup_advection(int kind, const double* vel, int nx, int ny, int nz, int p, int periodic, Setup& s);
 void uniform_vector(uint64_t seed, int64_t n, double scale, double* out);
 // build_cache of scalar upwind advection on the device (cache.cu); device pointers
+void launch_libm_eval(int fn, int64_t n, const double* x, const double* y, double* out, cudaStream_t st);
 void launch_build_cache_advection(int dim, int n_elements, int nvol, int nface, const double* adj,
                                   const double* vol_x, const double* face_n, const double* face_x,
                                   const int64_t* conn, int field, const double* vel, double* dft, double* dfm,

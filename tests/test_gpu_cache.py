@@ -8,16 +8,14 @@ import paper_1704_04549_b200 as T
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("kind,args,exact", [("const2d", dict(nx=8, ny=8, p=8, vel=(1.0, 0.5, 0.0)), True),
-                                             ("swirl2d", dict(nx=16, ny=16, p=15), False),
-                                             ("const3d", dict(nx=4, ny=4, nz=4, p=10, vel=(1.0, 0.7, 0.4)), True)])
-def test_device_cache_matches_host(kind, args, exact):
+@pytest.mark.parametrize("kind,args", [("const2d", dict(nx=8, ny=8, p=8, vel=(1.0, 0.5, 0.0))),
+                                       ("swirl2d", dict(nx=16, ny=16, p=15)), ("swirl2d", dict(nx=64, ny=64, p=15)),
+                                       ("const3d", dict(nx=4, ny=4, nz=4, p=10, vel=(1.0, 0.7, 0.4)))])
+def test_device_cache_matches_host(kind, args):
     ctx = T.Context(0)
     s = T.setup_advection(kind, **args)
     dft, dfm, dfp = T.build_advection_cache(ctx, s)
     for name, got in (("dft", dft), ("dfm", dfm), ("dfp", dfp)):
         ref = s.arrays[name]
-        if exact:
-            assert np.array_equal(got, ref), name
-        else:  # CUDA sin / cos vs glibc: <= 1-2 ulp of the velocity
-            assert np.max(np.abs(got - ref)) <= 4e-16 * max(1.0, np.max(np.abs(ref))), name
+        # the swirl field's sin / cos run in glibc's arithmetic on the device (csrc/glibm.cuh)
+        assert np.array_equal(got, ref), name

@@ -41,9 +41,9 @@ def test_cfg2_full_size(ctx, p):
     z, op, pc, res, ref_fb, got_fb, b = _solve(ctx, s, 0.005, f"cfg2_p{p}")
     assert res.converged
     assert res.iterations == int(z["gmres_meta"][0])
-    # decisions sit on a threshold with a few-percent margin: the reference's own
-    # FMA / no-FMA builds differ by one element at p=20, so allow at most 2 near-threshold flips
-    assert len(got_fb ^ ref_fb) <= 2
+    # fallback decisions sit on a threshold (the reference's own FMA / no-FMA builds
+    # differ by one element at p=20); the device formation follows the golden build's arithmetic
+    assert got_fb == ref_fb
     # size-independent properties: Jv linearity, PC apply linearity
     rng = np.random.default_rng(0)
     u, v = rng.uniform(-1, 1, s.N), rng.uniform(-1, 1, s.N)

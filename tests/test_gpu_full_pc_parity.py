@@ -69,7 +69,51 @@ def test_full_degree_pc_apply(ctx, p, faithful):
     # both kernel families in the default build are bit-faithful (kron_ew.cu / kron sized kernels);
     # the dense fallback's backward sweep runs column-descending (p = 30: ~1e-15)
     assert err_r <= 1e-12
-    assert err_f <= 1e-8
+    assert err_f <= 1e-12
+
+
+def _kron(fac, dim, q):
+    o = 0
+    a1 = fac[o:o + q * q].reshape(q, q); o += q * q
+    if dim == 2:
+        b1 = fac[o:o + q * q].reshape(q, q); o += q * q
+        a2 = fac[o:o + q * q].reshape(q, q); o += q * q
+        b2 = fac[o:o + q * q].reshape(q, q)
+        return np.kron(a1, b1) + np.kron(a2, b2)
+    b1, c1, b2, c2 = (fac[o + i * q * q:o + (i + 1) * q * q].reshape(q, q) for i in range(4))
+    return np.kron(a1, np.kron(b1, c1)) + np.kron(a1, np.kron(b2, c2))
+
+
+def _formed_parity(ctx, sub, osys, dt, dim, q, nblk):
+    """GPU-formed preconditioner of a full-degree slice vs the oracle's (bit-exact to the reference):
+    identical fallback set, Kronecker blocks <= 1e-10 rel-Frobenius, apply <= 1e-12."""
+    opc = osys.form()
+    op = T.LinearizedOperator(ctx, sub, dt)
+    pc = T.form_ksvd(op)
+    has = opc.has()
+    assert sorted(e for e, _ in pc.fallbacks) == [b for b in range(nblk) if not has[b]]
+    worst, exact = 0.0, 0
+    for b in range(nblk):
+        fac, h = pc.factors(b)
+        assert h == bool(has[b])
+        if not h:
+            continue
+        ref = opc.factors(b)
+        exact += int(np.array_equal(fac, ref))
+        P, Pr = _kron(fac, dim, q), _kron(ref, dim, q)
+        worst = max(worst, np.linalg.norm(P - Pr) / np.linalg.norm(Pr))
+    x = T.uniform_vector(7, sub.N, 1.0)
+    err = O.rel_l2(pc.apply(x), opc.apply(x))
+    print(f"q={q}: {int(has.sum())}/{nblk} factored, {exact} bit-identical factor sets, worst Kronecker block "
+          f"{worst:.3e}, GPU-formed apply vs reference {err:.3e}")
+    assert worst <= 1e-10
+    assert err <= 1e-12
+
+
+@pytest.mark.parametrize("p", [8, 15, 20, 30])
+def test_full_degree_gpu_formed(ctx, p):
+    sub, osys = slice_system(p)
+    _formed_parity(ctx, sub, osys, 0.005, 2, p + 1, K)
 
 
 
@@ -106,3 +150,8 @@ def test_full_size_cfg4_pc_apply(ctx):
     err = O.rel_l2(pc.apply(x), opc.apply(x))
     print(f"cfg4 slice: {len(fb)}/{K3} factored blocks, PC apply rel-L2 vs reference {err:.3e}")
     assert err <= 1e-12
+
+
+def test_full_size_cfg4_gpu_formed(ctx):
+    sub, osys, K3 = slice_system_3d()
+    _formed_parity(ctx, sub, osys, 0.01, 3, 11, K3)
