@@ -316,7 +316,7 @@ __device__ __forceinline__ void coop_barrier(unsigned* bar) {
   __syncthreads();
 }
 
-// L2 eviction-priority hints (createpolicy + .L2::cache_hint): in MODE 0 the working vector w
+// L2 eviction-priority hints (createpolicy + .L2::cache_hint): in mgs_global_kernel the working vector w
 // and the current basis vector are kept L2-resident across passes (evict_last), so a pass streams
 // only v_j from HBM instead of w (read + write), v_{j-1} and v_j.
 __device__ __forceinline__ uint64_t policy_evict_last() {
@@ -338,15 +338,12 @@ __device__ __forceinline__ void st2_hint(double* a, double2 v, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1,%2}, %3;" ::"l"(a), "d"(v.x), "d"(v.y), "l"(pol) : "memory");
 }
 
-// MODE 0: w in global/L2; 1: w slice in shared memory; 2: w and the previous basis vector's slice
-// in shared memory (each pass then streams only v_j from HBM).
-template <int MODE>
-__global__ void __launch_bounds__(kCoopThreads) mgs_coop_kernel(double* __restrict__ V, int64_t ldv, int k,
+// General fallback (slices too large to keep w on chip): w in global memory / L2.
+__global__ void __launch_bounds__(kCoopThreads) mgs_global_kernel(double* __restrict__ V, int64_t ldv, int k,
                                                                  int64_t n, int64_t chunk, double* __restrict__ hc,
                                                                  double* __restrict__ partial, unsigned* bar,
                                                                  const int* skip, GmresDev G, GmresStatus* gstatus) {
   if (skip && *skip) return;
-  extern __shared__ double wsm[];
   __shared__ double sh[32];
   __shared__ double hval;
   const unsigned nb = gridDim.x;
@@ -354,38 +351,25 @@ __global__ void __launch_bounds__(kCoopThreads) mgs_coop_kernel(double* __restri
   const int64_t hi = lo + chunk < n ? lo + chunk : n;
   const int64_t len = hi > lo ? hi - lo : 0;
   double* wg = V + int64_t(k + 1) * ldv + lo;
-  double* w = MODE >= 1 ? wsm : wg;
-  double* vs = wsm + chunk;  // MODE 2: previous basis vector slice
-  if (MODE >= 1) {
-    for (int64_t i = 2 * threadIdx.x; i + 1 < len; i += 2 * blockDim.x)
-      *reinterpret_cast<double2*>(wsm + i) = *reinterpret_cast<const double2*>(wg + i);
-    if ((len & 1) && threadIdx.x == 0) wsm[len - 1] = wg[len - 1];
-    __syncthreads();
-  }
+  double* w = wg;
   double h = 0.0;
   const uint64_t keep = policy_evict_last(), drop = policy_evict_first();
   for (int j = 0; j <= k + 1; ++j) {
-    const double* vp = j > 0 ? (MODE == 2 ? vs : V + int64_t(j - 1) * ldv + lo) : nullptr;
+    const double* vp = j > 0 ? V + int64_t(j - 1) * ldv + lo : nullptr;
     const double* vj = j <= k ? V + int64_t(j) * ldv + lo : nullptr;
     double s0 = 0.0, s1 = 0.0;
 #pragma unroll 4
     for (int64_t i = 2 * threadIdx.x; i < len; i += 2 * blockDim.x) {
       if (i + 1 < len) {
-        double2 wi = MODE == 0 ? ld2_hint(w + i, keep) : *reinterpret_cast<const double2*>(w + i);
+        double2 wi = ld2_hint(w + i, keep);
         if (vp) {
-          const double2 pv = MODE == 0 ? ld2_hint(vp + i, drop) : *reinterpret_cast<const double2*>(vp + i);
+          const double2 pv = ld2_hint(vp + i, drop);
           wi.x = wi.x - h * pv.x;
           wi.y = wi.y - h * pv.y;
-          if (MODE == 0)
-            st2_hint(w + i, wi, keep);
-          else
-            *reinterpret_cast<double2*>(w + i) = wi;
+          st2_hint(w + i, wi, keep);
         }
         double2 a = wi;
-        if (vj) {
-          a = MODE == 0 ? ld2_hint(vj + i, keep) : __ldg(reinterpret_cast<const double2*>(vj + i));
-          if (MODE == 2) *reinterpret_cast<double2*>(vs + i) = a;
-        }
+        if (vj) a = ld2_hint(vj + i, keep);
         s0 += a.x * wi.x;
         s1 += a.y * wi.y;
       } else {
@@ -395,10 +379,7 @@ __global__ void __launch_bounds__(kCoopThreads) mgs_coop_kernel(double* __restri
           w[i] = wi;
         }
         double a = wi;
-        if (vj) {
-          a = vj[i];
-          if (MODE == 2) vs[i] = a;
-        }
+        if (vj) a = vj[i];
         s0 += a * wi;
       }
     }
@@ -424,10 +405,6 @@ __global__ void __launch_bounds__(kCoopThreads) mgs_coop_kernel(double* __restri
   fused_givens(G, k, gstatus);
 }
 
-// MODE 3: w plus two basis-vector slices in shared memory; the slice of v_{j+1} is streamed with
-// cp.async (LDGSTS) right after pass j's arithmetic, so its HBM latency overlaps the grid barrier
-// and the reduction, and every pass computes from shared memory only. Each thread copies and later
-// reads exactly its own indices, so the only synchronization needed is its own cp.async.wait.
 // Grid reduction of one MGS pass: CTA partial (warp trees, then the 32 warp sums in order), the
 // generation barrier, and every thread summing the per-CTA partials in the same fixed order.
 // Three __syncthreads; bit-identical to block_sum + barrier + block_sum. Returns the total.
@@ -476,157 +453,9 @@ __device__ __forceinline__ double mgs_grid_sum(double v, double* part, unsigned*
   return shB[32];
 }
 
-__device__ __forceinline__ void cp16(double* smem, const double* gmem) {
-  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
-}
-
-__global__ void __launch_bounds__(kCoopThreads) mgs_pipe_kernel(double* __restrict__ V, int64_t ldv, int k, int64_t n,
-                                                                 int64_t chunk, double* __restrict__ hc,
-                                                                 double* __restrict__ partial, unsigned* bar,
-                                                                 const int* skip, GmresDev G, GmresStatus* gstatus) {
-  if (skip && *skip) return;
-  extern __shared__ double sm3[];
-  __shared__ double shA[32], shB[33];
-  const unsigned nb = gridDim.x;
-  const int64_t lo = int64_t(blockIdx.x) * chunk;
-  const int64_t hi = lo + chunk < n ? lo + chunk : n;
-  const int64_t len = hi > lo ? hi - lo : 0;  // even except possibly for the last CTA
-  double* w = sm3;
-  double* buf[2] = {sm3 + chunk, sm3 + 2 * chunk};
-  double* wg = V + int64_t(k + 1) * ldv + lo;
-  auto issue = [&](double* dst, const double* src) {
-    for (int64_t i = 2 * threadIdx.x; i + 1 < len; i += 2 * blockDim.x) cp16(dst + i, src + i);
-    if ((len & 1) && threadIdx.x == 0) dst[len - 1] = src[len - 1];
-  };
-  issue(w, wg);
-  issue(buf[0], V + lo);  // v_0
-  asm volatile("cp.async.wait_all;\n" ::: "memory");
-  __syncthreads();
-  double h = 0.0;
-  for (int j = 0; j <= k + 1; ++j) {
-    const double* vp = j > 0 ? buf[(j - 1) & 1] : nullptr;
-    const double* vj = j <= k ? buf[j & 1] : nullptr;
-    double s0 = 0.0, s1 = 0.0;
-    for (int64_t i = 2 * threadIdx.x; i < len; i += 2 * blockDim.x) {
-      if (i + 1 < len) {
-        double2 wi = *reinterpret_cast<const double2*>(w + i);
-        if (vp) {
-          const double2 pv = *reinterpret_cast<const double2*>(vp + i);
-          wi.x = wi.x - h * pv.x;
-          wi.y = wi.y - h * pv.y;
-          *reinterpret_cast<double2*>(w + i) = wi;
-        }
-        const double2 a = vj ? *reinterpret_cast<const double2*>(vj + i) : wi;
-        s0 += a.x * wi.x;
-        s1 += a.y * wi.y;
-      } else {
-        double wi = w[i];
-        if (vp) {
-          wi = wi - h * vp[i];
-          w[i] = wi;
-        }
-        s0 += (vj ? vj[i] : wi) * wi;
-      }
-    }
-    if (j + 1 <= k) issue(buf[(j + 1) & 1], V + int64_t(j + 1) * ldv + lo);  // v_{j+1} over v_{j-1}
-    {
-      const double tot = mgs_grid_sum(s0 + s1, partial + size_t(j) * nb, bar, shA, shB);
-      h = j <= k ? tot : sqrt(tot);
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0) hc[j] = h;
-    asm volatile("cp.async.wait_all;\n" ::: "memory");
-    if (len & 1) __syncthreads();  // the scalar tail element is copied by thread 0 only
-  }
-  for (int64_t i = threadIdx.x; i < len; i += blockDim.x) wg[i] = h > 0.0 ? w[i] / h : w[i];
-  fused_givens(G, k, gstatus);
-}
-
-// MODE 4 (chunk <= 8192): w and the previous basis vector live in registers (thread t owns the
-// pairs 2t + 2048 r, the same assignment and accumulation order as MODE 3, so the result is
-// bit-identical); only v_j passes through shared memory (cp.async double buffer).
-template <int R>
-__global__ void __launch_bounds__(kCoopThreads) mgs_reg_kernel(double* __restrict__ V, int64_t ldv, int k, int64_t n,
-                                                                int64_t chunk, double* __restrict__ hc,
-                                                                double* __restrict__ partial, unsigned* bar,
-                                                                const int* skip, GmresDev G, GmresStatus* gstatus) {
-  if (skip && *skip) return;
-  extern __shared__ double sm4[];
-  __shared__ double shA[32], shB[33];
-  const unsigned nb = gridDim.x;
-  const int64_t lo = int64_t(blockIdx.x) * chunk;
-  const int64_t hi = lo + chunk < n ? lo + chunk : n;
-  const int len = int(hi > lo ? hi - lo : 0);
-  double* buf[2] = {sm4, sm4 + chunk};
-  double* wg = V + int64_t(k + 1) * ldv + lo;
-  const int t = threadIdx.x;
-  auto issue = [&](double* dst, const double* src) {
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int i = 2 * t + 2 * kCoopThreads * r;
-      if (i + 1 < len) cp16(dst + i, src + i);
-      else if (i < len) dst[i] = src[i];
-    }
-  };
-  double2 w[R], vp[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int i = 2 * t + 2 * kCoopThreads * r;
-    w[r] = i + 1 < len ? *reinterpret_cast<const double2*>(wg + i) : make_double2(i < len ? wg[i] : 0.0, 0.0);
-    vp[r] = make_double2(0.0, 0.0);
-  }
-  issue(buf[0], V + lo);  // v_0
-  asm volatile("cp.async.wait_all;\n" ::: "memory");
-  __syncthreads();
-  double h = 0.0;
-  for (int j = 0; j <= k + 1; ++j) {
-    double s0 = 0.0, s1 = 0.0;
-    const double* vj = buf[j & 1];
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int i = 2 * t + 2 * kCoopThreads * r;
-      if (i < len) {
-        double2 wi = w[r];
-        if (j > 0) {
-          wi.x = wi.x - h * vp[r].x;
-          if (i + 1 < len) wi.y = wi.y - h * vp[r].y;
-          w[r] = wi;
-        }
-        if (i + 1 < len) {
-          const double2 a = j <= k ? *reinterpret_cast<const double2*>(vj + i) : wi;
-          s0 += a.x * wi.x;
-          s1 += a.y * wi.y;
-          vp[r] = a;
-        } else {
-          const double a = j <= k ? vj[i] : wi.x;
-          s0 += a * wi.x;
-          vp[r] = make_double2(a, 0.0);
-        }
-      }
-    }
-    if (j + 1 <= k) issue(buf[(j + 1) & 1], V + int64_t(j + 1) * ldv + lo);
-    const double tot = mgs_grid_sum(s0 + s1, partial + size_t(j) * nb, bar, shA, shB);
-    h = j <= k ? tot : sqrt(tot);
-    if (blockIdx.x == 0 && t == 0) hc[j] = h;
-    asm volatile("cp.async.wait_all;\n" ::: "memory");
-    if (len & 1) __syncthreads();  // a scalar tail element is copied by one thread only
-  }
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int i = 2 * t + 2 * kCoopThreads * r;
-    if (i + 1 < len) {
-      *reinterpret_cast<double2*>(wg + i) = h > 0.0 ? make_double2(w[r].x / h, w[r].y / h) : w[r];
-    } else if (i < len) {
-      wg[i] = h > 0.0 ? w[r].x / h : w[r].x;
-    }
-  }
-  fused_givens(G, k, gstatus);
-}
-
-// MODE 4 with the basis slice in registers (default for chunk <= 8192): the thread's pairs of v_j are
-// loaded straight into registers (16-byte loads) right after pass j-1's arithmetic, so they travel
-// during that pass's grid reduction; no shared-memory staging, no cp.async issue. Same pairs, same
-// operations and order as mgs_reg_kernel: bit-identical.
+// Slices of <= 8192 doubles per CTA (cfg2 p <= 15): w, v_{j-1} and v_j in registers. The thread's
+// pairs of v_j are loaded straight into registers (16-byte loads) right after pass j-1's arithmetic,
+// so they travel during that pass's grid reduction.
 template <int R>
 __global__ void __launch_bounds__(kCoopThreads) mgs_regv_kernel(double* __restrict__ V, int64_t ldv, int k, int64_t n,
                                                                  int64_t chunk, double* __restrict__ hc,
@@ -698,71 +527,140 @@ __global__ void __launch_bounds__(kCoopThreads) mgs_regv_kernel(double* __restri
   fused_givens(G, k, gstatus);
 }
 
-// MODE 9 (chunk too large for the shared-memory modes): w split between registers (the first
-// RR pairs of every thread) and shared memory (the rest), so a pass streams only v_{j-1} (L2) and
-// v_j (HBM, kept in L2 for the next pass). Same element assignment and accumulation order as
-// MODE 0 (pairs 2t + 2048 r, r ascending): bit-identical results.
-template <int RR>
-__global__ void __launch_bounds__(kCoopThreads) mgs_split_kernel(double* __restrict__ V, int64_t ldv, int k, int64_t n,
-                                                                  int64_t chunk, double* __restrict__ hc,
-                                                                  double* __restrict__ partial, unsigned* bar,
-                                                                  const int* skip, GmresDev G, GmresStatus* gstatus) {
+// ---- TMA bulk-copy MGS for large chunks (cfg4, cfg2 p >= 20) --------------------------------
+// mbarrier + cp.async.bulk (the TMA engine's 1D global->shared copy) helpers.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
+__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  unsigned ok;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n}"
+        : "=r"(ok)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* b, uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+          "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(b)), "l"(pol)
+      : "memory");
+}
+
+// Same passes, element assignment (thread t owns the pairs 2t + 2048 r of its CTA's slice) and
+// accumulation order (r ascending, even/odd elements in s0/s1) as every other MGS kernel, hence
+// bit-identical; the data movement differs: the basis rows a pass needs (v_j, and v_{j-1} for the
+// update) stream through an NS-stage shared-memory ring filled by the TMA engine (one thread issues
+// cp.async.bulk per row; completion on an mbarrier), so no register or issue slot is spent on loads
+// and a row's copies for the next pass are in flight during the grid reduction. w lives on chip for
+// the whole launch: rows r < RW in registers, the rest in shared memory behind the ring. v_j is
+// kept in L2 (evict_last) for the next pass's update read, v_{j-1} is then dropped (evict_first).
+template <int NT, int RW, int NS>
+__global__ void __launch_bounds__(NT, 1) mgs_bulk_kernel(double* __restrict__ V, int64_t ldv, int k, int64_t n,
+                                                         int64_t chunk, double* __restrict__ hc,
+                                                         double* __restrict__ partial, unsigned* bar, const int* skip,
+                                                         GmresDev G, GmresStatus* gstatus) {
   if (skip && *skip) return;
-  extern __shared__ double wsm5[];  // w pairs r >= RR: local index i - 2048 RR
+  constexpr int ROW = 2 * NT;  // doubles per row: one pair per thread
+  extern __shared__ __align__(128) double bsm[];
+  double* ring = bsm;             // stage s: v_j row at ring + 2 ROW s, v_{j-1} row at + ROW
+  double* wsm = bsm + 2 * ROW * NS;  // w rows RW.. (row r at wsm + (r - RW) ROW)
+  __shared__ __align__(8) uint64_t full[NS], empty[NS];
   __shared__ double shA[32], shB[33];
   const unsigned nb = gridDim.x;
   const int64_t lo = int64_t(blockIdx.x) * chunk;
   const int64_t hi = lo + chunk < n ? lo + chunk : n;
   const int len = int(hi > lo ? hi - lo : 0);
-  constexpr int SPLIT = 2 * kCoopThreads * RR;
+  const int nrows = (len + ROW - 1) / ROW;
   double* wg = V + int64_t(k + 1) * ldv + lo;
-  const int t = threadIdx.x;
-  const uint64_t keep = policy_evict_last(), drop = policy_evict_first();
-  double2 wr[RR];
+  const int t = threadIdx.x, lane = t & 31;
+  if (t == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NT / 32);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  double2 wr[RW];
 #pragma unroll
-  for (int r = 0; r < RR; ++r) {
-    const int i = 2 * t + 2 * kCoopThreads * r;
+  for (int r = 0; r < RW; ++r) {
+    const int i = 2 * t + ROW * r;
     wr[r] = i + 1 < len ? *reinterpret_cast<const double2*>(wg + i) : make_double2(i < len ? wg[i] : 0.0, 0.0);
   }
-  for (int i = SPLIT + 2 * t; i < len; i += 2 * kCoopThreads) {
+  for (int i = ROW * RW + 2 * t; i < len; i += ROW) {
     if (i + 1 < len)
-      *reinterpret_cast<double2*>(wsm5 + i - SPLIT) = *reinterpret_cast<const double2*>(wg + i);
+      *reinterpret_cast<double2*>(wsm + i - ROW * RW) = *reinterpret_cast<const double2*>(wg + i);
     else
-      wsm5[i - SPLIT] = wg[i];
+      wsm[i - ROW * RW] = wg[i];
   }
   __syncthreads();
+  const uint64_t keep = policy_evict_last(), drop = policy_evict_first();
+  const int ntask = (k + 2) * nrows;  // task = (pass j, row r), j-major; stage task % NS
+  auto issue = [&](int task) {        // thread 0: the copies of one task
+    const int j = task / nrows, r = task - j * nrows, s = task % NS;
+    const int cnt = min(ROW, len - r * ROW);
+    const unsigned bytes = unsigned((cnt + 1) & ~1) * 8u;  // V rows are padded: reading the pad is safe
+    mbar_expect_tx(&full[s], (j <= k ? bytes : 0u) + (j > 0 ? bytes : 0u));
+    if (j <= k) bulk_g2s(ring + 2 * ROW * s, V + int64_t(j) * ldv + lo + r * ROW, bytes, &full[s], keep);
+    if (j > 0) bulk_g2s(ring + 2 * ROW * s + ROW, V + int64_t(j - 1) * ldv + lo + r * ROW, bytes, &full[s], drop);
+  };
+  if (t == 0)
+    for (int q = 0; q < NS - 1 && q < ntask; ++q) issue(q);
   double h = 0.0;
+  int task = 0;
   for (int j = 0; j <= k + 1; ++j) {
-    const double* vp = j > 0 ? V + int64_t(j - 1) * ldv + lo : nullptr;
-    const double* vj = j <= k ? V + int64_t(j) * ldv + lo : nullptr;
     double s0 = 0.0, s1 = 0.0;
-    auto pass = [&](double2& wi, int i) {
+    auto row = [&](double2& wi, int r) {
+      const int s = task % NS;
+      if (t == 0 && task + NS - 1 < ntask) {  // refill the stage freed by task - 1
+        const int nt = task + NS - 1;
+        if (nt >= NS) mbar_wait(&empty[nt % NS], unsigned(nt / NS - 1) & 1u);
+        issue(nt);
+      }
+      mbar_wait(&full[s], unsigned(task / NS) & 1u);
+      const double* vjs = ring + 2 * ROW * s;
+      const double* vps = vjs + ROW;
+      const int i = 2 * t + ROW * r;
       if (i + 1 < len) {
-        if (vp) {
-          const double2 pv = ld2_hint(vp + i, drop);
+        if (j > 0) {
+          const double2 pv = *reinterpret_cast<const double2*>(vps + 2 * t);
           wi.x = wi.x - h * pv.x;
           wi.y = wi.y - h * pv.y;
         }
-        const double2 a = vj ? ld2_hint(vj + i, keep) : wi;
+        const double2 a = j <= k ? *reinterpret_cast<const double2*>(vjs + 2 * t) : wi;
         s0 += a.x * wi.x;
         s1 += a.y * wi.y;
       } else if (i < len) {
-        if (vp) wi.x = wi.x - h * vp[i];
-        const double a = vj ? vj[i] : wi.x;
+        if (j > 0) wi.x = wi.x - h * vps[2 * t];
+        const double a = j <= k ? vjs[2 * t] : wi.x;
         s0 += a * wi.x;
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+      ++task;
     };
 #pragma unroll
-    for (int r = 0; r < RR; ++r) pass(wr[r], 2 * t + 2 * kCoopThreads * r);
-#pragma unroll 4
-    for (int i = SPLIT + 2 * t; i < len; i += 2 * kCoopThreads) {
-      double2 wi = i + 1 < len ? *reinterpret_cast<const double2*>(wsm5 + i - SPLIT) : make_double2(wsm5[i - SPLIT], 0.0);
-      pass(wi, i);
-      if (vp) {
+    for (int r = 0; r < RW; ++r)
+      if (r < nrows) row(wr[r], r);
+    for (int r = RW; r < nrows; ++r) {
+      double* wp = wsm + ROW * (r - RW) + 2 * t;
+      const int i = 2 * t + ROW * r;
+      double2 wi = i + 1 < len ? *reinterpret_cast<const double2*>(wp) : make_double2(i < len ? wp[0] : 0.0, 0.0);
+      row(wi, r);
+      if (j > 0) {
         if (i + 1 < len)
-          *reinterpret_cast<double2*>(wsm5 + i - SPLIT) = wi;
-        else
-          wsm5[i - SPLIT] = wi.x;
+          *reinterpret_cast<double2*>(wp) = wi;
+        else if (i < len)
+          wp[0] = wi.x;
       }
     }
     const double tot = mgs_grid_sum(s0 + s1, partial + size_t(j) * nb, bar, shA, shB);
@@ -770,14 +668,14 @@ __global__ void __launch_bounds__(kCoopThreads) mgs_split_kernel(double* __restr
     if (blockIdx.x == 0 && t == 0) hc[j] = h;
   }
 #pragma unroll
-  for (int r = 0; r < RR; ++r) {
-    const int i = 2 * t + 2 * kCoopThreads * r;
+  for (int r = 0; r < RW; ++r) {
+    const int i = 2 * t + ROW * r;
     if (i + 1 < len)
       *reinterpret_cast<double2*>(wg + i) = h > 0.0 ? make_double2(wr[r].x / h, wr[r].y / h) : wr[r];
     else if (i < len)
       wg[i] = h > 0.0 ? wr[r].x / h : wr[r].x;
   }
-  for (int i = SPLIT + t; i < len; i += kCoopThreads) wg[i] = h > 0.0 ? wsm5[i - SPLIT] / h : wsm5[i - SPLIT];
+  for (int i = ROW * RW + t; i < len; i += NT) wg[i] = h > 0.0 ? wsm[i - ROW * RW] / h : wsm[i - ROW * RW];
   fused_givens(G, k, gstatus);
 }
 
@@ -785,65 +683,36 @@ struct CoopPlan {
   int grid;
   int64_t chunk;
   size_t smem;
-  int mode;
+  int mode;  // 1..4: mgs_regv_kernel<mode>; 5: mgs_bulk_kernel; 0: mgs_global_kernel
+  int threads = kCoopThreads;
 };
 
 // One 1024-thread CTA per SM (cheap barrier); the most shared-memory residency that fits.
-bool mgs_smem_slices() {  // TPDG_GPU_MGS=smem: the shared-memory staged basis slices (mgs_reg_kernel)
-  static const bool v = [] {
-    const char* f = std::getenv("TPDG_GPU_MGS");
-    return f && f[0] == 's';
-  }();
-  return v;
-}
+constexpr int kBulkThreads = 1024, kBulkRW = 8, kBulkStages = 2;
 
 CoopPlan mgs_coop_plan(int64_t n) {
   int dev = 0, sms = 0;
   TPDG_CUDA_CHECK(cudaGetDevice(&dev));
   TPDG_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  constexpr size_t kMax = 210 * 1024;
-  TPDG_CUDA_CHECK(cudaFuncSetAttribute(mgs_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kMax)));
-  TPDG_CUDA_CHECK(cudaFuncSetAttribute(mgs_coop_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kMax)));
-  TPDG_CUDA_CHECK(cudaFuncSetAttribute(mgs_coop_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kMax)));
   int64_t chunk = (n + sms - 1) / sms;
   chunk = (chunk + 1) & ~int64_t(1);
-  const size_t one = size_t(chunk) * sizeof(double);
-  int fit = 0;
-  if (chunk <= 4 * 2 * kCoopThreads && !mgs_smem_slices()) {  // w and v_j in registers (MODE 10 + R)
+  if (chunk <= 4 * 2 * kCoopThreads) {  // w and the basis slices in registers
     const int R = int((chunk + 2 * kCoopThreads - 1) / (2 * kCoopThreads));
-    return {sms, chunk, 0, 10 + R};
+    return {sms, chunk, 0, R};
   }
-  if (chunk <= 4 * 2 * kCoopThreads) {  // register-resident w (MODE 4 + R)
-    const int R = int((chunk + 2 * kCoopThreads - 1) / (2 * kCoopThreads));
-    const void* fns[4] = {reinterpret_cast<const void*>(mgs_reg_kernel<1>), reinterpret_cast<const void*>(mgs_reg_kernel<2>),
-                          reinterpret_cast<const void*>(mgs_reg_kernel<3>), reinterpret_cast<const void*>(mgs_reg_kernel<4>)};
-    TPDG_CUDA_CHECK(cudaFuncSetAttribute(fns[R - 1], cudaFuncAttributeMaxDynamicSharedMemorySize, int(2 * one)));
-    TPDG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, fns[R - 1], kCoopThreads, 2 * one));
-    if (fit >= 1) return {sms, chunk, 2 * one, 4 + R};
-  }
-  if (3 * one <= kMax) {
-    TPDG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, mgs_pipe_kernel, kCoopThreads, 3 * one));
-    if (fit >= 1) return {sms, chunk, 3 * one, 3};
-  }
-  if (2 * one <= kMax) {
-    TPDG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, mgs_coop_kernel<2>, kCoopThreads, 2 * one));
-    if (fit >= 1) return {sms, chunk, 2 * one, 2};
-  }
-  if (one <= kMax) {
-    TPDG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, mgs_coop_kernel<1>, kCoopThreads, one));
-    if (fit >= 1) return {sms, chunk, one, 1};
-  }
-  {  // MODE 9: w split registers (8 pairs per thread) + shared memory
-    constexpr int RR = 8;
-    const int64_t rest = chunk - 2 * kCoopThreads * RR;
-    if (rest > 0 && size_t(rest) * sizeof(double) <= kMax) {
-      const size_t sm = size_t(rest) * sizeof(double);
-      TPDG_CUDA_CHECK(cudaFuncSetAttribute(mgs_split_kernel<RR>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
-      TPDG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, mgs_split_kernel<RR>, kCoopThreads, sm));
-      if (fit >= 1) return {sms, chunk, sm, 9};
+  {  // w on chip (registers + shared memory), basis rows through the TMA ring
+    const int64_t rows = (chunk + 2 * kBulkThreads - 1) / (2 * kBulkThreads);
+    const size_t row_b = size_t(2 * kBulkThreads) * sizeof(double);
+    const size_t sm = row_b * (2 * kBulkStages + size_t(rows > kBulkRW ? rows - kBulkRW : 0));
+    const void* fn = reinterpret_cast<const void*>(mgs_bulk_kernel<kBulkThreads, kBulkRW, kBulkStages>);
+    int fit = 0;
+    if (sm <= 227 * 1024) {
+      TPDG_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+      TPDG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, fn, kBulkThreads, sm));
+      if (fit >= 1) return {sms, chunk, sm, 5, kBulkThreads};
     }
   }
-  return {sms, chunk, 0, 0};
+  return {sms, chunk, 0, 0};  // w in global memory
 }
 
 int stream_grid(int64_t n) {
@@ -907,20 +776,13 @@ void launch_mgs_iteration(double* V, int64_t ldv, int k, int64_t n, double* hc, 
   GmresDev g = G && G->m <= kFusedGivensMaxM ? *G : GmresDev{};
   GmresStatus* gs = G && G->m <= kFusedGivensMaxM ? status : nullptr;
   void* args[] = {&V, &ldv, &k, &n, &chunk, &hc, &partial, &bar, &skip, &g, &gs};
-  void* fn = plan.mode == 11  ? reinterpret_cast<void*>(mgs_regv_kernel<1>)
-             : plan.mode == 12 ? reinterpret_cast<void*>(mgs_regv_kernel<2>)
-             : plan.mode == 13 ? reinterpret_cast<void*>(mgs_regv_kernel<3>)
-             : plan.mode == 14 ? reinterpret_cast<void*>(mgs_regv_kernel<4>)
-             : plan.mode == 9  ? reinterpret_cast<void*>(mgs_split_kernel<8>)
-             : plan.mode == 5 ? reinterpret_cast<void*>(mgs_reg_kernel<1>)
-             : plan.mode == 6 ? reinterpret_cast<void*>(mgs_reg_kernel<2>)
-             : plan.mode == 7 ? reinterpret_cast<void*>(mgs_reg_kernel<3>)
-             : plan.mode == 8 ? reinterpret_cast<void*>(mgs_reg_kernel<4>)
-             : plan.mode == 3 ? reinterpret_cast<void*>(mgs_pipe_kernel)
-             : plan.mode == 2 ? reinterpret_cast<void*>(mgs_coop_kernel<2>)
-             : plan.mode == 1 ? reinterpret_cast<void*>(mgs_coop_kernel<1>)
-                              : reinterpret_cast<void*>(mgs_coop_kernel<0>);
-  TPDG_CUDA_CHECK(cudaLaunchCooperativeKernel(fn, dim3(plan.grid), dim3(kCoopThreads), args, plan.smem, st));
+  void* fn = plan.mode == 1   ? reinterpret_cast<void*>(mgs_regv_kernel<1>)
+             : plan.mode == 2 ? reinterpret_cast<void*>(mgs_regv_kernel<2>)
+             : plan.mode == 3 ? reinterpret_cast<void*>(mgs_regv_kernel<3>)
+             : plan.mode == 4 ? reinterpret_cast<void*>(mgs_regv_kernel<4>)
+             : plan.mode == 5 ? reinterpret_cast<void*>(mgs_bulk_kernel<kBulkThreads, kBulkRW, kBulkStages>)
+                              : reinterpret_cast<void*>(mgs_global_kernel);
+  TPDG_CUDA_CHECK(cudaLaunchCooperativeKernel(fn, dim3(plan.grid), dim3(plan.threads), args, plan.smem, st));
   ++g_launches;
 }
 

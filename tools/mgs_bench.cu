@@ -4,6 +4,8 @@
 //        -o /tmp/mgs_bench tools/mgs_bench.cu paper_1704_04549_b200/csrc/blas.cu
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
+#include <cmath>
 #include <vector>
 
 #include "tpdg_internal.hpp"
@@ -46,6 +48,57 @@ int main(int argc, char** argv) {
     cudaEventElapsedTime(&ms, a, b);
     if (rep == 2) printf("n=%lld K=%d: %.1f us per MGS launch (avg k+1 = %.1f), %.2f us per pass\n", (long long)n, K,
                          ms * 1e3 / K, (K + 1) / 2.0, ms * 1e3 / (K * ((K + 1) / 2.0 + 1)));
+  }
+  {  // host emulation of hc[0] of the last launch (<v_0, V[K]> in the kernels' fixed order)
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    int64_t chunk = (n + sms - 1) / sms;
+    chunk = (chunk + 1) & ~int64_t(1);
+    const double* v = h.data();
+    const double* w = h.data() + int64_t(K) * ldv;
+    std::vector<double> part(sms);
+    for (int b = 0; b < sms; ++b) {
+      const int64_t lo = b * chunk, hi = std::min<int64_t>(lo + chunk, n);
+      const int len = int(hi > lo ? hi - lo : 0);
+      double lanev[1024];
+      for (int t = 0; t < 1024; ++t) {
+        double s0 = 0.0, s1 = 0.0;
+        for (int i = 2 * t; i < len; i += 2048) {
+          if (i + 1 < len) {
+            s0 = fma(v[lo + i], w[lo + i], s0);
+            s1 = fma(v[lo + i + 1], w[lo + i + 1], s1);
+          } else {
+            s0 = fma(v[lo + i], w[lo + i], s0);
+          }
+        }
+        lanev[t] = s0 + s1;
+      }
+      double bs = 0.0;
+      for (int wi = 0; wi < 32; ++wi) {
+        double x[32];
+        for (int l = 0; l < 32; ++l) x[l] = lanev[32 * wi + l];
+        for (int o = 16; o > 0; o >>= 1) {
+          double y[32];
+          for (int l = 0; l < 32; ++l) y[l] = x[l] + x[l ^ o];
+          for (int l = 0; l < 32; ++l) x[l] = y[l];
+        }
+        bs += x[0];
+      }
+      part[b] = bs;
+    }
+    const int nw = (sms + 31) / 32;
+    double tot = 0.0;
+    for (int wi = 0; wi < nw; ++wi) {
+      double x[32];
+      for (int l = 0; l < 32; ++l) x[l] = 32 * wi + l < sms ? part[32 * wi + l] : 0.0;
+      for (int o = 16; o > 0; o >>= 1) {
+        double y[32];
+        for (int l = 0; l < 32; ++l) y[l] = x[l] + x[l ^ o];
+        for (int l = 0; l < 32; ++l) x[l] = y[l];
+      }
+      tot += x[0];
+    }
+    printf("host emulation h0 %.17g\n", tot);
   }
   std::vector<double> hh(64);
   cudaMemcpy(hh.data(), hc, sizeof(double) * 64, cudaMemcpyDeviceToHost);
