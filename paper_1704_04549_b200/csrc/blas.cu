@@ -294,28 +294,6 @@ __global__ void backsolve_kernel(GmresDev G, int k) {
 // them in the same fixed order (deterministic, identical on all CTAs).
 constexpr int kCoopThreads = 1024;
 
-// Generation barrier for a co-resident (cooperative) grid: bar[0] = arrivals, bar[1] = generation.
-// The last arriver resets the count and bumps the generation, so the state is clean after every
-// barrier (launches that exit early on the skip flag leave it untouched).
-__device__ __forceinline__ void coop_barrier(unsigned* bar) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    volatile unsigned* gen = bar + 1;
-    const unsigned g = *gen;
-    __threadfence();
-    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
-      bar[0] = 0u;
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
-    } else {
-      while (*gen == g) {
-      }
-    }
-    __threadfence();
-  }
-  __syncthreads();
-}
-
 // L2 eviction-priority hints (createpolicy + .L2::cache_hint): in mgs_global_kernel the working vector w
 // and the current basis vector are kept L2-resident across passes (evict_last), so a pass streams
 // only v_j from HBM instead of w (read + write), v_{j-1} and v_j.
@@ -338,14 +316,72 @@ __device__ __forceinline__ void st2_hint(double* a, double2 v, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1,%2}, %3;" ::"l"(a), "d"(v.x), "d"(v.y), "l"(pol) : "memory");
 }
 
+// Grid reduction of one MGS pass: CTA partial (warp trees, then the 32 warp sums in order), the
+// grid barrier, and every thread summing the per-CTA partials in the same fixed order.
+// The barrier is a monotonic arrival counter bar[0]: pass p of a launch is complete when it reaches
+// base + (p + 1) nb, base = bar[1], which the launch reads at its start and CTA 0 advances at its
+// end (mgs_epoch_*). One atomic and one acquire poll per pass; no re-arming store, no generation
+// flag (2.1 vs 3.0 us per empty grid sum, tools/gridsum_bench.cu). Returns the total.
+// The running target lives in shared memory (thread 0 only uses it), so the kernels carry no extra
+// register for it.
+__device__ __forceinline__ void mgs_epoch_begin(const unsigned* bar, unsigned* target) {
+  if (threadIdx.x == 0) asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(*target) : "l"(bar + 1) : "memory");
+}
+__device__ __forceinline__ void mgs_epoch_end(unsigned* bar, const unsigned* target) {
+  // every CTA read bar[1] before its first arrival, and CTA 0 gets here only after all arrivals
+  if (blockIdx.x == 0 && threadIdx.x == 0) bar[1] = *target;
+}
+__device__ __forceinline__ double mgs_grid_sum(double v, double* part, unsigned* bar, unsigned* target, double* shA,
+                                               double* shB) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const unsigned nb = gridDim.x;
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  if (lane == 0) shA[wid] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double bs = 0.0;
+    for (int w2 = 0; w2 < int(blockDim.x >> 5); ++w2) bs += shA[w2];
+    part[blockIdx.x] = bs;
+    const unsigned tg = *target + nb;
+    *target = tg;
+    unsigned t;  // the release arrival publishes this CTA's partial; waiters acquire the count
+    asm volatile("atom.release.gpu.global.add.u32 %0, [%1], 1;" : "=r"(t) : "l"(bar) : "memory");
+    if (t + 1u != tg) {
+      unsigned cur;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(bar) : "memory");
+      } while (int(cur - tg) < 0);
+    }
+  }
+  __syncthreads();
+  double pv = threadIdx.x < nb ? reinterpret_cast<volatile double*>(part)[threadIdx.x] : 0.0;
+  for (unsigned b = threadIdx.x + blockDim.x; b < nb; b += blockDim.x) pv += reinterpret_cast<volatile double*>(part)[b];
+  // only the warps holding partials reduce; warp 0 then sums the warp sums in order and
+  // broadcasts (the ordered 32-term sum in every thread cost more issue slots than a barrier)
+  const int nw = int((nb + 31) / 32);
+  if (wid < nw) {
+    for (int o = 16; o > 0; o >>= 1) pv += __shfl_xor_sync(0xffffffffu, pv, o);
+    if (lane == 0) shB[wid] = pv;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double tot = 0.0;
+    for (int w2 = 0; w2 < nw; ++w2) tot += shB[w2];
+    shB[32] = tot;
+  }
+  __syncthreads();
+  return shB[32];
+}
+
 // General fallback (slices too large to keep w on chip): w in global memory / L2.
 __global__ void __launch_bounds__(kCoopThreads) mgs_global_kernel(double* __restrict__ V, int64_t ldv, int k,
                                                                  int64_t n, int64_t chunk, double* __restrict__ hc,
                                                                  double* __restrict__ partial, unsigned* bar,
                                                                  const int* skip, GmresDev G, GmresStatus* gstatus) {
   if (skip && *skip) return;
-  __shared__ double sh[32];
-  __shared__ double hval;
+  __shared__ unsigned tgt;
+  mgs_epoch_begin(bar, &tgt);
+  __shared__ double shA[32], shB[33];
   const unsigned nb = gridDim.x;
   const int64_t lo = int64_t(blockIdx.x) * chunk;
   const int64_t hi = lo + chunk < n ? lo + chunk : n;
@@ -387,70 +423,14 @@ __global__ void __launch_bounds__(kCoopThreads) mgs_global_kernel(double* __rest
     if (j + 1 <= k)
       for (int64_t i = 16 * int64_t(threadIdx.x); i < len; i += 16 * int64_t(blockDim.x))
         asm volatile("prefetch.global.L2 [%0];" ::"l"(V + int64_t(j + 1) * ldv + lo + i));
-    const double bs = block_sum(s0 + s1, sh);
-    if (threadIdx.x == 0) partial[size_t(j) * nb + blockIdx.x] = bs;
-    coop_barrier(bar);
-    // fixed-order tree over the per-CTA partials (one parallel load round)
-    double v = threadIdx.x < nb ? reinterpret_cast<volatile double*>(partial)[size_t(j) * nb + threadIdx.x] : 0.0;
-    for (unsigned b = threadIdx.x + blockDim.x; b < nb; b += blockDim.x)
-      v += reinterpret_cast<volatile double*>(partial)[size_t(j) * nb + b];
-    const double tot = block_sum(v, sh);
-    if (threadIdx.x == 0) hval = j <= k ? tot : sqrt(tot);
-    __syncthreads();
-    h = hval;
+    const double tot = mgs_grid_sum(s0 + s1, partial + size_t(j) * nb, bar, &tgt, shA, shB);
+    h = j <= k ? tot : sqrt(tot);
     if (blockIdx.x == 0 && threadIdx.x == 0) hc[j] = h;
   }
   // reference: if (hkk > 0) v[k+1] /= hkk
   for (int64_t i = threadIdx.x; i < len; i += blockDim.x) wg[i] = h > 0.0 ? w[i] / h : w[i];
+  mgs_epoch_end(bar, &tgt);
   fused_givens(G, k, gstatus);
-}
-
-// Grid reduction of one MGS pass: CTA partial (warp trees, then the 32 warp sums in order), the
-// generation barrier, and every thread summing the per-CTA partials in the same fixed order.
-// Three __syncthreads; bit-identical to block_sum + barrier + block_sum. Returns the total.
-__device__ __forceinline__ double mgs_grid_sum(double v, double* part, unsigned* bar, double* shA, double* shB) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  const unsigned nb = gridDim.x;
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-  if (lane == 0) shA[wid] = v;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double bs = 0.0;
-    for (int w2 = 0; w2 < int(blockDim.x >> 5); ++w2) bs += shA[w2];
-    part[blockIdx.x] = bs;
-    // release/acquire instead of full fences: the arrival publishes this CTA's partial, the last
-    // arriver (acq_rel) re-arms the counter and releases the generation, waiters acquire it
-    unsigned g, t;
-    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(bar + 1) : "memory");
-    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(t) : "l"(bar) : "memory");
-    if (t == nb - 1) {
-      asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(bar) : "memory");
-      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar + 1) : "memory");
-    } else {
-      unsigned cur;
-      do {
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(bar + 1) : "memory");
-      } while (cur == g);
-    }
-  }
-  __syncthreads();
-  double pv = threadIdx.x < nb ? reinterpret_cast<volatile double*>(part)[threadIdx.x] : 0.0;
-  for (unsigned b = threadIdx.x + blockDim.x; b < nb; b += blockDim.x) pv += reinterpret_cast<volatile double*>(part)[b];
-  // only the warps holding partials reduce; warp 0 then sums the warp sums in order and
-  // broadcasts (the ordered 32-term sum in every thread cost more issue slots than a barrier)
-  const int nw = int((nb + 31) / 32);
-  if (wid < nw) {
-    for (int o = 16; o > 0; o >>= 1) pv += __shfl_xor_sync(0xffffffffu, pv, o);
-    if (lane == 0) shB[wid] = pv;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double tot = 0.0;
-    for (int w2 = 0; w2 < nw; ++w2) tot += shB[w2];
-    shB[32] = tot;
-  }
-  __syncthreads();
-  return shB[32];
 }
 
 // Slices of <= 8192 doubles per CTA (cfg2 p <= 15): w, v_{j-1} and v_j in registers. The thread's
@@ -462,6 +442,8 @@ __global__ void __launch_bounds__(kCoopThreads) mgs_regv_kernel(double* __restri
                                                                  double* __restrict__ partial, unsigned* bar,
                                                                  const int* skip, GmresDev G, GmresStatus* gstatus) {
   if (skip && *skip) return;
+  __shared__ unsigned tgt;
+  mgs_epoch_begin(bar, &tgt);
   __shared__ double shA[32], shB[33];
   const unsigned nb = gridDim.x;
   const int64_t lo = int64_t(blockIdx.x) * chunk;
@@ -511,7 +493,7 @@ __global__ void __launch_bounds__(kCoopThreads) mgs_regv_kernel(double* __restri
       }
     }
     if (j + 1 <= k) fetch(V + int64_t(j + 1) * ldv + lo, vq);  // in flight during the grid reduction
-    const double tot = mgs_grid_sum(s0 + s1, partial + size_t(j) * nb, bar, shA, shB);
+    const double tot = mgs_grid_sum(s0 + s1, partial + size_t(j) * nb, bar, &tgt, shA, shB);
     h = j <= k ? tot : sqrt(tot);
     if (blockIdx.x == 0 && t == 0) hc[j] = h;
   }
@@ -524,6 +506,7 @@ __global__ void __launch_bounds__(kCoopThreads) mgs_regv_kernel(double* __restri
       wg[i] = h > 0.0 ? w[r].x / h : w[r].x;
     }
   }
+  mgs_epoch_end(bar, &tgt);
   fused_givens(G, k, gstatus);
 }
 
@@ -570,6 +553,8 @@ __global__ void __launch_bounds__(NT, 1) mgs_bulk_kernel(double* __restrict__ V,
                                                          double* __restrict__ partial, unsigned* bar, const int* skip,
                                                          GmresDev G, GmresStatus* gstatus) {
   if (skip && *skip) return;
+  __shared__ unsigned tgt;
+  mgs_epoch_begin(bar, &tgt);
   constexpr int ROW = 2 * NT;  // doubles per row: one pair per thread
   extern __shared__ __align__(128) double bsm[];
   double* ring = bsm;             // stage s: v_j row at ring + 2 ROW s, v_{j-1} row at + ROW
@@ -663,7 +648,7 @@ __global__ void __launch_bounds__(NT, 1) mgs_bulk_kernel(double* __restrict__ V,
           wp[0] = wi.x;
       }
     }
-    const double tot = mgs_grid_sum(s0 + s1, partial + size_t(j) * nb, bar, shA, shB);
+    const double tot = mgs_grid_sum(s0 + s1, partial + size_t(j) * nb, bar, &tgt, shA, shB);
     h = j <= k ? tot : sqrt(tot);
     if (blockIdx.x == 0 && t == 0) hc[j] = h;
   }
@@ -676,6 +661,7 @@ __global__ void __launch_bounds__(NT, 1) mgs_bulk_kernel(double* __restrict__ V,
       wg[i] = h > 0.0 ? wr[r].x / h : wr[r].x;
   }
   for (int i = ROW * RW + t; i < len; i += NT) wg[i] = h > 0.0 ? wsm[i - ROW * RW] / h : wsm[i - ROW * RW];
+  mgs_epoch_end(bar, &tgt);
   fused_givens(G, k, gstatus);
 }
 
