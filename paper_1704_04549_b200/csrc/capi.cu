@@ -170,7 +170,7 @@ struct tpdg_gpu_pc_s {
   tpdg_gpu_op op = nullptr;
   DevPC pc{};
   int nblk = 0, raw_len = 0;
-  DevBuf raw, rec, piv, kind, fb_slot, fb_list, fb_lu, fb_piv, status, cells, cinv;
+  DevBuf raw, rec, piv, kind, fb_slot, fb_list, fb_lu, fb_piv, status, cells, cinv, irec;
   std::vector<int> kind_h;
   std::vector<int64_t> fallbacks;  // (element, component)
 };
@@ -605,13 +605,18 @@ void finish_pc(tpdg_gpu_pc pc) {
   TPDG_CUDA_CHECK(cudaMemsetAsync(pc->cells.p, 0, pc->cells.bytes, st));
   d.cells = pc->cells.as<double>();
   d.cinv = nullptr;
-  if (!d.faithful) {
-    const int t1 = op->dim == 2 ? d.n1 : op->q;
-    pc->cinv.alloc(sizeof(double) * size_t(pc->nblk) * 4 * t1 * op->q);
+  d.irec = nullptr;
+  if (!d.faithful && op->dim == 2) {  // rows of the inverted Sylvester cell systems (kron2d_mma_kernel)
+    pc->cinv.alloc(sizeof(double) * size_t(pc->nblk) * 4 * d.n1 * op->q);
     TPDG_CUDA_CHECK(cudaMemsetAsync(pc->cinv.p, 0, pc->cinv.bytes, st));
     d.cinv = pc->cinv.as<double>();
   }
-  launch_sylv_cells(d, pc->cells.as<double>(), pc->cinv.as<double>(), st);
+  launch_sylv_cells(d, pc->cells.as<double>(), d.cinv ? pc->cinv.as<double>() : nullptr, st);
+  if (!d.faithful && op->dim == 3 && op->q <= 16 && d.n1 <= 64) {  // tensor-core 3D apply operands
+    pc->irec.alloc(sizeof(double) * size_t(pc->nblk) * irec3_doubles(d.n1, op->q));
+    d.irec = pc->irec.as<double>();
+    launch_kron3d_inv_prep(d, pc->irec.as<double>(), st);
+  }
   TPDG_CUDA_CHECK(cudaStreamSynchronize(st));
 }
 

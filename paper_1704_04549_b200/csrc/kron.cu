@@ -1232,131 +1232,368 @@ __global__ void __launch_bounds__(k3Threads) kron3d_sized_kernel(DevPC pc, const
 }
 
 // ------------------------------------------------------------------------------------ 3D, DMMA
-// apply_factors_3d (precond/ksvd.hpp:132-153) on the tensor cores, one 128-thread CTA per block.
-// The element lives in shared memory as Xr[r][(s, j)] (B2 index r outermost, then the outer slice
-// s and the C1 index j), so that the rotations of all N1 slices are four single DMMA products:
-//   P = Q1^T Xr (Q x N1 Q),  M = P_rows Q2 ((N1 Q) x Q),  Z = Q1 Y,  out = Z_rows Q2^T,
-// with each product's C fragments stored straight into the layout the next one reads. The three
-// LU axis solves are register fibers over Xr (FMA) and the slices share one Sylvester wavefront
-// (inverse rows of the cell systems). Parity as the 2D tensor-core apply (<= 1e-12 gate).
+// apply_factors_3d (precond/ksvd.hpp:132-153) as dense products on the FP64 tensor cores. The
+// formation-time prep (kron3d_inv_prep_kernel) turns each block's record into
+//   A1^-1, L^T = B2^-T Q1, R = C1^-T Q2, Q1, Q2, T2 and G_b = (I (x) T1 + T2_bb (x) I)^-1 for every
+//   quasi-diagonal block b of T2 (1x1 or 2x2),
+// so that the three LU axis solves fold into the rotations: M_s = L (A1^-1 x)_s R. The Sylvester
+// solve T1 Y_s + Y_s T2^T = M_s runs over T2's blocks right to left; thread (s, i) owns row i of
+// slice s, forms its right-hand side from its own solved row and T2, and G_b mixes the rows of the
+// slice, which all sit in the thread's warp (SPW = 32 / Q slices per warp): one __syncwarp per block,
+// no CTA barrier. The apply is then five DMMA products plus that column sweep. Not bit-faithful
+// (explicit inverses; ~1e-13 from the reference at cfg4, tools/study/kron3d_inv_emul.py; gate 1e-12).
+
+// Dense inverse by Gauss-Jordan with partial pivoting (n <= 2 * 16), a in local memory.
+__device__ void gj_inverse(double* a, double* inv, int n) {
+  for (int i = 0; i < n * n; ++i) inv[i] = (i / n == i % n) ? 1.0 : 0.0;
+  for (int c = 0; c < n; ++c) {
+    int pr = c;
+    for (int r = c + 1; r < n; ++r)
+      if (fabs(a[r * n + c]) > fabs(a[pr * n + c])) pr = r;
+    if (pr != c)
+      for (int j = 0; j < n; ++j) {
+        double t = a[c * n + j]; a[c * n + j] = a[pr * n + j]; a[pr * n + j] = t;
+        t = inv[c * n + j]; inv[c * n + j] = inv[pr * n + j]; inv[pr * n + j] = t;
+      }
+    const double d = 1.0 / a[c * n + c];
+    for (int j = 0; j < n; ++j) {
+      a[c * n + j] *= d;
+      inv[c * n + j] *= d;
+    }
+    for (int r = 0; r < n; ++r) {
+      if (r == c) continue;
+      const double f = a[r * n + c];
+      if (f == 0.0) continue;
+      for (int j = 0; j < n; ++j) {
+        a[r * n + j] = fma(-f, a[c * n + j], a[r * n + j]);
+        inv[r * n + j] = fma(-f, inv[c * n + j], inv[r * n + j]);
+      }
+    }
+  }
+}
+
+// Column c of A^-1 from the packed LU (unit lower L, U, perm) of a record.
+__device__ void lu_inverse_col(const double* lu, const int* perm, int n, int c, double* x) {
+  for (int k = 0; k < n; ++k) x[k] = perm[k] == c ? 1.0 : 0.0;
+  for (int r = 1; r < n; ++r) {
+    double s = x[r];
+    for (int j = 0; j < r; ++j) s = fma(-lu[r * n + j], x[j], s);
+    x[r] = s;
+  }
+  for (int r = n - 1; r >= 0; --r) {
+    double s = x[r];
+    for (int j = r + 1; j < n; ++j) s = fma(-lu[r * n + j], x[j], s);
+    x[r] = s / lu[r * n + r];
+  }
+}
+
+// One thread per block: irec = A1^-1 | L^T | R | Q1 | Q2 | T2 | G blocks (block b: sz q rows of stride
+// g_row_stride, each of sz segments of q values padded to rs = even(q): 16-byte aligned segments, and
+// rows 2 (mod 4) doubles apart so that eight lanes reading eight rows hit eight bank groups).
+__global__ void kron3d_inv_prep_kernel(DevPC pc, double* __restrict__ irec) {
+  const int blk = blockIdx.x * blockDim.x + threadIdx.x;
+  if (blk >= pc.nblk || pc.kind[blk] == 0) return;
+  const int n1 = pc.n1, q = pc.q;
+  const double* r = pc.rec + size_t(blk) * pc.rec_len;  // LU(A1) | LU(B2) | LU(C1) | Q1 | T1 | Q2 | T2
+  const int* piv = pc.piv + size_t(blk) * pc.piv_len;
+  const double *luA1 = r, *luB2 = luA1 + n1 * n1, *luC1 = luB2 + q * q, *Q1 = luC1 + q * q, *T1 = Q1 + q * q,
+               *Q2 = T1 + q * q, *T2 = Q2 + q * q;
+  double* o = irec + size_t(blk) * irec3_doubles(n1, q);
+  double *oA = o, *oLt = oA + n1 * n1, *oR = oLt + q * q, *oQ1 = oR + q * q, *oQ2 = oQ1 + q * q, *oT2 = oQ2 + q * q,
+         *oG = oT2 + q * q;
+  double col[64], binv[16 * 16], cinv[16 * 16];
+  for (int c = 0; c < n1; ++c) {
+    lu_inverse_col(luA1, piv, n1, c, col);
+    for (int k = 0; k < n1; ++k) oA[k * n1 + c] = col[k];
+  }
+  for (int c = 0; c < q; ++c) {
+    lu_inverse_col(luB2, piv + n1, q, c, col);
+    for (int k = 0; k < q; ++k) binv[k * q + c] = col[k];
+    lu_inverse_col(luC1, piv + n1 + q, q, c, col);
+    for (int k = 0; k < q; ++k) cinv[k * q + c] = col[k];
+  }
+  for (int i = 0; i < q; ++i)
+    for (int j = 0; j < q; ++j) {
+      double lt = 0.0, rr = 0.0;
+      for (int k = 0; k < q; ++k) {
+        lt = fma(binv[k * q + i], Q1[k * q + j], lt);  // (B2^-T Q1)[i][j]
+        rr = fma(cinv[k * q + i], Q2[k * q + j], rr);  // (C1^-T Q2)[i][j]
+      }
+      oLt[i * q + j] = lt;
+      oR[i * q + j] = rr;
+      oQ1[i * q + j] = Q1[i * q + j];
+      oQ2[i * q + j] = Q2[i * q + j];
+      oT2[i * q + j] = T2[i * q + j];
+    }
+  double K[32 * 32], G[32 * 32];
+  int off = 0;
+  for (int k0 = 0; k0 < q;) {
+    const int sz = (k0 + 1 < q && T2[(k0 + 1) * q + k0] != 0.0) ? 2 : 1;
+    const int m = sz * q;  // vec(Y_b) column-major: index c q + i
+    for (int a = 0; a < m; ++a)
+      for (int b = 0; b < m; ++b) {
+        const int ca = a / q, ia = a % q, cb = b / q, ib = b % q;
+        K[a * m + b] = (ca == cb ? T1[ia * q + ib] : 0.0) + (ia == ib ? T2[(k0 + ca) * q + k0 + cb] : 0.0);
+      }
+    gj_inverse(K, G, m);
+    const int rs = (q + 1) & ~1, gs = g_row_stride(q, sz);  // row: sz segments of q values, each padded to rs
+    for (int a = 0; a < m; ++a)
+      for (int j = 0; j < gs; ++j) {
+        const int c = j / rs, jj = j - c * rs;
+        oG[off + a * gs + j] = (c < sz && jj < q) ? G[a * m + c * q + jj] : 0.0;
+      }
+    off += m * gs;
+    k0 += sz;
+  }
+}
+
 template <int N1, int Q>
-struct Kron3dMmaLayout {
+struct Kron3dInvLayout {
+  static constexpr int SPW = 32 / Q, NW = (N1 + SPW - 1) / SPW, NTH = 32 * NW;  // slices per warp, warps
+  static constexpr int N1P = p8(N1), K1 = p4(N1), QQ = Q * Q, QQP = p8(QQ);
   static constexpr int QP = p8(Q), KQ = p4(Q), NC = N1 * Q, NCP = p8(NC);
-  static constexpr int LDR = lda4(NCP), LDP = lda4(KQ), LQ = lda4(QP);
-  static constexpr int o_x = 0;                          // Xr: KQ x LDR
-  static constexpr int o_p = o_x + KQ * LDR;             // P / Z rows: NCP x LDP
-  static constexpr int o_q1 = o_p + NCP * LDP;           // Q1: QP x LQ (zero padded)
-  static constexpr int o_q2 = o_q1 + QP * LQ;            // Q2: QP x LQ
-  static constexpr int o_lu = o_q2 + QP * LQ;            // LU(A1) N1^2 | LU(B2) | LU(C1) | T1 | T2 (Q^2 each)
-  static constexpr int o_rcp = (o_lu + N1 * N1 + 4 * Q * Q + 1) & ~1;
-  static constexpr int hdr = (((4 + 4 * Q) / 2 + 2) & ~1);
-  static constexpr int o_h = (o_rcp + N1 + 2 * Q + 1) & ~1;
-  static constexpr int o_piv = o_h + hdr;
-  static constexpr int total = (o_piv + (N1 + 2 * Q + 1) / 2 + 1) & ~1;
-  static constexpr int NT = NCP / 8, NTW = (NT + 3) / 4;  // column tiles, per warp
+  static constexpr int LDS0 = lda4(QQP), LDA = lda4(K1), LDR = lda4(NCP), LDP = lda4(KQ), LQ = lda4(QP);
+  static constexpr int RS = (Q + 1) & ~1;  // padded row segment (G rows, rhs slices): 16-byte aligned
+  static constexpr int GS1 = g_row_stride(Q, 1), GS2 = g_row_stride(Q, 2);
+  static constexpr int GMAX = QQ * GS2, S0 = K1 * LDS0 > GMAX ? K1 * LDS0 : GMAX;
+  static constexpr int o_s0 = 0;                       // x staged as [s][(r, j)]: K1 x LDS0; later the G blocks
+  static constexpr int o_x = o_s0 + S0;                // Xr[r][(s, j)]: KQ x LDR
+  static constexpr int o_p = o_x + KQ * LDR;           // P / Z rows: NCP x LDP
+  static constexpr int o_a = o_p + NCP * LDP;          // A1^-1: N1P x LDA
+  static constexpr int o_lt = o_a + N1P * LDA;         // L^T, R, Q1, Q2: QP x LQ each
+  static constexpr int o_r = o_lt + QP * LQ;
+  static constexpr int o_q1 = o_r + QP * LQ;
+  static constexpr int o_q2 = o_q1 + QP * LQ;
+  static constexpr int o_t2 = o_q2 + QP * LQ;          // T2 masked to the columns right of each row's block
+  static constexpr int o_rhs = (o_t2 + QQ + 1) & ~1;   // per warp: 2 parities x 2 columns x SPW slices x RS
+  static constexpr int o_lut = o_rhs + NW * 4 * SPW * RS;  // int LUTs: Xr offset of (r, j) = n; P offset of (s, r')
+  static constexpr int total = o_lut + (QQP + NCP + 1) / 2 + 1;
 };
 
 template <int N1, int Q>
-__global__ void __launch_bounds__(k3Threads) kron3d_mma_kernel(DevPC pc, const double* __restrict__ in,
-                                                                double* __restrict__ out) {
+__global__ void __launch_bounds__(Kron3dInvLayout<N1, Q>::NTH) kron3d_inv_kernel(DevPC pc,
+                                                                                  const double* __restrict__ in,
+                                                                                  double* __restrict__ out) {
   const int blk = blockIdx.x;
   if (pc.kind[blk] == 0 || (pc.skip && *pc.skip)) return;
-  using L = Kron3dMmaLayout<N1, Q>;
-  constexpr int QP = L::QP, KQ = L::KQ, NC = L::NC, LDR = L::LDR, LDP = L::LDP, LQ = L::LQ, NTW = L::NTW,
-                NT = L::NT, hdr = L::hdr;
+  using L = Kron3dInvLayout<N1, Q>;
+  constexpr int NW = L::NW, NTH = L::NTH, SPW = L::SPW, QQ = L::QQ, QP = L::QP, KQ = L::KQ, NC = L::NC,
+                LDS0 = L::LDS0, LDA = L::LDA, LDR = L::LDR, LDP = L::LDP, LQ = L::LQ, K1 = L::K1;
   extern __shared__ double sm[];
+  double* S0 = sm + L::o_s0;
   double* Xr = sm + L::o_x;
   double* Pr = sm + L::o_p;
+  double* sA = sm + L::o_a;
+  double* sLt = sm + L::o_lt;
+  double* sR = sm + L::o_r;
   double* sQ1 = sm + L::o_q1;
   double* sQ2 = sm + L::o_q2;
-  double* sLU = sm + L::o_lu;
-  double* sRcp = sm + L::o_rcp;
-  double* sH = sm + L::o_h;
-  int* sPiv = reinterpret_cast<int*>(sm + L::o_piv);
+  double* sT2 = sm + L::o_t2;
+  int* lutX = reinterpret_cast<int*>(sm + L::o_lut);  // n = r Q + j -> r LDR + j
+  int* lutP = lutX + L::QQP;                          // n = s Q + j -> s Q LDP + j
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  for (int i = tid; i < L::o_lu; i += k3Threads) sm[i] = 0.0;  // pads of Xr, P/Z, Q1, Q2
-  __syncthreads();
+  __shared__ int bplan[34];  // T2 quasi-blocks: starts [0, 16), sizes [16, 32), total G length, count
+  const double* ir = pc.irec + size_t(blk) * int(irec3_doubles(N1, Q));
+  const double* gG = ir + N1 * N1 + 5 * QQ;
   {
-    const double* r = pc.rec + size_t(blk) * (N1 * N1 + 6 * Q * Q);
-    // record: LU(A1) | LU(B2) | LU(C1) | Q1 | T1 | Q2 | T2
-    for (int i = tid; i < N1 * N1 + 2 * Q * Q; i += k3Threads) cp_async8(sLU + i, r + i);
-    for (int i = tid; i < Q * Q; i += k3Threads) {
-      cp_async8(sQ1 + (i / Q) * LQ + i % Q, r + N1 * N1 + 2 * Q * Q + i);
-      cp_async8(sLU + N1 * N1 + 2 * Q * Q + i, r + N1 * N1 + 3 * Q * Q + i);  // T1
-      cp_async8(sQ2 + (i / Q) * LQ + i % Q, r + N1 * N1 + 4 * Q * Q + i);
-      cp_async8(sLU + N1 * N1 + 3 * Q * Q + i, r + N1 * N1 + 5 * Q * Q + i);  // T2
+    for (int i = tid; i < N1 * N1; i += NTH) cp_async8(sA + (i / N1) * LDA + i % N1, ir + i);
+    for (int i = tid; i < QQ; i += NTH) {
+      const int rr = i / Q, cc = i % Q;
+      cp_async8(sLt + rr * LQ + cc, ir + N1 * N1 + i);
+      cp_async8(sR + rr * LQ + cc, ir + N1 * N1 + QQ + i);
+      cp_async8(sQ1 + rr * LQ + cc, ir + N1 * N1 + 2 * QQ + i);
+      cp_async8(sQ2 + rr * LQ + cc, ir + N1 * N1 + 3 * QQ + i);
+      cp_async8(sT2 + i, ir + N1 * N1 + 4 * QQ + i);
     }
-    const double* cells = pc.cells + size_t(blk) * pc.cells_len;
-    for (int i = tid; i < hdr; i += k3Threads) cp_async8(sH + i, cells + i);
-    for (int i = tid; i < N1 + 2 * Q; i += k3Threads) cp_async4(sPiv + i, pc.piv + size_t(blk) * (N1 + 2 * Q) + i);
-    const double* x = in + size_t(blk) * (N1 * Q * Q);
-    for (int i = tid; i < N1 * Q * Q; i += k3Threads) {  // x[s][r][j] -> Xr[r][s Q + j]
-      const int j = i % Q, rr = (i / Q) % Q, s = i / (Q * Q);
-      cp_async8(Xr + rr * LDR + s * Q + j, x + i);
-    }
+    const double* x = in + size_t(blk) * (N1 * QQ);
+    for (int sl = 0; sl < N1; ++sl)
+      for (int n = tid; n < QQ; n += NTH) cp_async8(S0 + sl * LDS0 + n, x + sl * QQ + n);
+    // K-padding of every product operand must be zero (M / N padding only feeds discarded outputs)
+    for (int c = tid; c < LDS0; c += NTH)
+      for (int r = N1; r < K1; ++r) S0[r * LDS0 + c] = 0.0;
+    for (int r = tid; r < L::N1P; r += NTH)
+      for (int c = N1; c < K1; ++c) sA[r * LDA + c] = 0.0;
+    for (int c = tid; c < LDR; c += NTH)
+      for (int r = Q; r < KQ; ++r) Xr[r * LDR + c] = 0.0;
+    for (int r = tid; r < L::NCP; r += NTH)
+      for (int c = Q; c < KQ; ++c) Pr[r * LDP + c] = 0.0;
+    for (int c = tid; c < LQ; c += NTH)
+      for (int r = Q; r < KQ; ++r) sLt[r * LQ + c] = sR[r * LQ + c] = 0.0;
+    for (int r = tid; r < QP; r += NTH)
+      for (int c = Q; c < KQ; ++c) sQ1[r * LQ + c] = sQ2[r * LQ + c] = 0.0;
+    for (int n = tid; n < L::QQP; n += NTH) lutX[n] = (n / Q) * LDR + n % Q;
+    for (int n = tid; n < L::NCP; n += NTH) lutP[n] = (n / Q) * Q * LDP + n % Q;
     cp_async_wait_all();
   }
   __syncthreads();
-  const double* luA1 = sLU;
-  const double* luB2 = luA1 + N1 * N1;
-  const double* luC1 = luB2 + Q * Q;
-  const double* T1 = luC1 + Q * Q;
-  const double* T2 = T1 + Q * Q;
-  for (int i = tid; i < N1 + 2 * Q; i += k3Threads)
-    sRcp[i] = 1.0 / (i < N1 ? luA1[i * N1 + i] : i < N1 + Q ? luB2[(i - N1) * (Q + 1)] : luC1[(i - N1 - Q) * (Q + 1)]);
-  __syncthreads();
-  for (int f = tid; f < Q * Q; f += k3Threads) lu_fiber_fma<N1>(luA1, sRcp, sPiv, Xr + (f / Q) * LDR + f % Q, Q);
-  __syncthreads();
-  for (int f = tid; f < NC; f += k3Threads)
-    lu_fiber_fma<Q>(luB2, sRcp + N1, sPiv + N1, Xr + (f / Q) * Q + f % Q, LDR);
-  __syncthreads();
-  for (int f = tid; f < NC; f += k3Threads)
-    lu_fiber_fma<Q>(luC1, sRcp + N1 + Q, sPiv + N1 + Q, Xr + (f % Q) * LDR + (f / Q) * Q, 1);
-  __syncthreads();
+  if (tid == 0) {  // per column k: kind (0 single, 1 second column of a 2x2 block, 2 its first) and G offset
+    int goff = 0;
+    for (int k0 = 0; k0 < Q;) {
+      const int sz = (k0 + 1 < Q && sT2[(k0 + 1) * Q + k0] != 0.0) ? 2 : 1;
+      bplan[k0] = sz == 1 ? 0 : 2;
+      if (sz == 2) bplan[k0 + 1] = 1;
+      bplan[16 + k0 + sz - 1] = goff;
+      goff += sz * Q * (sz == 1 ? L::GS1 : L::GS2);
+      k0 += sz;
+    }
+    bplan[32] = goff;
+  }
   const int fr = lane >> 2, fc = 2 * (lane & 3);
-  {  // P = Q1^T Xr -> P rows (s Q + r', j)
+  {  // X = A1^-1 x along the outer axis: (N1 x N1)(N1 x Q^2) -> Xr[r][s Q + j]
+    constexpr int NT0 = L::QQP / 8, NTW0 = (NT0 + NW - 1) / NW;
+    double acc[L::N1P / 8][NTW0][2];
+    zero_tiles(acc);
+    const int nt0 = warp * NTW0;
+    if (nt0 < NT0) {
+      mma_tiles<L::N1P / 8, NTW0, L::K1 / 4, false>(acc, sA, LDA, S0 + 8 * nt0, LDS0, lane);
+#pragma unroll
+      for (int nt = 0; nt < NTW0; ++nt)
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int n = 8 * (nt0 + nt) + fc + u;
+          if (n < QQ) {
+            const int o = lutX[n];
+#pragma unroll
+            for (int mt = 0; mt < L::N1P / 8; ++mt)
+              if (8 * mt + fr < N1) Xr[o + (8 * mt + fr) * Q] = acc[mt][nt][u];
+          }
+        }
+    }
+  }
+  __syncthreads();
+  {  // S0 is dead: stage the G blocks there (lands during the two rotations)
+    const int glen = bplan[32];
+    for (int i = 2 * tid; i < glen; i += 2 * NTH) {
+      if (i + 1 < glen) cp_async16(S0 + i, gG + i);
+      else cp_async8(S0 + i, gG + i);
+    }
+  }
+  constexpr int NT = L::NCP / 8, NTW = (NT + NW - 1) / NW;
+  {  // P = L Xr (L read through L^T) -> P rows (s Q + r', j)
     double acc[QP / 8][NTW][2];
     zero_tiles(acc);
     const int nt0 = warp * NTW;
     if (nt0 < NT) {
-      mma_tiles<QP / 8, NTW, KQ / 4, false, true>(acc, sQ1, LQ, Xr + 8 * nt0, LDR, lane);
+      mma_tiles<QP / 8, NTW, KQ / 4, false, true>(acc, sLt, LQ, Xr + 8 * nt0, LDR, lane);
 #pragma unroll
-      for (int mt = 0; mt < QP / 8; ++mt)
+      for (int nt = 0; nt < NTW; ++nt)
 #pragma unroll
-        for (int nt = 0; nt < NTW; ++nt)
+        for (int u = 0; u < 2; ++u) {
+          const int n = 8 * (nt0 + nt) + fc + u;
+          if (n < NC) {
+            const int o = lutP[n];
 #pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int m = 8 * mt + fr, n = 8 * (nt0 + nt) + fc + u;
-            if (m < Q && n < NC) Pr[((n / Q) * Q + m) * LDP + n % Q] = acc[mt][nt][u];
+            for (int mt = 0; mt < QP / 8; ++mt)
+              if (8 * mt + fr < Q) Pr[o + (8 * mt + fr) * LDP] = acc[mt][nt][u];
           }
+        }
     }
   }
   __syncthreads();
-  {  // M = P_rows Q2 -> Xr[r'][s Q + j']
+  {  // M = P_rows R -> Xr[r'][s Q + j']
     double acc[NTW][QP / 8][2];
     zero_tiles(acc);
     const int mt0 = warp * NTW;
     if (mt0 < NT) {
-      mma_tiles<NTW, QP / 8, KQ / 4, false>(acc, Pr + 8 * mt0 * LDP, LDP, sQ2, LQ, lane);
+      mma_tiles<NTW, QP / 8, KQ / 4, false>(acc, Pr + 8 * mt0 * LDP, LDP, sR, LQ, lane);
 #pragma unroll
-      for (int mt = 0; mt < NTW; ++mt)
+      for (int mt = 0; mt < NTW; ++mt) {
+        const int m = 8 * (mt0 + mt) + fr;
+        if (m < NC) {
+          const int o = (m % Q) * LDR + (m / Q) * Q;
 #pragma unroll
-        for (int nt = 0; nt < QP / 8; ++nt)
+          for (int nt = 0; nt < QP / 8; ++nt)
 #pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int m = 8 * (mt0 + mt) + fr, n = 8 * nt + fc + u;
-            if (m < NC && n < Q) Xr[(m % Q) * LDR + (m / Q) * Q + n] = acc[mt][nt][u];
+            for (int u = 0; u < 2; ++u)
+              if (8 * nt + fc + u < Q) Xr[o + 8 * nt + fc + u] = acc[mt][nt][u];
+        }
+      }
+    }
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  {  // Sylvester T1 Y_s + Y_s T2^T = M_s, T2 columns right to left; thread (s, i), s = SPW warp + lane / Q,
+     // holds row i of Y_s in registers (compile-time column indices; the block structure is a uniform branch)
+    constexpr int RS = L::RS;
+    const int sub = lane / Q, i = lane - sub * Q, sl = warp * SPW + sub;
+    const bool act = sub < SPW && sl < N1;
+    double* row = Xr + i * LDR + (act ? sl : 0) * Q;
+    double* rb = sm + L::o_rhs + warp * (4 * SPW * RS);  // [parity][column c][slice sub][RS]
+    const int me = (sub < SPW ? sub : 0) * RS;
+    double yr[Q];
+#pragma unroll
+    for (int l = 0; l < Q; ++l) yr[l] = row[l];
+    int par = 0;
+#pragma unroll
+    for (int k = Q - 1; k >= 0; --k) {
+      const int kind = bplan[k];
+      if (kind == 2) continue;
+      double* rp = rb + par * (2 * SPW * RS);
+      const double* g = S0 + bplan[16 + k];
+      if (kind == 0) {
+        double s0 = yr[k], s1 = 0.0;
+#pragma unroll
+        for (int l = k + 1; l < Q; ++l) {
+          if ((l - k) & 1) s0 = fma(-yr[l], sT2[k * Q + l], s0);
+          else s1 = fma(-yr[l], sT2[k * Q + l], s1);
+        }
+        if (act) rp[me + i] = s0 + s1;
+        __syncwarp();
+        const double* gr = g + i * L::GS1;
+        double y0 = 0.0, y1 = 0.0;
+#pragma unroll
+        for (int j = 0; j + 1 < Q; j += 2) {
+          const double2 gv = *reinterpret_cast<const double2*>(gr + j);
+          const double2 rv = *reinterpret_cast<const double2*>(rp + me + j);
+          y0 = fma(gv.x, rv.x, y0);
+          y1 = fma(gv.y, rv.y, y1);
+        }
+        if (Q & 1) y0 = fma(gr[Q - 1], rp[me + Q - 1], y0);
+        yr[k] = y0 + y1;
+      } else if (k > 0) {  // 2x2 block (k - 1, k)
+        double a0 = yr[k - 1], a1 = yr[k];
+#pragma unroll
+        for (int l = k + 1; l < Q; ++l) {
+          a0 = fma(-yr[l], sT2[(k - 1) * Q + l], a0);
+          a1 = fma(-yr[l], sT2[k * Q + l], a1);
+        }
+        if (act) {
+          rp[me + i] = a0;
+          rp[SPW * RS + me + i] = a1;
+        }
+        __syncwarp();
+        const double* g0 = g + i * L::GS2;
+        const double* g1 = g + (Q + i) * L::GS2;
+        double y0 = 0.0, y1 = 0.0, z0 = 0.0, z1 = 0.0;
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const double* r = rp + c * SPW * RS + me;
+#pragma unroll
+          for (int j = 0; j + 1 < Q; j += 2) {
+            const double2 rv = *reinterpret_cast<const double2*>(r + j);
+            const double2 u0 = *reinterpret_cast<const double2*>(g0 + c * RS + j);
+            const double2 u1 = *reinterpret_cast<const double2*>(g1 + c * RS + j);
+            y0 = fma(u0.x, rv.x, y0);
+            z0 = fma(u0.y, rv.y, z0);
+            y1 = fma(u1.x, rv.x, y1);
+            z1 = fma(u1.y, rv.y, z1);
           }
+          if (Q & 1) {
+            y0 = fma(g0[c * RS + Q - 1], r[Q - 1], y0);
+            y1 = fma(g1[c * RS + Q - 1], r[Q - 1], y1);
+          }
+        }
+        yr[k - 1] = y0 + z0;
+        yr[k] = y1 + z1;
+      }
+      par ^= 1;
+    }
+    if (act) {
+#pragma unroll
+      for (int l = 0; l < Q; ++l) row[l] = yr[l];
     }
   }
   __syncthreads();
-  {  // Sylvester per slice (shared plan), Y over M in Xr: slice s at column s Q, rows stride LDR
-    const int* sb = reinterpret_cast<const int*>(sH);
-    if (sb[3]) atomicExch(pc.status, int(TPDG_SINGULAR));
-    sylv_wavefront<Q, Q, N1, k3Threads, true, true, true>(T1, T2, Xr, LDR, Q, pc.cinv + size_t(blk) * (4 * Q * Q), sb,
-                                                            tid, pc.status);
-    __syncthreads();
-  }
   {  // Z = Q1 Y -> Z rows (s Q + r, j')
     double acc[QP / 8][NTW][2];
     zero_tiles(acc);
@@ -1364,14 +1601,17 @@ __global__ void __launch_bounds__(k3Threads) kron3d_mma_kernel(DevPC pc, const d
     if (nt0 < NT) {
       mma_tiles<QP / 8, NTW, KQ / 4, false>(acc, sQ1, LQ, Xr + 8 * nt0, LDR, lane);
 #pragma unroll
-      for (int mt = 0; mt < QP / 8; ++mt)
+      for (int nt = 0; nt < NTW; ++nt)
 #pragma unroll
-        for (int nt = 0; nt < NTW; ++nt)
+        for (int u = 0; u < 2; ++u) {
+          const int n = 8 * (nt0 + nt) + fc + u;
+          if (n < NC) {
+            const int o = lutP[n];
 #pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int m = 8 * mt + fr, n = 8 * (nt0 + nt) + fc + u;
-            if (m < Q && n < NC) Pr[((n / Q) * Q + m) * LDP + n % Q] = acc[mt][nt][u];
+            for (int mt = 0; mt < QP / 8; ++mt)
+              if (8 * mt + fr < Q) Pr[o + (8 * mt + fr) * LDP] = acc[mt][nt][u];
           }
+        }
     }
   }
   __syncthreads();
@@ -1381,39 +1621,40 @@ __global__ void __launch_bounds__(k3Threads) kron3d_mma_kernel(DevPC pc, const d
     const int mt0 = warp * NTW;
     if (mt0 < NT) {
       mma_tiles<NTW, QP / 8, KQ / 4, true>(acc, Pr + 8 * mt0 * LDP, LDP, sQ2, LQ, lane);
-      double* o = out + size_t(blk) * (N1 * Q * Q);
+      double* o = out + size_t(blk) * (N1 * QQ);
 #pragma unroll
-      for (int mt = 0; mt < NTW; ++mt)
+      for (int mt = 0; mt < NTW; ++mt) {
+        const int m = 8 * (mt0 + mt) + fr;
+        if (m < NC)
 #pragma unroll
-        for (int nt = 0; nt < QP / 8; ++nt)
+          for (int nt = 0; nt < QP / 8; ++nt)
 #pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int m = 8 * (mt0 + mt) + fr, n = 8 * nt + fc + u;
-            if (m < NC && n < Q) o[m * Q + n] = acc[mt][nt][u];
-          }
+            for (int u = 0; u < 2; ++u)
+              if (8 * nt + fc + u < Q) o[m * Q + 8 * nt + fc + u] = acc[mt][nt][u];
+      }
     }
   }
 }
 
 template <int N1, int Q>
-bool try_kron3d_mma(const DevPC& pc, const double* in, double* out, cudaStream_t st) {
-  if (pc.dim != 3 || pc.n1 != N1 || pc.q != Q) return false;
-  const size_t smem = sizeof(double) * size_t(Kron3dMmaLayout<N1, Q>::total);
+bool try_kron3d_inv(const DevPC& pc, const double* in, double* out, cudaStream_t st) {
+  if (pc.dim != 3 || pc.n1 != N1 || pc.q != Q || !pc.irec) return false;
+  using L = Kron3dInvLayout<N1, Q>;
+  const size_t smem = sizeof(double) * size_t(L::total);
   static bool configured = false;
   if (!configured) {
-    TPDG_CUDA_CHECK(cudaFuncSetAttribute(kron3d_mma_kernel<N1, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    TPDG_CUDA_CHECK(cudaFuncSetAttribute(kron3d_inv_kernel<N1, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(smem)));
-    TPDG_CUDA_CHECK(cudaFuncSetAttribute(kron3d_mma_kernel<N1, Q>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                         100));
     configured = true;
   }
-  kron3d_mma_kernel<N1, Q><<<pc.nblk, k3Threads, smem, st>>>(pc, in, out);
+  kron3d_inv_kernel<N1, Q><<<pc.nblk, L::NTH, smem, st>>>(pc, in, out);
   return true;
 }
 
-bool launch_kron3d_mma(const DevPC& pc, const double* in, double* out, cudaStream_t st) {
-  return try_kron3d_mma<4, 4>(pc, in, out, st) || try_kron3d_mma<5, 5>(pc, in, out, st) ||
-         try_kron3d_mma<8, 8>(pc, in, out, st) || try_kron3d_mma<11, 11>(pc, in, out, st);
+bool launch_kron3d_inv(const DevPC& pc, const double* in, double* out, cudaStream_t st) {
+  return try_kron3d_inv<4, 4>(pc, in, out, st) || try_kron3d_inv<5, 5>(pc, in, out, st) ||
+         try_kron3d_inv<8, 8>(pc, in, out, st) || try_kron3d_inv<11, 11>(pc, in, out, st) ||
+         try_kron3d_inv<15, 3>(pc, in, out, st) || try_kron3d_inv<40, 8>(pc, in, out, st);
 }
 
 template <int N1, int Q>
@@ -1551,6 +1792,12 @@ void set_smem(K kernel, size_t bytes, size_t& configured) {
 
 } // namespace
 
+void launch_kron3d_inv_prep(const DevPC& pc, double* irec, cudaStream_t st) {
+  if (pc.nblk == 0) return;
+  kron3d_inv_prep_kernel<<<(pc.nblk + 63) / 64, 64, 0, st>>>(pc, irec);
+  TPDG_CUDA_CHECK(cudaGetLastError());
+}
+
 void launch_sylv_cells(const DevPC& pc, double* cells, double* cinv, cudaStream_t st) {
   if (pc.nblk == 0) return;
   sylv_cells_kernel<<<(pc.nblk + 3) / 4, 128, 0, st>>>(pc, cells, cinv);
@@ -1576,7 +1823,7 @@ void launch_pc_apply(const DevPC& pc, const double* in, double* out, cudaStream_
       set_smem(kron2d_apply_kernel, smem, c2);
       kron2d_apply_kernel<<<pc.nblk, kApplyThreads, smem, st>>>(pc, in, out);
     }
-  } else if (!(!pc.faithful && launch_kron3d_mma(pc, in, out, st)) && !launch_kron3d_sized(pc, in, out, st)) {
+  } else if (!(!pc.faithful && launch_kron3d_inv(pc, in, out, st)) && !launch_kron3d_sized(pc, in, out, st)) {
     set_smem(kron3d_apply_kernel, smem, c3);
     kron3d_apply_kernel<<<pc.nblk, kApplyThreads, smem, st>>>(pc, in, out);
   }

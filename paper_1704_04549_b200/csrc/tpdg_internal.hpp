@@ -91,7 +91,8 @@ struct DevPC {
   int faithful;          // 1: bit-faithful kernels only (TPDG_GPU_FAITHFUL=1), 0: tensor-core apply
   const double* cells;   // [nblk][cells_len]: Sylvester plan + factored tiny systems (sylv_cells_len)
   int cells_len;
-  const double* cinv;    // [nblk][4 t1 t2]: row e of the inverted cell system of every Sylvester entry
+  const double* cinv;    // [nblk][4 t1 t2]: row e of the inverted cell system of every Sylvester entry (2D)
+  const double* irec;    // [nblk][irec3_len]: 3D tensor-core apply operands (kron3d_inv_prep_kernel)
   int* status;           // device error flag (SingularError inside the Sylvester solve)
   const int* skip;       // optional device flag: kernels return immediately when *skip != 0
 };
@@ -117,6 +118,14 @@ bool launch_jv3d_fast(const DevSys& s, const double* vin, const double* halo, do
 bool launch_jv2d_mma(const DevSys& s, const double* vin, const double* halo, double* vout, cudaStream_t st);
 size_t jv_smem_bytes(const DevSys& s);
 void launch_pc_apply(const DevPC& pc, const double* in, double* out, cudaStream_t st);
+// 3D tensor-core apply operands of every factored block (formation time)
+void launch_kron3d_inv_prep(const DevPC& pc, double* irec, cudaStream_t st);
+// Row stride of the 3D Sylvester block inverses G (sz = 1, 2): segments of even(q) doubles, rows 2 (mod 4) apart
+__host__ __device__ constexpr int g_row_stride(int q, int sz) {
+  return sz == 1 ? (((q + 1) & ~1) % 4 == 2 ? ((q + 1) & ~1) : ((q + 1) & ~1) + 2) : 2 * ((q + 1) & ~1) + 2;
+}
+// A1^-1 | L^T | R | Q1 | Q2 | T2 | G blocks (<= q^2 g_row_stride(q, 2))
+__host__ __device__ inline size_t irec3_doubles(int n1, int q) { return size_t(n1) * n1 + 5 * q * q + size_t(q) * q * g_row_stride(q, 2); }
 // bit-faithful 2D apply, several blocks per warp (kron_ew.cu); false if no sized variant fits
 bool launch_kron2d_ew(const DevPC& pc, const double* in, double* out, cudaStream_t st);
 // dense-LU fallback blocks, one CTA per fallback block (kron_fallback.cu); false if n is too large
