@@ -160,9 +160,19 @@ int tpdg_halo_plan_create(const tpdg_gpu_system *sys, int rank, int nranks, tpdg
 int tpdg_halo_plan_query(tpdg_halo_plan h, int *e_begin, int *e_end, int *n_halo, int *n_peers);
 int tpdg_halo_plan_conn(tpdg_halo_plan h, int *conn_out);
 int tpdg_halo_plan_halo_gid(tpdg_halo_plan h, int *gid_out);
-int tpdg_halo_plan_peer(tpdg_halo_plan h, int i, int *rank, int *n_send, int *send_local, int *recv_first,
-                        int *recv_count);
+/* Per peer: n_send face layers sent (send_pairs: local element, face) and n_recv received (recv_pairs: halo
+ * slot, face of the halo element), both ordered by (global element, face); one layer = n_c q^(d-1) doubles
+ * (the neighbour trace of ops/discretization.hpp:89-97 / 170-181). Pair arrays may be NULL (counts only). */
+int tpdg_halo_plan_peer(tpdg_halo_plan h, int i, int *rank, int *n_send, int *send_pairs, int *n_recv,
+                        int *recv_pairs);
 int tpdg_halo_plan_destroy(tpdg_halo_plan h);
+/* In-process transport: nranks contexts in one process (one host thread each, same or different GPUs) run
+ * the multi-rank data plane (face-layer halo exchange, GMRES allreduces) with device copies and a fixed-order
+ * sum instead of NCCL. Used to validate the distributed path on one GPU (tests/test_gpu_loopback.py). */
+typedef struct tpdg_gpu_loopback_s *tpdg_gpu_loopback;
+int tpdg_gpu_loopback_create(int nranks, tpdg_gpu_loopback *out);
+int tpdg_gpu_loopback_destroy(tpdg_gpu_loopback h);
+int tpdg_gpu_ctx_create_loopback(int device, int rank, tpdg_gpu_loopback hub, tpdg_gpu_ctx *out);
 
 /* ---- host-side input production for the BASELINE configurations (out of the kernel scope;
  * restates build_reference / generate_mesh(cartesian) / build_cache for scalar advection).

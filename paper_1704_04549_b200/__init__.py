@@ -99,6 +99,7 @@ EXPORTS = [
     "tpdg_gpu_build_cache_advection", "tpdg_gpu_libm_eval",
     "tpdg_uniform_vector", "tpdg_seeded_unit_vector", "tpdg_halo_plan_create", "tpdg_halo_plan_query",
     "tpdg_halo_plan_conn", "tpdg_halo_plan_halo_gid", "tpdg_halo_plan_peer", "tpdg_halo_plan_destroy",
+    "tpdg_gpu_loopback_create", "tpdg_gpu_loopback_destroy", "tpdg_gpu_ctx_create_loopback",
 ]
 
 
@@ -157,6 +158,8 @@ def lib():
         "tpdg_halo_plan_conn": [v, C.POINTER(C.c_int)], "tpdg_halo_plan_halo_gid": [v, C.POINTER(C.c_int)],
         "tpdg_halo_plan_peer": [v, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int),
                                 C.POINTER(C.c_int), C.POINTER(C.c_int)],
+        "tpdg_gpu_loopback_create": [C.c_int, C.POINTER(v)], "tpdg_gpu_loopback_destroy": [v],
+        "tpdg_gpu_ctx_create_loopback": [C.c_int, C.c_int, v, C.POINTER(v)],
         "tpdg_halo_plan_destroy": [v],
     }
     for name, args in sig.items():
@@ -305,6 +308,17 @@ def libm_eval(ctx: "Context", fn: str, x, y=None) -> np.ndarray:
     return out.cpu().numpy()
 
 
+def face_layer_nodes(dim: int, q: int, face: int) -> np.ndarray:
+    """Element-block offsets of the node layer of `face` (lower tangential axis fastest): the nodal trace
+    of ops/discretization.hpp:89-97 with Gauss-Lobatto nodes; host mirror of face_layer_index."""
+    axis, layer = face // 2, (0 if face % 2 == 0 else q - 1)
+    t = np.arange(q ** (dim - 1))
+    if dim == 2:
+        return layer + q * t if axis == 0 else t + q * layer
+    u, w = t % q, t // q
+    return {0: layer + q * (u + q * w), 1: u + q * (layer + q * w), 2: u + q * (w + q * layer)}[axis]
+
+
 def halo_plan(sys: "System", rank: int, nranks: int) -> dict:
     """Element partition + face-neighbour halo plan of one rank (host only; op_create uses the
     same plan for nranks > 1). See include/tpdg_gpu.h."""
@@ -321,13 +335,14 @@ def halo_plan(sys: "System", rank: int, nranks: int) -> dict:
         _check(lib().tpdg_halo_plan_halo_gid(h, gid.ctypes.data_as(C.POINTER(C.c_int))))
         peers = []
         for i in range(npeer.value):
-            r, ns, rf, rc = C.c_int(), C.c_int(), C.c_int(), C.c_int()
-            _check(lib().tpdg_halo_plan_peer(h, i, C.byref(r), C.byref(ns), None, C.byref(rf), C.byref(rc)))
-            send = np.zeros(max(1, ns.value), dtype=np.int32)
-            _check(lib().tpdg_halo_plan_peer(h, i, C.byref(r), C.byref(ns),
-                                             send.ctypes.data_as(C.POINTER(C.c_int)), C.byref(rf), C.byref(rc)))
-            peers.append({"rank": r.value, "send_local": send[: ns.value].copy(), "recv_first": rf.value,
-                          "recv_count": rc.value})
+            r, ns, nr = C.c_int(), C.c_int(), C.c_int()
+            _check(lib().tpdg_halo_plan_peer(h, i, C.byref(r), C.byref(ns), None, C.byref(nr), None))
+            sp = np.zeros(max(2, 2 * ns.value), dtype=np.int32)
+            rp = np.zeros(max(2, 2 * nr.value), dtype=np.int32)
+            _check(lib().tpdg_halo_plan_peer(h, i, C.byref(r), C.byref(ns), sp.ctypes.data_as(C.POINTER(C.c_int)),
+                                             C.byref(nr), rp.ctypes.data_as(C.POINTER(C.c_int))))
+            peers.append({"rank": r.value, "send_pairs": sp[: 2 * ns.value].reshape(-1, 2).copy(),
+                          "recv_pairs": rp[: 2 * nr.value].reshape(-1, 2).copy()})
         return {"e_begin": eb.value, "e_end": ee.value, "n_halo": nh.value,
                 "conn": conn[: nl * 2 * sys.dim * 3].copy(), "halo_gid": gid[: nh.value].copy(), "peers": peers}
     finally:
@@ -338,9 +353,16 @@ def halo_plan(sys: "System", rank: int, nranks: int) -> dict:
 class Context:
     """One per GPU / rank: CUDA stream (+ NCCL communicator for nranks > 1)."""
 
-    def __init__(self, device=0, rank=0, nranks=1, nccl_id=None):
+    def __init__(self, device=0, rank=0, nranks=1, nccl_id=None, loopback=None):
+        """loopback: a Loopback hub; the context then runs the multi-rank data plane in-process (one
+        host thread per rank) instead of over NCCL."""
         self.h = C.c_void_p()
         self.rank, self.nranks, self.device = rank, nranks, device
+        self._hub = loopback
+        if loopback is not None:
+            self.nranks = loopback.nranks
+            _check(lib().tpdg_gpu_ctx_create_loopback(device, rank, loopback.h, C.byref(self.h)))
+            return
         idbuf = None
         if nccl_id is not None:
             idbuf = C.create_string_buffer(bytes(nccl_id), 128)
@@ -378,6 +400,26 @@ class Context:
     def close(self):
         if self.h:
             lib().tpdg_gpu_ctx_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Loopback:
+    """In-process transport hub for nranks contexts (tpdg_gpu_loopback_create)."""
+
+    def __init__(self, nranks):
+        self.nranks = nranks
+        self.h = C.c_void_p()
+        _check(lib().tpdg_gpu_loopback_create(nranks, C.byref(self.h)))
+
+    def close(self):
+        if self.h:
+            lib().tpdg_gpu_loopback_destroy(self.h)
             self.h = C.c_void_p()
 
     def __del__(self):

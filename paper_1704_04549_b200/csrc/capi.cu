@@ -10,7 +10,9 @@
 #include <cstdlib>
 #include <cmath>
 #include <cstdio>
+#include <condition_variable>
 #include <cstring>
+#include <mutex>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -103,10 +105,46 @@ void upload(DevBuf& buf, const T* host, size_t count, cudaStream_t st) {
 } // namespace
 
 // ------------------------------------------------------------------------------------ objects
+// In-process transport for nranks contexts that share one process (and GPU): the NCCL collectives
+// of the path (halo send/recv group, allreduce) as stream-ordered device copies / a fixed-order sum,
+// with a host barrier as the rendezvous. Used to run the multi-rank data plane on one GPU (one host
+// thread per rank); the NCCL path is unchanged.
+struct tpdg_gpu_loopback_s {
+  int n = 0;
+  std::mutex m;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t gen = 0;
+  struct Send {
+    const double* p;
+    size_t count;
+    int dst;
+  };
+  std::vector<std::vector<Send>> sends;
+  std::vector<double*> ar_ptr;
+  int ar_count = 0;
+  std::vector<cudaEvent_t> posted, copied;
+  cudaEvent_t reduced = nullptr;
+  void barrier() {
+    std::unique_lock<std::mutex> lk(m);
+    const uint64_t g = gen;
+    if (++arrived == n) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+  }
+};
+
 struct tpdg_gpu_ctx_s {
   int device = 0, rank = 0, nranks = 1;
   cudaStream_t stream = nullptr;
   ncclComm_t comm = nullptr;
+  tpdg_gpu_loopback_s* hub = nullptr;  // in-process transport instead of NCCL
+  cudaStream_t comm_stream = nullptr;  // halo exchange, overlapped with the interior Jv
+  cudaEvent_t ev_in = nullptr, ev_halo = nullptr;
   int64_t launches_at_create = 0;
   // optional per-class CUDA-event timing (0 PC apply, 1 Jv, 2 MGS/norm passes, 3 other GMRES vector ops)
   bool profiling = false;
@@ -151,15 +189,16 @@ struct tpdg_gpu_op_s {
   DevBuf io_a, io_b;  // staging for the host-pointer entry points
   DevBuf shuf_ws;
   DevBuf form_ws;  // Lanczos workspace of form_ksvd, kept across formations (up to ~4 GiB at cfg4)
-  // halo plan (multi-rank): for each peer rank, local elements to send and halo slots to fill
+  // halo plan (multi-rank, halo.cpp): per peer rank, the face node layers sent and received
   struct Peer {
     int rank = 0;
-    std::vector<int> send_local;  // local element ids
-    int recv_first = 0, recv_count = 0;  // halo slot range
-    DevBuf send_idx, send_buf;
+    int n_send = 0, n_recv = 0;     // layers
+    DevBuf send_pairs, recv_pairs;  // int (element, face) / (halo slot, face) per layer
+    DevBuf send_buf, recv_buf;      // n_c q^(d-1) doubles per layer
   };
   std::vector<Peer> peers;
   int n_halo = 0;
+  int int_lo = 0, int_hi = 0;  // interior local elements [int_lo, int_hi): no off-rank neighbour
   // GMRES workspace, allocated on first use and reused (no allocation inside a solve)
   GmresWork gws;
   MappedStatus gstatus;
@@ -210,6 +249,8 @@ DevSys make_devsys(const tpdg_gpu_op_s& op, int block_mode, double a, double b) 
   s.nqf = s.nqv / op.mu;
   s.n_local = op.e_end - op.e_begin;
   s.n_halo = op.n_halo;
+  s.e_lo = 0;
+  s.e_hi = s.n_local;
   s.small = block_mode;
   s.a = a;
   s.b = b;
@@ -233,51 +274,155 @@ DevSys make_devsys(const tpdg_gpu_op_s& op, int block_mode, double a, double b) 
   return s;
 }
 
-__global__ void gather_elems_kernel(const double* __restrict__ v, const int* __restrict__ idx, int count, int blk,
-                                    double* __restrict__ out) {
-  const int64_t total = int64_t(count) * blk;
+// Face node layers <-> contiguous buffers (layer p: n_c components x q^(d-1) nodes).
+__global__ void gather_layers_kernel(const double* __restrict__ v, const int* __restrict__ pairs, int count, int d,
+                                     int q, int nc, int npe, double* __restrict__ out) {
+  const int L = d == 2 ? q : q * q;
+  const int64_t total = int64_t(count) * nc * L;
   for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
-    const int e = int(t / blk), i = int(t % blk);
-    out[t] = v[int64_t(idx[e]) * blk + i];
+    const int pi = int(t / (nc * L)), r = int(t % (nc * L)), c = r / L, k = r % L;
+    out[t] = v[(int64_t(pairs[2 * pi]) * nc + c) * npe + face_layer_index(d, q, pairs[2 * pi + 1], k)];
+  }
+}
+__global__ void scatter_layers_kernel(const double* __restrict__ in, const int* __restrict__ pairs, int count, int d,
+                                      int q, int nc, int npe, double* __restrict__ halo) {
+  const int L = d == 2 ? q : q * q;
+  const int64_t total = int64_t(count) * nc * L;
+  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < total; t += int64_t(gridDim.x) * blockDim.x) {
+    const int pi = int(t / (nc * L)), r = int(t % (nc * L)), c = r / L, k = r % L;
+    halo[(int64_t(pairs[2 * pi]) * nc + c) * npe + face_layer_index(d, q, pairs[2 * pi + 1], k)] = in[t];
+  }
+}
+__global__ void loopback_sum_kernel(double* const* ptr, int nranks, int count) {
+  for (int i = threadIdx.x; i < count; i += blockDim.x) {
+    double s = 0.0;
+    for (int r = 0; r < nranks; ++r) s += ptr[r][i];  // fixed rank order
+    for (int r = 0; r < nranks; ++r) ptr[r][i] = s;
   }
 }
 
-// Face-neighbour halo exchange (whole element blocks of the elements referenced across ranks).
-void exchange_halo(tpdg_gpu_op op, const double* d_in) {
-  if (op->ctx->nranks == 1 || op->peers.empty()) return;
-  cudaStream_t st = op->ctx->stream;
-  const int blk = op->n_c * op->s.npe;
+// One group of point-to-point transfers on stream st: NCCL, or the in-process transport (each rank
+// copies its receives out of the peers' posted send buffers, then waits until the peers have copied
+// out of its own, so the buffers can be reused).
+struct Xfer {
+  double* p;
+  size_t count;
+  int peer;
+};
+void comm_sendrecv(tpdg_gpu_ctx ctx, const std::vector<Xfer>& sends, const std::vector<Xfer>& recvs, cudaStream_t st) {
+  if (!ctx->hub) {
+    NCCL_CHECK(ncclGroupStart());
+    for (const auto& x : sends)
+      if (x.count) NCCL_CHECK(ncclSend(x.p, x.count, ncclDouble, x.peer, ctx->comm, st));
+    for (const auto& x : recvs)
+      if (x.count) NCCL_CHECK(ncclRecv(x.p, x.count, ncclDouble, x.peer, ctx->comm, st));
+    NCCL_CHECK(ncclGroupEnd());
+    return;
+  }
+  tpdg_gpu_loopback_s& h = *ctx->hub;
+  const int r = ctx->rank;
+  h.sends[r].clear();
+  for (const auto& x : sends) h.sends[r].push_back({x.p, x.count, x.peer});
+  TPDG_CUDA_CHECK(cudaEventRecord(h.posted[r], st));
+  h.barrier();
+  for (const auto& x : recvs) {
+    if (!x.count) continue;
+    const tpdg_gpu_loopback_s::Send* src = nullptr;
+    for (const auto& sd : h.sends[x.peer])
+      if (sd.dst == r) src = &sd;
+    REQUIRE(src && src->count == x.count, TPDG_CONFIG, "loopback: unmatched receive");
+    TPDG_CUDA_CHECK(cudaStreamWaitEvent(st, h.posted[x.peer], 0));
+    TPDG_CUDA_CHECK(cudaMemcpyAsync(x.p, src->p, sizeof(double) * x.count, cudaMemcpyDeviceToDevice, st));
+  }
+  TPDG_CUDA_CHECK(cudaEventRecord(h.copied[r], st));
+  h.barrier();
+  for (const auto& x : sends)
+    if (x.count) TPDG_CUDA_CHECK(cudaStreamWaitEvent(st, h.copied[x.peer], 0));
+}
+
+// Face-neighbour halo exchange on the communication stream: gather the layers the peers need,
+// transfer, scatter the received layers into the halo blocks (only those layers are ever read).
+void exchange_halo(tpdg_gpu_op op, const double* d_in, cudaStream_t st) {
+  const int d = op->dim, q = op->q, nc = op->n_c, npe = op->s.npe;
+  const size_t L = size_t(nc) * (d == 2 ? q : q * q);
+  std::vector<Xfer> sends, recvs;
   for (auto& p : op->peers) {
-    const int cnt = int(p.send_local.size());
-    if (cnt) {
-      gather_elems_kernel<<<std::min(148 * 4, (cnt * blk + 255) / 256), 256, 0, st>>>(d_in, p.send_idx.as<int>(),
-                                                                                     cnt, blk,
-                                                                                     p.send_buf.as<double>());
+    if (p.n_send) {
+      gather_layers_kernel<<<std::min<int64_t>(148 * 4, (p.n_send * L + 255) / 256), 256, 0, st>>>(
+          d_in, p.send_pairs.as<int>(), p.n_send, d, q, nc, npe, p.send_buf.as<double>());
       TPDG_CUDA_CHECK(cudaGetLastError());
       ++g_launches;
     }
+    sends.push_back({p.send_buf.as<double>(), p.n_send * L, p.rank});
+    recvs.push_back({p.recv_buf.as<double>(), p.n_recv * L, p.rank});
   }
-  NCCL_CHECK(ncclGroupStart());
-  for (auto& p : op->peers) {
-    const size_t ns = p.send_local.size() * size_t(blk);
-    if (ns) NCCL_CHECK(ncclSend(p.send_buf.as<double>(), ns, ncclDouble, p.rank, op->ctx->comm, st));
-    const size_t nr = size_t(p.recv_count) * blk;
-    if (nr)
-      NCCL_CHECK(ncclRecv(op->halo.as<double>() + size_t(p.recv_first) * blk, nr, ncclDouble, p.rank, op->ctx->comm,
-                          st));
-  }
-  NCCL_CHECK(ncclGroupEnd());
+  comm_sendrecv(op->ctx, sends, recvs, st);
+  for (auto& p : op->peers)
+    if (p.n_recv) {
+      scatter_layers_kernel<<<std::min<int64_t>(148 * 4, (p.n_recv * L + 255) / 256), 256, 0, st>>>(
+          p.recv_buf.as<double>(), p.recv_pairs.as<int>(), p.n_recv, d, q, nc, npe, op->halo.as<double>());
+      TPDG_CUDA_CHECK(cudaGetLastError());
+      ++g_launches;
+    }
 }
 
 void allreduce_scalar(tpdg_gpu_ctx ctx, double* d_val, int count = 1) {
   if (ctx->nranks == 1) return;
-  NCCL_CHECK(ncclAllReduce(d_val, d_val, count, ncclDouble, ncclSum, ctx->comm, ctx->stream));
+  if (!ctx->hub) {
+    NCCL_CHECK(ncclAllReduce(d_val, d_val, count, ncclDouble, ncclSum, ctx->comm, ctx->stream));
+    return;
+  }
+  tpdg_gpu_loopback_s& h = *ctx->hub;
+  const int r = ctx->rank;
+  h.ar_ptr[r] = d_val;
+  h.ar_count = count;
+  TPDG_CUDA_CHECK(cudaEventRecord(h.posted[r], ctx->stream));
+  h.barrier();
+  if (r == 0) {
+    for (int k = 1; k < h.n; ++k) TPDG_CUDA_CHECK(cudaStreamWaitEvent(ctx->stream, h.posted[k], 0));
+    struct Ptrs {
+      double* p[8];
+    } pp{};
+    for (int k = 0; k < h.n; ++k) pp.p[k] = h.ar_ptr[k];
+    // the pointer table travels by value in a small device buffer of the hub's rank 0 stream order
+    static thread_local DevBuf tbl;
+    if (!tbl.p) tbl.alloc(sizeof(Ptrs));
+    TPDG_CUDA_CHECK(cudaMemcpyAsync(tbl.p, &pp, sizeof(Ptrs), cudaMemcpyHostToDevice, ctx->stream));
+    loopback_sum_kernel<<<1, 32, 0, ctx->stream>>>(tbl.as<double*>(), h.n, count);
+    TPDG_CUDA_CHECK(cudaGetLastError());
+    TPDG_CUDA_CHECK(cudaEventRecord(h.reduced, ctx->stream));
+    TPDG_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));  // pp is a host temporary
+  }
+  h.barrier();
+  if (r != 0) TPDG_CUDA_CHECK(cudaStreamWaitEvent(ctx->stream, h.reduced, 0));
 }
 
-void jv_device(tpdg_gpu_op op, const double* d_in, double* d_out) {
-  exchange_halo(op, d_in);
-  Prof pr(op->ctx, 1);
-  launch_jv(op->s, d_in, op->halo.as<double>(), d_out, op->ctx->stream);
+// Jv with the halo exchange overlapped: the interior elements (no off-rank neighbour) run on the
+// main stream while the communication stream moves the face layers; the boundary elements follow.
+void jv_device(tpdg_gpu_op op, const double* d_in, double* d_out, const DevSys* sys = nullptr) {
+  const DevSys& s0 = sys ? *sys : op->s;
+  tpdg_gpu_ctx ctx = op->ctx;
+  if (ctx->nranks == 1 || op->peers.empty()) {
+    Prof pr(ctx, 1);
+    launch_jv(s0, d_in, op->halo.as<double>(), d_out, ctx->stream);
+    return;
+  }
+  TPDG_CUDA_CHECK(cudaEventRecord(ctx->ev_in, ctx->stream));
+  TPDG_CUDA_CHECK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_in, 0));
+  exchange_halo(op, d_in, ctx->comm_stream);
+  TPDG_CUDA_CHECK(cudaEventRecord(ctx->ev_halo, ctx->comm_stream));
+  Prof pr(ctx, 1);
+  DevSys s = s0;
+  s.e_lo = op->int_lo;
+  s.e_hi = op->int_hi;
+  launch_jv(s, d_in, op->halo.as<double>(), d_out, ctx->stream);
+  TPDG_CUDA_CHECK(cudaStreamWaitEvent(ctx->stream, ctx->ev_halo, 0));
+  s.e_lo = 0;
+  s.e_hi = op->int_lo;
+  launch_jv(s, d_in, op->halo.as<double>(), d_out, ctx->stream);
+  s.e_lo = op->int_hi;
+  s.e_hi = s0.n_local;
+  launch_jv(s, d_in, op->halo.as<double>(), d_out, ctx->stream);
 }
 
 void pc_apply_device(tpdg_gpu_pc pc, const double* d_in, double* d_out) {
@@ -405,11 +550,7 @@ int run_gmres(tpdg_gpu_op op, tpdg_gpu_pc pc, const double* d_b, double* d_x, co
     else
       TPDG_CUDA_CHECK(cudaMemcpyAsync(out, in, sizeof(double) * n, cudaMemcpyDeviceToDevice, st));
   };
-  auto apply_op = [&](const double* in, double* out, bool guarded) {
-    exchange_halo(op, in);
-    Prof pr(ctx, 1);
-    launch_jv(guarded ? sk : op->s, in, op->halo.as<double>(), out, st);
-  };
+  auto apply_op = [&](const double* in, double* out, bool guarded) { jv_device(op, in, out, guarded ? &sk : nullptr); };
 
   int its = 0, nh = 0;
   bool conv = false;
@@ -672,7 +813,56 @@ int tpdg_gpu_ctx_create(int device, int rank, int nranks, const void* nccl_id, t
       ncclUniqueId id;
       std::memcpy(&id, nccl_id, sizeof(id));
       NCCL_CHECK(ncclCommInitRank(&c->comm, nranks, id, rank));
+      TPDG_CUDA_CHECK(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+      TPDG_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming));
+      TPDG_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming));
     }
+    c->launches_at_create = g_launches;
+    *out = c.release();
+  });
+}
+
+int tpdg_gpu_loopback_create(int nranks, tpdg_gpu_loopback* out) {
+  return guarded([&] {
+    REQUIRE(out && nranks >= 1 && nranks <= 8, TPDG_CONFIG, "loopback_create: 1 <= nranks <= 8");
+    std::unique_ptr<tpdg_gpu_loopback_s> h(new tpdg_gpu_loopback_s);
+    h->n = nranks;
+    h->sends.resize(nranks);
+    h->ar_ptr.assign(nranks, nullptr);
+    h->posted.resize(nranks);
+    h->copied.resize(nranks);
+    for (int r = 0; r < nranks; ++r) {
+      TPDG_CUDA_CHECK(cudaEventCreateWithFlags(&h->posted[r], cudaEventDisableTiming));
+      TPDG_CUDA_CHECK(cudaEventCreateWithFlags(&h->copied[r], cudaEventDisableTiming));
+    }
+    TPDG_CUDA_CHECK(cudaEventCreateWithFlags(&h->reduced, cudaEventDisableTiming));
+    *out = h.release();
+  });
+}
+
+int tpdg_gpu_loopback_destroy(tpdg_gpu_loopback h) {
+  return guarded([&] {
+    if (!h) return;
+    for (auto e : h->posted) cudaEventDestroy(e);
+    for (auto e : h->copied) cudaEventDestroy(e);
+    if (h->reduced) cudaEventDestroy(h->reduced);
+    delete h;
+  });
+}
+
+int tpdg_gpu_ctx_create_loopback(int device, int rank, tpdg_gpu_loopback hub, tpdg_gpu_ctx* out) {
+  return guarded([&] {
+    REQUIRE(out && hub && rank >= 0 && rank < hub->n, TPDG_CONFIG, "ctx_create_loopback: bad rank");
+    std::unique_ptr<tpdg_gpu_ctx_s> c(new tpdg_gpu_ctx_s);
+    c->device = device;
+    c->rank = rank;
+    c->nranks = hub->n;
+    c->hub = hub;
+    TPDG_CUDA_CHECK(cudaSetDevice(device));
+    TPDG_CUDA_CHECK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    TPDG_CUDA_CHECK(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+    TPDG_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_in, cudaEventDisableTiming));
+    TPDG_CUDA_CHECK(cudaEventCreateWithFlags(&c->ev_halo, cudaEventDisableTiming));
     c->launches_at_create = g_launches;
     *out = c.release();
   });
@@ -686,6 +876,9 @@ int tpdg_gpu_ctx_destroy(tpdg_gpu_ctx ctx) {
       cudaEventDestroy(pr.second);
     }
     if (ctx->comm) ncclCommDestroy(ctx->comm);
+    if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
+    if (ctx->ev_halo) cudaEventDestroy(ctx->ev_halo);
+    if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
     if (ctx->stream) cudaStreamDestroy(ctx->stream);
     delete ctx;
   });
@@ -800,19 +993,45 @@ int tpdg_gpu_op_create(tpdg_gpu_ctx ctx, const tpdg_gpu_system* sys, double dt, 
     const HaloPlan plan = build_halo_plan(sys, ctx->rank, ctx->nranks, e_begin, e_end);
     const std::vector<int>& conn = plan.conn;
     op->n_halo = plan.n_halo;
+    const size_t layer = size_t(nc) * (d == 2 ? q : size_t(q) * q);
     for (const auto& pp : plan.peers) {
       tpdg_gpu_op_s::Peer p;
       p.rank = pp.rank;
-      p.send_local = pp.send_local;
-      p.recv_first = pp.recv_first;
-      p.recv_count = pp.recv_count;
-      if (!p.send_local.empty()) {
-        upload(p.send_idx, p.send_local.data(), p.send_local.size(), st);
-        p.send_buf.alloc(sizeof(double) * p.send_local.size() * nc * npe);
+      p.n_send = int(pp.send_elem.size());
+      p.n_recv = int(pp.recv_slot.size());
+      std::vector<int> sp(2 * size_t(p.n_send)), rp(2 * size_t(p.n_recv));
+      for (int i = 0; i < p.n_send; ++i) {
+        sp[2 * i] = pp.send_elem[i];
+        sp[2 * i + 1] = pp.send_face[i];
       }
+      for (int i = 0; i < p.n_recv; ++i) {
+        rp[2 * i] = pp.recv_slot[i];
+        rp[2 * i + 1] = pp.recv_face[i];
+      }
+      upload(p.send_pairs, sp.data(), sp.size(), st);
+      upload(p.recv_pairs, rp.data(), rp.size(), st);
+      p.send_buf.alloc(sizeof(double) * std::max<size_t>(1, p.n_send * layer));
+      p.recv_buf.alloc(sizeof(double) * std::max<size_t>(1, p.n_recv * layer));
       op->peers.push_back(std::move(p));
     }
-    if (ctx->nranks > 1) op->halo.alloc(sizeof(double) * std::max<size_t>(1, size_t(op->n_halo) * nc * npe));
+    if (ctx->nranks > 1) {
+      op->halo.alloc(sizeof(double) * std::max<size_t>(1, size_t(op->n_halo) * nc * npe));
+      // the halo blocks hold only the received layers; fill the rest with NaN so that a kernel reading
+      // anything else cannot go unnoticed
+      TPDG_CUDA_CHECK(cudaMemsetAsync(op->halo.p, 0xff, op->halo.bytes, st));
+    }
+    {  // interior range: local elements before the first / after the last one with an off-rank neighbour
+      const int nl_i = e_end - e_begin;
+      int lo_b = -1, hi_b = nl_i;
+      for (int le = 0; le < nl_i; ++le)
+        for (int f = 0; f < 2 * d; ++f)
+          if (conn[(size_t(le) * 2 * d + f) * 3] >= nl_i) {
+            if (le < nl_i / 2) lo_b = std::max(lo_b, le);
+            else hi_b = std::min(hi_b, le);
+          }
+      op->int_lo = lo_b + 1;
+      op->int_hi = std::max(hi_b, op->int_lo);
+    }
     upload(op->conn, conn.data(), conn.size(), st);
     const double a = jacobian_only ? 0.0 : 1.0, b = jacobian_only ? 1.0 : -dt;
     op->s = make_devsys(*op, block_mode, a, b);
@@ -1092,16 +1311,24 @@ int tpdg_halo_plan_halo_gid(tpdg_halo_plan h, int* gid_out) {
   return guarded([&] { std::copy(h->p.halo_gid.begin(), h->p.halo_gid.end(), gid_out); });
 }
 
-int tpdg_halo_plan_peer(tpdg_halo_plan h, int i, int* rank, int* n_send, int* send_local, int* recv_first,
-                        int* recv_count) {
+int tpdg_halo_plan_peer(tpdg_halo_plan h, int i, int* rank, int* n_send, int* send_pairs, int* n_recv,
+                        int* recv_pairs) {
   return guarded([&] {
     REQUIRE(i >= 0 && i < int(h->p.peers.size()), TPDG_SHAPE, "halo_plan_peer: index out of range");
     const auto& p = h->p.peers[i];
     *rank = p.rank;
-    *n_send = int(p.send_local.size());
-    if (send_local) std::copy(p.send_local.begin(), p.send_local.end(), send_local);
-    *recv_first = p.recv_first;
-    *recv_count = p.recv_count;
+    *n_send = int(p.send_elem.size());
+    *n_recv = int(p.recv_slot.size());
+    if (send_pairs)
+      for (size_t k = 0; k < p.send_elem.size(); ++k) {
+        send_pairs[2 * k] = p.send_elem[k];
+        send_pairs[2 * k + 1] = p.send_face[k];
+      }
+    if (recv_pairs)
+      for (size_t k = 0; k < p.recv_slot.size(); ++k) {
+        recv_pairs[2 * k] = p.recv_slot[k];
+        recv_pairs[2 * k + 1] = p.recv_face[k];
+      }
   });
 }
 

@@ -3,11 +3,16 @@
 // Rank r owns the contiguous element range [E r / N, E (r+1) / N): element rows in 2D and slabs in
 // 3D, because the reference numbers elements e = (k ny + j) nx + i (reference dg/mesh.hpp:312).
 // The only cross-element data dependence of the hot path is the neighbour trace inside
-// jacobian_apply (ops/linearized.hpp:216-236, ops/discretization.hpp:170-181), so a rank needs
-// the state blocks of the off-rank face neighbours of its elements: the halo. Halo slots are
-// grouped by owner rank and sorted by global id; the owner sends exactly the elements that have
-// a face neighbour on the receiving rank, in ascending order (face adjacency is symmetric), so
-// send and receive orders agree without any index exchange.
+// jacobian_apply (ops/linearized.hpp:216-236, ops/discretization.hpp:170-181), and with
+// Gauss-Lobatto nodes that trace is the neighbour's face node layer (discretization.hpp:89-97):
+// a rank needs, per cut face, n_c q^(d-1) values of the off-rank neighbour, not its element block.
+// Off-rank neighbours still get a halo slot (an element-block-sized place where the layers they
+// contribute are written, so the operator kernels address them like local neighbours); slots are
+// grouped by owner rank and sorted by global id. The owner sends the layers (element, face) of its
+// faces whose neighbour is on the receiving rank, ordered by (global element, face); the receiver
+// lists the layers it needs, (neighbour, neighbour face), in the same order. Face adjacency is
+// symmetric (the neighbour of (nb, nf) is the requesting face), so both lists are the same set in
+// the same order without any index exchange.
 #include <algorithm>
 #include <string>
 #include <vector>
@@ -32,7 +37,8 @@ HaloPlan build_halo_plan(const tpdg_gpu_system* sys, int rank, int nranks, int e
   P.e_end = e_end;
   const size_t nl = size_t(e_end - e_begin);
   P.conn.assign(nl * 2 * d * 3, 0);
-  std::vector<std::vector<int>> need(nranks);
+  std::vector<std::vector<int>> need(nranks);                      // remote neighbour elements per owner
+  std::vector<std::vector<std::pair<int, int>>> need_layer(nranks);  // (neighbour gid, neighbour face)
   for (size_t le = 0; le < nl; ++le)
     for (int f = 0; f < 2 * d; ++f) {
       const int64_t* fc = sys->conn + ((size_t(e_begin) + le) * 2 * d + f) * 3;
@@ -48,6 +54,7 @@ HaloPlan build_halo_plan(const tpdg_gpu_system* sys, int rank, int nranks, int e
         if (nranks == 1) throw Failure{TPDG_CONFIG, "neighbour outside the local range needs nranks > 1"};
         out[0] = -2 - int(nb);
         need[owner_of(int(nb))].push_back(int(nb));
+        need_layer[owner_of(int(nb))].push_back({int(nb), int(fc[1])});
       }
     }
   std::vector<std::pair<int, int>> gid_slot;
@@ -56,45 +63,39 @@ HaloPlan build_halo_plan(const tpdg_gpu_system* sys, int rank, int nranks, int e
     auto& nd = need[r];
     std::sort(nd.begin(), nd.end());
     nd.erase(std::unique(nd.begin(), nd.end()), nd.end());
-    if (r == rank || nd.empty()) continue;
-    HaloPlan::Peer p;
-    p.rank = r;
-    p.recv_first = slot;
-    p.recv_count = int(nd.size());
     for (int gid : nd) {
       gid_slot.push_back({gid, int(nl) + slot++});
       P.halo_gid.push_back(gid);
     }
-    P.peers.push_back(p);
   }
   std::sort(gid_slot.begin(), gid_slot.end());
+  auto slot_of = [&](int gid) {
+    return std::lower_bound(gid_slot.begin(), gid_slot.end(), std::make_pair(gid, -1))->second;
+  };
   for (size_t i = 0; i < P.conn.size(); i += 3)
-    if (P.conn[i] <= -2) {
-      const int gid = -2 - P.conn[i];
-      P.conn[i] = std::lower_bound(gid_slot.begin(), gid_slot.end(), std::make_pair(gid, -1))->second;
-    }
+    if (P.conn[i] <= -2) P.conn[i] = slot_of(-2 - P.conn[i]);
   P.n_halo = slot;
   if (nranks > 1)
     for (int r = 0; r < nranks; ++r) {
       if (r == rank) continue;
-      std::vector<int> send;
-      for (size_t le = 0; le < nl; ++le)
+      HaloPlan::Peer p;
+      p.rank = r;
+      auto& nlay = need_layer[r];
+      std::sort(nlay.begin(), nlay.end());
+      nlay.erase(std::unique(nlay.begin(), nlay.end()), nlay.end());
+      for (const auto& gf : nlay) {
+        p.recv_slot.push_back(slot_of(gf.first) - int(nl));
+        p.recv_face.push_back(gf.second);
+      }
+      for (size_t le = 0; le < nl; ++le)  // ascending (gid, face): the peer's need list, by symmetry
         for (int f = 0; f < 2 * d; ++f) {
           const int64_t nb = sys->conn[((size_t(e_begin) + le) * 2 * d + f) * 3];
           if (nb >= 0 && (nb < e_begin || nb >= e_end) && owner_of(int(nb)) == r) {
-            send.push_back(int(le));
-            break;
+            p.send_elem.push_back(int(le));
+            p.send_face.push_back(f);
           }
         }
-      if (send.empty()) continue;
-      auto it = std::find_if(P.peers.begin(), P.peers.end(), [&](const HaloPlan::Peer& p) { return p.rank == r; });
-      if (it == P.peers.end()) {
-        HaloPlan::Peer p;
-        p.rank = r;
-        P.peers.push_back(p);
-        it = P.peers.end() - 1;
-      }
-      it->send_local = send;
+      if (!p.recv_slot.empty() || !p.send_elem.empty()) P.peers.push_back(std::move(p));
     }
   return P;
 }

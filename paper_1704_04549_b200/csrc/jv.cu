@@ -30,7 +30,7 @@ __global__ void __launch_bounds__(256) jv2d_kernel(DevSys s, const double* __res
                                                     const double* __restrict__ halo, double* __restrict__ vout) {
   extern __shared__ double sm[];
   if (s.skip && *s.skip) return;
-  const int e = blockIdx.x;
+  const int e = s.e_lo + blockIdx.x;
   const int q = s.q, mu = s.mu, nc = s.n_c, qq = q * q, mm = mu * mu;
   const int tid = threadIdx.x, nt = blockDim.x;
   double* sG = sm;                 // mu*q
@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(128) jv2d_sized_kernel(DevSys s, const double*
   __syncthreads();
   if (warp >= NW) return;
   const double* G = W + L::w_G;
-  for (int e = blockIdx.x * NW + warp; e < s.n_local; e += gridDim.x * NW) {
+  for (int e = s.e_lo + blockIdx.x * NW + warp; e < s.e_hi; e += gridDim.x * NW) {
     double* v = E + L::e_v;
     double* t = E + L::e_t;
     double* ab = E + L::e_t;
@@ -357,7 +357,7 @@ bool try_jv2d_sized(const DevSys& s, const double* vin, const double* halo, doub
     TPDG_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     grid = std::max(1, per_sm) * sms;
   }
-  const int need = (s.n_local + L::warps - 1) / L::warps;
+  const int need = (s.e_hi - s.e_lo + L::warps - 1) / L::warps;
   jv2d_sized_kernel<Q, MU><<<std::min(grid, need), 128, smem, st>>>(s, vin, halo, vout);
   return true;
 }
@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(256) jv3d_kernel(DevSys s, const double* __res
                                                     const double* __restrict__ halo, double* __restrict__ vout) {
   extern __shared__ double sm[];
   if (s.skip && *s.skip) return;
-  const int e = blockIdx.x;
+  const int e = s.e_lo + blockIdx.x;
   const int q = s.q, mu = s.mu, nc = s.n_c;
   const int q3 = q * q * q, m3 = mu * mu * mu, m2 = mu * mu, q2 = q * q;
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -631,7 +631,7 @@ __global__ void __launch_bounds__(256) jv3d_sized_kernel(DevSys s, const double*
     GW[i] = s.gw[i];
     DW[i] = s.dw[i];
   }
-  for (int e = blockIdx.x; e < s.n_local; e += gridDim.x) {
+  for (int e = s.e_lo + blockIdx.x; e < s.e_hi; e += gridDim.x) {
     __syncthreads();
     const double* ve = vin + size_t(e) * Q3;
     for (int i = tid; i < Q3; i += nt) v[i] = ve[i];
@@ -856,7 +856,7 @@ bool try_jv3d_sized(const DevSys& s, const double* vin, const double* halo, doub
     TPDG_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     grid = std::max(1, per_sm) * sms;
   }
-  jv3d_sized_kernel<Q, MU><<<std::min(grid, s.n_local), 256, smem, st>>>(s, vin, halo, vout);
+  jv3d_sized_kernel<Q, MU><<<std::min(grid, s.e_hi - s.e_lo), 256, smem, st>>>(s, vin, halo, vout);
   return true;
 }
 
@@ -878,7 +878,7 @@ size_t jv3d_smem(const DevSys& s) {
 size_t jv_smem_bytes(const DevSys& s) { return s.dim == 2 ? jv2d_smem(s) : jv3d_smem(s); }
 
 void launch_jv(const DevSys& s, const double* vin, const double* halo, double* vout, cudaStream_t st) {
-  if (s.n_local == 0) return;
+  if (s.e_hi <= s.e_lo) return;
   const size_t smem = jv_smem_bytes(s);
   if (s.dim == 2 && (launch_jv2d_mma(s, vin, halo, vout, st) || launch_jv2d_sized(s, vin, halo, vout, st))) {
     TPDG_CUDA_CHECK(cudaGetLastError());
@@ -896,14 +896,14 @@ void launch_jv(const DevSys& s, const double* vin, const double* halo, double* v
       TPDG_CUDA_CHECK(cudaFuncSetAttribute(jv2d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
       configured = smem;
     }
-    jv2d_kernel<<<s.n_local, 256, smem, st>>>(s, vin, halo, vout);
+    jv2d_kernel<<<s.e_hi - s.e_lo, 256, smem, st>>>(s, vin, halo, vout);
   } else {
     static size_t configured = 0;
     if (smem > configured) {
       TPDG_CUDA_CHECK(cudaFuncSetAttribute(jv3d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
       configured = smem;
     }
-    jv3d_kernel<<<s.n_local, 256, smem, st>>>(s, vin, halo, vout);
+    jv3d_kernel<<<s.e_hi - s.e_lo, 256, smem, st>>>(s, vin, halo, vout);
   }
   TPDG_CUDA_CHECK(cudaGetLastError());
   ++g_launches;

@@ -153,13 +153,13 @@ __global__ void __launch_bounds__(NT, MINB) jv3d_fast_kernel(DevSys s, const dou
   constexpr int Q2 = L::Q2, Q3 = L::Q3, M2 = L::M2, M3 = L::M3;
   extern __shared__ double sm[];
   const int tid = threadIdx.x;
-  if (int(blockIdx.x) < s.n_local) {
-    prefetch_element<Q, MU>(s, vin, blockIdx.x);
-    load_element_async<Q, NT>(s, vin, halo, blockIdx.x, sm + L::v, sm + L::nbl);
+  if (s.e_lo + int(blockIdx.x) < s.e_hi) {
+    prefetch_element<Q, MU>(s, vin, s.e_lo + blockIdx.x);
+    load_element_async<Q, NT>(s, vin, halo, s.e_lo + blockIdx.x, sm + L::v, sm + L::nbl);
   }
-  for (int e = blockIdx.x; e < s.n_local; e += gridDim.x) {
+  for (int e = s.e_lo + blockIdx.x; e < s.e_hi; e += gridDim.x) {
     const int e_next = e + int(gridDim.x);
-    if (e_next < s.n_local) prefetch_element<Q, MU>(s, vin, e_next);
+    if (e_next < s.e_hi) prefetch_element<Q, MU>(s, vin, e_next);
     // ---- E0: this element's v and neighbour layers (cp.async issued during the previous element's E4)
     asm volatile("cp.async.wait_all;\n" ::: "memory");
     __syncthreads();
@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(NT, MINB) jv3d_fast_kernel(DevSys s, const dou
     }
     __syncthreads();
     // the next element's v and neighbour layers travel during E4 / E5 (X2 is free from here on)
-    if (e_next < s.n_local) load_element_async<Q, NT>(s, vin, halo, e_next, sm + L::v, sm + L::nbl);
+    if (e_next < s.e_hi) load_element_async<Q, NT>(s, vin, halo, e_next, sm + L::v, sm + L::nbl);
     // ---- E4: y integration, pencils (k, al): S1 = Gy A1 + Dy A3 (-> A1 slots), S2 = Gy A2 (-> A2 slots)
     for (int p = tid; p < Q * MU; p += NT) {
       const int k = p / MU, al = p % MU;
@@ -392,7 +392,7 @@ bool try_jv3d_fast(const DevSys& s, const double* vin, const double* halo, doubl
       has[dev] = true;
     }
   }
-  jv3d_fast_kernel<SLOT, Q, MU, NT, MINB><<<std::min(grid[dev], s.n_local), NT, smem, st>>>(s, vin, halo, vout);
+  jv3d_fast_kernel<SLOT, Q, MU, NT, MINB><<<std::min(grid[dev], s.e_hi - s.e_lo), NT, smem, st>>>(s, vin, halo, vout);
   return true;
 }
 

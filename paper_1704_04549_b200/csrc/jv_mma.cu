@@ -115,7 +115,7 @@ __global__ void __launch_bounds__(32 * kJvWarps) jv2d_mma_kernel(DevSys s, const
   // per-element global data, fetched one element ahead: v and the neighbour face layers into
   // registers, jd / dft into shared memory with cp.async (consumed by the point-wise pass)
   auto fetch_regs = [&](int e, double (&vr)[NV], double (&nr)[NL]) {
-    if (e >= s.n_local) return;
+    if (e >= s.e_hi) return;
     const double* ve = vin + size_t(e) * QQ;
 #pragma unroll
     for (int u = 0; u < NV; ++u) {
@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(32 * kJvWarps) jv2d_mma_kernel(DevSys s, const
     }
   };
   auto fetch_pw = [&](int e) {
-    if (e >= s.n_local) return;
+    if (e >= s.e_hi) return;
     const double* jd = s.jdet + size_t(e) * MM;
     const double* d0 = s.dft + size_t(e) * 2 * MM;
     for (int i = lane; i < MM; i += 32) cp_async8(spw + i, jd + i);
@@ -147,10 +147,10 @@ __global__ void __launch_bounds__(32 * kJvWarps) jv2d_mma_kernel(DevSys s, const
   };
   const int stride = gridDim.x * NW;
   double vr[NV], nr[NL];
-  int e = blockIdx.x * NW + warp;
+  int e = s.e_lo + blockIdx.x * NW + warp;
   fetch_regs(e, vr, nr);
   fetch_pw(e);
-  for (; e < s.n_local; e += stride) {
+  for (; e < s.e_hi; e += stride) {
     // face data of this element (registers; consumed after step 2)
     double fdm[NF], fdp[NF], ffw[NF];
     int fnb[NF], ffl[NF];
@@ -295,7 +295,7 @@ bool try_jv2d_mma(const DevSys& s, const double* vin, const double* halo, double
     TPDG_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     grid = std::max(1, per_sm) * sms;
   }
-  const int need = (s.n_local + L::warps - 1) / L::warps;
+  const int need = (s.e_hi - s.e_lo + L::warps - 1) / L::warps;
   jv2d_mma_kernel<Q, MU><<<std::min(grid, need), 32 * L::warps, smem, st>>>(s, vin, halo, vout);
   return true;
 }

@@ -48,19 +48,29 @@ struct HaloPlan {
   int e_begin = 0, e_end = 0, n_halo = 0;
   std::vector<int> conn;          // [n_local][2d][3]: neighbour -> local id (< n_local) or halo slot
   std::vector<int> halo_gid;      // global element id of each halo slot
+  // Face traces: what crosses ranks is, per cut face, the neighbour's face node layer (GL nodes: the
+  // trace is that layer, ops/discretization.hpp:89-97), n_c q^(d-1) doubles, not the element block.
   struct Peer {
     int rank = 0;
-    std::vector<int> send_local;  // local elements sent to this peer (ascending)
-    int recv_first = 0, recv_count = 0;  // halo slot range received from this peer
+    std::vector<int> send_elem, send_face;  // local element and face of each layer sent (ascending (gid, face))
+    std::vector<int> recv_slot, recv_face;  // halo slot and face of each layer received (same order)
   };
   std::vector<Peer> peers;
 };
 HaloPlan build_halo_plan(const tpdg_gpu_system* sys, int rank, int nranks, int e_begin, int e_end);
+// Element-block offset of node t of face f's node layer (t < q^(d-1); lower tangential axis fastest).
+__host__ __device__ inline int face_layer_index(int d, int q, int f, int t) {
+  const int axis = f / 2, layer = (f % 2) == 0 ? 0 : q - 1;
+  if (d == 2) return axis == 0 ? layer + q * t : t + q * layer;
+  const int u = t % q, v = t / q;
+  return axis == 0 ? layer + q * (u + q * v) : axis == 1 ? u + q * (layer + q * v) : u + q * (v + q * layer);
+}
 
 // ---------------------------------------------------------------- device views (POD, by value)
 // Discretization + linearization of the local elements, reference layouts.
 struct DevSys {
   int dim, n_c, q, mu, npe, nqv, nqf, n_local, n_halo;
+  int e_lo, e_hi;     // the launch processes local elements [e_lo, e_hi) (interior / boundary split)
   int small;          // BlockMode::small
   double a, b;        // mass / jacobian coefficients (ops/linearized.hpp:177-178)
   const double *g, *d, *gw, *dw, *w;

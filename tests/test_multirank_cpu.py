@@ -2,8 +2,9 @@
 plan the CUDA library uses for nranks > 1 (paper_1704_04549_b200/csrc/halo.cpp, exported through
 the C ABI), driven with the oracle as the per-rank compute:
 
-  * distributed Jv = halo exchange (torch.distributed send/recv of the planned element blocks) +
-    local operator apply; must equal the single-rank reference Jv bit for bit;
+  * distributed Jv = halo exchange (torch.distributed send/recv of the planned face node layers,
+    n_c q^(d-1) doubles per cut face; the rest of each halo block is NaN) + local operator apply;
+    must equal the single-rank reference Jv bit for bit;
   * distributed right-preconditioned MGS-GMRES with every dot product all-reduced (the structure of
     the multi-rank path in capi.cu: halo before each Jv, element-local KSVD apply, allreduce per
     MGS dot); must take the reference's iteration count.
@@ -48,17 +49,22 @@ def local_system(z, plan):
     return O.System(arrays)
 
 
-def exchange(plan, v_local, blk):
-    """Halo of one rank per the plan (the NCCL group of capi.cu's exchange_halo, over gloo)."""
-    halo = np.zeros(plan["n_halo"] * blk)
+def exchange(plan, v_local, nc, npe, dim, q):
+    """Halo of one rank per the plan (capi.cu's exchange_halo over gloo): the face node layers the
+    peers need cross ranks, n_c q^(d-1) values per cut face; everything else in the halo blocks is
+    NaN, so an operator that read beyond the layers would not reproduce the reference."""
+    L = q ** (dim - 1)
+    idx = [T.face_layer_nodes(dim, q, f) for f in range(2 * dim)]
+    halo = np.full(plan["n_halo"] * nc * npe, np.nan)
     reqs, bufs = [], []
     for p in plan["peers"]:
-        if len(p["send_local"]):
-            send = torch.from_numpy(np.concatenate([v_local[e * blk:(e + 1) * blk] for e in p["send_local"]]))
+        if len(p["send_pairs"]):
+            send = torch.from_numpy(np.concatenate([v_local[(e * nc + c) * npe + idx[f]]
+                                                    for e, f in p["send_pairs"] for c in range(nc)]))
             reqs.append(dist.isend(send, p["rank"]))
             bufs.append(send)
-        if p["recv_count"]:
-            recv = torch.zeros(p["recv_count"] * blk, dtype=torch.float64)
+        if len(p["recv_pairs"]):
+            recv = torch.zeros(len(p["recv_pairs"]) * nc * L, dtype=torch.float64)
             reqs.append(dist.irecv(recv, p["rank"]))
             bufs.append((p, recv))
     for r in reqs:
@@ -66,7 +72,10 @@ def exchange(plan, v_local, blk):
     for b in bufs:
         if isinstance(b, tuple):
             p, recv = b
-            halo[p["recv_first"] * blk:(p["recv_first"] + p["recv_count"]) * blk] = recv.numpy()
+            r = recv.numpy()
+            for k, (slot, f) in enumerate(p["recv_pairs"]):
+                for c in range(nc):
+                    halo[(slot * nc + c) * npe + idx[f]] = r[(k * nc + c) * L:(k * nc + c + 1) * L]
     return halo
 
 
@@ -136,7 +145,7 @@ def _worker(rank, world, port, case, q):
         a, b = loc.coeffs
 
         def jv(v_local):
-            ext = np.concatenate([v_local, exchange(plan, v_local, blk)])
+            ext = np.concatenate([v_local, exchange(plan, v_local, loc.n_c, loc.npe, loc.dim, loc.q)])
             out = np.zeros(v_local.size)
             O.lib().or_jv(O.C.byref(loc._or), O.C.c_double(a), O.C.c_double(b), loc.small, O.ptr(ext), O.ptr(out))
             return out
@@ -175,20 +184,33 @@ def test_two_rank_jv_pc_gmres(case):
 
 @pytest.mark.parametrize("nranks", [2, 3, 4, 8])
 def test_halo_plan_is_consistent(nranks):
-    """Every rank's receive list equals what its peers send, in the same order."""
+    """Every rank's received layers (halo element, face) are what its peers send, in the same order,
+    and they are exactly the faces the rank's elements see across the cut."""
     for case in ["cfg1", "adv3d_p4"]:
         z = O.load_raw(case)
         s = T.System.from_golden(z)
+        dim = s.dim
         plans = [T.halo_plan(s, r, nranks) for r in range(nranks)]
         E = int(z["meta"][4])
+        gconn = np.asarray(z["conn"]).reshape(E, 2 * dim, 3)
         assert plans[0]["e_begin"] == 0 and plans[-1]["e_end"] == E
         for r, p in enumerate(plans):
+            nl = p["e_end"] - p["e_begin"]
+            need = set()
+            for le in range(nl):
+                for f in range(2 * dim):
+                    nb, nf = int(gconn[p["e_begin"] + le, f, 0]), int(gconn[p["e_begin"] + le, f, 1])
+                    if nb >= 0 and not (p["e_begin"] <= nb < p["e_end"]):
+                        need.add((nb, nf))
+            got = set()
             for peer in p["peers"]:
                 other = plans[peer["rank"]]
                 back = [q for q in other["peers"] if q["rank"] == r]
-                recv_gids = p["halo_gid"][peer["recv_first"]:peer["recv_first"] + peer["recv_count"]]
-                sent = (back[0]["send_local"] + other["e_begin"]) if back else np.zeros(0, dtype=np.int32)
-                assert np.array_equal(recv_gids, sent)
+                recv = [(int(p["halo_gid"][slot]), int(f)) for slot, f in peer["recv_pairs"]]
+                sent = [(int(e) + other["e_begin"], int(f)) for e, f in back[0]["send_pairs"]] if back else []
+                assert recv == sent
+                got |= set(recv)
+            assert got == need
             conn = p["conn"].reshape(-1, 3)
             nl = p["e_end"] - p["e_begin"]
             assert conn[:, 0].max() < nl + p["n_halo"]
