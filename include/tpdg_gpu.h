@@ -197,6 +197,17 @@ int tpdg_gpu_build_cache_advection(tpdg_gpu_ctx ctx, int dim, int n_elements, in
 /* Test hook: the device libm of the formation (csrc/glibm.cuh, glibc 2.39's sin/cos/atan/atan2 as called by
  * standardize_2x2, tensor/schur.hpp:91-108) on n device arguments. fn: 0 sin, 1 cos, 2 atan, 3 atan2(x, y). */
 int tpdg_gpu_libm_eval(tpdg_gpu_ctx ctx, int fn, int64_t n, const double *d_x, const double *d_y, double *d_out);
+/* build_cache (ops/linearized.hpp:38-100) of the LLF Euler law (laws/euler.hpp:106-211) on the device from the
+ * nodal linearization state [e][c][node] and the quadrature-point geometry (adj [e][q][d][d], face_n
+ * [e][f][qf][d]); G is the reference element's (mu x p+1) interpolation matrix. TPDG_STATE on a
+ * non-physical state (check_state, euler.hpp:14-27). Single rank (neighbour states are local). */
+int tpdg_gpu_build_cache_euler(tpdg_gpu_ctx ctx, int dim, int p, int mu, int n_elements, const double *d_g,
+                               const double *d_state, const double *d_adj, const double *d_face_n,
+                               const int64_t *d_conn, double *d_dft, double *d_dfm, double *d_dfp);
+/* Euler stand-ins of BASELINE configs[2] (case 3: 2D, [0,10]^2) and configs[4] (case 5: 3D, [0,2pi]^3):
+ * geometry plus the interpolated nodal state (host_setup.cpp); the cache is left zero for the device. */
+int tpdg_setup_euler(int case_kind, int nx, int ny, int nz, int p, tpdg_setup *out);
+int tpdg_setup_state(tpdg_setup s, const double **state, int64_t *n);
 int tpdg_setup_destroy(tpdg_setup s);
 /* libstdc++ std::mt19937_64 + uniform_real_distribution(-scale, scale) (tests/support/test_rng.hpp) */
 int tpdg_uniform_vector(uint64_t seed, int64_t n, double scale, double *out);

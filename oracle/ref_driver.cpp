@@ -69,7 +69,9 @@ void dump_m(const std::string& dir, const std::string& name, const SmallMatrix& 
 // ---------------------------------------------------------------- cases
 struct CaseSpec {
   int dim = 2;
-  std::string law;            // adv_const | adv_swirl | adv_b | euler
+  std::string law;            // adv_const | adv_swirl | adv_b | euler | euler_cfg3 | euler_cfg5
+  double hi = 1.0;            // domain [0, hi]^d
+  int gmres_budget = 0;       // > 0: fixed GMRES iteration budget (history gate)
   double vel[3] = {1.0, 0.5, 0.0};
   int counts[3] = {1, 1, 1};
   int p = 1;
@@ -123,6 +125,21 @@ CaseSpec lookup(const std::string& name) {
   if (name == "euler3d") {
     c.dim = 3; c.law = "euler"; c.counts[0] = 2; c.counts[1] = 2; c.counts[2] = 1; c.p = 2;
     c.dt = 2.5e-3; c.rhs_scale = 1e-3; return c;
+  }
+  // Euler stand-ins of BASELINE configs[2] / configs[4] (LLF flux: the reference has no Roe flux and no
+  // BR2 viscous terms), states of host_setup.cpp's euler_state; reduced sizes with full dumps, and the
+  // configured sizes with a fixed GMRES budget (neither converges to 1e-10).
+  if (name == "cfg3s" || name == "cfg3") {
+    c.dim = 2; c.law = "euler_cfg3"; c.hi = 10.0; c.dt = 0.05; c.rhs_scale = 1e-3;
+    if (name == "cfg3s") { c.counts[0] = c.counts[1] = 4; c.p = 4; }
+    else { c.counts[0] = c.counts[1] = 32; c.p = 15; c.light = true; c.gmres_budget = 40; }
+    return c;
+  }
+  if (name == "cfg5s" || name == "cfg5") {
+    c.dim = 3; c.law = "euler_cfg5"; c.hi = 2.0 * M_PI; c.dt = 0.01; c.rhs_scale = 1e-3;
+    if (name == "cfg5s") { c.counts[0] = c.counts[1] = c.counts[2] = 2; c.p = 3; }
+    else { c.counts[0] = c.counts[1] = c.counts[2] = 8; c.p = 7; c.light = true; c.gmres_budget = 40; }
+    return c;
   }
   std::fprintf(stderr, "unknown case %s\n", name.c_str());
   std::exit(2);
@@ -179,6 +196,7 @@ Built build(const CaseSpec& c) {
   spec.amplitude = c.amplitude;
   spec.seed = c.mesh_seed;
   spec.periodic = c.periodic;
+  for (int a = 0; a < c.dim; ++a) spec.hi[a] = c.hi;
   auto mesh = generate_mesh(spec, ref);
   Law law;
   if (c.law == "adv_const") {
@@ -193,7 +211,7 @@ Built build(const CaseSpec& c) {
   } else if (c.law == "adv_b") {
     law = advection_law(AdvectionField::b);
   } else {
-    law = euler_law(c.dim);
+    law = euler_law(c.dim);  // also euler_cfg3 / euler_cfg5
   }
   Built b{make_discretization(std::move(ref), std::move(mesh), std::move(law)), StateVector()};
   if (c.law == "euler" && c.dim == 2) {
@@ -205,6 +223,32 @@ Built build(const CaseSpec& c) {
       const double p = 1.0 + 0.1 * std::cos(2.0 * M_PI * x[0]);
       u[0] = rho; u[1] = rho * vx; u[2] = rho * vy;
       u[3] = p / 0.4 + 0.5 * rho * (vx * vx + vy * vy);
+    });
+  } else if (c.law == "euler_cfg3") {
+    b.state = interpolate(b.sys, [](const double* x, double* u) {
+      const double gamma = 1.4;
+      const double dx = x[0] - 5.0, dy = x[1] - 5.0;
+      const double r2 = dx * dx + dy * dy;
+      const double rho = 1.0 + 0.2 * std::exp(-0.5 * r2);
+      const double sw = 0.5 * std::exp(0.5 * (1.0 - r2));
+      const double vx = 1.0 - sw * dy, vy = 1.0 + sw * dx;
+      const double pr = std::pow(rho, gamma);
+      u[0] = rho;
+      u[1] = rho * vx;
+      u[2] = rho * vy;
+      u[3] = pr / (gamma - 1.0) + 0.5 * rho * (vx * vx + vy * vy);
+    });
+  } else if (c.law == "euler_cfg5") {
+    b.state = interpolate(b.sys, [](const double* x, double* u) {
+      const double gamma = 1.4, mach = 0.1, p0 = 1.0 / (gamma * mach * mach);
+      const double vx = std::sin(x[0]) * std::cos(x[1]) * std::cos(x[2]);
+      const double vy = -std::cos(x[0]) * std::sin(x[1]) * std::cos(x[2]);
+      const double pr = p0 + (std::cos(2.0 * x[0]) + std::cos(2.0 * x[1])) * (std::cos(2.0 * x[2]) + 2.0) / 16.0;
+      u[0] = 1.0;
+      u[1] = vx;
+      u[2] = vy;
+      u[3] = 0.0;
+      u[4] = pr / (gamma - 1.0) + 0.5 * (vx * vx + vy * vy);
     });
   } else if (c.law == "euler") {
     // reference tests/unit/test_precond.cpp:266-273.
@@ -400,7 +444,7 @@ int run_golden(const std::string& name, const std::string& dir) {
   GmresResult gr;
   bool converged = true;
   try {
-    gr = gmres(op, pca, b, gmres_cfg(c.light ? 400 : 2000));
+    gr = gmres(op, pca, b, gmres_cfg(c.gmres_budget > 0 ? c.gmres_budget : c.light ? 400 : 2000));
   } catch (const GmresFailure& f) {
     gr = f.result;
     converged = false;

@@ -96,7 +96,8 @@ EXPORTS = [
     "tpdg_gpu_pc_import_factors", "tpdg_gpu_pc_import_record", "tpdg_gpu_form_block_jacobi", "tpdg_gpu_pc_destroy", "tpdg_gpu_pc_num_fallbacks", "tpdg_gpu_pc_fallbacks",
     "tpdg_gpu_pc_factor_len", "tpdg_gpu_pc_export_factors", "tpdg_gpu_pc_apply", "tpdg_gpu_pc_apply_host",
     "tpdg_gpu_gmres", "tpdg_gpu_gmres_host", "tpdg_setup_advection", "tpdg_setup_system", "tpdg_setup_destroy", "tpdg_setup_geometry",
-    "tpdg_gpu_build_cache_advection", "tpdg_gpu_libm_eval",
+    "tpdg_gpu_build_cache_advection", "tpdg_gpu_libm_eval", "tpdg_gpu_build_cache_euler", "tpdg_setup_euler",
+    "tpdg_setup_state",
     "tpdg_uniform_vector", "tpdg_seeded_unit_vector", "tpdg_halo_plan_create", "tpdg_halo_plan_query",
     "tpdg_halo_plan_conn", "tpdg_halo_plan_halo_gid", "tpdg_halo_plan_peer", "tpdg_halo_plan_destroy",
     "tpdg_gpu_loopback_create", "tpdg_gpu_loopback_destroy", "tpdg_gpu_ctx_create_loopback",
@@ -151,6 +152,9 @@ def lib():
                                 C.POINTER(C.c_int)],
         "tpdg_gpu_build_cache_advection": [v, C.c_int, C.c_int, C.c_int, C.c_int, v, v, v, v, v, C.c_int, dp, v, v, v],
         "tpdg_gpu_libm_eval": [v, C.c_int, C.c_int64, v, v, v],
+        "tpdg_gpu_build_cache_euler": [v, C.c_int, C.c_int, C.c_int, C.c_int, v, v, v, v, v, v, v, v],
+        "tpdg_setup_euler": [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(v)],
+        "tpdg_setup_state": [v, C.POINTER(dp), C.POINTER(C.c_int64)],
         "tpdg_uniform_vector": [C.c_uint64, C.c_int64, C.c_double, dp],
         "tpdg_seeded_unit_vector": [C.c_int64, C.c_uint64, dp],
         "tpdg_halo_plan_create": [C.POINTER(_System), C.c_int, C.c_int, C.POINTER(v)],
@@ -233,6 +237,37 @@ class System:
                        C.c_uint64(self.state_hash))
 
 
+def _system_from_setup(h, field, v):
+    s = _System()
+    _check(lib().tpdg_setup_system(h, C.byref(s)))
+    dim, nc = s.dim, s.n_c
+    q, mu = s.p + 1, s.mu
+    E = s.n_elements
+    nqv = mu ** dim
+    nqf = nqv // mu
+
+    def arr(ptr, n, dtype=np.float64):
+        return np.ctypeslib.as_array(ptr, shape=(n,)).astype(dtype, copy=True)
+
+    arrays = {"g": arr(s.g, mu * q), "d": arr(s.d, mu * q), "gw": arr(s.gw, mu * q), "dw": arr(s.dw, mu * q),
+              "w": arr(s.w, mu), "jdet": arr(s.jdet, E * nqv), "face_w": arr(s.face_w, E * 2 * dim * nqf),
+              "conn": arr(s.conn, E * 2 * dim * 3, np.int64), "dft": arr(s.dft, E * dim * nqv * nc * nc),
+              "dfm": arr(s.dfm, E * 2 * dim * nqf * nc * nc), "dfp": arr(s.dfp, E * 2 * dim * nqf * nc * nc)}
+    sysm = System(dim, nc, s.p, mu, E, arrays, s.state_hash)
+    ga, gx, gn, gf = dp(), dp(), dp(), dp()
+    nv, nf = C.c_int(), C.c_int()
+    _check(lib().tpdg_setup_geometry(h, C.byref(ga), C.byref(gx), C.byref(gn), C.byref(gf), C.byref(nv),
+                                     C.byref(nf)))
+    sysm.geometry = {"adj": arr(ga, E * nv.value * dim * dim), "vol_x": arr(gx, E * nv.value * dim),
+                     "face_n": arr(gn, E * 2 * dim * nf.value * dim), "face_x": arr(gf, E * 2 * dim * nf.value * dim),
+                     "field": field, "vel": np.array([v[0], v[1], v[2] if dim == 3 else 0.0])}
+    if nc > 1:
+        sp, ns = dp(), C.c_int64()
+        _check(lib().tpdg_setup_state(h, C.byref(sp), C.byref(ns)))
+        sysm.state = arr(sp, ns.value)
+    return sysm
+
+
 def setup_advection(kind, nx, ny=None, nz=1, p=1, vel=(1.0, 0.5, 0.0), periodic=True):
     """Host input production for the BASELINE advection configs.
 
@@ -243,34 +278,51 @@ def setup_advection(kind, nx, ny=None, nz=1, p=1, vel=(1.0, 0.5, 0.0), periodic=
     v = np.asarray(vel, dtype=np.float64)
     _check(lib().tpdg_setup_advection(k, _ptr(v), nx, ny, nz, p, int(periodic), C.byref(h)))
     try:
-        s = _System()
-        _check(lib().tpdg_setup_system(h, C.byref(s)))
-        dim = s.dim
-        q, mu = s.p + 1, s.mu
-        E = s.n_elements
-        nqv = mu ** dim
-        nqf = nqv // mu
-        npe = q ** dim
-
-        def arr(ptr, n, dtype=np.float64):
-            return np.ctypeslib.as_array(ptr, shape=(n,)).astype(dtype, copy=True)
-
-        arrays = {"g": arr(s.g, mu * q), "d": arr(s.d, mu * q), "gw": arr(s.gw, mu * q), "dw": arr(s.dw, mu * q),
-                  "w": arr(s.w, mu), "jdet": arr(s.jdet, E * nqv), "face_w": arr(s.face_w, E * 2 * dim * nqf),
-                  "conn": arr(s.conn, E * 2 * dim * 3, np.int64), "dft": arr(s.dft, E * dim * nqv),
-                  "dfm": arr(s.dfm, E * 2 * dim * nqf), "dfp": arr(s.dfp, E * 2 * dim * nqf)}
-        del npe
-        sysm = System(dim, 1, s.p, mu, E, arrays, s.state_hash)
-        ga, gx, gn, gf = dp(), dp(), dp(), dp()
-        nv, nf = C.c_int(), C.c_int()
-        _check(lib().tpdg_setup_geometry(h, C.byref(ga), C.byref(gx), C.byref(gn), C.byref(gf), C.byref(nv),
-                                         C.byref(nf)))
-        sysm.geometry = {"adj": arr(ga, E * nv.value * dim * dim), "vol_x": arr(gx, E * nv.value * dim),
-                         "face_n": arr(gn, E * 2 * dim * nf.value * dim), "face_x": arr(gf, E * 2 * dim * nf.value * dim),
-                         "field": k, "vel": np.array([v[0], v[1], v[2] if dim == 3 else 0.0])}
-        return sysm
+        return _system_from_setup(h, k, v)
     finally:
         lib().tpdg_setup_destroy(h)
+
+
+def setup_euler(case, nx, ny=None, nz=1, p=1):
+    """Euler stand-ins of BASELINE configs[2] ("cfg3": 2D, [0,10]^2, Gaussian density + swirl, p = rho^gamma)
+    and configs[4] ("cfg5": 3D Taylor-Green on [0,2pi]^3, Mach 0.1), LLF flux (the reference's euler_law; the
+    Roe flux of cfg3 and the BR2 viscous terms of cfg5 have no reference implementation). Returns a System with
+    the interpolated nodal state in .state and a zero cache: fill it with build_euler_cache."""
+    k = {"cfg3": 3, "cfg5": 5}[case]
+    ny = nx if ny is None else ny
+    h = C.c_void_p()
+    _check(lib().tpdg_setup_euler(k, nx, ny, nz, p, C.byref(h)))
+    try:
+        return _system_from_setup(h, k, np.zeros(3))
+    finally:
+        lib().tpdg_setup_destroy(h)
+
+
+def build_euler_cache(ctx: "Context", sysm: "System", state=None):
+    """build_cache (ops/linearized.hpp:38-100) of the LLF Euler law on the device; stores host copies of
+    (dft, dfm, dfp) in sysm.arrays and returns them."""
+    import torch
+    g = sysm.geometry
+    dim, E, mu, q = sysm.dim, sysm.n_elements, sysm.mu, sysm.q
+    nc = sysm.n_c
+    nvol, nface = mu ** dim, mu ** (dim - 1)
+    dev = torch.device("cuda", ctx.device)
+    st = np.ascontiguousarray(sysm.state if state is None else state, dtype=np.float64)
+    t = {k: torch.from_numpy(np.ascontiguousarray(g[k])).to(dev) for k in ("adj", "face_n")}
+    dg = torch.from_numpy(np.ascontiguousarray(sysm.arrays["g"])).to(dev)
+    dst = torch.from_numpy(st).to(dev)
+    conn = torch.from_numpy(sysm.arrays["conn"]).to(dev)
+    dft = torch.zeros(E * dim * nvol * nc * nc, dtype=torch.float64, device=dev)
+    dfm = torch.zeros(E * 2 * dim * nface * nc * nc, dtype=torch.float64, device=dev)
+    dfp = torch.zeros_like(dfm)
+    _check(lib().tpdg_gpu_build_cache_euler(ctx.h, dim, q - 1, mu, E, C.c_void_p(dg.data_ptr()),
+                                            C.c_void_p(dst.data_ptr()), C.c_void_p(t["adj"].data_ptr()),
+                                            C.c_void_p(t["face_n"].data_ptr()), C.c_void_p(conn.data_ptr()),
+                                            C.c_void_p(dft.data_ptr()), C.c_void_p(dfm.data_ptr()),
+                                            C.c_void_p(dfp.data_ptr())))
+    out = dft.cpu().numpy(), dfm.cpu().numpy(), dfp.cpu().numpy()
+    sysm.arrays["dft"], sysm.arrays["dfm"], sysm.arrays["dfp"] = out
+    return out
 
 
 def build_advection_cache(ctx: "Context", sysm: "System"):

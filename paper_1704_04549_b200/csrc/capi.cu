@@ -1388,6 +1388,44 @@ int tpdg_gpu_libm_eval(tpdg_gpu_ctx ctx, int fn, int64_t n, const double* d_x, c
   });
 }
 
+int tpdg_gpu_build_cache_euler(tpdg_gpu_ctx ctx, int dim, int p, int mu, int n_elements, const double* d_g,
+                               const double* d_state, const double* d_adj, const double* d_face_n,
+                               const int64_t* d_conn, double* d_dft, double* d_dfm, double* d_dfp) {
+  return guarded([&] {
+    REQUIRE(ctx && d_g && d_state && d_adj && d_face_n && d_conn && d_dft && d_dfm && d_dfp, TPDG_CONFIG,
+            "build_cache_euler: null argument");
+    REQUIRE((dim == 2 || dim == 3) && p >= 1 && mu >= 1 && n_elements >= 0, TPDG_CONFIG, "build_cache_euler: bad shape");
+    DevBuf st;
+    st.alloc(sizeof(int));
+    TPDG_CUDA_CHECK(cudaMemsetAsync(st.p, 0, sizeof(int), ctx->stream));
+    launch_build_cache_euler(dim, p + 1, mu, n_elements, d_g, d_state, d_adj, d_face_n, d_conn, d_dft, d_dfm, d_dfp,
+                             st.as<int>(), ctx->stream);
+    int bad = 0;
+    TPDG_CUDA_CHECK(cudaMemcpyAsync(&bad, st.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    TPDG_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    // euler_detail::check_state (laws/euler.hpp:14-27)
+    REQUIRE(bad == 0, TPDG_STATE, "euler: non-physical state (rho <= 0 or p <= 0) in the linearization state");
+  });
+}
+
+int tpdg_setup_euler(int case_kind, int nx, int ny, int nz, int p, tpdg_setup* out) {
+  return guarded([&] {
+    REQUIRE(case_kind == 3 || case_kind == 5, TPDG_CONFIG, "setup_euler: case_kind must be 3 (cfg3) or 5 (cfg5)");
+    REQUIRE(nx >= 1 && ny >= 1 && (case_kind != 5 || nz >= 1) && p >= 1, TPDG_CONFIG, "setup_euler: bad sizes");
+    std::unique_ptr<tpdg_setup_s> s(new tpdg_setup_s);
+    const double zero[3] = {0, 0, 0};
+    setup_advection(case_kind, zero, nx, ny, nz, p, 1, s->s);
+    *out = s.release();
+  });
+}
+
+int tpdg_setup_state(tpdg_setup st, const double** state, int64_t* n) {
+  return guarded([&] {
+    *state = st->s.state.data();
+    *n = int64_t(st->s.state.size());
+  });
+}
+
 int tpdg_setup_system(tpdg_setup st, tpdg_gpu_system* sys) {
   return guarded([&] {
     const Setup& s = st->s;

@@ -175,8 +175,44 @@ void face_tangents(int dim, int axis, int* t) {
 
 } // namespace
 
+namespace {
+// Linearization states of the Euler stand-ins (BASELINE.json configs[2] / configs[4], inviscid): the
+// reference interpolates a pointwise state onto the nodes (ops/discretization.hpp:356-375). cfg3:
+// rho = 1 + 0.2 exp(-r^2/2) about the centre of [0,10]^2, velocity (1, 1) plus the tangential swirl
+// 0.5 r exp((1 - r^2)/2), pressure from the isentropic relation p = rho^gamma. cfg5: Taylor-Green on
+// [0, 2 pi]^3 at Mach 0.1 (rho = 1, p0 = 1 / (gamma M^2)). gamma = 1.4. The same expressions are in
+// oracle/ref_driver.cpp (the reference's own interpolate), so the states agree bit for bit.
+void euler_state(int kind, const double* x, double* u) {
+  const double gamma = 1.4;
+  if (kind == 3) {
+    const double dx = x[0] - 5.0, dy = x[1] - 5.0;
+    const double r2 = dx * dx + dy * dy;
+    const double rho = 1.0 + 0.2 * std::exp(-0.5 * r2);
+    const double sw = 0.5 * std::exp(0.5 * (1.0 - r2));  // swirl speed / r
+    const double vx = 1.0 - sw * dy, vy = 1.0 + sw * dx;
+    const double pr = std::pow(rho, gamma);
+    u[0] = rho;
+    u[1] = rho * vx;
+    u[2] = rho * vy;
+    u[3] = pr / (gamma - 1.0) + 0.5 * rho * (vx * vx + vy * vy);
+  } else {
+    const double mach = 0.1, p0 = 1.0 / (gamma * mach * mach);
+    const double vx = std::sin(x[0]) * std::cos(x[1]) * std::cos(x[2]);
+    const double vy = -std::cos(x[0]) * std::sin(x[1]) * std::cos(x[2]);
+    const double pr = p0 + (std::cos(2.0 * x[0]) + std::cos(2.0 * x[1])) * (std::cos(2.0 * x[2]) + 2.0) / 16.0;
+    u[0] = 1.0;
+    u[1] = vx;
+    u[2] = vy;
+    u[3] = 0.0;
+    u[4] = pr / (gamma - 1.0) + 0.5 * (vx * vx + vy * vy);
+  }
+}
+} // namespace
+
 int setup_advection(int kind, const double* vel, int nx, int ny, int nz, int p, int periodic, Setup& S) {
-  const int dim = kind == 2 ? 3 : 2;
+  const bool euler = kind == 3 || kind == 5;
+  const int dim = kind == 2 || kind == 5 ? 3 : 2;
+  const double lo = 0.0, hi = kind == 3 ? 10.0 : kind == 5 ? 2.0 * M_PI : 1.0;
   const int n = p + 1, mu = p + 2;
   S.dim = dim;
   S.n_c = 1;
@@ -205,13 +241,13 @@ int setup_advection(int kind, const double* vel, int nx, int ny, int nz, int p, 
   const int cnt[3] = {nx, ny, dim == 3 ? nz : 1};
   const int nv[3] = {nx + 1, ny + 1, dim == 3 ? nz + 1 : 1};
   double h[3] = {1.0, 1.0, 1.0};
-  for (int a = 0; a < dim; ++a) h[a] = (1.0 - 0.0) / cnt[a];
+  for (int a = 0; a < dim; ++a) h[a] = (hi - lo) / cnt[a];
   G.nodes.resize(std::size_t(nv[0]) * nv[1] * nv[2]);
   for (int k = 0; k < nv[2]; ++k)
     for (int j = 0; j < nv[1]; ++j)
       for (int i = 0; i < nv[0]; ++i)
-        G.nodes[(std::size_t(k) * nv[1] + j) * nv[0] + i] = {0.0 + i * h[0], 0.0 + j * h[1],
-                                                             dim == 3 ? 0.0 + k * h[2] : 0.0};
+        G.nodes[(std::size_t(k) * nv[1] + j) * nv[0] + i] = {lo + i * h[0], lo + j * h[1],
+                                                             dim == 3 ? lo + k * h[2] : 0.0};
   const int E = cnt[0] * cnt[1] * cnt[2];
   S.n_elements = E;
   G.n_elements = E;
@@ -303,6 +339,35 @@ int setup_advection(int kind, const double* vel, int nx, int ny, int nz, int p, 
   S.adj = adj;
   S.face_n = face_n;
   S.face_x = face_x;
+  if (euler) {  // nodal linearization state (ops/discretization.hpp:356-375); the cache is built on the device
+    const int nc = dim + 2, npe = dim == 2 ? n * n : n * n * n;
+    S.n_c = nc;
+    S.state.assign(std::size_t(E) * nc * npe, 0.0);
+    double u[5];
+    for (int e = 0; e < E; ++e)
+      for (int qn = 0; qn < npe; ++qn) {
+        int rem = qn;
+        for (int a = 0; a < dim; ++a) {
+          xi[a] = nodes[rem % n];
+          rem /= n;
+        }
+        G.map_point(e, xi, x);
+        euler_state(kind, x, u);
+        for (int c = 0; c < nc; ++c) S.state[(std::size_t(e) * nc + c) * npe + qn] = u[c];
+      }
+    S.dft.assign(std::size_t(E) * dim * nvol * nc * nc, 0.0);
+    S.dfm.assign(std::size_t(E) * 2 * dim * nface * nc * nc, 0.0);
+    S.dfp.assign(S.dfm.size(), 0.0);
+    // FNV-1a of the state bytes (ops/state.hpp:52-61)
+    std::uint64_t hsh = 1469598103934665603ULL;
+    const unsigned char* bytes = reinterpret_cast<const unsigned char*>(S.state.data());
+    for (std::size_t i = 0; i < S.state.size() * sizeof(double); ++i) {
+      hsh ^= bytes[i];
+      hsh *= 1099511628211ULL;
+    }
+    S.state_hash = hsh;
+    return TPDG_OK;
+  }
   // ---- linearization cache of scalar upwind advection (ops/linearized.hpp:38-100)
   auto velocity = [&](const double* xx, double* v) {
     if (kind == 1) {

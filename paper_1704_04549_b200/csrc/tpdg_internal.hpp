@@ -30,6 +30,7 @@ struct Setup {
   int dim = 2, n_c = 1, p = 1, mu = 3, n_elements = 0;
   std::vector<double> g, d, gw, dw, w, qpoints, jdet, face_w, dft, dfm, dfp, vol_x;
   std::vector<double> adj, face_n, face_x;  // geometry at the quadrature points (build_cache inputs)
+  std::vector<double> state;                // nodal linearization state (Euler stand-ins) [e][c][node]
   std::vector<int64_t> conn;
   uint64_t state_hash = 0;
 };
@@ -37,6 +38,10 @@ int setup_advection(int kind, const double* vel, int nx, int ny, int nz, int p, 
 void uniform_vector(uint64_t seed, int64_t n, double scale, double* out);
 // build_cache of scalar upwind advection on the device (cache.cu); device pointers
 void launch_libm_eval(int fn, int64_t n, const double* x, const double* y, double* out, cudaStream_t st);
+// build_cache of the LLF Euler law (laws/euler.hpp) on the device from the nodal state
+void launch_build_cache_euler(int dim, int q, int mu, int n_elements, const double* g, const double* state,
+                              const double* adj, const double* face_n, const int64_t* conn, double* dft, double* dfm,
+                              double* dfp, int* status, cudaStream_t st);
 void launch_build_cache_advection(int dim, int n_elements, int nvol, int nface, const double* adj,
                                   const double* vol_x, const double* face_n, const double* face_x,
                                   const int64_t* conn, int field, const double* vel, double* dft, double* dfm,

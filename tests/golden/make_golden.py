@@ -21,7 +21,9 @@ ROOT = os.path.dirname(os.path.dirname(HERE))
 CASES = ["cfg1", "cfg2s_p4", "cfg2s_p8", "cfg2s_p15", "pert2d", "adv3d_p3", "adv3d_p4",
          "euler2d", "euler2d_small", "euler3d",
          # full-size BASELINE configs: fallback decisions + GMRES counts/histories only
-         "cfg2_p4", "cfg2_p8", "cfg2_p15", "cfg2_p20", "cfg2_p30", "cfg4"]
+         "cfg2_p4", "cfg2_p8", "cfg2_p15", "cfg2_p20", "cfg2_p30", "cfg4",
+         # Euler stand-ins of configs[2] / configs[4] (LLF): reduced sizes, then fixed-budget histories at size
+         "cfg3s", "cfg5s", "cfg3", "cfg5"]
 
 
 def main(argv):

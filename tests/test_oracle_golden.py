@@ -11,7 +11,7 @@ import pytest
 import _oracle as O
 
 SMALL = ["cfg1", "cfg2s_p4", "cfg2s_p8", "cfg2s_p15", "pert2d", "adv3d_p3", "adv3d_p4",
-         "euler2d", "euler2d_small", "euler3d"]
+         "euler2d", "euler2d_small", "euler3d", "cfg3s", "cfg5s"]
 
 
 @pytest.fixture(scope="module", params=SMALL)
