@@ -204,6 +204,22 @@ int tpdg_gpu_libm_eval(tpdg_gpu_ctx ctx, int fn, int64_t n, const double *d_x, c
 int tpdg_gpu_build_cache_euler(tpdg_gpu_ctx ctx, int dim, int p, int mu, int n_elements, const double *d_g,
                                const double *d_state, const double *d_adj, const double *d_face_n,
                                const int64_t *d_conn, double *d_dft, double *d_dfm, double *d_dfp);
+/* residual r(u, t) (ops/discretization.hpp:188-254) of the LLF Euler law on the device (device pointers,
+ * global mesh, single rank). TPDG_STATE on a non-physical state. */
+int tpdg_gpu_residual_euler(tpdg_gpu_ctx ctx, int dim, int p, int mu, int n_elements, const double *d_g,
+                            const double *d_gw, const double *d_dw, const double *d_state, const double *d_adj,
+                            const double *d_face_n, const double *d_face_w, const int64_t *d_conn, double *d_out);
+/* One backward Euler step of the Euler law by Newton-GMRES with the KSVD preconditioner, everything on the
+ * device (step_backward_euler, solve/time_step.hpp:136-146; newton, solve/newton.hpp:32-68;
+ * newton_linear_solve, time_step.hpp:57-122): per Newton step the linearization cache is rebuilt at the
+ * iterate, the preconditioner formed, GMRES run on -G(w), G(w) = M (w - u) - dt r(w). h_u: u in, u' out
+ * (host, [e][c][node]); newton_tol / max_iterations / floor as NewtonConfig; statistics per solve are
+ * written up to cap entries (residual_norms: cap + 1). TPDG_CONVERGENCE on the reference's failure modes. */
+int tpdg_gpu_step_backward_euler(tpdg_gpu_ctx ctx, const tpdg_gpu_system *sys, const double *h_adj,
+                                 const double *h_face_n, double *h_u, double dt, double newton_tol,
+                                 int newton_max_iterations, double newton_floor, const tpdg_gpu_gmres_config *gcfg,
+                                 const tpdg_gpu_ksvd_config *kcfg, int block_mode, int *newton_steps,
+                                 int *gmres_per_solve, double *residual_norms, int cap);
 /* Euler stand-ins of BASELINE configs[2] (case 3: 2D, [0,10]^2) and configs[4] (case 5: 3D, [0,2pi]^3):
  * geometry plus the interpolated nodal state (host_setup.cpp); the cache is left zero for the device. */
 int tpdg_setup_euler(int case_kind, int nx, int ny, int nz, int p, tpdg_setup *out);

@@ -29,6 +29,7 @@
 #include "tpdg/laws/euler.hpp"
 #include "tpdg/precond/ksvd.hpp"
 #include "tpdg/solve/gmres.hpp"
+#include "tpdg/solve/time_step.hpp"
 
 using namespace tpdg;
 
@@ -395,6 +396,31 @@ int run_golden(const std::string& name, const std::string& dir) {
       dump(dir, "start_vec", detail::seeded_unit_vector(n2d, 0x5eedULL));
       if (d == 3) dump(dir, "start_vec2", detail::seeded_unit_vector(long(q) * q, 0x5eedULL));
     }
+  }
+
+  if (!c.light && c.law.rfind("euler_cfg", 0) == 0) {
+    // residual r(u, t) (ops/discretization.hpp:188-254) at the linearization state, M v on the seeded vector
+    // (mass_apply), and one backward Euler step by Newton-GMRES with the KSVD preconditioner
+    // (solve/time_step.hpp:126-146, newton.hpp:32-68): GMRES(30) to 1e-10, Newton defaults.
+    dump(dir, "resid", residual(sys, bt.state, 0.0).data);
+    {
+      StateVector v = sys.make_state();
+      v.data = uniform_vector(1001, N, 1.0);
+      dump(dir, "mass_out", mass_apply(sys, v).data);
+    }
+    ImplicitConfig icfg;
+    icfg.gmres = gmres_cfg(2000);
+    icfg.precond = c.mode == BlockMode::full ? PrecondKind::ksvd_full : PrecondKind::ksvd_small;
+    StepStats st;
+    st.keep_residual_history = true;
+    const StateVector u1 = step_backward_euler(sys, bt.state, 0.0, c.dt, icfg, &st);
+    dump(dir, "newton_state", u1.data);
+    std::vector<double> gits(st.gmres_per_solve.begin(), st.gmres_per_solve.end());
+    dump(dir, "newton_gmres", gits);
+    dump(dir, "newton_steps", {double(st.newton_steps)});
+    std::printf("%s: newton steps %d, gmres per solve:", name.c_str(), st.newton_steps);
+    for (int g : st.gmres_per_solve) std::printf(" %d", g);
+    std::printf("\n");
   }
 
   const PcHolder pc = form(lin, d, c.mode);

@@ -97,7 +97,7 @@ EXPORTS = [
     "tpdg_gpu_pc_factor_len", "tpdg_gpu_pc_export_factors", "tpdg_gpu_pc_apply", "tpdg_gpu_pc_apply_host",
     "tpdg_gpu_gmres", "tpdg_gpu_gmres_host", "tpdg_setup_advection", "tpdg_setup_system", "tpdg_setup_destroy", "tpdg_setup_geometry",
     "tpdg_gpu_build_cache_advection", "tpdg_gpu_libm_eval", "tpdg_gpu_build_cache_euler", "tpdg_setup_euler",
-    "tpdg_setup_state",
+    "tpdg_setup_state", "tpdg_gpu_residual_euler", "tpdg_gpu_step_backward_euler",
     "tpdg_uniform_vector", "tpdg_seeded_unit_vector", "tpdg_halo_plan_create", "tpdg_halo_plan_query",
     "tpdg_halo_plan_conn", "tpdg_halo_plan_halo_gid", "tpdg_halo_plan_peer", "tpdg_halo_plan_destroy",
     "tpdg_gpu_loopback_create", "tpdg_gpu_loopback_destroy", "tpdg_gpu_ctx_create_loopback",
@@ -155,6 +155,10 @@ def lib():
         "tpdg_gpu_build_cache_euler": [v, C.c_int, C.c_int, C.c_int, C.c_int, v, v, v, v, v, v, v, v],
         "tpdg_setup_euler": [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(v)],
         "tpdg_setup_state": [v, C.POINTER(dp), C.POINTER(C.c_int64)],
+        "tpdg_gpu_residual_euler": [v, C.c_int, C.c_int, C.c_int, C.c_int, v, v, v, v, v, v, v, v, v],
+        "tpdg_gpu_step_backward_euler": [v, C.POINTER(_System), dp, dp, dp, C.c_double, C.c_double, C.c_int,
+                                         C.c_double, C.POINTER(_GmresCfg), C.POINTER(_KsvdCfg), C.c_int,
+                                         C.POINTER(C.c_int), C.POINTER(C.c_int), dp, C.c_int],
         "tpdg_uniform_vector": [C.c_uint64, C.c_int64, C.c_double, dp],
         "tpdg_seeded_unit_vector": [C.c_int64, C.c_uint64, dp],
         "tpdg_halo_plan_create": [C.POINTER(_System), C.c_int, C.c_int, C.POINTER(v)],
@@ -344,6 +348,67 @@ def build_advection_cache(ctx: "Context", sysm: "System"):
                                                 int(g["field"]), _ptr(vel), C.c_void_p(dft.data_ptr()),
                                                 C.c_void_p(dfm.data_ptr()), C.c_void_p(dfp.data_ptr())))
     return dft.cpu().numpy(), dfm.cpu().numpy(), dfp.cpu().numpy()
+
+
+def residual_euler(ctx: "Context", sysm: "System", state=None) -> np.ndarray:
+    """residual r(u, t) (ops/discretization.hpp:188-254) of the LLF Euler law on the device (host in/out)."""
+    import torch
+    g = sysm.geometry
+    dev = torch.device("cuda", ctx.device)
+    t = {k: torch.from_numpy(np.ascontiguousarray(v)).to(dev) for k, v in
+         (("g", sysm.arrays["g"]), ("gw", sysm.arrays["gw"]), ("dw", sysm.arrays["dw"]), ("adj", g["adj"]),
+          ("face_n", g["face_n"]), ("face_w", sysm.arrays["face_w"]), ("conn", sysm.arrays["conn"]),
+          ("state", sysm.state if state is None else np.asarray(state, dtype=np.float64)))}
+    out = torch.empty_like(t["state"])
+    _check(lib().tpdg_gpu_residual_euler(ctx.h, sysm.dim, sysm.p, sysm.mu, sysm.n_elements,
+                                         *(C.c_void_p(t[k].data_ptr()) for k in
+                                           ("g", "gw", "dw", "state", "adj", "face_n", "face_w", "conn")),
+                                         C.c_void_p(out.data_ptr())))
+    return out.cpu().numpy()
+
+
+@dataclass
+class NewtonConfig:
+    """NewtonConfig (solve/newton.hpp:11-21)."""
+    tol: float = 1e-8
+    max_iterations: int = 30
+    absolute_floor: float = 1e-14
+
+
+@dataclass
+class StepStats:
+    newton_steps: int = 0
+    gmres_per_solve: list = field(default_factory=list)
+    residual_norms: list = field(default_factory=list)
+
+
+def step_backward_euler(ctx: "Context", sysm: "System", u, dt: float, gmres_cfg: "GmresConfig | None" = None,
+                        newton_cfg: NewtonConfig | None = None, ksvd_cfg: "KsvdConfig | None" = None,
+                        block_mode="full"):
+    """One backward Euler step of the Euler law by Newton-GMRES with the KSVD preconditioner on the device
+    (step_backward_euler, solve/time_step.hpp:136-146). Returns (u', StepStats)."""
+    gmres_cfg = gmres_cfg or GmresConfig(tol=1e-10, restart=30, max_iterations=2000)
+    newton_cfg = newton_cfg or NewtonConfig()
+    ksvd_cfg = ksvd_cfg or KsvdConfig()
+    uu = np.array(u, dtype=np.float64, copy=True)
+    g = sysm.geometry
+    adj = np.ascontiguousarray(g["adj"])
+    fn = np.ascontiguousarray(g["face_n"])
+    cap = newton_cfg.max_iterations + 1
+    gits = np.zeros(cap, dtype=np.int32)
+    norms = np.zeros(cap + 1)
+    steps = C.c_int()
+    gc = _gcfg(gmres_cfg)
+    kc = _KsvdCfg(ksvd_cfg.terms, ksvd_cfg.lanczos_max_it, ksvd_cfg.breakdown_tol, C.c_uint64(ksvd_cfg.seed),
+                  ksvd_cfg.degenerate_tol)
+    cs = sysm._c()
+    _check(lib().tpdg_gpu_step_backward_euler(ctx.h, C.byref(cs), _ptr(adj), _ptr(fn), _ptr(uu), C.c_double(dt),
+                                              C.c_double(newton_cfg.tol), newton_cfg.max_iterations,
+                                              C.c_double(newton_cfg.absolute_floor), C.byref(gc), C.byref(kc),
+                                              {"full": 0, "small": 1}[block_mode], C.byref(steps),
+                                              gits.ctypes.data_as(C.POINTER(C.c_int)), _ptr(norms), cap))
+    n = steps.value
+    return uu, StepStats(n, [int(x) for x in gits[:n]], [float(x) for x in norms[:n + 1]])
 
 
 def libm_eval(ctx: "Context", fn: str, x, y=None) -> np.ndarray:

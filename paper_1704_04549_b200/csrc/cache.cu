@@ -290,6 +290,202 @@ __global__ void cache_euler_kernel(int d, int q, int mu, const double* __restric
   }
 }
 
+// ------------------------------------------------------------------ residual r(u, t) of the Euler law
+// ops/discretization.hpp:188-254: volume fluxes contracted with the adjugate and integrated against the
+// test-function gradients (integrate_back, kernels.hpp:82-104), minus the lifted LLF numerical flux
+// (face_lift, discretization.hpp:133-166). Per output entry the reference's accumulation sequence:
+// out = 0; += the d volume terms (k ascending); += the 2d face lifts (f ascending).
+__device__ void eu_flux(int d, const double* u, double* f) {  // laws/euler.hpp:125-136, F[dir][c]
+  const int nc = d + 2;
+  const double inv_rho = 1.0 / u[0];
+  const double p = eu_pressure(d, u);
+  for (int dir = 0; dir < d; ++dir) {
+    const double vd = u[1 + dir] * inv_rho;
+    double* fd = f + dir * nc;
+    fd[0] = u[1 + dir];
+    for (int i = 0; i < d; ++i) fd[1 + i] = u[1 + i] * vd;
+    fd[1 + dir] += p;
+    fd[nc - 1] = (u[nc - 1] + p) * vd;
+  }
+}
+__device__ void eu_num_flux(int d, const double* um, const double* up, const double* n, double* fhat) {
+  const int nc = d + 2;  // laws/euler.hpp:138-162
+  const double sm = eu_wave_speed(d, um, n, nullptr), sp = eu_wave_speed(d, up, n, nullptr);
+  const double lam = sm > sp ? sm : sp;
+  double fm[5], fp[5];
+  const double invm = 1.0 / um[0], invp = 1.0 / up[0];
+  const double pm = eu_pressure(d, um), pp = eu_pressure(d, up);
+  for (int c = 0; c < nc; ++c) fhat[c] = 0.0;
+  for (int dir = 0; dir < d; ++dir) {
+    const double vdm = um[1 + dir] * invm, vdp = up[1 + dir] * invp;
+    fm[0] = um[1 + dir];
+    fp[0] = up[1 + dir];
+    for (int i = 0; i < d; ++i) {
+      fm[1 + i] = um[1 + i] * vdm;
+      fp[1 + i] = up[1 + i] * vdp;
+    }
+    fm[1 + dir] += pm;
+    fp[1 + dir] += pp;
+    fm[nc - 1] = (um[nc - 1] + pm) * vdm;
+    fp[nc - 1] = (up[nc - 1] + pp) * vdp;
+    for (int c = 0; c < nc; ++c) fhat[c] += 0.5 * n[dir] * (fm[c] + fp[c]);
+  }
+  for (int c = 0; c < nc; ++c) fhat[c] += 0.5 * lam * (um[c] - up[c]);
+}
+
+// One element per CTA. Shared: vals [c][nqv] (reused for ft), scratch, out [c][npe], face buffers.
+__global__ void residual_euler_kernel(int d, int q, int mu, const double* __restrict__ g,
+                                      const double* __restrict__ gw, const double* __restrict__ dw,
+                                      const double* __restrict__ state, const double* __restrict__ adj,
+                                      const double* __restrict__ face_n, const double* __restrict__ face_w,
+                                      const int64_t* __restrict__ conn, double* __restrict__ out, int* status) {
+  extern __shared__ double rs[];
+  const int e = blockIdx.x, nc = d + 2;
+  const int npe = d == 2 ? q * q : q * q * q, nqv = d == 2 ? mu * mu : mu * mu * mu, nqf = nqv / mu;
+  double* vals = rs;                 // [c][nqv]
+  double* ft = vals + nc * nqv;      // [k][c][nqv]
+  double* w1 = ft + d * nc * nqv;    // mu q^2 (>= q mu^2 for the back integration)
+  double* w2 = w1 + mu * mu * q;     // mu^2 q
+  double* acc = w2 + mu * mu * q;    // [c][npe]
+  double* lift = acc + nc * npe;     // [c][nqf]
+  double* tr = lift + nc * nqf;      // [side][c][nqf]
+  const double* ue = state + size_t(e) * nc * npe;
+  for (int c = 0; c < nc; ++c) {  // eval_at_quad
+    const double* coeff = ue + size_t(c) * npe;
+    if (d == 2) {
+      eu_axis_apply(g, mu, q, 1, q, coeff, w1);
+      __syncthreads();
+      eu_axis_apply(g, mu, q, mu, 1, w1, vals + c * nqv);
+    } else {
+      eu_axis_apply(g, mu, q, 1, q * q, coeff, w1);
+      __syncthreads();
+      eu_axis_apply(g, mu, q, mu, q, w1, w2);
+      __syncthreads();
+      eu_axis_apply(g, mu, q, mu * mu, 1, w2, vals + c * nqv);
+    }
+    __syncthreads();
+  }
+  for (int qv = threadIdx.x; qv < nqv; qv += blockDim.x) {
+    double uq[5], fq[15];
+    for (int c = 0; c < nc; ++c) uq[c] = vals[c * nqv + qv];
+    eu_check(d, uq, status);
+    eu_flux(d, uq, fq);
+    const double* a = adj + (size_t(e) * nqv + qv) * d * d;
+    for (int k = 0; k < d; ++k)
+      for (int c = 0; c < nc; ++c) {
+        double s = 0.0;
+        for (int m = 0; m < d; ++m) s += a[k * d + m] * fq[m * nc + c];
+        ft[(k * nc + c) * nqv + qv] = s;
+      }
+  }
+  for (int i = threadIdx.x; i < nc * npe; i += blockDim.x) acc[i] = 0.0;
+  __syncthreads();
+  for (int k = 0; k < d; ++k)  // integrate_back(gw, dw, d, dslot = k): M_0 along x, M_1 along y (, M_2 along z)
+    for (int c = 0; c < nc; ++c) {
+      const double* field = ft + (k * nc + c) * nqv;
+      const double* m0 = k == 0 ? dw : gw;
+      const double* m1 = k == 1 ? dw : gw;
+      if (d == 2) {
+        eu_axis_apply(m0, q, mu, 1, mu, field, w1);
+        __syncthreads();
+        for (int t = threadIdx.x; t < npe; t += blockDim.x) {  // second pass fused with out += ws.d
+          const int i = t % q, j = t / q;
+          double s = 0.0;
+          for (int b = 0; b < mu; ++b) {
+            const double mij = m1[j * mu + b];
+            if (mij == 0.0) continue;
+            s += mij * w1[b * q + i];
+          }
+          acc[c * npe + t] += s;
+        }
+      } else {
+        const double* m2 = k == 2 ? dw : gw;
+        eu_axis_apply(m0, q, mu, 1, mu * mu, field, w1);
+        __syncthreads();
+        eu_axis_apply(m1, q, mu, q, mu, w1, w2);
+        __syncthreads();
+        for (int t = threadIdx.x; t < npe; t += blockDim.x) {
+          const int ij = t % (q * q), l = t / (q * q);
+          double s = 0.0;
+          for (int b = 0; b < mu; ++b) {
+            const double mij = m2[l * mu + b];
+            if (mij == 0.0) continue;
+            s += mij * w2[b * q * q + ij];
+          }
+          acc[c * npe + t] += s;
+        }
+      }
+      __syncthreads();
+    }
+  for (int f = 0; f < 2 * d; ++f) {
+    const int64_t* fc = conn + (size_t(e) * 2 * d + f) * 3;
+    const bool interior = fc[0] >= 0;
+    for (int t = threadIdx.x; t < nc * nqf; t += blockDim.x) {
+      const int c = t / nqf, qf = t % nqf;
+      tr[t] = eu_face_trace_point(d, q, mu, g, f, ue + size_t(c) * npe, qf);
+      if (interior) {
+        const int code = int(fc[2]);
+        int qa, qb;
+        if (d == 2) {
+          qa = code == 0 ? qf : mu - 1 - qf;
+          qb = 0;
+        } else {
+          const int a0 = qf % mu, b0 = qf / mu;
+          int u = (code & 4) ? b0 : a0, v = (code & 4) ? a0 : b0;
+          if (code & 1) u = mu - 1 - u;
+          if (code & 2) v = mu - 1 - v;
+          qa = u;
+          qb = v;
+        }
+        const double* un = state + (size_t(fc[0]) * nc + c) * npe;
+        tr[nc * nqf + t] = eu_face_trace_point(d, q, mu, g, int(fc[1]), un, (d == 3 ? qb * mu : 0) + qa);
+      }
+    }
+    __syncthreads();
+    for (int qf = threadIdx.x; qf < nqf; qf += blockDim.x) {
+      double um[5], up[5], fh[5];
+      for (int c = 0; c < nc; ++c) {
+        um[c] = tr[c * nqf + qf];
+        up[c] = interior ? tr[nc * nqf + c * nqf + qf] : um[c];
+      }
+      eu_check(d, um, status);
+      eu_check(d, up, status);
+      const size_t fq = (size_t(e) * 2 * d + f) * nqf + qf;
+      eu_num_flux(d, um, up, face_n + fq * d, fh);
+      for (int c = 0; c < nc; ++c) lift[c * nqf + qf] = -face_w[fq] * fh[c];
+    }
+    __syncthreads();
+    // face_lift (discretization.hpp:133-166) into the face node layer
+    const int axis = f / 2, layer = (f % 2) == 0 ? 0 : q - 1;
+    if (d == 2) {
+      for (int t = threadIdx.x; t < nc * q; t += blockDim.x) {
+        const int c = t / q, j = t % q;
+        double s = 0.0;
+        for (int a = 0; a < mu; ++a) s += g[a * q + j] * lift[c * nqf + a];
+        acc[c * npe + (axis == 0 ? j * q + layer : layer * q + j)] += s;
+      }
+    } else {
+      const int t0 = axis == 0 ? 1 : 0, t1 = axis == 2 ? 1 : 2;
+      for (int t = threadIdx.x; t < nc * q * q; t += blockDim.x) {
+        const int c = t / (q * q), j0 = t % q, j1 = (t / q) % q;
+        double s = 0.0;
+        for (int b = 0; b < mu; ++b) {
+          double sa = 0.0;  // ws.a[j0 * mu + b]
+          for (int a = 0; a < mu; ++a) sa += g[a * q + j0] * lift[c * nqf + b * mu + a];
+          s += g[b * q + j1] * sa;
+        }
+        int idx[3];
+        idx[axis] = layer;
+        idx[t0] = j0;
+        idx[t1] = j1;
+        acc[c * npe + (idx[2] * q + idx[1]) * q + idx[0]] += s;
+      }
+    }
+    __syncthreads();
+  }
+  for (int i = threadIdx.x; i < nc * npe; i += blockDim.x) out[size_t(e) * nc * npe + i] = acc[i];
+}
+
 // Test hook: fn 0 sin, 1 cos, 2 atan, 3 atan2(x, y) of glibm.cuh over n arguments.
 __global__ void libm_eval_kernel(int fn, int64_t n, const double* x, const double* y, double* out) {
   for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
@@ -314,6 +510,21 @@ void launch_build_cache_euler(int dim, int q, int mu, int n_elements, const doub
   TPDG_CUDA_CHECK(cudaFuncSetAttribute(cache_euler_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   if (n_elements) cache_euler_kernel<<<n_elements, 256, smem, st>>>(dim, q, mu, g, state, adj, face_n, conn, dft, dfm,
                                                                     dfp, status);
+  TPDG_CUDA_CHECK(cudaGetLastError());
+  g_launches += 1;
+}
+
+void launch_residual_euler(int dim, int q, int mu, int n_elements, const double* g, const double* gw, const double* dw,
+                           const double* state, const double* adj, const double* face_n, const double* face_w,
+                           const int64_t* conn, double* out, int* status, cudaStream_t st) {
+  const int nc = dim + 2, nqv = dim == 2 ? mu * mu : mu * mu * mu, nqf = nqv / mu;
+  const int npe = dim == 2 ? q * q : q * q * q;
+  const size_t smem = sizeof(double) * (size_t(nc) * nqv * (1 + dim) + 2 * size_t(mu) * mu * q + size_t(nc) * npe +
+                                        3 * size_t(nc) * nqf);
+  TPDG_CUDA_CHECK(cudaFuncSetAttribute(residual_euler_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  if (n_elements)
+    residual_euler_kernel<<<n_elements, 256, smem, st>>>(dim, q, mu, g, gw, dw, state, adj, face_n, face_w, conn, out,
+                                                         status);
   TPDG_CUDA_CHECK(cudaGetLastError());
   g_launches += 1;
 }

@@ -1408,6 +1408,172 @@ int tpdg_gpu_build_cache_euler(tpdg_gpu_ctx ctx, int dim, int p, int mu, int n_e
   });
 }
 
+int tpdg_gpu_residual_euler(tpdg_gpu_ctx ctx, int dim, int p, int mu, int n_elements, const double* d_g,
+                            const double* d_gw, const double* d_dw, const double* d_state, const double* d_adj,
+                            const double* d_face_n, const double* d_face_w, const int64_t* d_conn, double* d_out) {
+  return guarded([&] {
+    REQUIRE(ctx && d_g && d_gw && d_dw && d_state && d_adj && d_face_n && d_face_w && d_conn && d_out, TPDG_CONFIG,
+            "residual_euler: null argument");
+    DevBuf st;
+    st.alloc(sizeof(int));
+    TPDG_CUDA_CHECK(cudaMemsetAsync(st.p, 0, sizeof(int), ctx->stream));
+    launch_residual_euler(dim, p + 1, mu, n_elements, d_g, d_gw, d_dw, d_state, d_adj, d_face_n, d_face_w, d_conn,
+                          d_out, st.as<int>(), ctx->stream);
+    int bad = 0;
+    TPDG_CUDA_CHECK(cudaMemcpyAsync(&bad, st.p, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    TPDG_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+    REQUIRE(bad == 0, TPDG_STATE, "euler: non-physical state (rho <= 0 or p <= 0)");
+  });
+}
+
+namespace {
+__global__ void newton_combine_kernel(const double* __restrict__ mdiff, const double* __restrict__ r, double gdt,
+                                      double* __restrict__ out, int64_t n) {
+  // solve_stage's residual_fn (time_step.hpp:129-138): M (w - base) - gdt r(w)
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    out[i] = mdiff[i] - gdt * r[i];
+}
+__global__ void neg_kernel(double* __restrict__ v, int64_t n) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    v[i] = -v[i];
+}
+__global__ void axpy_kernel(double* __restrict__ w, const double* __restrict__ s, int64_t n) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    w[i] += s[i];
+}
+void check_status(int rc) {
+  if (rc != TPDG_OK) throw Failure{rc, g_last_error};
+}
+}  // namespace
+
+int tpdg_gpu_step_backward_euler(tpdg_gpu_ctx ctx, const tpdg_gpu_system* sys, const double* h_adj,
+                                 const double* h_face_n, double* h_u, double dt, double newton_tol,
+                                 int newton_max_iterations, double newton_floor, const tpdg_gpu_gmres_config* gcfg,
+                                 const tpdg_gpu_ksvd_config* kcfg, int block_mode, int* newton_steps,
+                                 int* gmres_per_solve, double* residual_norms, int cap) {
+  return guarded([&] {
+    REQUIRE(ctx && sys && h_adj && h_face_n && h_u && gcfg, TPDG_CONFIG, "step_backward_euler: null argument");
+    REQUIRE(sys->n_c == sys->dim + 2, TPDG_CONFIG, "step_backward_euler: the device residual is the Euler law's");
+    REQUIRE(ctx->nranks == 1, TPDG_CONFIG, "step_backward_euler: single rank");
+    REQUIRE(dt > 0.0 && newton_tol > 0.0 && newton_max_iterations >= 1, TPDG_CONFIG, "step_backward_euler: bad config");
+    cudaStream_t st = ctx->stream;
+    const int d = sys->dim, nc = sys->n_c, q = sys->p + 1, mu = sys->mu, E = sys->n_elements;
+    const size_t nqv = d == 2 ? size_t(mu) * mu : size_t(mu) * mu * mu, nqf = nqv / mu;
+    const size_t npe = d == 2 ? size_t(q) * q : size_t(q) * q * q;
+    const int64_t n = int64_t(E) * nc * npe;
+    const size_t nft = size_t(E) * d * nqv * nc * nc, nff = size_t(E) * 2 * d * nqf * nc * nc;
+    DevBuf dg, dgw, ddw, dadj, dfn, dfw, dconn, base, w, diff, mdiff, rr, G, s, cft, cfm, cfp;
+    upload(dg, sys->g, size_t(mu) * q, st);
+    upload(dgw, sys->gw, size_t(mu) * q, st);
+    upload(ddw, sys->dw, size_t(mu) * q, st);
+    upload(dadj, h_adj, size_t(E) * nqv * d * d, st);
+    upload(dfn, h_face_n, size_t(E) * 2 * d * nqf * d, st);
+    upload(dfw, sys->face_w, size_t(E) * 2 * d * nqf, st);
+    upload(dconn, sys->conn, size_t(E) * 2 * d * 3, st);
+    upload(base, h_u, size_t(n), st);
+    upload(w, h_u, size_t(n), st);
+    for (DevBuf* b : {&diff, &mdiff, &rr, &G, &s}) b->alloc(sizeof(double) * size_t(n));
+    cft.alloc(sizeof(double) * nft);
+    cfm.alloc(sizeof(double) * nff);
+    cfp.alloc(sizeof(double) * nff);
+    // mass operator: a = 1, b = -0 with a zero cache (M v, ops/discretization.hpp mass_apply)
+    std::vector<double> zft(nft, 0.0), zff(nff, 0.0), hft(nft), hfm(nff), hfp(nff);
+    tpdg_gpu_system ms = *sys;
+    ms.dft = zft.data();
+    ms.dfm = zff.data();
+    ms.dfp = zff.data();
+    tpdg_gpu_op mop = nullptr;
+    check_status(tpdg_gpu_op_create(ctx, &ms, 0.0, 0, 0, 0, E, &mop));
+    std::unique_ptr<tpdg_gpu_op_s> mop_own(mop);
+    const int grid = std::max<int64_t>(1, std::min<int64_t>(148 * 8, (n + 255) / 256));
+    GmresWork W;
+    W.partial.alloc(sizeof(double) * 4096);
+    W.counter.alloc(sizeof(unsigned) * 8);
+    W.scal.alloc(sizeof(double) * 8);
+    TPDG_CUDA_CHECK(cudaMemsetAsync(W.counter.p, 0, W.counter.bytes, st));
+    auto residual_fn = [&]() {  // G = M (w - base) - dt r(w, t + dt); returns ||G||
+      launch_sub(w.as<double>(), base.as<double>(), diff.as<double>(), n, st);  // diff = w - base
+      launch_jv(mop->s, diff.as<double>(), nullptr, mdiff.as<double>(), st);
+      check_status(tpdg_gpu_residual_euler(ctx, d, sys->p, mu, E, dg.as<double>(), dgw.as<double>(), ddw.as<double>(),
+                                           w.as<double>(), dadj.as<double>(), dfn.as<double>(), dfw.as<double>(),
+                                           dconn.as<int64_t>(), rr.as<double>()));
+      newton_combine_kernel<<<grid, 256, 0, st>>>(mdiff.as<double>(), rr.as<double>(), dt, G.as<double>(), n);
+      TPDG_CUDA_CHECK(cudaGetLastError());
+      g_launches += 1;
+      return host_norm(ctx, G.as<double>(), n, W);
+    };
+    int steps = 0, nsolve = 0, nnorm = 0;
+    auto record_norm = [&](double v) {
+      if (residual_norms && nnorm < cap + 1) residual_norms[nnorm] = v;
+      ++nnorm;
+    };
+    // newton (solve/newton.hpp:32-68) on solve_stage's residual (time_step.hpp:126-146)
+    double norm = residual_fn();
+    const double norm0 = norm;
+    record_norm(norm);
+    if (norm0 > newton_floor) {
+      const double target = std::max(newton_tol * norm0, newton_floor);
+      double best = norm0;
+      int stale = 0;
+      while (norm > target) {
+        REQUIRE(steps < newton_max_iterations, TPDG_CONVERGENCE,
+                "newton: no convergence within " + std::to_string(newton_max_iterations) + " steps (residual " +
+                    std::to_string(norm) + ")");
+        // newton_linear_solve (time_step.hpp:57-122): linearize at w, form the KSVD preconditioner, GMRES on -G
+        int bad = 0;
+        {
+          DevBuf stbuf;
+          stbuf.alloc(sizeof(int));
+          TPDG_CUDA_CHECK(cudaMemsetAsync(stbuf.p, 0, sizeof(int), st));
+          launch_build_cache_euler(d, q, mu, E, dg.as<double>(), w.as<double>(), dadj.as<double>(), dfn.as<double>(),
+                                   dconn.as<int64_t>(), cft.as<double>(), cfm.as<double>(), cfp.as<double>(),
+                                   stbuf.as<int>(), st);
+          TPDG_CUDA_CHECK(cudaMemcpyAsync(&bad, stbuf.p, sizeof(int), cudaMemcpyDeviceToHost, st));
+          TPDG_CUDA_CHECK(cudaMemcpyAsync(hft.data(), cft.p, cft.bytes, cudaMemcpyDeviceToHost, st));
+          TPDG_CUDA_CHECK(cudaMemcpyAsync(hfm.data(), cfm.p, cfm.bytes, cudaMemcpyDeviceToHost, st));
+          TPDG_CUDA_CHECK(cudaMemcpyAsync(hfp.data(), cfp.p, cfp.bytes, cudaMemcpyDeviceToHost, st));
+          TPDG_CUDA_CHECK(cudaStreamSynchronize(st));
+        }
+        REQUIRE(bad == 0, TPDG_STATE, "euler: non-physical state in the Newton iterate");
+        tpdg_gpu_system ls = *sys;
+        ls.dft = hft.data();
+        ls.dfm = hfm.data();
+        ls.dfp = hfp.data();
+        tpdg_gpu_op lop = nullptr;
+        check_status(tpdg_gpu_op_create(ctx, &ls, dt, 0, block_mode, 0, E, &lop));
+        std::unique_ptr<tpdg_gpu_op_s> lop_own(lop);
+        tpdg_gpu_pc pc = nullptr;
+        check_status(tpdg_gpu_form_ksvd(lop, kcfg, &pc));
+        std::unique_ptr<tpdg_gpu_pc_s> pc_own(pc);
+        neg_kernel<<<grid, 256, 0, st>>>(G.as<double>(), n);  // rhs = -G (time_step.hpp:108-109)
+        TPDG_CUDA_CHECK(cudaGetLastError());
+        g_launches += 1;
+        TPDG_CUDA_CHECK(cudaMemsetAsync(s.p, 0, s.bytes, st));
+        int its = 0, conv = 0;
+        check_status(tpdg_gpu_gmres(lop, pc, G.as<double>(), s.as<double>(), gcfg, &its, nullptr, 0, &conv));
+        if (gmres_per_solve && nsolve < cap) gmres_per_solve[nsolve] = its;
+        ++nsolve;
+        axpy_kernel<<<grid, 256, 0, st>>>(w.as<double>(), s.as<double>(), n);
+        TPDG_CUDA_CHECK(cudaGetLastError());
+        g_launches += 1;
+        ++steps;
+        norm = residual_fn();
+        record_norm(norm);
+        if (norm < best) {
+          best = norm;
+          stale = 0;
+        } else if (++stale >= 3) {
+          throw Failure{TPDG_CONVERGENCE, "newton: residual stagnated/diverged at " + std::to_string(norm) +
+                                              " after " + std::to_string(steps) + " steps"};
+        }
+      }
+    }
+    TPDG_CUDA_CHECK(cudaMemcpyAsync(h_u, w.p, sizeof(double) * size_t(n), cudaMemcpyDeviceToHost, st));
+    TPDG_CUDA_CHECK(cudaStreamSynchronize(st));
+    if (newton_steps) *newton_steps = steps;
+  });
+}
+
 int tpdg_setup_euler(int case_kind, int nx, int ny, int nz, int p, tpdg_setup* out) {
   return guarded([&] {
     REQUIRE(case_kind == 3 || case_kind == 5, TPDG_CONFIG, "setup_euler: case_kind must be 3 (cfg3) or 5 (cfg5)");

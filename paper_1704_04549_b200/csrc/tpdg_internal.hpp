@@ -42,6 +42,10 @@ void launch_libm_eval(int fn, int64_t n, const double* x, const double* y, doubl
 void launch_build_cache_euler(int dim, int q, int mu, int n_elements, const double* g, const double* state,
                               const double* adj, const double* face_n, const int64_t* conn, double* dft, double* dfm,
                               double* dfp, int* status, cudaStream_t st);
+// residual r(u) of the LLF Euler law (ops/discretization.hpp:188-254) on the device
+void launch_residual_euler(int dim, int q, int mu, int n_elements, const double* g, const double* gw, const double* dw,
+                           const double* state, const double* adj, const double* face_n, const double* face_w,
+                           const int64_t* conn, double* out, int* status, cudaStream_t st);
 void launch_build_cache_advection(int dim, int n_elements, int nvol, int nface, const double* adj,
                                   const double* vol_x, const double* face_n, const double* face_x,
                                   const int64_t* conn, int field, const double* vel, double* dft, double* dfm,

@@ -77,3 +77,25 @@ def test_standin_configured_size_history(ctx, case):
           f"max relative difference {rel:.3e}")
     assert res.iterations == budget and len(h) == len(h_ref)
     assert rel <= 1e-8
+
+
+@pytest.mark.parametrize("case", list(SMALL))
+def test_residual_and_newton_step(ctx, case):
+    """Newton outer loop + residual on the device: r(u) (ops/discretization.hpp:
+    188-254) against the reference's, and one backward Euler step by Newton-GMRES with the KSVD
+    preconditioner (solve/time_step.hpp:136-146) taking the reference's Newton steps and GMRES counts per
+    solve, with the new state within 1e-10 of the reference's."""
+    z = O.load(case)
+    kind, n, p = SMALL[case]
+    s = T.setup_euler(kind, n[0], n[1], n[2], p=p)
+    r = T.residual_euler(ctx, s)
+    err_r = O.rel_l2(r, z["resid"])
+    dt = float(z["meta"][5])
+    u1, st = T.step_backward_euler(ctx, s, s.state, dt)
+    err_u = O.rel_l2(u1 - s.state, z["newton_state"] - s.state)
+    ref_g = [int(x) for x in z["newton_gmres"]]
+    print(f"{case}: residual rel-L2 {err_r:.3e}; Newton steps {st.newton_steps} (ref {int(z['newton_steps'][0])}), "
+          f"GMRES per solve {st.gmres_per_solve} (ref {ref_g}), norms {st.residual_norms}, update rel-L2 {err_u:.3e}")
+    assert err_r <= 1e-12
+    assert st.newton_steps == int(z["newton_steps"][0]) and st.gmres_per_solve == ref_g
+    assert err_u <= 1e-10
