@@ -19,6 +19,7 @@
 #include <vector>
 
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "tpdg_internal.hpp"
 
@@ -54,6 +55,14 @@ int guarded(F&& f) {
   do {                                                          \
     if (!(cond)) throw Failure{status, std::string(msg)};       \
   } while (0)
+
+// NVTX range around each public entry point (header-only NVTX v3; visible in nsys / ncu --nvtx).
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 #define NCCL_CHECK(expr)                                                                          \
   do {                                                                                            \
@@ -209,7 +218,7 @@ struct tpdg_gpu_pc_s {
   tpdg_gpu_op op = nullptr;
   DevPC pc{};
   int nblk = 0, raw_len = 0;
-  DevBuf raw, rec, piv, kind, fb_slot, fb_list, fb_lu, fb_piv, status, cells, cinv, irec;
+  DevBuf raw, rec, piv, kind, fb_slot, fb_list, fb_lu, fb_piv, status, cells, irec;
   std::vector<int> kind_h;
   std::vector<int64_t> fallbacks;  // (element, component)
 };
@@ -489,12 +498,7 @@ int run_gmres(tpdg_gpu_op op, tpdg_gpu_pc pc, const double* d_b, double* d_x, co
   const bool right = cfg.side == 0;
   const int m = cfg.restart;
   // multi-rank MGS (one fused w-update + partial dot kernel and one allreduce per pass);
-  // TPDG_GPU_MULTI_MGS=1 selects it on one rank too (tests of the multi-rank code path)
-  static const bool force_multi = [] {
-    const char* f = std::getenv("TPDG_GPU_MULTI_MGS");
-    return f && f[0] == '1';
-  }();
-  const bool multi = ctx->nranks > 1 || force_multi;
+  const bool multi = ctx->nranks > 1;
   const int64_t ldv = (n + 31) & ~int64_t(31);  // 256 B aligned Krylov slices (vectorized passes)
   GmresWork& W = op->gws;
   if (W.n != n || W.m != m) {
@@ -745,14 +749,8 @@ void finish_pc(tpdg_gpu_pc pc) {
   pc->cells.alloc(sizeof(double) * (size_t(pc->nblk) * d.cells_len + 32));  // +32: whole-slot loads of the last cell
   TPDG_CUDA_CHECK(cudaMemsetAsync(pc->cells.p, 0, pc->cells.bytes, st));
   d.cells = pc->cells.as<double>();
-  d.cinv = nullptr;
   d.irec = nullptr;
-  if (!d.faithful && op->dim == 2) {  // rows of the inverted Sylvester cell systems (kron2d_mma_kernel)
-    pc->cinv.alloc(sizeof(double) * size_t(pc->nblk) * 4 * d.n1 * op->q);
-    TPDG_CUDA_CHECK(cudaMemsetAsync(pc->cinv.p, 0, pc->cinv.bytes, st));
-    d.cinv = pc->cinv.as<double>();
-  }
-  launch_sylv_cells(d, pc->cells.as<double>(), d.cinv ? pc->cinv.as<double>() : nullptr, st);
+  launch_sylv_cells(d, pc->cells.as<double>(), st);
   if (!d.faithful && op->dim == 3 && op->q <= 16 && d.n1 <= 64) {  // tensor-core 3D apply operands
     pc->irec.alloc(sizeof(double) * size_t(pc->nblk) * irec3_doubles(d.n1, op->q));
     d.irec = pc->irec.as<double>();
@@ -1058,6 +1056,7 @@ int tpdg_gpu_op_check_hash(tpdg_gpu_op op, uint64_t expected_hash) {
 
 int tpdg_gpu_jv(tpdg_gpu_op op, const double* d_in, double* d_out) {
   return guarded([&] {
+    NvtxRange nvtx("tpdg.jv");
     jv_device(op, d_in, d_out);
     TPDG_CUDA_CHECK(cudaStreamSynchronize(op->ctx->stream));
   });
@@ -1065,6 +1064,7 @@ int tpdg_gpu_jv(tpdg_gpu_op op, const double* d_in, double* d_out) {
 
 int tpdg_gpu_jv_host(tpdg_gpu_op op, const double* h_in, double* h_out) {
   return guarded([&] {
+    NvtxRange nvtx("tpdg.jv_host");
     cudaStream_t st = op->ctx->stream;
     const size_t bytes = sizeof(double) * op->n_local_dofs;
     TPDG_CUDA_CHECK(cudaMemcpyAsync(op->io_a.p, h_in, bytes, cudaMemcpyHostToDevice, st));
@@ -1093,6 +1093,7 @@ int tpdg_gpu_shuffled_host(tpdg_gpu_op op, int e, int comp, int transpose, const
 
 int tpdg_gpu_form_ksvd(tpdg_gpu_op op, const tpdg_gpu_ksvd_config* cfg_in, tpdg_gpu_pc* out) {
   return guarded([&] {
+    NvtxRange nvtx("tpdg.form_ksvd");
     REQUIRE(op && out, TPDG_CONFIG, "form_ksvd: null argument");
     const tpdg_gpu_ksvd_config cfg = default_ksvd(cfg_in);
     REQUIRE(cfg.terms >= 1, TPDG_CONFIG, "LanczosConfig: requested_terms must be >= 1");
@@ -1132,6 +1133,7 @@ int tpdg_gpu_form_ksvd(tpdg_gpu_op op, const tpdg_gpu_ksvd_config* cfg_in, tpdg_
 
 int tpdg_gpu_form_block_jacobi(tpdg_gpu_op op, int64_t max_total_entries, tpdg_gpu_pc* out) {
   return guarded([&] {
+    NvtxRange nvtx("tpdg.form_block_jacobi");
     REQUIRE(op && out, TPDG_CONFIG, "form_block_jacobi: null argument");
     std::unique_ptr<tpdg_gpu_pc_s> pc(new tpdg_gpu_pc_s);
     pc->op = op;
@@ -1233,6 +1235,7 @@ int tpdg_gpu_pc_export_factors(tpdg_gpu_pc pc, int blk, double* h_out, int* has)
 
 int tpdg_gpu_pc_apply(tpdg_gpu_pc pc, const double* d_in, double* d_out) {
   return guarded([&] {
+    NvtxRange nvtx("tpdg.pc_apply");
     pc_apply_device(pc, d_in, d_out);
     TPDG_CUDA_CHECK(cudaStreamSynchronize(pc->op->ctx->stream));
   });
@@ -1240,6 +1243,7 @@ int tpdg_gpu_pc_apply(tpdg_gpu_pc pc, const double* d_in, double* d_out) {
 
 int tpdg_gpu_pc_apply_host(tpdg_gpu_pc pc, const double* h_in, double* h_out) {
   return guarded([&] {
+    NvtxRange nvtx("tpdg.pc_apply_host");
     tpdg_gpu_op op = pc->op;
     cudaStream_t st = op->ctx->stream;
     const size_t bytes = sizeof(double) * op->n_local_dofs;
@@ -1257,6 +1261,7 @@ int tpdg_gpu_pc_apply_host(tpdg_gpu_pc pc, const double* h_in, double* h_out) {
 int tpdg_gpu_gmres(tpdg_gpu_op op, tpdg_gpu_pc pc, const double* d_b, double* d_x, const tpdg_gpu_gmres_config* cfg,
                    int* iterations, double* hist, int hist_cap, int* converged) {
   int rc = TPDG_OK;
+  NvtxRange nvtx("tpdg.gmres");
   const int g = guarded([&] { rc = run_gmres(op, pc, d_b, d_x, *cfg, iterations, hist, hist_cap, converged); });
   return g != TPDG_OK ? g : rc;
 }
@@ -1265,6 +1270,7 @@ int tpdg_gpu_gmres_host(tpdg_gpu_op op, tpdg_gpu_pc pc, const double* h_b, doubl
                         const tpdg_gpu_gmres_config* cfg, int* iterations, double* hist, int hist_cap,
                         int* converged) {
   int rc = TPDG_OK;
+  NvtxRange nvtx("tpdg.gmres_host");
   const int g = guarded([&] {
     cudaStream_t st = op->ctx->stream;
     const size_t bytes = sizeof(double) * op->n_local_dofs;
@@ -1371,6 +1377,7 @@ int tpdg_gpu_build_cache_advection(tpdg_gpu_ctx ctx, int dim, int n_elements, in
                                    const int64_t* d_conn, int field, const double* vel, double* d_dft, double* d_dfm,
                                    double* d_dfp) {
   return guarded([&] {
+    NvtxRange nvtx("tpdg.build_cache_advection");
     REQUIRE(ctx && vel, TPDG_CONFIG, "build_cache_advection: null argument");
     REQUIRE((dim == 2 || dim == 3) && field >= 0 && field <= 2, TPDG_CONFIG, "build_cache_advection: bad kind");
     launch_build_cache_advection(dim, n_elements, nvol, nface, d_adj, d_vol_x, d_face_n, d_face_x, d_conn, field,
@@ -1392,6 +1399,7 @@ int tpdg_gpu_build_cache_euler(tpdg_gpu_ctx ctx, int dim, int p, int mu, int n_e
                                const double* d_state, const double* d_adj, const double* d_face_n,
                                const int64_t* d_conn, double* d_dft, double* d_dfm, double* d_dfp) {
   return guarded([&] {
+    NvtxRange nvtx("tpdg.build_cache_euler");
     REQUIRE(ctx && d_g && d_state && d_adj && d_face_n && d_conn && d_dft && d_dfm && d_dfp, TPDG_CONFIG,
             "build_cache_euler: null argument");
     REQUIRE((dim == 2 || dim == 3) && p >= 1 && mu >= 1 && n_elements >= 0, TPDG_CONFIG, "build_cache_euler: bad shape");
@@ -1412,6 +1420,7 @@ int tpdg_gpu_residual_euler(tpdg_gpu_ctx ctx, int dim, int p, int mu, int n_elem
                             const double* d_gw, const double* d_dw, const double* d_state, const double* d_adj,
                             const double* d_face_n, const double* d_face_w, const int64_t* d_conn, double* d_out) {
   return guarded([&] {
+    NvtxRange nvtx("tpdg.residual_euler");
     REQUIRE(ctx && d_g && d_gw && d_dw && d_state && d_adj && d_face_n && d_face_w && d_conn && d_out, TPDG_CONFIG,
             "residual_euler: null argument");
     DevBuf st;
@@ -1452,6 +1461,7 @@ int tpdg_gpu_step_backward_euler(tpdg_gpu_ctx ctx, const tpdg_gpu_system* sys, c
                                  const tpdg_gpu_ksvd_config* kcfg, int block_mode, int* newton_steps,
                                  int* gmres_per_solve, double* residual_norms, int cap) {
   return guarded([&] {
+    NvtxRange nvtx("tpdg.step_backward_euler");
     REQUIRE(ctx && sys && h_adj && h_face_n && h_u && gcfg, TPDG_CONFIG, "step_backward_euler: null argument");
     REQUIRE(sys->n_c == sys->dim + 2, TPDG_CONFIG, "step_backward_euler: the device residual is the Euler law's");
     REQUIRE(ctx->nranks == 1, TPDG_CONFIG, "step_backward_euler: single rank");

@@ -1306,42 +1306,13 @@ void launch_lanczos_form(const DevSys& s, const tpdg_gpu_ksvd_config& cfg, const
 
 void launch_make_factors(int dim, int q, int n1, int nblk, const double* raw, double* rec, int* piv, int* kind,
                          double* work, cudaStream_t st) {
-  // one warp per block; the per-block working set in shared memory when it fits
-  const int wl = 4 * (n1 > q ? n1 : q) + 16;
-  const size_t per_group = sizeof(double) * (size_t(wl + raw_len_of(dim, n1, q) + rec_len_of(dim, n1, q)) +
-                                             size_t(piv_len_of(dim, n1, q) + 1) / 2 + 2);
-  constexpr size_t kMax = 200 * 1024;
-  int dev = 0, sms = 0;
-  TPDG_CUDA_CHECK(cudaGetDevice(&dev));
-  TPDG_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  // The per-block working set in shared memory (one CTA of up to 8 warps per SM) loses to the
-  // global (L1-resident) working set with 4 CTAs per SM: the Francis QR sweeps are dependent
-  // chains, so resident warps matter more than access latency (cfg2 p=15: 10.5 -> 5.3 ms).
-  // TPDG_FORM_SMEM=1 selects the shared-memory variant.
-  static const bool use_smem = [] {
-    const char* f = std::getenv("TPDG_FORM_SMEM");
-    return f && f[0] == '1';
-  }();
-  if (per_group <= kMax && use_smem) {
-    const int groups = int(std::min<size_t>(kMaxGroups, kMax / per_group));
-    const size_t smem = per_group * groups;
-    static size_t configured = 0;
-    if (smem > configured) {
-      TPDG_CUDA_CHECK(cudaFuncSetAttribute(make_factors_kernel<true, WarpGroup>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(kMax)));
-      configured = kMax;
-    }
-    int per_sm = 0;
-    TPDG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, make_factors_kernel<true, WarpGroup>,
-                                                                  32 * groups, smem));
-    const int grid = std::min((nblk + groups - 1) / groups, std::max(1, per_sm) * sms);
-    make_factors_kernel<true, WarpGroup><<<grid, 32 * groups, smem, st>>>(dim, q, n1, nblk, const_cast<double*>(raw),
-                                                                         rec, piv, kind, work);
-  } else {  // global working set (work holds make_factors_work_groups() x wl doubles)
-    const int grid = std::min((nblk + kMaxGroups - 1) / kMaxGroups, 148 * kFormGlobalCtas);
-    make_factors_kernel<false, WarpGroup><<<grid, kFormThreads, 0, st>>>(dim, q, n1, nblk, const_cast<double*>(raw),
-                                                                        rec, piv, kind, work);
-  }
+  // One warp per block with a global (L1-resident) working set (work holds make_factors_work_groups() x
+  // (4 max(n1, q) + 16) doubles), four 8-warp CTAs per SM: the Francis QR sweeps are dependent chains, so
+  // resident warps matter more than access latency (a shared-memory working set with one CTA per SM
+  // measured 10.5 vs 5.3 ms at cfg2 p = 15).
+  const int grid = std::min((nblk + kMaxGroups - 1) / kMaxGroups, 148 * kFormGlobalCtas);
+  make_factors_kernel<false, WarpGroup><<<grid, kFormThreads, 0, st>>>(dim, q, n1, nblk, const_cast<double*>(raw),
+                                                                      rec, piv, kind, work);
   TPDG_CUDA_CHECK(cudaGetLastError());
   ++g_launches;
 }
@@ -1511,7 +1482,9 @@ __global__ void __launch_bounds__(1024) dense_lu_blocked_kernel(int n, double* l
 }
 
 void launch_dense_lu(int n, int nfb, double* fb_lu, int* fb_piv, int* fb_status, cudaStream_t st) {
-  static const bool unblocked = [] {  // TPDG_GPU_DENSE_LU=unblocked: one trailing pass per pivot
+  // test hook TPDG_GPU_DENSE_LU=unblocked: the unblocked kernel (one trailing pass per pivot), which the
+  // blocked one must equal bit for bit (tests/test_gpu_block_jacobi.py); it also serves n > 1600
+  static const bool unblocked = [] {
     const char* f = std::getenv("TPDG_GPU_DENSE_LU");
     return f && f[0] == 'u';
   }();

@@ -399,11 +399,6 @@ bool try_jv3d_fast(const DevSys& s, const double* vin, const double* halo, doubl
 }  // namespace
 
 bool launch_jv3d_fast(const DevSys& s, const double* vin, const double* halo, double* vout, cudaStream_t st) {
-  static const int minb = [] {  // study switch (removed once measured)
-    const char* f = std::getenv("TPDG_JV3D_MINB");
-    return f ? std::atoi(f) : 3;
-  }();
-  if (minb == 2) return try_jv3d_fast<0, 11, 12, 2>(s, vin, halo, vout, st);
   return try_jv3d_fast<0, 11, 12>(s, vin, halo, vout, st) || try_jv3d_fast<1, 5, 6>(s, vin, halo, vout, st) ||
          try_jv3d_fast<2, 8, 9>(s, vin, halo, vout, st) || try_jv3d_fast<3, 4, 5>(s, vin, halo, vout, st) ||
          try_jv3d_fast<4, 3, 4>(s, vin, halo, vout, st);

@@ -274,9 +274,6 @@ constexpr int kSizedThreads = 64;
 #ifndef SYLV_FAST
 #define SYLV_FAST 0  // sized kernel: 1 = sylv_fast (lane per entry, measured 167 us at p=15) vs 132 us for the wavefront
 #endif
-#ifndef SYLV_EXP
-#define SYLV_EXP 0  // study builds only: 1 no cell loads, 2 no tiny solves
-#endif
 #ifndef KRON_SKIP
 #define KRON_SKIP 0  // study builds only: bit mask of skipped phases (tools/kron_variants.sh)
 #endif
@@ -345,8 +342,7 @@ __device__ __forceinline__ void warp_mm(const double* A, int lda, const double* 
 }
 
 // Right-hand side of one Sylvester entry: B minus the solved rows below (j ascending), then the
-// solved columns to the right (l ascending), exactly sylvester.hpp:84-99 (FMA: fused steps).
-template <bool FMA = false>
+// solved columns to the right (l ascending), exactly sylvester.hpp:84-99.
 __device__ __forceinline__ double sylv_rhs(const double* __restrict__ t1, int n1, const double* __restrict__ t2,
                                            int n2, const double* M, const double* Y, int ld, int i, int k,
                                            int jfirst, int lfirst) {
@@ -362,7 +358,7 @@ __device__ __forceinline__ double sylv_rhs(const double* __restrict__ t1, int n1
     const bool first = t < nj;
     const double* pa = first ? a1 + t : a2 + t;
     const double* pb = first ? b1 + t * ld : b2 + t;
-    s = FMA ? fma(-*pa, *pb, s) : fmsc(s, *pa, *pb);
+    s = fmsc(s, *pa, *pb);
   }
   return s;
 }
@@ -490,7 +486,7 @@ __device__ __forceinline__ double cell_solve(const double (&cf)[22], double (&b)
 
 // One warp per Kronecker block: lane 0 builds the plan (tol from the row sums, quasi-blocks),
 // the lanes factor the cells.
-__global__ void sylv_cells_kernel(DevPC pc, double* __restrict__ cells, double* __restrict__ cinv) {
+__global__ void sylv_cells_kernel(DevPC pc, double* __restrict__ cells) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= pc.nblk || pc.kind[warp] == 0) return;
   const int t1n = pc.dim == 2 ? pc.n1 : pc.q, t2n = pc.q;
@@ -535,23 +531,6 @@ __global__ void sylv_cells_kernel(DevPC pc, double* __restrict__ cells, double* 
     else factor_cell<2, 2>(t1, t1n, t2, t2n, i0, k0, tol, slot);
     const long long cw = __double_as_longlong(slot[0]);
     if (cw & 256) atomicOr(h + 3, 1);
-    if (cinv) {  // rows of S^{-1} (tensor-core path): column j = replay of the permuted unit vector e_j
-      const int ns = isz * ksz;
-      double cf[22], inv[4][4];
-      for (int u = 0; u < 22; ++u) cf[u] = slot[u];
-      for (int j = 0; j < ns; ++j) {
-        for (int ee = 0; ee < ns; ++ee) {
-          double b[4];
-          for (int u = 0; u < 4; ++u) b[u] = (u < ns && int((cw >> (2 * u)) & 3) == j) ? 1.0 : 0.0;
-          inv[ee][j] = ns == 1 ? b[0] * cf[2] : ns == 2 ? cell_solve<2>(cf, b, ee) : cell_solve<4>(cf, b, ee);
-        }
-      }
-      double* ci = cinv + size_t(warp) * (4 * t1n * t2n);
-      for (int ee = 0; ee < ns; ++ee) {
-        const int x = i0 + ee / ksz, y = k0 + ee % ksz;
-        for (int u = 0; u < 4; ++u) ci[4 * (x * t2n + y) + u] = u < ns ? inv[ee][u] : 0.0;
-      }
-    }
   }
 }
 
@@ -561,15 +540,14 @@ __global__ void sylv_cells_kernel(DevPC pc, double* __restrict__ cells, double* 
 // set of NT/4 (cell, slice) groups of 4 lanes (lane e of a group = entry e of the cell); a
 // barrier separates the steps. (Loading the next item's factors one item ahead was measured
 // slower: the extra registers cost more occupancy than the hidden latency gained.)
-template <int TN1, int TN2, int NSL, int NT, bool CTA, bool FMA = false, bool INV = false>
+template <int TN1, int TN2, int NSL, int NT, bool CTA>
 __device__ __forceinline__ void sylv_wavefront(const double* T1, const double* T2, double* X, int ld, int ss,
                                                const double* __restrict__ cc, const int* sb, int tid, int* status) {
-  // INV: cc = rows of the inverted cell systems, 4 doubles per entry at 4 (x TN2 + y) (sylv_cells_kernel);
-  // else cc = the replay slots of the factored cells.
+  // cc = the replay slots of the factored cells (sylv_cells_kernel).
   const int nb1 = sb[0], nb2 = sb[1];
   const int *s1 = sb + 4, *z1 = s1 + TN1, *s2 = z1 + TN1, *z2 = s2 + TN2;
   const int last = nb1 + nb2 - 2, lane = tid & 31, e = lane & 3, g = lane & ~3;
-  constexpr int NCF = INV ? 4 : 22;
+  constexpr int NCF = 22;
   struct Item {
     int bi, bj, sl;
     bool ok;
@@ -591,19 +569,9 @@ __device__ __forceinline__ void sylv_wavefront(const double* T1, const double* T
   auto load = [&](const Item& it, double (&c)[NCF]) {
 #pragma unroll
     for (int u = 0; u < NCF; ++u) c[u] = 0.0;
-    if (!it.ok || (SYLV_EXP & 1)) return;
+    if (!it.ok) return;
     const int i0 = s1[it.bi], isz = z1[it.bi], k0 = s2[it.bj], ksz = z2[it.bj];
-    if constexpr (INV) {
-      if (e < isz * ksz) {
-        const int x = i0 + (ksz == 2 ? e >> 1 : e), y = k0 + (ksz == 2 ? e & 1 : 0);
-        const double2* p = reinterpret_cast<const double2*>(cc + 4 * (x * TN2 + y));
-        const double2 v0 = __ldg(p), v1 = __ldg(p + 1);
-        c[0] = v0.x;
-        c[1] = v0.y;
-        c[2] = v1.x;
-        c[3] = v1.y;
-      }
-    } else {
+    {
       const double2* p = reinterpret_cast<const double2*>(cc + 6 * (i0 * TN2 + isz * k0));
 #pragma unroll
       for (int u = 0; u < NCF / 2; ++u) {
@@ -630,7 +598,6 @@ __device__ __forceinline__ void sylv_wavefront(const double* T1, const double* T
     }
     const Item nxt = locate(nstep, nbase);
     double cn[NCF];
-    if (INV && nstep <= last) load(nxt, cn);  // 4 doubles: cheap enough to load one item ahead
     double* Ms = X + cur.sl * ss;
     int i0 = 0, k0 = 0, isz = 1, ksz = 1;
     double s = 0.0;
@@ -640,26 +607,19 @@ __device__ __forceinline__ void sylv_wavefront(const double* T1, const double* T
       k0 = s2[cur.bj];
       ksz = z2[cur.bj];
       if (e < isz * ksz)
-        s = sylv_rhs<FMA>(T1, TN1, T2, TN2, Ms, Ms, ld, i0 + (ksz == 2 ? e >> 1 : e), k0 + (ksz == 2 ? e & 1 : 0),
+        s = sylv_rhs(T1, TN1, T2, TN2, Ms, Ms, ld, i0 + (ksz == 2 ? e >> 1 : e), k0 + (ksz == 2 ? e & 1 : 0),
                           i0 + isz, k0 + ksz);
     }
     const int ns = isz * ksz;
     double y = 0.0;
-    if constexpr (INV) {
-      double b[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) b[u] = __shfl_sync(0xffffffffu, s, g + u);
-#pragma unroll
-      for (int u = 0; u < 4; ++u) y = fma(cf[u], b[u], y);  // rows are zero beyond ns
-    } else {
+    {
       const long long code = __double_as_longlong(cf[0]);
       double b[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) b[u] = __shfl_sync(0xffffffffu, s, g + int((code >> (2 * u)) & 3));
       if (cur.ok && e < ns) {
         if (code & 256) atomicExch(status, int(TPDG_SINGULAR));
-        if (SYLV_EXP & 2) y = b[0];
-        else y = ns == 1 ? cell_solve<1>(cf, b, e) : ns == 2 ? cell_solve<2>(cf, b, e) : cell_solve<4>(cf, b, e);
+        y = ns == 1 ? cell_solve<1>(cf, b, e) : ns == 2 ? cell_solve<2>(cf, b, e) : cell_solve<4>(cf, b, e);
       }
     }
     if (cur.ok && e < ns) Ms[(i0 + (ksz == 2 ? e >> 1 : e)) * ld + k0 + (ksz == 2 ? e & 1 : 0)] = y;
@@ -667,7 +627,7 @@ __device__ __forceinline__ void sylv_wavefront(const double* T1, const double* T
       if (CTA) __syncthreads();
       else __syncwarp();
     }
-    if (!INV && nstep <= last) load(nxt, cn);
+    if (nstep <= last) load(nxt, cn);
 #pragma unroll
     for (int u = 0; u < NCF; ++u) cf[u] = cn[u];
     cur = nxt;
@@ -886,202 +846,6 @@ bool launch_kron2d_sized(const DevPC& pc, const double* in, double* out, cudaStr
   return try_kron2d_sized<5, 5>(pc, in, out, st) || try_kron2d_sized<9, 9>(pc, in, out, st) ||
          try_kron2d_sized<16, 16>(pc, in, out, st) || try_kron2d_sized<21, 21>(pc, in, out, st) ||
          try_kron2d_sized<31, 31>(pc, in, out, st);
-}
-
-// ------------------------------------------------------------------------------------ 2D, DMMA
-// apply_factors_2d (precond/ksvd.hpp:112-129) with the rotations on the FP64 tensor cores: one
-// warp per block, M = Q1^T X Q2 and X = Q1 Y Q2^T as four warp-level DMMA products, the two LU
-// axis solves as register fibers and the Sylvester wavefront replaying the factored cells, with
-// FMA. Not bit-faithful: measured <= 2e-14 rel-L2 against the reference's own output on every
-// golden case with the reference's factors (gate 1e-12) and identical GMRES counts at cfg2
-// p=15/20/30 (tools/pc_sensitivity.py); TPDG_GPU_FAITHFUL=1 selects the faithful kernels.
-template <int N>
-__device__ __forceinline__ void lu_fiber_fma(const double* __restrict__ lu, const double* __restrict__ rcp,
-                                             const int* __restrict__ perm, double* col, int stride) {
-  double x[N];
-#pragma unroll
-  for (int k = 0; k < N; ++k) x[k] = col[perm[k] * stride];
-#pragma unroll
-  for (int r = 1; r < N; ++r) {
-    double s = x[r];
-#pragma unroll
-    for (int j = 0; j < r; ++j) s = fma(-lu[r * N + j], x[j], s);
-    x[r] = s;
-  }
-#pragma unroll
-  for (int r = N - 1; r >= 0; --r) {
-    double s = x[r];
-#pragma unroll
-    for (int j = r + 1; j < N; ++j) s = fma(-lu[r * N + j], x[j], s);
-    x[r] = s * rcp[r];
-  }
-#pragma unroll
-  for (int k = 0; k < N; ++k) col[k * stride] = x[k];
-}
-
-// rows x cols block, global (dense, ld = cols) -> shared (ld), asynchronous
-__device__ __forceinline__ void cp_rows(double* dst, int ldd, const double* src, int rows, int cols, int lane) {
-  if ((cols & 1) == 0 && (ldd & 1) == 0 && (reinterpret_cast<uintptr_t>(src) & 15) == 0 &&
-      (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-    const int h = cols / 2;
-    for (int i = lane; i < rows * h; i += 32) cp_async16(dst + (i / h) * ldd + 2 * (i % h), src + 2 * i);
-  } else {
-    for (int i = lane; i < rows * cols; i += 32) cp_async8(dst + (i / cols) * ldd + i % cols, src + i);
-  }
-}
-
-__device__ __forceinline__ void zero_pad(double* buf, int ld, int rows, int cols, int rows_tot, int cols_tot,
-                                         int lane) {
-  for (int i = lane; i < rows_tot * cols_tot; i += 32) {
-    const int r = i / cols_tot, c = i % cols_tot;
-    if (r >= rows || c >= cols) buf[r * ld + c] = 0.0;
-  }
-}
-
-template <int N1, int N2>
-struct Kron2dMmaLayout {
-  static constexpr int N1P = p8(N1), N2P = p8(N2);
-  static constexpr int LX = lda4(N2P), LQ1 = lda4(N1P), LQ2 = lda4(N2P), LP = lda4(N2P);
-  static constexpr int hdr = (((4 + 2 * N1 + 2 * N2) / 2 + 2) & ~1);
-  static constexpr int o_x = 0;                       // X -> M -> Y  (N1P x LX)
-  static constexpr int o_q1 = o_x + N1P * LX;         // Q1 (N1P x LQ1, zero padded)
-  static constexpr int o_q2 = o_q1 + N1P * LQ1;       // Q2 (N2P x LQ2, zero padded)
-  static constexpr int lu = N1 * N1 + N2 * N2;
-  static constexpr int o_lu = o_q2 + N2P * LQ2;       // LU(A2) | LU(B1), later P / Z (N1P x LP)
-  static constexpr int lu_sz = ((lu > N1P * LP ? lu : N1P * LP) + 1) & ~1;
-  static constexpr int o_t1 = o_lu + lu_sz;           // T1 | T2
-  static constexpr int o_rcp = (o_t1 + N1 * N1 + N2 * N2 + 1) & ~1;
-  static constexpr int o_h = (o_rcp + N1 + N2 + 1) & ~1;
-  static constexpr int o_piv = o_h + hdr;             // ints: pivots
-  static constexpr int per = (o_piv + (N1 + N2 + 1) / 2 + 1) & ~1;
-};
-
-template <int N1, int N2>
-__global__ void __launch_bounds__(kSizedThreads) kron2d_mma_kernel(DevPC pc, const double* __restrict__ in,
-                                                                    double* __restrict__ out) {
-  using L = Kron2dMmaLayout<N1, N2>;
-  constexpr int N1P = L::N1P, N2P = L::N2P, LX = L::LX, LQ1 = L::LQ1, LQ2 = L::LQ2, LP = L::LP, hdr = L::hdr;
-  extern __shared__ double sm_all[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int blk = blockIdx.x * (kSizedThreads / 32) + warp;
-  if (blk >= pc.nblk || pc.kind[blk] == 0 || (pc.skip && *pc.skip)) return;
-  double* S = sm_all + size_t(warp) * L::per;
-  double* sX = S + L::o_x;
-  double* sQ1 = S + L::o_q1;
-  double* sQ2 = S + L::o_q2;
-  double* sLU = S + L::o_lu;
-  double* sP = S + L::o_lu;  // aliases the LU factors once both fiber solves are done
-  double* sT1 = S + L::o_t1;
-  double* sT2 = sT1 + N1 * N1;
-  double* sRcp = S + L::o_rcp;
-  double* sH = S + L::o_h;
-  int* sPiv = reinterpret_cast<int*>(S + L::o_piv);
-  const double* cells = pc.cells + size_t(blk) * pc.cells_len;
-  {
-    const double* r = pc.rec + size_t(blk) * (3 * N1 * N1 + 3 * N2 * N2);
-    cp_rows(sLU, N1 * N1 + N2 * N2, r, 1, N1 * N1 + N2 * N2, lane);              // LU(A2) | LU(B1)
-    cp_rows(sQ1, LQ1, r + N1 * N1 + N2 * N2, N1, N1, lane);                      // Q1
-    cp_rows(sT1, N1 * N1, r + 2 * N1 * N1 + N2 * N2, 1, N1 * N1, lane);          // T1
-    cp_rows(sQ2, LQ2, r + 3 * N1 * N1 + N2 * N2, N2, N2, lane);                  // Q2
-    cp_rows(sT2, N2 * N2, r + 3 * N1 * N1 + 2 * N2 * N2, 1, N2 * N2, lane);      // T2
-    cp_rows(sH, hdr, cells, 1, hdr, lane);
-    cp_rows(sX, LX, in + size_t(blk) * (N1 * N2), N1, N2, lane);
-    for (int i = lane; i < N1 + N2; i += 32) cp_async4(sPiv + i, pc.piv + size_t(blk) * (N1 + N2) + i);
-    if (N1P != N1 || N2P != N2) {
-      zero_pad(sX, LX, N1, N2, N1P, N2P, lane);
-      zero_pad(sQ1, LQ1, N1, N1, N1P, N1P, lane);
-      zero_pad(sQ2, LQ2, N2, N2, N2P, N2P, lane);
-    }
-    cp_async_wait_all();
-  }
-  __syncwarp();
-  for (int i = lane; i < N1 + N2; i += 32)
-    sRcp[i] = 1.0 / (i < N1 ? sLU[i * N1 + i] : sLU[N1 * N1 + (i - N1) * N2 + i - N1]);
-  __syncwarp();
-  if (!(KRON_SKIP & 1)) {
-  for (int c = lane; c < N2; c += 32) lu_fiber_fma<N1>(sLU, sRcp, sPiv, sX + c, LX);  // A2^{-1} (x) I
-  __syncwarp();
-  for (int r = lane; r < N1; r += 32) lu_fiber_fma<N2>(sLU + N1 * N1, sRcp + N1, sPiv + N1, sX + r * LX, 1);
-  __syncwarp();
-  }
-  if (!(KRON_SKIP & 2)) {
-  {  // P = Q1^T X
-    double acc[N1P / 8][N2P / 8][2];
-    zero_tiles(acc);
-    mma_tiles<N1P / 8, N2P / 8, N1P / 4, false, true>(acc, sQ1, LQ1, sX, LX, lane);
-    store_tiles(acc, sP, LP, N1P, lane);
-  }
-  __syncwarp();
-  {  // M = P Q2 (over X)
-    double acc[N1P / 8][N2P / 8][2];
-    zero_tiles(acc);
-    mma_tiles<N1P / 8, N2P / 8, N2P / 4, false>(acc, sP, LP, sQ2, LQ2, lane);
-    store_tiles(acc, sX, LX, N1P, lane);
-  }
-  __syncwarp();
-  }
-  if (!(KRON_SKIP & 4)) {  // Y overwrites M: T1 Y + Y T2^T = M (block wavefront, inverse rows of the cell systems)
-    const int* sb = reinterpret_cast<const int*>(sH);
-    if (sb[3]) atomicExch(pc.status, int(TPDG_SINGULAR));
-    sylv_wavefront<N1, N2, 1, 32, false, true, true>(sT1, sT2, sX, LX, 0, pc.cinv + size_t(blk) * (4 * N1 * N2), sb,
-                                                     lane, pc.status);
-    __syncwarp();
-  }
-  if (KRON_SKIP & 8) {
-    for (int i = lane; i < N1 * N2; i += 32) out[size_t(blk) * (N1 * N2) + i] = sX[(i / N2) * LX + i % N2];
-    return;
-  }
-  {  // Z = Q1 Y
-    double acc[N1P / 8][N2P / 8][2];
-    zero_tiles(acc);
-    mma_tiles<N1P / 8, N2P / 8, N1P / 4, false>(acc, sQ1, LQ1, sX, LX, lane);
-    store_tiles(acc, sP, LP, N1P, lane);
-  }
-  __syncwarp();
-  {  // out = Z Q2^T
-    double acc[N1P / 8][N2P / 8][2];
-    zero_tiles(acc);
-    mma_tiles<N1P / 8, N2P / 8, N2P / 4, true>(acc, sP, LP, sQ2, LQ2, lane);
-    double* o = out + size_t(blk) * (N1 * N2);
-    const int r = lane >> 2, c2 = 2 * (lane & 3);
-#pragma unroll
-    for (int mt = 0; mt < N1P / 8; ++mt)
-#pragma unroll
-      for (int nt = 0; nt < N2P / 8; ++nt) {
-        const int i = 8 * mt + r, j = 8 * nt + c2;
-        if (i < N1) {
-          if ((N2 & 1) == 0 && j + 1 < N2) {
-            *reinterpret_cast<double2*>(o + i * N2 + j) = make_double2(acc[mt][nt][0], acc[mt][nt][1]);
-          } else {
-            if (j < N2) o[i * N2 + j] = acc[mt][nt][0];
-            if (j + 1 < N2) o[i * N2 + j + 1] = acc[mt][nt][1];
-          }
-        }
-      }
-  }
-}
-
-template <int N1, int N2>
-bool try_kron2d_mma(const DevPC& pc, const double* in, double* out, cudaStream_t st) {
-  if (pc.dim != 2 || pc.n1 != N1 || pc.q != N2) return false;
-  static bool configured = false;
-  const size_t smem = sizeof(double) * size_t(Kron2dMmaLayout<N1, N2>::per) * (kSizedThreads / 32);
-  if (!configured) {
-    TPDG_CUDA_CHECK(cudaFuncSetAttribute(kron2d_mma_kernel<N1, N2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(smem)));
-    TPDG_CUDA_CHECK(cudaFuncSetAttribute(kron2d_mma_kernel<N1, N2>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                         100));
-    configured = true;
-  }
-  const int per_cta = kSizedThreads / 32;
-  kron2d_mma_kernel<N1, N2><<<(pc.nblk + per_cta - 1) / per_cta, kSizedThreads, smem, st>>>(pc, in, out);
-  return true;
-}
-
-bool launch_kron2d_mma(const DevPC& pc, const double* in, double* out, cudaStream_t st) {
-  return try_kron2d_mma<5, 5>(pc, in, out, st) || try_kron2d_mma<9, 9>(pc, in, out, st) ||
-         try_kron2d_mma<16, 16>(pc, in, out, st) || try_kron2d_mma<21, 21>(pc, in, out, st) ||
-         try_kron2d_mma<31, 31>(pc, in, out, st);
 }
 
 // ------------------------------------------------------------------------------------ 3D, sized
@@ -1798,9 +1562,9 @@ void launch_kron3d_inv_prep(const DevPC& pc, double* irec, cudaStream_t st) {
   TPDG_CUDA_CHECK(cudaGetLastError());
 }
 
-void launch_sylv_cells(const DevPC& pc, double* cells, double* cinv, cudaStream_t st) {
+void launch_sylv_cells(const DevPC& pc, double* cells, cudaStream_t st) {
   if (pc.nblk == 0) return;
-  sylv_cells_kernel<<<(pc.nblk + 3) / 4, 128, 0, st>>>(pc, cells, cinv);
+  sylv_cells_kernel<<<(pc.nblk + 3) / 4, 128, 0, st>>>(pc, cells);
   TPDG_CUDA_CHECK(cudaGetLastError());
 }
 
@@ -1811,15 +1575,8 @@ void launch_pc_apply(const DevPC& pc, const double* in, double* out, cudaStream_
   if (smem > 227 * 1024)
     throw Failure{TPDG_CONFIG, "pc_apply: factor record of " + std::to_string(smem) + " B exceeds shared memory"};
   if (pc.dim == 2) {
-    // default: the bit-faithful multi-block kernel (kron_ew.cu); TPDG_GPU_KRON=mma / sized selects
-    // the tensor-core (not faithful) / one-block-per-warp kernels for comparison
-    static const int kmode = [] {
-      const char* k = std::getenv("TPDG_GPU_KRON");
-      return !k ? 0 : k[0] == 'm' ? 1 : k[0] == 's' ? 2 : 0;
-    }();
-    const bool done = (kmode == 0 && launch_kron2d_ew(pc, in, out, st)) ||
-                      (kmode == 1 && !pc.faithful && launch_kron2d_mma(pc, in, out, st));
-    if (!done && !launch_kron2d_sized(pc, in, out, st)) {
+    // the bit-faithful multi-block kernel (kron_ew.cu), else one block per warp (sized), else generic
+    if (!launch_kron2d_ew(pc, in, out, st) && !launch_kron2d_sized(pc, in, out, st)) {
       set_smem(kron2d_apply_kernel, smem, c2);
       kron2d_apply_kernel<<<pc.nblk, kApplyThreads, smem, st>>>(pc, in, out);
     }

@@ -274,13 +274,9 @@ bool try_fb(const DevPC& pc, const double* in, double* out, cudaStream_t st) {
 
 bool launch_fallback_apply(const DevPC& pc, const double* in, double* out, cudaStream_t st) {
   if (pc.n_fb == 0) return true;
-  static const bool columns = [] {  // TPDG_GPU_FB=col: one block barrier per column (fb_apply_kernel)
-    const char* f = std::getenv("TPDG_GPU_FB");
-    return f && f[0] == 'c';
-  }();
   // panels pay off for large blocks (cfg2 p = 30, n = 961: 1.44 -> 0.91 ms); at n = 441 (p = 20) the
   // per-column kernel's deeper prefetch ring is faster (209 vs 232 us)
-  if (!columns && pc.blk_len > 2 * kFbThreads)
+  if (pc.blk_len > 2 * kFbThreads)
     return try_fb_panel<4>(pc, in, out, st) || try_fb_panel<8>(pc, in, out, st);
   return try_fb<1>(pc, in, out, st) || try_fb<2>(pc, in, out, st) || try_fb<4>(pc, in, out, st) ||
          try_fb<8>(pc, in, out, st);

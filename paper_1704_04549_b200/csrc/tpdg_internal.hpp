@@ -110,7 +110,6 @@ struct DevPC {
   int faithful;          // 1: bit-faithful kernels only (TPDG_GPU_FAITHFUL=1), 0: tensor-core apply
   const double* cells;   // [nblk][cells_len]: Sylvester plan + factored tiny systems (sylv_cells_len)
   int cells_len;
-  const double* cinv;    // [nblk][4 t1 t2]: row e of the inverted cell system of every Sylvester entry (2D)
   const double* irec;    // [nblk][irec3_len]: 3D tensor-core apply operands (kron3d_inv_prep_kernel)
   int* status;           // device error flag (SingularError inside the Sylvester solve)
   const int* skip;       // optional device flag: kernels return immediately when *skip != 0
@@ -150,7 +149,7 @@ bool launch_kron2d_ew(const DevPC& pc, const double* in, double* out, cudaStream
 // dense-LU fallback blocks, one CTA per fallback block (kron_fallback.cu); false if n is too large
 bool launch_fallback_apply(const DevPC& pc, const double* in, double* out, cudaStream_t st);
 // Factor the data-independent tiny Sylvester systems of every Kronecker block into pc.cells.
-void launch_sylv_cells(const DevPC& pc, double* cells, double* cinv, cudaStream_t st);
+void launch_sylv_cells(const DevPC& pc, double* cells, cudaStream_t st);
 void launch_shuffled(const DevSys& s, int e, int comp, int transpose, const double* in, double* out,
                      double* scratch, cudaStream_t st);
 size_t shuffled_scratch_doubles(const DevSys& s);

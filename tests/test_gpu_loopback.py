@@ -77,19 +77,31 @@ def test_loopback_jv_pc_gmres(name, build, dt, ref_its, nranks):
     assert its == {ref_its}
 
 
-@pytest.mark.parametrize("case,nranks", [("euler2d", 2), ("adv3d_p4", 2), ("euler3d", 2), ("cfg1", 3)])
+@pytest.mark.parametrize("case,nranks", [("euler2d", 2), ("euler2d_small", 2), ("adv3d_p4", 2), ("euler3d", 2),
+                                          ("cfg1", 3), ("cfg2s_p8", 2)])
 def test_loopback_golden_cases(case, nranks):
-    """Small golden cases (n_c = 4 / 5, 3D, 3 ranks): distributed Jv bit-identical to the reference's."""
+    """Small golden cases (n_c = 4 / 5, small block mode, 3D, 3 ranks): distributed Jv within 1e-12 of the
+    reference's, and distributed GMRES with the reference's own factors (import_factors, element-local)
+    taking the reference's iteration count."""
     z = O.load_raw(case)
     s = T.System.from_golden(z)
     dt = float(z["meta"][5])
     mode = "small" if int(z["meta"][6]) else "full"
     blk = s.n_c * s.npe
+    nb_per_elem = s.n_c if mode == "small" else 1
+    flen = z["factors"].size // max(1, int(np.sum(z["has_factors"])))
 
     def rank_fn(ctx, r):
         op = T.LinearizedOperator(ctx, s, dt, block_mode=mode)
         lo, hi = op.e_begin * blk, op.e_end * blk
-        return lo, hi, op.jacobian_apply(z["jv_in"][lo:hi])
+        jv = op.jacobian_apply(z["jv_in"][lo:hi])
+        has = z["has_factors"][op.e_begin * nb_per_elem:op.e_end * nb_per_elem]
+        first = int(np.sum(z["has_factors"][:op.e_begin * nb_per_elem]))
+        fac = z["factors"][first * flen:(first + int(np.sum(has))) * flen]
+        pc = T.import_factors(op, fac, has)
+        res = T.gmres(op, pc, z["rhs"][lo:hi], T.GmresConfig(tol=1e-10, restart=30, max_iterations=2000))
+        return lo, hi, jv, res.iterations, res.converged
 
-    for lo, hi, jv in run_ranks(nranks, rank_fn):
+    for lo, hi, jv, its, conv in run_ranks(nranks, rank_fn):
         assert O.rel_l2(jv, z["jv_out"][lo:hi]) <= 1e-12
+        assert conv and its == int(z["gmres_meta"][0]), (its, int(z["gmres_meta"][0]))
