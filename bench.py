@@ -337,6 +337,8 @@ def measure_case(T, torch, ctx, dev, args, case, p, rank, world, local_rank, dis
     bytes_mgs = float(np.mean([n_local * 8.0 * (k + 3) for k in ks])) if ks else 0.0
     flops_mgs = float(np.mean([n_local * (4.0 * (k + 1) + 3) for k in ks])) if ks else 0.0
     traffic = load_traffic(case, p)
+    if "mgs_bytes_per_pass" in traffic and ks:  # measured DRAM bytes per pass x the mean pass count (k + 2)
+        traffic["mgs"] = traffic["mgs_bytes_per_pass"] * float(np.mean([k + 2 for k in ks]))
     # FP64 ceiling per kernel family: the bit-faithful 2D apply issues one FP64 instruction per flop
     # (no FMA): half the DFMA rate; 3D apply and the Jv kernels contract with FMA / DMMA
     p_pc = dfma / 2 if sysm.dim == 2 else dmma

@@ -1,0 +1,19 @@
+cd $GRAFT_REPO_ROOT; mkdir -p gpurun_out
+M=dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum
+run() {  # case p regex skip count tag
+  CMD="python bench.py --case $1 --p $2 --steps 1 --warmup 1 --no-extras --no-cpu-baseline --no-clocks --no-profile"
+  timeout 900 ncu --metrics $M --clock-control none -k regex:"$3" -s $4 -c $5 --csv $CMD 2>/dev/null | grep -E "dram__|gpu__time" > gpurun_out/traffic_$6.csv
+  echo "$6 $(wc -l < gpurun_out/traffic_$6.csv)"
+}
+python bench.py --case cfg4 --steps 1 --warmup 1 --no-extras --no-cpu-baseline --no-clocks --no-profile > gpurun_out/plain.log 2>&1 || exit 1
+run cfg4 15 "kron3d_inv|jv3d_fast" 20 2 cfg4_pcjv
+run cfg4 15 "mgs_bulk" 40 1 cfg4_mgs
+run cfg2 15 "kron2d_ew|jv2d_mma" 20 2 cfg2p15_pcjv
+run cfg2 15 "mgs_regv" 40 1 cfg2p15_mgs
+run cfg2 30 "kron2d_ew|fb_panel|jv2d_mma" 30 3 cfg2p30_pcjv
+run cfg2 30 "mgs_bulk" 40 1 cfg2p30_mgs
+ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/r02_launches_cfg4.csv python bench.py --case cfg4 --steps 1 --warmup 1 --no-extras --no-cpu-baseline --no-clocks --no-profile > /dev/null 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/r02_launches_cfg2p15.csv python bench.py --case cfg2 --p 15 --steps 1 --warmup 1 --no-extras --no-cpu-baseline --no-clocks --no-profile > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"kron2d_ew" -s 20 -c 1 -o gpurun_out/r02_cfg2p15_kron2d_ew python bench.py --case cfg2 --p 15 --steps 1 --warmup 1 --no-extras --no-cpu-baseline --no-clocks --no-profile > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"mgs_bulk" -s 40 -c 1 -o gpurun_out/r02_cfg4_mgs_bulk python bench.py --case cfg4 --steps 1 --warmup 1 --no-extras --no-cpu-baseline --no-clocks --no-profile > /dev/null 2>&1
+ls gpurun_out | grep -E "traffic|r02_"
