@@ -16,6 +16,7 @@
 
 #include <cstdlib>
 
+#include "tma.cuh"
 #include "tpdg_internal.hpp"
 
 namespace tpdg_gpu {
@@ -511,34 +512,6 @@ __global__ void __launch_bounds__(kCoopThreads) mgs_regv_kernel(double* __restri
 }
 
 // ---- TMA bulk-copy MGS for large chunks (cfg4, cfg2 p >= 20) --------------------------------
-// mbarrier + cp.async.bulk (the TMA engine's 1D global->shared copy) helpers.
-__device__ __forceinline__ uint32_t smem_u32(const void* p) { return uint32_t(__cvta_generic_to_shared(p)); }
-__device__ __forceinline__ void mbar_init(uint64_t* b, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
-  unsigned ok;
-  do {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n}"
-        : "=r"(ok)
-        : "r"(smem_u32(b)), "r"(parity)
-        : "memory");
-  } while (!ok);
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* b, uint64_t pol) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
-          "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(b)), "l"(pol)
-      : "memory");
-}
-
 // Same passes, element assignment (thread t owns the pairs 2t + 2048 r of its CTA's slice) and
 // accumulation order (r ascending, even/odd elements in s0/s1) as every other MGS kernel, hence
 // bit-identical; the data movement differs: the basis rows a pass needs (v_j, and v_{j-1} for the
@@ -573,7 +546,7 @@ __global__ void __launch_bounds__(NT, 1) mgs_bulk_kernel(double* __restrict__ V,
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], NT / 32);
     }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    mbar_fence_init();
   }
   double2 wr[RW];
 #pragma unroll

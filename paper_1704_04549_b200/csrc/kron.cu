@@ -20,6 +20,7 @@
 
 #include "faithful.cuh"
 #include "mma.cuh"
+#include "tma.cuh"
 #include "tpdg_internal.hpp"
 
 namespace tpdg_gpu {
@@ -1119,16 +1120,19 @@ struct Kron3dInvLayout {
   static constexpr int LDS0 = lda4(QQP), LDA = lda4(K1), LDR = lda4(NCP), LDP = lda4(KQ), LQ = lda4(QP);
   static constexpr int RS = (Q + 1) & ~1;  // padded row segment (G rows, rhs slices): 16-byte aligned
   static constexpr int GS1 = g_row_stride(Q, 1), GS2 = g_row_stride(Q, 2);
-  static constexpr int GMAX = QQ * GS2, S0 = K1 * LDS0 > GMAX ? K1 * LDS0 : GMAX;
-  static constexpr int o_s0 = 0;                       // x staged as [s][(r, j)]: K1 x LDS0; later the G blocks
+  static constexpr int GB = 2 * Q * GS2;   // largest G block (a 2x2 T2 block), doubles
+  static constexpr int NG = 3;             // G ring slots (two blocks in flight ahead of the one in use)
+  static constexpr int mx(int a, int b) { return a > b ? a : b; }
+  // one region, reused: x staged as [s][(r, j)] (GEMM 0) -> P rows (GEMM 1/2) -> G ring (Sylvester) -> Z rows
+  static constexpr int S0 = mx(mx(K1 * LDS0, NCP * LDP), NG * GB);
+  static constexpr int o_s0 = 0;
   static constexpr int o_x = o_s0 + S0;                // Xr[r][(s, j)]: KQ x LDR
-  static constexpr int o_p = o_x + KQ * LDR;           // P / Z rows: NCP x LDP
-  static constexpr int o_a = o_p + NCP * LDP;          // A1^-1: N1P x LDA
+  static constexpr int o_a = o_x + KQ * LDR;           // A1^-1: N1P x LDA
   static constexpr int o_lt = o_a + N1P * LDA;         // L^T, R, Q1, Q2: QP x LQ each
   static constexpr int o_r = o_lt + QP * LQ;
   static constexpr int o_q1 = o_r + QP * LQ;
   static constexpr int o_q2 = o_q1 + QP * LQ;
-  static constexpr int o_t2 = o_q2 + QP * LQ;          // T2 masked to the columns right of each row's block
+  static constexpr int o_t2 = o_q2 + QP * LQ;          // T2
   static constexpr int o_rhs = (o_t2 + QQ + 1) & ~1;   // per warp: 2 parities x 2 columns x SPW slices x RS
   static constexpr int o_lut = o_rhs + NW * 4 * SPW * RS;  // int LUTs: Xr offset of (r, j) = n; P offset of (s, r')
   static constexpr int total = o_lut + (QQP + NCP + 1) / 2 + 1;
@@ -1146,7 +1150,7 @@ __global__ void __launch_bounds__(Kron3dInvLayout<N1, Q>::NTH) kron3d_inv_kernel
   extern __shared__ double sm[];
   double* S0 = sm + L::o_s0;
   double* Xr = sm + L::o_x;
-  double* Pr = sm + L::o_p;
+  double* Pr = sm + L::o_s0;  // aliases S0 (x staging is dead after GEMM 0, the G ring before GEMM 3)
   double* sA = sm + L::o_a;
   double* sLt = sm + L::o_lt;
   double* sR = sm + L::o_r;
@@ -1156,7 +1160,10 @@ __global__ void __launch_bounds__(Kron3dInvLayout<N1, Q>::NTH) kron3d_inv_kernel
   int* lutX = reinterpret_cast<int*>(sm + L::o_lut);  // n = r Q + j -> r LDR + j
   int* lutP = lutX + L::QQP;                          // n = s Q + j -> s Q LDP + j
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  __shared__ int bplan[34];  // T2 quasi-blocks: starts [0, 16), sizes [16, 32), total G length, count
+  // per column k: kind [0, 16) (0 single, 1 second column of a 2x2 block, 2 its first), G offset [16, 32);
+  // per Sylvester step (right to left): G offset [34, 50), bytes [50, 66); [32] total G length, [33] steps
+  __shared__ int bplan[66];
+  __shared__ __align__(8) uint64_t gfull[3], gempty[3];
   const double* ir = pc.irec + size_t(blk) * int(irec3_doubles(N1, Q));
   const double* gG = ir + N1 * N1 + 5 * QQ;
   {
@@ -1179,8 +1186,6 @@ __global__ void __launch_bounds__(Kron3dInvLayout<N1, Q>::NTH) kron3d_inv_kernel
       for (int c = N1; c < K1; ++c) sA[r * LDA + c] = 0.0;
     for (int c = tid; c < LDR; c += NTH)
       for (int r = Q; r < KQ; ++r) Xr[r * LDR + c] = 0.0;
-    for (int r = tid; r < L::NCP; r += NTH)
-      for (int c = Q; c < KQ; ++c) Pr[r * LDP + c] = 0.0;
     for (int c = tid; c < LQ; c += NTH)
       for (int r = Q; r < KQ; ++r) sLt[r * LQ + c] = sR[r * LQ + c] = 0.0;
     for (int r = tid; r < QP; r += NTH)
@@ -1190,7 +1195,7 @@ __global__ void __launch_bounds__(Kron3dInvLayout<N1, Q>::NTH) kron3d_inv_kernel
     cp_async_wait_all();
   }
   __syncthreads();
-  if (tid == 0) {  // per column k: kind (0 single, 1 second column of a 2x2 block, 2 its first) and G offset
+  if (tid == 0) {
     int goff = 0;
     for (int k0 = 0; k0 < Q;) {
       const int sz = (k0 + 1 < Q && sT2[(k0 + 1) * Q + k0] != 0.0) ? 2 : 1;
@@ -1201,6 +1206,19 @@ __global__ void __launch_bounds__(Kron3dInvLayout<N1, Q>::NTH) kron3d_inv_kernel
       k0 += sz;
     }
     bplan[32] = goff;
+    int ns = 0;
+    for (int k = Q - 1; k >= 0; --k) {
+      if (bplan[k] == 2) continue;
+      const int sz = bplan[k] == 0 ? 1 : 2;
+      bplan[34 + ns] = bplan[16 + k];
+      bplan[50 + ns++] = 8 * sz * Q * (sz == 1 ? L::GS1 : L::GS2);
+    }
+    bplan[33] = ns;
+    for (int i = 0; i < L::NG; ++i) {
+      mbar_init(&gfull[i], 1);
+      mbar_init(&gempty[i], NW);
+    }
+    mbar_fence_init();
   }
   const int fr = lane >> 2, fc = 2 * (lane & 3);
   {  // X = A1^-1 x along the outer axis: (N1 x N1)(N1 x Q^2) -> Xr[r][s Q + j]
@@ -1225,13 +1243,8 @@ __global__ void __launch_bounds__(Kron3dInvLayout<N1, Q>::NTH) kron3d_inv_kernel
     }
   }
   __syncthreads();
-  {  // S0 is dead: stage the G blocks there (lands during the two rotations)
-    const int glen = bplan[32];
-    for (int i = 2 * tid; i < glen; i += 2 * NTH) {
-      if (i + 1 < glen) cp_async16(S0 + i, gG + i);
-      else cp_async8(S0 + i, gG + i);
-    }
-  }
+  for (int r = tid; r < L::NCP; r += NTH)  // S0 now holds P: its K padding (column Q) must be zero
+    for (int c = Q; c < KQ; ++c) Pr[r * LDP + c] = 0.0;
   constexpr int NT = L::NCP / 8, NTW = (NT + NW - 1) / NW;
   {  // P = L Xr (L read through L^T) -> P rows (s Q + r', j)
     double acc[QP / 8][NTW][2];
@@ -1274,8 +1287,17 @@ __global__ void __launch_bounds__(Kron3dInvLayout<N1, Q>::NTH) kron3d_inv_kernel
       }
     }
   }
-  cp_async_wait_all();
   __syncthreads();
+  // G ring (TMA): slot u % NG holds the block of Sylvester step u; the first two are issued now (P is dead)
+  auto g_issue = [&](int u) {
+    const int slot = u % L::NG;
+    mbar_expect_tx(&gfull[slot], unsigned(bplan[50 + u]));
+    bulk_g2s(S0 + slot * L::GB, gG + bplan[34 + u], unsigned(bplan[50 + u]), &gfull[slot]);
+  };
+  if (tid == 0) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic accesses to P before the TMA writes
+    for (int u = 0; u < 2 && u < bplan[33]; ++u) g_issue(u);
+  }
   {  // Sylvester T1 Y_s + Y_s T2^T = M_s, T2 columns right to left; thread (s, i), s = SPW warp + lane / Q,
      // holds row i of Y_s in registers (compile-time column indices; the block structure is a uniform branch)
     constexpr int RS = L::RS;
@@ -1287,13 +1309,19 @@ __global__ void __launch_bounds__(Kron3dInvLayout<N1, Q>::NTH) kron3d_inv_kernel
     double yr[Q];
 #pragma unroll
     for (int l = 0; l < Q; ++l) yr[l] = row[l];
-    int par = 0;
+    int par = 0, step = 0;
 #pragma unroll
     for (int k = Q - 1; k >= 0; --k) {
       const int kind = bplan[k];
       if (kind == 2) continue;
       double* rp = rb + par * (2 * SPW * RS);
-      const double* g = S0 + bplan[16 + k];
+      const int slot = step % L::NG;
+      const double* g = S0 + slot * L::GB;
+      if (tid == 0 && step + 2 < bplan[33]) {  // refill the slot freed by step - 1
+        if (step >= 1) mbar_wait(&gempty[(step + 2) % L::NG], unsigned((step - 1) / L::NG) & 1u);
+        g_issue(step + 2);
+      }
+      mbar_wait(&gfull[slot], unsigned(step / L::NG) & 1u);
       if (kind == 0) {
         double s0 = yr[k], s1 = 0.0;
 #pragma unroll
@@ -1350,6 +1378,9 @@ __global__ void __launch_bounds__(Kron3dInvLayout<N1, Q>::NTH) kron3d_inv_kernel
         yr[k - 1] = y0 + z0;
         yr[k] = y1 + z1;
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&gempty[slot]);
+      ++step;
       par ^= 1;
     }
     if (act) {
@@ -1358,6 +1389,8 @@ __global__ void __launch_bounds__(Kron3dInvLayout<N1, Q>::NTH) kron3d_inv_kernel
     }
   }
   __syncthreads();
+  for (int r = tid; r < L::NCP; r += NTH)  // the G ring overwrote P's K padding
+    for (int c = Q; c < KQ; ++c) Pr[r * LDP + c] = 0.0;
   {  // Z = Q1 Y -> Z rows (s Q + r, j')
     double acc[QP / 8][NTW][2];
     zero_tiles(acc);
