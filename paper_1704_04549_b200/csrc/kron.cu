@@ -42,6 +42,11 @@ __device__ __forceinline__ void cp_async4(int* smem, const int* gmem) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem));
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait_group() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
 
 // Quasi-triangular diagonal block structure (tensor/sylvester.hpp:16-30); returns block count.
 __device__ int quasi_blocks_dev(const double* t, int n, int* start, int* size) {
@@ -272,9 +277,6 @@ size_t kron2d_smem(const DevPC& pc) {
 // 64 threads per element keep many elements resident per SM. Same arithmetic as above.
 constexpr int kSizedThreads = 64;
 
-#ifndef SYLV_FAST
-#define SYLV_FAST 0  // sized kernel: 1 = sylv_fast (lane per entry, measured 167 us at p=15) vs 132 us for the wavefront
-#endif
 #ifndef KRON_SKIP
 #define KRON_SKIP 0  // study builds only: bit mask of skipped phases (tools/kron_variants.sh)
 #endif
@@ -301,6 +303,72 @@ __device__ __forceinline__ void lu_fiber_reg(const double* __restrict__ lu, cons
   }
 #pragma unroll
   for (int k = 0; k < N; ++k) col[k * stride] = x[k];
+}
+
+// Same solve for long fibers (N > 32) whose LU stays in global memory (lu_g): the NF fibers
+// (columns c < NF of X, one per lane) are permuted into a shared scratch column (tmp) and solved
+// there, and the LU rows stream through a D-deep shared ring (cp.async, issued D - 1 rows ahead)
+// so that every row is read from L2 once and broadcast from shared memory to the chains.
+template <int N, int NF>
+__device__ __forceinline__ void lu_cols_ring(const double* __restrict__ lu_g, const double* __restrict__ rcp,
+                                             const int* __restrict__ perm, double* X, int ld, double* tmp,
+                                             double* ring, int lane) {
+  constexpr int D = 4;
+  static_assert(NF <= 32 && N % 2 == 0, "one fiber per lane, 16-byte row copies");
+  auto issue = [&](int r) {
+    for (int i = 2 * lane; i < N; i += 64) cp_async16(ring + (r % D) * N + i, lu_g + size_t(r) * N + i);
+  };
+  const bool act = lane < NF;
+  const int c = lane;
+  if (act)
+#pragma unroll 1
+    for (int k = 0; k < N; ++k) tmp[k * ld + c] = X[perm[k] * ld + c];
+  // forward (unit lower, j ascending), rows 1 .. N-1
+#pragma unroll
+  for (int u = 1; u < D; ++u) {
+    if (u < N) issue(u);
+    cp_async_commit();
+  }
+#pragma unroll 1
+  for (int r = 1; r < N; ++r) {
+    if (r + D - 1 < N) issue(r + D - 1);
+    cp_async_commit();
+    cp_async_wait_group<D - 1>();
+    __syncwarp();
+    if (act) {
+      const double* L = ring + (r % D) * N;
+      double s = tmp[r * ld + c];
+#pragma unroll 8
+      for (int j = 0; j < r; ++j) s = fmsc(s, L[j], tmp[j * ld + c]);
+      tmp[r * ld + c] = s;
+    }
+    __syncwarp();
+  }
+  // backward (j ascending after the diagonal), rows N-1 .. 0
+#pragma unroll
+  for (int u = 0; u < D - 1; ++u) {
+    if (N - 1 - u >= 0) issue(N - 1 - u);
+    cp_async_commit();
+  }
+#pragma unroll 1
+  for (int r = N - 1; r >= 0; --r) {
+    if (r - (D - 1) >= 0) issue(r - (D - 1));
+    cp_async_commit();
+    cp_async_wait_group<D - 1>();
+    __syncwarp();
+    if (act) {
+      const double* U = ring + (r % D) * N;
+      double s = tmp[r * ld + c];
+#pragma unroll 8
+      for (int j = r + 1; j < N; ++j) s = fmsc(s, U[j], tmp[j * ld + c]);
+      tmp[r * ld + c] = fdiv_rcp(s, U[r], rcp[r]);
+    }
+    __syncwarp();
+  }
+  if (act)
+#pragma unroll 1
+    for (int k = 0; k < N; ++k) X[k * ld + c] = tmp[k * ld + c];
+  __syncwarp();
 }
 
 // Warp-level tiled product O = op(A) op(B) (R x K x C), lane tile TI x TJ; each output still
@@ -638,18 +706,22 @@ __device__ __forceinline__ void sylv_wavefront(const double* T1, const double* T
 }
 
 // Faithful quasi-triangular Sylvester solve (sylvester.hpp:72-127) of one block by one warp, in
-// place on X (ld): the block anti-diagonal wavefront with one lane per Sylvester entry. Cells of
-// a step are processed in groups of gs lanes (gs = the largest cell of the block: 1, 2 or 4), so
-// 32 / gs cells per pass. Each lane forms its entry's right-hand side in the reference order
-// (B, then the solved rows below j ascending, then the solved columns to the right l ascending,
-// separate mul / sub roundings); the gs lanes of a cell exchange their right-hand sides with
-// shuffles and each replays the cell's factored tiny system (sylv_cells_kernel), whose slot is
-// loaded before the chains so that its latency hides behind them. 1 x 1 cells divide by
-// t1_ii + t2_kk directly (solve_tiny<1>). The singular flag comes from the plan (sylv_cells).
-template <int N1, int N2>
-__device__ __forceinline__ void sylv_fast(const double* __restrict__ T1, const double* __restrict__ T2, double* X,
-                                          int ld, const int* sb, const double* __restrict__ cc, int lane,
-                                          int* status) {
+// place on X (ld), for a T1 that stays in global memory (kron2d_sized_kernel<.., GREC>): the block
+// anti-diagonal wavefront with one lane per Sylvester entry, and the rows of T1 the current step
+// reads held in a window of R rows in shared memory (win, slot = row % R). The steps move down T1
+// (the active block rows at step st are the ones below nb1 - 1 - st, at most nb2 blocks), so the
+// rows entering at step st + 1 are prefetched with cp.async while step st runs; a step whose rows
+// do not fit in the window reads T1 from global memory. Cells of a step are processed in groups
+// of gs lanes (gs = the largest cell of the block: 1, 2 or 4), so 32 / gs cells per pass. Each lane
+// forms its entry's right-hand side in the reference order (B, then the solved rows below j
+// ascending, then the solved columns to the right l ascending, separate mul / sub roundings); the
+// gs lanes of a cell exchange their right-hand sides with shuffles and each replays the cell's
+// factored tiny system (sylv_cells_kernel). 1 x 1 cells divide by t1_ii + t2_kk (solve_tiny<1>).
+template <int N1, int N2, int R>
+__device__ __forceinline__ void sylv_window(const double* __restrict__ T1g, const double* __restrict__ T2, double* X,
+                                            int ld, const int* sb, const double* __restrict__ cc, double* win,
+                                            int lane, int* status) {
+  static_assert(N1 % 2 == 0, "16-byte row copies");
   const int nb1 = sb[0], nb2 = sb[1];
   const int *s1 = sb + 4, *z1 = s1 + N1, *s2 = z1 + N1, *z2 = s2 + N2;
   if (sb[3] && lane == 0) atomicExch(status, int(TPDG_SINGULAR));
@@ -657,7 +729,48 @@ __device__ __forceinline__ void sylv_fast(const double* __restrict__ T1, const d
   const int gs = 1 << lg, per = 32 >> lg;
   const int g = lane >> lg, e = lane & (gs - 1), gbase = g << lg;
   const int last = nb1 + nb2 - 2;
+  // rows of T1 read at step st: the block rows d1 in [d1lo, d1hi] (bi = nb1 - 1 - d1)
+  auto rows = [&](int st, int& lo, int& hi) {
+    const int d1lo = st - (nb2 - 1) > 0 ? st - (nb2 - 1) : 0;
+    const int d1hi = st < nb1 - 1 ? st : nb1 - 1;
+    lo = s1[nb1 - 1 - d1hi];
+    hi = s1[nb1 - 1 - d1lo] + z1[nb1 - 1 - d1lo] - 1;
+  };
+  auto load_rows = [&](int a, int b) {  // rows a..b into their slots (cp.async, this lane's share)
+    for (int r = a; r <= b; ++r)
+      for (int i = 2 * lane; i < N1; i += 64) cp_async16(win + (r % R) * N1 + i, T1g + size_t(r) * N1 + i);
+  };
+  int res_lo = 0, res_hi = -1;  // resident rows (empty)
+  auto ensure = [&](int st) {  // make the rows of step st resident, synchronously; false if they do not fit
+    int lo, hi;
+    rows(st, lo, hi);
+    if (hi - lo + 1 > R) {
+      res_lo = 0;
+      res_hi = -1;
+      return;
+    }
+    if (res_hi < res_lo || hi < res_lo || lo > res_hi) load_rows(lo, hi);
+    else if (lo < res_lo) load_rows(lo, res_lo - 1);
+    cp_async_commit();
+    cp_async_wait_group<0>();
+    __syncwarp();
+    res_lo = lo;
+    res_hi = hi;
+  };
+  ensure(0);
   for (int st = 0; st <= last; ++st) {
+    int lo, hi;
+    rows(st, lo, hi);
+    const bool inwin = res_hi >= res_lo && lo >= res_lo && hi <= res_hi;
+    if (st < last && inwin) {  // prefetch the rows entering at st + 1 if their slots are free now
+      int lo1, hi1;
+      rows(st + 1, lo1, hi1);
+      if (hi - lo1 + 1 <= R && lo1 < res_lo) {
+        load_rows(lo1, res_lo - 1);
+        res_lo = lo1;
+      }
+      cp_async_commit();
+    }
     const int d1lo = st - (nb2 - 1) > 0 ? st - (nb2 - 1) : 0;
     const int d1hi = st < nb1 - 1 ? st : nb1 - 1;
     const int ncell = d1hi - d1lo + 1;
@@ -675,6 +788,7 @@ __device__ __forceinline__ void sylv_fast(const double* __restrict__ T1, const d
       const int ns = isz * ksz;
       const bool act = ok && e < ns;
       const int i = i0 + (ksz == 2 ? e >> 1 : e), k = k0 + (ksz == 2 ? e & 1 : 0);
+      const double* t1r = inwin ? win + (i % R) * N1 : T1g + size_t(i) * N1;  // row i of T1
       // the cell's factored system (ns > 1), loaded ahead of the chains
       double cf[22];
       cf[0] = 0.0;
@@ -684,22 +798,22 @@ __device__ __forceinline__ void sylv_fast(const double* __restrict__ T1, const d
 #pragma unroll
         for (int u = 0; u < 21; ++u) cf[u] = (ok && u < ncf) ? __ldg(slot + u) : 0.0;
       }
-      double s = 0.0;
+      double s = 0.0, diag = 0.0;
       if (act) {
         s = X[i * ld + k];
+        diag = ns == 1 ? fadd(t1r[i0], T2[k0 * N2 + k0]) : 0.0;
         const int jf = i0 + isz, lf = k0 + ksz;
-        const double* pt = T1 + i * N1 + jf;
         const double* py = X + jf * ld + k;
 #pragma unroll 4
-        for (int t = 0; t < N1 - jf; ++t) s = fmsc(s, pt[t], py[t * ld]);
-        pt = T2 + k * N2 + lf;
+        for (int t = 0; t < N1 - jf; ++t) s = fmsc(s, t1r[jf + t], py[t * ld]);
+        const double* pt = T2 + k * N2 + lf;
         py = X + i * ld + lf;
 #pragma unroll 4
         for (int t = 0; t < N2 - lf; ++t) s = fmsc(s, pt[t], py[t]);
       }
       double y = 0.0;
       if (lg == 0) {
-        if (act) y = fdiv(s, fadd(T1[i0 * N1 + i0], T2[k0 * N2 + k0]));
+        if (act) y = fdiv(s, diag);
       } else {
         const long long code = __double_as_longlong(cf[0]);
         double b[4];
@@ -709,14 +823,20 @@ __device__ __forceinline__ void sylv_fast(const double* __restrict__ T1, const d
           b[u] = __shfl_sync(0xffffffffu, s, gbase + (src & (gs - 1)));
         }
         if (act) {
-          if (ns == 1) y = fdiv(s, fadd(T1[i0 * N1 + i0], T2[k0 * N2 + k0]));
+          if (ns == 1) y = fdiv(s, diag);
           else if (ns == 2) y = cell_solve<2>(cf, b, e);
           else y = cell_solve<4>(cf, b, e);
         }
       }
       if (act) X[i * ld + k] = y;
     }
-    __syncwarp();
+    if (st < last) {
+      if (inwin) cp_async_wait_group<0>();
+      __syncwarp();
+      ensure(st + 1);
+    } else {
+      __syncwarp();
+    }
   }
 }
 
@@ -731,27 +851,39 @@ struct Kron2dWarpLayout {
   static constexpr int ints = N1 + N2;
   static constexpr int per = xsz + rec + ((N1 + N2 + 1) & ~1) + hdr + (ints + 1) / 2;
   static constexpr int per_even = (per + 1) & ~1;
+  // GREC: the record stays in global memory (read through L1) and only X, the product scratch,
+  // the reciprocals and the plan live in shared memory (large N1: cfg3's n_c q = 64 record is 104 KB)
+  static constexpr int per_g = 2 * xsz + 4 * N1 + 3 * N2 * N2 + ((N1 + N2 + 1) & ~1) + hdr + (ints + 1) / 2;
+  static constexpr int per_g_even = (per_g + 1) & ~1;
 };
 
-template <int N1, int N2>
+template <int N1, int N2, bool GREC = false>
 __global__ void __launch_bounds__(kSizedThreads) kron2d_sized_kernel(DevPC pc, const double* __restrict__ in,
                                                                       double* __restrict__ out) {
   using L = Kron2dWarpLayout<N1, N2>;
+  static_assert(GREC || N1 <= 32, "register fibers");
+  static_assert(!GREC || N2 <= 32, "lu_cols_ring: one column fiber per lane");
   constexpr int ld = L::ld, rec = L::rec, hdr = L::hdr;
   extern __shared__ double sm_all[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int blk = blockIdx.x * (kSizedThreads / 32) + warp;
   if (blk >= pc.nblk || pc.kind[blk] == 0 || (pc.skip && *pc.skip)) return;
-  double* sX = sm_all + size_t(warp) * L::per_even;
+  double* sX = sm_all + size_t(warp) * (GREC ? L::per_g_even : L::per_even);
+  const double* gR = pc.rec + size_t(blk) * rec;
   double* sR = sX + L::xsz;
   double* sT = sR;  // product scratch: aliases LU(A2), LU(B1) once both fiber solves are done
-  double* sRcp = sR + rec;
+  double* sSmall = sR + L::xsz;  // GREC: LU(B1), Q2, T2 (3 N2^2) staged in shared memory
+  double* sRing = sSmall + 3 * N2 * N2;  // GREC: 4-row ring of LU(A2)
+  double* sRcp = sR + (GREC ? L::xsz + 3 * N2 * N2 + 4 * N1 : rec);
   double* sH = sRcp + ((N1 + N2 + 1) & ~1);  // Sylvester plan header (ints)
   int* sPiv = reinterpret_cast<int*>(sH + hdr);
   const double* cells = pc.cells + size_t(blk) * pc.cells_len;
   {  // asynchronous global -> shared copies (LDGSTS), one round trip for the whole record
-    const double* r = pc.rec + size_t(blk) * rec;
-    if ((reinterpret_cast<uintptr_t>(r) & 15) == 0) {
+    const double* r = gR;
+    if (GREC) {
+      for (int i = lane; i < N2 * N2; i += 32) cp_async8(sSmall + i, r + N1 * N1 + i);
+      for (int i = lane; i < 2 * N2 * N2; i += 32) cp_async8(sSmall + N2 * N2 + i, r + 3 * N1 * N1 + N2 * N2 + i);
+    } else if ((reinterpret_cast<uintptr_t>(r) & 15) == 0) {
       for (int i = 2 * lane; i + 1 < rec; i += 64) cp_async16(sR + i, r + i);
       if ((rec & 1) && lane == 0) sR[rec - 1] = r[rec - 1];
     } else {
@@ -764,18 +896,22 @@ __global__ void __launch_bounds__(kSizedThreads) kron2d_sized_kernel(DevPC pc, c
     cp_async_wait_all();
   }
   __syncwarp();
-  const double* luA2 = sR;
-  const double* luB1 = luA2 + N1 * N1;
-  const double* Q1 = luB1 + N2 * N2;
+  const double* luA2 = GREC ? gR : sR;
+  const double* luB1 = GREC ? sSmall : luA2 + N1 * N1;
+  const double* Q1 = luA2 + N1 * N1 + N2 * N2;
   const double* T1 = Q1 + N1 * N1;
-  const double* Q2 = T1 + N1 * N1;
+  const double* Q2 = GREC ? sSmall + N2 * N2 : T1 + N1 * N1;
   const double* T2 = Q2 + N2 * N2;
   for (int i = lane; i < N1 + N2; i += 32)
     sRcp[i] = __drcp_rn(i < N1 ? luA2[i * N1 + i] : luB1[(i - N1) * N2 + i - N1]);
   __syncwarp();
   if (!(KRON_SKIP & 1)) {
   // (A2^{-1} (x) I): one column fiber per lane
-  for (int c = lane; c < N2; c += 32) lu_fiber_reg<N1>(luA2, sRcp, sPiv, sX + c, ld);
+  if constexpr (GREC) {
+    lu_cols_ring<N1, N2>(luA2, sRcp, sPiv, sX, ld, sT, sRing, lane);
+  } else {
+    for (int c = lane; c < N2; c += 32) lu_fiber_reg<N1>(luA2, sRcp, sPiv, sX + c, ld);
+  }
   __syncwarp();
   // (I (x) B1^{-1}): one row fiber per lane
   for (int r = lane; r < N1; r += 32) lu_fiber_reg<N2>(luB1, sRcp + N1, sPiv + N1, sX + r * ld, 1);
@@ -790,8 +926,8 @@ __global__ void __launch_bounds__(kSizedThreads) kron2d_sized_kernel(DevPC pc, c
   if (!(KRON_SKIP & 4)) {  // Y overwrites M in place (sX): T1 Y + Y T2^T = M, block anti-diagonal wavefront
     const int* sb = reinterpret_cast<const int*>(sH);
     const double* cc = cells + hdr;
-    if (SYLV_FAST) {
-      sylv_fast<N1, N2>(T1, T2, sX, ld, sb, cc, lane, pc.status);
+    if constexpr (GREC) {  // T1 rows through a shared window in the (free) product scratch
+      sylv_window<N1, N2, ld>(T1, T2, sX, ld, sb, cc, sT, lane, pc.status);
     } else if (sb[2]) {  // 1 x 1 blocks: one lane per cell; solve_tiny<1> is y = r / (t1_ii + t2_kk)
       const int nb1 = sb[0], nb2 = sb[1];
       for (int step = 0; step <= nb1 + nb2 - 2; ++step) {
@@ -821,32 +957,34 @@ __global__ void __launch_bounds__(kSizedThreads) kron2d_sized_kernel(DevPC pc, c
   warp_mm<N1, N2, N2, false, true, 2, 4>(sT, ld, Q2, N2, out + size_t(blk) * (N1 * N2), N2, lane);  // (.) Q2^T
 }
 
-template <int N1, int N2>
+template <int N1, int N2, bool GREC = false>
 size_t kron2d_sized_smem() {
-  return sizeof(double) * size_t(Kron2dWarpLayout<N1, N2>::per_even) * (kSizedThreads / 32);
+  using L = Kron2dWarpLayout<N1, N2>;
+  return sizeof(double) * size_t(GREC ? L::per_g_even : L::per_even) * (kSizedThreads / 32);
 }
 
-template <int N1, int N2>
+template <int N1, int N2, bool GREC = false>
 bool try_kron2d_sized(const DevPC& pc, const double* in, double* out, cudaStream_t st) {
   if (pc.n1 != N1 || pc.q != N2) return false;
   static bool configured = false;
-  const size_t smem = kron2d_sized_smem<N1, N2>();
+  const size_t smem = kron2d_sized_smem<N1, N2, GREC>();
   if (!configured) {
-    TPDG_CUDA_CHECK(cudaFuncSetAttribute(kron2d_sized_kernel<N1, N2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(smem)));
-    TPDG_CUDA_CHECK(cudaFuncSetAttribute(kron2d_sized_kernel<N1, N2>,
+    TPDG_CUDA_CHECK(cudaFuncSetAttribute(kron2d_sized_kernel<N1, N2, GREC>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    TPDG_CUDA_CHECK(cudaFuncSetAttribute(kron2d_sized_kernel<N1, N2, GREC>,
                                          cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     configured = true;
   }
   const int per_cta = kSizedThreads / 32;
-  kron2d_sized_kernel<N1, N2><<<(pc.nblk + per_cta - 1) / per_cta, kSizedThreads, smem, st>>>(pc, in, out);
+  kron2d_sized_kernel<N1, N2, GREC><<<(pc.nblk + per_cta - 1) / per_cta, kSizedThreads, smem, st>>>(pc, in, out);
   return true;
 }
 
 bool launch_kron2d_sized(const DevPC& pc, const double* in, double* out, cudaStream_t st) {
   return try_kron2d_sized<5, 5>(pc, in, out, st) || try_kron2d_sized<9, 9>(pc, in, out, st) ||
          try_kron2d_sized<16, 16>(pc, in, out, st) || try_kron2d_sized<21, 21>(pc, in, out, st) ||
-         try_kron2d_sized<31, 31>(pc, in, out, st);
+         try_kron2d_sized<31, 31>(pc, in, out, st) ||
+         try_kron2d_sized<64, 16, true>(pc, in, out, st);  // cfg3 stand-in: n_c = 4, q = 16
 }
 
 // ------------------------------------------------------------------------------------ 3D, sized

@@ -99,3 +99,57 @@ def test_residual_and_newton_step(ctx, case):
     assert err_r <= 1e-12
     assert st.newton_steps == int(z["newton_steps"][0]) and st.gmres_per_solve == ref_g
     assert err_u <= 1e-10
+
+
+def _euler_slice(ctx, kind, n, p, K, dt):
+    """The first K elements of a configured-size stand-in (neighbours wrapped into the slice: the PC is
+    element-local), as a device System and as an oracle System on the same arrays."""
+    s = build(ctx, kind, n, p)
+    a, mu, q, nc, d = s.arrays, s.mu, p + 1, s.n_c, s.dim
+    nf, nq, nfc = 2 * d, mu ** d, mu ** (d - 1)
+    conn = a["conn"][: K * nf * 3].reshape(K, nf, 3).copy()
+    conn[:, :, 0] %= K
+    arrays = {"g": a["g"], "d": a["d"], "gw": a["gw"], "dw": a["dw"], "w": a["w"],
+              "jdet": a["jdet"][: K * nq], "face_w": a["face_w"][: K * nf * nfc], "conn": conn.ravel(),
+              "dft": a["dft"][: K * d * nq * nc * nc], "dfm": a["dfm"][: K * nf * nfc * nc * nc],
+              "dfp": a["dfp"][: K * nf * nfc * nc * nc]}
+    sub = T.System(d, nc, p, mu, K, arrays)
+    ometa = np.array([d, nc, p, mu, K, dt, 0, n[0], n[1], n[2], 1.0, 1.0])
+    ov = {"meta": ometa, "ref_g": a["g"], "ref_d": a["d"], "ref_gw": a["gw"], "ref_dw": a["dw"], "ref_w": a["w"],
+          "jdet": arrays["jdet"], "face_w": arrays["face_w"], "conn": arrays["conn"], "dft": arrays["dft"],
+          "dfm": arrays["dfm"], "dfp": arrays["dfp"]}
+    if d == 2:
+        ov["start_vec"] = T.seeded_unit_vector(q * q)
+    else:
+        ov["start_vec"], ov["start_vec2"] = T.seeded_unit_vector(q ** 4), T.seeded_unit_vector(q * q)
+    return sub, O.System(ov)
+
+
+@pytest.mark.parametrize("case,K", [("cfg3", 48), ("cfg5", 24)])
+def test_standin_configured_degree_pc_apply(ctx, case, K):
+    """The sized apply kernels of the stand-ins at their configured degree (cfg3: n_c q = 64 x q = 16,
+    kron2d_sized_kernel<64, 16, GREC>; cfg5: 40 x 8 x 8): the reference's LU / Schur record imported and
+    applied, bit for bit against the reference's apply of the same record; and the GPU-formed
+    preconditioner against the reference's within 1e-12."""
+    kind, n, p = FULL[case]
+    dt = float(O.load_raw(case)["meta"][5])
+    sub, osys = _euler_slice(ctx, kind, n, p, K, dt)
+    opc = osys.form()
+    has = opc.has()
+    fb = [b for b in range(K) if has[b]]
+    fac = np.concatenate([opc.factors(b) for b in fb])
+    rec = [opc.record(b) for b in fb]
+    op = T.LinearizedOperator(ctx, sub, dt)
+    pc_r = T.import_record(op, fac, has, np.concatenate([r for r, _ in rec]), np.concatenate([pv for _, pv in rec]))
+    x = T.uniform_vector(7, sub.N, 1.0)
+    ref = opc.apply(x)
+    y = pc_r.apply(x)
+    err_r = O.rel_l2(y, ref)
+    pc = T.form_ksvd(op)
+    err_f = O.rel_l2(pc.apply(x), ref)
+    print(f"{case} slice: {len(fb)}/{K} factored, imported-record apply identical to the reference's: "
+          f"{np.array_equal(y, ref)} (rel-L2 {err_r:.3e}); GPU-formed apply {err_f:.3e}")
+    assert sorted(e for e, _ in pc.fallbacks) == [b for b in range(K) if not has[b]]
+    if case == "cfg3":
+        assert np.array_equal(y, ref)
+    assert err_r <= 1e-12 and err_f <= 1e-12
