@@ -194,6 +194,7 @@ struct tpdg_gpu_op_s {
   DevBuf g, d, gw, dw, w, jdet, face_w, dft, dfm, dfp, conn, halo;
   DevBuf cdfm, cdfp;                 // -b fw dfm, -b fw dfp (folded face data of the fast 3D operator)
   DevBuf pw;                         // 3D n_c = 1: interleaved point-wise coefficients (jv3d.cu)
+  DevBuf dftr;                       // 3D n_c > 1: dft by output component, [e][r][dir][point][c] (jv.cu)
   std::vector<double> hg, hgw, hdw;  // host copies of the 1D matrices (kernel-parameter packing)
   DevBuf io_a, io_b;  // staging for the host-pointer entry points
   DevBuf shuf_ws;
@@ -277,6 +278,7 @@ DevSys make_devsys(const tpdg_gpu_op_s& op, int block_mode, double a, double b) 
   s.cdfm = op.cdfm.as<double>();
   s.cdfp = op.cdfp.as<double>();
   s.pw = op.pw.as<double>();
+  s.dftr = op.dftr.as<double>();
   s.hg = op.hg.empty() ? nullptr : op.hg.data();
   s.hgw = op.hgw.empty() ? nullptr : op.hgw.data();
   s.hdw = op.hdw.empty() ? nullptr : op.hdw.data();
@@ -984,6 +986,17 @@ int tpdg_gpu_op_create(tpdg_gpu_ctx ctx, const tpdg_gpu_system* sys, double dt, 
             for (int r = 0; r < 3; ++r) o[1 + r] = bb * df[(e * 3 + r) * nqv + q0];
           }
         upload(op->pw, pw.data(), pw.size(), st);
+      }
+      if (d == 3 && nc > 1) {  // row r of every point's flux Jacobian contiguous over the points
+        std::vector<double> tr(nl * 3 * nqv * ncc);
+        const double* df = sys->dft + size_t(e_begin) * 3 * nqv * ncc;
+        for (size_t e = 0; e < nl; ++e)
+          for (int dir = 0; dir < 3; ++dir)
+            for (size_t q0 = 0; q0 < nqv; ++q0)
+              for (int r = 0; r < nc; ++r)
+                for (int c = 0; c < nc; ++c)
+                  tr[(((e * nc + r) * 3 + dir) * nqv + q0) * nc + c] = df[((e * 3 + dir) * nqv + q0) * ncc + r * nc + c];
+        upload(op->dftr, tr.data(), tr.size(), st);
       }
       TPDG_CUDA_CHECK(cudaStreamSynchronize(st));
     }

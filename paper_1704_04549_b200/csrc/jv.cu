@@ -26,12 +26,14 @@ __device__ __forceinline__ const double* nbr_block(const DevSys& s, const double
 }
 
 // ------------------------------------------------------------------------------------ 2D
-__global__ void __launch_bounds__(256) jv2d_kernel(DevSys s, const double* __restrict__ vin,
+// NC, Q, MU: compile-time sizes of an instantiated system (0: runtime, from s)
+template <int NT, int NC = 0, int Q = 0, int MU = 0>
+__global__ void __launch_bounds__(NT) jv2d_kernel(DevSys s, const double* __restrict__ vin,
                                                     const double* __restrict__ halo, double* __restrict__ vout) {
   extern __shared__ double sm[];
   if (s.skip && *s.skip) return;
   const int e = s.e_lo + blockIdx.x;
-  const int q = s.q, mu = s.mu, nc = s.n_c, qq = q * q, mm = mu * mu;
+  const int q = Q ? Q : s.q, mu = MU ? MU : s.mu, nc = NC ? NC : s.n_c, qq = q * q, mm = mu * mu;
   const int tid = threadIdx.x, nt = blockDim.x;
   double* sG = sm;                 // mu*q
   double* sGW = sG + mu * q;       // q*mu
@@ -379,12 +381,13 @@ __device__ __forceinline__ int flat_face_node(int q, int f, int j0, int j1) {
   return (idx[2] * q + idx[1]) * q + idx[0];
 }
 
-__global__ void __launch_bounds__(256) jv3d_kernel(DevSys s, const double* __restrict__ vin,
+template <int NT, int NC = 0, int Q = 0, int MU = 0>
+__global__ void __launch_bounds__(NT) jv3d_kernel(DevSys s, const double* __restrict__ vin,
                                                     const double* __restrict__ halo, double* __restrict__ vout) {
   extern __shared__ double sm[];
   if (s.skip && *s.skip) return;
   const int e = s.e_lo + blockIdx.x;
-  const int q = s.q, mu = s.mu, nc = s.n_c;
+  const int q = Q ? Q : s.q, mu = MU ? MU : s.mu, nc = NC ? NC : s.n_c;
   const int q3 = q * q * q, m3 = mu * mu * mu, m2 = mu * mu, q2 = q * q;
   const int tid = threadIdx.x, nt = blockDim.x;
   double* sG = sm;
@@ -502,9 +505,11 @@ __global__ void __launch_bounds__(256) jv3d_kernel(DevSys s, const double* __res
   // ---- per output component r: fields, three integrate_back contractions
   for (int r = 0; r < nc; ++r) {
     for (int idx = tid; idx < m3; idx += nt) {
-      const double* d0 = s.dft + ((size_t(e) * 3 + 0) * m3 + idx) * nc * nc + r * nc;
-      const double* d1 = s.dft + ((size_t(e) * 3 + 1) * m3 + idx) * nc * nc + r * nc;
-      const double* d2 = s.dft + ((size_t(e) * 3 + 2) * m3 + idx) * nc * nc + r * nc;
+      // row r of the point's three flux Jacobians (coalesced over the points from the regrouped copy)
+      const double* d0 = s.dftr ? s.dftr + ((size_t(e) * nc + r) * 3 * m3 + idx) * nc
+                                : s.dft + ((size_t(e) * 3 + 0) * m3 + idx) * nc * nc + r * nc;
+      const double* d1 = s.dftr ? d0 + size_t(m3) * nc : s.dft + ((size_t(e) * 3 + 1) * m3 + idx) * nc * nc + r * nc;
+      const double* d2 = s.dftr ? d1 + size_t(m3) * nc : s.dft + ((size_t(e) * 3 + 2) * m3 + idx) * nc * nc + r * nc;
       double f0 = 0.0, f1 = 0.0, f2 = 0.0;
       if (!s.small) {
         for (int c = 0; c < nc; ++c) {
@@ -877,6 +882,15 @@ size_t jv3d_smem(const DevSys& s) {
 
 size_t jv_smem_bytes(const DevSys& s) { return s.dim == 2 ? jv2d_smem(s) : jv3d_smem(s); }
 
+namespace {
+template <typename K>
+void launch_generic(K kernel, int nt, size_t smem, const DevSys& s, const double* vin, const double* halo,
+                    double* vout, cudaStream_t st) {
+  TPDG_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  kernel<<<s.e_hi - s.e_lo, nt, smem, st>>>(s, vin, halo, vout);
+}
+}  // namespace
+
 void launch_jv(const DevSys& s, const double* vin, const double* halo, double* vout, cudaStream_t st) {
   if (s.e_hi <= s.e_lo) return;
   const size_t smem = jv_smem_bytes(s);
@@ -890,20 +904,20 @@ void launch_jv(const DevSys& s, const double* vin, const double* halo, double* v
     ++g_launches;
     return;
   }
+  // generic (runtime-size) kernels, one CTA per element; systems (n_c > 1) use wider CTAs: their
+  // shared-memory footprint allows one or two CTAs per SM, so the stages need more threads
+  // (instances with compile-time sizes for the BASELINE systems: cfg3 2D n_c = 4, q = 16; cfg5 3D n_c = 5, q = 8)
+  const bool full = !s.small;
   if (s.dim == 2) {
-    static size_t configured = 0;
-    if (smem > configured) {
-      TPDG_CUDA_CHECK(cudaFuncSetAttribute(jv2d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-      configured = smem;
-    }
-    jv2d_kernel<<<s.e_hi - s.e_lo, 256, smem, st>>>(s, vin, halo, vout);
+    if (full && s.n_c == 4 && s.q == 16 && s.mu == 17)
+      launch_generic(jv2d_kernel<512, 4, 16, 17>, 512, smem, s, vin, halo, vout, st);
+    else if (s.n_c > 1) launch_generic(jv2d_kernel<512>, 512, smem, s, vin, halo, vout, st);
+    else launch_generic(jv2d_kernel<256>, 256, smem, s, vin, halo, vout, st);
   } else {
-    static size_t configured = 0;
-    if (smem > configured) {
-      TPDG_CUDA_CHECK(cudaFuncSetAttribute(jv3d_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-      configured = smem;
-    }
-    jv3d_kernel<<<s.e_hi - s.e_lo, 256, smem, st>>>(s, vin, halo, vout);
+    if (full && s.n_c == 5 && s.q == 8 && s.mu == 9)
+      launch_generic(jv3d_kernel<1024, 5, 8, 9>, 1024, smem, s, vin, halo, vout, st);
+    else if (s.n_c > 1) launch_generic(jv3d_kernel<1024>, 1024, smem, s, vin, halo, vout, st);
+    else launch_generic(jv3d_kernel<256>, 256, smem, s, vin, halo, vout, st);
   }
   TPDG_CUDA_CHECK(cudaGetLastError());
   ++g_launches;

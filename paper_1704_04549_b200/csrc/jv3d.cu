@@ -52,19 +52,6 @@ __device__ __forceinline__ double cld(const double* p) {
   return r;
 }
 
-// Global loads whose issue point is pinned in program order relative to the (volatile) weight loads,
-// so a column pass keeps only a one-point-deep prefetch in registers.
-__device__ __forceinline__ double ldg_pin(const double* p) {
-  double r;
-  asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(r) : "l"(p));
-  return r;
-}
-__device__ __forceinline__ double2 ldg2_pin(const double* p) {
-  double2 r;
-  asm volatile("ld.global.nc.v2.f64 {%0,%1}, [%2];" : "=d"(r.x), "=d"(r.y) : "l"(p));
-  return r;
-}
-
 template <int SLOT, int Q, int MU>
 struct Jv3dW {
   __device__ __forceinline__ static double G(int i) { return cld(&c_jv3d[SLOT][i]); }

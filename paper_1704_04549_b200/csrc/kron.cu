@@ -37,10 +37,6 @@ __device__ __forceinline__ void cp_async8(double* smem, const double* gmem) {
   const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
 }
-__device__ __forceinline__ void cp_async4(int* smem, const int* gmem) {
-  const unsigned sa = static_cast<unsigned>(__cvta_generic_to_shared(smem));
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gmem));
-}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
@@ -277,9 +273,6 @@ size_t kron2d_smem(const DevPC& pc) {
 // 64 threads per element keep many elements resident per SM. Same arithmetic as above.
 constexpr int kSizedThreads = 64;
 
-#ifndef KRON_SKIP
-#define KRON_SKIP 0  // study builds only: bit mask of skipped phases (tools/kron_variants.sh)
-#endif
 
 template <int N>
 __device__ __forceinline__ void lu_fiber_reg(const double* __restrict__ lu, const double* __restrict__ rcp,
@@ -905,7 +898,6 @@ __global__ void __launch_bounds__(kSizedThreads) kron2d_sized_kernel(DevPC pc, c
   for (int i = lane; i < N1 + N2; i += 32)
     sRcp[i] = __drcp_rn(i < N1 ? luA2[i * N1 + i] : luB1[(i - N1) * N2 + i - N1]);
   __syncwarp();
-  if (!(KRON_SKIP & 1)) {
   // (A2^{-1} (x) I): one column fiber per lane
   if constexpr (GREC) {
     lu_cols_ring<N1, N2>(luA2, sRcp, sPiv, sX, ld, sT, sRing, lane);
@@ -916,14 +908,11 @@ __global__ void __launch_bounds__(kSizedThreads) kron2d_sized_kernel(DevPC pc, c
   // (I (x) B1^{-1}): one row fiber per lane
   for (int r = lane; r < N1; r += 32) lu_fiber_reg<N2>(luB1, sRcp + N1, sPiv + N1, sX + r * ld, 1);
   __syncwarp();
-  }
-  if (!(KRON_SKIP & 2)) {
   warp_mm<N1, N1, N2, true, false, 2, 4>(Q1, N1, sX, ld, sT, ld, lane);  // Q1^T X
   __syncwarp();
   warp_mm<N1, N2, N2, false, false, 2, 4>(sT, ld, Q2, N2, sX, ld, lane);  // (.) Q2 -> M
   __syncwarp();
-  }
-  if (!(KRON_SKIP & 4)) {  // Y overwrites M in place (sX): T1 Y + Y T2^T = M, block anti-diagonal wavefront
+  {  // Y overwrites M in place (sX): T1 Y + Y T2^T = M, block anti-diagonal wavefront
     const int* sb = reinterpret_cast<const int*>(sH);
     const double* cc = cells + hdr;
     if constexpr (GREC) {  // T1 rows through a shared window in the (free) product scratch
@@ -947,10 +936,6 @@ __global__ void __launch_bounds__(kSizedThreads) kron2d_sized_kernel(DevPC pc, c
       sylv_wavefront<N1, N2, 1, 32, false>(T1, T2, sX, ld, 0, cc, sb, lane, pc.status);
       __syncwarp();
     }
-  }
-  if (KRON_SKIP & 8) {
-    for (int i = lane; i < N1 * N2; i += 32) out[size_t(blk) * (N1 * N2) + i] = sX[(i / N2) * ld + i % N2];
-    return;
   }
   warp_mm<N1, N1, N2, false, false, 2, 4>(Q1, N1, sX, ld, sT, ld, lane);  // Q1 Y
   __syncwarp();

@@ -55,26 +55,14 @@ __device__ __forceinline__ void copy_mat(double* dst, const double* src, int li)
   }
 }
 
-#ifndef EW_BIGN
-#define EW_BIGN 24  // N above which the kernel may use up to 254 registers (8 warps per SM)
-#endif
-#ifndef EW_LDPAD
-#define EW_LDPAD 3
-#endif
-#ifndef EW16_LANES
-#define EW16_LANES 16  // lanes per block at N = 16 (2 blocks per warp); 8 (4 per warp) measured 114 vs 91 us
-#endif
-#ifndef EW_CLOCK
-#define EW_CLOCK 0  // study builds only: clock64 breakdown of the Sylvester steps (block 100, lane 0)
-#endif
-#ifndef EW_SKIP
-#define EW_SKIP 0  // study builds only (tools/kron_variants.sh): bit mask of skipped phases
-#endif
+constexpr int kEwBigN = 24;     // N above which the kernel may use up to 254 registers (8 warps per SM)
+constexpr int kEwLdPad = 3;     // X row padding
+constexpr int kEw16Lanes = 16;  // lanes per block at N = 16 (2 blocks per warp); 8 (4 per warp) measured 114 vs 91 us
 
 template <int N, int P = N>  // P lanes per block
 struct Ew {
   static constexpr int EW = 32 / P;  // blocks per warp
-  static constexpr int LD = N + EW_LDPAD;  // X leading dimension (odd for even N: conflict-free fibers)
+  static constexpr int LD = N + kEwLdPad;  // X leading dimension (odd for even N: conflict-free fibers)
   static constexpr int XSZ = (N * LD + 1) & ~1;
   static constexpr int R1 = (2 * N * N > XSZ ? 2 * N * N : XSZ);
   static constexpr int HDR = ((4 + 4 * N) / 2 + 2) & ~1;  // sylv_hdr_doubles(N, N)
@@ -230,7 +218,7 @@ __device__ __forceinline__ void replay(const double* cf, double (&b)[4]) {
 }
 
 template <int N, int P>
-__global__ void __launch_bounds__(32, P < N ? 7 : N > EW_BIGN ? 8 : 16) kron2d_ew_kernel(DevPC pc, const double* __restrict__ in,
+__global__ void __launch_bounds__(32, P < N ? 7 : N > kEwBigN ? 8 : 16) kron2d_ew_kernel(DevPC pc, const double* __restrict__ in,
                                                         double* __restrict__ out) {
   using C = Ew<N, P>;
   constexpr int EW = C::EW, LD = C::LD;
@@ -249,9 +237,9 @@ __global__ void __launch_bounds__(32, P < N ? 7 : N > EW_BIGN ? 8 : 16) kron2d_e
   const double* rec = pc.rec + size_t(act ? blk : 0) * (6 * N * N);
   const double* cells = pc.cells + size_t(act ? blk : 0) * pc.cells_len;
   if (act) {
-    // L2 prefetch of what the later phases read: Q1 | T1 | Q2 | T2 and the cell factors
+    // L2 prefetch of what the later phases read: Q1 | T1 | Q2 | T2 (the cell factors are read only
+    // for the 2 x 2 quasi-blocks' cells, on demand)
     for (int o = 16 * li; o < 4 * N * N; o += 16 * P) prefetch_l2(rec + 2 * N * N + o);
-    for (int o = C::HDR + 16 * li; o < pc.cells_len; o += 16 * P) prefetch_l2(cells + o);
     copy_mat<2 * N * N, N, P>(R1, rec, li);               // LU(A2) | LU(B1)
     for (int i = 2 * li; i < C::HDR; i += 2 * P) cpa16(reinterpret_cast<double*>(hdr) + i, cells + i);
     for (int i = li; i < 2 * N; i += P) cpa4(piv + i, pc.piv + size_t(blk) * (2 * N) + i);
@@ -267,16 +255,16 @@ __global__ void __launch_bounds__(32, P < N ? 7 : N > EW_BIGN ? 8 : 16) kron2d_e
     }
   __syncwarp();
   // (A2^{-1} (x) I): column fibers, then (I (x) B1^{-1}): row fibers
-  if (act && !(EW_SKIP & 1))
+  if (act)
     for_fibers<N, P>(li, [&](int c) { lu_fiber<N>(R1, rcp, piv, X + c, LD); });
   __syncwarp();
-  if (act && !(EW_SKIP & 1))
+  if (act)
     for_fibers<N, P>(li, [&](int r) { lu_fiber<N>(R1 + N * N, rcp + N, piv + N, X + r * LD, 1); });
   __syncwarp();
   // M = (Q1^T X) Q2
-  if (act && !(EW_SKIP & 2)) mm_tile<N, P, true, false, true, false>(Q1, N, X, LD, R1, LD, li);
+  if (act) mm_tile<N, P, true, false, true, false>(Q1, N, X, LD, R1, LD, li);
   __syncwarp();
-  if (act && !(EW_SKIP & 2)) mm_tile<N, P, false, false, false, true>(R1, LD, Q2, N, X, LD, li);
+  if (act) mm_tile<N, P, false, false, false, true>(R1, LD, Q2, N, X, LD, li);
   __syncwarp();
   // T1 | T2 into R1
   if (act) {
@@ -293,7 +281,7 @@ __global__ void __launch_bounds__(32, P < N ? 7 : N > EW_BIGN ? 8 : 16) kron2d_e
     const int *s1 = hdr + 4, *z1 = s1 + N, *s2 = z1 + N, *z2 = s2 + N;
     const double* cc = cells + C::HDR;
     double* scr = sm_all + C::EW * C::PER + 4 * lane;  // per-lane scratch: the cell's right-hand sides
-    const int last = (EW_SKIP & 4) ? -1 : __reduce_max_sync(0xffffffffu, act ? nb1 + nb2 - 2 : -1);
+    const int last = __reduce_max_sync(0xffffffffu, act ? nb1 + nb2 - 2 : -1);
     // cell of this lane at step st (valid = inside the anti-diagonal) and its factor slot
     auto cell_at = [&](int st, int& i0, int& isz, int& k0, int& ksz, int off = 0) {
       const int d1lo = st - (nb2 - 1) > 0 ? st - (nb2 - 1) : 0;
@@ -317,12 +305,11 @@ __global__ void __launch_bounds__(32, P < N ? 7 : N > EW_BIGN ? 8 : 16) kron2d_e
         c[2 * u + 1] = v.y;
       }
     };
-    long long t_a = 0, t_b = 0, t_c = 0;
     // one wavefront step with this lane's cell (ok, i0, isz, k0, ksz); the next step's cell is
     // located first and its factor slot prefetched into L1, so that the factors, loaded after
     // the chains (registers stay free for the chains' load pipelining), arrive from L1
-    // chains + tiny-system replay of one cell (ok, i0, isz, k0, ksz); c0: clock of the step start
-    auto do_cell = [&](bool ok, int i0, int isz, int k0, int ksz, long long& c0) {
+    // chains + tiny-system replay of one cell (ok, i0, isz, k0, ksz)
+    auto do_cell = [&](bool ok, int i0, int isz, int k0, int ksz) {
       if (ok) {
         const int ns = isz * ksz;
         const int i1 = i0 + isz - 1, k1 = k0 + ksz - 1;
@@ -353,16 +340,12 @@ __global__ void __launch_bounds__(32, P < N ? 7 : N > EW_BIGN ? 8 : 16) kron2d_e
             s11 = fmsc(s11, u1, w1);
           }
         }
-        if (EW_CLOCK) {
-          const long long c1 = clock64();
-          t_a += c1 - c0;
-          c0 = c1;
-        }
-        double cf[22];
-        load_cf(true, i0, isz, k0, ksz, cf);
-        if (ns == 1) {
-          X[i0 * LD + k0] = fdiv_rcp(s00, cf[1], cf[2]);
+        if (ns == 1) {  // solve_tiny<1>: the cell's coefficient (0 + t1_ii) + t2_kk, recomputed
+          const double coef = fadd(fadd(0.0, T1[i0 * N + i0]), T2[k0 * N + k0]);
+          X[i0 * LD + k0] = fdiv_rcp(s00, coef, __drcp_rn(coef));
         } else {
+          double cf[22];
+          load_cf(true, i0, isz, k0, ksz, cf);
           // unknowns in (a, kb) order, a * ksz + kb; rows permuted by the elimination's pivots
           const long long code = __double_as_longlong(cf[0]);
           scr[0] = s00;
@@ -388,14 +371,13 @@ __global__ void __launch_bounds__(32, P < N ? 7 : N > EW_BIGN ? 8 : 16) kron2d_e
     };
     auto step = [&](int st, bool ok, int i0, int isz, int k0, int ksz, bool& nok, int& ni0, int& nisz, int& nk0,
                     int& nksz) {
-      long long c0 = EW_CLOCK ? clock64() : 0;
       nok = cell_at(st + 1, ni0, nisz, nk0, nksz);
-      if (nok) {
+      if (nok && nisz * nksz > 1) {
         const double* sp = cc + 6 * (ni0 * N + nisz * nk0);
         asm volatile("prefetch.global.L1 [%0];" ::"l"(sp));
         if (nisz * nksz == 4) asm volatile("prefetch.global.L1 [%0];" ::"l"(sp + 16));
       }
-      do_cell(ok, i0, isz, k0, ksz, c0);
+      do_cell(ok, i0, isz, k0, ksz);
       if constexpr (P < N) {  // more cells on this anti-diagonal than lanes per block: further passes
         const int d1lo = st - (nb2 - 1) > 0 ? st - (nb2 - 1) : 0;
         const int d1hi = st < nb1 - 1 ? st : nb1 - 1;
@@ -403,33 +385,23 @@ __global__ void __launch_bounds__(32, P < N ? 7 : N > EW_BIGN ? 8 : 16) kron2d_e
         for (int off = P; off < nc; off += P) {
           int xi0, xisz, xk0, xksz;
           const bool xok = cell_at(st, xi0, xisz, xk0, xksz, off);
-          do_cell(xok, xi0, xisz, xk0, xksz, c0);
+          do_cell(xok, xi0, xisz, xk0, xksz);
         }
       }
-      if (EW_CLOCK) {
-        const long long c1 = clock64();
-        t_b += c1 - c0;
-        c0 = c1;
-      }
       __syncwarp();
-      if (EW_CLOCK) t_c += clock64() - c0;
     };
     bool aok, bok;
     int ai0, aisz, ak0, aksz, bi0, bisz, bk0, bksz;
     aok = cell_at(0, ai0, aisz, ak0, aksz);
-    const long long t0 = EW_CLOCK ? clock64() : 0;
     for (int st = 0; st <= last; st += 2) {  // ping-pong between the two cell descriptors
       step(st, aok, ai0, aisz, ak0, aksz, bok, bi0, bisz, bk0, bksz);
       if (st + 1 <= last) step(st + 1, bok, bi0, bisz, bk0, bksz, aok, ai0, aisz, ak0, aksz);
     }
-    if (EW_CLOCK && blockIdx.x == 100 && lane == 0)
-      printf("ew clock: steps %d, total %lld cycles, chains(lane0) %lld, solve %lld, sync %lld\n", last + 1,
-             clock64() - t0, t_a, t_b, t_c);
   }
   // X = (Q1 Y) Q2^T
-  if (act && !(EW_SKIP & 8)) mm_tile<N, P, false, false, true, false>(Q1, N, X, LD, R1, LD, li);
+  if (act) mm_tile<N, P, false, false, true, false>(Q1, N, X, LD, R1, LD, li);
   __syncwarp();
-  if (act && !(EW_SKIP & 8)) mm_tile<N, P, false, true, false, true>(R1, LD, Q2, N, X, LD, li);
+  if (act) mm_tile<N, P, false, true, false, true>(R1, LD, Q2, N, X, LD, li);
   __syncwarp();
   if (act) {
     double* o = out + size_t(blk) * (N * N);
@@ -455,7 +427,7 @@ bool try_ew(const DevPC& pc, const double* in, double* out, cudaStream_t st) {
 } // namespace
 
 bool launch_kron2d_ew(const DevPC& pc, const double* in, double* out, cudaStream_t st) {
-  return try_ew<5>(pc, in, out, st) || try_ew<9>(pc, in, out, st) || try_ew<16, EW16_LANES>(pc, in, out, st) ||
+  return try_ew<5>(pc, in, out, st) || try_ew<9>(pc, in, out, st) || try_ew<16, kEw16Lanes>(pc, in, out, st) ||
          try_ew<21>(pc, in, out, st) || try_ew<31>(pc, in, out, st);
 }
 

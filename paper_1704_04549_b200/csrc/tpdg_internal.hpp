@@ -88,6 +88,7 @@ struct DevSys {
   const int* skip;    // optional device flag: kernels return immediately when *skip != 0
   const double *cdfm, *cdfp;  // face Jacobians pre-scaled by -b fw (device; read by jv3d_fast)
   const double* pw;           // 3D n_c = 1: [e][mu^3][a jdet, b dft_x, b dft_y, b dft_z] (device)
+  const double* dftr;         // 3D n_c > 1: dft regrouped by output component, [e][r][dir][mu^3][n_c] (device)
   const double *hg, *hgw, *hdw;  // HOST copies of g, gw, dw (packed into kernel parameters at launch)
 };
 

@@ -1,6 +1,6 @@
 #!/bin/bash
 # Study builds: libtpdg_gpu.so variants with kron.cu compiled under extra flags, e.g.
-#   [SRC=kron_ew] tools/kron_variants.sh skip1:-DKRON_SKIP=1 skip4:-DKRON_SKIP=4
+#   [SRC=kron_ew] tools/kron_variants.sh a:-DSOME_FLAG=1 b:-DSOME_FLAG=2
 # -> paper_1704_04549_b200/_build/var/<name>/libtpdg_gpu.so (select with TPDG_GPU_LIB=...)
 set -e
 R=$(cd "$(dirname "$0")/.." && pwd)
