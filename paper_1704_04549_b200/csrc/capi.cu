@@ -194,7 +194,7 @@ struct tpdg_gpu_op_s {
   DevBuf g, d, gw, dw, w, jdet, face_w, dft, dfm, dfp, conn, halo;
   DevBuf cdfm, cdfp;                 // -b fw dfm, -b fw dfp (folded face data of the fast 3D operator)
   DevBuf pw;                         // 3D n_c = 1: interleaved point-wise coefficients (jv3d.cu)
-  DevBuf dftr;                       // 3D n_c > 1: dft by output component, [e][r][dir][point][c] (jv.cu)
+  DevBuf dftr, dfmr, dfpr;           // n_c > 1: Jacobians by output component (jv.cu generic kernels)
   std::vector<double> hg, hgw, hdw;  // host copies of the 1D matrices (kernel-parameter packing)
   DevBuf io_a, io_b;  // staging for the host-pointer entry points
   DevBuf shuf_ws;
@@ -279,6 +279,8 @@ DevSys make_devsys(const tpdg_gpu_op_s& op, int block_mode, double a, double b) 
   s.cdfp = op.cdfp.as<double>();
   s.pw = op.pw.as<double>();
   s.dftr = op.dftr.as<double>();
+  s.dfmr = op.dfmr.as<double>();
+  s.dfpr = op.dfpr.as<double>();
   s.hg = op.hg.empty() ? nullptr : op.hg.data();
   s.hgw = op.hgw.empty() ? nullptr : op.hgw.data();
   s.hdw = op.hdw.empty() ? nullptr : op.hdw.data();
@@ -987,16 +989,28 @@ int tpdg_gpu_op_create(tpdg_gpu_ctx ctx, const tpdg_gpu_system* sys, double dt, 
           }
         upload(op->pw, pw.data(), pw.size(), st);
       }
-      if (d == 3 && nc > 1) {  // row r of every point's flux Jacobian contiguous over the points
-        std::vector<double> tr(nl * 3 * nqv * ncc);
-        const double* df = sys->dft + size_t(e_begin) * 3 * nqv * ncc;
+      if (nc > 1) {  // row r of every point's Jacobians contiguous over the points
+        std::vector<double> tr(nl * d * nqv * ncc);
+        const double* df = sys->dft + size_t(e_begin) * d * nqv * ncc;
         for (size_t e = 0; e < nl; ++e)
-          for (int dir = 0; dir < 3; ++dir)
+          for (int dir = 0; dir < d; ++dir)
             for (size_t q0 = 0; q0 < nqv; ++q0)
               for (int r = 0; r < nc; ++r)
                 for (int c = 0; c < nc; ++c)
-                  tr[(((e * nc + r) * 3 + dir) * nqv + q0) * nc + c] = df[((e * 3 + dir) * nqv + q0) * ncc + r * nc + c];
+                  tr[(((e * nc + r) * d + dir) * nqv + q0) * nc + c] = df[((e * d + dir) * nqv + q0) * ncc + r * nc + c];
         upload(op->dftr, tr.data(), tr.size(), st);
+        std::vector<double> fm(nf * ncc), fp(nf * ncc);
+        for (size_t ef = 0; ef < nl * 2 * d; ++ef)
+          for (size_t q0 = 0; q0 < nqf; ++q0)
+            for (int r = 0; r < nc; ++r)
+              for (int c = 0; c < nc; ++c) {
+                const size_t src = (ef * nqf + q0) * ncc + r * nc + c, dst = ((ef * nc + r) * nqf + q0) * nc + c;
+                fm[dst] = dm[src];
+                fp[dst] = dp[src];
+              }
+        upload(op->dfmr, fm.data(), fm.size(), st);
+        upload(op->dfpr, fp.data(), fp.size(), st);
+        TPDG_CUDA_CHECK(cudaStreamSynchronize(st));  // host staging buffers go out of scope
       }
       TPDG_CUDA_CHECK(cudaStreamSynchronize(st));
     }

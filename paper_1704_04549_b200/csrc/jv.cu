@@ -100,8 +100,9 @@ __global__ void __launch_bounds__(NT) jv2d_kernel(DevSys s, const double* __rest
   for (int idx = tid; idx < 4 * nc * mu; idx += nt) {
     const int a = idx % mu, r = (idx / mu) % nc, f = idx / (mu * nc);
     const size_t fq = (size_t(e) * 4 + f) * mu + a;
-    const double* dfm = s.dfm + fq * nc * nc + r * nc;
-    const double* dfp = s.dfp + fq * nc * nc + r * nc;
+    const size_t fr = (((size_t(e) * 4 + f) * nc + r) * mu + a) * nc;  // regrouped: [e][f][r][a][c]
+    const double* dfm = s.dfmr ? s.dfmr + fr : s.dfm + fq * nc * nc + r * nc;
+    const double* dfp = s.dfpr ? s.dfpr + fr : s.dfp + fq * nc * nc + r * nc;
     const double* tm = str + (f * nc) * mu + a;
     const double* tp = str + ((4 + f) * nc) * mu + a;
     double acc = 0.0;
@@ -116,8 +117,9 @@ __global__ void __launch_bounds__(NT) jv2d_kernel(DevSys s, const double* __rest
   // point-wise fields: M = a jd vals_r ; F_dir = b sum_c dft[dir][q][r][c] vals_c
   for (int idx = tid; idx < nc * mm; idx += nt) {
     const int qv = idx % mm, r = idx / mm;
-    const double* d0 = s.dft + ((size_t(e) * 2 + 0) * mm + qv) * nc * nc + r * nc;
-    const double* d1 = s.dft + ((size_t(e) * 2 + 1) * mm + qv) * nc * nc + r * nc;
+    const double* d0 = s.dftr ? s.dftr + ((size_t(e) * nc + r) * 2 * mm + qv) * nc
+                              : s.dft + ((size_t(e) * 2 + 0) * mm + qv) * nc * nc + r * nc;
+    const double* d1 = s.dftr ? d0 + size_t(mm) * nc : s.dft + ((size_t(e) * 2 + 1) * mm + qv) * nc * nc + r * nc;
     double f0 = 0.0, f1 = 0.0;
     if (!s.small) {
       for (int c = 0; c < nc; ++c) {
@@ -472,8 +474,9 @@ __global__ void __launch_bounds__(NT) jv3d_kernel(DevSys s, const double* __rest
     const int qf = idx % m2, r = (idx / m2) % nc, f = idx / (m2 * nc);
     const int* fc = s.conn + (size_t(e) * 6 + f) * 3;
     const size_t fq = (size_t(e) * 6 + f) * m2 + qf;
-    const double* dfm = s.dfm + fq * nc * nc + r * nc;
-    const double* dfp = s.dfp + fq * nc * nc + r * nc;
+    const size_t fr = (((size_t(e) * 6 + f) * nc + r) * m2 + qf) * nc;  // regrouped: [e][f][r][point][c]
+    const double* dfm = s.dfmr ? s.dfmr + fr : s.dfm + fq * nc * nc + r * nc;
+    const double* dfp = s.dfpr ? s.dfpr + fr : s.dfp + fq * nc * nc + r * nc;
     // neighbour trace permuted into this face's enumeration (orient_face_coords, dg/mesh.hpp:57-67)
     const int qa = qf % mu, qb = qf / mu;
     const int code = fc[2];

@@ -88,7 +88,9 @@ struct DevSys {
   const int* skip;    // optional device flag: kernels return immediately when *skip != 0
   const double *cdfm, *cdfp;  // face Jacobians pre-scaled by -b fw (device; read by jv3d_fast)
   const double* pw;           // 3D n_c = 1: [e][mu^3][a jdet, b dft_x, b dft_y, b dft_z] (device)
-  const double* dftr;         // 3D n_c > 1: dft regrouped by output component, [e][r][dir][mu^3][n_c] (device)
+  // n_c > 1: the Jacobians regrouped by output component (row r of every point contiguous over the
+  // points), dftr [e][r][dir][point][n_c], dfmr / dfpr [e][f][r][face point][n_c] (device; generic Jv)
+  const double *dftr, *dfmr, *dfpr;
   const double *hg, *hgw, *hdw;  // HOST copies of g, gw, dw (packed into kernel parameters at launch)
 };
 
