@@ -647,7 +647,7 @@ struct CoopPlan {
 };
 
 // One 1024-thread CTA per SM (cheap barrier); the most shared-memory residency that fits.
-constexpr int kBulkThreads = 1024, kBulkRW = 8, kBulkStages = 2;  // measured best (cfg4 MGS 301 us): 1024/10/3 (spills) 307, 768/12/3 338, 512/16/4 354
+constexpr int kBulkThreads = 1024, kBulkRW = 8, kBulkStages = 2;  // measured best (cfg4 MGS 301 us): 1024/10/3 (spills) 307, 768/12/3 338, 512/16/4 354; v_{j-1} by per-thread L2 loads + 4-stage v_j ring 352
 
 CoopPlan mgs_coop_plan(int64_t n) {
   int dev = 0, sms = 0;
