@@ -9,6 +9,8 @@
 //
 // MGS is fused: pass j computes w <- w - h_{j-1} v_{j-1} and the partial dot <v_j, w> in one read
 // of (w, v_{j-1}, v_j) and one write of w, so the k+1 MGS steps of iteration k cost k+2 passes.
+#include <map>
+#include <mutex>
 #include <algorithm>
 #include <cstdint>
 
@@ -666,7 +668,7 @@ CoopPlan mgs_coop_plan(int64_t n) {
     const void* fn = reinterpret_cast<const void*>(mgs_bulk_kernel<kBulkThreads, kBulkRW, kBulkStages>);
     int fit = 0;
     if (sm <= 227 * 1024) {
-      TPDG_CUDA_CHECK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+      ensure_smem(fn, sm);
       TPDG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, fn, kBulkThreads, sm));
       if (fit >= 1) return {sms, chunk, sm, 5, kBulkThreads};
     }
@@ -725,11 +727,17 @@ void launch_scale_div(const double* in, const double* den, double* out, int64_t 
 
 void launch_mgs_iteration(double* V, int64_t ldv, int k, int64_t n, double* hc, double* partial, unsigned* bar,
                           const int* skip, cudaStream_t st, const GmresDev* G, GmresStatus* status) {
-  static int64_t planned_n = -1;
-  static CoopPlan plan;
-  if (planned_n != n) {
-    plan = mgs_coop_plan(n);
-    planned_n = n;
+  // plans per (device, slice length): rank threads of the loopback transport may hold different n
+  static std::mutex mu;
+  static std::map<std::pair<int, int64_t>, CoopPlan> plans;
+  int dev = 0;
+  TPDG_CUDA_CHECK(cudaGetDevice(&dev));
+  CoopPlan plan;
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = plans.find({dev, n});
+    if (it == plans.end()) it = plans.emplace(std::make_pair(dev, n), mgs_coop_plan(n)).first;
+    plan = it->second;
   }
   int64_t chunk = plan.chunk;
   GmresDev g = G && G->m <= kFusedGivensMaxM ? *G : GmresDev{};

@@ -507,7 +507,7 @@ void launch_build_cache_euler(int dim, int q, int mu, int n_elements, const doub
                               double* dfp, int* status, cudaStream_t st) {
   const int nc = dim + 2, nqv = dim == 2 ? mu * mu : mu * mu * mu, nqf = nqv / mu;
   const size_t smem = sizeof(double) * (size_t(nc) * nqv + size_t(mu) * q * q + size_t(mu) * mu * q + 2 * nc * nqf);
-  TPDG_CUDA_CHECK(cudaFuncSetAttribute(cache_euler_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  ensure_smem(cache_euler_kernel, smem);
   if (n_elements) cache_euler_kernel<<<n_elements, 256, smem, st>>>(dim, q, mu, g, state, adj, face_n, conn, dft, dfm,
                                                                     dfp, status);
   TPDG_CUDA_CHECK(cudaGetLastError());
@@ -521,7 +521,7 @@ void launch_residual_euler(int dim, int q, int mu, int n_elements, const double*
   const int npe = dim == 2 ? q * q : q * q * q;
   const size_t smem = sizeof(double) * (size_t(nc) * nqv * (1 + dim) + 2 * size_t(mu) * mu * q + size_t(nc) * npe +
                                         3 * size_t(nc) * nqf);
-  TPDG_CUDA_CHECK(cudaFuncSetAttribute(residual_euler_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  ensure_smem(residual_euler_kernel, smem);
   if (n_elements)
     residual_euler_kernel<<<n_elements, 256, smem, st>>>(dim, q, mu, g, gw, dw, state, adj, face_n, face_w, conn, out,
                                                          status);

@@ -1491,12 +1491,7 @@ void launch_dense_lu(int n, int nfb, double* fb_lu, int* fb_piv, int* fb_status,
   constexpr int KB = 16;
   const size_t ls = sizeof(double) * size_t(KB) * size_t(n);
   if (!unblocked && ls <= 200 * 1024) {
-    static size_t configured = 0;
-    if (ls > configured) {
-      TPDG_CUDA_CHECK(cudaFuncSetAttribute(dense_lu_blocked_kernel<KB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           int(ls)));
-      configured = ls;
-    }
+    ensure_smem(dense_lu_blocked_kernel<KB>, ls);
     dense_lu_blocked_kernel<KB><<<nfb, 1024, ls, st>>>(n, fb_lu, fb_piv, fb_status);
   } else {
     dense_lu_kernel<<<nfb, 1024, 0, st>>>(n, fb_lu, fb_piv, fb_status);

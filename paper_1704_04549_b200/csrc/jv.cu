@@ -348,12 +348,9 @@ bool try_jv2d_sized(const DevSys& s, const double* vin, const double* halo, doub
   if (s.dim != 2 || s.n_c != 1 || s.q != Q || s.mu != MU) return false;
   using L = Jv2dLayout<Q, MU>;
   const size_t smem = sizeof(double) * size_t(L::weights + L::warps * L::per_elem);
+  ensure_smem(jv2d_sized_kernel<Q, MU>, smem, true);
   static int grid = 0;
   if (!grid) {
-    TPDG_CUDA_CHECK(cudaFuncSetAttribute(jv2d_sized_kernel<Q, MU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(smem)));
-    TPDG_CUDA_CHECK(cudaFuncSetAttribute(jv2d_sized_kernel<Q, MU>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                         100));
     int per_sm = 0;
     TPDG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jv2d_sized_kernel<Q, MU>, 128, smem));
     int dev = 0, sms = 0;
@@ -852,12 +849,9 @@ template <int Q, int MU>
 bool try_jv3d_sized(const DevSys& s, const double* vin, const double* halo, double* vout, cudaStream_t st) {
   if (s.dim != 3 || s.n_c != 1 || s.q != Q || s.mu != MU) return false;
   const size_t smem = sizeof(double) * size_t(Jv3dLayout<Q, MU>::total);
+  ensure_smem(jv3d_sized_kernel<Q, MU>, smem, true);
   static int grid = 0;
   if (!grid) {
-    TPDG_CUDA_CHECK(cudaFuncSetAttribute(jv3d_sized_kernel<Q, MU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(smem)));
-    TPDG_CUDA_CHECK(cudaFuncSetAttribute(jv3d_sized_kernel<Q, MU>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                         100));
     int per_sm = 0, dev = 0, sms = 0;
     TPDG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jv3d_sized_kernel<Q, MU>, 256, smem));
     TPDG_CUDA_CHECK(cudaGetDevice(&dev));
@@ -889,7 +883,7 @@ namespace {
 template <typename K>
 void launch_generic(K kernel, int nt, size_t smem, const DevSys& s, const double* vin, const double* halo,
                     double* vout, cudaStream_t st) {
-  TPDG_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  ensure_smem(kernel, smem);
   kernel<<<s.e_hi - s.e_lo, nt, smem, st>>>(s, vin, halo, vout);
 }
 }  // namespace

@@ -358,11 +358,10 @@ bool try_jv3d_fast(const DevSys& s, const double* vin, const double* halo, doubl
   std::copy(s.hg, s.hg + MU * Q, w);
   std::copy(s.hgw, s.hgw + MU * Q, w + MU * Q);
   std::copy(s.hdw, s.hdw + MU * Q, w + 2 * MU * Q);
+  ensure_smem(jv3d_fast_kernel<SLOT, Q, MU, NT, MINB>, smem);
   {
     std::lock_guard<std::mutex> lock(mu);
     if (!grid[dev]) {
-      TPDG_CUDA_CHECK(cudaFuncSetAttribute(jv3d_fast_kernel<SLOT, Q, MU, NT, MINB>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
       int per_sm = 0, sms = 0;
       TPDG_CUDA_CHECK(
           cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jv3d_fast_kernel<SLOT, Q, MU, NT, MINB>, NT, smem));

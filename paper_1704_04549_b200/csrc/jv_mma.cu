@@ -281,12 +281,9 @@ bool try_jv2d_mma(const DevSys& s, const double* vin, const double* halo, double
   using L = JvMmaLayout<Q, MU>;
   static_assert(L::warps >= 1, "element workspace exceeds shared memory");
   const size_t smem = sizeof(double) * size_t(L::weights + L::warps * L::per_warp);
+  ensure_smem(jv2d_mma_kernel<Q, MU>, smem, true);
   static int grid = 0;
   if (!grid) {
-    TPDG_CUDA_CHECK(cudaFuncSetAttribute(jv2d_mma_kernel<Q, MU>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(smem)));
-    TPDG_CUDA_CHECK(cudaFuncSetAttribute(jv2d_mma_kernel<Q, MU>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                         100));
     int per_sm = 0;
     TPDG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, jv2d_mma_kernel<Q, MU>, 32 * L::warps,
                                                                   smem));

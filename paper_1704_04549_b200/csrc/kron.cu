@@ -861,15 +861,8 @@ size_t kron2d_sized_smem() {
 template <int N1, int N2, bool GREC = false>
 bool try_kron2d_sized(const DevPC& pc, const double* in, double* out, cudaStream_t st) {
   if (pc.n1 != N1 || pc.q != N2) return false;
-  static bool configured = false;
   const size_t smem = kron2d_sized_smem<N1, N2, GREC>();
-  if (!configured) {
-    TPDG_CUDA_CHECK(cudaFuncSetAttribute(kron2d_sized_kernel<N1, N2, GREC>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    TPDG_CUDA_CHECK(cudaFuncSetAttribute(kron2d_sized_kernel<N1, N2, GREC>,
-                                         cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    configured = true;
-  }
+  ensure_smem(kron2d_sized_kernel<N1, N2, GREC>, smem, true);
   const int per_cta = kSizedThreads / 32;
   kron2d_sized_kernel<N1, N2, GREC><<<(pc.nblk + per_cta - 1) / per_cta, kSizedThreads, smem, st>>>(pc, in, out);
   return true;
@@ -1471,12 +1464,7 @@ bool try_kron3d_inv(const DevPC& pc, const double* in, double* out, cudaStream_t
   if (pc.dim != 3 || pc.n1 != N1 || pc.q != Q || !pc.irec) return false;
   using L = Kron3dInvLayout<N1, Q>;
   const size_t smem = sizeof(double) * size_t(L::total);
-  static bool configured = false;
-  if (!configured) {
-    TPDG_CUDA_CHECK(cudaFuncSetAttribute(kron3d_inv_kernel<N1, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(smem)));
-    configured = true;
-  }
+  ensure_smem(kron3d_inv_kernel<N1, Q>, smem);
   kron3d_inv_kernel<N1, Q><<<pc.nblk, L::NTH, smem, st>>>(pc, in, out);
   return true;
 }
@@ -1491,14 +1479,7 @@ template <int N1, int Q>
 bool try_kron3d_sized(const DevPC& pc, const double* in, double* out, cudaStream_t st) {
   if (pc.dim != 3 || pc.n1 != N1 || pc.q != Q) return false;
   const size_t smem = sizeof(double) * size_t(Kron3dLayout<N1, Q>::total);
-  static bool configured = false;
-  if (!configured) {
-    TPDG_CUDA_CHECK(cudaFuncSetAttribute(kron3d_sized_kernel<N1, Q>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(smem)));
-    TPDG_CUDA_CHECK(cudaFuncSetAttribute(kron3d_sized_kernel<N1, Q>, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                         100));
-    configured = true;
-  }
+  ensure_smem(kron3d_sized_kernel<N1, Q>, smem, true);
   kron3d_sized_kernel<N1, Q><<<pc.nblk, k3Threads, smem, st>>>(pc, in, out);
   return true;
 }
@@ -1612,13 +1593,6 @@ __global__ void __launch_bounds__(256) kron_fallback_kernel(DevPC pc, const doub
   for (int i = threadIdx.x; i < n; i += blockDim.x) o[i] = sx[i];
 }
 
-template <typename K>
-void set_smem(K kernel, size_t bytes, size_t& configured) {
-  if (bytes > configured) {
-    TPDG_CUDA_CHECK(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)));
-    configured = bytes;
-  }
-}
 
 } // namespace
 
@@ -1636,18 +1610,17 @@ void launch_sylv_cells(const DevPC& pc, double* cells, cudaStream_t st) {
 
 void launch_pc_apply(const DevPC& pc, const double* in, double* out, cudaStream_t st) {
   if (pc.nblk == 0) return;
-  static size_t c2 = 0, c3 = 0, cf = 0;
   const size_t smem = pc.dim == 2 ? kron2d_smem(pc) : kron3d_smem(pc);
   if (smem > 227 * 1024)
     throw Failure{TPDG_CONFIG, "pc_apply: factor record of " + std::to_string(smem) + " B exceeds shared memory"};
   if (pc.dim == 2) {
     // the bit-faithful multi-block kernel (kron_ew.cu), else one block per warp (sized), else generic
     if (!launch_kron2d_ew(pc, in, out, st) && !launch_kron2d_sized(pc, in, out, st)) {
-      set_smem(kron2d_apply_kernel, smem, c2);
+      ensure_smem(kron2d_apply_kernel, smem);
       kron2d_apply_kernel<<<pc.nblk, kApplyThreads, smem, st>>>(pc, in, out);
     }
   } else if (!(!pc.faithful && launch_kron3d_inv(pc, in, out, st)) && !launch_kron3d_sized(pc, in, out, st)) {
-    set_smem(kron3d_apply_kernel, smem, c3);
+    ensure_smem(kron3d_apply_kernel, smem);
     kron3d_apply_kernel<<<pc.nblk, kApplyThreads, smem, st>>>(pc, in, out);
   }
   TPDG_CUDA_CHECK(cudaGetLastError());
@@ -1655,7 +1628,7 @@ void launch_pc_apply(const DevPC& pc, const double* in, double* out, cudaStream_
   if (pc.fb_lu) {
     const size_t fsm = sizeof(double) * size_t(pc.blk_len);
     if (!launch_fallback_apply(pc, in, out, st)) {  // blocks beyond 2048 rows: one column sweep per step
-      set_smem(kron_fallback_kernel, fsm, cf);
+      ensure_smem(kron_fallback_kernel, fsm);
       kron_fallback_kernel<<<pc.nblk, 256, fsm, st>>>(pc, in, out);
     }
     TPDG_CUDA_CHECK(cudaGetLastError());

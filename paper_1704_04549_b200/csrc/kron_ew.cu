@@ -413,13 +413,8 @@ template <int N, int P = N>
 bool try_ew(const DevPC& pc, const double* in, double* out, cudaStream_t st) {
   if (pc.dim != 2 || pc.n1 != N || pc.q != N) return false;
   using C = Ew<N, P>;
-  static bool configured = false;
   const size_t smem = sizeof(double) * (size_t(C::PER) * C::EW + 4 * 32);
-  if (!configured) {
-    TPDG_CUDA_CHECK(cudaFuncSetAttribute(kron2d_ew_kernel<N, P>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    TPDG_CUDA_CHECK(cudaFuncSetAttribute(kron2d_ew_kernel<N, P>, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
-    configured = true;
-  }
+  ensure_smem(kron2d_ew_kernel<N, P>, smem, true);
   kron2d_ew_kernel<N, P><<<(pc.nblk + C::EW - 1) / C::EW, 32, smem, st>>>(pc, in, out);
   return true;
 }

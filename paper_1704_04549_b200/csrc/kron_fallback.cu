@@ -247,11 +247,7 @@ template <int R>
 bool try_fb_panel(const DevPC& pc, const double* in, double* out, cudaStream_t st) {
   if (pc.blk_len > R * kFbThreads) return false;
   const size_t smem = sizeof(double) * size_t(pc.blk_len + kPanel);
-  static size_t configured = 0;
-  if (smem > configured) {
-    TPDG_CUDA_CHECK(cudaFuncSetAttribute(fb_panel_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    configured = smem;
-  }
+  ensure_smem(fb_panel_kernel<R>, smem);
   fb_panel_kernel<R><<<pc.n_fb, kFbThreads, smem, st>>>(pc, in, out);
   return true;
 }
@@ -261,11 +257,7 @@ bool try_fb(const DevPC& pc, const double* in, double* out, cudaStream_t st) {
   if (pc.blk_len > R * kFbThreads) return false;
   constexpr int D = R <= 2 ? 16 : 8;
   const size_t smem = sizeof(double) * size_t(pc.blk_len);
-  static size_t configured = 0;
-  if (smem > configured) {
-    TPDG_CUDA_CHECK(cudaFuncSetAttribute(fb_apply_kernel<R, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    configured = smem;
-  }
+  ensure_smem(fb_apply_kernel<R, D>, smem);
   fb_apply_kernel<R, D><<<pc.n_fb, kFbThreads, smem, st>>>(pc, in, out);
   return true;
 }

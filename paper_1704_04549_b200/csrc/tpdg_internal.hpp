@@ -217,4 +217,14 @@ int reduce_grid(int64_t n);
 
 extern thread_local int64_t g_launches;
 
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize = bytes [, carveout 100 %]) once per (device, kernel)
+// and size (launch_cfg.cpp; thread-safe, per device).
+void ensure_smem(const void* fn, size_t bytes, bool carveout = false);
+template <typename K>
+inline void ensure_smem(K* kernel, size_t bytes, bool carveout = false) {
+  ensure_smem(reinterpret_cast<const void*>(kernel), bytes, carveout);
+}
+
+
 } // namespace tpdg_gpu
