@@ -522,7 +522,7 @@ __global__ void __launch_bounds__(kCoopThreads) mgs_regv_kernel(double* __restri
 // and a row's copies for the next pass are in flight during the grid reduction. w lives on chip for
 // the whole launch: rows r < RW in registers, the rest in shared memory behind the ring. v_j is
 // kept in L2 (evict_last) for the next pass's update read, v_{j-1} is then dropped (evict_first).
-template <int NT, int RW, int NS>
+template <int NT, int RW, int NS, int PPT>
 __global__ void __launch_bounds__(NT, 1) mgs_bulk_kernel(double* __restrict__ V, int64_t ldv, int k, int64_t n,
                                                          int64_t chunk, double* __restrict__ hc,
                                                          double* __restrict__ partial, unsigned* bar, const int* skip,
@@ -530,7 +530,7 @@ __global__ void __launch_bounds__(NT, 1) mgs_bulk_kernel(double* __restrict__ V,
   if (skip && *skip) return;
   __shared__ unsigned tgt;
   mgs_epoch_begin(bar, &tgt);
-  constexpr int ROW = 2 * NT;  // doubles per row: one pair per thread
+  constexpr int ROW = 2 * NT * PPT;  // doubles per row: PPT pairs per thread (pair t + NT u)
   extern __shared__ __align__(128) double bsm[];
   double* ring = bsm;             // stage s: v_j row at ring + 2 ROW s, v_{j-1} row at + ROW
   double* wsm = bsm + 2 * ROW * NS;  // w rows RW.. (row r at wsm + (r - RW) ROW)
@@ -550,13 +550,15 @@ __global__ void __launch_bounds__(NT, 1) mgs_bulk_kernel(double* __restrict__ V,
     }
     mbar_fence_init();
   }
-  double2 wr[RW];
+  double2 wr[RW][PPT];
 #pragma unroll
-  for (int r = 0; r < RW; ++r) {
-    const int i = 2 * t + ROW * r;
-    wr[r] = i + 1 < len ? *reinterpret_cast<const double2*>(wg + i) : make_double2(i < len ? wg[i] : 0.0, 0.0);
-  }
-  for (int i = ROW * RW + 2 * t; i < len; i += ROW) {
+  for (int r = 0; r < RW; ++r)
+#pragma unroll
+    for (int u = 0; u < PPT; ++u) {
+      const int i = 2 * (t + NT * u) + ROW * r;
+      wr[r][u] = i + 1 < len ? *reinterpret_cast<const double2*>(wg + i) : make_double2(i < len ? wg[i] : 0.0, 0.0);
+    }
+  for (int i = ROW * RW + 2 * t; i < len; i += 2 * NT) {
     if (i + 1 < len)
       *reinterpret_cast<double2*>(wsm + i - ROW * RW) = *reinterpret_cast<const double2*>(wg + i);
     else
@@ -579,7 +581,7 @@ __global__ void __launch_bounds__(NT, 1) mgs_bulk_kernel(double* __restrict__ V,
   int task = 0;
   for (int j = 0; j <= k + 1; ++j) {
     double s0 = 0.0, s1 = 0.0;
-    auto row = [&](double2& wi, int r) {
+    auto row = [&](double2 (&wi)[PPT], int r) {
       const int s = task % NS;
       if (t == 0 && task + NS - 1 < ntask) {  // refill the stage freed by task - 1
         const int nt = task + NS - 1;
@@ -589,20 +591,23 @@ __global__ void __launch_bounds__(NT, 1) mgs_bulk_kernel(double* __restrict__ V,
       mbar_wait(&full[s], unsigned(task / NS) & 1u);
       const double* vjs = ring + 2 * ROW * s;
       const double* vps = vjs + ROW;
-      const int i = 2 * t + ROW * r;
-      if (i + 1 < len) {
-        if (j > 0) {
-          const double2 pv = *reinterpret_cast<const double2*>(vps + 2 * t);
-          wi.x = wi.x - h * pv.x;
-          wi.y = wi.y - h * pv.y;
+#pragma unroll
+      for (int u = 0; u < PPT; ++u) {
+        const int pr = 2 * (t + NT * u), i = pr + ROW * r;
+        if (i + 1 < len) {
+          if (j > 0) {
+            const double2 pv = *reinterpret_cast<const double2*>(vps + pr);
+            wi[u].x = wi[u].x - h * pv.x;
+            wi[u].y = wi[u].y - h * pv.y;
+          }
+          const double2 a = j <= k ? *reinterpret_cast<const double2*>(vjs + pr) : wi[u];
+          s0 += a.x * wi[u].x;
+          s1 += a.y * wi[u].y;
+        } else if (i < len) {
+          if (j > 0) wi[u].x = wi[u].x - h * vps[pr];
+          const double a = j <= k ? vjs[pr] : wi[u].x;
+          s0 += a * wi[u].x;
         }
-        const double2 a = j <= k ? *reinterpret_cast<const double2*>(vjs + 2 * t) : wi;
-        s0 += a.x * wi.x;
-        s1 += a.y * wi.y;
-      } else if (i < len) {
-        if (j > 0) wi.x = wi.x - h * vps[2 * t];
-        const double a = j <= k ? vjs[2 * t] : wi.x;
-        s0 += a * wi.x;
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
@@ -612,15 +617,24 @@ __global__ void __launch_bounds__(NT, 1) mgs_bulk_kernel(double* __restrict__ V,
     for (int r = 0; r < RW; ++r)
       if (r < nrows) row(wr[r], r);
     for (int r = RW; r < nrows; ++r) {
-      double* wp = wsm + ROW * (r - RW) + 2 * t;
-      const int i = 2 * t + ROW * r;
-      double2 wi = i + 1 < len ? *reinterpret_cast<const double2*>(wp) : make_double2(i < len ? wp[0] : 0.0, 0.0);
+      double2 wi[PPT];
+#pragma unroll
+      for (int u = 0; u < PPT; ++u) {
+        const int pr = 2 * (t + NT * u), i = pr + ROW * r;
+        const double* wp = wsm + ROW * (r - RW) + pr;
+        wi[u] = i + 1 < len ? *reinterpret_cast<const double2*>(wp) : make_double2(i < len ? wp[0] : 0.0, 0.0);
+      }
       row(wi, r);
       if (j > 0) {
-        if (i + 1 < len)
-          *reinterpret_cast<double2*>(wp) = wi;
-        else if (i < len)
-          wp[0] = wi.x;
+#pragma unroll
+        for (int u = 0; u < PPT; ++u) {
+          const int pr = 2 * (t + NT * u), i = pr + ROW * r;
+          double* wp = wsm + ROW * (r - RW) + pr;
+          if (i + 1 < len)
+            *reinterpret_cast<double2*>(wp) = wi[u];
+          else if (i < len)
+            wp[0] = wi[u].x;
+        }
       }
     }
     const double tot = mgs_grid_sum(s0 + s1, partial + size_t(j) * nb, bar, &tgt, shA, shB);
@@ -628,13 +642,15 @@ __global__ void __launch_bounds__(NT, 1) mgs_bulk_kernel(double* __restrict__ V,
     if (blockIdx.x == 0 && t == 0) hc[j] = h;
   }
 #pragma unroll
-  for (int r = 0; r < RW; ++r) {
-    const int i = 2 * t + ROW * r;
-    if (i + 1 < len)
-      *reinterpret_cast<double2*>(wg + i) = h > 0.0 ? make_double2(wr[r].x / h, wr[r].y / h) : wr[r];
-    else if (i < len)
-      wg[i] = h > 0.0 ? wr[r].x / h : wr[r].x;
-  }
+  for (int r = 0; r < RW; ++r)
+#pragma unroll
+    for (int u = 0; u < PPT; ++u) {
+      const int i = 2 * (t + NT * u) + ROW * r;
+      if (i + 1 < len)
+        *reinterpret_cast<double2*>(wg + i) = h > 0.0 ? make_double2(wr[r][u].x / h, wr[r][u].y / h) : wr[r][u];
+      else if (i < len)
+        wg[i] = h > 0.0 ? wr[r][u].x / h : wr[r][u].x;
+    }
   for (int i = ROW * RW + t; i < len; i += NT) wg[i] = h > 0.0 ? wsm[i - ROW * RW] / h : wsm[i - ROW * RW];
   mgs_epoch_end(bar, &tgt);
   fused_givens(G, k, gstatus);
@@ -649,7 +665,7 @@ struct CoopPlan {
 };
 
 // One 1024-thread CTA per SM (cheap barrier); the most shared-memory residency that fits.
-constexpr int kBulkThreads = 1024, kBulkRW = 8, kBulkStages = 2;  // measured best (cfg4 MGS 301 us): 1024/10/3 (spills) 307, 768/12/3 338, 512/16/4 354; v_{j-1} by per-thread L2 loads + 4-stage v_j ring 352
+constexpr int kBulkThreads = 512, kBulkRW = 10, kBulkStages = 3, kBulkPPT = 2;  // tools/mgs_bench at cfg4 size, us per pass: 1024/8/2/1 19.3, 512/8/2/2 16.7, 512/10/3/2 16.3, 512/10/2/2 17.2, 256/8/2/4 19.3, 256/14/5/4 25.1 (spills)
 
 CoopPlan mgs_coop_plan(int64_t n) {
   int dev = 0, sms = 0;
@@ -662,10 +678,10 @@ CoopPlan mgs_coop_plan(int64_t n) {
     return {sms, chunk, 0, R};
   }
   {  // w on chip (registers + shared memory), basis rows through the TMA ring
-    const int64_t rows = (chunk + 2 * kBulkThreads - 1) / (2 * kBulkThreads);
-    const size_t row_b = size_t(2 * kBulkThreads) * sizeof(double);
+    const int64_t rows = (chunk + 2 * kBulkThreads * kBulkPPT - 1) / (2 * kBulkThreads * kBulkPPT);
+    const size_t row_b = size_t(2 * kBulkThreads * kBulkPPT) * sizeof(double);
     const size_t sm = row_b * (2 * kBulkStages + size_t(rows > kBulkRW ? rows - kBulkRW : 0));
-    const void* fn = reinterpret_cast<const void*>(mgs_bulk_kernel<kBulkThreads, kBulkRW, kBulkStages>);
+    const void* fn = reinterpret_cast<const void*>(mgs_bulk_kernel<kBulkThreads, kBulkRW, kBulkStages, kBulkPPT>);
     int fit = 0;
     if (sm <= 227 * 1024) {
       ensure_smem(fn, sm);
@@ -747,7 +763,7 @@ void launch_mgs_iteration(double* V, int64_t ldv, int k, int64_t n, double* hc, 
              : plan.mode == 2 ? reinterpret_cast<void*>(mgs_regv_kernel<2>)
              : plan.mode == 3 ? reinterpret_cast<void*>(mgs_regv_kernel<3>)
              : plan.mode == 4 ? reinterpret_cast<void*>(mgs_regv_kernel<4>)
-             : plan.mode == 5 ? reinterpret_cast<void*>(mgs_bulk_kernel<kBulkThreads, kBulkRW, kBulkStages>)
+             : plan.mode == 5 ? reinterpret_cast<void*>(mgs_bulk_kernel<kBulkThreads, kBulkRW, kBulkStages, kBulkPPT>)
                               : reinterpret_cast<void*>(mgs_global_kernel);
   TPDG_CUDA_CHECK(cudaLaunchCooperativeKernel(fn, dim3(plan.grid), dim3(plan.threads), args, plan.smem, st));
   ++g_launches;

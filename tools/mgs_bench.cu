@@ -60,21 +60,26 @@ int main(int argc, char** argv) {
     for (int b = 0; b < sms; ++b) {
       const int64_t lo = b * chunk, hi = std::min<int64_t>(lo + chunk, n);
       const int len = int(hi > lo ? hi - lo : 0);
-      double lanev[1024];
-      for (int t = 0; t < 1024; ++t) {
+      // ownership of the bulk kernel (blas.cu kBulkThreads = 512, kBulkPPT = 2): thread t sums the pairs
+      // t + 512 u (u = 0, 1) of every 2048-double row, rows ascending; 16 warp sums in order
+      constexpr int NT = 512, PPT = 2, ROW = 2 * NT * PPT;
+      double lanev[NT];
+      for (int t = 0; t < NT; ++t) {
         double s0 = 0.0, s1 = 0.0;
-        for (int i = 2 * t; i < len; i += 2048) {
-          if (i + 1 < len) {
-            s0 = fma(v[lo + i], w[lo + i], s0);
-            s1 = fma(v[lo + i + 1], w[lo + i + 1], s1);
-          } else {
-            s0 = fma(v[lo + i], w[lo + i], s0);
+        for (int r0 = 0; r0 < len; r0 += ROW)
+          for (int u = 0; u < PPT; ++u) {
+            const int i = r0 + 2 * (t + NT * u);
+            if (i + 1 < len) {
+              s0 = fma(v[lo + i], w[lo + i], s0);
+              s1 = fma(v[lo + i + 1], w[lo + i + 1], s1);
+            } else if (i < len) {
+              s0 = fma(v[lo + i], w[lo + i], s0);
+            }
           }
-        }
         lanev[t] = s0 + s1;
       }
       double bs = 0.0;
-      for (int wi = 0; wi < 32; ++wi) {
+      for (int wi = 0; wi < NT / 32; ++wi) {
         double x[32];
         for (int l = 0; l < 32; ++l) x[l] = lanev[32 * wi + l];
         for (int o = 16; o > 0; o >>= 1) {
