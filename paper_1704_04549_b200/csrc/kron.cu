@@ -1034,35 +1034,6 @@ __global__ void __launch_bounds__(k3Threads) kron3d_sized_kernel(DevPC pc, const
 // no CTA barrier. The apply is then five DMMA products plus that column sweep. Not bit-faithful
 // (explicit inverses; ~1e-13 from the reference at cfg4, tools/study/kron3d_inv_emul.py; gate 1e-12).
 
-// Dense inverse by Gauss-Jordan with partial pivoting (n <= 2 * 16), a in local memory.
-__device__ void gj_inverse(double* a, double* inv, int n) {
-  for (int i = 0; i < n * n; ++i) inv[i] = (i / n == i % n) ? 1.0 : 0.0;
-  for (int c = 0; c < n; ++c) {
-    int pr = c;
-    for (int r = c + 1; r < n; ++r)
-      if (fabs(a[r * n + c]) > fabs(a[pr * n + c])) pr = r;
-    if (pr != c)
-      for (int j = 0; j < n; ++j) {
-        double t = a[c * n + j]; a[c * n + j] = a[pr * n + j]; a[pr * n + j] = t;
-        t = inv[c * n + j]; inv[c * n + j] = inv[pr * n + j]; inv[pr * n + j] = t;
-      }
-    const double d = 1.0 / a[c * n + c];
-    for (int j = 0; j < n; ++j) {
-      a[c * n + j] *= d;
-      inv[c * n + j] *= d;
-    }
-    for (int r = 0; r < n; ++r) {
-      if (r == c) continue;
-      const double f = a[r * n + c];
-      if (f == 0.0) continue;
-      for (int j = 0; j < n; ++j) {
-        a[r * n + j] = fma(-f, a[c * n + j], a[r * n + j]);
-        inv[r * n + j] = fma(-f, inv[c * n + j], inv[r * n + j]);
-      }
-    }
-  }
-}
-
 // Column c of A^-1 from the packed LU (unit lower L, U, perm) of a record.
 __device__ void lu_inverse_col(const double* lu, const int* perm, int n, int c, double* x) {
   for (int k = 0; k < n; ++k) x[k] = perm[k] == c ? 1.0 : 0.0;
@@ -1078,11 +1049,19 @@ __device__ void lu_inverse_col(const double* lu, const int* perm, int n, int c, 
   }
 }
 
-// One thread per block: irec = A1^-1 | L^T | R | Q1 | Q2 | T2 | G blocks (block b: sz q rows of stride
+// One warp per block: irec = A1^-1 | L^T | R | Q1 | Q2 | T2 | G blocks (block b: sz q rows of stride
 // g_row_stride, each of sz segments of q values padded to rs = even(q): 16-byte aligned segments, and
 // rows 2 (mod 4) doubles apart so that eight lanes reading eight rows hit eight bank groups).
-__global__ void kron3d_inv_prep_kernel(DevPC pc, double* __restrict__ irec) {
-  const int blk = blockIdx.x * blockDim.x + threadIdx.x;
+// Lanes take inverse columns, product entries and, in the Gauss-Jordan inverse of (I (x) T1 + T2_bb (x) I),
+// rows (elimination) or columns (swap / scaling); every entry sees the same operations in the same
+// order as a serial elimination. Shared memory per warp: K, G (m x m, m <= 2 q) and B2^-1, C1^-1.
+constexpr int kPrepWarps = 4;
+__host__ __device__ inline size_t kron3d_prep_smem_per_warp(int q) { return sizeof(double) * size_t(2 * 4 * q * q + 2 * q * q); }
+
+__global__ void __launch_bounds__(32 * kPrepWarps) kron3d_inv_prep_kernel(DevPC pc, double* __restrict__ irec) {
+  extern __shared__ double prep_sm[];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int blk = blockIdx.x * kPrepWarps + wid;
   if (blk >= pc.nblk || pc.kind[blk] == 0) return;
   const int n1 = pc.n1, q = pc.q;
   const double* r = pc.rec + size_t(blk) * pc.rec_len;  // LU(A1) | LU(B2) | LU(C1) | Q1 | T1 | Q2 | T2
@@ -1092,47 +1071,79 @@ __global__ void kron3d_inv_prep_kernel(DevPC pc, double* __restrict__ irec) {
   double* o = irec + size_t(blk) * irec3_doubles(n1, q);
   double *oA = o, *oLt = oA + n1 * n1, *oR = oLt + q * q, *oQ1 = oR + q * q, *oQ2 = oQ1 + q * q, *oT2 = oQ2 + q * q,
          *oG = oT2 + q * q;
-  double col[64], binv[16 * 16], cinv[16 * 16];
-  for (int c = 0; c < n1; ++c) {
+  double* K = prep_sm + size_t(wid) * (kron3d_prep_smem_per_warp(q) / sizeof(double));
+  double* G = K + 4 * q * q;
+  double* binv = G + 4 * q * q;
+  double* cinv = binv + q * q;
+  double col[64];
+  for (int c = lane; c < n1; c += 32) {
     lu_inverse_col(luA1, piv, n1, c, col);
     for (int k = 0; k < n1; ++k) oA[k * n1 + c] = col[k];
   }
-  for (int c = 0; c < q; ++c) {
+  for (int c = lane; c < q; c += 32) {
     lu_inverse_col(luB2, piv + n1, q, c, col);
     for (int k = 0; k < q; ++k) binv[k * q + c] = col[k];
     lu_inverse_col(luC1, piv + n1 + q, q, c, col);
     for (int k = 0; k < q; ++k) cinv[k * q + c] = col[k];
   }
-  for (int i = 0; i < q; ++i)
-    for (int j = 0; j < q; ++j) {
-      double lt = 0.0, rr = 0.0;
-      for (int k = 0; k < q; ++k) {
-        lt = fma(binv[k * q + i], Q1[k * q + j], lt);  // (B2^-T Q1)[i][j]
-        rr = fma(cinv[k * q + i], Q2[k * q + j], rr);  // (C1^-T Q2)[i][j]
-      }
-      oLt[i * q + j] = lt;
-      oR[i * q + j] = rr;
-      oQ1[i * q + j] = Q1[i * q + j];
-      oQ2[i * q + j] = Q2[i * q + j];
-      oT2[i * q + j] = T2[i * q + j];
+  __syncwarp();
+  for (int e = lane; e < q * q; e += 32) {
+    const int i = e / q, j = e % q;
+    double lt = 0.0, rr = 0.0;
+    for (int k = 0; k < q; ++k) {
+      lt = fma(binv[k * q + i], Q1[k * q + j], lt);  // (B2^-T Q1)[i][j]
+      rr = fma(cinv[k * q + i], Q2[k * q + j], rr);  // (C1^-T Q2)[i][j]
     }
-  double K[32 * 32], G[32 * 32];
+    oLt[e] = lt;
+    oR[e] = rr;
+    oQ1[e] = Q1[e];
+    oQ2[e] = Q2[e];
+    oT2[e] = T2[e];
+  }
   int off = 0;
   for (int k0 = 0; k0 < q;) {
     const int sz = (k0 + 1 < q && T2[(k0 + 1) * q + k0] != 0.0) ? 2 : 1;
     const int m = sz * q;  // vec(Y_b) column-major: index c q + i
-    for (int a = 0; a < m; ++a)
-      for (int b = 0; b < m; ++b) {
-        const int ca = a / q, ia = a % q, cb = b / q, ib = b % q;
-        K[a * m + b] = (ca == cb ? T1[ia * q + ib] : 0.0) + (ia == ib ? T2[(k0 + ca) * q + k0 + cb] : 0.0);
+    for (int e = lane; e < m * m; e += 32) {
+      const int a = e / m, b = e % m, ca = a / q, ia = a % q, cb = b / q, ib = b % q;
+      K[e] = (ca == cb ? T1[ia * q + ib] : 0.0) + (ia == ib ? T2[(k0 + ca) * q + k0 + cb] : 0.0);
+      G[e] = a == b ? 1.0 : 0.0;
+    }
+    __syncwarp();
+    for (int c = 0; c < m; ++c) {  // Gauss-Jordan with partial pivoting (first maximum), as a serial sweep
+      int pr = c;
+      for (int rr = c + 1; rr < m; ++rr)
+        if (fabs(K[rr * m + c]) > fabs(K[pr * m + c])) pr = rr;
+      if (pr != c)
+        for (int j = lane; j < m; j += 32) {
+          double t = K[c * m + j]; K[c * m + j] = K[pr * m + j]; K[pr * m + j] = t;
+          t = G[c * m + j]; G[c * m + j] = G[pr * m + j]; G[pr * m + j] = t;
+        }
+      __syncwarp();
+      const double d = 1.0 / K[c * m + c];
+      __syncwarp();
+      for (int j = lane; j < m; j += 32) {
+        K[c * m + j] *= d;
+        G[c * m + j] *= d;
       }
-    gj_inverse(K, G, m);
+      __syncwarp();
+      for (int rr = lane; rr < m; rr += 32) {  // lane = row: each row's entries in j order
+        if (rr == c) continue;
+        const double f = K[rr * m + c];
+        if (f == 0.0) continue;
+        for (int j = 0; j < m; ++j) {
+          K[rr * m + j] = fma(-f, K[c * m + j], K[rr * m + j]);
+          G[rr * m + j] = fma(-f, G[c * m + j], G[rr * m + j]);
+        }
+      }
+      __syncwarp();
+    }
     const int rs = (q + 1) & ~1, gs = g_row_stride(q, sz);  // row: sz segments of q values, each padded to rs
-    for (int a = 0; a < m; ++a)
-      for (int j = 0; j < gs; ++j) {
-        const int c = j / rs, jj = j - c * rs;
-        oG[off + a * gs + j] = (c < sz && jj < q) ? G[a * m + c * q + jj] : 0.0;
-      }
+    for (int e = lane; e < m * gs; e += 32) {
+      const int a = e / gs, j = e % gs, c = j / rs, jj = j - c * rs;
+      oG[off + e] = (c < sz && jj < q) ? G[a * m + c * q + jj] : 0.0;
+    }
+    __syncwarp();
     off += m * gs;
     k0 += sz;
   }
@@ -1598,7 +1609,9 @@ __global__ void __launch_bounds__(256) kron_fallback_kernel(DevPC pc, const doub
 
 void launch_kron3d_inv_prep(const DevPC& pc, double* irec, cudaStream_t st) {
   if (pc.nblk == 0) return;
-  kron3d_inv_prep_kernel<<<(pc.nblk + 63) / 64, 64, 0, st>>>(pc, irec);
+  const size_t smem = kron3d_prep_smem_per_warp(pc.q) * kPrepWarps;
+  ensure_smem(kron3d_inv_prep_kernel, smem);
+  kron3d_inv_prep_kernel<<<(pc.nblk + kPrepWarps - 1) / kPrepWarps, 32 * kPrepWarps, smem, st>>>(pc, irec);
   TPDG_CUDA_CHECK(cudaGetLastError());
 }
 
