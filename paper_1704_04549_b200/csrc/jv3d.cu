@@ -73,6 +73,10 @@ struct Jv3dLayout {
   static constexpr int x2 = cmax(Q * M2 + 12 * M2, Q3 + 6 * Q2);
   static constexpr int wa = x1 + x2;
   static constexpr int total = wa + 6 * Q * MU;
+  // X2 tail (free while the next element's v | neighbour layers travel, E4 -> E1): a shared copy of G
+  // and the lifted face contributions lift[f][j1][j0] (E5a), read by the x-integration pencils (E5b)
+  static constexpr int sg = v + Q3 + 6 * Q2, lift = sg + MU * Q;
+  static_assert(lift + 6 * Q2 <= x1 + x2, "X2 tail too small for the lifted face layers");
 };
 
 __device__ __forceinline__ void prefetch_l2(const void* p, unsigned bytes) {
@@ -270,7 +274,10 @@ __global__ void __launch_bounds__(NT, MINB) jv3d_fast_kernel(DevSys s, const dou
     __syncthreads();
     // the next element's v and neighbour layers travel during E4 / E5 (X2 is free from here on)
     if (e_next < s.e_hi) load_element_async<Q, NT>(s, vin, halo, e_next, sm + L::v, sm + L::nbl);
-    // ---- E4: y integration, pencils (k, al): S1 = Gy A1 + Dy A3 (-> A1 slots), S2 = Gy A2 (-> A2 slots)
+    // ---- E4: y integration, pencils (k, al): S1 = Gy A1 + Dy A3 (-> A1 slots), S2 = Gy A2 (-> A2 slots);
+    //      the threads without a pencil stage G in shared memory for E5a
+    for (int p = Q * MU + (tid - Q * MU); tid >= Q * MU && p < Q * MU + MU * Q; p += NT - Q * MU)
+      sm[L::sg + p - Q * MU] = W::G(p - Q * MU);
     for (int p = tid; p < Q * MU; p += NT) {
       const int k = p / MU, al = p % MU;
       const int base = k * M2 + al;
@@ -294,8 +301,18 @@ __global__ void __launch_bounds__(NT, MINB) jv3d_fast_kernel(DevSys s, const dou
       }
     }
     __syncthreads();
-    // ---- E5: x integration, pencils (k, j): out = Gx S1 + Dx S2, plus the face lifts of the layers
-    //      (face_lift, discretization.hpp:133-166), straight to HBM
+    // ---- E5a: second stage of the face lifts (face_lift, discretization.hpp:133-166), spread over all
+    //      threads: lift[f][j1][j0] = sum_bb G(bb, j1) wa[f][j0][bb]
+    for (int it = tid; it < 6 * Q2; it += NT) {
+      const int f = it / Q2, j1 = (it % Q2) / Q, j0 = it % Q;
+      const double* w = sm + L::wa + (f * Q + j0) * MU;
+      double l = 0.0;
+#pragma unroll
+      for (int bb = 0; bb < MU; ++bb) l = fma(sm[L::sg + bb * Q + j1], w[bb], l);
+      sm[L::lift + it] = l;
+    }
+    __syncthreads();
+    // ---- E5b: x integration, pencils (k, j): out = Gx S1 + Dx S2, plus the lifted layers, straight to HBM
     for (int p = tid; p < Q2; p += NT) {
       const int k = p / Q, j = p % Q;
       const int base = k * M2 + j * MU;
@@ -305,34 +322,18 @@ __global__ void __launch_bounds__(NT, MINB) jv3d_fast_kernel(DevSys s, const dou
         x1[al] = sm[L::A1 + base + al];
         x2[al] = sm[L::A2 + base + al];
       }
-      // lifts of the faces whose layer contains the whole pencil (y, z faces), tangential (i, k) / (i, j)
-      const double* ly = (j == 0) ? sm + L::wa + 2 * Q * MU : (j == Q - 1 ? sm + L::wa + 3 * Q * MU : nullptr);
-      const double* lz = (k == 0) ? sm + L::wa + 4 * Q * MU : (k == Q - 1 ? sm + L::wa + 5 * Q * MU : nullptr);
+      // lifted layers of the faces whose layer contains the whole pencil (y, z faces), tangential (i, k) / (i, j)
+      const double* ly = (j == 0) ? sm + L::lift + 2 * Q2 + k * Q : (j == Q - 1 ? sm + L::lift + 3 * Q2 + k * Q : nullptr);
+      const double* lz = (k == 0) ? sm + L::lift + 4 * Q2 + j * Q : (k == Q - 1 ? sm + L::lift + 5 * Q2 + j * Q : nullptr);
       double* oe = vout + size_t(e) * Q3 + p * Q;
 #pragma unroll
       for (int i = 0; i < Q; ++i) {
         double acc = 0.0;
 #pragma unroll
         for (int al = 0; al < MU; ++al) acc = fma(W::GW(i * MU + al), x1[al], fma(W::DW(i * MU + al), x2[al], acc));
-        if (ly) {  // face 2/3: (j0, j1) = (i, k)
-          double l = 0.0;
-#pragma unroll
-          for (int bb = 0; bb < MU; ++bb) l = fma(W::G(bb * Q + k), ly[i * MU + bb], l);
-          acc += l;
-        }
-        if (lz) {  // face 4/5: (j0, j1) = (i, j)
-          double l = 0.0;
-#pragma unroll
-          for (int bb = 0; bb < MU; ++bb) l = fma(W::G(bb * Q + j), lz[i * MU + bb], l);
-          acc += l;
-        }
-        if (i == 0 || i == Q - 1) {  // face 0/1: (j0, j1) = (j, k)
-          const double* lx = sm + L::wa + (i == 0 ? 0 : 1) * Q * MU + j * MU;
-          double l = 0.0;
-#pragma unroll
-          for (int bb = 0; bb < MU; ++bb) l = fma(W::G(bb * Q + k), lx[bb], l);
-          acc += l;
-        }
+        if (ly) acc += ly[i];  // face 2/3: (j0, j1) = (i, k)
+        if (lz) acc += lz[i];  // face 4/5: (j0, j1) = (i, j)
+        if (i == 0 || i == Q - 1) acc += sm[L::lift + (i == 0 ? 0 : 1) * Q2 + k * Q + j];  // face 0/1: (j0, j1) = (j, k)
         oe[i] = acc;
       }
     }
