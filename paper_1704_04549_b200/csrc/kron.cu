@@ -1028,10 +1028,12 @@ __global__ void __launch_bounds__(k3Threads) kron3d_sized_kernel(DevPC pc, const
 //   A1^-1, L^T = B2^-T Q1, R = C1^-T Q2, Q1, Q2, T2 and G_b = (I (x) T1 + T2_bb (x) I)^-1 for every
 //   quasi-diagonal block b of T2 (1x1 or 2x2),
 // so that the three LU axis solves fold into the rotations: M_s = L (A1^-1 x)_s R. The Sylvester
-// solve T1 Y_s + Y_s T2^T = M_s runs over T2's blocks right to left; thread (s, i) owns row i of
-// slice s, forms its right-hand side from its own solved row and T2, and G_b mixes the rows of the
-// slice, which all sit in the thread's warp (SPW = 32 / Q slices per warp): one __syncwarp per block,
-// no CTA barrier. The apply is then five DMMA products plus that column sweep. Not bit-faithful
+// solve T1 Y_s + Y_s T2^T = M_s runs over T2's blocks right to left, as DMMA products of the
+// right-hand sides of eight slices with G_b^T per block (each lane forms the right-hand sides of its own
+// (slice, row) entries from its solved entries and T2; no barrier). The whole apply is DMMA products
+// plus those right-hand sides. (Round 2's first version applied G_b row by row on the CUDA cores, one
+// thread per (slice, row): 8.9k shared-memory wavefronts per element, 85 % of the SM's shared-memory
+// bandwidth, most of them G_b rows re-read by every warp.) Not bit-faithful
 // (explicit inverses; ~1e-13 from the reference at cfg4, tools/study/kron3d_inv_emul.py; gate 1e-12).
 
 // Column c of A^-1 from the packed LU (unit lower L, U, perm) of a record.
@@ -1049,9 +1051,9 @@ __device__ void lu_inverse_col(const double* lu, const int* perm, int n, int c, 
   }
 }
 
-// One warp per block: irec = A1^-1 | L^T | R | Q1 | Q2 | T2 | G blocks (block b: sz q rows of stride
-// g_row_stride, each of sz segments of q values padded to rs = even(q): 16-byte aligned segments, and
-// rows 2 (mod 4) doubles apart so that eight lanes reading eight rows hit eight bank groups).
+// One warp per block: irec = A1^-1 | L^T | R | Q1 | Q2 | T2 | G blocks (block b of size m = sz q stored
+// transposed, Gt[k'][n] = G_b[n][k'], m rows of g_t_ld(q, sz) = 4 (mod 8) doubles: the DMMA B-fragment loads
+// of the apply's Sylvester sweep -- eight consecutive n by four k' two rows apart -- are conflict-free).
 // Lanes take inverse columns, product entries and, in the Gauss-Jordan inverse of (I (x) T1 + T2_bb (x) I),
 // rows (elimination) or columns (swap / scaling); every entry sees the same operations in the same
 // order as a serial elimination. Shared memory per warp: K, G (m x m, m <= 2 q) and B2^-1, C1^-1.
@@ -1138,13 +1140,13 @@ __global__ void __launch_bounds__(32 * kPrepWarps) kron3d_inv_prep_kernel(DevPC 
       }
       __syncwarp();
     }
-    const int rs = (q + 1) & ~1, gs = g_row_stride(q, sz);  // row: sz segments of q values, each padded to rs
-    for (int e = lane; e < m * gs; e += 32) {
-      const int a = e / gs, j = e % gs, c = j / rs, jj = j - c * rs;
-      oG[off + e] = (c < sz && jj < q) ? G[a * m + c * q + jj] : 0.0;
+    const int ld = g_t_ld(q, sz);  // transposed: Gt[k'][n] = G[n][k'], m rows of ld (= 4 mod 8) doubles
+    for (int e = lane; e < m * ld; e += 32) {
+      const int kk = e / ld, n = e % ld;
+      oG[off + e] = n < m ? G[n * m + kk] : 0.0;
     }
     __syncwarp();
-    off += m * gs;
+    off += m * ld;
     k0 += sz;
   }
 }
@@ -1155,9 +1157,10 @@ struct Kron3dInvLayout {
   static constexpr int N1P = p8(N1), K1 = p4(N1), QQ = Q * Q, QQP = p8(QQ);
   static constexpr int QP = p8(Q), KQ = p4(Q), NC = N1 * Q, NCP = p8(NC);
   static constexpr int LDS0 = lda4(QQP), LDA = lda4(K1), LDR = lda4(NCP), LDP = lda4(KQ), LQ = lda4(QP);
-  static constexpr int RS = (Q + 1) & ~1;  // padded row segment (G rows, rhs slices): 16-byte aligned
-  static constexpr int GS1 = g_row_stride(Q, 1), GS2 = g_row_stride(Q, 2);
-  static constexpr int GB = 2 * Q * GS2;   // largest G block (a 2x2 T2 block), doubles
+  static constexpr int NWS = (N1 + 7) / 8;  // Sylvester warps: slices 8 w .. 8 w + 7 are the rows of their tiles
+  static_assert(NWS <= NW, "Sylvester warps");
+  static constexpr int LD1 = g_t_ld(Q, 1), LD2 = g_t_ld(Q, 2);
+  static constexpr int GB = 2 * Q * LD2;   // largest G block (a 2x2 T2 block), doubles
   static constexpr int NG = 3;             // G ring slots (two blocks in flight ahead of the one in use)
   static constexpr int mx(int a, int b) { return a > b ? a : b; }
   // one region, reused: x staged as [s][(r, j)] (GEMM 0) -> P rows (GEMM 1/2) -> G ring (Sylvester) -> Z rows
@@ -1170,8 +1173,7 @@ struct Kron3dInvLayout {
   static constexpr int o_q1 = o_r + QP * LQ;
   static constexpr int o_q2 = o_q1 + QP * LQ;
   static constexpr int o_t2 = o_q2 + QP * LQ;          // T2
-  static constexpr int o_rhs = (o_t2 + QQ + 1) & ~1;   // per warp: 2 parities x 2 columns x SPW slices x RS
-  static constexpr int o_lut = o_rhs + NW * 4 * SPW * RS;  // int LUTs: Xr offset of (r, j) = n; P offset of (s, r')
+  static constexpr int o_lut = (o_t2 + QQ + 1) & ~1;  // int LUTs: Xr offset of (r, j) = n; P offset of (s, r')
   static constexpr int total = o_lut + (QQP + NCP + 1) / 2 + 1;
 };
 
@@ -1182,7 +1184,7 @@ __global__ void __launch_bounds__(Kron3dInvLayout<N1, Q>::NTH) kron3d_inv_kernel
   const int blk = blockIdx.x;
   if (pc.kind[blk] == 0 || (pc.skip && *pc.skip)) return;
   using L = Kron3dInvLayout<N1, Q>;
-  constexpr int NW = L::NW, NTH = L::NTH, SPW = L::SPW, QQ = L::QQ, QP = L::QP, KQ = L::KQ, NC = L::NC,
+  constexpr int NW = L::NW, NTH = L::NTH, QQ = L::QQ, QP = L::QP, KQ = L::KQ, NC = L::NC,
                 LDS0 = L::LDS0, LDA = L::LDA, LDR = L::LDR, LDP = L::LDP, LQ = L::LQ, K1 = L::K1;
   extern __shared__ double sm[];
   double* S0 = sm + L::o_s0;
@@ -1239,7 +1241,7 @@ __global__ void __launch_bounds__(Kron3dInvLayout<N1, Q>::NTH) kron3d_inv_kernel
       bplan[k0] = sz == 1 ? 0 : 2;
       if (sz == 2) bplan[k0 + 1] = 1;
       bplan[16 + k0 + sz - 1] = goff;
-      goff += sz * Q * (sz == 1 ? L::GS1 : L::GS2);
+      goff += sz * Q * (sz == 1 ? L::LD1 : L::LD2);
       k0 += sz;
     }
     bplan[32] = goff;
@@ -1248,12 +1250,12 @@ __global__ void __launch_bounds__(Kron3dInvLayout<N1, Q>::NTH) kron3d_inv_kernel
       if (bplan[k] == 2) continue;
       const int sz = bplan[k] == 0 ? 1 : 2;
       bplan[34 + ns] = bplan[16 + k];
-      bplan[50 + ns++] = 8 * sz * Q * (sz == 1 ? L::GS1 : L::GS2);
+      bplan[50 + ns++] = 8 * sz * Q * (sz == 1 ? L::LD1 : L::LD2);
     }
     bplan[33] = ns;
     for (int i = 0; i < L::NG; ++i) {
       mbar_init(&gfull[i], 1);
-      mbar_init(&gempty[i], NW);
+      mbar_init(&gempty[i], L::NWS);
     }
     mbar_fence_init();
   }
@@ -1335,94 +1337,120 @@ __global__ void __launch_bounds__(Kron3dInvLayout<N1, Q>::NTH) kron3d_inv_kernel
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic accesses to P before the TMA writes
     for (int u = 0; u < 2 && u < bplan[33]; ++u) g_issue(u);
   }
-  {  // Sylvester T1 Y_s + Y_s T2^T = M_s, T2 columns right to left; thread (s, i), s = SPW warp + lane / Q,
-     // holds row i of Y_s in registers (compile-time column indices; the block structure is a uniform branch)
-    constexpr int RS = L::RS;
-    const int sub = lane / Q, i = lane - sub * Q, sl = warp * SPW + sub;
-    const bool act = sub < SPW && sl < N1;
-    double* row = Xr + i * LDR + (act ? sl : 0) * Q;
-    double* rb = sm + L::o_rhs + warp * (4 * SPW * RS);  // [parity][column c][slice sub][RS]
-    const int me = (sub < SPW ? sub : 0) * RS;
-    double yr[Q];
-#pragma unroll
-    for (int l = 0; l < Q; ++l) yr[l] = row[l];
-    int par = 0, step = 0;
+  if (warp < L::NWS) {
+    // Sylvester T1 Y_s + Y_s T2^T = M_s over T2's quasi-diagonal blocks, right to left, on the tensor cores:
+    // for block b (columns c of Y_s, m = |b| q unknowns per slice) [y_c]^T = [rhs_c]^T G_b^T with
+    // rhs_c = m_c - sum_{l > b} T2[c][l] y_l, all slices of the warp at once. Warp w takes slices
+    // s = 8 w + lane / 4 (the rows of its DMMA tiles); lane quad q = lane % 4 owns the rows
+    // i = 8 (t >> 1) + 2 q + (t & 1), t < 2 NTQ, of every column of its slice: exactly the accumulator
+    // entries (tile t >> 1, entry t & 1) a product returns to it and the A-fragment entries it supplies
+    // at k-step t (the K order of the product is permuted accordingly, Gt rows read in the same order).
+    // A lane reads and writes only its own (s, i) entries of Xr, so the sweep needs no barrier.
+    constexpr int NTQ = (Q + 7) / 8, NSL = 2 * NTQ, LD1 = L::LD1, LD2 = L::LD2;
+    const int r8 = lane >> 2, q4 = lane & 3, sl = 8 * warp + r8;
+    const bool sok = sl < N1;
+    double* xs = Xr + (sok ? sl : 0) * Q;  // Y_s[i][l] at xs[i LDR + l]
+    int step = 0;
 #pragma unroll
     for (int k = Q - 1; k >= 0; --k) {
       const int kind = bplan[k];
       if (kind == 2) continue;
-      double* rp = rb + par * (2 * SPW * RS);
       const int slot = step % L::NG;
       const double* g = S0 + slot * L::GB;
       if (tid == 0 && step + 2 < bplan[33]) {  // refill the slot freed by step - 1
         if (step >= 1) mbar_wait(&gempty[(step + 2) % L::NG], unsigned((step - 1) / L::NG) & 1u);
         g_issue(step + 2);
       }
-      mbar_wait(&gfull[slot], unsigned(step / L::NG) & 1u);
-      if (kind == 0) {
-        double s0 = yr[k], s1 = 0.0;
+      if (kind == 0) {  // 1x1 block, column k
+        double a[NSL];
 #pragma unroll
-        for (int l = k + 1; l < Q; ++l) {
-          if ((l - k) & 1) s0 = fma(-yr[l], sT2[k * Q + l], s0);
-          else s1 = fma(-yr[l], sT2[k * Q + l], s1);
-        }
-        if (act) rp[me + i] = s0 + s1;
-        __syncwarp();
-        const double* gr = g + i * L::GS1;
-        double y0 = 0.0, y1 = 0.0;
+        for (int t = 0; t < NSL; ++t) {
+          const int i = 8 * (t >> 1) + 2 * q4 + (t & 1);
+          double s0 = 0.0, s1 = 0.0;
+          if (sok && i < Q) {
+            const double* xr = xs + i * LDR;
+            s0 = xr[k];
 #pragma unroll
-        for (int j = 0; j + 1 < Q; j += 2) {
-          const double2 gv = *reinterpret_cast<const double2*>(gr + j);
-          const double2 rv = *reinterpret_cast<const double2*>(rp + me + j);
-          y0 = fma(gv.x, rv.x, y0);
-          y1 = fma(gv.y, rv.y, y1);
-        }
-        if (Q & 1) y0 = fma(gr[Q - 1], rp[me + Q - 1], y0);
-        yr[k] = y0 + y1;
-      } else if (k > 0) {  // 2x2 block (k - 1, k)
-        double a0 = yr[k - 1], a1 = yr[k];
-#pragma unroll
-        for (int l = k + 1; l < Q; ++l) {
-          a0 = fma(-yr[l], sT2[(k - 1) * Q + l], a0);
-          a1 = fma(-yr[l], sT2[k * Q + l], a1);
-        }
-        if (act) {
-          rp[me + i] = a0;
-          rp[SPW * RS + me + i] = a1;
-        }
-        __syncwarp();
-        const double* g0 = g + i * L::GS2;
-        const double* g1 = g + (Q + i) * L::GS2;
-        double y0 = 0.0, y1 = 0.0, z0 = 0.0, z1 = 0.0;
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          const double* r = rp + c * SPW * RS + me;
-#pragma unroll
-          for (int j = 0; j + 1 < Q; j += 2) {
-            const double2 rv = *reinterpret_cast<const double2*>(r + j);
-            const double2 u0 = *reinterpret_cast<const double2*>(g0 + c * RS + j);
-            const double2 u1 = *reinterpret_cast<const double2*>(g1 + c * RS + j);
-            y0 = fma(u0.x, rv.x, y0);
-            z0 = fma(u0.y, rv.y, z0);
-            y1 = fma(u1.x, rv.x, y1);
-            z1 = fma(u1.y, rv.y, z1);
+            for (int l = k + 1; l < Q; ++l) {
+              if ((l - k) & 1) s0 = fma(-xr[l], sT2[k * Q + l], s0);
+              else s1 = fma(-xr[l], sT2[k * Q + l], s1);
+            }
           }
-          if (Q & 1) {
-            y0 = fma(g0[c * RS + Q - 1], r[Q - 1], y0);
-            y1 = fma(g1[c * RS + Q - 1], r[Q - 1], y1);
+          a[t] = s0 + s1;
+        }
+        mbar_wait(&gfull[slot], unsigned(step / L::NG) & 1u);
+        double acc[NTQ][2];
+#pragma unroll
+        for (int nt = 0; nt < NTQ; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
+#pragma unroll
+        for (int kc = 0; kc < NSL; ++kc) {
+          const int kk = 8 * (kc >> 1) + 2 * q4 + (kc & 1);
+#pragma unroll
+          for (int nt = 0; nt < NTQ; ++nt) {
+            const int n = 8 * nt + r8;
+            dmma(acc[nt], a[kc], (kk < Q && n < Q) ? g[kk * LD1 + n] : 0.0);
           }
         }
-        yr[k - 1] = y0 + z0;
-        yr[k] = y1 + z1;
+        if (sok)
+#pragma unroll
+          for (int nt = 0; nt < NTQ; ++nt)
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const int i = 8 * nt + 2 * q4 + u;
+              if (i < Q) xs[i * LDR + k] = acc[nt][u];
+            }
+      } else if (k > 0) {  // 2x2 block, columns k - 1, k
+        double a[2][NSL];
+#pragma unroll
+        for (int t = 0; t < NSL; ++t) {
+          const int i = 8 * (t >> 1) + 2 * q4 + (t & 1);
+          double a0 = 0.0, a1 = 0.0;
+          if (sok && i < Q) {
+            const double* xr = xs + i * LDR;
+            a0 = xr[k - 1];
+            a1 = xr[k];
+#pragma unroll
+            for (int l = k + 1; l < Q; ++l) {
+              a0 = fma(-xr[l], sT2[(k - 1) * Q + l], a0);
+              a1 = fma(-xr[l], sT2[k * Q + l], a1);
+            }
+          }
+          a[0][t] = a0;
+          a[1][t] = a1;
+        }
+        mbar_wait(&gfull[slot], unsigned(step / L::NG) & 1u);
+        double acc[2][NTQ][2];
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+          for (int nt = 0; nt < NTQ; ++nt) acc[c][nt][0] = acc[c][nt][1] = 0.0;
+#pragma unroll
+        for (int cp = 0; cp < 2; ++cp)
+#pragma unroll
+          for (int kc = 0; kc < NSL; ++kc) {
+            const int kk = 8 * (kc >> 1) + 2 * q4 + (kc & 1);
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+#pragma unroll
+              for (int nt = 0; nt < NTQ; ++nt) {
+                const int n = 8 * nt + r8;
+                dmma(acc[c][nt], a[cp][kc], (kk < Q && n < Q) ? g[(cp * Q + kk) * LD2 + c * Q + n] : 0.0);
+              }
+          }
+        if (sok)
+#pragma unroll
+          for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int nt = 0; nt < NTQ; ++nt)
+#pragma unroll
+              for (int u = 0; u < 2; ++u) {
+                const int i = 8 * nt + 2 * q4 + u;
+                if (i < Q) xs[i * LDR + k - 1 + c] = acc[c][nt][u];
+              }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&gempty[slot]);
       ++step;
-      par ^= 1;
-    }
-    if (act) {
-#pragma unroll
-      for (int l = 0; l < Q; ++l) row[l] = yr[l];
     }
   }
   __syncthreads();

@@ -142,11 +142,10 @@ void launch_pc_apply(const DevPC& pc, const double* in, double* out, cudaStream_
 // 3D tensor-core apply operands of every factored block (formation time)
 void launch_kron3d_inv_prep(const DevPC& pc, double* irec, cudaStream_t st);
 // Row stride of the 3D Sylvester block inverses G (sz = 1, 2): segments of even(q) doubles, rows 2 (mod 4) apart
-__host__ __device__ constexpr int g_row_stride(int q, int sz) {
-  return sz == 1 ? (((q + 1) & ~1) % 4 == 2 ? ((q + 1) & ~1) : ((q + 1) & ~1) + 2) : 2 * ((q + 1) & ~1) + 2;
-}
-// A1^-1 | L^T | R | Q1 | Q2 | T2 | G blocks (<= q^2 g_row_stride(q, 2))
-__host__ __device__ inline size_t irec3_doubles(int n1, int q) { return size_t(n1) * n1 + 5 * q * q + size_t(q) * q * g_row_stride(q, 2); }
+// leading dimension of a transposed G block of sz x sz T2 cells: the smallest >= sz q that is 4 (mod 8)
+__host__ __device__ constexpr int g_t_ld(int q, int sz) { return (sz * q + 3) / 8 * 8 + 4; }
+// A1^-1 | L^T | R | Q1 | Q2 | T2 | G blocks (<= q^2 g_t_ld(q, 2): every block 2 x 2)
+__host__ __device__ inline size_t irec3_doubles(int n1, int q) { return size_t(n1) * n1 + 5 * q * q + size_t(q) * q * g_t_ld(q, 2); }
 // bit-faithful 2D apply, several blocks per warp (kron_ew.cu); false if no sized variant fits
 bool launch_kron2d_ew(const DevPC& pc, const double* in, double* out, cudaStream_t st);
 // dense-LU fallback blocks, one CTA per fallback block (kron_fallback.cu); false if n is too large

@@ -110,5 +110,12 @@ int main(int argc, char** argv) {
   unsigned long long x = 0;
   for (int j = 0; j <= K; ++j) x ^= reinterpret_cast<unsigned long long&>(hh[j]) * (j + 1);
   printf("hc checksum %016llx (h0 %.17g)\n", x, hh[0]);
+  {  // the whole basis after the last launch (w normalized into V[K])
+    std::vector<double> vv(ldv * 32);
+    cudaMemcpy(vv.data(), V, sizeof(double) * ldv * 32, cudaMemcpyDeviceToHost);
+    unsigned long long y = 0;
+    for (size_t i = 0; i < vv.size(); ++i) y = y * 1000003ull + reinterpret_cast<unsigned long long&>(vv[i]);
+    printf("V checksum %016llx\n", y);
+  }
   return 0;
 }
