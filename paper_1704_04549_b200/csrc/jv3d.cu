@@ -67,12 +67,16 @@ struct Jv3dLayout {
   //   X1: t1 | tw (E1-E2), then A1 | A2 | A3 (E3-E4; S1, S2 over A1, A2 until E5)
   //   X2: t2 | str (E2-E3), then the next element's v | neighbour face layers (cp.async, E4 -> E1)
   //   X3: lifted face data wa (E3-E5)
-  static constexpr int t1 = 0, tw = Q2 * MU, A1 = 0, A2 = Q * M2, A3 = 2 * Q * M2;
-  static constexpr int x1 = cmax(3 * Q * M2, Q2 * MU + 12 * Q * MU);
+  // Rows of MU entries that consecutive lanes read or write one row apart (t1 / tw stores, str, wa and
+  // S loads) are MP = MU | 1 doubles apart: an odd stride spreads the 16 lanes of a 64-bit wavefront
+  // over all banks (stride 12 was a 4-way conflict).
+  static constexpr int MP = MU | 1;
+  static constexpr int t1 = 0, tw = Q2 * MP, A1 = 0, A2 = Q * M2, A3 = 2 * Q * M2;
+  static constexpr int x1 = cmax(3 * Q * M2, Q2 * MP + 12 * Q * MP);
   static constexpr int t2 = x1, str = t2 + Q * M2, v = x1, nbl = v + Q3;
-  static constexpr int x2 = cmax(Q * M2 + 12 * M2, Q3 + 6 * Q2);
+  static constexpr int x2 = cmax(Q * M2 + 12 * MU * MP, Q3 + 6 * Q2);
   static constexpr int wa = x1 + x2;
-  static constexpr int total = wa + 6 * Q * MU;
+  static constexpr int total = wa + 6 * Q * MP;
   // X2 tail (free while the next element's v | neighbour layers travel, E4 -> E1): a shared copy of G
   // and the lifted face contributions lift[f][j1][j0] (E5a), read by the x-integration pencils (E5b)
   static constexpr int sg = v + Q3 + 6 * Q2, lift = sg + MU * Q;
@@ -161,7 +165,7 @@ __global__ void __launch_bounds__(NT, MINB) jv3d_fast_kernel(DevSys s, const dou
       if (p < Q2) {
 #pragma unroll
         for (int i = 0; i < Q; ++i) x[i] = sm[L::v + p * Q + i];
-        dst = sm + L::t1 + p * MU;
+        dst = sm + L::t1 + p * L::MP;
       } else {
         const int idx = p - Q2, j1 = idx % Q, sf = idx / Q, f = sf % 6;
         if (sf < 6) {
@@ -171,7 +175,7 @@ __global__ void __launch_bounds__(NT, MINB) jv3d_fast_kernel(DevSys s, const dou
 #pragma unroll
           for (int j0 = 0; j0 < Q; ++j0) x[j0] = sm[L::nbl + f * Q2 + j0 * Q + j1];
         }
-        dst = sm + L::tw + (sf * Q + j1) * MU;
+        dst = sm + L::tw + (sf * Q + j1) * L::MP;
       }
 #pragma unroll
       for (int al = 0; al < MU; ++al) {
@@ -188,7 +192,7 @@ __global__ void __launch_bounds__(NT, MINB) jv3d_fast_kernel(DevSys s, const dou
       if (p < Q * MU) {
         const int k = p / MU, al = p % MU;
 #pragma unroll
-        for (int j = 0; j < Q; ++j) x[j] = sm[L::t1 + (k * Q + j) * MU + al];
+        for (int j = 0; j < Q; ++j) x[j] = sm[L::t1 + (k * Q + j) * L::MP + al];
 #pragma unroll
         for (int be = 0; be < MU; ++be) {
           double acc = 0.0;
@@ -199,13 +203,13 @@ __global__ void __launch_bounds__(NT, MINB) jv3d_fast_kernel(DevSys s, const dou
       } else {
         const int idx = p - Q * MU, a = idx % MU, sf = idx / MU;
 #pragma unroll
-        for (int j1 = 0; j1 < Q; ++j1) x[j1] = sm[L::tw + (sf * Q + j1) * MU + a];
+        for (int j1 = 0; j1 < Q; ++j1) x[j1] = sm[L::tw + (sf * Q + j1) * L::MP + a];
 #pragma unroll
         for (int b = 0; b < MU; ++b) {
           double acc = 0.0;
 #pragma unroll
           for (int j1 = 0; j1 < Q; ++j1) acc = fma(W::G(b * Q + j1), x[j1], acc);
-          sm[L::str + sf * M2 + b * MU + a] = acc;
+          sm[L::str + (sf * MU + b) * L::MP + a] = acc;
         }
       }
     }
@@ -226,7 +230,7 @@ __global__ void __launch_bounds__(NT, MINB) jv3d_fast_kernel(DevSys s, const dou
           int u = (code & 4) ? b : a, w = (code & 4) ? a : b;  // orient_face_coords (mesh.hpp:57-67)
           if (code & 1) u = MU - 1 - u;
           if (code & 2) w = MU - 1 - w;
-          const double tm = sm[L::str + f * M2 + b * MU + a], tp = sm[L::str + (6 + f) * M2 + w * MU + u];
+          const double tm = sm[L::str + (f * MU + b) * L::MP + a], tp = sm[L::str + ((6 + f) * MU + w) * L::MP + u];
           g[a] = fma(__ldg(cm + a), tm, __ldg(cp + a) * tp);
         }
 #pragma unroll
@@ -234,7 +238,7 @@ __global__ void __launch_bounds__(NT, MINB) jv3d_fast_kernel(DevSys s, const dou
           double acc = 0.0;
 #pragma unroll
           for (int a = 0; a < MU; ++a) acc = fma(W::G(a * Q + j), g[a], acc);
-          sm[L::wa + (f * Q + j) * MU + b] = acc;
+          sm[L::wa + (f * Q + j) * L::MP + b] = acc;
         }
       } else {
         const int c = p - 6 * MU;  // column (be, al) = c
@@ -258,9 +262,10 @@ __global__ void __launch_bounds__(NT, MINB) jv3d_fast_kernel(DevSys s, const dou
           const double f2 = c23.y * val;
 #pragma unroll
           for (int k = 0; k < Q; ++k) {
-            A1[k] = fma(W::GW(k * MU + ga), fm, fma(W::DW(k * MU + ga), f2, A1[k]));
-            A2[k] = fma(W::GW(k * MU + ga), f0, A2[k]);
-            A3[k] = fma(W::GW(k * MU + ga), f1, A3[k]);
+            const double gw = W::GW(k * MU + ga);
+            A1[k] = fma(gw, fm, fma(W::DW(k * MU + ga), f2, A1[k]));
+            A2[k] = fma(gw, f0, A2[k]);
+            A3[k] = fma(gw, f1, A3[k]);
           }
         }
 #pragma unroll
@@ -293,8 +298,9 @@ __global__ void __launch_bounds__(NT, MINB) jv3d_fast_kernel(DevSys s, const dou
         double s1 = 0.0, s2 = 0.0;
 #pragma unroll
         for (int be = 0; be < MU; ++be) {
-          s1 = fma(W::GW(j * MU + be), x1[be], fma(W::DW(j * MU + be), x3[be], s1));
-          s2 = fma(W::GW(j * MU + be), x2[be], s2);
+          const double gw = W::GW(j * MU + be);
+          s1 = fma(gw, x1[be], fma(W::DW(j * MU + be), x3[be], s1));
+          s2 = fma(gw, x2[be], s2);
         }
         sm[L::A1 + base + j * MU] = s1;
         sm[L::A2 + base + j * MU] = s2;
@@ -305,7 +311,7 @@ __global__ void __launch_bounds__(NT, MINB) jv3d_fast_kernel(DevSys s, const dou
     //      threads: lift[f][j1][j0] = sum_bb G(bb, j1) wa[f][j0][bb]
     for (int it = tid; it < 6 * Q2; it += NT) {
       const int f = it / Q2, j1 = (it % Q2) / Q, j0 = it % Q;
-      const double* w = sm + L::wa + (f * Q + j0) * MU;
+      const double* w = sm + L::wa + (f * Q + j0) * L::MP;
       double l = 0.0;
 #pragma unroll
       for (int bb = 0; bb < MU; ++bb) l = fma(sm[L::sg + bb * Q + j1], w[bb], l);
@@ -317,10 +323,19 @@ __global__ void __launch_bounds__(NT, MINB) jv3d_fast_kernel(DevSys s, const dou
       const int k = p / Q, j = p % Q;
       const int base = k * M2 + j * MU;
       double x1[MU], x2[MU];
+      if constexpr (MU % 2 == 0) {  // rows are 16-byte aligned: 16-byte loads halve the cost of the stride-MU bank conflict
 #pragma unroll
-      for (int al = 0; al < MU; ++al) {
-        x1[al] = sm[L::A1 + base + al];
-        x2[al] = sm[L::A2 + base + al];
+        for (int al = 0; al < MU; al += 2) {
+          const double2 a = *reinterpret_cast<const double2*>(sm + L::A1 + base + al);
+          const double2 b = *reinterpret_cast<const double2*>(sm + L::A2 + base + al);
+          x1[al] = a.x, x1[al + 1] = a.y, x2[al] = b.x, x2[al + 1] = b.y;
+        }
+      } else {
+#pragma unroll
+        for (int al = 0; al < MU; ++al) {
+          x1[al] = sm[L::A1 + base + al];
+          x2[al] = sm[L::A2 + base + al];
+        }
       }
       // lifted layers of the faces whose layer contains the whole pencil (y, z faces), tangential (i, k) / (i, j)
       const double* ly = (j == 0) ? sm + L::lift + 2 * Q2 + k * Q : (j == Q - 1 ? sm + L::lift + 3 * Q2 + k * Q : nullptr);
