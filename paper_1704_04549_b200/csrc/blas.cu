@@ -11,6 +11,7 @@
 // of (w, v_{j-1}, v_j) and one write of w, so the k+1 MGS steps of iteration k cost k+2 passes.
 #include <map>
 #include <mutex>
+#include <type_traits>
 #include <algorithm>
 #include <cstdint>
 
@@ -300,6 +301,23 @@ constexpr int kCoopThreads = 1024;
 // L2 eviction-priority hints (createpolicy + .L2::cache_hint): in mgs_global_kernel the working vector w
 // and the current basis vector are kept L2-resident across passes (evict_last), so a pass streams
 // only v_j from HBM instead of w (read + write), v_{j-1} and v_j.
+// thread-private cp.async ring of the streaming MGS kernel (dst: shared-space byte address)
+__device__ __forceinline__ void cp_async16z(uint32_t dst, const double* gmem, unsigned src_bytes) {  // rest zero-filled
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(gmem), "r"(src_bytes) : "memory");
+}
+__device__ __forceinline__ double2 lds128(uint32_t addr) {
+  double2 v;
+  asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(addr) : "memory");
+  return v;
+}
+__device__ __forceinline__ void sts128(uint32_t addr, double2 v) {
+  asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(addr), "d"(v.x), "d"(v.y) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
 __device__ __forceinline__ uint64_t policy_evict_last() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
@@ -513,43 +531,77 @@ __global__ void __launch_bounds__(kCoopThreads) mgs_regv_kernel(double* __restri
   fused_givens(G, k, gstatus);
 }
 
-// ---- TMA bulk-copy MGS for large chunks (cfg4, cfg2 p >= 20) --------------------------------
-// Same passes, element assignment (thread t owns the pairs 2t + 2048 r of its CTA's slice) and
-// accumulation order (r ascending, even/odd elements in s0/s1) as every other MGS kernel, hence
-// bit-identical; the data movement differs: the basis rows a pass needs (v_j, and v_{j-1} for the
-// update) stream through an NS-stage shared-memory ring filled by the TMA engine (one thread issues
-// cp.async.bulk per row; completion on an mbarrier), so no register or issue slot is spent on loads
-// and a row's copies for the next pass are in flight during the grid reduction. w lives on chip for
-// the whole launch: rows r < RW in registers, the rest in shared memory behind the ring. v_j is
-// kept in L2 (evict_last) for the next pass's update read, v_{j-1} is then dropped (evict_first).
-template <int NT, int RW, int NS, int PPT>
-__global__ void __launch_bounds__(NT, 1) mgs_bulk_kernel(double* __restrict__ V, int64_t ldv, int k, int64_t n,
-                                                         int64_t chunk, double* __restrict__ hc,
-                                                         double* __restrict__ partial, unsigned* bar, const int* skip,
-                                                         GmresDev G, GmresStatus* gstatus) {
+// ---- streaming MGS for large chunks (cfg4, cfg2 p >= 20) -------------------------------------
+// Same passes, element assignment (thread t of 512 owns the pairs t + 512 u, u < PPT, of every
+// 2048-double row of its CTA's slice) and accumulation order (rows ascending, even/odd elements in
+// s0/s1) as before, hence bit-identical; what differs is how a basis row reaches its thread:
+//  * v_j comes from HBM once, through a thread-private cp.async ring: every thread copies the 16-byte
+//    pieces it will consume itself (a warp's pieces are 512 contiguous bytes), D rows ahead, and waits
+//    on its own cp.async groups only -- no mbarrier, no producer, no block-level handshake per row
+//    (tools/tma_ring_bench.cu: a cp.async.bulk ring with full/empty mbarriers costs 700-900 cycles per
+//    row whatever the row size or depth, 11.7 us per cfg4 pass; tools/cpasync_ring_bench.cu: this ring
+//    streams the same pass in 6.0 us, HBM speed);
+//  * v_{j-1}, needed for the update w -= h_{j-1} v_{j-1} one pass later, does not come back through L2:
+//    after using its pairs of v_j for the dot, the thread parks them in tensor memory (rows r < TMR:
+//    8 columns per row, the four warps of a TMEM lane quarter take 128 columns each; tcgen05.st, read
+//    back with tcgen05.ld one pass later). 256 KB of TMEM hold 16 rows per SM; rows >= TMR (two at
+//    cfg4) are parked in shared memory instead. Every basis vector is read exactly once per pass.
+// w lives on chip for the whole launch: rows r < RW in registers, the rest in shared memory.
+template <int NT, int RW, int D, int PPT, int TMR>
+__global__ void __launch_bounds__(NT, 1) mgs_stream_kernel(double* __restrict__ V, int64_t ldv, int k, int64_t n,
+                                                           int64_t chunk, double* __restrict__ hc,
+                                                           double* __restrict__ partial, unsigned* bar, const int* skip,
+                                                           GmresDev G, GmresStatus* gstatus) {
   if (skip && *skip) return;
+  static_assert(PPT == 2 && RW <= TMR && TMR * 8 * (NT / 128) <= 512 && (D & (D - 1)) == 0, "TMEM rows / ring depth");
   __shared__ unsigned tgt;
   mgs_epoch_begin(bar, &tgt);
-  constexpr int ROW = 2 * NT * PPT;  // doubles per row: PPT pairs per thread (pair t + NT u)
+  constexpr int ROW = 2 * NT * PPT;      // doubles per row
+  constexpr unsigned ROWB = 8u * ROW;    // bytes per row
+  constexpr unsigned P1 = 16u * NT;      // byte offset of a thread's second pair in a row
   extern __shared__ __align__(128) double bsm[];
-  double* ring = bsm;             // stage s: v_j row at ring + 2 ROW s, v_{j-1} row at + ROW
-  double* wsm = bsm + 2 * ROW * NS;  // w rows RW.. (row r at wsm + (r - RW) ROW)
-  __shared__ __align__(8) uint64_t full[NS], empty[NS];
   __shared__ double shA[32], shB[33];
+  __shared__ uint32_t tm_slot;
   const unsigned nb = gridDim.x;
   const int64_t lo = int64_t(blockIdx.x) * chunk;
   const int64_t hi = lo + chunk < n ? lo + chunk : n;
   const int len = int(hi > lo ? hi - lo : 0);
-  const int nrows = (len + ROW - 1) / ROW;
+  const int nrows = (len + ROW - 1) / ROW, nfull = len / ROW;  // rows, rows with every pair inside len
+  // shared memory: ring of D rows (v_j of task q in slot q % D) | parked rows r >= TMR of v_{j-1} | w rows r >= RW
+  double* wsm = bsm + (D + (nrows > TMR ? nrows - TMR : 0)) * ROW;
   double* wg = V + int64_t(k + 1) * ldv + lo;
-  const int t = threadIdx.x, lane = t & 31;
-  if (t == 0) {
-    for (int s = 0; s < NS; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], NT / 32);
-    }
-    mbar_fence_init();
-  }
+  const int t = threadIdx.x;
+  if (t < 32) tmem_alloc512(&tm_slot);
+  tmem_fence_before_sync();
+  // every shared-memory access below is to the thread's own pairs, through 32-bit shared-space addresses
+  const uint32_t ring_s = smem_u32(bsm) + 16u * unsigned(t);
+  const uint32_t park_s = ring_s + D * ROWB - TMR * ROWB;  // row r >= TMR parked at park_s + ROWB r
+  const uint32_t w_s = smem_u32(wsm) + 16u * unsigned(t) - RW * ROWB;  // w row r >= RW at w_s + ROWB r
+  // The copies of v-task q = (pass j <= k, row r), j-major, by their consumer, D - 1 tasks ahead; one cp.async group
+  // per task. Pieces past len are zero-filled (src-size 8 / 0) and w is zero there too, so the row arithmetic needs
+  // no bounds: the padding adds +0.0 to the sums and stays zero under the update.
+  auto piece_bytes = [&](int r, int u) {  // bytes of pair t + NT u of row r inside len
+    const int left = len - (r * ROW + 2 * (t + NT * u));
+    return unsigned(left >= 2 ? 16 : left > 0 ? 8 : 0);
+  };
+  const unsigned pb0 = piece_bytes(nfull, 0), pb1 = piece_bytes(nfull, 1);
+  const int nvtask = (k + 1) * nrows;
+  const int64_t wrapinc = ldv - int64_t(nrows - 1) * ROW;
+  const double* isrc = V + lo + 2 * t;  // this thread's first pair of the next task's row
+  int iq = 0, ir = 0;
+  unsigned islot = 0;
+  auto issue = [&]() {
+    const bool live = iq < nvtask, fullrow = ir < nfull, wrap = ir + 1 == nrows;
+    const unsigned z0 = live ? (fullrow ? 16u : pb0) : 0u, z1 = live ? (fullrow ? 16u : pb1) : 0u;
+    cp_async16z(ring_s + islot, isrc, z0);
+    cp_async16z(ring_s + islot + P1, isrc + 2 * NT, z1);
+    cp_async_commit();
+    islot = (islot + ROWB) & (D * ROWB - 1);
+    ++iq;
+    isrc += live ? (wrap ? wrapinc : int64_t(ROW)) : int64_t(0);
+    ir = wrap ? 0 : ir + 1;
+  };
+  for (int q = 0; q < D - 1; ++q) issue();
   double2 wr[RW][PPT];
 #pragma unroll
   for (int r = 0; r < RW; ++r)
@@ -558,89 +610,93 @@ __global__ void __launch_bounds__(NT, 1) mgs_bulk_kernel(double* __restrict__ V,
       const int i = 2 * (t + NT * u) + ROW * r;
       wr[r][u] = i + 1 < len ? *reinterpret_cast<const double2*>(wg + i) : make_double2(i < len ? wg[i] : 0.0, 0.0);
     }
-  for (int i = ROW * RW + 2 * t; i < len; i += 2 * NT) {
-    if (i + 1 < len)
-      *reinterpret_cast<double2*>(wsm + i - ROW * RW) = *reinterpret_cast<const double2*>(wg + i);
-    else
-      wsm[i - ROW * RW] = wg[i];
-  }
+  for (int i = ROW * RW + 2 * t; i < nrows * ROW; i += 2 * NT)  // a thread reads back only what it wrote
+    *reinterpret_cast<double2*>(wsm + i - ROW * RW) =
+        i + 1 < len ? *reinterpret_cast<const double2*>(wg + i) : make_double2(i < len ? wg[i] : 0.0, 0.0);
   __syncthreads();
-  const uint64_t keep = policy_evict_last(), drop = policy_evict_first();
-  const int ntask = (k + 2) * nrows;  // task = (pass j, row r), j-major; stage task % NS
-  auto issue = [&](int task) {        // thread 0: the copies of one task
-    const int j = task / nrows, r = task - j * nrows, s = task % NS;
-    const int cnt = min(ROW, len - r * ROW);
-    const unsigned bytes = unsigned((cnt + 1) & ~1) * 8u;  // V rows are padded: reading the pad is safe
-    mbar_expect_tx(&full[s], (j <= k ? bytes : 0u) + (j > 0 ? bytes : 0u));
-    if (j <= k) bulk_g2s(ring + 2 * ROW * s, V + int64_t(j) * ldv + lo + r * ROW, bytes, &full[s], keep);
-    if (j > 0) bulk_g2s(ring + 2 * ROW * s + ROW, V + int64_t(j - 1) * ldv + lo + r * ROW, bytes, &full[s], drop);
-  };
-  if (t == 0)
-    for (int q = 0; q < NS - 1 && q < ntask; ++q) issue(q);
-  double h = 0.0;
-  int task = 0;
-  for (int j = 0; j <= k + 1; ++j) {
-    double s0 = 0.0, s1 = 0.0;
-    auto row = [&](double2 (&wi)[PPT], int r) {
-      const int s = task % NS;
-      if (t == 0 && task + NS - 1 < ntask) {  // refill the stage freed by task - 1
-        const int nt = task + NS - 1;
-        if (nt >= NS) mbar_wait(&empty[nt % NS], unsigned(nt / NS - 1) & 1u);
-        issue(nt);
+  tmem_fence_after_sync();
+  const uint32_t tm = tm_slot + ((32u * unsigned((t >> 5) & 3)) << 16) + unsigned(t >> 7) * (512u / (NT / 128));
+  double h = 0.0, s0 = 0.0, s1 = 0.0;
+  unsigned cslot = 0;
+  // KIND 0: first pass (dot with v_0); 1: update with v_{j-1}, dot with v_j; 2: last update and <w, w>
+  auto row = [&](auto kind, double2 (&wi)[PPT], int r) {
+    constexpr int KIND = decltype(kind)::value;
+    const bool tmrow = r < TMR;  // uniform over the CTA; folds for the register rows
+    double2 pv[PPT];
+    if (KIND > 0 && tmrow) {
+      tmem_ld4(tm + 8u * unsigned(r), pv[0]);
+      tmem_ld4(tm + 8u * unsigned(r) + 4u, pv[1]);
+    }
+    if (KIND < 2) {
+      issue();  // v-task + D - 1, into the slot this thread finished reading one row ago
+      cp_async_wait<D - 1>();
+    }
+    if (KIND > 0) {
+      if (tmrow) {
+        tmem_wait_ld(pv[0], pv[1]);
+      } else {
+        pv[0] = lds128(park_s + ROWB * unsigned(r));
+        pv[1] = lds128(park_s + ROWB * unsigned(r) + P1);
       }
-      mbar_wait(&full[s], unsigned(task / NS) & 1u);
-      const double* vjs = ring + 2 * ROW * s;
-      const double* vps = vjs + ROW;
 #pragma unroll
       for (int u = 0; u < PPT; ++u) {
-        const int pr = 2 * (t + NT * u), i = pr + ROW * r;
-        if (i + 1 < len) {
-          if (j > 0) {
-            const double2 pv = *reinterpret_cast<const double2*>(vps + pr);
-            wi[u].x = wi[u].x - h * pv.x;
-            wi[u].y = wi[u].y - h * pv.y;
-          }
-          const double2 a = j <= k ? *reinterpret_cast<const double2*>(vjs + pr) : wi[u];
-          s0 += a.x * wi[u].x;
-          s1 += a.y * wi[u].y;
-        } else if (i < len) {
-          if (j > 0) wi[u].x = wi[u].x - h * vps[pr];
-          const double a = j <= k ? vjs[pr] : wi[u].x;
-          s0 += a * wi[u].x;
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-      ++task;
-    };
-#pragma unroll
-    for (int r = 0; r < RW; ++r)
-      if (r < nrows) row(wr[r], r);
-    for (int r = RW; r < nrows; ++r) {
-      double2 wi[PPT];
-#pragma unroll
-      for (int u = 0; u < PPT; ++u) {
-        const int pr = 2 * (t + NT * u), i = pr + ROW * r;
-        const double* wp = wsm + ROW * (r - RW) + pr;
-        wi[u] = i + 1 < len ? *reinterpret_cast<const double2*>(wp) : make_double2(i < len ? wp[0] : 0.0, 0.0);
-      }
-      row(wi, r);
-      if (j > 0) {
-#pragma unroll
-        for (int u = 0; u < PPT; ++u) {
-          const int pr = 2 * (t + NT * u), i = pr + ROW * r;
-          double* wp = wsm + ROW * (r - RW) + pr;
-          if (i + 1 < len)
-            *reinterpret_cast<double2*>(wp) = wi[u];
-          else if (i < len)
-            wp[0] = wi[u].x;
-        }
+        wi[u].x = fma(-h, pv[u].x, wi[u].x);
+        wi[u].y = fma(-h, pv[u].y, wi[u].y);
       }
     }
+    if (KIND < 2) {
+      double2 vj[PPT];
+      vj[0] = lds128(ring_s + cslot);
+      vj[1] = lds128(ring_s + cslot + P1);
+      cslot = (cslot + ROWB) & (D * ROWB - 1);
+      if (tmrow) {
+        tmem_st4(tm + 8u * unsigned(r), vj[0]);
+        tmem_st4(tm + 8u * unsigned(r) + 4u, vj[1]);
+      } else {
+        sts128(park_s + ROWB * unsigned(r), vj[0]);
+        sts128(park_s + ROWB * unsigned(r) + P1, vj[1]);
+      }
+#pragma unroll
+      for (int u = 0; u < PPT; ++u) {
+        s0 = fma(vj[u].x, wi[u].x, s0);
+        s1 = fma(vj[u].y, wi[u].y, s1);
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < PPT; ++u) {
+        s0 = fma(wi[u].x, wi[u].x, s0);
+        s1 = fma(wi[u].y, wi[u].y, s1);
+      }
+    }
+  };
+  auto pass = [&](auto kind, int j) {
+    constexpr int KIND = decltype(kind)::value;
+    s0 = s1 = 0.0;
+#pragma unroll
+    for (int r = 0; r < RW; ++r)
+      if (r < nrows) row(kind, wr[r], r);
+    for (int r = RW; r < nrows; ++r) {
+      double2 wi[PPT];
+      wi[0] = lds128(w_s + ROWB * unsigned(r));
+      wi[1] = lds128(w_s + ROWB * unsigned(r) + P1);
+      row(kind, wi, r);
+      if (KIND > 0) {
+        sts128(w_s + ROWB * unsigned(r), wi[0]);
+        sts128(w_s + ROWB * unsigned(r) + P1, wi[1]);
+      }
+    }
+    if (KIND < 2) tmem_wait_st();
     const double tot = mgs_grid_sum(s0 + s1, partial + size_t(j) * nb, bar, &tgt, shA, shB);
-    h = j <= k ? tot : sqrt(tot);
+    h = KIND < 2 ? tot : sqrt(tot);
     if (blockIdx.x == 0 && t == 0) hc[j] = h;
-  }
+  };
+  pass(std::integral_constant<int, 0>{}, 0);
+  for (int j = 1; j <= k; ++j) pass(std::integral_constant<int, 1>{}, j);
+  pass(std::integral_constant<int, 2>{}, k + 1);
+  cp_async_wait<0>();
+  tmem_fence_before_sync();
+  __syncthreads();
+  if (t < 32) tmem_dealloc512(tm_slot);
 #pragma unroll
   for (int r = 0; r < RW; ++r)
 #pragma unroll
@@ -651,7 +707,10 @@ __global__ void __launch_bounds__(NT, 1) mgs_bulk_kernel(double* __restrict__ V,
       else if (i < len)
         wg[i] = h > 0.0 ? wr[r][u].x / h : wr[r][u].x;
     }
-  for (int i = ROW * RW + t; i < len; i += NT) wg[i] = h > 0.0 ? wsm[i - ROW * RW] / h : wsm[i - ROW * RW];
+  for (int i = ROW * RW + 2 * t; i < len; i += 2 * NT) {  // the pairs this thread owns
+    wg[i] = h > 0.0 ? wsm[i - ROW * RW] / h : wsm[i - ROW * RW];
+    if (i + 1 < len) wg[i + 1] = h > 0.0 ? wsm[i + 1 - ROW * RW] / h : wsm[i + 1 - ROW * RW];
+  }
   mgs_epoch_end(bar, &tgt);
   fused_givens(G, k, gstatus);
 }
@@ -660,12 +719,13 @@ struct CoopPlan {
   int grid;
   int64_t chunk;
   size_t smem;
-  int mode;  // 1..4: mgs_regv_kernel<mode>; 5: mgs_bulk_kernel; 0: mgs_global_kernel
+  int mode;  // 1..4: mgs_regv_kernel<mode>; 5: mgs_stream_kernel; 0: mgs_global_kernel
   int threads = kCoopThreads;
 };
 
-// One 1024-thread CTA per SM (cheap barrier); the most shared-memory residency that fits.
-constexpr int kBulkThreads = 512, kBulkRW = 10, kBulkStages = 3, kBulkPPT = 2;  // tools/mgs_bench at cfg4 size, us per pass: 1024/8/2/1 19.3, 512/8/2/2 16.7, 512/10/3/2 16.3, 512/10/2/2 17.2, 256/8/2/4 19.3, 256/14/5/4 25.1 (spills)
+// One CTA per SM (cheap barrier); the most on-chip residency that fits. Shape of the streaming kernel: 512 threads
+// x 2 pairs per 2048-double row, 10 register rows of w, cp.async ring depth 4, 16 rows of v_{j-1} in tensor memory.
+constexpr int kBulkThreads = 512, kBulkRW = 10, kBulkDepth = 4, kBulkPPT = 2, kBulkTMR = 16;
 
 CoopPlan mgs_coop_plan(int64_t n) {
   int dev = 0, sms = 0;
@@ -677,11 +737,13 @@ CoopPlan mgs_coop_plan(int64_t n) {
     const int R = int((chunk + 2 * kCoopThreads - 1) / (2 * kCoopThreads));
     return {sms, chunk, 0, R};
   }
-  {  // w on chip (registers + shared memory), basis rows through the TMA ring
+  {  // w on chip (registers + shared memory), v_j through the cp.async ring, v_{j-1} in tensor memory
     const int64_t rows = (chunk + 2 * kBulkThreads * kBulkPPT - 1) / (2 * kBulkThreads * kBulkPPT);
     const size_t row_b = size_t(2 * kBulkThreads * kBulkPPT) * sizeof(double);
-    const size_t sm = row_b * (2 * kBulkStages + size_t(rows > kBulkRW ? rows - kBulkRW : 0));
-    const void* fn = reinterpret_cast<const void*>(mgs_bulk_kernel<kBulkThreads, kBulkRW, kBulkStages, kBulkPPT>);
+    const size_t sm = row_b * (kBulkDepth + size_t(rows > kBulkTMR ? rows - kBulkTMR : 0) +
+                               size_t(rows > kBulkRW ? rows - kBulkRW : 0));
+    const void* fn =
+        reinterpret_cast<const void*>(mgs_stream_kernel<kBulkThreads, kBulkRW, kBulkDepth, kBulkPPT, kBulkTMR>);
     int fit = 0;
     if (sm <= 227 * 1024) {
       ensure_smem(fn, sm);
@@ -763,7 +825,7 @@ void launch_mgs_iteration(double* V, int64_t ldv, int k, int64_t n, double* hc, 
              : plan.mode == 2 ? reinterpret_cast<void*>(mgs_regv_kernel<2>)
              : plan.mode == 3 ? reinterpret_cast<void*>(mgs_regv_kernel<3>)
              : plan.mode == 4 ? reinterpret_cast<void*>(mgs_regv_kernel<4>)
-             : plan.mode == 5 ? reinterpret_cast<void*>(mgs_bulk_kernel<kBulkThreads, kBulkRW, kBulkStages, kBulkPPT>)
+             : plan.mode == 5 ? reinterpret_cast<void*>(mgs_stream_kernel<kBulkThreads, kBulkRW, kBulkDepth, kBulkPPT, kBulkTMR>)
                               : reinterpret_cast<void*>(mgs_global_kernel);
   TPDG_CUDA_CHECK(cudaLaunchCooperativeKernel(fn, dim3(plan.grid), dim3(plan.threads), args, plan.smem, st));
   ++g_launches;

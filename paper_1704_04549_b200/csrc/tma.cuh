@@ -1,5 +1,5 @@
 // tma.cuh — mbarrier + cp.async.bulk (TMA 1D global -> shared) helpers shared by the MGS ring (blas.cu)
-// and the 3D preconditioner's G-block ring (kron.cu).
+// and the 3D preconditioner's G-block ring (kron.cu); tensor-memory (TMEM) scratch helpers for the MGS kernel.
 #pragma once
 #include <cstdint>
 
@@ -39,5 +39,38 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
           "r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(b)), "l"(pol)
       : "memory");
 }
+
+// ---- tensor memory as a per-thread scratchpad (tcgen05.ld / st, shape 32x32b: lane l of warp w reads
+// and writes TMEM lane 32 (w % 4) + l, consecutive 32-bit columns). One warp allocates all 512 columns.
+__device__ __forceinline__ void tmem_alloc512(uint32_t* slot) {  // one converged warp; *slot (shared) = base address
+  asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(slot)) : "memory");
+  asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tmem_dealloc512(uint32_t base) {  // one converged warp
+  asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(base) : "memory");
+}
+__device__ __forceinline__ void tmem_fence_before_sync() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tmem_fence_after_sync() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+// one double2 per access (4 columns)
+__device__ __forceinline__ void tmem_ld4(uint32_t addr, double2& v) {
+  asm volatile(
+      "{\n\t.reg .b32 a, b, c, d;\n\ttcgen05.ld.sync.aligned.32x32b.x4.b32 {a, b, c, d}, [%2];\n\t"
+      "mov.b64 %0, {a, b};\n\tmov.b64 %1, {c, d};\n}"
+      : "=d"(v.x), "=d"(v.y)
+      : "r"(addr)
+      : "memory");
+}
+// the wait carries the loaded values so that no use is scheduled before it
+__device__ __forceinline__ void tmem_wait_ld(double2& a, double2& b) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" : "+d"(a.x), "+d"(a.y), "+d"(b.x), "+d"(b.y) : : "memory");
+}
+__device__ __forceinline__ void tmem_st4(uint32_t addr, double2 v) {
+  asm volatile(
+      "{\n\t.reg .b32 a, b, c, d;\n\tmov.b64 {a, b}, %1;\n\tmov.b64 {c, d}, %2;\n\t"
+      "tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {a, b, c, d};\n}" ::"r"(addr),
+      "d"(v.x), "d"(v.y)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 } // namespace tpdg_gpu
