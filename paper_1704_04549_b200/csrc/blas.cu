@@ -302,6 +302,9 @@ constexpr int kCoopThreads = 1024;
 // and the current basis vector are kept L2-resident across passes (evict_last), so a pass streams
 // only v_j from HBM instead of w (read + write), v_{j-1} and v_j.
 // thread-private cp.async ring of the streaming MGS kernel (dst: shared-space byte address)
+__device__ __forceinline__ void cp_async16(uint32_t dst, const double* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(gmem) : "memory");
+}
 __device__ __forceinline__ void cp_async16z(uint32_t dst, const double* gmem, unsigned src_bytes) {  // rest zero-filled
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(gmem), "r"(src_bytes) : "memory");
 }
@@ -584,14 +587,14 @@ __global__ void __launch_bounds__(NT, 1) mgs_stream_kernel(double* __restrict__ 
     const int left = len - (r * ROW + 2 * (t + NT * u));
     return unsigned(left >= 2 ? 16 : left > 0 ? 8 : 0);
   };
-  const unsigned pb0 = piece_bytes(nfull, 0), pb1 = piece_bytes(nfull, 1);
   const int nvtask = (k + 1) * nrows;
   const int64_t wrapinc = ldv - int64_t(nrows - 1) * ROW;
   const double* isrc = V + lo + 2 * t;  // this thread's first pair of the next task's row
   int iq = 0, ir = 0;
   unsigned islot = 0;
-  auto issue = [&]() {
+  auto issue_any = [&]() {  // any task: partial last row, pass wrap, past the last v-task (zero-fill, no read)
     const bool live = iq < nvtask, fullrow = ir < nfull, wrap = ir + 1 == nrows;
+    const unsigned pb0 = piece_bytes(nfull, 0), pb1 = piece_bytes(nfull, 1);
     const unsigned z0 = live ? (fullrow ? 16u : pb0) : 0u, z1 = live ? (fullrow ? 16u : pb1) : 0u;
     cp_async16z(ring_s + islot, isrc, z0);
     cp_async16z(ring_s + islot + P1, isrc + 2 * NT, z1);
@@ -601,7 +604,16 @@ __global__ void __launch_bounds__(NT, 1) mgs_stream_kernel(double* __restrict__ 
     isrc += live ? (wrap ? wrapinc : int64_t(ROW)) : int64_t(0);
     ir = wrap ? 0 : ir + 1;
   };
-  for (int q = 0; q < D - 1; ++q) issue();
+  auto issue_mid = [&]() {  // a full row of a pass j <= k that is not the pass's last row
+    cp_async16(ring_s + islot, isrc);
+    cp_async16(ring_s + islot + P1, isrc + 2 * NT);
+    cp_async_commit();
+    islot = (islot + ROWB) & (D * ROWB - 1);
+    ++iq;
+    isrc += ROW;
+    ++ir;
+  };
+  for (int q = 0; q < D - 1; ++q) issue_any();
   double2 wr[RW][PPT];
 #pragma unroll
   for (int r = 0; r < RW; ++r)
@@ -619,16 +631,18 @@ __global__ void __launch_bounds__(NT, 1) mgs_stream_kernel(double* __restrict__ 
   double h = 0.0, s0 = 0.0, s1 = 0.0;
   unsigned cslot = 0;
   // KIND 0: first pass (dot with v_0); 1: update with v_{j-1}, dot with v_j; 2: last update and <w, w>
-  auto row = [&](auto kind, double2 (&wi)[PPT], int r) {
+  auto row = [&](auto kind, auto mid, double2 (&wi)[PPT], int r) {
     constexpr int KIND = decltype(kind)::value;
+    constexpr bool MID = decltype(mid)::value;  // the task issued here is a full, non-last row of this pass
     const bool tmrow = r < TMR;  // uniform over the CTA; folds for the register rows
     double2 pv[PPT];
     if (KIND > 0 && tmrow) {
       tmem_ld4(tm + 8u * unsigned(r), pv[0]);
       tmem_ld4(tm + 8u * unsigned(r) + 4u, pv[1]);
     }
-    if (KIND < 2) {
-      issue();  // v-task + D - 1, into the slot this thread finished reading one row ago
+    if (KIND < 2) {  // v-task + D - 1, into the slot this thread finished reading one row ago
+      if (MID) issue_mid();
+      else issue_any();
       cp_async_wait<D - 1>();
     }
     if (KIND > 0) {
@@ -669,17 +683,27 @@ __global__ void __launch_bounds__(NT, 1) mgs_stream_kernel(double* __restrict__ 
       }
     }
   };
+  // Row r issues the task of row r + D - 1: a full row inside the same pass as long as r + D - 1 < nrows - 1.
+  const bool regs_mid = nrows - 1 > RW - 1 + D - 1;
   auto pass = [&](auto kind, int j) {
     constexpr int KIND = decltype(kind)::value;
+    constexpr std::true_type yes{};
+    constexpr std::false_type no{};
     s0 = s1 = 0.0;
+    if (regs_mid) {
 #pragma unroll
-    for (int r = 0; r < RW; ++r)
-      if (r < nrows) row(kind, wr[r], r);
+      for (int r = 0; r < RW; ++r) row(kind, yes, wr[r], r);
+    } else {
+#pragma unroll
+      for (int r = 0; r < RW; ++r)
+        if (r < nrows) row(kind, no, wr[r], r);
+    }
     for (int r = RW; r < nrows; ++r) {
       double2 wi[PPT];
       wi[0] = lds128(w_s + ROWB * unsigned(r));
       wi[1] = lds128(w_s + ROWB * unsigned(r) + P1);
-      row(kind, wi, r);
+      if (r + D - 1 < nrows - 1) row(kind, yes, wi, r);
+      else row(kind, no, wi, r);
       if (KIND > 0) {
         sts128(w_s + ROWB * unsigned(r), wi[0]);
         sts128(w_s + ROWB * unsigned(r) + P1, wi[1]);
