@@ -457,87 +457,11 @@ __global__ void __launch_bounds__(kCoopThreads) mgs_global_kernel(double* __rest
   fused_givens(G, k, gstatus);
 }
 
-// Slices of <= 8192 doubles per CTA (cfg2 p <= 15): w, v_{j-1} and v_j in registers. The thread's
-// pairs of v_j are loaded straight into registers (16-byte loads) right after pass j-1's arithmetic,
-// so they travel during that pass's grid reduction.
-template <int R>
-__global__ void __launch_bounds__(kCoopThreads) mgs_regv_kernel(double* __restrict__ V, int64_t ldv, int k, int64_t n,
-                                                                 int64_t chunk, double* __restrict__ hc,
-                                                                 double* __restrict__ partial, unsigned* bar,
-                                                                 const int* skip, GmresDev G, GmresStatus* gstatus) {
-  if (skip && *skip) return;
-  __shared__ unsigned tgt;
-  mgs_epoch_begin(bar, &tgt);
-  __shared__ double shA[32], shB[33];
-  const unsigned nb = gridDim.x;
-  const int64_t lo = int64_t(blockIdx.x) * chunk;
-  const int64_t hi = lo + chunk < n ? lo + chunk : n;
-  const int len = int(hi > lo ? hi - lo : 0);
-  double* wg = V + int64_t(k + 1) * ldv + lo;
-  const int t = threadIdx.x;
-  auto fetch = [&](const double* src, double2 (&dst)[R]) {
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int i = 2 * t + 2 * kCoopThreads * r;
-      dst[r] = i + 1 < len ? __ldcg(reinterpret_cast<const double2*>(src + i))
-                           : make_double2(i < len ? __ldcg(src + i) : 0.0, 0.0);
-    }
-  };
-  double2 w[R], vp[R], vq[R];
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int i = 2 * t + 2 * kCoopThreads * r;
-    w[r] = i + 1 < len ? *reinterpret_cast<const double2*>(wg + i) : make_double2(i < len ? wg[i] : 0.0, 0.0);
-    vp[r] = make_double2(0.0, 0.0);
-  }
-  fetch(V + lo, vq);  // v_0
-  double h = 0.0;
-  for (int j = 0; j <= k + 1; ++j) {
-    double s0 = 0.0, s1 = 0.0;
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int i = 2 * t + 2 * kCoopThreads * r;
-      if (i < len) {
-        double2 wi = w[r];
-        if (j > 0) {
-          wi.x = wi.x - h * vp[r].x;
-          if (i + 1 < len) wi.y = wi.y - h * vp[r].y;
-          w[r] = wi;
-        }
-        if (i + 1 < len) {
-          const double2 a = j <= k ? vq[r] : wi;
-          s0 += a.x * wi.x;
-          s1 += a.y * wi.y;
-          vp[r] = a;
-        } else {
-          const double a = j <= k ? vq[r].x : wi.x;
-          s0 += a * wi.x;
-          vp[r] = make_double2(a, 0.0);
-        }
-      }
-    }
-    if (j + 1 <= k) fetch(V + int64_t(j + 1) * ldv + lo, vq);  // in flight during the grid reduction
-    const double tot = mgs_grid_sum(s0 + s1, partial + size_t(j) * nb, bar, &tgt, shA, shB);
-    h = j <= k ? tot : sqrt(tot);
-    if (blockIdx.x == 0 && t == 0) hc[j] = h;
-  }
-#pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int i = 2 * t + 2 * kCoopThreads * r;
-    if (i + 1 < len) {
-      *reinterpret_cast<double2*>(wg + i) = h > 0.0 ? make_double2(w[r].x / h, w[r].y / h) : w[r];
-    } else if (i < len) {
-      wg[i] = h > 0.0 ? w[r].x / h : w[r].x;
-    }
-  }
-  mgs_epoch_end(bar, &tgt);
-  fused_givens(G, k, gstatus);
-}
-
-// ---- streaming MGS for large chunks (cfg4, cfg2 p >= 20) -------------------------------------
-// Same passes, element assignment (thread t of 512 owns the pairs t + 512 u, u < PPT, of every
-// 2048-double row of its CTA's slice) and accumulation order (rows ascending, even/odd elements in
-// s0/s1) as before, hence bit-identical; what differs is how a basis row reaches its thread:
+// ---- streaming MGS: every slice that fits on chip (all BASELINE configs) ----------------------
+// Element assignment: thread t of 512 owns the pairs t + 512 u, u < PPT, of every 2048-double row of
+// its CTA's slice; accumulation order: rows ascending, even/odd elements in s0/s1, then warp
+// butterflies, the warp sums and the CTA partials in index order (tools/mgs_bench.cu checks the first
+// dot against a host emulation of this order bit for bit). How a basis row reaches its thread:
 //  * v_j comes from HBM once, through a thread-private cp.async ring: every thread copies the 16-byte
 //    pieces it will consume itself (a warp's pieces are 512 contiguous bytes), D rows ahead, and waits
 //    on its own cp.async groups only -- no mbarrier, no producer, no block-level handshake per row
@@ -743,13 +667,34 @@ struct CoopPlan {
   int grid;
   int64_t chunk;
   size_t smem;
-  int mode;  // 1..4: mgs_regv_kernel<mode>; 5: mgs_stream_kernel; 0: mgs_global_kernel
+  int mode;  // 1..3: mgs_stream_kernel shapes (mgs_coop_plan); 0: mgs_global_kernel
   int threads = kCoopThreads;
 };
 
-// One CTA per SM (cheap barrier); the most on-chip residency that fits. Shape of the streaming kernel: 512 threads
-// x 2 pairs per 2048-double row, 10 register rows of w, cp.async ring depth 4, 16 rows of v_{j-1} in tensor memory.
-constexpr int kBulkThreads = 512, kBulkRW = 10, kBulkDepth = 4, kBulkPPT = 2, kBulkTMR = 16;
+// One CTA per SM (cheap barrier); the most on-chip residency that fits. Shapes of the streaming kernel: 512 threads
+// x 2 pairs per 2048-double row, 16 rows of v_{j-1} in tensor memory, and by slice length (rows per CTA):
+//   <= 4 rows  (cfg2 p <= 15): 4 register rows of w, ring depth 8 (the ring reaches two passes ahead);
+//   <= 10 rows (cfg2 p = 20):  10 register rows, ring depth 8;
+//   <= 18 rows (cfg2 p = 30, cfg4): 10 register rows + w rows in shared memory, ring depth 4.
+// tools/mgs_bench.cu, us per launch at K = 25: n = 1048576: 63.0 (registers only, round-2 kernel) -> 54.8;
+// 1806336: 104.1 (TMA ring) -> 73.4; 3936256: 190.1 -> 125; 5451776: 264.6 -> 160.
+constexpr int kBulkThreads = 512, kBulkPPT = 2, kBulkTMR = 16;
+constexpr int kBulkRow = 2 * kBulkThreads * kBulkPPT;
+
+template <int RW, int D>
+bool stream_plan(int sms, int64_t chunk, int mode, CoopPlan* out) {
+  const int64_t rows = (chunk + kBulkRow - 1) / kBulkRow;
+  const size_t sm = sizeof(double) * kBulkRow *
+                    (D + size_t(rows > kBulkTMR ? rows - kBulkTMR : 0) + size_t(rows > RW ? rows - RW : 0));
+  if (sm > 227 * 1024) return false;
+  const void* fn = reinterpret_cast<const void*>(mgs_stream_kernel<kBulkThreads, RW, D, kBulkPPT, kBulkTMR>);
+  ensure_smem(fn, sm);
+  int fit = 0;
+  TPDG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, fn, kBulkThreads, sm));
+  if (fit < 1) return false;
+  *out = {sms, chunk, sm, mode, kBulkThreads};
+  return true;
+}
 
 CoopPlan mgs_coop_plan(int64_t n) {
   int dev = 0, sms = 0;
@@ -757,25 +702,11 @@ CoopPlan mgs_coop_plan(int64_t n) {
   TPDG_CUDA_CHECK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
   int64_t chunk = (n + sms - 1) / sms;
   chunk = (chunk + 1) & ~int64_t(1);
-  if (chunk <= 4 * 2 * kCoopThreads) {  // w and the basis slices in registers
-    const int R = int((chunk + 2 * kCoopThreads - 1) / (2 * kCoopThreads));
-    return {sms, chunk, 0, R};
-  }
-  {  // w on chip (registers + shared memory), v_j through the cp.async ring, v_{j-1} in tensor memory
-    const int64_t rows = (chunk + 2 * kBulkThreads * kBulkPPT - 1) / (2 * kBulkThreads * kBulkPPT);
-    const size_t row_b = size_t(2 * kBulkThreads * kBulkPPT) * sizeof(double);
-    const size_t sm = row_b * (kBulkDepth + size_t(rows > kBulkTMR ? rows - kBulkTMR : 0) +
-                               size_t(rows > kBulkRW ? rows - kBulkRW : 0));
-    const void* fn =
-        reinterpret_cast<const void*>(mgs_stream_kernel<kBulkThreads, kBulkRW, kBulkDepth, kBulkPPT, kBulkTMR>);
-    int fit = 0;
-    if (sm <= 227 * 1024) {
-      ensure_smem(fn, sm);
-      TPDG_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&fit, fn, kBulkThreads, sm));
-      if (fit >= 1) return {sms, chunk, sm, 5, kBulkThreads};
-    }
-  }
-  return {sms, chunk, 0, 0};  // w in global memory
+  CoopPlan plan{sms, chunk, 0, 0};  // fallback: w in global memory
+  if (chunk <= 4 * kBulkRow && stream_plan<4, 8>(sms, chunk, 1, &plan)) return plan;
+  if (chunk <= 10 * kBulkRow && stream_plan<10, 8>(sms, chunk, 2, &plan)) return plan;
+  if (stream_plan<10, 4>(sms, chunk, 3, &plan)) return plan;
+  return plan;
 }
 
 int stream_grid(int64_t n) {
@@ -845,11 +776,9 @@ void launch_mgs_iteration(double* V, int64_t ldv, int k, int64_t n, double* hc, 
   GmresDev g = G && G->m <= kFusedGivensMaxM ? *G : GmresDev{};
   GmresStatus* gs = G && G->m <= kFusedGivensMaxM ? status : nullptr;
   void* args[] = {&V, &ldv, &k, &n, &chunk, &hc, &partial, &bar, &skip, &g, &gs};
-  void* fn = plan.mode == 1   ? reinterpret_cast<void*>(mgs_regv_kernel<1>)
-             : plan.mode == 2 ? reinterpret_cast<void*>(mgs_regv_kernel<2>)
-             : plan.mode == 3 ? reinterpret_cast<void*>(mgs_regv_kernel<3>)
-             : plan.mode == 4 ? reinterpret_cast<void*>(mgs_regv_kernel<4>)
-             : plan.mode == 5 ? reinterpret_cast<void*>(mgs_stream_kernel<kBulkThreads, kBulkRW, kBulkDepth, kBulkPPT, kBulkTMR>)
+  void* fn = plan.mode == 1   ? reinterpret_cast<void*>(mgs_stream_kernel<kBulkThreads, 4, 8, kBulkPPT, kBulkTMR>)
+             : plan.mode == 2 ? reinterpret_cast<void*>(mgs_stream_kernel<kBulkThreads, 10, 8, kBulkPPT, kBulkTMR>)
+             : plan.mode == 3 ? reinterpret_cast<void*>(mgs_stream_kernel<kBulkThreads, 10, 4, kBulkPPT, kBulkTMR>)
                               : reinterpret_cast<void*>(mgs_global_kernel);
   TPDG_CUDA_CHECK(cudaLaunchCooperativeKernel(fn, dim3(plan.grid), dim3(plan.threads), args, plan.smem, st));
   ++g_launches;
