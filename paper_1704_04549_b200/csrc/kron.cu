@@ -1253,6 +1253,9 @@ __global__ void __launch_bounds__(Kron3dInvLayout<N1, Q>::NTH) kron3d_inv_kernel
       bplan[50 + ns++] = 8 * sz * Q * (sz == 1 ? L::LD1 : L::LD2);
     }
     bplan[33] = ns;
+    // the element's G blocks go HBM -> L2 now, during the rotations: the ring's copies (two blocks ahead of the
+    // sweep) then see L2 latency instead of HBM latency, which paced the sweep
+    bulk_prefetch_l2(gG, unsigned(goff) * 8u);
     for (int i = 0; i < L::NG; ++i) {
       mbar_init(&gfull[i], 1);
       mbar_init(&gempty[i], L::NWS);
@@ -1399,54 +1402,47 @@ __global__ void __launch_bounds__(Kron3dInvLayout<N1, Q>::NTH) kron3d_inv_kernel
               const int i = 8 * nt + 2 * q4 + u;
               if (i < Q) xs[i * LDR + k] = acc[nt][u];
             }
-      } else if (k > 0) {  // 2x2 block, columns k - 1, k
-        double a[2][NSL];
+      } else if (k > 0) {  // 2x2 block, columns k - 1, k: the 2 Q unknowns (c, i) of a slice as one index n' = c Q + i
+        // lane quad q owns n' = 8 (t >> 1) + 2 q + (t & 1), t < NS2: the accumulator entries a product returns to it
+        // and the A entries it supplies at k-step t (K order permuted accordingly, Gt rows read in that order)
+        constexpr int NT2 = (2 * Q + 7) / 8, NS2 = 2 * NT2;
+        double a[NS2];
 #pragma unroll
-        for (int t = 0; t < NSL; ++t) {
-          const int i = 8 * (t >> 1) + 2 * q4 + (t & 1);
-          double a0 = 0.0, a1 = 0.0;
-          if (sok && i < Q) {
+        for (int t = 0; t < NS2; ++t) {
+          const int np = 8 * (t >> 1) + 2 * q4 + (t & 1);
+          const int c = np >= Q ? 1 : 0, i = np - c * Q;
+          double v = 0.0;
+          if (sok && np < 2 * Q) {
             const double* xr = xs + i * LDR;
-            a0 = xr[k - 1];
-            a1 = xr[k];
+            const double* t2 = sT2 + (k - 1 + c) * Q;
+            v = xr[k - 1 + c];
 #pragma unroll
-            for (int l = k + 1; l < Q; ++l) {
-              a0 = fma(-xr[l], sT2[(k - 1) * Q + l], a0);
-              a1 = fma(-xr[l], sT2[k * Q + l], a1);
-            }
+            for (int l = k + 1; l < Q; ++l) v = fma(-xr[l], t2[l], v);
           }
-          a[0][t] = a0;
-          a[1][t] = a1;
+          a[t] = v;
         }
         mbar_wait(&gfull[slot], unsigned(step / L::NG) & 1u);
-        double acc[2][NTQ][2];
+        double acc[NT2][2];
 #pragma unroll
-        for (int c = 0; c < 2; ++c)
+        for (int nt = 0; nt < NT2; ++nt) acc[nt][0] = acc[nt][1] = 0.0;
 #pragma unroll
-          for (int nt = 0; nt < NTQ; ++nt) acc[c][nt][0] = acc[c][nt][1] = 0.0;
+        for (int kc = 0; kc < NS2; ++kc) {
+          const int kk = 8 * (kc >> 1) + 2 * q4 + (kc & 1);
 #pragma unroll
-        for (int cp = 0; cp < 2; ++cp)
-#pragma unroll
-          for (int kc = 0; kc < NSL; ++kc) {
-            const int kk = 8 * (kc >> 1) + 2 * q4 + (kc & 1);
-#pragma unroll
-            for (int c = 0; c < 2; ++c)
-#pragma unroll
-              for (int nt = 0; nt < NTQ; ++nt) {
-                const int n = 8 * nt + r8;
-                dmma(acc[c][nt], a[cp][kc], (kk < Q && n < Q) ? g[(cp * Q + kk) * LD2 + c * Q + n] : 0.0);
-              }
+          for (int nt = 0; nt < NT2; ++nt) {
+            const int n = 8 * nt + r8;
+            dmma(acc[nt], a[kc], (kk < 2 * Q && n < 2 * Q) ? g[kk * LD2 + n] : 0.0);
           }
+        }
         if (sok)
 #pragma unroll
-          for (int c = 0; c < 2; ++c)
+          for (int nt = 0; nt < NT2; ++nt)
 #pragma unroll
-            for (int nt = 0; nt < NTQ; ++nt)
-#pragma unroll
-              for (int u = 0; u < 2; ++u) {
-                const int i = 8 * nt + 2 * q4 + u;
-                if (i < Q) xs[i * LDR + k - 1 + c] = acc[c][nt][u];
-              }
+            for (int u = 0; u < 2; ++u) {
+              const int np = 8 * nt + 2 * q4 + u;
+              const int c = np >= Q ? 1 : 0, i = np - c * Q;
+              if (np < 2 * Q) xs[i * LDR + k - 1 + c] = acc[nt][u];
+            }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&gempty[slot]);

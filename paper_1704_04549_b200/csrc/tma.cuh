@@ -40,6 +40,11 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned by
       : "memory");
 }
 
+// HBM -> L2 only (no shared-memory destination, nothing to wait for); bytes: multiple of 16, src 16-byte aligned
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
+
 // ---- tensor memory as a per-thread scratchpad (tcgen05.ld / st, shape 32x32b: lane l of warp w reads
 // and writes TMEM lane 32 (w % 4) + l, consecutive 32-bit columns). One warp allocates all 512 columns.
 __device__ __forceinline__ void tmem_alloc512(uint32_t* slot) {  // one converged warp; *slot (shared) = base address
