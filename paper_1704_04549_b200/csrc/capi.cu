@@ -1140,9 +1140,10 @@ int tpdg_gpu_form_ksvd(tpdg_gpu_op op, const tpdg_gpu_ksvd_config* cfg_in, tpdg_
     upload(dsv2, sv2.data(), sv2.size(), st);
     const int J = std::max(cfg.lanczos_max_it > 0 ? cfg.lanczos_max_it : 2 * cfg.terms + 20, 22);
     const size_t per = lanczos_work_doubles(op->s, J);
-    // persistent grid of 8-warp CTAs, one block per warp, bounded workspace (<= ~4 GiB)
+    // persistent grid of 8-warp CTAs (two resident per SM: the kernel is latency-bound, ncu), one block per warp,
+    // bounded workspace (<= ~16 GiB; cfg4: 2368 groups x 5.6 MB)
     int groups = std::min(pc->nblk, 148 * 16);
-    while (groups > 148 && double(groups) * per * 8.0 > 4.0 * (1 << 30)) groups /= 2;
+    while (groups > 148 && double(groups) * per * 8.0 > 16.0 * (1 << 30)) groups /= 2;
     const int grid = (groups + 7) / 8;
     if (pc->nblk > 0) {
       const size_t need = sizeof(double) * size_t(grid) * 8 * per;

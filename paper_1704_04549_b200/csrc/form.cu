@@ -21,6 +21,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <cstdio>
+#include <type_traits>
 
 #include "faithful.cuh"
 #include "glibm.cuh"
@@ -50,30 +51,67 @@ __device__ __forceinline__ int groups_per_cta<WarpGroup>() {
 __device__ __forceinline__ void bsync() { __syncthreads(); }
 
 // ---------------------------------------------------------------- sequential reductions
-// dot / norm in the reference's order (single thread), broadcast through shared memory.
+// dot / norm in the reference's order. A CTA group sums on one thread and broadcasts through shared memory. A warp
+// group spreads the loads and the products over its lanes (coalesced; each product is rounded on its own, as in the
+// serial loop: no FMA in this file) and every lane then adds the 32 products of a chunk in index order, fetched by
+// shuffle: the same additions in the same order, so the same bits, but the chain is one DADD per element instead of
+// a load-to-use latency per element (the serial sums were 34 % of the cfg4 Lanczos kernel, ncu).
+__device__ __forceinline__ double warp_ordered_sum(double s, double p, int cnt) {
+  if (cnt == 32) {
+#pragma unroll
+    for (int l = 0; l < 32; ++l) s += __shfl_sync(0xffffffffu, p, l);
+  } else {
+    for (int l = 0; l < cnt; ++l) s += __shfl_sync(0xffffffffu, p, l);
+  }
+  return s;
+}
 template <class Grp>
 __device__ double seq_dot(const Grp& g, const double* a, const double* b, long n, double* sh) {
-  if (g.rank() == 0) {
+  if constexpr (std::is_same<Grp, WarpGroup>::value) {
+    const int lane = g.rank();
     double s = 0.0;
-    for (long i = 0; i < n; ++i) s += a[i] * b[i];
-    *sh = s;
+    for (long base = 0; base < n; base += 32) {
+      const long i = base + lane;
+      const double p = i < n ? a[i] * b[i] : 0.0;
+      s = warp_ordered_sum(s, p, int(n - base < 32 ? n - base : 32));
+    }
+    g.sync();
+    return s;
+  } else {
+    if (g.rank() == 0) {
+      double s = 0.0;
+      for (long i = 0; i < n; ++i) s += a[i] * b[i];
+      *sh = s;
+    }
+    g.sync();
+    const double r = *sh;
+    g.sync();
+    return r;
   }
-  g.sync();
-  const double r = *sh;
-  g.sync();
-  return r;
 }
 template <class Grp>
 __device__ double seq_norm(const Grp& g, const double* a, long n, double* sh) {
-  if (g.rank() == 0) {
+  if constexpr (std::is_same<Grp, WarpGroup>::value) {
+    const int lane = g.rank();
     double s = 0.0;
-    for (long i = 0; i < n; ++i) s += a[i] * a[i];
-    *sh = sqrt(s);
+    for (long base = 0; base < n; base += 32) {
+      const long i = base + lane;
+      const double p = i < n ? a[i] * a[i] : 0.0;
+      s = warp_ordered_sum(s, p, int(n - base < 32 ? n - base : 32));
+    }
+    g.sync();
+    return sqrt(s);
+  } else {
+    if (g.rank() == 0) {
+      double s = 0.0;
+      for (long i = 0; i < n; ++i) s += a[i] * a[i];
+      *sh = sqrt(s);
+    }
+    g.sync();
+    const double r = *sh;
+    g.sync();
+    return r;
   }
-  g.sync();
-  const double r = *sh;
-  g.sync();
-  return r;
 }
 
 // ---------------------------------------------------------------- shuffled operator wrapper
@@ -322,7 +360,7 @@ __device__ LzWork carve_lz(double* base, int J, long rows, long cols) {
 // Per block: raw factors (2D: a1 b1 a2 b2 ; 3D: a1 b1 c1 b2 c2) after the degenerate collapse;
 // kind[blk] = 0 when the 3D stage-1 singular value vanishes (-> fallback), else 1 (pending).
 template <class Grp>
-__global__ void __launch_bounds__(kFormThreads) lanczos_form_kernel(DevSys s, tpdg_gpu_ksvd_config cfg,
+__global__ void __launch_bounds__(kFormThreads, 2) lanczos_form_kernel(DevSys s, tpdg_gpu_ksvd_config cfg,
                                                                      const double* start_vec,
                                                                      const double* start_vec2, double* raw,
                                                                      int* kind, double* work, size_t work_per_cta,
