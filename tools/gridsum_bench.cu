@@ -3,6 +3,8 @@
 //   A: generation barrier (atomic arrival + generation flag) then every CTA reads all partials
 //   B: monotonic arrival counter (target known from the pass index) then every CTA reads all partials
 //   C: per-CTA slots {value, epoch} (16 B, st.release), spread 512 B apart, polled by lanes 0..nb-1
+//   D<S>: B with the arrival counter sharded over S counters 256 B apart (CTA b arrives on counter b % S; same-address
+//         L2 atomics serialize at ~27 cycles each, 148 of them ~2 us); lanes 0..S-1 of warp 0 each poll one shard
 // nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -o /tmp/gsb tools/gridsum_bench.cu
 #include <cstdio>
 #include <cstdint>
@@ -40,7 +42,7 @@ __device__ __forceinline__ double finish(double pv, double* shB) {
   return shB[32];
 }
 
-template <int V>
+template <int V, int S = 1>
 __global__ void __launch_bounds__(NT) gsum(int P, double* part, unsigned* bar, double* out, unsigned base) {
   __shared__ double shA[32], shB[33];
   const unsigned nb = gridDim.x;
@@ -81,6 +83,20 @@ __global__ void __launch_bounds__(NT) gsum(int P, double* part, unsigned* bar, d
       }
       __syncthreads();
       pv = threadIdx.x < nb ? reinterpret_cast<volatile double*>(part)[size_t(p % 64) * nb + threadIdx.x] : 0.0;
+    } else if (V == 3) {
+      if (threadIdx.x == 0) {
+        part[size_t(p % 64) * nb + blockIdx.x] = bs;
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar + 64 * (blockIdx.x % S)) : "memory");
+      }
+      if (threadIdx.x < S) {  // shard c gets the CTAs b = c (mod S)
+        const unsigned nc = (nb - threadIdx.x + S - 1) / S, target = (base + p + 1) * nc;
+        unsigned cur;
+        do {
+          asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(bar + 64 * threadIdx.x) : "memory");
+        } while (int(cur - target) < 0);
+      }
+      __syncthreads();
+      pv = threadIdx.x < nb ? reinterpret_cast<volatile double*>(part)[size_t(p % 64) * nb + threadIdx.x] : 0.0;
     } else {
       // slot b at part + 64 b doubles (512 B apart): {value, epoch}
       const unsigned epoch = base + p + 1;
@@ -113,19 +129,20 @@ int main() {
   unsigned* bar;
   cudaMalloc(&part, sizeof(double) * 64 * 256 * 2);
   cudaMalloc(&out, 8);
-  cudaMalloc(&bar, 64);
+  cudaMalloc(&bar, 256 * 64);
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   const int P = 2000;
-  for (int v = 0; v < 3; ++v) {
+  for (int v = 0; v < 8; ++v) {
     for (int rep = 0; rep < 3; ++rep) {
-      cudaMemset(bar, 0, 64);
+      cudaMemset(bar, 0, 256 * 64);
       cudaMemset(part, 0, sizeof(double) * 64 * 256 * 2);
       unsigned base = 0;
       int Pv = P;
       void* args[] = {&Pv, &part, &bar, &out, &base};
-      void* fn = v == 0 ? (void*)gsum<0> : v == 1 ? (void*)gsum<1> : (void*)gsum<2>;
+      void* fn = v == 0 ? (void*)gsum<0> : v == 1 ? (void*)gsum<1> : v == 2 ? (void*)gsum<2> : v == 3 ? (void*)gsum<3, 4>
+                 : v == 4 ? (void*)gsum<3, 8> : v == 5 ? (void*)gsum<3, 16> : v == 6 ? (void*)gsum<3, 32> : (void*)gsum<3, 1>;
       cudaEventRecord(a);
       cudaLaunchCooperativeKernel(fn, dim3(sms), dim3(NT), args, 0, 0);
       cudaEventRecord(b);
@@ -134,7 +151,8 @@ int main() {
       cudaEventElapsedTime(&ms, a, b);
       double o = 0;
       cudaMemcpy(&o, out, 8, cudaMemcpyDeviceToHost);
-      if (rep == 2) printf("variant %c: %.3f us per grid sum (%s) acc %.17g\n", 'A' + v, ms * 1e3 / P,
+      const char* names[] = {"A", "B", "C", "D<4>", "D<8>", "D<16>", "D<32>", "D<1>"};
+      if (rep == 2) printf("variant %s: %.3f us per grid sum (%s) acc %.17g\n", names[v], ms * 1e3 / P,
                            cudaGetErrorString(cudaGetLastError()), o);
     }
   }
