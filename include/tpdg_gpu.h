@@ -197,6 +197,11 @@ int tpdg_gpu_build_cache_advection(tpdg_gpu_ctx ctx, int dim, int n_elements, in
 /* Test hook: the device libm of the formation (csrc/glibm.cuh, glibc 2.39's sin/cos/atan/atan2 as called by
  * standardize_2x2, tensor/schur.hpp:91-108) on n device arguments. fn: 0 sin, 1 cos, 2 atan, 3 atan2(x, y). */
 int tpdg_gpu_libm_eval(tpdg_gpu_ctx ctx, int fn, int64_t n, const double *d_x, const double *d_y, double *d_out);
+/* Test hook: one modified Gram-Schmidt step of the Arnoldi process as the GMRES driver launches it
+ * (solve/gmres.hpp:112-121): d_V holds rows v_0 .. v_k (orthonormal basis) and row k+1 = w, each of n doubles at
+ * stride ldv (a multiple of 2, >= n); on return h[0 .. k] = the projections, h[k+1] = ||w||, and row k+1 is the
+ * normalized w. h: host array of k + 2 doubles. */
+int tpdg_gpu_mgs_step(tpdg_gpu_ctx ctx, double *d_V, int64_t ldv, int k, int64_t n, double *h);
 /* build_cache (ops/linearized.hpp:38-100) of the LLF Euler law (laws/euler.hpp:106-211) on the device from the
  * nodal linearization state [e][c][node] and the quadrature-point geometry (adj [e][q][d][d], face_n
  * [e][f][qf][d]); G is the reference element's (mu x p+1) interpolation matrix. TPDG_STATE on a

@@ -96,7 +96,7 @@ EXPORTS = [
     "tpdg_gpu_pc_import_factors", "tpdg_gpu_pc_import_record", "tpdg_gpu_form_block_jacobi", "tpdg_gpu_pc_destroy", "tpdg_gpu_pc_num_fallbacks", "tpdg_gpu_pc_fallbacks",
     "tpdg_gpu_pc_factor_len", "tpdg_gpu_pc_export_factors", "tpdg_gpu_pc_apply", "tpdg_gpu_pc_apply_host",
     "tpdg_gpu_gmres", "tpdg_gpu_gmres_host", "tpdg_setup_advection", "tpdg_setup_system", "tpdg_setup_destroy", "tpdg_setup_geometry",
-    "tpdg_gpu_build_cache_advection", "tpdg_gpu_libm_eval", "tpdg_gpu_build_cache_euler", "tpdg_setup_euler",
+    "tpdg_gpu_build_cache_advection", "tpdg_gpu_libm_eval", "tpdg_gpu_mgs_step", "tpdg_gpu_build_cache_euler", "tpdg_setup_euler",
     "tpdg_setup_state", "tpdg_gpu_residual_euler", "tpdg_gpu_step_backward_euler",
     "tpdg_uniform_vector", "tpdg_seeded_unit_vector", "tpdg_halo_plan_create", "tpdg_halo_plan_query",
     "tpdg_halo_plan_conn", "tpdg_halo_plan_halo_gid", "tpdg_halo_plan_peer", "tpdg_halo_plan_destroy",
@@ -152,6 +152,7 @@ def lib():
                                 C.POINTER(C.c_int)],
         "tpdg_gpu_build_cache_advection": [v, C.c_int, C.c_int, C.c_int, C.c_int, v, v, v, v, v, C.c_int, dp, v, v, v],
         "tpdg_gpu_libm_eval": [v, C.c_int, C.c_int64, v, v, v],
+        "tpdg_gpu_mgs_step": [v, v, C.c_int64, C.c_int, C.c_int64, v],
         "tpdg_gpu_build_cache_euler": [v, C.c_int, C.c_int, C.c_int, C.c_int, v, v, v, v, v, v, v, v],
         "tpdg_setup_euler": [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(v)],
         "tpdg_setup_state": [v, C.POINTER(dp), C.POINTER(C.c_int64)],
@@ -423,6 +424,15 @@ def libm_eval(ctx: "Context", fn: str, x, y=None) -> np.ndarray:
     _check(lib().tpdg_gpu_libm_eval(ctx.h, code, dx.numel(), C.c_void_p(dx.data_ptr()),
                                     C.c_void_p(dy.data_ptr()) if dy is not None else None, C.c_void_p(out.data_ptr())))
     return out.cpu().numpy()
+
+
+def mgs_step(ctx: "Context", V, k: int, n: int) -> np.ndarray:
+    """Test hook: one modified Gram-Schmidt step (solve/gmres.hpp:112-121) on the device tensor V (rows v_0 .. v_k
+    and w = row k + 1, row stride V.stride(0)), in place; returns h[0 .. k + 1] (projections, then the norm)."""
+    h = np.zeros(k + 2)
+    _check(lib().tpdg_gpu_mgs_step(ctx.h, C.c_void_p(V.data_ptr()), V.stride(0), k, n,
+                                   h.ctypes.data_as(C.c_void_p)))
+    return h
 
 
 def face_layer_nodes(dim: int, q: int, face: int) -> np.ndarray:

@@ -1423,6 +1423,22 @@ int tpdg_gpu_libm_eval(tpdg_gpu_ctx ctx, int fn, int64_t n, const double* d_x, c
   });
 }
 
+int tpdg_gpu_mgs_step(tpdg_gpu_ctx ctx, double* d_V, int64_t ldv, int k, int64_t n, double* h) {
+  return guarded([&] {
+    REQUIRE(ctx && d_V && h, TPDG_CONFIG, "mgs_step: null argument");
+    REQUIRE(k >= 0 && n >= 1 && ldv >= n && ldv % 2 == 0, TPDG_CONFIG, "mgs_step: bad shape");
+    DevBuf hc, partial, counter;
+    hc.alloc(sizeof(double) * (k + 2));
+    partial.alloc(sizeof(double) * std::max<size_t>(148 * 8, size_t(mgs_partial_doubles(k + 1))));
+    counter.alloc(sizeof(unsigned) * 8);
+    TPDG_CUDA_CHECK(cudaMemsetAsync(counter.p, 0, counter.bytes, ctx->stream));
+    launch_mgs_iteration(d_V, ldv, k, n, hc.as<double>(), partial.as<double>(), counter.as<unsigned>() + 4, nullptr,
+                         ctx->stream, nullptr, nullptr);
+    TPDG_CUDA_CHECK(cudaMemcpyAsync(h, hc.p, sizeof(double) * (k + 2), cudaMemcpyDeviceToHost, ctx->stream));
+    TPDG_CUDA_CHECK(cudaStreamSynchronize(ctx->stream));
+  });
+}
+
 int tpdg_gpu_build_cache_euler(tpdg_gpu_ctx ctx, int dim, int p, int mu, int n_elements, const double* d_g,
                                const double* d_state, const double* d_adj, const double* d_face_n,
                                const int64_t* d_conn, double* d_dft, double* d_dfm, double* d_dfp) {
