@@ -538,6 +538,14 @@ __global__ void __launch_bounds__(NT, 1) mgs_stream_kernel(double* __restrict__ 
     ++ir;
   };
   for (int q = 0; q < D - 1; ++q) issue_any();
+  // w rows >= RW go straight to shared memory (the thread's own pairs, zero-filled past len) as one cp.async group
+  // behind the ring's first rows: all of them in flight at once, complete by the third row of pass 0 (group order)
+  for (int r = RW; r < nrows; ++r) {
+#pragma unroll
+    for (int u = 0; u < PPT; ++u)
+      cp_async16z(w_s + ROWB * unsigned(r) + P1 * unsigned(u), wg + r * ROW + 2 * (t + NT * u), piece_bytes(r, u));
+  }
+  cp_async_commit();
   double2 wr[RW][PPT];
 #pragma unroll
   for (int r = 0; r < RW; ++r)
@@ -546,9 +554,6 @@ __global__ void __launch_bounds__(NT, 1) mgs_stream_kernel(double* __restrict__ 
       const int i = 2 * (t + NT * u) + ROW * r;
       wr[r][u] = i + 1 < len ? *reinterpret_cast<const double2*>(wg + i) : make_double2(i < len ? wg[i] : 0.0, 0.0);
     }
-  for (int i = ROW * RW + 2 * t; i < nrows * ROW; i += 2 * NT)  // a thread reads back only what it wrote
-    *reinterpret_cast<double2*>(wsm + i - ROW * RW) =
-        i + 1 < len ? *reinterpret_cast<const double2*>(wg + i) : make_double2(i < len ? wg[i] : 0.0, 0.0);
   __syncthreads();
   tmem_fence_after_sync();
   const uint32_t tm = tm_slot + ((32u * unsigned((t >> 5) & 3)) << 16) + unsigned(t >> 7) * (512u / (NT / 128));
