@@ -1052,7 +1052,7 @@ __device__ void lu_inverse_col(const double* lu, const int* perm, int n, int c, 
 }
 
 // One warp per block: irec = A1^-1 | L^T | R | Q1 | Q2 | T2 | G blocks (block b of size m = sz q stored
-// transposed, Gt[k'][n] = G_b[n][k'], m rows of g_t_ld(q, sz) = 4 (mod 8) doubles: the DMMA B-fragment loads
+// transposed, Gt[k'][n] = G_b[n][k'], m rows of g_t_ld(q, sz) = 2 (mod 8) doubles: the DMMA B-fragment loads
 // of the apply's Sylvester sweep -- eight consecutive n by four k' two rows apart -- are conflict-free).
 // Lanes take inverse columns, product entries and, in the Gauss-Jordan inverse of (I (x) T1 + T2_bb (x) I),
 // rows (elimination) or columns (swap / scaling); every entry sees the same operations in the same
@@ -1140,7 +1140,7 @@ __global__ void __launch_bounds__(32 * kPrepWarps) kron3d_inv_prep_kernel(DevPC 
       }
       __syncwarp();
     }
-    const int ld = g_t_ld(q, sz);  // transposed: Gt[k'][n] = G[n][k'], m rows of ld (= 4 mod 8) doubles
+    const int ld = g_t_ld(q, sz);  // transposed: Gt[k'][n] = G[n][k'], m rows of ld (= 2 mod 8) doubles
     for (int e = lane; e < m * ld; e += 32) {
       const int kk = e / ld, n = e % ld;
       oG[off + e] = n < m ? G[n * m + kk] : 0.0;

@@ -143,7 +143,11 @@ void launch_pc_apply(const DevPC& pc, const double* in, double* out, cudaStream_
 void launch_kron3d_inv_prep(const DevPC& pc, double* irec, cudaStream_t st);
 // Row stride of the 3D Sylvester block inverses G (sz = 1, 2): segments of even(q) doubles, rows 2 (mod 4) apart
 // leading dimension of a transposed G block of sz x sz T2 cells: the smallest >= sz q that is 4 (mod 8)
-__host__ __device__ constexpr int g_t_ld(int q, int sz) { return (sz * q + 3) / 8 * 8 + 4; }
+// Row stride of a transposed G block: >= sz q and = 2 (mod 8). The Sylvester sweep's DMMA B fragments read, per
+// half-warp (LDS.64 is served one half-warp at a time), four rows k' two apart by four consecutive n: with
+// 2 ld = 4 (mod 16) doubles those 16 lanes hit 16 distinct bank pairs (ld = 4 (mod 8) gave a two-way conflict:
+// 4 wavefronts per load instead of 2, 19 % of the apply kernel's shared-memory wavefronts, ncu).
+__host__ __device__ constexpr int g_t_ld(int q, int sz) { return (sz * q + 5) / 8 * 8 + 2; }
 // A1^-1 | L^T | R | Q1 | Q2 | T2 | G blocks (<= q^2 g_t_ld(q, 2): every block 2 x 2)
 __host__ __device__ inline size_t irec3_doubles(int n1, int q) { return size_t(n1) * n1 + 5 * q * q + size_t(q) * q * g_t_ld(q, 2); }
 // bit-faithful 2D apply, several blocks per warp (kron_ew.cu); false if no sized variant fits
