@@ -62,7 +62,12 @@ constexpr int kEw16Lanes = 16;  // lanes per block at N = 16 (2 blocks per warp)
 template <int N, int P = N>  // P lanes per block
 struct Ew {
   static constexpr int EW = 32 / P;  // blocks per warp
-  static constexpr int LD = N + kEwLdPad;  // X leading dimension (odd for even N: conflict-free fibers)
+  // X leading dimension. The Sylvester wavefront's lanes sit on an anti-diagonal of X, one quasi-block apart:
+  // consecutive lanes' right-hand-side loads are (LD - 1) doubles apart for 1 x 1 blocks and 2 (LD - 1) for 2 x 2
+  // blocks, so LD - 1 must be odd for those (up to 8 / 16) lanes to hit distinct bank pairs. N + 3 is even for the
+  // odd N; N = 16 takes N + 2 (N + 3 = 19 was a two-way conflict on 54 % of the kernel's shared-memory wavefronts,
+  // ncu; the row fibers' two-way conflict at an even LD costs far less).
+  static constexpr int LD = N + (N % 2 == 0 ? 2 : kEwLdPad);
   static constexpr int XSZ = (N * LD + 1) & ~1;
   static constexpr int R1 = (2 * N * N > XSZ ? 2 * N * N : XSZ);
   static constexpr int HDR = ((4 + 4 * N) / 2 + 2) & ~1;  // sylv_hdr_doubles(N, N)
