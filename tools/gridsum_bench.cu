@@ -5,6 +5,8 @@
 //   C: per-CTA slots {value, epoch} (16 B, st.release), spread 512 B apart, polled by lanes 0..nb-1
 //   D<S>: B with the arrival counter sharded over S counters 256 B apart (CTA b arrives on counter b % S; same-address
 //         L2 atomics serialize at ~27 cycles each, 148 of them ~2 us); lanes 0..S-1 of warp 0 each poll one shard
+//   E: per-CTA slots of two 8-byte words {32 bits of the partial | 32-bit epoch} (each word single-copy atomic: the data
+//      carries its own flag, no fence, no atomic, relaxed stores and polls), parity double buffer, polled by lanes 0..nb-1
 // nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -o /tmp/gsb tools/gridsum_bench.cu
 #include <cstdio>
 #include <cstdint>
@@ -97,6 +99,22 @@ __global__ void __launch_bounds__(NT) gsum(int P, double* part, unsigned* bar, d
       }
       __syncthreads();
       pv = threadIdx.x < nb ? reinterpret_cast<volatile double*>(part)[size_t(p % 64) * nb + threadIdx.x] : 0.0;
+    } else if (V == 4) {
+      const unsigned epoch = base + p + 1;
+      unsigned long long* slots = reinterpret_cast<unsigned long long*>(part) + 2 * size_t(nb) * (p & 1);
+      if (threadIdx.x == 0) {
+        const unsigned long long bits = (unsigned long long)__double_as_longlong(bs);
+        const unsigned long long w0 = (bits & 0xffffffffull) | ((unsigned long long)epoch << 32);
+        const unsigned long long w1 = (bits >> 32) | ((unsigned long long)epoch << 32);
+        asm volatile("st.relaxed.gpu.global.v2.u64 [%0], {%1, %2};" ::"l"(slots + 2 * blockIdx.x), "l"(w0), "l"(w1) : "memory");
+      }
+      if (threadIdx.x < nb) {
+        unsigned long long w0, w1;
+        do {
+          asm volatile("ld.relaxed.gpu.global.v2.u64 {%0, %1}, [%2];" : "=l"(w0), "=l"(w1) : "l"(slots + 2 * threadIdx.x) : "memory");
+        } while (unsigned(w0 >> 32) != epoch || unsigned(w1 >> 32) != epoch);
+        pv = __longlong_as_double((long long)((w0 & 0xffffffffull) | (w1 << 32)));
+      }
     } else {
       // slot b at part + 64 b doubles (512 B apart): {value, epoch}
       const unsigned epoch = base + p + 1;
@@ -134,7 +152,22 @@ int main() {
   cudaEventCreate(&a);
   cudaEventCreate(&b);
   const int P = 2000;
-  for (int v = 0; v < 8; ++v) {
+  for (int grid : {sms, sms / 2, sms / 4}) {  // variant B with fewer CTAs: does the reduction get cheaper?
+    for (int rep = 0; rep < 3; ++rep) {
+      cudaMemset(bar, 0, 256 * 64);
+      unsigned base = 0;
+      int Pv = P;
+      void* args[] = {&Pv, &part, &bar, &out, &base};
+      cudaEventRecord(a);
+      cudaLaunchCooperativeKernel((void*)gsum<1>, dim3(grid), dim3(NT), args, 0, 0);
+      cudaEventRecord(b);
+      cudaEventSynchronize(b);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, a, b);
+      if (rep == 2) printf("variant B, %d CTAs: %.3f us per grid sum\n", grid, ms * 1e3 / P);
+    }
+  }
+  for (int v = 0; v < 9; ++v) {
     for (int rep = 0; rep < 3; ++rep) {
       cudaMemset(bar, 0, 256 * 64);
       cudaMemset(part, 0, sizeof(double) * 64 * 256 * 2);
@@ -142,7 +175,7 @@ int main() {
       int Pv = P;
       void* args[] = {&Pv, &part, &bar, &out, &base};
       void* fn = v == 0 ? (void*)gsum<0> : v == 1 ? (void*)gsum<1> : v == 2 ? (void*)gsum<2> : v == 3 ? (void*)gsum<3, 4>
-                 : v == 4 ? (void*)gsum<3, 8> : v == 5 ? (void*)gsum<3, 16> : v == 6 ? (void*)gsum<3, 32> : (void*)gsum<3, 1>;
+                 : v == 4 ? (void*)gsum<3, 8> : v == 5 ? (void*)gsum<3, 16> : v == 6 ? (void*)gsum<3, 32> : v == 7 ? (void*)gsum<3, 1> : (void*)gsum<4>;
       cudaEventRecord(a);
       cudaLaunchCooperativeKernel(fn, dim3(sms), dim3(NT), args, 0, 0);
       cudaEventRecord(b);
@@ -151,7 +184,7 @@ int main() {
       cudaEventElapsedTime(&ms, a, b);
       double o = 0;
       cudaMemcpy(&o, out, 8, cudaMemcpyDeviceToHost);
-      const char* names[] = {"A", "B", "C", "D<4>", "D<8>", "D<16>", "D<32>", "D<1>"};
+      const char* names[] = {"A", "B", "C", "D<4>", "D<8>", "D<16>", "D<32>", "D<1>", "E"};
       if (rep == 2) printf("variant %s: %.3f us per grid sum (%s) acc %.17g\n", names[v], ms * 1e3 / P,
                            cudaGetErrorString(cudaGetLastError()), o);
     }
