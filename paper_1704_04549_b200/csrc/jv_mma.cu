@@ -39,7 +39,7 @@ __device__ __forceinline__ const double* nbr_vals(const DevSys& s, const double*
   return nbr < s.n_local ? vin + size_t(nbr) * qq : halo + size_t(nbr - s.n_local) * qq;
 }
 
-constexpr int kJvWarps = 12;
+constexpr int kJvWarps = 16;  // most warps per CTA (q = 16); JvMmaLayout::wcap per instantiation
 
 template <int Q, int MU>
 struct JvMmaLayout {
@@ -67,15 +67,19 @@ struct JvMmaLayout {
   static constexpr int e_g = mf_in_r0 ? e_val + MP * LVAL : e_mf + MP * LMF;  // g[4][MU]
   static constexpr int e_lift = e_g + 4 * MU;          // lift vectors [4][Q]
   static constexpr int e_pw = (e_lift + 4 * Q + 1) & ~1; // jd | dft0 | dft1 of the element (cp.async, prefetched)
-  static constexpr int per_warp = (e_pw + 3 * MU * MU + 1) & ~1;
+  // q <= 16: the element's jd / dft are not staged (they are read once, from L2, bulk-prefetched one element ahead):
+  // the workspace shrinks by a third and 16 warps fit (cfg2 p = 15: 36.2 -> 34.0 us); larger q keeps the staging
+  // (p = 30 measured 190 us staged vs 197 direct)
+  static constexpr bool stage_pw = Q > 16;
+  static constexpr int per_warp = stage_pw ? ((e_pw + 3 * MU * MU + 1) & ~1) : e_pw;
   static constexpr int budget = (227 * 1024) / 8 - weights - 16;
   // 12 warps pay at q >= 16 (p = 15 / 20 / 30: 42 -> 41, 83 -> 81, 249 -> 207 us); p = 8 is faster with 8
-  static constexpr int wcap = Q >= 16 ? kJvWarps : 8;
+  static constexpr int wcap = Q > 16 ? 12 : Q == 16 ? kJvWarps : 8;
   static constexpr int warps = budget / per_warp > wcap ? wcap : budget / per_warp;
 };
 
 template <int Q, int MU>
-__global__ void __launch_bounds__(32 * kJvWarps) jv2d_mma_kernel(DevSys s, const double* __restrict__ vin,
+__global__ void __launch_bounds__(32 * JvMmaLayout<Q, MU>::wcap) jv2d_mma_kernel(DevSys s, const double* __restrict__ vin,
                                                         const double* __restrict__ halo, double* __restrict__ vout) {
   if (s.skip && *s.skip) return;
   using L = JvMmaLayout<Q, MU>;
@@ -142,8 +146,14 @@ __global__ void __launch_bounds__(32 * kJvWarps) jv2d_mma_kernel(DevSys s, const
     if (e >= s.e_hi) return;
     const double* jd = s.jdet + size_t(e) * MM;
     const double* d0 = s.dft + size_t(e) * 2 * MM;
-    for (int i = lane; i < MM; i += 32) cp_async8(spw + i, jd + i);
-    for (int i = lane; i < 2 * MM; i += 32) cp_async8(spw + MM + i, d0 + i);
+    if constexpr (L::stage_pw) {
+      for (int i = lane; i < MM; i += 32) cp_async8(spw + i, jd + i);
+      for (int i = lane; i < 2 * MM; i += 32) cp_async8(spw + MM + i, d0 + i);
+    } else if (lane == 0) {  // HBM -> L2; ranges widened to 16-byte boundaries
+      const uintptr_t a = reinterpret_cast<uintptr_t>(jd) & ~uintptr_t(15), b = reinterpret_cast<uintptr_t>(d0) & ~uintptr_t(15);
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(unsigned((MM * 8 + 31) & ~15)) : "memory");
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(b), "r"(unsigned((2 * MM * 8 + 31) & ~15)) : "memory");
+    }
   };
   const int stride = gridDim.x * NW;
   double vr[NV], nr[NL];
@@ -223,9 +233,16 @@ __global__ void __launch_bounds__(32 * kJvWarps) jv2d_mma_kernel(DevSys s, const
     for (int qv = lane; qv < MM; qv += 32) {
       const int be = qv / MU, al = qv % MU;
       const double x = sval[be * LVAL + al];
-      smf[be * LMF + al] = s.a * spw[qv] * x;
-      smf[be * LMF + MU + al] = s.b * (spw[MM + qv] * x);
-      sval[be * LVAL + al] = s.b * (spw[2 * MM + qv] * x);
+      double cj, c0, c1;
+      if constexpr (L::stage_pw) {
+        cj = spw[qv], c0 = spw[MM + qv], c1 = spw[2 * MM + qv];
+      } else {
+        const double* pd = s.dft + size_t(e) * 2 * MM;
+        cj = __ldg(s.jdet + size_t(e) * MM + qv), c0 = __ldg(pd + qv), c1 = __ldg(pd + MM + qv);
+      }
+      smf[be * LMF + al] = s.a * cj * x;
+      smf[be * LMF + MU + al] = s.b * (c0 * x);
+      sval[be * LVAL + al] = s.b * (c1 * x);
     }
     __syncwarp();
     fetch_pw(e + stride);  // the buffer is free: next element's jd / dft
